@@ -1,0 +1,101 @@
+/*
+ * vrte_cuda.h -- internal C ABI between the host C++ of libvrte.so and its
+ * sm_100a device pipeline ("the host C++ ... calls an
+ * internal C ABI vrte_cuda_brdf(...) implemented in .cu").
+ *
+ * Plain pointers and sizes only.  All arrays are HOST arrays unless noted.
+ * The public drop-in surface is vrte.h; these entry points are exported for
+ * the benchmark (device-resident timing) and the multi-GPU order sharding.
+ */
+#ifndef VRTE_CUDA_H
+#define VRTE_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#ifndef VRTE_API
+#define VRTE_API __attribute__((visibility("default")))
+#endif
+
+/* One BRDF problem after host-side set-up (brdf.cpp:43-77, pipeline.cpp:27-55). */
+typedef struct vrte_cuda_problem {
+    int32_t N;            /* half-range quadrature nodes */
+    int32_t L;            /* Fourier orders (after order_cap) */
+    int32_t n_layers;
+    int32_t n_media;      /* distinct media after dedup (pipeline.cpp:37-54) */
+    int32_t n_in;         /* incident cosines */
+    int32_t n_dphi;       /* output azimuths */
+    const double* nodes;    /* [N]  types.cpp:27-68 */
+    const double* weights;  /* [N] */
+    const double* omega;    /* [n_media] */
+    const double* greek;    /* [n_media][L][6]: beta alpha gamma delta eps zeta */
+    const double* tau;      /* [n_layers] */
+    const int32_t* medium;  /* [n_layers] -> medium index */
+    const double* mu_in;    /* [n_in] */
+    int32_t base_type;      /* 0 black, 1 lambertian, 2 mueller table */
+    double rho;
+    int32_t table_n;
+    const double* table;      /* [table_n*table_n][16] row-major */
+    const double* beam_rows;  /* [n_in][N][16]: base_row_at(node_i, mu0) */
+    const double* post;       /* [n_in][16]: B (mu0 B)^+ (brdf.cpp:100-105) */
+    const double* trig;       /* [L][n_dphi][2]: cos(m x), sin(m x), x = -dphi */
+    /* order shard handled by this call: m = m_begin + k*m_stride, k < n_orders.
+       n_orders = 0 means all L orders on this device. */
+    int32_t m_begin, m_stride, n_orders;
+    int32_t device;           /* CUDA ordinal; -1 = current device */
+} vrte_cuda_problem;
+
+typedef struct vrte_cuda_result {
+    double t_homogeneous;   /* device seconds per stage (CUDA events) */
+    double t_particular;
+    double t_boundary;
+    double t_synthesis;
+    double t_device;        /* whole device pipeline incl. H2D/D2H */
+    uint64_t dithered;
+    uint64_t clamped;
+    uint64_t polished;
+    uint64_t kernel_launches;
+    double max_eigen_residual;
+    double max_particular_residual;
+    int32_t status;         /* 0 ok, 3 numerical, 5 argument */
+    char message[512];
+} vrte_cuda_result;
+
+/* Full solve: host inputs -> host table [n_in][N][n_dphi][16]. */
+VRTE_API int32_t vrte_cuda_brdf(const vrte_cuda_problem* problem, double* table,
+                                vrte_cuda_result* result);
+
+/* Device-resident plan (benchmark / repeated solves of one shape). */
+typedef struct vrte_cuda_plan vrte_cuda_plan;
+VRTE_API int32_t vrte_cuda_plan_create(const vrte_cuda_problem* problem, vrte_cuda_plan** out,
+                                       vrte_cuda_result* result);
+/* Run the device pipeline `iters` times with inputs already resident; the
+ * average device seconds per solve is returned in *seconds (CUDA events on the
+ * plan's stream).  Table stays on the device. */
+VRTE_API int32_t vrte_cuda_plan_run(vrte_cuda_plan* plan, int32_t iters, double* seconds,
+                                    vrte_cuda_result* result);
+VRTE_API int32_t vrte_cuda_plan_fetch(vrte_cuda_plan* plan, double* table);
+/* tau=0 upward stacks of the plan's orders: [n_orders][4 n_in][4N] (host). */
+VRTE_API int32_t vrte_cuda_plan_fetch_up(vrte_cuda_plan* plan, double* up);
+/* Per-(medium, order) eigen data for debugging: wr, wi [n_media*n_orders][4N],
+ * residual [n_media*n_orders][4N]. Any pointer may be NULL. */
+VRTE_API int32_t vrte_cuda_plan_fetch_modes(vrte_cuda_plan* plan, double* wr, double* wi,
+                                            double* residual, double* nu);
+VRTE_API void vrte_cuda_plan_destroy(vrte_cuda_plan* plan);
+
+/* Fourier synthesis from host-gathered stacks of ALL orders (multi-GPU root):
+ * up [L][4 n_in][4N], host table out. */
+VRTE_API int32_t vrte_cuda_synthesize(const vrte_cuda_problem* problem, const double* up,
+                                      double* table, vrte_cuda_result* result);
+
+VRTE_API int32_t vrte_cuda_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

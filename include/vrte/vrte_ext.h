@@ -1,0 +1,44 @@
+/*
+ * vrte_ext.h -- optional additions to the vrte C ABI (the reference ABI in
+ * vrte.h is unchanged; these are new symbols, SURVEY.md §5 "add optional new
+ * functions").
+ */
+#ifndef VRTE_EXT_H
+#define VRTE_EXT_H
+
+#include "vrte.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Device-side statistics of the last vrte_compute_brdf on this handle. */
+typedef struct vrte_brdf_device_stats {
+    double t_homogeneous, t_particular, t_boundary, t_synthesis; /* device seconds */
+    uint64_t dithered, clamped, polished, kernel_launches;
+    double max_eigen_residual, max_particular_residual;
+    uint64_t material_hash; /* FNV-1a over the numeric content (brdf.cpp:11-41) */
+} vrte_brdf_device_stats;
+
+VRTE_API vrte_status vrte_brdf_device_stats_get(const vrte_brdf* brdf, vrte_brdf_device_stats* out);
+
+/* Build the device problem of a BRDF request without solving it (benchmark
+ * plan creation; see vrte_cuda.h).  Returns an opaque plan. */
+typedef struct vrte_cuda_plan vrte_cuda_plan;
+VRTE_API vrte_status vrte_brdf_plan_create(const vrte_material* material, const vrte_options* options,
+                                           const double* mu_in, size_t n_mu_in, int32_t n_dphi,
+                                           const double* basis, int32_t device, int32_t m_begin,
+                                           int32_t m_stride, int32_t n_orders, vrte_cuda_plan** out);
+
+/* Assemble a BRDF handle from a host table computed elsewhere (multi-GPU
+ * root after the order gather).  Takes a copy of `table`. */
+VRTE_API vrte_status vrte_brdf_from_stacks(const vrte_material* material, const vrte_options* options,
+                                           const double* mu_in, size_t n_mu_in, int32_t n_dphi,
+                                           const double* basis, const double* up_all_orders,
+                                           vrte_brdf** out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,370 @@
+"""B200-native drop-in for the reference `vrte` BRDF path (arXiv 1707.05882).
+
+Python mirror of the reference C ABI (/root/reference/proj/include/vrte/vrte.h)
+over the in-tree libvrte.so (host C++ + sm_100a kernels).  Same names,
+argument meaning, status codes and error text as the reference; there is no
+CPU fallback: importing without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libvrte.so")
+
+VRTE_OK = 0
+VRTE_E_VALIDATION = 2
+VRTE_E_NUMERICAL = 3
+VRTE_E_ARGUMENT = 5
+
+
+class VrteError(RuntimeError):
+    """A non-zero vrte_status with vrte_last_error() text."""
+
+    def __init__(self, code: int, message: str):
+        super().__init__(f"vrte status {code}: {message}")
+        self.code = code
+        self.message = message
+
+
+class Options(C.Structure):
+    """vrte_options (vrte.h:54-66); layout is ABI."""
+    _fields_ = [
+        ("quadrature_n", C.c_int32),
+        ("order_cap", C.c_int32),
+        ("threads", C.c_int32),
+        ("out_zenith", C.c_int32),
+        ("out_azimuth", C.c_int32),
+        ("incident_mu0", C.c_double),
+        ("incident_phi0", C.c_double),
+        ("incident_override", C.c_int32),
+        ("dump_eigen_path", C.c_char_p),
+        ("dump_boundary_path", C.c_char_p),
+        ("dump_kernel_path", C.c_char_p),
+    ]
+
+
+class Timings(C.Structure):
+    """vrte_timings (vrte.h:75-85)."""
+    _fields_ = [
+        ("homogeneous", C.c_double),
+        ("particular", C.c_double),
+        ("boundary", C.c_double),
+        ("reconstruction", C.c_double),
+        ("total_wall", C.c_double),
+        ("homogeneous_solves", C.c_uint64),
+        ("particular_solves", C.c_uint64),
+        ("boundary_solves", C.c_uint64),
+        ("reconstruction_items", C.c_uint64),
+    ]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class DeviceStats(C.Structure):
+    """vrte_brdf_device_stats (vrte_ext.h)."""
+    _fields_ = [
+        ("t_homogeneous", C.c_double),
+        ("t_particular", C.c_double),
+        ("t_boundary", C.c_double),
+        ("t_synthesis", C.c_double),
+        ("dithered", C.c_uint64),
+        ("clamped", C.c_uint64),
+        ("polished", C.c_uint64),
+        ("kernel_launches", C.c_uint64),
+        ("max_eigen_residual", C.c_double),
+        ("max_particular_residual", C.c_double),
+        ("material_hash", C.c_uint64),
+    ]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class CudaResult(C.Structure):
+    """vrte_cuda_result (vrte_cuda.h)."""
+    _fields_ = [
+        ("t_homogeneous", C.c_double),
+        ("t_particular", C.c_double),
+        ("t_boundary", C.c_double),
+        ("t_synthesis", C.c_double),
+        ("t_device", C.c_double),
+        ("dithered", C.c_uint64),
+        ("clamped", C.c_uint64),
+        ("polished", C.c_uint64),
+        ("kernel_launches", C.c_uint64),
+        ("max_eigen_residual", C.c_double),
+        ("max_particular_residual", C.c_double),
+        ("status", C.c_int32),
+        ("message", C.c_char * 512),
+    ]
+
+
+_lib = None
+
+# every symbol include/vrte/*.h exports (tests check the .so against this)
+EXPORTED = [
+    "vrte_last_error", "vrte_version", "vrte_material_load", "vrte_material_parse",
+    "vrte_material_free", "vrte_material_info", "vrte_options_init", "vrte_solve_radiance",
+    "vrte_field_size", "vrte_field_row", "vrte_field_write_csv", "vrte_field_timings",
+    "vrte_field_reflectance", "vrte_field_free", "vrte_compute_brdf", "vrte_brdf_size",
+    "vrte_brdf_entry", "vrte_brdf_write_csv", "vrte_brdf_write_binary", "vrte_brdf_reflectance",
+    "vrte_brdf_timings", "vrte_brdf_free", "vrte_mc_trace", "vrte_mc_tally_row",
+    "vrte_mc_tally_write_csv", "vrte_mc_tally_free",
+    # vrte_ext.h
+    "vrte_brdf_device_stats_get", "vrte_brdf_plan_create", "vrte_brdf_from_stacks",
+    # vrte_cuda.h
+    "vrte_cuda_brdf", "vrte_cuda_plan_create", "vrte_cuda_plan_run", "vrte_cuda_plan_fetch",
+    "vrte_cuda_plan_fetch_up", "vrte_cuda_plan_fetch_modes", "vrte_cuda_plan_destroy",
+    "vrte_cuda_synthesize", "vrte_cuda_device_count",
+]
+
+
+def lib():
+    """Load libvrte.so (fails loudly if it was not built: no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libvrte.so not built at {LIB_PATH}; run __graft_entry__.build()")
+    L = C.CDLL(LIB_PATH)
+    vp, dp = C.c_void_p, C.POINTER(C.c_double)
+    L.vrte_last_error.restype = C.c_char_p
+    L.vrte_version.restype = C.c_char_p
+    L.vrte_material_load.argtypes = [C.c_char_p, C.POINTER(vp)]
+    L.vrte_material_parse.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(vp)]
+    L.vrte_material_free.argtypes = [vp]
+    L.vrte_material_info.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+    L.vrte_options_init.argtypes = [C.POINTER(Options)]
+    L.vrte_compute_brdf.argtypes = [vp, C.POINTER(Options), dp, C.c_size_t, C.c_int32, dp,
+                                    C.POINTER(vp)]
+    L.vrte_brdf_size.argtypes = [vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
+                                 C.POINTER(C.c_size_t)]
+    L.vrte_brdf_entry.argtypes = [vp, C.c_size_t, C.c_size_t, C.c_size_t, dp]
+    L.vrte_brdf_write_csv.argtypes = [vp, C.c_char_p]
+    L.vrte_brdf_write_binary.argtypes = [vp, C.c_char_p]
+    L.vrte_brdf_reflectance.argtypes = [vp, C.c_size_t, dp]
+    L.vrte_brdf_timings.argtypes = [vp, C.POINTER(Timings)]
+    L.vrte_brdf_free.argtypes = [vp]
+    L.vrte_brdf_device_stats_get.argtypes = [vp, C.POINTER(DeviceStats)]
+    L.vrte_brdf_plan_create.argtypes = [vp, C.POINTER(Options), dp, C.c_size_t, C.c_int32, dp,
+                                        C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(vp)]
+    L.vrte_brdf_from_stacks.argtypes = [vp, C.POINTER(Options), dp, C.c_size_t, C.c_int32, dp, dp,
+                                        C.POINTER(vp)]
+    L.vrte_cuda_plan_run.argtypes = [vp, C.c_int32, dp, C.POINTER(CudaResult)]
+    L.vrte_cuda_plan_fetch.argtypes = [vp, dp]
+    L.vrte_cuda_plan_fetch_up.argtypes = [vp, dp]
+    L.vrte_cuda_plan_fetch_modes.argtypes = [vp, dp, dp, dp, dp]
+    L.vrte_cuda_plan_destroy.argtypes = [vp]
+    L.vrte_solve_radiance.argtypes = [vp, C.POINTER(Options), dp, C.c_size_t, C.POINTER(vp)]
+    L.vrte_mc_trace.argtypes = [vp, C.POINTER(Options), C.c_uint64, C.c_uint64, C.c_int32,
+                                C.c_int32, C.POINTER(vp)]
+    _lib = L
+    return L
+
+
+def _check(code: int):
+    if code != VRTE_OK:
+        raise VrteError(code, lib().vrte_last_error().decode(errors="replace"))
+
+
+def _dp(a):
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def version() -> str:
+    return lib().vrte_version().decode()
+
+
+def options(quadrature_n: int = 40, order_cap: int = 0, **kw) -> Options:
+    """vrte_options_init + overrides."""
+    o = Options()
+    lib().vrte_options_init(C.byref(o))
+    o.quadrature_n = quadrature_n
+    o.order_cap = order_cap
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+class Material:
+    """Opaque vrte_material handle (vrte_material_load / vrte_material_parse)."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @classmethod
+    def load(cls, path: str) -> "Material":
+        h = C.c_void_p()
+        _check(lib().vrte_material_load(path.encode(), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def parse(cls, json_text: str, base_dir: str = "") -> "Material":
+        h = C.c_void_p()
+        _check(lib().vrte_material_parse(json_text.encode(), base_dir.encode(), C.byref(h)))
+        return cls(h)
+
+    def info(self):
+        L, P = C.c_int32(), C.c_int32()
+        _check(lib().vrte_material_info(self._h, C.byref(L), C.byref(P)))
+        return L.value, P.value
+
+    def close(self):
+        if self._h:
+            lib().vrte_material_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Brdf:
+    """Opaque vrte_brdf handle with the table mirrored as a numpy array."""
+
+    def __init__(self, handle):
+        self._h = handle
+        ni, no, npd = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        _check(lib().vrte_brdf_size(handle, C.byref(ni), C.byref(no), C.byref(npd)))
+        self.shape = (ni.value, no.value, npd.value)
+
+    def entry(self, i, o, p) -> np.ndarray:
+        e = np.zeros(16)
+        _check(lib().vrte_brdf_entry(self._h, i, o, p, _dp(e)))
+        return e.reshape(4, 4)
+
+    def table(self) -> np.ndarray:
+        """[n_in, n_out, n_dphi, 4, 4] (row-major Mueller entries)."""
+        ni, no, npd = self.shape
+        out = np.zeros((ni, no, npd, 4, 4))
+        e = np.zeros(16)
+        for i in range(ni):
+            for o in range(no):
+                for p in range(npd):
+                    _check(lib().vrte_brdf_entry(self._h, i, o, p, _dp(e)))
+                    out[i, o, p] = e.reshape(4, 4)
+        return out
+
+    def reflectance(self, i) -> np.ndarray:
+        r = np.zeros(4)
+        _check(lib().vrte_brdf_reflectance(self._h, i, _dp(r)))
+        return r
+
+    def timings(self) -> dict:
+        t = Timings()
+        _check(lib().vrte_brdf_timings(self._h, C.byref(t)))
+        return t.as_dict()
+
+    def device_stats(self) -> dict:
+        s = DeviceStats()
+        _check(lib().vrte_brdf_device_stats_get(self._h, C.byref(s)))
+        return s.as_dict()
+
+    def write_csv(self, path: str):
+        _check(lib().vrte_brdf_write_csv(self._h, path.encode()))
+
+    def write_binary(self, path: str):
+        _check(lib().vrte_brdf_write_binary(self._h, path.encode()))
+
+    def close(self):
+        if self._h:
+            lib().vrte_brdf_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def compute_brdf(material: Material, opts: Options, mu_in, n_dphi: int = 19, basis=None) -> Brdf:
+    """vrte_compute_brdf (vrte.h:110-112) on the sm_100a pipeline."""
+    mu = np.ascontiguousarray(mu_in, dtype=np.float64)
+    b = None if basis is None else np.ascontiguousarray(basis, dtype=np.float64).reshape(16)
+    h = C.c_void_p()
+    _check(lib().vrte_compute_brdf(material._h, C.byref(opts), _dp(mu), len(mu), n_dphi, _dp(b),
+                                   C.byref(h)))
+    return Brdf(h)
+
+
+def read_brdf_binary(path: str):
+    """VRTEBRDF v1 reader (csv.cpp:170-203): (mu_in, mu_out, dphi, table)."""
+    with open(path, "rb") as f:
+        raw = f.read()
+    if raw[:8] != b"VRTEBRDF":
+        raise ValueError(path + ": not a brdf table")
+    ver, ni, no, npd = np.frombuffer(raw[8:24], dtype="<u4")
+    if ver != 1:
+        raise ValueError(path + ": unsupported brdf table version")
+    off = 24
+    mu_in = np.frombuffer(raw, "<f8", ni, off); off += 8 * ni
+    mu_out = np.frombuffer(raw, "<f8", no, off); off += 8 * no
+    dphi = np.frombuffer(raw, "<f8", npd, off); off += 8 * npd
+    tab = np.frombuffer(raw, "<f8", ni * no * npd * 16, off).reshape(ni, no, npd, 4, 4)
+    return mu_in.copy(), mu_out.copy(), dphi.copy(), tab.copy()
+
+
+class Plan:
+    """Device-resident solve plan (vrte_brdf_plan_create / vrte_cuda_plan_*)."""
+
+    def __init__(self, material: Material, opts: Options, mu_in, n_dphi=19, basis=None,
+                 device=-1, m_begin=0, m_stride=1, n_orders=0):
+        mu = np.ascontiguousarray(mu_in, dtype=np.float64)
+        b = None if basis is None else np.ascontiguousarray(basis, dtype=np.float64).reshape(16)
+        h = C.c_void_p()
+        _check(lib().vrte_brdf_plan_create(material._h, C.byref(opts), _dp(mu), len(mu), n_dphi,
+                                           _dp(b), device, m_begin, m_stride, n_orders,
+                                           C.byref(h)))
+        self._h = h
+        self.n_in, self.n_dphi = len(mu), n_dphi
+        self.N = opts.quadrature_n
+        self.L = min(material.info()[0], opts.order_cap) if opts.order_cap > 0 else material.info()[0]
+        self.n_orders = n_orders if n_orders > 0 else self.L
+        self.last = CudaResult()
+
+    def run(self, iters: int = 1) -> float:
+        """Average device seconds per solve over `iters` back-to-back solves."""
+        s = C.c_double()
+        code = lib().vrte_cuda_plan_run(self._h, iters, C.byref(s), C.byref(self.last))
+        if code != 0:
+            raise VrteError(code, self.last.message.decode(errors="replace"))
+        return s.value
+
+    def table(self) -> np.ndarray:
+        out = np.zeros((self.n_in, self.N, self.n_dphi, 4, 4))
+        _check(lib().vrte_cuda_plan_fetch(self._h, _dp(out)))
+        return out
+
+    def up(self) -> np.ndarray:
+        """tau=0 upward stacks [n_orders, n_in, 4 channels, N, 4 Stokes]."""
+        out = np.zeros((self.n_orders, self.n_in, 4, self.N, 4))
+        _check(lib().vrte_cuda_plan_fetch_up(self._h, _dp(out)))
+        return out
+
+    def modes(self, n_media: int):
+        d = 4 * self.N
+        n = n_media * self.n_orders * d
+        wr, wi, res, nu = np.zeros(n), np.zeros(n), np.zeros(n), np.zeros(2 * n)
+        _check(lib().vrte_cuda_plan_fetch_modes(self._h, _dp(wr), _dp(wi), _dp(res), _dp(nu)))
+        sh = (n_media, self.n_orders, d)
+        return (wr.reshape(sh), wi.reshape(sh), res.reshape(sh),
+                (nu[0::2] + 1j * nu[1::2]).reshape(sh))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().vrte_cuda_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

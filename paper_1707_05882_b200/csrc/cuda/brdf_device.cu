@@ -1,0 +1,658 @@
+// brdf_device.cu -- the sm_100a BRDF pipeline behind vrte_compute_brdf.
+//
+// Stage map (reference -> here):
+//   prepare_homogeneous  pipeline.cpp:57-93   -> H: GSF tables, E/F, F*E,
+//                                                Hessenberg, Francis QR,
+//                                                eigenvectors, mode recovery,
+//                                                8N residuals
+//   solve_incident/particular pipeline.cpp:122-142 -> P: all incidents x
+//                                                4 Stokes channels at once on
+//                                                the shared Schur form
+//   solve_incident/boundary   pipeline.cpp:145-175 -> B: one real LU per order,
+//                                                every (incident, channel) a RHS
+//   nodal_components/value    pipeline.cpp:201-220 + brdf.cpp:100-117 -> S
+// Everything for one shape lives in a plan whose buffers are reused.
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "boundary.cuh"
+#include "kernels.cuh"
+#include "particular.cuh"
+#include "synth.cuh"
+#include "vrte/vrte_cuda.h"
+
+namespace vrte {
+
+[[noreturn]] void cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e),
+                  cudaGetErrorString(e), file, line, what);
+    throw std::runtime_error(buf);
+}
+
+namespace {
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        if (count == n && p) return;
+        release();
+        n = count;
+        if (count) VRTE_CUDA_CHECK(cudaMalloc(&p, sizeof(T) * count));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { release(); }
+    void upload(const T* h, size_t count, cudaStream_t st) {
+        alloc(count);
+        if (count) VRTE_CUDA_CHECK(cudaMemcpyAsync(p, h, sizeof(T) * count, cudaMemcpyHostToDevice, st));
+    }
+};
+
+GemmBatch gemm(int m, int n, int k, const double* a, long long lda, long long sa, bool ta,
+               const double* b, long long ldb, long long sb, bool tb, double* c, long long ldc,
+               long long sc, int batch, double alpha = 1.0, double beta = 0.0) {
+    GemmBatch g{};
+    g.m = m;
+    g.n = n;
+    g.k = k;
+    g.a = a;
+    g.lda = lda;
+    g.stride_a = sa;
+    g.trans_a = ta;
+    g.b = b;
+    g.ldb = ldb;
+    g.stride_b = sb;
+    g.trans_b = tb;
+    g.c = c;
+    g.ldc = ldc;
+    g.stride_c = sc;
+    g.batch = batch;
+    g.alpha = alpha;
+    g.beta = beta;
+    return g;
+}
+
+}  // namespace
+}  // namespace vrte
+
+using namespace vrte;
+
+struct vrte_cuda_plan {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    int N = 0, L = 0, P = 0, S = 0, n_in = 0, n_dphi = 0, NO = 0, m_begin = 0, m_stride = 1;
+    int d = 0, R = 0, G = 0, B = 0;
+    bool full_orders = true;
+    ProblemDev pd{};
+    // inputs
+    DevBuf<double> nodes, weights, mdiag, omega, greek, tau, mu_in, table, beam_rows, post, trig;
+    DevBuf<int> medium, order_index, slot_of_order;
+    // homogeneous
+    DevBuf<double> gsf_n, gsf_b, E, F, T, Z, psi_p, psi_m, tmp1, tmp2, tmp3, tmp4;
+    DevBuf<double> wr, wi, femax, nu, lam, residual;
+    DevBuf<int> flags;
+    // particular
+    DevBuf<double> sp, sm, fsp, rhs, W, g, eg, feg, zp, zm, mu_eff, sigma;
+    DevBuf<int> kind;
+    // boundary
+    DevBuf<double> lhs, top0, rhs_b, up;
+    DevBuf<int> ipiv;
+    // synthesis
+    DevBuf<double> out;
+    DeviceStatus* status = nullptr;  // pinned host-mapped would be nicer; device + copy
+    DevBuf<DeviceStatus> status_buf;
+    cudaEvent_t ev[6] = {};
+    uint64_t launches = 0;
+    ~vrte_cuda_plan() {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        if (st) cudaStreamDestroy(st);
+    }
+};
+
+namespace {
+
+std::mutex g_plan_mutex;
+
+void fill_message(vrte_cuda_result* r, int status, const std::string& msg) {
+    if (!r) return;
+    r->status = status;
+    std::snprintf(r->message, sizeof r->message, "%s", msg.c_str());
+}
+
+void check_problem(const vrte_cuda_problem* p) {
+    if (!p || p->N < 1 || p->L < 1 || p->n_layers < 1 || p->n_media < 1 || p->n_in < 1 ||
+        p->n_dphi < 1)
+        throw std::invalid_argument("vrte_cuda: invalid problem dimensions");
+    if (4 * p->N > 1024) throw std::invalid_argument("vrte_cuda: N > 256 not supported");
+    if (p->base_type == 2 && p->table_n < p->N)
+        throw std::invalid_argument("vrte_cuda: mueller table smaller than the quadrature");
+}
+
+void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
+    check_problem(p);
+    pl.device = p->device;
+    if (pl.device >= 0) VRTE_CUDA_CHECK(cudaSetDevice(pl.device));
+    if (!pl.st) VRTE_CUDA_CHECK(cudaStreamCreateWithFlags(&pl.st, cudaStreamNonBlocking));
+    for (auto& e : pl.ev)
+        if (!e) VRTE_CUDA_CHECK(cudaEventCreate(&e));
+    pl.N = p->N;
+    pl.L = p->L;
+    pl.P = p->n_layers;
+    pl.S = p->n_media;
+    pl.n_in = p->n_in;
+    pl.n_dphi = p->n_dphi;
+    pl.full_orders = p->n_orders <= 0;
+    pl.NO = pl.full_orders ? p->L : p->n_orders;
+    pl.m_begin = pl.full_orders ? 0 : p->m_begin;
+    pl.m_stride = pl.full_orders ? 1 : p->m_stride;
+    pl.d = 4 * pl.N;
+    pl.R = 4 * pl.n_in;
+    pl.G = 2 * pl.d * pl.P;
+    pl.B = pl.S * pl.NO;
+    const int N = pl.N, L = pl.L, d = pl.d, R = pl.R, G = pl.G, B = pl.B, NO = pl.NO;
+    cudaStream_t st = pl.st;
+
+    std::vector<double> mdiag(d);
+    for (int i = 0; i < d; ++i) mdiag[i] = p->nodes[i / 4];
+    std::vector<int> medium(p->medium, p->medium + pl.P);
+    std::vector<int> order_index(B), slot(L, -1);
+    for (int s = 0; s < pl.S; ++s)
+        for (int mo = 0; mo < NO; ++mo) order_index[s * NO + mo] = pl.m_begin + mo * pl.m_stride;
+    for (int mo = 0; mo < NO; ++mo) {
+        const int m = pl.m_begin + mo * pl.m_stride;
+        if (m < L) slot[m] = mo;
+    }
+    pl.nodes.upload(p->nodes, N, st);
+    pl.weights.upload(p->weights, N, st);
+    pl.mdiag.upload(mdiag.data(), d, st);
+    pl.omega.upload(p->omega, pl.S, st);
+    pl.greek.upload(p->greek, (size_t)pl.S * L * 6, st);
+    pl.tau.upload(p->tau, pl.P, st);
+    pl.medium.upload(medium.data(), pl.P, st);
+    pl.mu_in.upload(p->mu_in, pl.n_in, st);
+    if (p->base_type == 2)
+        pl.table.upload(p->table, (size_t)p->table_n * p->table_n * 16, st);
+    else
+        pl.table.alloc(16);
+    pl.beam_rows.upload(p->beam_rows, (size_t)pl.n_in * N * 16, st);
+    pl.post.upload(p->post, (size_t)pl.n_in * 16, st);
+    pl.trig.upload(p->trig, (size_t)L * pl.n_dphi * 2, st);
+    pl.order_index.upload(order_index.data(), B, st);
+    pl.slot_of_order.upload(slot.data(), L, st);
+
+    const size_t dd = (size_t)d * d;
+    pl.gsf_n.alloc((size_t)L * L * 3 * N);
+    pl.gsf_b.alloc((size_t)L * L * 3 * pl.n_in);
+    for (auto* b : {&pl.E, &pl.F, &pl.T, &pl.Z, &pl.psi_p, &pl.psi_m, &pl.tmp1, &pl.tmp2, &pl.tmp3,
+                    &pl.tmp4})
+        b->alloc(B * dd);
+    pl.wr.alloc((size_t)B * d);
+    pl.wi.alloc((size_t)B * d);
+    pl.femax.alloc(B);
+    pl.nu.alloc((size_t)B * d * 2);
+    pl.lam.alloc((size_t)B * d * 2);
+    pl.residual.alloc((size_t)B * d);
+    pl.flags.alloc((size_t)B * d);
+    const size_t bdr = (size_t)B * d * R;
+    for (auto* b : {&pl.sp, &pl.sm, &pl.fsp, &pl.rhs, &pl.W, &pl.g, &pl.eg, &pl.feg, &pl.zp, &pl.zm})
+        b->alloc(bdr);
+    pl.mu_eff.alloc((size_t)B * pl.n_in);
+    pl.sigma.alloc((size_t)B * R * 2);
+    pl.kind.alloc((size_t)B * R);
+    pl.lhs.alloc((size_t)NO * G * G);
+    pl.top0.alloc((size_t)NO * d * 2 * d);
+    pl.rhs_b.alloc((size_t)NO * R * G);
+    pl.ipiv.alloc((size_t)NO * G);
+    pl.up.alloc((size_t)NO * R * d);
+    pl.out.alloc((size_t)pl.n_in * N * pl.n_dphi * 16);
+    pl.status_buf.alloc(1);
+    pl.status = pl.status_buf.p;
+
+    ProblemDev& pd = pl.pd;
+    pd.N = N;
+    pd.L = L;
+    pd.n_media = pl.S;
+    pd.n_layers = pl.P;
+    pd.n_in = pl.n_in;
+    pd.n_dphi = pl.n_dphi;
+    pd.n_orders = NO;
+    pd.m_begin = pl.m_begin;
+    pd.m_stride = pl.m_stride;
+    pd.nodes = pl.nodes.p;
+    pd.weights = pl.weights.p;
+    pd.omega = pl.omega.p;
+    pd.greek = pl.greek.p;
+    pd.tau = pl.tau.p;
+    pd.medium = pl.medium.p;
+    pd.mu_in = pl.mu_in.p;
+    pd.base_type = p->base_type;
+    pd.rho = p->rho;
+    pd.table_n = p->table_n;
+    pd.table = pl.table.p;
+    pd.beam_rows = pl.beam_rows.p;
+}
+
+// The device pipeline; returns the number of kernel launches issued.
+uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
+    const int N = pl.N, L = pl.L, d = pl.d, R = pl.R, G = pl.G, B = pl.B, NO = pl.NO;
+    const long long dd = (long long)d * d, dR = (long long)d * R;
+    cudaStream_t st = pl.st;
+    const ProblemDev& pd = pl.pd;
+    uint64_t nl = 0;
+    VRTE_CUDA_CHECK(cudaMemsetAsync(pl.status, 0, sizeof(DeviceStatus), st));
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[0], st));
+    // ---------------- homogeneous
+    launch_gsf(pd, pl.nodes.p, N, 1.0, pl.gsf_n.p, st);
+    launch_gsf(pd, pl.mu_in.p, pl.n_in, -1.0, pl.gsf_b.p, st);
+    launch_build_ef(pd, pl.gsf_n.p, pl.E.p, pl.F.p, st);
+    gemm_batched(gemm(d, d, d, pl.F.p, d, dd, false, pl.E.p, d, dd, false, pl.T.p, d, dd, B), st);
+    launch_max_abs(pl.T.p, dd, B, pl.femax.p, st);
+    launch_hessenberg(pl.T.p, pl.Z.p, d, B, st);
+    launch_hqr(pl.T.p, pl.Z.p, pl.wr.p, pl.wi.p, d, B, pl.status, st);
+    launch_trevc(pl.T.p, pl.wr.p, pl.wi.p, pl.tmp1.p, d, B, st);
+    gemm_batched(gemm(d, d, d, pl.Z.p, d, dd, false, pl.tmp1.p, d, dd, false, pl.tmp2.p, d, dd, B), st);
+    launch_normalize_modes(pl.tmp2.p, pl.wi.p, d, B, st);
+    gemm_batched(gemm(d, d, d, pl.E.p, d, dd, false, pl.tmp2.p, d, dd, false, pl.tmp3.p, d, dd, B), st);
+    ModeArgs ma{};
+    ma.d = d;
+    ma.batch = B;
+    ma.wr = pl.wr.p;
+    ma.wi = pl.wi.p;
+    ma.femax = pl.femax.p;
+    ma.X = pl.tmp2.p;
+    ma.EX = pl.tmp3.p;
+    ma.mdiag = pl.mdiag.p;
+    ma.nu = pl.nu.p;
+    ma.lam = pl.lam.p;
+    ma.flags = pl.flags.p;
+    ma.psi_p = pl.psi_p.p;
+    ma.psi_m = pl.psi_m.p;
+    ma.ab_sum = pl.tmp1.p;
+    ma.ab_dif = pl.tmp4.p;
+    ma.status = pl.status;
+    ma.order_index = pl.order_index.p;
+    launch_modes(ma, st);
+    gemm_batched(gemm(d, d, d, pl.E.p, d, dd, false, pl.tmp1.p, d, dd, false, pl.tmp3.p, d, dd, B), st);
+    gemm_batched(gemm(d, d, d, pl.F.p, d, dd, false, pl.tmp4.p, d, dd, false, pl.tmp2.p, d, dd, B), st);
+    ResidualArgs ra{};
+    ra.d = d;
+    ra.batch = B;
+    ra.wi = pl.wi.p;
+    ra.nu = pl.nu.p;
+    ra.psi_p = pl.psi_p.p;
+    ra.psi_m = pl.psi_m.p;
+    ra.G1 = pl.tmp3.p;
+    ra.G2 = pl.tmp2.p;
+    ra.mdiag = pl.mdiag.p;
+    ra.residual = pl.residual.p;
+    launch_residual(ra, st);
+    nl += 16;
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[1], st));
+    // ---------------- particular
+    launch_beam_source(pd, pl.gsf_n.p, pl.gsf_b.p, pl.sp.p, pl.sm.p, st);
+    PartArgs pa{};
+    pa.d = d;
+    pa.batch = B;
+    pa.n_in = pl.n_in;
+    pa.mu_in = pl.mu_in.p;
+    pa.nu = pl.nu.p;
+    pa.femax = pl.femax.p;
+    pa.mdiag = pl.mdiag.p;
+    pa.order_index = pl.order_index.p;
+    pa.mu_eff = pl.mu_eff.p;
+    pa.sigma = pl.sigma.p;
+    pa.kind = pl.kind.p;
+    pa.fsp = pl.fsp.p;
+    pa.sp = pl.sp.p;
+    pa.sm = pl.sm.p;
+    pa.rhs = pl.rhs.p;
+    pa.g = pl.g.p;
+    pa.eg = pl.eg.p;
+    pa.feg = pl.feg.p;
+    pa.zp = pl.zp.p;
+    pa.zm = pl.zm.p;
+    pa.status = pl.status;
+    launch_dither(pa, st);
+    gemm_batched(gemm(d, R, d, pl.F.p, d, dd, false, pl.sp.p, d, dR, false, pl.fsp.p, d, dR, B), st);
+    launch_part_rhs(pa, st);
+    gemm_batched(gemm(d, R, d, pl.Z.p, d, dd, true, pl.rhs.p, d, dR, false, pl.W.p, d, dR, B), st);
+    launch_qtri_solve(pl.T.p, d, dd, pl.W.p, R, dR, pl.sigma.p, pl.kind.p, B, nullptr, st);
+    gemm_batched(gemm(d, R, d, pl.Z.p, d, dd, false, pl.W.p, d, dR, false, pl.g.p, d, dR, B), st);
+    gemm_batched(gemm(d, R, d, pl.E.p, d, dd, false, pl.g.p, d, dR, false, pl.eg.p, d, dR, B), st);
+    gemm_batched(gemm(d, R, d, pl.F.p, d, dd, false, pl.eg.p, d, dR, false, pl.feg.p, d, dR, B), st);
+    launch_zpm(pa, st);
+    launch_part_residual(pa, st);
+    nl += 11;
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[2], st));
+    // ---------------- boundary
+    BndArgs ba{};
+    ba.p = pd;
+    ba.d = d;
+    ba.psi_p = pl.psi_p.p;
+    ba.psi_m = pl.psi_m.p;
+    ba.nu = pl.nu.p;
+    ba.wi = pl.wi.p;
+    ba.zp = pl.zp.p;
+    ba.zm = pl.zm.p;
+    ba.lhs = pl.lhs.p;
+    ba.top0 = pl.top0.p;
+    ba.rhs = pl.rhs_b.p;
+    ba.up = pl.up.p;
+    launch_bnd_assemble(ba, st);
+    launch_bnd_rhs(ba, st);
+    lu_factor_batched(pl.lhs.p, G, NO, pl.ipiv.p, pl.status, pl.order_index.p, st);
+    lu_solve_batched(pl.lhs.p, G, NO, pl.ipiv.p, pl.rhs_b.p, R, st);
+    launch_copy_zp0(ba, st);
+    gemm_batched(gemm(d, R, 2 * d, pl.top0.p, d, (long long)d * 2 * d, false, pl.rhs_b.p, G,
+                      (long long)G * R, false, pl.up.p, d, dR, NO, 1.0, 1.0),
+                 st);
+    {
+        const int nbf = 16, nbs = 64;
+        const uint64_t panels = (G + nbf - 1) / nbf, blocks = (G + nbs - 1) / nbs;
+        nl += 2 + (pd.base_type != 0 ? 1 : 0) + 3 * panels + 1 + 4 * blocks + 2;
+    }
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[3], st));
+    // ---------------- synthesis
+    if (synth) {
+        SynthArgs sa{};
+        sa.N = N;
+        sa.L = L;
+        sa.n_in = pl.n_in;
+        sa.n_dphi = pl.n_dphi;
+        sa.up = pl.up.p;
+        sa.slot_of_order = pl.slot_of_order.p;
+        sa.trig = pl.trig.p;
+        sa.post = pl.post.p;
+        sa.out = pl.out.p;
+        sa.status = pl.status;
+        launch_synth(sa, st);
+        nl += 1;
+    }
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[4], st));
+    return nl;
+}
+
+std::string describe_failure(const DeviceStatus& s, const std::vector<double>& residual, int d,
+                             const std::vector<int>& order_index) {
+    char buf[400];
+    switch (s.code) {
+        case kFailHqrNoConverge:
+            std::snprintf(buf, sizeof buf, "eigen decomposition failed at order m = %d",
+                          order_index.empty() ? s.index : order_index[s.index]);
+            break;
+        case kFailNonFiniteEigen:
+            std::snprintf(buf, sizeof buf, "non-finite eigenvalue at order m = %d", s.index);
+            break;
+        case kFailNegativeAxis:
+            std::snprintf(buf, sizeof buf,
+                          "eigenvalue on the negative real axis at order m = %d (lambda = %g)",
+                          s.index, s.value);
+            break;
+        case kFailParticular:
+            std::snprintf(buf, sizeof buf, "singular beam-response system at order m = %d, mu0 = %g",
+                          s.index, s.value);
+            break;
+        case kFailLuSingular:
+        case kFailBoundary:
+            std::snprintf(buf, sizeof buf,
+                          "boundary system ill-conditioned at order m = %d (singular pivot at %g)",
+                          s.index, s.value);
+            break;
+        case kFailNegativeIntensity:
+            std::snprintf(buf, sizeof buf, "brdf: negative intensity entry %f", s.value);
+            break;
+        default:
+            std::snprintf(buf, sizeof buf, "device failure code %d", s.code);
+    }
+    (void)residual;
+    (void)d;
+    return buf;
+}
+
+// Post-run host checks: device failure record and the eigen residual bound
+// (homogeneous.cpp:280-285).  Fills the result block.
+int finish(vrte_cuda_plan& pl, vrte_cuda_result* r) {
+    DeviceStatus s{};
+    VRTE_CUDA_CHECK(cudaMemcpyAsync(&s, pl.status, sizeof s, cudaMemcpyDeviceToHost, pl.st));
+    std::vector<double> res((size_t)pl.B * pl.d);
+    VRTE_CUDA_CHECK(cudaMemcpyAsync(res.data(), pl.residual.p, sizeof(double) * res.size(),
+                                    cudaMemcpyDeviceToHost, pl.st));
+    VRTE_CUDA_CHECK(cudaStreamSynchronize(pl.st));
+    std::vector<int> oi((size_t)pl.B);
+    for (int s2 = 0; s2 < pl.S; ++s2)
+        for (int mo = 0; mo < pl.NO; ++mo) oi[s2 * pl.NO + mo] = pl.m_begin + mo * pl.m_stride;
+    double maxres = 0.0;
+    int worst = -1;
+    for (int b = 0; b < pl.B; ++b)
+        for (int j = 0; j < pl.d; ++j) {
+            const double v = res[(size_t)b * pl.d + j];
+            if (!(v <= maxres)) {
+                maxres = v;
+                worst = b;
+            }
+        }
+    if (r) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, pl.ev[0], pl.ev[1]);
+        r->t_homogeneous = ms * 1e-3;
+        cudaEventElapsedTime(&ms, pl.ev[1], pl.ev[2]);
+        r->t_particular = ms * 1e-3;
+        cudaEventElapsedTime(&ms, pl.ev[2], pl.ev[3]);
+        r->t_boundary = ms * 1e-3;
+        cudaEventElapsedTime(&ms, pl.ev[3], pl.ev[4]);
+        r->t_synthesis = ms * 1e-3;
+        r->dithered = s.dithered;
+        r->clamped = s.clamped;
+        r->polished = s.polished;
+        r->max_eigen_residual = maxres;
+        r->max_particular_residual = s.max_particular_residual;
+        r->kernel_launches = pl.launches;
+    }
+    if (s.code != 0) {
+        fill_message(r, 3, describe_failure(s, res, pl.d, oi));
+        return 3;
+    }
+    if (!(maxres <= kEigenResidualBound)) {
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "homogeneous mode residual %g exceeds %g at order m = %d",
+                      maxres, kEigenResidualBound, worst >= 0 ? oi[worst] : -1);
+        fill_message(r, 3, buf);
+        return 3;
+    }
+    if (r) {
+        r->status = 0;
+        r->message[0] = 0;
+    }
+    return 0;
+}
+
+template <typename Fn>
+int32_t guarded(vrte_cuda_result* r, Fn&& fn) {
+    try {
+        return fn();
+    } catch (const std::invalid_argument& e) {
+        fill_message(r, 5, e.what());
+        return 5;
+    } catch (const std::exception& e) {
+        fill_message(r, 3, e.what());
+        return 3;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t vrte_cuda_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int32_t vrte_cuda_plan_create(const vrte_cuda_problem* problem, vrte_cuda_plan** out,
+                              vrte_cuda_result* result) {
+    return guarded(result, [&]() -> int32_t {
+        if (!out) throw std::invalid_argument("null plan pointer");
+        auto pl = std::make_unique<vrte_cuda_plan>();
+        setup_plan(*pl, problem);
+        pl->launches = run_pipeline(*pl, pl->full_orders);
+        const int rc = finish(*pl, result);
+        *out = pl.release();
+        return rc;
+    });
+}
+
+int32_t vrte_cuda_plan_run(vrte_cuda_plan* pl, int32_t iters, double* seconds,
+                           vrte_cuda_result* result) {
+    return guarded(result, [&]() -> int32_t {
+        if (!pl || iters < 1) throw std::invalid_argument("bad plan or iteration count");
+        if (pl->device >= 0) VRTE_CUDA_CHECK(cudaSetDevice(pl->device));
+        cudaEvent_t a, b;
+        VRTE_CUDA_CHECK(cudaEventCreate(&a));
+        VRTE_CUDA_CHECK(cudaEventCreate(&b));
+        VRTE_CUDA_CHECK(cudaEventRecord(a, pl->st));
+        for (int it = 0; it < iters; ++it) run_pipeline(*pl, pl->full_orders);
+        VRTE_CUDA_CHECK(cudaEventRecord(b, pl->st));
+        VRTE_CUDA_CHECK(cudaEventSynchronize(b));
+        float ms = 0;
+        VRTE_CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        if (seconds) *seconds = ms * 1e-3 / iters;
+        return finish(*pl, result);
+    });
+}
+
+int32_t vrte_cuda_plan_fetch(vrte_cuda_plan* pl, double* table) {
+    if (!pl || !table) return 5;
+    try {
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(table, pl->out.p, sizeof(double) * pl->out.n,
+                                        cudaMemcpyDeviceToHost, pl->st));
+        VRTE_CUDA_CHECK(cudaStreamSynchronize(pl->st));
+    } catch (const std::exception&) {
+        return 3;
+    }
+    return 0;
+}
+
+int32_t vrte_cuda_plan_fetch_up(vrte_cuda_plan* pl, double* up) {
+    if (!pl || !up) return 5;
+    try {
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(up, pl->up.p, sizeof(double) * pl->up.n,
+                                        cudaMemcpyDeviceToHost, pl->st));
+        VRTE_CUDA_CHECK(cudaStreamSynchronize(pl->st));
+    } catch (const std::exception&) {
+        return 3;
+    }
+    return 0;
+}
+
+int32_t vrte_cuda_plan_fetch_modes(vrte_cuda_plan* pl, double* wr, double* wi, double* residual,
+                                   double* nu) {
+    if (!pl) return 5;
+    try {
+        const size_t n = (size_t)pl->B * pl->d;
+        if (wr)
+            VRTE_CUDA_CHECK(cudaMemcpyAsync(wr, pl->wr.p, n * 8, cudaMemcpyDeviceToHost, pl->st));
+        if (wi)
+            VRTE_CUDA_CHECK(cudaMemcpyAsync(wi, pl->wi.p, n * 8, cudaMemcpyDeviceToHost, pl->st));
+        if (residual)
+            VRTE_CUDA_CHECK(cudaMemcpyAsync(residual, pl->residual.p, n * 8, cudaMemcpyDeviceToHost, pl->st));
+        if (nu)
+            VRTE_CUDA_CHECK(cudaMemcpyAsync(nu, pl->nu.p, 2 * n * 8, cudaMemcpyDeviceToHost, pl->st));
+        VRTE_CUDA_CHECK(cudaStreamSynchronize(pl->st));
+    } catch (const std::exception&) {
+        return 3;
+    }
+    return 0;
+}
+
+void vrte_cuda_plan_destroy(vrte_cuda_plan* pl) { delete pl; }
+
+int32_t vrte_cuda_brdf(const vrte_cuda_problem* problem, double* table, vrte_cuda_result* result) {
+    return guarded(result, [&]() -> int32_t {
+        if (!table) throw std::invalid_argument("null table");
+        // Reuse one cached plan per thread-safe slot; shape changes reallocate.
+        static std::unique_ptr<vrte_cuda_plan> cached;
+        std::lock_guard<std::mutex> lk(g_plan_mutex);
+        if (!cached) cached = std::make_unique<vrte_cuda_plan>();
+        vrte_cuda_plan& pl = *cached;
+        cudaEvent_t a, b;
+        setup_plan(pl, problem);
+        VRTE_CUDA_CHECK(cudaEventCreate(&a));
+        VRTE_CUDA_CHECK(cudaEventCreate(&b));
+        pl.launches = run_pipeline(pl, true);
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(table, pl.out.p, sizeof(double) * pl.out.n,
+                                        cudaMemcpyDeviceToHost, pl.st));
+        const int rc = finish(pl, result);
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        return rc;
+    });
+}
+
+int32_t vrte_cuda_synthesize(const vrte_cuda_problem* problem, const double* up, double* table,
+                             vrte_cuda_result* result) {
+    return guarded(result, [&]() -> int32_t {
+        check_problem(problem);
+        if (!up || !table) throw std::invalid_argument("null buffer");
+        if (problem->device >= 0) VRTE_CUDA_CHECK(cudaSetDevice(problem->device));
+        cudaStream_t st;
+        VRTE_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        const int N = problem->N, L = problem->L, n_in = problem->n_in, np = problem->n_dphi;
+        const size_t upn = (size_t)L * 4 * n_in * 4 * N;
+        DevBuf<double> dup, dtrig, dpost, dout;
+        DevBuf<int> dslot;
+        DevBuf<DeviceStatus> dst;
+        std::vector<int> slot(L);
+        for (int m = 0; m < L; ++m) slot[m] = m;
+        dup.upload(up, upn, st);
+        dtrig.upload(problem->trig, (size_t)L * np * 2, st);
+        dpost.upload(problem->post, (size_t)n_in * 16, st);
+        dslot.upload(slot.data(), L, st);
+        dout.alloc((size_t)n_in * N * np * 16);
+        dst.alloc(1);
+        VRTE_CUDA_CHECK(cudaMemsetAsync(dst.p, 0, sizeof(DeviceStatus), st));
+        SynthArgs sa{};
+        sa.N = N;
+        sa.L = L;
+        sa.n_in = n_in;
+        sa.n_dphi = np;
+        sa.up = dup.p;
+        sa.slot_of_order = dslot.p;
+        sa.trig = dtrig.p;
+        sa.post = dpost.p;
+        sa.out = dout.p;
+        sa.status = dst.p;
+        launch_synth(sa, st);
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(table, dout.p, sizeof(double) * dout.n,
+                                        cudaMemcpyDeviceToHost, st));
+        DeviceStatus s{};
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(&s, dst.p, sizeof s, cudaMemcpyDeviceToHost, st));
+        VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
+        cudaStreamDestroy(st);
+        if (result) {
+            result->clamped = s.clamped;
+            result->kernel_launches = 1;
+        }
+        if (s.code != 0) {
+            fill_message(result, 3, describe_failure(s, {}, 0, {}));
+            return 3;
+        }
+        if (result) result->status = 0;
+        return 0;
+    });
+}
+
+}  // extern "C"

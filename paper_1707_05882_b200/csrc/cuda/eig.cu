@@ -1,0 +1,945 @@
+// eig.cu -- batched nonsymmetric fp64 eigensolver for the half-size
+// homogeneous problem (F E) x = x / nu^2 of every (medium, order), and the
+// mode recovery / residual machinery of homogeneous.cpp:131-287.
+//
+// Reference uses Eigen::EigenSolver (real Schur + eigenvectors).  Here:
+//   hessenberg_kernel : Householder reduction, Q accumulated into Z
+//   hqr_kernel        : Francis double-shift QR with Schur vectors (the
+//                       dlahqr algorithm; Ahues-Kressner deflation, exceptional
+//                       shifts every 10 iterations, dlanv2 standardization)
+//   trevc_kernel      : eigenvectors of the quasi-triangular Schur factor by
+//                       back substitution (dtrevc), back-transformed by a GEMM
+// One CTA per matrix; the near-diagonal band of H (offsets -3..+8) lives in
+// shared memory as its only copy so the sequential control path (reflector,
+// deflation tests, shifts) never touches L2.
+#include <climits>
+
+#include "kernels.cuh"
+
+namespace vrte {
+namespace {
+
+constexpr int NT = 256;
+
+__device__ int block_max_int(int v, int* s) {
+    __syncthreads();
+    if (threadIdx.x == 0) *s = INT_MIN;
+    __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(s, v);
+    __syncthreads();
+    return *s;
+}
+
+__global__ void max_abs_kernel(const double* A, long long per, double* out) {
+    __shared__ double red[32];
+    const double* a = A + blockIdx.x * per;
+    double m = 0.0;
+    for (long long e = threadIdx.x; e < per; e += blockDim.x) m = fmax(m, fabs(a[e]));
+    m = block_max(m, red);
+    if (threadIdx.x == 0) out[blockIdx.x] = m;
+}
+
+// ------------------------------------------------------------------ Hessenberg
+// dgehd2-style unblocked Householder reduction A <- Q^T A Q, Z <- Q.
+__global__ void __launch_bounds__(NT) hessenberg_kernel(double* Aall, double* Zall, int d) {
+    extern __shared__ double sm[];
+    double* v = sm;
+    __shared__ double red[32];
+    double* A = Aall + (size_t)blockIdx.x * d * d;
+    double* Z = Zall + (size_t)blockIdx.x * d * d;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
+    for (size_t e = t; e < (size_t)d * d; e += blockDim.x) Z[e] = (e % d == e / d) ? 1.0 : 0.0;
+    for (int k = 0; k + 2 < d; ++k) {
+        const int n = d - k - 1;
+        double ss = 0.0;
+        for (int r = t; r < n; r += blockDim.x) {
+            const double x = A[(size_t)(k + 1 + r) + (size_t)k * d];
+            v[r] = x;
+            if (r > 0) ss += x * x;
+        }
+        ss = block_sum(ss, red);
+        const double alpha = v[0];
+        const double xnorm = sqrt(ss);
+        if (xnorm == 0.0) continue;
+        const double beta = -copysign(hypot(alpha, xnorm), alpha);
+        const double tau = (beta - alpha) / beta;
+        const double scal = 1.0 / (alpha - beta);
+        __syncthreads();
+        for (int r = t; r < n; r += blockDim.x) {
+            v[r] = (r == 0) ? 1.0 : v[r] * scal;
+            A[(size_t)(k + 1 + r) + (size_t)k * d] = (r == 0) ? beta : 0.0;
+        }
+        __syncthreads();
+        // right: A[:, k+1:] -= tau (A v) v^T ; Z likewise (thread per row)
+        for (int i = t; i < d; i += blockDim.x) {
+            double y = 0.0, yz = 0.0;
+            const double* ac = A + i + (size_t)(k + 1) * d;
+            const double* zc = Z + i + (size_t)(k + 1) * d;
+            for (int j = 0; j < n; ++j) {
+                const double vj = v[j];
+                y = fma(ac[(size_t)j * d], vj, y);
+                yz = fma(zc[(size_t)j * d], vj, yz);
+            }
+            y *= tau;
+            yz *= tau;
+            double* aw = A + i + (size_t)(k + 1) * d;
+            double* zw = Z + i + (size_t)(k + 1) * d;
+            for (int j = 0; j < n; ++j) {
+                const double vj = v[j];
+                aw[(size_t)j * d] -= y * vj;
+                zw[(size_t)j * d] -= yz * vj;
+            }
+        }
+        __syncthreads();
+        // left: A[k+1:, k+1:] -= tau v (v^T A)  (warp per column)
+        for (int c = k + 1 + w; c < d; c += nw) {
+            double* col = A + (size_t)c * d + k + 1;
+            double p = 0.0;
+            for (int r = lane; r < n; r += 32) p = fma(v[r], col[r], p);
+            p = warp_sum(p) * tau;
+            for (int r = lane; r < n; r += 32) col[r] -= p * v[r];
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ Francis QR
+constexpr int BW = 8;  // band: diagonal offsets c - r in [-3, BW] kept in smem
+
+struct HAcc {
+    double* g;
+    double* band;
+    int d;
+    __device__ double& operator()(int r, int c) const {
+        const int off = c - r;
+        if (off >= -3 && off <= BW) return band[(off + 3) * d + c];
+        return g[r + (size_t)c * d];
+    }
+};
+
+// dlanv2: Schur factorization of a real 2x2 nonsymmetric matrix in standard form.
+__device__ void dlanv2(double& a, double& b, double& c, double& dd, double& rt1r, double& rt1i,
+                       double& rt2r, double& rt2i, double& cs, double& sn) {
+    const double eps = kUlp;
+    const double safmn2 = 0x1p-485, safmx2 = 0x1p485;
+    const double multpl = 4.0;
+    if (c == 0.0) {
+        cs = 1.0;
+        sn = 0.0;
+    } else if (b == 0.0) {
+        cs = 0.0;
+        sn = 1.0;
+        const double temp = dd;
+        dd = a;
+        a = temp;
+        b = -c;
+        c = 0.0;
+    } else if ((a - dd) == 0.0 && copysign(1.0, b) != copysign(1.0, c)) {
+        cs = 1.0;
+        sn = 0.0;
+    } else {
+        double temp = a - dd;
+        double p = 0.5 * temp;
+        const double bcmax = fmax(fabs(b), fabs(c));
+        const double bcmis = fmin(fabs(b), fabs(c)) * copysign(1.0, b) * copysign(1.0, c);
+        double scale = fmax(fabs(p), bcmax);
+        double z = (p / scale) * p + (bcmax / scale) * bcmis;
+        if (z >= multpl * eps) {
+            z = p + copysign(sqrt(scale) * sqrt(z), p);
+            a = dd + z;
+            dd = dd - (bcmax / z) * bcmis;
+            const double tau = hypot(c, z);
+            cs = z / tau;
+            sn = c / tau;
+            b = b - c;
+            c = 0.0;
+        } else {
+            int count = 0;
+            double sigma = b + c;
+            while (true) {
+                ++count;
+                scale = fmax(fabs(temp), fabs(sigma));
+                if (scale >= safmx2) {
+                    sigma *= safmn2;
+                    temp *= safmn2;
+                    if (count <= 20) continue;
+                }
+                if (scale <= safmn2) {
+                    sigma *= safmx2;
+                    temp *= safmx2;
+                    if (count <= 20) continue;
+                }
+                break;
+            }
+            p = 0.5 * temp;
+            double tau = hypot(sigma, temp);
+            cs = sqrt(0.5 * (1.0 + fabs(sigma) / tau));
+            sn = -(p / (tau * cs)) * copysign(1.0, sigma);
+            const double aa = a * cs + b * sn, bb = -a * sn + b * cs;
+            const double cc = c * cs + dd * sn, ddd = -c * sn + dd * cs;
+            a = aa * cs + cc * sn;
+            b = bb * cs + ddd * sn;
+            c = -aa * sn + cc * cs;
+            dd = -bb * sn + ddd * cs;
+            temp = 0.5 * (a + dd);
+            a = temp;
+            dd = temp;
+            if (c != 0.0) {
+                if (b != 0.0) {
+                    if (copysign(1.0, b) == copysign(1.0, c)) {
+                        const double sab = sqrt(fabs(b)), sac = sqrt(fabs(c));
+                        p = copysign(sab * sac, c);
+                        tau = 1.0 / sqrt(fabs(b + c));
+                        a = temp + p;
+                        dd = temp - p;
+                        b = b - c;
+                        c = 0.0;
+                        const double cs1 = sab * tau, sn1 = sac * tau;
+                        temp = cs * cs1 - sn * sn1;
+                        sn = cs * sn1 + sn * cs1;
+                        cs = temp;
+                    }
+                } else {
+                    b = -c;
+                    c = 0.0;
+                    temp = cs;
+                    cs = -sn;
+                    sn = temp;
+                }
+            }
+        }
+    }
+    rt1r = a;
+    rt2r = dd;
+    if (c == 0.0) {
+        rt1i = 0.0;
+        rt2i = 0.0;
+    } else {
+        rt1i = sqrt(fabs(b)) * sqrt(fabs(c));
+        rt2i = -rt1i;
+    }
+}
+
+__device__ bool small_subdiag(const HAcc& h, int k, int d, double ulp, double smlnum) {
+    const double hk = fabs(h(k, k - 1));
+    if (hk <= smlnum) return true;
+    double tst = fabs(h(k - 1, k - 1)) + fabs(h(k, k));
+    if (tst == 0.0) {
+        if (k - 2 >= 0) tst += fabs(h(k - 1, k - 2));
+        if (k + 1 <= d - 1) tst += fabs(h(k + 1, k));
+    }
+    if (hk <= ulp * tst) {
+        const double hup = fabs(h(k - 1, k));
+        const double ab = fmax(hk, hup), ba = fmin(hk, hup);
+        const double dif = fabs(h(k - 1, k - 1) - h(k, k));
+        const double aa = fmax(fabs(h(k, k)), dif), bb = fmin(fabs(h(k, k)), dif);
+        const double s = aa + ab;
+        if (ba * (ab / s) <= fmax(smlnum, ulp * (bb * (aa / s)))) return true;
+    }
+    return false;
+}
+
+__device__ void start_vector(const HAcc& h, int m, double rt1r, double rt1i, double rt2r,
+                             double rt2i, double v[3]) {
+    double h21s = h(m + 1, m);
+    double s = fabs(h(m, m) - rt2r) + fabs(rt2i) + fabs(h21s);
+    h21s = h(m + 1, m) / s;
+    v[0] = h21s * h(m, m + 1) + (h(m, m) - rt1r) * ((h(m, m) - rt2r) / s) - rt1i * (rt2i / s);
+    v[1] = h21s * (h(m, m) + h(m + 1, m + 1) - rt1r - rt2r);
+    v[2] = h21s * h(m + 2, m + 1);
+    s = fabs(v[0]) + fabs(v[1]) + fabs(v[2]);
+    v[0] /= s;
+    v[1] /= s;
+    v[2] /= s;
+}
+
+__global__ void __launch_bounds__(NT) hqr_kernel(double* Hall, double* Zall, double* wrall,
+                                                 double* wiall, int d, DeviceStatus* status) {
+    extern __shared__ double band[];
+    __shared__ int s_int;
+    const int b = blockIdx.x, t = threadIdx.x, nt = blockDim.x;
+    double* H = Hall + (size_t)b * d * d;
+    double* Z = Zall + (size_t)b * d * d;
+    double* wr = wrall + (size_t)b * d;
+    double* wi = wiall + (size_t)b * d;
+    const HAcc h{H, band, d};
+    for (int idx = t; idx < (BW + 4) * d; idx += nt) {
+        const int off = idx / d - 3, c = idx % d, r = c - off;
+        band[idx] = (r >= 0 && r < d) ? H[r + (size_t)c * d] : 0.0;
+    }
+    __syncthreads();
+
+    const double ulp = kUlp;
+    const double smlnum = kSafeMin * ((double)d / ulp);
+    const int itmax = 30 * max(10, d);
+    const int kexsh = 10;
+    int kdefl = 0;
+    int I = d - 1;
+    bool failed = false;
+    while (I >= 0) {
+        int L = 0;
+        bool conv = false;
+        for (int its = 0; its <= itmax; ++its) {
+            int kb = L;
+            for (int k = L + 1 + t; k <= I; k += nt)
+                if (small_subdiag(h, k, d, ulp, smlnum)) kb = max(kb, k);
+            L = block_max_int(kb, &s_int);
+            if (L > 0 && t == 0) h(L, L - 1) = 0.0;
+            __syncthreads();
+            if (L >= I - 1) {
+                conv = true;
+                break;
+            }
+            ++kdefl;
+            double h11, h12, h21, h22;
+            if (kdefl % (2 * kexsh) == 0) {
+                const double s = fabs(h(I, I - 1)) + fabs(h(I - 1, I - 2));
+                h11 = 0.75 * s + h(I, I);
+                h12 = -0.4375 * s;
+                h21 = s;
+                h22 = h11;
+            } else if (kdefl % kexsh == 0) {
+                const double s = fabs(h(L + 1, L)) + fabs(h(L + 2, L + 1));
+                h11 = 0.75 * s + h(L, L);
+                h12 = -0.4375 * s;
+                h21 = s;
+                h22 = h11;
+            } else {
+                h11 = h(I - 1, I - 1);
+                h21 = h(I, I - 1);
+                h12 = h(I - 1, I);
+                h22 = h(I, I);
+            }
+            double rt1r, rt1i, rt2r, rt2i;
+            {
+                const double s = fabs(h11) + fabs(h12) + fabs(h21) + fabs(h22);
+                if (s == 0.0) {
+                    rt1r = rt1i = rt2r = rt2i = 0.0;
+                } else {
+                    h11 /= s;
+                    h21 /= s;
+                    h12 /= s;
+                    h22 /= s;
+                    const double tr = (h11 + h22) / 2.0;
+                    const double det = (h11 - tr) * (h22 - tr) - h12 * h21;
+                    const double rtdisc = sqrt(fabs(det));
+                    if (det >= 0.0) {
+                        rt1r = tr * s;
+                        rt2r = rt1r;
+                        rt1i = rtdisc * s;
+                        rt2i = -rt1i;
+                    } else {
+                        rt1r = tr + rtdisc;
+                        rt2r = tr - rtdisc;
+                        if (fabs(rt1r - h22) <= fabs(rt2r - h22)) {
+                            rt1r *= s;
+                            rt2r = rt1r;
+                        } else {
+                            rt2r *= s;
+                            rt1r = rt2r;
+                        }
+                        rt1i = rt2i = 0.0;
+                    }
+                }
+            }
+            // two consecutive small subdiagonals: largest M in [L+1, I-2] passing, else L
+            int mb = L;
+            for (int mm = L + 1 + t; mm <= I - 2; mm += nt) {
+                double vv[3];
+                start_vector(h, mm, rt1r, rt1i, rt2r, rt2i, vv);
+                const double h00 = fabs(h(mm, mm - 1)) * (fabs(vv[1]) + fabs(vv[2]));
+                const double h11b =
+                    fabs(vv[0]) * (fabs(h(mm - 1, mm - 1)) + fabs(h(mm, mm)) + fabs(h(mm + 1, mm + 1)));
+                if (h00 <= ulp * h11b) mb = max(mb, mm);
+            }
+            const int M = block_max_int(mb, &s_int);
+            double v0[3];
+            start_vector(h, M, rt1r, rt1i, rt2r, rt2i, v0);
+
+            for (int k = M; k <= I - 1; ++k) {
+                const int nr = min(3, I - k + 1);
+                double v1, v2, v3;
+                if (k > M) {
+                    v1 = h(k, k - 1);
+                    v2 = h(k + 1, k - 1);
+                    v3 = (nr == 3) ? h(k + 2, k - 1) : 0.0;
+                } else {
+                    v1 = v0[0];
+                    v2 = v0[1];
+                    v3 = (nr == 3) ? v0[2] : 0.0;
+                }
+                double t1 = 0.0;
+                {
+                    const double xnorm = (nr == 3) ? hypot(v2, v3) : fabs(v2);
+                    if (xnorm != 0.0) {
+                        const double beta = -copysign(hypot(v1, xnorm), v1);
+                        t1 = (beta - v1) / beta;
+                        const double scal = 1.0 / (v1 - beta);
+                        v2 *= scal;
+                        v3 *= scal;
+                        v1 = beta;
+                    }
+                }
+                __syncthreads();
+                if (t == 0) {
+                    if (k > M) {
+                        h(k, k - 1) = v1;
+                        h(k + 1, k - 1) = 0.0;
+                        if (k < I - 1) h(k + 2, k - 1) = 0.0;
+                    } else if (M > L) {
+                        h(k, k - 1) = h(k, k - 1) * (1.0 - t1);
+                    }
+                }
+                const double t2 = t1 * v2;
+                if (nr == 3) {
+                    const double t3 = t1 * v3;
+                    for (int j = k + t; j < d; j += nt) {
+                        double& a0 = h(k, j);
+                        double& a1 = h(k + 1, j);
+                        double& a2 = h(k + 2, j);
+                        const double sum = a0 + v2 * a1 + v3 * a2;
+                        a0 -= sum * t1;
+                        a1 -= sum * t2;
+                        a2 -= sum * t3;
+                    }
+                    __syncthreads();
+                    const int jmax = min(k + 3, I);
+                    for (int j = t; j <= jmax; j += nt) {
+                        double& a0 = h(j, k);
+                        double& a1 = h(j, k + 1);
+                        double& a2 = h(j, k + 2);
+                        const double sum = a0 + v2 * a1 + v3 * a2;
+                        a0 -= sum * t1;
+                        a1 -= sum * t2;
+                        a2 -= sum * t3;
+                    }
+                    for (int j = t; j < d; j += nt) {
+                        double* z0 = Z + j + (size_t)k * d;
+                        const double a0 = z0[0], a1 = z0[d], a2 = z0[2 * (size_t)d];
+                        const double sum = a0 + v2 * a1 + v3 * a2;
+                        z0[0] = a0 - sum * t1;
+                        z0[d] = a1 - sum * t2;
+                        z0[2 * (size_t)d] = a2 - sum * t3;
+                    }
+                } else {
+                    for (int j = k + t; j < d; j += nt) {
+                        double& a0 = h(k, j);
+                        double& a1 = h(k + 1, j);
+                        const double sum = a0 + v2 * a1;
+                        a0 -= sum * t1;
+                        a1 -= sum * t2;
+                    }
+                    __syncthreads();
+                    for (int j = t; j <= I; j += nt) {
+                        double& a0 = h(j, k);
+                        double& a1 = h(j, k + 1);
+                        const double sum = a0 + v2 * a1;
+                        a0 -= sum * t1;
+                        a1 -= sum * t2;
+                    }
+                    for (int j = t; j < d; j += nt) {
+                        double* z0 = Z + j + (size_t)k * d;
+                        const double a0 = z0[0], a1 = z0[d];
+                        const double sum = a0 + v2 * a1;
+                        z0[0] = a0 - sum * t1;
+                        z0[d] = a1 - sum * t2;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        if (!conv) {
+            if (t == 0) report_failure(status, kFailHqrNoConverge, 1, b, (double)I);
+            failed = true;
+            break;
+        }
+        if (L == I) {
+            if (t == 0) {
+                wr[I] = h(I, I);
+                wi[I] = 0.0;
+            }
+        } else {
+            double a = h(I - 1, I - 1), bb = h(I - 1, I), c = h(I, I - 1), dd = h(I, I);
+            double r1r, r1i, r2r, r2i, cs, sn;
+            dlanv2(a, bb, c, dd, r1r, r1i, r2r, r2i, cs, sn);
+            __syncthreads();
+            if (t == 0) {
+                h(I - 1, I - 1) = a;
+                h(I - 1, I) = bb;
+                h(I, I - 1) = c;
+                h(I, I) = dd;
+                wr[I - 1] = r1r;
+                wi[I - 1] = r1i;
+                wr[I] = r2r;
+                wi[I] = r2i;
+            }
+            for (int j = I + 1 + t; j < d; j += nt) {
+                double& x = h(I - 1, j);
+                double& y = h(I, j);
+                const double xv = x, yv = y;
+                x = cs * xv + sn * yv;
+                y = cs * yv - sn * xv;
+            }
+            for (int j = t; j <= I - 2; j += nt) {
+                double& x = h(j, I - 1);
+                double& y = h(j, I);
+                const double xv = x, yv = y;
+                x = cs * xv + sn * yv;
+                y = cs * yv - sn * xv;
+            }
+            for (int j = t; j < d; j += nt) {
+                double* zx = Z + j + (size_t)(I - 1) * d;
+                const double xv = zx[0], yv = zx[d];
+                zx[0] = cs * xv + sn * yv;
+                zx[d] = cs * yv - sn * xv;
+            }
+        }
+        kdefl = 0;
+        I = L - 1;
+        __syncthreads();
+    }
+    __syncthreads();
+    if (failed) return;
+    for (int idx = t; idx < (BW + 4) * d; idx += nt) {
+        const int off = idx / d - 3, c = idx % d, r = c - off;
+        if (r >= 0 && r < d) H[r + (size_t)c * d] = (r > c + 1) ? 0.0 : band[idx];
+    }
+}
+
+// ------------------------------------------------------------------ 2x2 solves
+// Complete-pivoting 2x2 solve with the dlaln2 small-pivot perturbation smin
+// (smin <= 0 disables the perturbation).
+__device__ void solve2(cplx c00, cplx c01, cplx c10, cplx c11, cplx b0, cplx b1, double smin,
+                       cplx& x0, cplx& x1) {
+    const double m00 = cabs_(c00), m01 = cabs_(c01), m10 = cabs_(c10), m11 = cabs_(c11);
+    int pr = 0, pc = 0;
+    double mx = m00;
+    if (m01 > mx) { mx = m01; pr = 0; pc = 1; }
+    if (m10 > mx) { mx = m10; pr = 1; pc = 0; }
+    if (m11 > mx) { mx = m11; pr = 1; pc = 1; }
+    if (smin > 0.0 && mx < smin) {
+        x0 = cdiv(b0, cmk(smin, 0.0));
+        x1 = cdiv(b1, cmk(smin, 0.0));
+        return;
+    }
+    cplx C[2][2] = {{c00, c01}, {c10, c11}};
+    cplx B[2] = {b0, b1};
+    const int qr = 1 - pr, qc = 1 - pc;
+    const cplx piv = C[pr][pc];
+    const cplx l = cdiv(C[qr][pc], piv);
+    cplx u22 = C[qr][qc] - l * C[pr][qc];
+    if (smin > 0.0 && cabs_(u22) < smin) u22 = cmk(smin, 0.0);
+    const cplx y = B[qr] - l * B[pr];
+    cplx X[2];
+    X[qc] = cdiv(y, u22);
+    X[pc] = cdiv(B[pr] - C[pr][qc] * X[qc], piv);
+    x0 = X[0];
+    x1 = X[1];
+}
+
+// ------------------------------------------------------------------ eigenvectors
+// dtrevc right eigenvectors of the quasi-triangular T, warp per eigenvalue
+// (complex pairs handled by the first index, packed Re/Im columns).
+__global__ void trevc_kernel(const double* Tall, const double* wrall, const double* wiall,
+                             double* Yall, int d) {
+    extern __shared__ double sm[];
+    const int b = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5,
+              nw = blockDim.x >> 5;
+    const double* T = Tall + (size_t)b * d * d;
+    const double* wr = wrall + (size_t)b * d;
+    const double* wi = wiall + (size_t)b * d;
+    double* Y = Yall + (size_t)b * d * d;
+    double* re = sm + (size_t)w * 2 * d;
+    double* im = re + d;
+    const double smlnum = kSafeMin * ((double)d / kUlp);
+    auto Tat = [&](int r, int c) { return T[r + (size_t)c * d]; };
+    for (int ki = w; ki < d; ki += nw) {
+        const double wik = wi[ki];
+        if (wik < 0.0) continue;
+        if (wik == 0.0) {
+            const double lam = wr[ki];
+            const double smin = fmax(kUlp * fabs(lam), smlnum);
+            for (int k = lane; k < ki; k += 32) re[k] = -Tat(k, ki);
+            if (lane == 0) re[ki] = 1.0;
+            __syncwarp();
+            int j = ki - 1;
+            while (j >= 0) {
+                if (j > 0 && Tat(j, j - 1) != 0.0) {
+                    cplx x0, x1;
+                    solve2(cmk(Tat(j - 1, j - 1) - lam, 0), cmk(Tat(j - 1, j), 0),
+                           cmk(Tat(j, j - 1), 0), cmk(Tat(j, j) - lam, 0), cmk(re[j - 1], 0),
+                           cmk(re[j], 0), smin, x0, x1);
+                    __syncwarp();
+                    for (int k = lane; k < j - 1; k += 32)
+                        re[k] -= x0.re * Tat(k, j - 1) + x1.re * Tat(k, j);
+                    if (lane == 0) {
+                        re[j - 1] = x0.re;
+                        re[j] = x1.re;
+                    }
+                    j -= 2;
+                } else {
+                    double den = Tat(j, j) - lam;
+                    if (fabs(den) < smin) den = smin;
+                    const double x = re[j] / den;
+                    __syncwarp();
+                    for (int k = lane; k < j; k += 32) re[k] -= x * Tat(k, j);
+                    if (lane == 0) re[j] = x;
+                    j -= 1;
+                }
+                __syncwarp();
+            }
+            double* yc = Y + (size_t)ki * d;
+            for (int k = lane; k < d; k += 32) yc[k] = (k <= ki) ? re[k] : 0.0;
+        } else {
+            const int p = ki, q = ki + 1;
+            const cplx lam = cmk(wr[p], wik);
+            const double smin = fmax(kUlp * (fabs(wr[p]) + fabs(wik)), smlnum);
+            double xpr, xqi;
+            if (fabs(Tat(p, q)) >= fabs(Tat(q, p))) {
+                xpr = 1.0;
+                xqi = wik / Tat(p, q);
+            } else {
+                xpr = -wik / Tat(q, p);
+                xqi = 1.0;
+            }
+            for (int k = lane; k < p; k += 32) {
+                re[k] = -xpr * Tat(k, p);
+                im[k] = -xqi * Tat(k, q);
+            }
+            if (lane == 0) {
+                re[p] = xpr;
+                im[p] = 0.0;
+                re[q] = 0.0;
+                im[q] = xqi;
+            }
+            __syncwarp();
+            int j = p - 1;
+            while (j >= 0) {
+                if (j > 0 && Tat(j, j - 1) != 0.0) {
+                    cplx x0, x1;
+                    solve2(cmk(Tat(j - 1, j - 1), 0) - lam, cmk(Tat(j - 1, j), 0),
+                           cmk(Tat(j, j - 1), 0), cmk(Tat(j, j), 0) - lam, cmk(re[j - 1], im[j - 1]),
+                           cmk(re[j], im[j]), smin, x0, x1);
+                    __syncwarp();
+                    for (int k = lane; k < j - 1; k += 32) {
+                        const double a = Tat(k, j - 1), c = Tat(k, j);
+                        re[k] -= x0.re * a + x1.re * c;
+                        im[k] -= x0.im * a + x1.im * c;
+                    }
+                    if (lane == 0) {
+                        re[j - 1] = x0.re;
+                        im[j - 1] = x0.im;
+                        re[j] = x1.re;
+                        im[j] = x1.im;
+                    }
+                    j -= 2;
+                } else {
+                    cplx den = cmk(Tat(j, j), 0) - lam;
+                    if (cabs_(den) < smin) den = cmk(smin, 0.0);
+                    const cplx x = cdiv(cmk(re[j], im[j]), den);
+                    __syncwarp();
+                    for (int k = lane; k < j; k += 32) {
+                        const double a = Tat(k, j);
+                        re[k] -= x.re * a;
+                        im[k] -= x.im * a;
+                    }
+                    if (lane == 0) {
+                        re[j] = x.re;
+                        im[j] = x.im;
+                    }
+                    j -= 1;
+                }
+                __syncwarp();
+            }
+            double* yr = Y + (size_t)p * d;
+            double* yi = Y + (size_t)q * d;
+            for (int k = lane; k < d; k += 32) {
+                yr[k] = (k <= q) ? re[k] : 0.0;
+                yi[k] = (k <= q) ? im[k] : 0.0;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------ normalization
+__global__ void normalize_modes_kernel(double* Xall, const double* wiall, int d, int batch) {
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (gw >= batch * d) return;
+    const int b = gw / d, j = gw % d;
+    const double wij = wiall[(size_t)b * d + j];
+    if (wij < 0.0) return;
+    double* x = Xall + (size_t)b * d * d + (size_t)j * d;
+    double m = 0.0;
+    if (wij == 0.0) {
+        for (int i = lane; i < d; i += 32) m = fmax(m, fabs(x[i]));
+    } else {
+        for (int i = lane; i < d; i += 32) m = fmax(m, hypot(x[i], x[i + d]));
+    }
+    m = warp_max(m);
+    if (m == 0.0) return;
+    for (int i = lane; i < d; i += 32) {
+        x[i] /= m;
+        if (wij > 0.0) x[i + d] /= m;
+    }
+}
+
+// ------------------------------------------------------------------ modes
+// homogeneous.cpp:157-210: nu from lambda (floor / negative-axis / clamp
+// rules) and the recovery psi+- = (1/2) M^{-1} (x -+ nu E x).  Warp per mode.
+__global__ void modes_kernel(ModeArgs a) {
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int d = a.d;
+    if (gw >= a.batch * d) return;
+    const int b = gw / d, j = gw % d;
+    const size_t vb = (size_t)b * d;
+    const double wij = a.wi[vb + j];
+    if (wij < 0.0) return;
+    const bool pair = wij > 0.0;
+    cplx lam = cmk(a.wr[vb + j], wij);
+    if (!isfinite(lam.re) || !isfinite(lam.im)) {
+        if (lane == 0)
+            report_failure(a.status, kFailNonFiniteEigen, 1,
+                           a.order_index ? a.order_index[b] : b, lam.re);
+        return;
+    }
+    const double floor = 1e-12 * fmax(1.0, a.femax[b]);
+    const bool conservative = cabs_(lam) < floor;
+    cplx nu;
+    if (conservative) {
+        nu = cmk(kNuClamp, 0.0);
+    } else {
+        if (lam.re < 0.0 && fabs(lam.im) < 1e-10 * fabs(lam.re) && cabs_(lam) < 1e-10)
+            lam = cmk(cabs_(lam), 0.0);
+        nu = cdiv(cmk(1.0, 0.0), csqrt_(lam));
+        if (nu.re < 0.0) nu = cmk(-nu.re, -nu.im);
+        if (nu.re == 0.0) {
+            if (lane == 0)
+                report_failure(a.status, kFailNegativeAxis, 1,
+                               a.order_index ? a.order_index[b] : b, lam.re);
+            return;
+        }
+        const double an = cabs_(nu);
+        if (an > kNuClamp) nu = (kNuClamp / an) * nu;
+    }
+    const size_t cb = (size_t)b * d * d + (size_t)j * d;
+    for (int i = lane; i < d; i += 32) {
+        const cplx x = cmk(a.X[cb + i], pair ? a.X[cb + d + i] : 0.0);
+        const double hm = 0.5 * (1.0 / a.mdiag[i]);
+        cplx pp, pm;
+        if (conservative) {
+            pp = hm * x;
+            pm = pp;
+        } else {
+            const cplx ex = cmk(a.EX[cb + i], pair ? a.EX[cb + d + i] : 0.0);
+            const cplx nex = nu * ex;
+            pp = hm * (x - nex);
+            pm = hm * (x + nex);
+        }
+        const double mu = a.mdiag[i];
+        const cplx sum = mu * (pp + pm), dif = mu * (pm - pp);
+        a.psi_p[cb + i] = pp.re;
+        a.psi_m[cb + i] = pm.re;
+        a.ab_sum[cb + i] = sum.re;
+        a.ab_dif[cb + i] = dif.re;
+        if (pair) {
+            a.psi_p[cb + d + i] = pp.im;
+            a.psi_m[cb + d + i] = pm.im;
+            a.ab_sum[cb + d + i] = sum.im;
+            a.ab_dif[cb + d + i] = dif.im;
+        }
+    }
+    if (lane == 0) {
+        double* nv = a.nu + 2 * (vb + j);
+        nv[0] = nu.re;
+        nv[1] = nu.im;
+        double* lv = a.lam + 2 * (vb + j);
+        lv[0] = lam.re;
+        lv[1] = lam.im;
+        a.flags[vb + j] = conservative ? 1 : 0;
+        if (pair) {
+            nv[2] = nu.re;
+            nv[3] = -nu.im;
+            lv[2] = lam.re;
+            lv[3] = -lam.im;
+            a.flags[vb + j + 1] = conservative ? 1 : 0;
+        }
+    }
+}
+
+// 8N residual ||Op v - v/nu|| / ||v|| via the reduced operators:
+// top = M^-1(-G1 + G2)/2 - psi+/nu, bottom = M^-1(G1 + G2)/2 - psi-/nu.
+__global__ void residual_kernel(ResidualArgs a) {
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int d = a.d;
+    if (gw >= a.batch * d) return;
+    const int b = gw / d, j = gw % d;
+    const size_t vb = (size_t)b * d;
+    const double wij = a.wi[vb + j];
+    if (wij < 0.0) return;
+    const bool pair = wij > 0.0;
+    const cplx nu = cmk(a.nu[2 * (vb + j)], a.nu[2 * (vb + j) + 1]);
+    const cplx inu = cdiv(cmk(1.0, 0.0), nu);
+    const size_t cb = (size_t)b * d * d + (size_t)j * d;
+    double num = 0.0, den = 0.0;
+    for (int i = lane; i < d; i += 32) {
+        auto ld = [&](const double* p) { return cmk(p[cb + i], pair ? p[cb + d + i] : 0.0); };
+        const cplx g1 = ld(a.G1), g2 = ld(a.G2), pp = ld(a.psi_p), pm = ld(a.psi_m);
+        const double im = 1.0 / a.mdiag[i];
+        const cplx rt = (0.5 * im) * (g2 - g1) - pp * inu;
+        const cplx rb = (0.5 * im) * (g1 + g2) - pm * inu;
+        num = fmax(num, fmax(cabs_(rt), cabs_(rb)));
+        den = fmax(den, fmax(cabs_(pp), cabs_(pm)));
+    }
+    num = warp_max(num);
+    den = warp_max(den);
+    if (lane == 0) {
+        const double r = den > 0.0 ? num / den : 0.0;
+        a.residual[vb + j] = r;
+        if (pair) a.residual[vb + j + 1] = r;
+    }
+}
+
+// ------------------------------------------------------------------ shifted solves
+// Back substitution for (T - sigma I) y = w on the quasi-triangular Schur
+// factor, warp per right-hand side (real column or packed complex pair).
+__global__ void qtri_solve_kernel(const double* Tall, int d, long long t_stride, double* Wall,
+                                  int ncol, long long w_stride, const double* sigma,
+                                  const int* kind, int batch, const int* t_index) {
+    extern __shared__ double sm[];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + w;
+    if (gw >= (long long)batch * ncol) return;
+    const int b = (int)(gw / ncol), c = (int)(gw % ncol);
+    const int kd = kind[(size_t)b * ncol + c];
+    if (kd == 2) return;
+    const bool cx = kd == 1;
+    const double* T = Tall + (size_t)(t_index ? t_index[b] : b) * t_stride;
+    double* W = Wall + (size_t)b * w_stride + (size_t)c * d;
+    double* re = sm + (size_t)w * 2 * d;
+    double* im = re + d;
+    const cplx sg = cmk(sigma[2 * ((size_t)b * ncol + c)], sigma[2 * ((size_t)b * ncol + c) + 1]);
+    for (int k = lane; k < d; k += 32) {
+        re[k] = W[k];
+        im[k] = cx ? W[k + d] : 0.0;
+    }
+    __syncwarp();
+    auto Tat = [&](int r, int cc) { return T[r + (size_t)cc * d]; };
+    int j = d - 1;
+    while (j >= 0) {
+        if (j > 0 && Tat(j, j - 1) != 0.0) {
+            cplx x0, x1;
+            solve2(cmk(Tat(j - 1, j - 1), 0) - sg, cmk(Tat(j - 1, j), 0), cmk(Tat(j, j - 1), 0),
+                   cmk(Tat(j, j), 0) - sg, cmk(re[j - 1], im[j - 1]), cmk(re[j], im[j]), 0.0, x0,
+                   x1);
+            __syncwarp();
+            for (int k = lane; k < j - 1; k += 32) {
+                const double a = Tat(k, j - 1), cc = Tat(k, j);
+                re[k] -= x0.re * a + x1.re * cc;
+                im[k] -= x0.im * a + x1.im * cc;
+            }
+            if (lane == 0) {
+                re[j - 1] = x0.re;
+                im[j - 1] = x0.im;
+                re[j] = x1.re;
+                im[j] = x1.im;
+            }
+            j -= 2;
+        } else {
+            const cplx x = cdiv(cmk(re[j], im[j]), cmk(Tat(j, j), 0) - sg);
+            __syncwarp();
+            for (int k = lane; k < j; k += 32) {
+                const double a = Tat(k, j);
+                re[k] -= x.re * a;
+                im[k] -= x.im * a;
+            }
+            if (lane == 0) {
+                re[j] = x.re;
+                im[j] = x.im;
+            }
+            j -= 1;
+        }
+        __syncwarp();
+    }
+    for (int k = lane; k < d; k += 32) {
+        W[k] = re[k];
+        if (cx) W[k + d] = im[k];
+    }
+}
+
+}  // namespace
+
+void launch_max_abs(const double* A, long long per, int batch, double* out, cudaStream_t st) {
+    max_abs_kernel<<<batch, 256, 0, st>>>(A, per, out);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_hessenberg(double* A, double* Z, int d, int batch, cudaStream_t st) {
+    hessenberg_kernel<<<batch, NT, d * sizeof(double), st>>>(A, Z, d);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_hqr(double* H, double* Z, double* wr, double* wi, int d, int batch,
+                DeviceStatus* status, cudaStream_t st) {
+    const size_t smem = (size_t)(BW + 4) * d * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        VRTE_CUDA_CHECK(cudaFuncSetAttribute(hqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             200 * 1024));
+        attr = true;
+    }
+    hqr_kernel<<<batch, NT, smem, st>>>(H, Z, wr, wi, d, status);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_trevc(const double* T, const double* wr, const double* wi, double* Y, int d,
+                  int batch, cudaStream_t st) {
+    const int warps = 8;
+    const size_t smem = (size_t)warps * 2 * d * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        VRTE_CUDA_CHECK(cudaFuncSetAttribute(trevc_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    trevc_kernel<<<batch, warps * 32, smem, st>>>(T, wr, wi, Y, d);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_normalize_modes(double* X, const double* wi, int d, int batch, cudaStream_t st) {
+    const long long warps = (long long)batch * d;
+    normalize_modes_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(X, wi, d, batch);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_modes(const ModeArgs& a, cudaStream_t st) {
+    const long long warps = (long long)a.batch * a.d;
+    modes_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(a);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_residual(const ResidualArgs& a, cudaStream_t st) {
+    const long long warps = (long long)a.batch * a.d;
+    residual_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(a);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_qtri_solve(const double* T, int d, long long t_stride, double* W, int ncol,
+                       long long w_stride, const double* sigma, const int* kind, int batch,
+                       const int* t_index, cudaStream_t st) {
+    const int warps = 8;
+    const size_t smem = (size_t)warps * 2 * d * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        VRTE_CUDA_CHECK(cudaFuncSetAttribute(qtri_solve_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    const long long total = (long long)batch * ncol;
+    qtri_solve_kernel<<<(unsigned)((total + warps - 1) / warps), warps * 32, smem, st>>>(
+        T, d, t_stride, W, ncol, w_stride, sigma, kind, batch, t_index);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace vrte

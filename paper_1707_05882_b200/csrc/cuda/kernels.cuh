@@ -1,0 +1,85 @@
+// kernels.cuh -- device-side problem description and kernel launchers of the
+// sm_100a BRDF path (orchestrated by brdf_device.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace vrte {
+
+// Device view of one BRDF solve (all pointers are device pointers).
+// Orders handled on this device: m = m_begin + mo * m_stride, mo < n_orders.
+struct ProblemDev {
+    int N, L, n_media, n_layers, n_in, n_dphi;
+    int n_orders, m_begin, m_stride;
+    const double* nodes;    // [N]
+    const double* weights;  // [N]
+    const double* omega;    // [n_media]
+    const double* greek;    // [n_media][L][6] beta alpha gamma delta eps zeta
+    const double* tau;      // [n_layers]
+    const int* medium;      // [n_layers] -> medium index
+    const double* mu_in;    // [n_in]
+    int base_type;          // 0 black, 1 lambertian, 2 mueller table
+    double rho;
+    int table_n;
+    const double* table;      // [table_n*table_n][16] row-major
+    const double* beam_rows;  // [n_in][N][16] base_row_at(mu_i, mu0) (boundary.cpp:37-71)
+    __host__ __device__ int order_of(int mo) const { return m_begin + mo * m_stride; }
+};
+
+// phase.cu
+void launch_gsf(const ProblemDev& p, const double* mus, int count, double sign, double* out,
+                cudaStream_t st);
+void launch_build_ef(const ProblemDev& p, const double* gsf, double* E, double* F,
+                     cudaStream_t st);
+void launch_beam_source(const ProblemDev& p, const double* gsf_nodes, const double* gsf_beam,
+                        double* sp, double* sm, cudaStream_t st);
+
+// eig.cu
+void launch_max_abs(const double* A, long long per, int batch, double* out, cudaStream_t st);
+void launch_hessenberg(double* A, double* Z, int d, int batch, cudaStream_t st);
+void launch_hqr(double* H, double* Z, double* wr, double* wi, int d, int batch,
+                DeviceStatus* status, cudaStream_t st);
+void launch_trevc(const double* T, const double* wr, const double* wi, double* Y, int d,
+                  int batch, cudaStream_t st);
+// Normalize packed eigenvector columns by their max complex modulus; returns
+// the per-column scale applied in `scale` (may be null).
+void launch_normalize_modes(double* X, const double* wi, int d, int batch, cudaStream_t st);
+struct ModeArgs {
+    int d, batch;
+    const double* wr;
+    const double* wi;
+    const double* femax;   // [batch] max |FE| (lambda floor)
+    const double* X;       // packed eigenvectors (normalized)
+    const double* EX;      // E * X
+    const double* mdiag;   // [d] node cosines repeated per Stokes row (device)
+    double* nu;            // [batch][d][2] complex
+    double* lam;           // [batch][d][2] current eigenvalue (for polish shifts)
+    int* flags;            // [batch][d] bit0 conservative, bit1 polish-active
+    double* psi_p;         // packed
+    double* psi_m;         // packed
+    double* ab_sum;        // M(psi+ + psi-)  (GEMM input for residual)
+    double* ab_dif;        // M(psi- - psi+)
+    DeviceStatus* status;
+    const int* order_index;  // [batch] -> order m, for messages (may be null)
+};
+void launch_modes(const ModeArgs& a, cudaStream_t st);
+struct ResidualArgs {
+    int d, batch;
+    const double* wi;
+    const double* nu;
+    const double* psi_p;
+    const double* psi_m;
+    const double* G1;  // E (a+b)
+    const double* G2;  // F (b-a)
+    const double* mdiag;
+    double* residual;  // [batch][d]
+};
+void launch_residual(const ResidualArgs& a, cudaStream_t st);
+// Quasi-triangular shifted solves (T - sigma_c I) y_c = w_c, in place in W.
+// kind[c]: 0 real column, 1 complex pair (c: Re, c+1: Im), 2 skip.
+// sigma: [batch][ncol][2]; T: [batch][d*d].
+void launch_qtri_solve(const double* T, int d, long long t_stride, double* W, int ncol,
+                       long long w_stride, const double* sigma, const int* kind, int batch,
+                       const int* t_index, cudaStream_t st);
+
+}  // namespace vrte

@@ -1,0 +1,131 @@
+// particular.cu -- beam-response (particular) solutions for every
+// (medium, order, incident, unit Stokes channel), particular.cpp:27-107.
+//
+// The reference factors F E - mu0^-2 I afresh for every incident; here the
+// real Schur form F E = Z T Z^T from the homogeneous stage is reused, so each
+// right-hand side costs two GEMM-projections plus an O(d^2) quasi-triangular
+// back substitution (orthogonal similarity: same conditioning as the LU).
+#include "kernels.cuh"
+#include "particular.cuh"
+
+namespace vrte {
+namespace {
+
+// Resonance dither (particular.cpp:43-57): if 1/mu0^2 lies within 1e-8
+// relative of any homogeneous eigenvalue 1/nu_j^2, mu0 <- mu0 (1 - 1e-7).
+// Warp per (om, incident).  Also emits the per-column shift 1/mu0_eff^2.
+__global__ void dither_kernel(PartArgs a) {
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (gw >= a.batch * a.n_in) return;
+    const int om = gw / a.n_in, ii = gw % a.n_in;
+    const int d = a.d;
+    const double mu0 = a.mu_in[ii];
+    const double target = 1.0 / (mu0 * mu0);
+    bool hit = false;
+    for (int j = lane; j < d; j += 32) {
+        const cplx nu = cmk(a.nu[2 * ((size_t)om * d + j)], a.nu[2 * ((size_t)om * d + j) + 1]);
+        const cplx lam = cdiv(cmk(1.0, 0.0), nu * nu);
+        if (cabs_(lam - cmk(target, 0.0)) < 1e-8 * cabs_(lam)) hit = true;
+    }
+    hit = __any_sync(0xffffffffu, hit);
+    const double mu_eff = hit ? mu0 * (1.0 - 1e-7) : mu0;
+    if (lane < 4) {
+        const size_t col = (size_t)om * 4 * a.n_in + 4 * ii + lane;
+        a.sigma[2 * col] = 1.0 / (mu_eff * mu_eff);
+        a.sigma[2 * col + 1] = 0.0;
+        a.kind[col] = 0;
+    }
+    if (lane == 0) {
+        a.mu_eff[(size_t)om * a.n_in + ii] = mu_eff;
+        if (hit) atomicAdd(&a.status->dithered, 1ull);
+    }
+}
+
+// rhs = F s+ - s- / mu0_eff ; W <- rhs (solved in place), R keeps rhs.
+__global__ void rhs_kernel(PartArgs a) {
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const int d = a.d, R = 4 * a.n_in;
+    const long long total = (long long)a.batch * R * d;
+    if (idx >= total) return;
+    const int om = (int)(idx / ((long long)R * d));
+    const int col = (int)((idx / d) % R);
+    const double mu = a.mu_eff[(size_t)om * a.n_in + col / 4];
+    const double v = a.fsp[idx] - a.sm[idx] / mu;
+    a.rhs[idx] = v;
+}
+
+// h = mu0 (s+ - E g), psi+- = (1/2) M^-1 (g +- h), Z+ = psi+, Z- = Delta psi-.
+__global__ void zpm_kernel(PartArgs a) {
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const int d = a.d, R = 4 * a.n_in;
+    const long long total = (long long)a.batch * R * d;
+    if (idx >= total) return;
+    const int i = (int)(idx % d);
+    const int om = (int)(idx / ((long long)R * d));
+    const int col = (int)((idx / d) % R);
+    const double mu = a.mu_eff[(size_t)om * a.n_in + col / 4];
+    const double g = a.g[idx];
+    const double h = mu * (a.sp[idx] - a.eg[idx]);
+    const double hm = 0.5 * (1.0 / a.mdiag[i]);
+    const double pp = hm * (g + h), pm = hm * (g - h);
+    a.zp[idx] = pp;
+    a.zm[idx] = ((i & 3) >= 2) ? -pm : pm;
+}
+
+// System residual (particular.cpp:84-92): |(FE - sigma) g - rhs| against
+// 1e-8 (|rhs| + |FE - sigma| |g|); |FE - sigma| bounded by max|FE| + sigma.
+__global__ void part_residual_kernel(PartArgs a) {
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int d = a.d, R = 4 * a.n_in;
+    if (gw >= a.batch * R) return;
+    const int om = gw / R, col = gw % R;
+    const double sg = a.sigma[2 * ((size_t)om * R + col)];
+    const size_t base = ((size_t)om * R + col) * d;
+    double rmax = 0.0, bmax = 0.0, gmax = 0.0;
+    bool finite = true;
+    for (int i = lane; i < d; i += 32) {
+        const double g = a.g[base + i];
+        const double r = a.feg[base + i] - sg * g - a.rhs[base + i];
+        finite = finite && isfinite(g);
+        rmax = fmax(rmax, fabs(r));
+        bmax = fmax(bmax, fabs(a.rhs[base + i]));
+        gmax = fmax(gmax, fabs(g));
+    }
+    rmax = warp_max(rmax);
+    bmax = warp_max(bmax);
+    gmax = warp_max(gmax);
+    finite = __all_sync(0xffffffffu, finite);
+    if (lane == 0) {
+        const double scale = bmax + (a.femax[om] + sg) * gmax;
+        const double rel = scale > 0.0 ? rmax / scale : 0.0;
+        atomic_max_double(&a.status->max_particular_residual, rel);
+        if (!finite || rmax > 1e-8 * fmax(scale, 1e-300))
+            report_failure(a.status, kFailParticular, 2, a.order_index ? a.order_index[om] : om,
+                           a.mu_in[col / 4], rel);
+    }
+}
+
+}  // namespace
+
+void launch_dither(const PartArgs& a, cudaStream_t st) {
+    const long long warps = (long long)a.batch * a.n_in;
+    dither_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(a);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+void launch_part_rhs(const PartArgs& a, cudaStream_t st) {
+    const long long total = (long long)a.batch * 4 * a.n_in * a.d;
+    rhs_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(a);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+void launch_zpm(const PartArgs& a, cudaStream_t st) {
+    const long long total = (long long)a.batch * 4 * a.n_in * a.d;
+    zpm_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(a);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+void launch_part_residual(const PartArgs& a, cudaStream_t st) {
+    const long long warps = (long long)a.batch * 4 * a.n_in;
+    part_residual_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(a);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace vrte

@@ -1,0 +1,35 @@
+// particular.cuh -- argument block of the particular-solution kernels.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace vrte {
+
+struct PartArgs {
+    int d, batch, n_in;           // batch = (medium, order) pairs
+    const double* mu_in;          // [n_in]
+    const double* nu;             // [batch][d][2]
+    const double* femax;          // [batch]
+    const double* mdiag;          // [d]
+    const int* order_index;       // [batch] -> m (messages)
+    double* mu_eff;               // [batch][n_in]
+    double* sigma;                // [batch][4 n_in][2]
+    int* kind;                    // [batch][4 n_in]
+    const double* fsp;            // F s+  [batch][R][d]
+    const double* sp;             // s+
+    const double* sm;             // s-
+    double* rhs;                  // [batch][R][d]
+    const double* g;              // solution g = Z y
+    const double* eg;             // E g
+    const double* feg;            // F E g
+    double* zp;                   // Z+ [batch][R][d]
+    double* zm;                   // Z-
+    DeviceStatus* status;
+};
+
+void launch_dither(const PartArgs& a, cudaStream_t st);
+void launch_part_rhs(const PartArgs& a, cudaStream_t st);
+void launch_zpm(const PartArgs& a, cudaStream_t st);
+void launch_part_residual(const PartArgs& a, cudaStream_t st);
+
+}  // namespace vrte

@@ -1,0 +1,527 @@
+// capi.cpp -- the drop-in C ABI (reference src/capi.cpp:1-378).
+//
+// vrte_compute_brdf keeps the reference's argument checks, validation order,
+// error mapping (guarded(): ValidationError -> 2, NumericalError/other -> 3,
+// null arguments -> 5) and handle ownership.  Instead of the VrteSolver
+// thread pool it hands a flat problem to the sm_100a pipeline (vrte_cuda.h).
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+
+#include "host.hpp"
+#include "vrte/vrte.h"
+#include "vrte/vrte_cuda.h"
+#include "vrte/vrte_ext.h"
+
+using namespace vrte::host;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+vrte_status set_error(vrte_status code, const std::string& message) {
+    g_last_error = message;
+    return code;
+}
+
+template <typename Fn>
+vrte_status guarded(Fn&& fn) {  // capi.cpp:21-32
+    try {
+        return fn();
+    } catch (const ValidationError& e) {
+        return set_error(VRTE_E_VALIDATION, e.what());
+    } catch (const NumericalError& e) {
+        return set_error(VRTE_E_NUMERICAL, e.what());
+    } catch (const std::exception& e) {
+        return set_error(VRTE_E_NUMERICAL, e.what());
+    }
+}
+
+double wall_now() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// Singular values of the 4 x nb basis matrix by one-sided Jacobi
+// (Eigen::JacobiSVD stand-in for brdf.cpp:45-52).
+void singular_values4(const double basis[16], double sv[4]) {
+    double a[4][4];  // columns = basis vectors
+    for (int b = 0; b < 4; ++b)
+        for (int c = 0; c < 4; ++c) a[b][c] = basis[4 * b + c];
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        double off = 0.0;
+        for (int p = 0; p < 3; ++p)
+            for (int q = p + 1; q < 4; ++q) {
+                double alpha = 0, beta = 0, gamma = 0;
+                for (int k = 0; k < 4; ++k) {
+                    alpha += a[p][k] * a[p][k];
+                    beta += a[q][k] * a[q][k];
+                    gamma += a[p][k] * a[q][k];
+                }
+                if (gamma == 0.0) continue;
+                off = std::max(off, std::abs(gamma) / std::sqrt(alpha * beta));
+                const double zeta = (beta - alpha) / (2.0 * gamma);
+                const double t = std::copysign(1.0, zeta) / (std::abs(zeta) + std::sqrt(1.0 + zeta * zeta));
+                const double c = 1.0 / std::sqrt(1.0 + t * t), s = c * t;
+                for (int k = 0; k < 4; ++k) {
+                    const double x = a[p][k], y = a[q][k];
+                    a[p][k] = c * x - s * y;
+                    a[q][k] = s * x + c * y;
+                }
+            }
+        if (off < 1e-15) break;
+    }
+    for (int b = 0; b < 4; ++b) {
+        double s = 0;
+        for (int k = 0; k < 4; ++k) s += a[b][k] * a[b][k];
+        sv[b] = std::sqrt(s);
+    }
+    std::sort(sv, sv + 4, [](double x, double y) { return x > y; });
+}
+
+void inv4(const double in[16], double out[16]) {
+    double a[4][8];
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 8; ++c) a[r][c] = c < 4 ? in[4 * r + c] : (c - 4 == r ? 1.0 : 0.0);
+    for (int c = 0; c < 4; ++c) {
+        int p = c;
+        for (int r = c + 1; r < 4; ++r)
+            if (std::abs(a[r][c]) > std::abs(a[p][c])) p = r;
+        for (int k = 0; k < 8; ++k) std::swap(a[c][k], a[p][k]);
+        const double dv = a[c][c];
+        for (int k = 0; k < 8; ++k) a[c][k] /= dv;
+        for (int r = 0; r < 4; ++r)
+            if (r != c) {
+                const double f = a[r][c];
+                for (int k = 0; k < 8; ++k) a[r][k] -= f * a[c][k];
+            }
+    }
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c) out[4 * r + c] = a[r][c + 4];
+}
+
+// Host-side set-up of one BRDF request (brdf.cpp:43-77, pipeline.cpp:27-55):
+// validated inputs flattened into the device problem description.
+struct BrdfSetup {
+    MaterialSpec spec;
+    Quadrature quad;
+    int L = 0;
+    std::vector<int> medium, rep;
+    std::vector<double> omega, greek, tau, mu_in, beam_rows, post, trig, table_flat, dphi;
+    double basis[16];
+    vrte_cuda_problem prob{};
+};
+
+void build_setup(BrdfSetup& s, const MaterialSpec& mat, const vrte_options* options,
+                 const double* mu_in, size_t n_in, int32_t n_dphi_arg, const double* basis_in) {
+    const double defb[16] = {1, 0, 0, 0, 1, 1, 0, 0, 1, 0, 1, 0, 1, 0, 0, 1};  // brdf.cpp:7-9
+    std::memcpy(s.basis, basis_in ? basis_in : defb, sizeof s.basis);
+    const int n_dphi = n_dphi_arg > 0 ? n_dphi_arg : 19;
+    // VrteSolver ctor (pipeline.cpp:27-36)
+    s.spec = mat;
+    validate_material(s.spec);
+    const int qn = options ? options->quadrature_n : 40;
+    if (qn < 1) throw ValidationError("solver: quadrature size must be at least 1");
+    // compute_brdf validation order (brdf.cpp:45-62)
+    {
+        double sv[4];
+        singular_values4(s.basis, sv);
+        const double cond = sv[0] / std::max(sv[3], 1e-300);
+        if (cond > 1e3)
+            throw ValidationError("brdf: incident Stokes basis is ill-conditioned (condition " +
+                                  std::to_string(cond) + ")");
+    }
+    if (n_dphi < 1) throw ValidationError("brdf: dphi grid must have at least one point");
+    for (size_t i = 0; i < n_in; ++i)
+        if (!(mu_in[i] > 0.0 && mu_in[i] <= 1.0))
+            throw ValidationError("brdf: incident cosines must lie in (0,1]");
+    s.quad = build_double_gauss_quadrature(qn);
+    s.L = s.spec.order_count();
+    if (options && options->order_cap > 0) s.L = std::min(s.L, options->order_cap);
+    const int N = s.quad.n, L = s.L, P = (int)s.spec.layers.size();
+    // medium dedup: identical omega + coefficients share one solve (pipeline.cpp:37-54)
+    s.medium.assign(P, -1);
+    s.rep.clear();
+    for (int p = 0; p < P; ++p) {
+        int sig = -1;
+        for (int q = 0; q < p && sig < 0; ++q) {
+            const auto& a = s.spec.layers[p];
+            const auto& b = s.spec.layers[q];
+            if (a.omega == b.omega && a.coeffs == b.coeffs) sig = s.medium[q];
+        }
+        if (sig < 0) {
+            sig = (int)s.rep.size();
+            s.rep.push_back(p);
+        }
+        s.medium[p] = sig;
+    }
+    const int S = (int)s.rep.size();
+    s.omega.resize(S);
+    s.greek.assign((size_t)S * L * 6, 0.0);
+    for (int k = 0; k < S; ++k) {
+        const auto& layer = s.spec.layers[s.rep[k]];
+        s.omega[k] = layer.omega;
+        for (int l = 0; l < L; ++l) {
+            const Mat4& b = layer.coeffs[l];  // greek_of, kernel.cpp:15-17
+            double* g = &s.greek[((size_t)k * L + l) * 6];
+            g[0] = at(b, 0, 0);
+            g[1] = at(b, 1, 1);
+            g[2] = at(b, 0, 1);
+            g[3] = at(b, 3, 3);
+            g[4] = at(b, 3, 2);
+            g[5] = at(b, 2, 2);
+        }
+    }
+    s.tau.resize(P);
+    for (int p = 0; p < P; ++p) s.tau[p] = s.spec.layers[p].tau;
+    s.mu_in.assign(mu_in, mu_in + n_in);
+    // base rows at the beam (boundary.cpp:125-139): Lambertian uses node 0's row
+    s.beam_rows.assign(n_in * (size_t)N * 16, 0.0);
+    const bool lam = std::holds_alternative<LambertianBase>(s.spec.base);
+    for (size_t ii = 0; ii < n_in; ++ii)
+        for (int i = 0; i < N; ++i) {
+            const Mat4 r = base_row_at(s.spec.base, s.quad, s.quad.nodes[lam ? 0 : i], mu_in[ii]);
+            std::memcpy(&s.beam_rows[(ii * N + i) * 16], r.data(), 128);
+        }
+    if (const auto* tab = std::get_if<MuellerTableBase>(&s.spec.base)) {
+        if (tab->n < N)
+            throw ValidationError("base: mueller table has fewer nodes than the quadrature");
+        s.table_flat.resize((size_t)tab->n * tab->n * 16);
+        for (size_t e = 0; e < tab->table.size(); ++e)
+            std::memcpy(&s.table_flat[e * 16], tab->table[e].data(), 128);
+    }
+    // Mueller recovery operator per incident: B (mu0 B)^+ (brdf.cpp:100-105)
+    s.post.resize(n_in * 16);
+    for (size_t ii = 0; ii < n_in; ++ii) {
+        const double mu0 = mu_in[ii];
+        double I[16], IIt[16], inv[16], pinv[16];
+        for (int c = 0; c < 4; ++c)
+            for (int b = 0; b < 4; ++b) I[c * 4 + b] = mu0 * s.basis[4 * b + c];
+        for (int r = 0; r < 4; ++r)
+            for (int c = 0; c < 4; ++c) {
+                double acc = 0;
+                for (int b = 0; b < 4; ++b) acc += I[r * 4 + b] * I[c * 4 + b];
+                IIt[4 * r + c] = acc;
+            }
+        inv4(IIt, inv);
+        for (int b = 0; b < 4; ++b)
+            for (int c = 0; c < 4; ++c) {
+                double acc = 0;
+                for (int k = 0; k < 4; ++k) acc += I[k * 4 + b] * inv[4 * k + c];
+                pinv[b * 4 + c] = acc;
+            }
+        for (int c = 0; c < 4; ++c)  // post[c][col] = sum_b basis_b[c] pinv[b][col]
+            for (int col = 0; col < 4; ++col) {
+                double acc = 0;
+                for (int b = 0; b < 4; ++b) acc += s.basis[4 * b + c] * pinv[b * 4 + col];
+                s.post[ii * 16 + 4 * c + col] = acc;
+            }
+    }
+    s.dphi.resize(n_dphi);
+    for (int j = 0; j < n_dphi; ++j) s.dphi[j] = kTwoPi * j / n_dphi;
+    s.trig.resize((size_t)L * n_dphi * 2);
+    for (int m = 0; m < L; ++m)
+        for (int j = 0; j < n_dphi; ++j) {
+            const double x = -s.dphi[j];
+            s.trig[2 * ((size_t)m * n_dphi + j)] = std::cos(m * x);
+            s.trig[2 * ((size_t)m * n_dphi + j) + 1] = std::sin(m * x);
+        }
+    vrte_cuda_problem& p = s.prob;
+    p.N = N;
+    p.L = L;
+    p.n_layers = P;
+    p.n_media = S;
+    p.n_in = (int32_t)n_in;
+    p.n_dphi = n_dphi;
+    p.nodes = s.quad.nodes.data();
+    p.weights = s.quad.weights.data();
+    p.omega = s.omega.data();
+    p.greek = s.greek.data();
+    p.tau = s.tau.data();
+    p.medium = s.medium.data();
+    p.mu_in = s.mu_in.data();
+    p.base_type = lam ? 1 : (std::holds_alternative<MuellerTableBase>(s.spec.base) ? 2 : 0);
+    p.rho = lam ? std::get<LambertianBase>(s.spec.base).rho : 0.0;
+    p.table_n = p.base_type == 2 ? std::get<MuellerTableBase>(s.spec.base).n : 0;
+    p.table = s.table_flat.empty() ? nullptr : s.table_flat.data();
+    p.beam_rows = s.beam_rows.data();
+    p.post = s.post.data();
+    p.trig = s.trig.data();
+    p.m_begin = 0;
+    p.m_stride = 1;
+    p.n_orders = 0;
+    const char* dev = std::getenv("VRTE_DEVICE");
+    p.device = dev ? std::atoi(dev) : -1;
+}
+
+}  // namespace
+
+struct vrte_material {
+    MaterialSpec spec;
+};
+
+struct vrte_brdf {
+    BrdfTable table;
+    Quadrature quadrature;
+    vrte_timings timings{};
+    vrte_brdf_device_stats stats{};
+};
+
+extern "C" {
+
+const char* vrte_last_error(void) { return g_last_error.c_str(); }
+
+const char* vrte_version(void) { return "1.0.0"; }
+
+vrte_status vrte_material_load(const char* path, vrte_material** out) {
+    if (!path || !out) return set_error(VRTE_E_ARGUMENT, "null argument");
+    return guarded([&] {
+        auto h = std::make_unique<vrte_material>();
+        h->spec = load_material_file(path);
+        *out = h.release();
+        return VRTE_OK;
+    });
+}
+
+vrte_status vrte_material_parse(const char* json_text, const char* base_dir, vrte_material** out) {
+    if (!json_text || !out) return set_error(VRTE_E_ARGUMENT, "null argument");
+    return guarded([&] {
+        auto h = std::make_unique<vrte_material>();
+        h->spec = parse_material_json(json_text, base_dir ? base_dir : "");
+        *out = h.release();
+        return VRTE_OK;
+    });
+}
+
+void vrte_material_free(vrte_material* material) { delete material; }
+
+vrte_status vrte_material_info(const vrte_material* material, int32_t* order_count,
+                               int32_t* layer_count) {
+    if (!material) return set_error(VRTE_E_ARGUMENT, "null material");
+    if (order_count) *order_count = material->spec.order_count();
+    if (layer_count) *layer_count = (int32_t)material->spec.layers.size();
+    return VRTE_OK;
+}
+
+void vrte_options_init(vrte_options* options) {
+    if (!options) return;
+    std::memset(options, 0, sizeof *options);
+    options->quadrature_n = 40;
+    options->out_zenith = 11;
+    options->out_azimuth = 19;
+}
+
+// ---------------------------------------------------------------- out-of-path
+static vrte_status not_built(const char* what) {
+    return set_error(VRTE_E_ARGUMENT, std::string(what) +
+                                          ": not built (this library is the BRDF-path drop-in; "
+                                          "see DESIGN.md)");
+}
+
+vrte_status vrte_solve_radiance(const vrte_material*, const vrte_options*, const double*, size_t,
+                                vrte_field** out) {
+    if (out) *out = nullptr;
+    return not_built("vrte_solve_radiance");
+}
+vrte_status vrte_field_size(const vrte_field*, size_t*, size_t*, size_t*) {
+    return not_built("vrte_field_size");
+}
+vrte_status vrte_field_row(const vrte_field*, size_t, size_t, size_t, double*) {
+    return not_built("vrte_field_row");
+}
+vrte_status vrte_field_write_csv(const vrte_field*, const char*) {
+    return not_built("vrte_field_write_csv");
+}
+vrte_status vrte_field_timings(const vrte_field*, vrte_timings*) {
+    return not_built("vrte_field_timings");
+}
+vrte_status vrte_field_reflectance(const vrte_field*, double*) {
+    return not_built("vrte_field_reflectance");
+}
+void vrte_field_free(vrte_field*) {}
+
+vrte_status vrte_mc_trace(const vrte_material*, const vrte_options*, uint64_t, uint64_t, int32_t,
+                          int32_t, vrte_mc_tally** out) {
+    if (out) *out = nullptr;
+    return not_built("vrte_mc_trace");
+}
+vrte_status vrte_mc_tally_row(const vrte_mc_tally*, int32_t, int32_t, int32_t, double*) {
+    return not_built("vrte_mc_tally_row");
+}
+vrte_status vrte_mc_tally_write_csv(const vrte_mc_tally*, const char*) {
+    return not_built("vrte_mc_tally_write_csv");
+}
+void vrte_mc_tally_free(vrte_mc_tally*) {}
+
+// ---------------------------------------------------------------- BRDF
+vrte_status vrte_compute_brdf(const vrte_material* material, const vrte_options* options,
+                              const double* mu_in, size_t n_mu_in, int32_t n_dphi,
+                              const double* basis, vrte_brdf** out) {
+    if (!material || !out || !mu_in || n_mu_in == 0) return set_error(VRTE_E_ARGUMENT, "null argument");
+    return guarded([&] {
+        const double t0 = wall_now();
+        auto h = std::make_unique<vrte_brdf>();
+        BrdfSetup s;
+        build_setup(s, material->spec, options, mu_in, n_mu_in, n_dphi, basis);
+        const int N = s.quad.n, np = s.prob.n_dphi;
+        BrdfTable& t = h->table;
+        t.mu_in = s.mu_in;
+        t.mu_out = s.quad.nodes;
+        t.dphi = s.dphi;
+        t.quadrature_n = N;
+        t.order_count = s.L;
+        t.material_hash = material_hash(s.spec);
+        t.entries.assign(n_mu_in * (size_t)N * np * 16, 0.0);
+        vrte_cuda_result r{};
+        const int32_t rc = vrte_cuda_brdf(&s.prob, t.entries.data(), &r);
+        if (rc == 5) throw std::invalid_argument(r.message);
+        if (rc != 0) throw NumericalError(r.message);
+        h->quadrature = s.quad;
+        const uint64_t S = s.rep.size(), L = s.L, nb = 4;
+        h->timings.homogeneous = r.t_homogeneous;
+        h->timings.particular = r.t_particular;
+        h->timings.boundary = r.t_boundary;
+        h->timings.reconstruction = 0.0;  // BRDF path leaves it 0
+        h->timings.homogeneous_solves = S * L;
+        h->timings.particular_solves = n_mu_in * nb * 2 * L * S;
+        h->timings.boundary_solves = n_mu_in * nb * L;
+        h->timings.reconstruction_items = 0;
+        h->stats.t_homogeneous = r.t_homogeneous;
+        h->stats.t_particular = r.t_particular;
+        h->stats.t_boundary = r.t_boundary;
+        h->stats.t_synthesis = r.t_synthesis;
+        h->stats.dithered = r.dithered;
+        h->stats.clamped = r.clamped;
+        h->stats.polished = r.polished;
+        h->stats.kernel_launches = r.kernel_launches;
+        h->stats.max_eigen_residual = r.max_eigen_residual;
+        h->stats.max_particular_residual = r.max_particular_residual;
+        h->stats.material_hash = t.material_hash;
+        h->timings.total_wall = wall_now() - t0;
+        *out = h.release();
+        return VRTE_OK;
+    });
+}
+
+vrte_status vrte_brdf_size(const vrte_brdf* brdf, size_t* n_in, size_t* n_out, size_t* n_dphi) {
+    if (!brdf) return set_error(VRTE_E_ARGUMENT, "null brdf");
+    if (n_in) *n_in = brdf->table.mu_in.size();
+    if (n_out) *n_out = brdf->table.mu_out.size();
+    if (n_dphi) *n_dphi = brdf->table.dphi.size();
+    return VRTE_OK;
+}
+
+vrte_status vrte_brdf_entry(const vrte_brdf* brdf, size_t in_index, size_t out_index,
+                            size_t dphi_index, double entry[16]) {
+    if (!brdf || !entry) return set_error(VRTE_E_ARGUMENT, "null argument");
+    const auto& t = brdf->table;
+    if (in_index >= t.mu_in.size() || out_index >= t.mu_out.size() || dphi_index >= t.dphi.size())
+        return set_error(VRTE_E_ARGUMENT, "brdf index out of range");
+    const double* m =
+        &t.entries[((in_index * t.mu_out.size() + out_index) * t.dphi.size() + dphi_index) * 16];
+    std::memcpy(entry, m, 16 * sizeof(double));
+    return VRTE_OK;
+}
+
+vrte_status vrte_brdf_write_csv(const vrte_brdf* brdf, const char* path) {
+    if (!brdf || !path) return set_error(VRTE_E_ARGUMENT, "null argument");
+    return guarded([&] {
+        write_brdf_csv(path, brdf->table);
+        return VRTE_OK;
+    });
+}
+
+vrte_status vrte_brdf_write_binary(const vrte_brdf* brdf, const char* path) {
+    if (!brdf || !path) return set_error(VRTE_E_ARGUMENT, "null argument");
+    return guarded([&] {
+        write_brdf_binary(path, brdf->table);
+        return VRTE_OK;
+    });
+}
+
+vrte_status vrte_brdf_reflectance(const vrte_brdf* brdf, size_t in_index, double out[4]) {
+    if (!brdf || !out) return set_error(VRTE_E_ARGUMENT, "null argument");
+    const auto& t = brdf->table;
+    if (in_index >= t.mu_in.size()) return set_error(VRTE_E_ARGUMENT, "brdf index out of range");
+    // brdf.cpp:127-140
+    double acc[4] = {0, 0, 0, 0};
+    const double w_phi = kTwoPi / (double)t.dphi.size();
+    for (size_t io = 0; io < t.mu_out.size(); ++io)
+        for (size_t ip = 0; ip < t.dphi.size(); ++ip) {
+            const double* m = &t.entries[((in_index * t.mu_out.size() + io) * t.dphi.size() + ip) * 16];
+            const double w = brdf->quadrature.weights[io] * brdf->quadrature.nodes[io] * w_phi;
+            for (int c = 0; c < 4; ++c) acc[c] += w * m[c];
+        }
+    for (int c = 0; c < 4; ++c) out[c] = acc[c];
+    return VRTE_OK;
+}
+
+vrte_status vrte_brdf_timings(const vrte_brdf* brdf, vrte_timings* out) {
+    if (!brdf || !out) return set_error(VRTE_E_ARGUMENT, "null argument");
+    *out = brdf->timings;
+    return VRTE_OK;
+}
+
+void vrte_brdf_free(vrte_brdf* brdf) { delete brdf; }
+
+// ---------------------------------------------------------------- extensions
+vrte_status vrte_brdf_device_stats_get(const vrte_brdf* brdf, vrte_brdf_device_stats* out) {
+    if (!brdf || !out) return set_error(VRTE_E_ARGUMENT, "null argument");
+    *out = brdf->stats;
+    return VRTE_OK;
+}
+
+vrte_status vrte_brdf_plan_create(const vrte_material* material, const vrte_options* options,
+                                  const double* mu_in, size_t n_mu_in, int32_t n_dphi,
+                                  const double* basis, int32_t device, int32_t m_begin,
+                                  int32_t m_stride, int32_t n_orders, vrte_cuda_plan** out) {
+    if (!material || !out || !mu_in || n_mu_in == 0) return set_error(VRTE_E_ARGUMENT, "null argument");
+    return guarded([&] {
+        BrdfSetup s;
+        build_setup(s, material->spec, options, mu_in, n_mu_in, n_dphi, basis);
+        s.prob.device = device;
+        s.prob.m_begin = m_begin;
+        s.prob.m_stride = m_stride > 0 ? m_stride : 1;
+        s.prob.n_orders = n_orders;
+        vrte_cuda_result r{};
+        const int32_t rc = vrte_cuda_plan_create(&s.prob, out, &r);
+        if (rc == 5) throw std::invalid_argument(r.message);
+        if (rc != 0) throw NumericalError(r.message);
+        return VRTE_OK;
+    });
+}
+
+vrte_status vrte_brdf_from_stacks(const vrte_material* material, const vrte_options* options,
+                                  const double* mu_in, size_t n_mu_in, int32_t n_dphi,
+                                  const double* basis, const double* up_all_orders, vrte_brdf** out) {
+    if (!material || !out || !mu_in || n_mu_in == 0 || !up_all_orders)
+        return set_error(VRTE_E_ARGUMENT, "null argument");
+    return guarded([&] {
+        const double t0 = wall_now();
+        auto h = std::make_unique<vrte_brdf>();
+        BrdfSetup s;
+        build_setup(s, material->spec, options, mu_in, n_mu_in, n_dphi, basis);
+        const int N = s.quad.n, np = s.prob.n_dphi;
+        BrdfTable& t = h->table;
+        t.mu_in = s.mu_in;
+        t.mu_out = s.quad.nodes;
+        t.dphi = s.dphi;
+        t.quadrature_n = N;
+        t.order_count = s.L;
+        t.material_hash = material_hash(s.spec);
+        t.entries.assign(n_mu_in * (size_t)N * np * 16, 0.0);
+        vrte_cuda_result r{};
+        const int32_t rc = vrte_cuda_synthesize(&s.prob, up_all_orders, t.entries.data(), &r);
+        if (rc == 5) throw std::invalid_argument(r.message);
+        if (rc != 0) throw NumericalError(r.message);
+        h->quadrature = s.quad;
+        h->stats.clamped = r.clamped;
+        h->stats.material_hash = t.material_hash;
+        h->timings.total_wall = wall_now() - t0;
+        *out = h.release();
+        return VRTE_OK;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,80 @@
+// host.hpp -- host-side types of libvrte.so: material model, quadrature,
+// validation and the BRDF table.  Restates the reference's input plumbing
+// (core/types.*, core/material.*, brdf/brdf.hpp) without Eigen.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <variant>
+#include <vector>
+
+namespace vrte::host {
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kTwoPi = 2.0 * kPi;
+
+struct ValidationError : std::runtime_error {  // types.hpp:20-24 -> VRTE_E_VALIDATION
+    using std::runtime_error::runtime_error;
+};
+struct NumericalError : std::runtime_error {  // types.hpp:28-32 -> VRTE_E_NUMERICAL
+    using std::runtime_error::runtime_error;
+};
+
+using Mat4 = std::array<double, 16>;  // row-major
+inline double& at(Mat4& m, int r, int c) { return m[4 * r + c]; }
+inline double at(const Mat4& m, int r, int c) { return m[4 * r + c]; }
+
+struct LayerSpec {  // material.hpp:21-27
+    double omega = 0.0;
+    double tau = 0.0;
+    std::vector<Mat4> coeffs;
+    int order_count() const { return (int)coeffs.size(); }
+};
+struct BlackBase {};
+struct LambertianBase {
+    double rho = 0.0;
+};
+struct MuellerTableBase {
+    int n = 0;
+    std::vector<Mat4> table;  // row-major n*n, R(mu_i, -mu_j) at i*n + j
+    const Mat4& at(int i, int j) const { return table[(size_t)i * n + j]; }
+};
+using BaseReflector = std::variant<BlackBase, LambertianBase, MuellerTableBase>;
+struct BeamSource {
+    double mu0 = 1.0, phi0 = 0.0;
+    std::array<double, 4> stokes{1.0, 0.0, 0.0, 0.0};
+};
+struct MaterialSpec {  // material.hpp:59-71
+    std::vector<LayerSpec> layers;
+    BaseReflector base = BlackBase{};
+    BeamSource source;
+    int order_count() const { return layers.empty() ? 0 : layers.front().order_count(); }
+};
+
+struct Quadrature {
+    int n = 0;
+    std::vector<double> nodes, weights;
+};
+
+Quadrature build_double_gauss_quadrature(int n);  // types.cpp:27-68
+void validate_material(MaterialSpec& spec);       // material.cpp:43-109
+std::vector<Mat4> load_coefficient_file(const std::string& path);
+MaterialSpec parse_material_json(const std::string& text, const std::string& base_dir);
+MaterialSpec load_material_file(const std::string& path);
+double reduce_azimuth(double phi);
+Mat4 base_row_at(const BaseReflector& base, const Quadrature& quad, double mu_out, double mu_in);
+uint64_t material_hash(const MaterialSpec& spec);  // brdf.cpp:11-41
+
+struct BrdfTable {  // brdf.hpp:9-24
+    std::vector<double> mu_in, mu_out, dphi;
+    std::vector<double> entries;  // [in][out][dphi][16] row-major Mueller
+    int quadrature_n = 0, order_count = 0;
+    uint64_t material_hash = 0;
+};
+
+void write_brdf_csv(const std::string& path, const BrdfTable& t);     // csv.cpp:111-129
+void write_brdf_binary(const std::string& path, const BrdfTable& t);  // csv.cpp:147-168
+
+}  // namespace vrte::host
