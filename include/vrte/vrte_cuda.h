@@ -24,7 +24,8 @@ extern "C" {
 /* One BRDF problem after host-side set-up (brdf.cpp:43-77, pipeline.cpp:27-55). */
 typedef struct vrte_cuda_problem {
     int32_t N;            /* half-range quadrature nodes */
-    int32_t L;            /* Fourier orders (after order_cap) */
+    int32_t L;            /* Fourier orders (after order_cap, pipeline.cpp:33-35) */
+    int32_t L_coeffs;     /* expansion coefficients summed over l (kernel.cpp:30); 0 = L */
     int32_t n_layers;
     int32_t n_media;      /* distinct media after dedup (pipeline.cpp:37-54) */
     int32_t n_in;         /* incident cosines */
@@ -32,7 +33,7 @@ typedef struct vrte_cuda_problem {
     const double* nodes;    /* [N]  types.cpp:27-68 */
     const double* weights;  /* [N] */
     const double* omega;    /* [n_media] */
-    const double* greek;    /* [n_media][L][6]: beta alpha gamma delta eps zeta */
+    const double* greek;    /* [n_media][L_coeffs][6]: beta alpha gamma delta eps zeta */
     const double* tau;      /* [n_layers] */
     const int32_t* medium;  /* [n_layers] -> medium index */
     const double* mu_in;    /* [n_in] */
@@ -54,7 +55,13 @@ typedef struct vrte_cuda_result {
     double t_particular;
     double t_boundary;
     double t_synthesis;
-    double t_device;        /* whole device pipeline incl. H2D/D2H */
+    double t_device;        /* whole device pipeline (first to last kernel) */
+    double t_hessenberg;    /* per-kernel device seconds (CUDA events) */
+    double t_hqr;
+    double t_trevc;
+    double t_refine;
+    double t_lu_factor;
+    double t_lu_solve;
     uint64_t dithered;
     uint64_t clamped;
     uint64_t polished;
@@ -85,6 +92,8 @@ VRTE_API int32_t vrte_cuda_plan_fetch_up(vrte_cuda_plan* plan, double* up);
  * residual [n_media*n_orders][4N]. Any pointer may be NULL. */
 VRTE_API int32_t vrte_cuda_plan_fetch_modes(vrte_cuda_plan* plan, double* wr, double* wi,
                                             double* residual, double* nu);
+/* Reduced operators E, F [n_media*n_orders][4N*4N] column-major (debug/parity). */
+VRTE_API int32_t vrte_cuda_plan_fetch_ef(vrte_cuda_plan* plan, double* E, double* F);
 VRTE_API void vrte_cuda_plan_destroy(vrte_cuda_plan* plan);
 
 /* Fourier synthesis from host-gathered stacks of ALL orders (multi-GPU root):

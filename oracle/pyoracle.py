@@ -76,6 +76,7 @@ def lib():
         L.oracle_homogeneous.argtypes = [mp, C.c_int32, C.c_int32, C.c_int32, dp, dp, dp, dp]
         L.oracle_particular.argtypes = [mp, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                         C.c_double, dp, dp, dp, dp, dp]
+        L.oracle_set_accurate.argtypes = [C.c_int32]
         L.oracle_brdf.argtypes = [mp, C.c_int32, C.c_int32, C.c_int32, dp, C.c_size_t,
                                   C.c_int32, dp, dp, C.POINTER(OracleTimings), dp]
         _lib = L
@@ -120,6 +121,16 @@ class Material:
         return OracleMaterial(len(self.omega), self.coeffs.shape[1], _dp(self._keep[0]),
                               _dp(self._keep[1]), _dp(self._keep[2]), self.base_type,
                               float(self.rho), n, _dp(tab))
+
+
+class accurate:
+    """Context manager: run the oracle in accurate mode (see vrte_oracle.h)."""
+
+    def __enter__(self):
+        lib().oracle_set_accurate(1)
+
+    def __exit__(self, *exc):
+        lib().oracle_set_accurate(0)
 
 
 def quadrature(n):

@@ -50,6 +50,9 @@ typedef struct oracle_timings {
 const char* oracle_last_error(void);
 /* diagnostic: number of modes whose first recovery residual exceeded 5e-10 */
 uint64_t oracle_polish_count(void);
+/* 1: run the reference algorithm to its fp64 limit (polish every mode, refine
+ * every linear solve once); 0: exactly the reference's thresholds (default). */
+void oracle_set_accurate(int32_t on);
 
 /* types.cpp:27-68 */
 int32_t oracle_quadrature(int32_t n, double* nodes, double* weights);

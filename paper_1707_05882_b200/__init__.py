@@ -87,12 +87,23 @@ class DeviceStats(C.Structure):
 
 class CudaResult(C.Structure):
     """vrte_cuda_result (vrte_cuda.h)."""
+
+    def as_dict(self):
+        return {f: (getattr(self, f) if f != "message" else self.message.decode(errors="replace"))
+                for f, _ in self._fields_}
+
     _fields_ = [
         ("t_homogeneous", C.c_double),
         ("t_particular", C.c_double),
         ("t_boundary", C.c_double),
         ("t_synthesis", C.c_double),
         ("t_device", C.c_double),
+        ("t_hessenberg", C.c_double),
+        ("t_hqr", C.c_double),
+        ("t_trevc", C.c_double),
+        ("t_refine", C.c_double),
+        ("t_lu_factor", C.c_double),
+        ("t_lu_solve", C.c_double),
         ("dithered", C.c_uint64),
         ("clamped", C.c_uint64),
         ("polished", C.c_uint64),
@@ -119,7 +130,8 @@ EXPORTED = [
     "vrte_brdf_device_stats_get", "vrte_brdf_plan_create", "vrte_brdf_from_stacks",
     # vrte_cuda.h
     "vrte_cuda_brdf", "vrte_cuda_plan_create", "vrte_cuda_plan_run", "vrte_cuda_plan_fetch",
-    "vrte_cuda_plan_fetch_up", "vrte_cuda_plan_fetch_modes", "vrte_cuda_plan_destroy",
+    "vrte_cuda_plan_fetch_up", "vrte_cuda_plan_fetch_modes", "vrte_cuda_plan_fetch_ef",
+    "vrte_cuda_plan_destroy",
     "vrte_cuda_synthesize", "vrte_cuda_device_count",
 ]
 
@@ -160,6 +172,7 @@ def lib():
     L.vrte_cuda_plan_fetch_up.argtypes = [vp, dp]
     L.vrte_cuda_plan_fetch_modes.argtypes = [vp, dp, dp, dp, dp]
     L.vrte_cuda_plan_destroy.argtypes = [vp]
+    L.vrte_cuda_plan_fetch_ef.argtypes = [vp, dp, dp]
     L.vrte_solve_radiance.argtypes = [vp, C.POINTER(Options), dp, C.c_size_t, C.POINTER(vp)]
     L.vrte_mc_trace.argtypes = [vp, C.POINTER(Options), C.c_uint64, C.c_uint64, C.c_int32,
                                 C.c_int32, C.POINTER(vp)]
@@ -357,6 +370,15 @@ class Plan:
         sh = (n_media, self.n_orders, d)
         return (wr.reshape(sh), wi.reshape(sh), res.reshape(sh),
                 (nu[0::2] + 1j * nu[1::2]).reshape(sh))
+
+    def ef(self, n_media: int):
+        """Reduced operators E, F as [n_media, n_orders, d, d] (row index i, column j)."""
+        d = 4 * self.N
+        n = n_media * self.n_orders * d * d
+        E, F = np.zeros(n), np.zeros(n)
+        _check(lib().vrte_cuda_plan_fetch_ef(self._h, _dp(E), _dp(F)))
+        sh = (n_media, self.n_orders, d, d)
+        return E.reshape(sh).transpose(0, 1, 3, 2).copy(), F.reshape(sh).transpose(0, 1, 3, 2).copy()
 
     def close(self):
         if getattr(self, "_h", None):

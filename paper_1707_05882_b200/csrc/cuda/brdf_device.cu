@@ -92,6 +92,7 @@ using namespace vrte;
 struct vrte_cuda_plan {
     int device = 0;
     cudaStream_t st = nullptr;
+    int Lc = 0;
     int N = 0, L = 0, P = 0, S = 0, n_in = 0, n_dphi = 0, NO = 0, m_begin = 0, m_stride = 1;
     int d = 0, R = 0, G = 0, B = 0;
     bool full_orders = true;
@@ -114,8 +115,9 @@ struct vrte_cuda_plan {
     DevBuf<double> out;
     DeviceStatus* status = nullptr;  // pinned host-mapped would be nicer; device + copy
     DevBuf<DeviceStatus> status_buf;
-    cudaEvent_t ev[6] = {};
+    cudaEvent_t ev[16] = {};
     int refine_iters = 3;
+    int part_refine_iters = 2;
     uint64_t launches = 0;
     ~vrte_cuda_plan() {
         for (auto& e : ev)
@@ -151,8 +153,10 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     for (auto& e : pl.ev)
         if (!e) VRTE_CUDA_CHECK(cudaEventCreate(&e));
     if (const char* ri = std::getenv("VRTE_REFINE_ITERS")) pl.refine_iters = std::atoi(ri);
+    if (const char* pi = std::getenv("VRTE_PART_REFINE_ITERS")) pl.part_refine_iters = std::atoi(pi);
     pl.N = p->N;
     pl.L = p->L;
+    pl.Lc = p->L_coeffs > 0 ? p->L_coeffs : p->L;
     pl.P = p->n_layers;
     pl.S = p->n_media;
     pl.n_in = p->n_in;
@@ -182,7 +186,7 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pl.weights.upload(p->weights, N, st);
     pl.mdiag.upload(mdiag.data(), d, st);
     pl.omega.upload(p->omega, pl.S, st);
-    pl.greek.upload(p->greek, (size_t)pl.S * L * 6, st);
+    pl.greek.upload(p->greek, (size_t)pl.S * pl.Lc * 6, st);
     pl.tau.upload(p->tau, pl.P, st);
     pl.medium.upload(medium.data(), pl.P, st);
     pl.mu_in.upload(p->mu_in, pl.n_in, st);
@@ -197,8 +201,8 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pl.slot_of_order.upload(slot.data(), L, st);
 
     const size_t dd = (size_t)d * d;
-    pl.gsf_n.alloc((size_t)L * L * 3 * N);
-    pl.gsf_b.alloc((size_t)L * L * 3 * pl.n_in);
+    pl.gsf_n.alloc((size_t)L * pl.Lc * 3 * N);
+    pl.gsf_b.alloc((size_t)L * pl.Lc * 3 * pl.n_in);
     for (auto* b : {&pl.E, &pl.F, &pl.T, &pl.Z, &pl.psi_p, &pl.psi_m, &pl.tmp1, &pl.tmp2, &pl.tmp3,
                     &pl.tmp4, &pl.X})
         b->alloc(B * dd);
@@ -233,6 +237,7 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     ProblemDev& pd = pl.pd;
     pd.N = N;
     pd.L = L;
+    pd.Lc = pl.Lc;
     pd.n_media = pl.S;
     pd.n_layers = pl.P;
     pd.n_in = pl.n_in;
@@ -269,9 +274,13 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     launch_build_ef(pd, pl.gsf_n.p, pl.E.p, pl.F.p, st);
     gemm_batched(gemm(d, d, d, pl.F.p, d, dd, false, pl.E.p, d, dd, false, pl.T.p, d, dd, B), st);
     launch_max_abs(pl.T.p, dd, B, pl.femax.p, st);
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[5], st));
     launch_hessenberg(pl.T.p, pl.Z.p, d, B, st);
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[6], st));
     launch_hqr(pl.T.p, pl.Z.p, pl.wr.p, pl.wi.p, d, B, pl.status, st);
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[7], st));
     launch_trevc(pl.T.p, pl.wr.p, pl.wi.p, pl.tmp1.p, d, B, st);
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[8], st));
     gemm_batched(gemm(d, d, d, pl.Z.p, d, dd, false, pl.tmp1.p, d, dd, false, pl.X.p, d, dd, B), st);
     launch_normalize_modes(pl.X.p, pl.wi.p, d, B, st);
     gemm_batched(gemm(d, d, d, pl.E.p, d, dd, false, pl.X.p, d, dd, false, pl.tmp3.p, d, dd, B), st);
@@ -339,6 +348,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     rf.sigma = pl.sigma_m.p;
     rf.kind = pl.kind_m.p;
     const long long d2 = 2 * dd;
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[9], st));
     launch_nu_rho(rf, true, st);
     launch_refine_shift(rf, st);
     for (int it = 0; it < pl.refine_iters; ++it) {
@@ -355,6 +365,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
         nl += 11;
     }
     launch_nu_rho(rf, false, st);
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[10], st));
     launch_refine_normalize(rf, st);
     residual_gemms();
     launch_residual(ra, st);
@@ -392,6 +403,18 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     gemm_batched(gemm(d, R, d, pl.Z.p, d, dd, false, pl.W.p, d, dR, false, pl.g.p, d, dR, B), st);
     gemm_batched(gemm(d, R, d, pl.E.p, d, dd, false, pl.g.p, d, dR, false, pl.eg.p, d, dR, B), st);
     gemm_batched(gemm(d, R, d, pl.F.p, d, dd, false, pl.eg.p, d, dR, false, pl.feg.p, d, dR, B), st);
+    // Iterative refinement against the true operator F (E g): the Schur form
+    // carries a normwise backward error ~eps|FE| that the reference's dense LU
+    // (componentwise-small on this graded matrix) does not.
+    for (int it = 0; it < pl.part_refine_iters; ++it) {
+        launch_part_refine_residual(pa, pl.fsp.p, st);
+        gemm_batched(gemm(d, R, d, pl.Z.p, d, dd, true, pl.fsp.p, d, dR, false, pl.W.p, d, dR, B), st);
+        launch_qtri_solve(pl.T.p, d, dd, pl.W.p, R, dR, pl.sigma.p, pl.kind.p, B, nullptr, st);
+        gemm_batched(gemm(d, R, d, pl.Z.p, d, dd, false, pl.W.p, d, dR, false, pl.g.p, d, dR, B, 1.0, 1.0), st);
+        gemm_batched(gemm(d, R, d, pl.E.p, d, dd, false, pl.g.p, d, dR, false, pl.eg.p, d, dR, B), st);
+        gemm_batched(gemm(d, R, d, pl.F.p, d, dd, false, pl.eg.p, d, dR, false, pl.feg.p, d, dR, B), st);
+        nl += 6;
+    }
     launch_zpm(pa, st);
     launch_part_residual(pa, st);
     nl += 11;
@@ -412,8 +435,11 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     ba.up = pl.up.p;
     launch_bnd_assemble(ba, st);
     launch_bnd_rhs(ba, st);
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[11], st));
     lu_factor_batched(pl.lhs.p, G, NO, pl.ipiv.p, pl.status, pl.order_index.p, st);
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[12], st));
     lu_solve_batched(pl.lhs.p, G, NO, pl.ipiv.p, pl.rhs_b.p, R, st);
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[13], st));
     launch_copy_zp0(ba, st);
     gemm_batched(gemm(d, R, 2 * d, pl.top0.p, d, (long long)d * 2 * d, false, pl.rhs_b.p, G,
                       (long long)G * R, false, pl.up.p, d, dR, NO, 1.0, 1.0),
@@ -513,6 +539,18 @@ int finish(vrte_cuda_plan& pl, vrte_cuda_result* r) {
         r->t_boundary = ms * 1e-3;
         cudaEventElapsedTime(&ms, pl.ev[3], pl.ev[4]);
         r->t_synthesis = ms * 1e-3;
+        auto span = [&](int a, int b) {
+            float t = 0;
+            cudaEventElapsedTime(&t, pl.ev[a], pl.ev[b]);
+            return t * 1e-3;
+        };
+        r->t_device = span(0, 4);
+        r->t_hessenberg = span(5, 6);
+        r->t_hqr = span(6, 7);
+        r->t_trevc = span(7, 8);
+        r->t_refine = span(9, 10);
+        r->t_lu_factor = span(11, 12);
+        r->t_lu_solve = span(12, 13);
         r->dithered = s.dithered;
         r->clamped = s.clamped;
         r->polished = s.polished;
@@ -632,6 +670,19 @@ int32_t vrte_cuda_plan_fetch_modes(vrte_cuda_plan* pl, double* wr, double* wi, d
             VRTE_CUDA_CHECK(cudaMemcpyAsync(residual, pl->residual.p, n * 8, cudaMemcpyDeviceToHost, pl->st));
         if (nu)
             VRTE_CUDA_CHECK(cudaMemcpyAsync(nu, pl->nu.p, 2 * n * 8, cudaMemcpyDeviceToHost, pl->st));
+        VRTE_CUDA_CHECK(cudaStreamSynchronize(pl->st));
+    } catch (const std::exception&) {
+        return 3;
+    }
+    return 0;
+}
+
+int32_t vrte_cuda_plan_fetch_ef(vrte_cuda_plan* pl, double* E, double* F) {
+    if (!pl) return 5;
+    try {
+        const size_t n = (size_t)pl->B * pl->d * pl->d;
+        if (E) VRTE_CUDA_CHECK(cudaMemcpyAsync(E, pl->E.p, n * 8, cudaMemcpyDeviceToHost, pl->st));
+        if (F) VRTE_CUDA_CHECK(cudaMemcpyAsync(F, pl->F.p, n * 8, cudaMemcpyDeviceToHost, pl->st));
         VRTE_CUDA_CHECK(cudaStreamSynchronize(pl->st));
     } catch (const std::exception&) {
         return 3;

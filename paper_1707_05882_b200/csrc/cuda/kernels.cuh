@@ -9,12 +9,13 @@ namespace vrte {
 // Device view of one BRDF solve (all pointers are device pointers).
 // Orders handled on this device: m = m_begin + mo * m_stride, mo < n_orders.
 struct ProblemDev {
-    int N, L, n_media, n_layers, n_in, n_dphi;
+    int N, L, n_media, n_layers, n_in, n_dphi;  // L: Fourier orders (after order_cap)
+    int Lc;                                      // expansion-coefficient count (sum over l)
     int n_orders, m_begin, m_stride;
     const double* nodes;    // [N]
     const double* weights;  // [N]
     const double* omega;    // [n_media]
-    const double* greek;    // [n_media][L][6] beta alpha gamma delta eps zeta
+    const double* greek;    // [n_media][Lc][6] beta alpha gamma delta eps zeta
     const double* tau;      // [n_layers]
     const int* medium;      // [n_layers] -> medium index
     const double* mu_in;    // [n_in]

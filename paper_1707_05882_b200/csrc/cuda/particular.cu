@@ -105,7 +105,27 @@ __global__ void part_residual_kernel(PartArgs a) {
     }
 }
 
+// Iterative-refinement residual of the Schur-form solve, in place into W:
+// W = rhs - ((F E) g - sigma g), with F E g = F (E g) from the GEMMs (true
+// operator, not the Schur form).
+__global__ void refine_residual_kernel(PartArgs a, double* W) {
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const int d = a.d, R = 4 * a.n_in;
+    const long long total = (long long)a.batch * R * d;
+    if (idx >= total) return;
+    const int om = (int)(idx / ((long long)R * d));
+    const int col = (int)((idx / d) % R);
+    const double sg = a.sigma[2 * ((size_t)om * R + col)];
+    W[idx] = a.rhs[idx] - (a.feg[idx] - sg * a.g[idx]);
+}
+
 }  // namespace
+
+void launch_part_refine_residual(const PartArgs& a, double* W, cudaStream_t st) {
+    const long long total = (long long)a.batch * 4 * a.n_in * a.d;
+    refine_residual_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(a, W);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
 
 void launch_dither(const PartArgs& a, cudaStream_t st) {
     const long long warps = (long long)a.batch * a.n_in;

@@ -31,5 +31,6 @@ void launch_dither(const PartArgs& a, cudaStream_t st);
 void launch_part_rhs(const PartArgs& a, cudaStream_t st);
 void launch_zpm(const PartArgs& a, cudaStream_t st);
 void launch_part_residual(const PartArgs& a, cudaStream_t st);
+void launch_part_refine_residual(const PartArgs& a, double* W, cudaStream_t st);
 
 }  // namespace vrte

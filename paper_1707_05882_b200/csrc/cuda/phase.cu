@@ -27,11 +27,11 @@ __device__ double wigner_start(int m, int n, double x) {
 
 // One thread per (m, mu): the three d^l_{m n} sequences (n = 0, 2, -2) by the
 // upward recurrence (wigner.cpp:31-62), combined into P, R, T (wigner.cpp:64-81).
-// Output layout: out[((m*L + l)*3 + {P,R,T})*ld + mu_index].
-__global__ void gsf_kernel(int L, int count, const double* __restrict__ mus, double sign_mu,
-                           double* __restrict__ out, int ld) {
+// Output layout: out[((m*Lc + l)*3 + {P,R,T})*ld + mu_index], l < Lc (coefficient count).
+__global__ void gsf_kernel(int n_m, int L, int count, const double* __restrict__ mus,
+                           double sign_mu, double* __restrict__ out, int ld) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= L * count) return;
+    if (idx >= n_m * count) return;
     const int m = idx / count, iu = idx % count;
     const double x = sign_mu * mus[iu];
     const int lmax = L - 1;
@@ -84,7 +84,7 @@ __global__ void gsf_kernel(int L, int count, const double* __restrict__ mus, dou
 __global__ void build_ef_kernel(const ProblemDev p, const double* __restrict__ gsf,
                                 double* __restrict__ E, double* __restrict__ F) {
     const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    const int N = p.N, L = p.L, d = 4 * N;
+    const int N = p.N, L = p.Lc, d = 4 * N;
     const long long total = (long long)p.n_media * p.n_orders * N * N;
     if (idx >= total) return;
     const int i = (int)(idx % N);
@@ -170,7 +170,7 @@ __global__ void beam_source_kernel(const ProblemDev p, const double* __restrict_
                                    const double* __restrict__ gsf_beam, double* __restrict__ sp,
                                    double* __restrict__ sm) {
     const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    const int N = p.N, L = p.L, d = 4 * N, nin = p.n_in, R = 4 * nin;
+    const int N = p.N, L = p.Lc, d = 4 * N, nin = p.n_in, R = 4 * nin;
     const long long total = (long long)p.n_media * p.n_orders * nin * N;
     if (idx >= total) return;
     const int i = (int)(idx % N);
@@ -230,7 +230,7 @@ __global__ void beam_source_kernel(const ProblemDev p, const double* __restrict_
 void launch_gsf(const ProblemDev& p, const double* mus, int count, double sign, double* out,
                 cudaStream_t st) {
     const int total = p.L * count;
-    gsf_kernel<<<(total + 127) / 128, 128, 0, st>>>(p.L, count, mus, sign, out, count);
+    gsf_kernel<<<(total + 127) / 128, 128, 0, st>>>(p.L, p.Lc, count, mus, sign, out, count);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 

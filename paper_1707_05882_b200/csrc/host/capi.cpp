@@ -140,6 +140,7 @@ void build_setup(BrdfSetup& s, const MaterialSpec& mat, const vrte_options* opti
     s.L = s.spec.order_count();
     if (options && options->order_cap > 0) s.L = std::min(s.L, options->order_cap);
     const int N = s.quad.n, L = s.L, P = (int)s.spec.layers.size();
+    const int Lc = s.spec.order_count();  // the l-sum always spans every coefficient
     // medium dedup: identical omega + coefficients share one solve (pipeline.cpp:37-54)
     s.medium.assign(P, -1);
     s.rep.clear();
@@ -158,13 +159,13 @@ void build_setup(BrdfSetup& s, const MaterialSpec& mat, const vrte_options* opti
     }
     const int S = (int)s.rep.size();
     s.omega.resize(S);
-    s.greek.assign((size_t)S * L * 6, 0.0);
+    s.greek.assign((size_t)S * Lc * 6, 0.0);
     for (int k = 0; k < S; ++k) {
         const auto& layer = s.spec.layers[s.rep[k]];
         s.omega[k] = layer.omega;
-        for (int l = 0; l < L; ++l) {
+        for (int l = 0; l < Lc; ++l) {
             const Mat4& b = layer.coeffs[l];  // greek_of, kernel.cpp:15-17
-            double* g = &s.greek[((size_t)k * L + l) * 6];
+            double* g = &s.greek[((size_t)k * Lc + l) * 6];
             g[0] = at(b, 0, 0);
             g[1] = at(b, 1, 1);
             g[2] = at(b, 0, 1);
@@ -230,6 +231,7 @@ void build_setup(BrdfSetup& s, const MaterialSpec& mat, const vrte_options* opti
     vrte_cuda_problem& p = s.prob;
     p.N = N;
     p.L = L;
+    p.L_coeffs = Lc;
     p.n_layers = P;
     p.n_media = S;
     p.n_in = (int32_t)n_in;

@@ -1,0 +1,176 @@
+"""Parity of the sm_100a BRDF path (through the C ABI) with the oracles.
+
+Tolerances (written here, justified in DESIGN.md §Parity; measured values in
+profiles/parity_r01.json):
+  * vs the EXACT discrete-ordinate answer (mpmath, 32 digits, tests/golden):
+      max_rc |G - X| / max_rc |X|            <= 2e-12   (per Mueller matrix; measured <= 2.2e-13)
+      SURVEY §8(d) metric (floor 1e-3 |X00|)  <= 1e-9    (measured <= 4.8e-11)
+  * vs the fp64 CPU restatement of the reference (oracle/): the SURVEY metric
+      <= max(1e-9, 1.05 * oracle's own distance to the exact answer + 1e-11),
+    i.e. the GPU agrees with the reference to 1e-9 wherever the reference
+    itself is that accurate, and never disagrees by more than the
+    reference's own fp64 error where it is not.
+  * full-size (C2, C3) configurations: GPU vs oracle on full/partial incident
+    sets, plus size-independent properties (basis invariance, linearity,
+    layer splitting, determinism, order-shard equality).
+"""
+import glob
+import os
+import tempfile
+
+import numpy as np
+import pytest
+
+import paper_1707_05882_b200 as V
+import pyoracle as O
+from paper_1707_05882_b200 import materials as M
+
+from helpers import (GOLDEN, desc_from_golden, load_golden, matrix_metric, oracle_material,
+                     product_material, survey_metric)
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN_CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+
+
+def gpu_table(desc, N, mu, n_dphi, basis=None, order_cap=0):
+    mat = product_material(desc)
+    b = V.compute_brdf(mat, V.options(N, order_cap), mu, n_dphi, basis)
+    return b.table(), b
+
+
+@pytest.mark.parametrize("case", GOLDEN_CASES)
+def test_golden_fixture_parity(case):
+    z, meta = load_golden(case)
+    desc = desc_from_golden(z, meta)
+    g, _ = gpu_table(desc, meta["N"], z["mu_in"], meta["n_dphi"])
+    exact, oracle = z["exact"], z["oracle"]
+    if np.abs(exact).max() == 0:
+        assert np.abs(g).max() < 1e-12
+        return
+    assert matrix_metric(g, exact) <= 2e-12
+    assert survey_metric(g, exact) <= 1e-9
+    oracle_err = survey_metric(oracle, exact)
+    assert survey_metric(g, oracle) <= max(1e-9, 1.05 * oracle_err + 1e-11)
+
+
+def test_reduced_operators_match_oracle():
+    w = M.config("C1")
+    mat = product_material(w.material)
+    nodes, _ = O.quadrature(8)
+    plan = V.Plan(mat, V.options(8), nodes, 19)
+    E, F = plan.ef(1)
+    om = oracle_material(w.material)
+    for m in range(12):
+        e, f = O.reduced_ops(om, 0, 8, m)
+        sc = np.abs(e).max()
+        assert np.abs(E[0, m] - e).max() < 1e-13 * sc
+        assert np.abs(F[0, m] - f).max() < 1e-13 * sc
+
+
+@pytest.mark.parametrize("cfg,orders", [("C1", range(12)), ("C2", (0, 1, 7, 30, 63))])
+def test_separation_constants_match_oracle(cfg, orders):
+    w = M.config(cfg)
+    mat = product_material(w.material)
+    nodes, _ = O.quadrature(w.N)
+    plan = V.Plan(mat, V.options(w.N), nodes[:2], 5)
+    _, _, res, nu = plan.modes(1)
+    om = oracle_material(w.material)
+    assert res.max() < 1e-10  # reference bound is 1e-9 (homogeneous.cpp:280)
+    for m in orders:
+        onu, ores = O.homogeneous(om, 0, w.N, m)
+        g = nu[0, m]
+        for v in onu:
+            assert np.min(np.abs(g - v)) <= 1e-9 * abs(v)
+
+
+def test_c2_full_table_matches_oracle():
+    w = M.config("C2")
+    nodes, _ = O.quadrature(w.N)
+    g, b = gpu_table(w.material, w.N, nodes, 19)
+    r, tm = O.brdf(oracle_material(w.material), w.N, nodes, 19)
+    st = b.device_stats()
+    assert st["max_eigen_residual"] < 1e-10 and tm["max_eigen_residual"] <= 1e-9
+    # vs the reference algorithm as written (its own fp64 error ~1e-9 here)
+    assert matrix_metric(g, r) < 5e-9
+    # vs the same algorithm run to its fp64 limit (every solve refined)
+    with O.accurate():
+        ra, _ = O.brdf(oracle_material(w.material), w.N, nodes, 19)
+    assert matrix_metric(g, ra) < 2e-10
+
+
+def test_c3_partial_table_matches_oracle():
+    w = M.config("C3")
+    nodes, _ = O.quadrature(w.N)
+    g, b = gpu_table(w.material, w.N, nodes, 19)
+    pick = [0, 40, 63]
+    r, _ = O.brdf(oracle_material(w.material), w.N, nodes[pick], 19)
+    assert matrix_metric(g[pick], r) < 5e-9  # measured 7e-10 (reference's own error)
+    assert b.device_stats()["max_eigen_residual"] < 1e-10
+    with O.accurate():
+        ra, _ = O.brdf(oracle_material(w.material), w.N, nodes[[40]], 19)
+    assert matrix_metric(g[[40]], ra) < 5e-10  # measured 4.4e-11
+
+
+# ------------------------------------------------------------ properties (full size)
+def test_vacuum_is_zero_and_isotropic_decouples():
+    g, _ = gpu_table(M.single_layer(M.ISOTROPIC, 0.0, 1.0), 4, [0.6], 8)
+    assert np.abs(g).max() < 1e-12
+    g, _ = gpu_table(M.single_layer(M.ISOTROPIC, 0.7, 1.0), 6, [0.6], 6)
+    assert np.abs(g[..., 2:, :]).max() < 1e-9 and np.abs(g[..., :, 2:]).max() < 1e-9
+    assert np.abs(g - g[:, :, :1]).max() < 1e-9 * np.abs(g).max()
+    assert np.all(g[..., 0, 0] >= 0)
+
+
+def test_basis_invariance_c3():
+    w = M.config("C3")
+    nodes, _ = O.quadrature(64)
+    mu = nodes[::8]
+    a, _ = gpu_table(w.material, 64, mu, 19)
+    alt = np.array([[1, 0, 0, 0], [1, -0.8, 0, 0], [1, 0.2, 0.7, 0], [1, 0.1, -0.2, 0.6]], float)
+    b, _ = gpu_table(w.material, 64, mu, 19, alt)
+    assert np.abs(a - b).max() < 1e-8 * np.abs(a).max()  # test_brdf.cpp:43-61
+
+
+def test_layer_splitting_invariance():
+    # test_boundary.cpp:205-240 at table level: one layer == identical sublayers
+    layer = M.generator_G(0.6, 16)
+    whole = M.single_layer(layer, 0.9, 2.0, "lambertian", 0.2)
+    split = M.MaterialDesc([M.LayerDesc(0.9, 0.5, layer)] * 4, "lambertian", 0.2)
+    nodes, _ = O.quadrature(12)
+    a, _ = gpu_table(whole, 12, nodes, 9)
+    b, _ = gpu_table(split, 12, nodes, 9)
+    assert matrix_metric(b, a) < 1e-8
+
+
+def test_flux_conservation_lossless_lambertian():
+    # test_brdf.cpp:98-114: omega = 1 slab over a perfect diffuse base
+    desc = M.single_layer(M.ISOTROPIC, 1.0, 1.0, "lambertian", 1.0)
+    mat = product_material(desc)
+    b = V.compute_brdf(mat, V.options(16), [0.6], 19)
+    assert b.reflectance(0)[0] == pytest.approx(1.0, rel=1e-3)
+
+
+def test_passive_bound():
+    for coeffs, om in ((M.RAYLEIGH, 0.9), (M.ISOTROPIC, 0.5)):
+        mat = product_material(M.single_layer(coeffs, om, 2.0, "lambertian", 0.8))
+        b = V.compute_brdf(mat, V.options(8), [0.8], 8)
+        r = b.reflectance(0)[0]
+        assert 0.0 <= r <= 1.0 + 1e-6
+
+
+def test_determinism_and_order_sharding_c3():
+    w = M.config("C3")
+    mat = product_material(w.material)
+    nodes, _ = O.quadrature(64)
+    mu = nodes[::4]
+    full = V.Plan(mat, V.options(64), mu, 19)
+    t1 = full.table()
+    full.run(1)
+    assert np.array_equal(t1, full.table())  # bitwise repeatable
+    up_full = full.up()
+    for world in (2, 3):
+        for rank in range(world):
+            orders = list(range(rank, 64, world))
+            p = V.Plan(mat, V.options(64), mu, 19, m_begin=rank, m_stride=world, n_orders=len(orders))
+            assert np.array_equal(p.up(), up_full[orders])
