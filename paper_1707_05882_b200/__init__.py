@@ -308,6 +308,18 @@ def compute_brdf(material: Material, opts: Options, mu_in, n_dphi: int = 19, bas
     return Brdf(h)
 
 
+def brdf_from_stacks(material: Material, opts: Options, mu_in, n_dphi, basis, up_all) -> Brdf:
+    """vrte_brdf_from_stacks: BRDF handle from gathered per-order tau=0 stacks
+    [L, n_in, 4, N, 4] (the multi-GPU root step; synthesis runs on the GPU)."""
+    mu = np.ascontiguousarray(mu_in, dtype=np.float64)
+    b = None if basis is None else np.ascontiguousarray(basis, dtype=np.float64).reshape(16)
+    up = np.ascontiguousarray(up_all, dtype=np.float64)
+    h = C.c_void_p()
+    _check(lib().vrte_brdf_from_stacks(material._h, C.byref(opts), _dp(mu), len(mu), n_dphi, _dp(b),
+                                       _dp(up), C.byref(h)))
+    return Brdf(h)
+
+
 def read_brdf_binary(path: str):
     """VRTEBRDF v1 reader (csv.cpp:170-203): (mu_in, mu_out, dphi, table)."""
     with open(path, "rb") as f:
