@@ -802,69 +802,134 @@ __global__ void residual_kernel(ResidualArgs a) {
 }
 
 // ------------------------------------------------------------------ shifted solves
-// Back substitution for (T - sigma I) y = w on the quasi-triangular Schur
-// factor, warp per right-hand side (real column or packed complex pair).
-__global__ void qtri_solve_kernel(const double* Tall, int d, long long t_stride, double* Wall,
-                                  int ncol, long long w_stride, const double* sigma,
-                                  const int* kind, int batch, const int* t_index) {
+// Blocked back substitution for (T - sigma_c I) y_c = w_c on the quasi-
+// triangular Schur factor, many right-hand sides with per-column shifts.
+// CTA per (matrix, 32-column tile); the tile lives in shared memory.  Row
+// blocks are processed bottom-up: the strictly-upper coupling
+// W[J,:] -= T[J, J+1:] Y[J+1:, :] is shift independent (a shared panel product,
+// T read coalesced from L2 once per tile), and only the small diagonal block
+// is solved per column with its own shift (1x1 / 2x2 Schur blocks, complex
+// pairs = packed Re/Im columns handled by one thread).  kind[c]: 0 real,
+// 1 complex pair (c: Re, c+1: Im), 2 skip.
+constexpr int QBS = 32;   // row block
+constexpr int QCT = 32;   // column tile
+
+__global__ void __launch_bounds__(256) qtri_blocked_kernel(const double* Tall, int d, long long t_stride,
+                                                           double* Wall, int ncol, long long w_stride,
+                                                           const double* sigma, const int* kind,
+                                                           const int* t_index) {
     extern __shared__ double sm[];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + w;
-    if (gw >= (long long)batch * ncol) return;
-    const int b = (int)(gw / ncol), c = (int)(gw % ncol);
-    const int kd = kind[(size_t)b * ncol + c];
-    if (kd == 2) return;
-    const bool cx = kd == 1;
+    const int ld = QCT + 1;               // tile columns (+1 for a pair straddling the edge)
+    double* Y = sm;                       // d x ld, row-major Y[k*ld + c]
+    double* Td = Y + (size_t)d * ld;      // (QBS+1)^2 diagonal block, Td[r*(QBS+1)+c]
+    __shared__ int s_kind[QCT + 1];
+    __shared__ double s_sig[2 * (QCT + 1)];
+    const int tiles = (ncol + QCT - 1) / QCT;
+    const int b = blockIdx.x / tiles, c0 = (blockIdx.x % tiles) * QCT;
     const double* T = Tall + (size_t)(t_index ? t_index[b] : b) * t_stride;
-    double* W = Wall + (size_t)b * w_stride + (size_t)c * d;
-    double* re = sm + (size_t)w * 2 * d;
-    double* im = re + d;
-    const cplx sg = cmk(sigma[2 * ((size_t)b * ncol + c)], sigma[2 * ((size_t)b * ncol + c) + 1]);
-    for (int k = lane; k < d; k += 32) {
-        re[k] = W[k];
-        im[k] = cx ? W[k + d] : 0.0;
+    double* W = Wall + (size_t)b * w_stride;
+    const int t = threadIdx.x, nt = blockDim.x;
+    const int width = min(QCT + 1, ncol - c0);
+    for (int c = t; c < QCT + 1; c += nt) {
+        const int gc = c0 + c;
+        int k = (c < width) ? kind[(size_t)b * ncol + gc] : 2;
+        if (c == 0 && k == 2 && gc > 0 && kind[(size_t)b * ncol + gc - 1] == 1) k = 3;  // Im half owned by previous tile
+        if (c == QCT && k != 1) k = 2;  // extra column only for a straddling pair
+        s_kind[c] = k;
+        s_sig[2 * c] = (c < width) ? sigma[2 * ((size_t)b * ncol + gc)] : 0.0;
+        s_sig[2 * c + 1] = (c < width) ? sigma[2 * ((size_t)b * ncol + gc) + 1] : 0.0;
     }
-    __syncwarp();
-    auto Tat = [&](int r, int cc) { return T[r + (size_t)cc * d]; };
-    int j = d - 1;
-    while (j >= 0) {
-        if (j > 0 && Tat(j, j - 1) != 0.0) {
-            cplx x0, x1;
-            solve2(cmk(Tat(j - 1, j - 1), 0) - sg, cmk(Tat(j - 1, j), 0), cmk(Tat(j, j - 1), 0),
-                   cmk(Tat(j, j), 0) - sg, cmk(re[j - 1], im[j - 1]), cmk(re[j], im[j]), 0.0, x0,
-                   x1);
-            __syncwarp();
-            for (int k = lane; k < j - 1; k += 32) {
-                const double a = Tat(k, j - 1), cc = Tat(k, j);
-                re[k] -= x0.re * a + x1.re * cc;
-                im[k] -= x0.im * a + x1.im * cc;
+    // the tile's last column: include the Im partner of a pair that starts at QCT-1
+    for (int idx = t; idx < d * ld; idx += nt) {
+        const int k = idx / ld, c = idx % ld;
+        Y[idx] = (c < width) ? W[(size_t)(c0 + c) * d + k] : 0.0;
+    }
+    __syncthreads();
+    const bool extra = (width == QCT + 1) && s_kind[QCT - 1] == 1;
+    const int r_t = t & 31, cg = t >> 5;  // update-phase mapping: row r_t, columns cg*4..cg*4+3
+    int j1 = d;
+    while (j1 > 0) {
+        int j0 = max(0, j1 - QBS);
+        if (j0 > 0 && T[j0 + (size_t)(j0 - 1) * d] != 0.0) --j0;  // keep 2x2 blocks whole
+        const int nb = j1 - j0;
+        // (a) panel update rows [j0, j1): Y[J,:] -= T[J, j1:] Y[j1:, :]
+        if (j1 < d) {
+            for (int rr = r_t; rr < nb; rr += 32) {
+                double acc[5] = {0, 0, 0, 0, 0};
+                const double* trow = T + j0 + rr;
+                for (int k = j1; k < d; ++k) {
+                    const double tv = trow[(size_t)k * d];
+                    const double* yk = Y + (size_t)k * ld + cg * 4;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc[q] = fma(tv, yk[q], acc[q]);
+                    if (cg == 7) acc[4] = fma(tv, Y[(size_t)k * ld + QCT], acc[4]);
+                }
+                double* yr = Y + (size_t)(j0 + rr) * ld + cg * 4;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) yr[q] -= acc[q];
+                if (cg == 7) Y[(size_t)(j0 + rr) * ld + QCT] -= acc[4];
             }
-            if (lane == 0) {
-                re[j - 1] = x0.re;
-                im[j - 1] = x0.im;
-                re[j] = x1.re;
-                im[j] = x1.im;
-            }
-            j -= 2;
-        } else {
-            const cplx x = cdiv(cmk(re[j], im[j]), cmk(Tat(j, j), 0) - sg);
-            __syncwarp();
-            for (int k = lane; k < j; k += 32) {
-                const double a = Tat(k, j);
-                re[k] -= x.re * a;
-                im[k] -= x.im * a;
-            }
-            if (lane == 0) {
-                re[j] = x.re;
-                im[j] = x.im;
-            }
-            j -= 1;
         }
-        __syncwarp();
+        for (int idx = t; idx < nb * nb; idx += nt) {
+            const int r = idx % nb, c = idx / nb;
+            Td[r * (QBS + 1) + c] = T[(j0 + r) + (size_t)(j0 + c) * d];
+        }
+        __syncthreads();
+        // (b) diagonal block, one thread per column (pairs: the Re column's thread)
+        if (t < QCT + 1) {
+            const int kd = s_kind[t];
+            const bool run = (kd == 0 || kd == 1) && (t < QCT || extra);
+            if (run) {
+                const bool cx = kd == 1;
+                const cplx sg = cmk(s_sig[2 * t], s_sig[2 * t + 1]);
+                auto TD = [&](int r, int c) { return Td[r * (QBS + 1) + c]; };
+                int j = nb - 1;
+                while (j >= 0) {
+                    if (j > 0 && TD(j, j - 1) != 0.0) {
+                        const cplx b0 = cmk(Y[(size_t)(j0 + j - 1) * ld + t], cx ? Y[(size_t)(j0 + j - 1) * ld + t + 1] : 0.0);
+                        const cplx b1 = cmk(Y[(size_t)(j0 + j) * ld + t], cx ? Y[(size_t)(j0 + j) * ld + t + 1] : 0.0);
+                        cplx x0, x1;
+                        solve2(cmk(TD(j - 1, j - 1), 0) - sg, cmk(TD(j - 1, j), 0), cmk(TD(j, j - 1), 0),
+                               cmk(TD(j, j), 0) - sg, b0, b1, 0.0, x0, x1);
+                        for (int k = 0; k < j - 1; ++k) {
+                            const double a0 = TD(k, j - 1), a1 = TD(k, j);
+                            double* yk = Y + (size_t)(j0 + k) * ld + t;
+                            yk[0] -= x0.re * a0 + x1.re * a1;
+                            if (cx) yk[1] -= x0.im * a0 + x1.im * a1;
+                        }
+                        Y[(size_t)(j0 + j - 1) * ld + t] = x0.re;
+                        Y[(size_t)(j0 + j) * ld + t] = x1.re;
+                        if (cx) {
+                            Y[(size_t)(j0 + j - 1) * ld + t + 1] = x0.im;
+                            Y[(size_t)(j0 + j) * ld + t + 1] = x1.im;
+                        }
+                        j -= 2;
+                    } else {
+                        const cplx rhs = cmk(Y[(size_t)(j0 + j) * ld + t], cx ? Y[(size_t)(j0 + j) * ld + t + 1] : 0.0);
+                        const cplx x = cdiv(rhs, cmk(TD(j, j), 0) - sg);
+                        for (int k = 0; k < j; ++k) {
+                            const double a = TD(k, j);
+                            double* yk = Y + (size_t)(j0 + k) * ld + t;
+                            yk[0] -= x.re * a;
+                            if (cx) yk[1] -= x.im * a;
+                        }
+                        Y[(size_t)(j0 + j) * ld + t] = x.re;
+                        if (cx) Y[(size_t)(j0 + j) * ld + t + 1] = x.im;
+                        j -= 1;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        j1 = j0;
     }
-    for (int k = lane; k < d; k += 32) {
-        W[k] = re[k];
-        if (cx) W[k + d] = im[k];
+    // write back the columns this tile owns (a straddling pair's Im column too)
+    for (int idx = t; idx < d * ld; idx += nt) {
+        const int k = idx / ld, c = idx % ld;
+        if (c >= width) continue;
+        if (c == QCT && !extra) continue;
+        if (s_kind[c] == 3) continue;  // owned by the previous tile
+        W[(size_t)(c0 + c) * d + k] = Y[idx];
     }
 }
 
@@ -928,17 +993,16 @@ void launch_residual(const ResidualArgs& a, cudaStream_t st) {
 void launch_qtri_solve(const double* T, int d, long long t_stride, double* W, int ncol,
                        long long w_stride, const double* sigma, const int* kind, int batch,
                        const int* t_index, cudaStream_t st) {
-    const int warps = 8;
-    const size_t smem = (size_t)warps * 2 * d * sizeof(double);
+    const size_t smem = ((size_t)d * (QCT + 1) + (size_t)(QBS + 1) * (QBS + 1)) * sizeof(double);
     static bool attr = false;
     if (!attr) {
-        VRTE_CUDA_CHECK(cudaFuncSetAttribute(qtri_solve_kernel,
+        VRTE_CUDA_CHECK(cudaFuncSetAttribute(qtri_blocked_kernel,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    const long long total = (long long)batch * ncol;
-    qtri_solve_kernel<<<(unsigned)((total + warps - 1) / warps), warps * 32, smem, st>>>(
-        T, d, t_stride, W, ncol, w_stride, sigma, kind, batch, t_index);
+    const int tiles = (ncol + QCT - 1) / QCT;
+    qtri_blocked_kernel<<<(unsigned)(batch * tiles), 256, smem, st>>>(T, d, t_stride, W, ncol, w_stride,
+                                                                     sigma, kind, t_index);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
