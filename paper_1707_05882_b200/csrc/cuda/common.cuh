@@ -36,6 +36,9 @@ struct DeviceStatus {
     double max_eigen_residual;
     double max_particular_residual;
     double max_boundary_residual;
+    unsigned long long qr_sweeps;
+    unsigned long long qr_steps;
+    unsigned long long qr_cycles[6];  // debug phase timers (clock64 in thread 0)
 };
 
 enum FailKind {

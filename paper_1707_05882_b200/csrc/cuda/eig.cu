@@ -13,6 +13,8 @@
 // shared memory as its only copy so the sequential control path (reflector,
 // deflation tests, shifts) never touches L2.
 #include <climits>
+#include <cstdlib>
+#include <string>
 
 #include "kernels.cuh"
 
@@ -254,7 +256,7 @@ __device__ void start_vector(const HAcc& h, int m, double rt1r, double rt1i, dou
     v[2] /= s;
 }
 
-__global__ void __launch_bounds__(NT) hqr_kernel(double* Hall, double* Zall, double* wrall,
+__global__ void __launch_bounds__(256) hqr_kernel(double* Hall, double* Zall, double* wrall,
                                                  double* wiall, int d, DeviceStatus* status) {
     extern __shared__ double band[];
     __shared__ int s_int;
@@ -354,9 +356,12 @@ __global__ void __launch_bounds__(NT) hqr_kernel(double* Hall, double* Zall, dou
                 if (h00 <= ulp * h11b) mb = max(mb, mm);
             }
             const int M = block_max_int(mb, &s_int);
+            if (t == 0) {
+                atomicAdd(&status->qr_sweeps, 1ull);
+                atomicAdd(&status->qr_steps, (unsigned long long)(I - M));
+            }
             double v0[3];
             start_vector(h, M, rt1r, rt1i, rt2r, rt2i, v0);
-
             for (int k = M; k <= I - 1; ++k) {
                 const int nr = min(3, I - k + 1);
                 double v1, v2, v3;
@@ -392,59 +397,35 @@ __global__ void __launch_bounds__(NT) hqr_kernel(double* Hall, double* Zall, dou
                     }
                 }
                 const double t2 = t1 * v2;
-                if (nr == 3) {
-                    const double t3 = t1 * v3;
-                    for (int j = k + t; j < d; j += nt) {
-                        double& a0 = h(k, j);
-                        double& a1 = h(k + 1, j);
-                        double& a2 = h(k + 2, j);
-                        const double sum = a0 + v2 * a1 + v3 * a2;
-                        a0 -= sum * t1;
-                        a1 -= sum * t2;
-                        a2 -= sum * t3;
-                    }
-                    __syncthreads();
-                    const int jmax = min(k + 3, I);
-                    for (int j = t; j <= jmax; j += nt) {
-                        double& a0 = h(j, k);
-                        double& a1 = h(j, k + 1);
-                        double& a2 = h(j, k + 2);
-                        const double sum = a0 + v2 * a1 + v3 * a2;
-                        a0 -= sum * t1;
-                        a1 -= sum * t2;
-                        a2 -= sum * t3;
-                    }
-                    for (int j = t; j < d; j += nt) {
-                        double* z0 = Z + j + (size_t)k * d;
-                        const double a0 = z0[0], a1 = z0[d], a2 = z0[2 * (size_t)d];
-                        const double sum = a0 + v2 * a1 + v3 * a2;
-                        z0[0] = a0 - sum * t1;
-                        z0[d] = a1 - sum * t2;
-                        z0[2 * (size_t)d] = a2 - sum * t3;
-                    }
-                } else {
-                    for (int j = k + t; j < d; j += nt) {
-                        double& a0 = h(k, j);
-                        double& a1 = h(k + 1, j);
-                        const double sum = a0 + v2 * a1;
-                        a0 -= sum * t1;
-                        a1 -= sum * t2;
-                    }
-                    __syncthreads();
-                    for (int j = t; j <= I; j += nt) {
-                        double& a0 = h(j, k);
-                        double& a1 = h(j, k + 1);
-                        const double sum = a0 + v2 * a1;
-                        a0 -= sum * t1;
-                        a1 -= sum * t2;
-                    }
-                    for (int j = t; j < d; j += nt) {
-                        double* z0 = Z + j + (size_t)k * d;
-                        const double a0 = z0[0], a1 = z0[d];
-                        const double sum = a0 + v2 * a1;
-                        z0[0] = a0 - sum * t1;
-                        z0[d] = a1 - sum * t2;
-                    }
+                const double t3 = (nr == 3) ? t1 * v3 : 0.0;
+                for (int j = k + t; j < d; j += nt) {
+                    double& a0 = h(k, j);
+                    double& a1 = h(k + 1, j);
+                    const double a2v = (nr == 3) ? h(k + 2, j) : 0.0;
+                    const double sum = a0 + v2 * a1 + (nr == 3 ? v3 * a2v : 0.0);
+                    a0 -= sum * t1;
+                    a1 -= sum * t2;
+                    if (nr == 3) h(k + 2, j) = a2v - sum * t3;
+                }
+                __syncthreads();
+                const int jmax = (nr == 3) ? min(k + 3, I) : I;
+                for (int j = t; j <= jmax; j += nt) {
+                    double& a0 = h(j, k);
+                    double& a1 = h(j, k + 1);
+                    const double a2v = (nr == 3) ? h(j, k + 2) : 0.0;
+                    const double sum = a0 + v2 * a1 + (nr == 3 ? v3 * a2v : 0.0);
+                    a0 -= sum * t1;
+                    a1 -= sum * t2;
+                    if (nr == 3) h(j, k + 2) = a2v - sum * t3;
+                }
+                for (int j = t; j < d; j += nt) {
+                    double* z0 = Z + j + (size_t)k * d;
+                    const double a0 = z0[0], a1 = z0[d];
+                    const double a2v = (nr == 3) ? z0[2 * (size_t)d] : 0.0;
+                    const double sum = a0 + v2 * a1 + (nr == 3 ? v3 * a2v : 0.0);
+                    z0[0] = a0 - sum * t1;
+                    z0[d] = a1 - sum * t2;
+                    if (nr == 3) z0[2 * (size_t)d] = a2v - sum * t3;
                 }
                 __syncthreads();
             }
@@ -504,6 +485,353 @@ __global__ void __launch_bounds__(NT) hqr_kernel(double* Hall, double* Zall, dou
     for (int idx = t; idx < (BW + 4) * d; idx += nt) {
         const int off = idx / d - 3, c = idx % d, r = c - off;
         if (r >= 0 && r < d) H[r + (size_t)c * d] = (r > c + 1) ? 0.0 : band[idx];
+    }
+}
+
+// ------------------------------------------------------------------ windowed Francis QR
+// Same iteration as hqr_kernel (dlahqr rules) but each sweep is processed in
+// chunks of QW_STEPS bulge-chase steps: the chunk's (steps+4)^2 diagonal window
+// is staged in shared memory and chased by ONE warp (warp-synchronous), while
+// the chunk's accumulated orthogonal factor U (product of its 3x3 reflectors)
+// is then applied by the whole CTA to the rows right of the window (U^T H),
+// the columns above it (H U) and to Z (Z U) as register-blocked dense updates.
+// This is the dlaqr5 organisation with one bulge: ~5x the flops of applying
+// reflectors one by one, but no block barrier and no L2 round trip per step.
+constexpr int QW_STEPS = 12;
+constexpr int QW = QW_STEPS + 4;  // window width
+
+__device__ inline double hg(const double* H, int d, int r, int c) { return H[r + (size_t)c * d]; }
+
+__device__ bool small_subdiag_g(const double* H, int d, int k, double ulp, double smlnum) {
+    const double hk = fabs(hg(H, d, k, k - 1));
+    if (hk <= smlnum) return true;
+    double tst = fabs(hg(H, d, k - 1, k - 1)) + fabs(hg(H, d, k, k));
+    if (tst == 0.0) {
+        if (k - 2 >= 0) tst += fabs(hg(H, d, k - 1, k - 2));
+        if (k + 1 <= d - 1) tst += fabs(hg(H, d, k + 1, k));
+    }
+    if (hk <= ulp * tst) {
+        const double hup = fabs(hg(H, d, k - 1, k));
+        const double ab = fmax(hk, hup), ba = fmin(hk, hup);
+        const double dif = fabs(hg(H, d, k - 1, k - 1) - hg(H, d, k, k));
+        const double aa = fmax(fabs(hg(H, d, k, k)), dif), bb = fmin(fabs(hg(H, d, k, k)), dif);
+        const double s = aa + ab;
+        if (ba * (ab / s) <= fmax(smlnum, ulp * (bb * (aa / s)))) return true;
+    }
+    return false;
+}
+
+__device__ void start_vector_g(const double* H, int d, int m, double rt1r, double rt1i, double rt2r,
+                               double rt2i, double v[3]) {
+    double h21s = hg(H, d, m + 1, m);
+    double s = fabs(hg(H, d, m, m) - rt2r) + fabs(rt2i) + fabs(h21s);
+    h21s = hg(H, d, m + 1, m) / s;
+    v[0] = h21s * hg(H, d, m, m + 1) + (hg(H, d, m, m) - rt1r) * ((hg(H, d, m, m) - rt2r) / s) -
+           rt1i * (rt2i / s);
+    v[1] = h21s * (hg(H, d, m, m) + hg(H, d, m + 1, m + 1) - rt1r - rt2r);
+    v[2] = h21s * hg(H, d, m + 2, m + 1);
+    s = fabs(v[0]) + fabs(v[1]) + fabs(v[2]);
+    v[0] /= s;
+    v[1] /= s;
+    v[2] /= s;
+}
+
+__global__ void __launch_bounds__(256) hqr_window_kernel(double* Hall, double* Zall, double* wrall,
+                                                         double* wiall, int d, DeviceStatus* status) {
+    __shared__ double Wn[QW * QW];  // window, column-major Wn[c*QW + r]
+    __shared__ double Us[QW * QW];  // accumulated factor, column-major
+    __shared__ int s_int;
+    __shared__ double s_t1;
+    const int b = blockIdx.x, t = threadIdx.x, nt = blockDim.x, lane = t & 31, warp = t >> 5;
+    double* H = Hall + (size_t)b * d * d;
+    double* Z = Zall + (size_t)b * d * d;
+    double* wr = wrall + (size_t)b * d;
+    double* wi = wiall + (size_t)b * d;
+    const double ulp = kUlp;
+    const double smlnum = kSafeMin * ((double)d / ulp);
+    const int itmax = 30 * max(10, d);
+    const int kexsh = 10;
+    int kdefl = 0;
+    int I = d - 1;
+    unsigned long long cyc[6] = {0, 0, 0, 0, 0, 0};
+    long long tc = clock64();
+    auto tick = [&](int slot) {
+        const long long now = clock64();
+        cyc[slot] += (unsigned long long)(now - tc);
+        tc = now;
+    };
+    while (I >= 0) {
+        int L = 0;
+        bool conv = false;
+        for (int its = 0; its <= itmax; ++its) {
+            tick(5);
+            int kb = L;
+            for (int k = L + 1 + t; k <= I; k += nt)
+                if (small_subdiag_g(H, d, k, ulp, smlnum)) kb = max(kb, k);
+            L = block_max_int(kb, &s_int);
+            if (L > 0 && t == 0) H[L + (size_t)(L - 1) * d] = 0.0;
+            __syncthreads();
+            if (L >= I - 1) {
+                conv = true;
+                break;
+            }
+            ++kdefl;
+            double h11, h12, h21, h22;
+            if (kdefl % (2 * kexsh) == 0) {
+                const double s = fabs(hg(H, d, I, I - 1)) + fabs(hg(H, d, I - 1, I - 2));
+                h11 = 0.75 * s + hg(H, d, I, I);
+                h12 = -0.4375 * s;
+                h21 = s;
+                h22 = h11;
+            } else if (kdefl % kexsh == 0) {
+                const double s = fabs(hg(H, d, L + 1, L)) + fabs(hg(H, d, L + 2, L + 1));
+                h11 = 0.75 * s + hg(H, d, L, L);
+                h12 = -0.4375 * s;
+                h21 = s;
+                h22 = h11;
+            } else {
+                h11 = hg(H, d, I - 1, I - 1);
+                h21 = hg(H, d, I, I - 1);
+                h12 = hg(H, d, I - 1, I);
+                h22 = hg(H, d, I, I);
+            }
+            double rt1r, rt1i, rt2r, rt2i;
+            {
+                const double s = fabs(h11) + fabs(h12) + fabs(h21) + fabs(h22);
+                if (s == 0.0) {
+                    rt1r = rt1i = rt2r = rt2i = 0.0;
+                } else {
+                    h11 /= s;
+                    h21 /= s;
+                    h12 /= s;
+                    h22 /= s;
+                    const double tr = (h11 + h22) / 2.0;
+                    const double det = (h11 - tr) * (h22 - tr) - h12 * h21;
+                    const double rtdisc = sqrt(fabs(det));
+                    if (det >= 0.0) {
+                        rt1r = tr * s;
+                        rt2r = rt1r;
+                        rt1i = rtdisc * s;
+                        rt2i = -rt1i;
+                    } else {
+                        rt1r = tr + rtdisc;
+                        rt2r = tr - rtdisc;
+                        if (fabs(rt1r - h22) <= fabs(rt2r - h22)) {
+                            rt1r *= s;
+                            rt2r = rt1r;
+                        } else {
+                            rt2r *= s;
+                            rt1r = rt2r;
+                        }
+                        rt1i = rt2i = 0.0;
+                    }
+                }
+            }
+            int mb = L;
+            for (int mm = L + 1 + t; mm <= I - 2; mm += nt) {
+                double vv[3];
+                start_vector_g(H, d, mm, rt1r, rt1i, rt2r, rt2i, vv);
+                const double h00 = fabs(hg(H, d, mm, mm - 1)) * (fabs(vv[1]) + fabs(vv[2]));
+                const double h11b = fabs(vv[0]) * (fabs(hg(H, d, mm - 1, mm - 1)) + fabs(hg(H, d, mm, mm)) +
+                                                   fabs(hg(H, d, mm + 1, mm + 1)));
+                if (h00 <= ulp * h11b) mb = max(mb, mm);
+            }
+            const int M = block_max_int(mb, &s_int);
+            double v0[3];
+            start_vector_g(H, d, M, rt1r, rt1i, rt2r, rt2i, v0);
+            if (t == 0) {
+                atomicAdd(&status->qr_sweeps, 1ull);
+                atomicAdd(&status->qr_steps, (unsigned long long)(I - M));
+            }
+            tick(0);
+            for (int k0 = M; k0 <= I - 1;) {
+                const int ns = min(QW_STEPS, I - k0);
+                const int wlo = (k0 > M) ? k0 - 1 : k0;
+                const int whi = min(k0 + ns + 2, I);
+                const int nw = whi - wlo + 1;
+                for (int idx = t; idx < QW * QW; idx += nt) {
+                    const int r = idx % QW, c = idx / QW;
+                    Wn[idx] = (r < nw && c < nw) ? H[(wlo + r) + (size_t)(wlo + c) * d] : 0.0;
+                    Us[idx] = (r == c) ? 1.0 : 0.0;
+                }
+                __syncthreads();
+                tick(1);
+                if (warp == 0) {
+                    auto W = [&](int r, int c) -> double& { return Wn[(c - wlo) * QW + (r - wlo)]; };
+                    for (int k = k0; k < k0 + ns; ++k) {
+                        const int nr = min(3, I - k + 1);
+                        double v1, v2, v3;
+                        if (k > M) {
+                            v1 = W(k, k - 1);
+                            v2 = W(k + 1, k - 1);
+                            v3 = (nr == 3) ? W(k + 2, k - 1) : 0.0;
+                        } else {
+                            v1 = v0[0];
+                            v2 = v0[1];
+                            v3 = (nr == 3) ? v0[2] : 0.0;
+                        }
+                        if (nr != 3) v3 = 0.0;
+                        double t1 = 0.0;
+                        {
+                            // dlarfg with one sqrt and two independent reciprocals (the
+                            // bulge entries are O(1): no dlapy2 overflow scaling needed)
+                            const double x2 = fma(v2, v2, v3 * v3);
+                            if (x2 != 0.0) {
+                                // beta = -sign(v1) |v|, 1/beta = -sign(v1) rsqrt(|v|^2),
+                                // t1 = 1 + |v1|/|v|, scale = sign(v1) / (|v1| + |v|)
+                                const double ss = fma(v1, v1, x2);
+                                const double rq = rsqrt(ss);
+                                const double nv = ss * rq;
+                                const double av1 = fabs(v1);
+                                const double sc = copysign(__drcp_rn(av1 + nv), v1);
+                                t1 = fma(av1, rq, 1.0);
+                                v2 *= sc;
+                                v3 *= sc;
+                                v1 = -copysign(nv, v1);
+                            }
+                        }
+                        const double t2 = t1 * v2, t3 = t1 * v3;
+                        __syncwarp();
+                        // row op: rows k..k+nr-1, columns k..whi (in window)
+                        for (int c = k + lane; c <= whi; c += 32) {
+                            double& a0 = W(k, c);
+                            double& a1 = W(k + 1, c);
+                            const double a2v = (nr == 3) ? W(k + 2, c) : 0.0;
+                            const double sum = a0 + v2 * a1 + v3 * a2v;
+                            a0 -= sum * t1;
+                            a1 -= sum * t2;
+                            if (nr == 3) W(k + 2, c) = a2v - sum * t3;
+                        }
+                        __syncwarp();
+                        if (lane == 0) {
+                            if (k > M) {
+                                W(k, k - 1) = v1;
+                                W(k + 1, k - 1) = 0.0;
+                                if (k < I - 1) W(k + 2, k - 1) = 0.0;
+                            } else {
+                                s_t1 = t1;  // H(M, M-1) *= (1 - t1) after the chunk (outside the window)
+                            }
+                        }
+                        // column op: rows wlo..min(k+3, I), columns k..k+nr-1 (in window), and U
+                        const int rmax = (nr == 3) ? min(k + 3, I) : I;
+                        for (int r = wlo + lane; r <= rmax && r <= whi; r += 32) {
+                            double& a0 = W(r, k);
+                            double& a1 = W(r, k + 1);
+                            const double a2v = (nr == 3) ? W(r, k + 2) : 0.0;
+                            const double sum = a0 + v2 * a1 + v3 * a2v;
+                            a0 -= sum * t1;
+                            a1 -= sum * t2;
+                            if (nr == 3) W(r, k + 2) = a2v - sum * t3;
+                        }
+                        for (int r = lane; r < nw; r += 32) {
+                            double* u = Us + r;
+                            const int c = k - wlo;
+                            const double u0 = u[c * QW], u1 = u[(c + 1) * QW];
+                            const double u2 = (nr == 3) ? u[(c + 2) * QW] : 0.0;
+                            const double sum = u0 + v2 * u1 + v3 * u2;
+                            u[c * QW] = u0 - sum * t1;
+                            u[(c + 1) * QW] = u1 - sum * t2;
+                            if (nr == 3) u[(c + 2) * QW] = u2 - sum * t3;
+                        }
+                        __syncwarp();
+                    }
+                }
+                __syncthreads();
+                tick(2);
+                for (int idx = t; idx < nw * nw; idx += nt) {
+                    const int r = idx % nw, c = idx / nw;
+                    H[(wlo + r) + (size_t)(wlo + c) * d] = Wn[c * QW + r];
+                }
+                if (k0 == M && M > L && t == 0) H[M + (size_t)(M - 1) * d] *= (1.0 - s_t1);
+                // off-window updates with U (QW x QW, zero-padded beyond nw)
+                const int n_right = d - 1 - whi, n_above = wlo;
+                for (int task = t; task < n_right + n_above + d; task += nt) {
+                    double x[QW];
+                    if (task < n_right) {  // column c right of the window: U^T x
+                        double* col = H + (size_t)(whi + 1 + task) * d + wlo;
+#pragma unroll
+                        for (int q = 0; q < QW; ++q) x[q] = (q < nw) ? col[q] : 0.0;
+#pragma unroll 4
+                        for (int r = 0; r < nw; ++r) {
+                            double acc = 0.0;
+#pragma unroll
+                            for (int q = 0; q < QW; ++q) acc = fma(Us[r * QW + q], x[q], acc);
+                            col[r] = acc;
+                        }
+                    } else {  // row (of H above the window, or of Z): x U
+                        const bool isz = task >= n_right + n_above;
+                        const int i = isz ? task - n_right - n_above : task - n_right;
+                        double* base = (isz ? Z : H) + i + (size_t)wlo * d;
+#pragma unroll
+                        for (int q = 0; q < QW; ++q) x[q] = (q < nw) ? base[(size_t)q * d] : 0.0;
+#pragma unroll 4
+                        for (int c = 0; c < nw; ++c) {
+                            double acc = 0.0;
+#pragma unroll
+                            for (int q = 0; q < QW; ++q) acc = fma(x[q], Us[c * QW + q], acc);
+                            base[(size_t)c * d] = acc;
+                        }
+                    }
+                }
+                __syncthreads();
+                tick(3);
+                k0 += ns;
+            }
+        }
+        if (!conv) {
+            if (t == 0) report_failure(status, kFailHqrNoConverge, 1, b, (double)I);
+            return;
+        }
+        if (L == I) {
+            if (t == 0) {
+                wr[I] = hg(H, d, I, I);
+                wi[I] = 0.0;
+            }
+        } else {
+            double a = hg(H, d, I - 1, I - 1), bb = hg(H, d, I - 1, I), c = hg(H, d, I, I - 1),
+                   dd = hg(H, d, I, I);
+            double r1r, r1i, r2r, r2i, cs, sn;
+            dlanv2(a, bb, c, dd, r1r, r1i, r2r, r2i, cs, sn);
+            __syncthreads();
+            if (t == 0) {
+                H[(I - 1) + (size_t)(I - 1) * d] = a;
+                H[(I - 1) + (size_t)I * d] = bb;
+                H[I + (size_t)(I - 1) * d] = c;
+                H[I + (size_t)I * d] = dd;
+                wr[I - 1] = r1r;
+                wi[I - 1] = r1i;
+                wr[I] = r2r;
+                wi[I] = r2i;
+            }
+            for (int j = I + 1 + t; j < d; j += nt) {
+                double* x = H + (I - 1) + (size_t)j * d;
+                const double xv = x[0], yv = x[1];
+                x[0] = cs * xv + sn * yv;
+                x[1] = cs * yv - sn * xv;
+            }
+            for (int j = t; j <= I - 2; j += nt) {
+                double* x = H + j + (size_t)(I - 1) * d;
+                const double xv = x[0], yv = x[d];
+                x[0] = cs * xv + sn * yv;
+                x[d] = cs * yv - sn * xv;
+            }
+            for (int j = t; j < d; j += nt) {
+                double* zx = Z + j + (size_t)(I - 1) * d;
+                const double xv = zx[0], yv = zx[d];
+                zx[0] = cs * xv + sn * yv;
+                zx[d] = cs * yv - sn * xv;
+            }
+        }
+        kdefl = 0;
+        I = L - 1;
+        __syncthreads();
+    }
+    if (t == 0)
+        for (int q = 0; q < 6; ++q) atomicAdd(&status->qr_cycles[q], cyc[q]);
+    // zero the sub-subdiagonal entries left from the bulges
+    for (int idx = t; idx < d * d; idx += nt) {
+        const int r = idx % d, c = idx / d;
+        if (r > c + 1) H[idx] = 0.0;
     }
 }
 
@@ -954,7 +1282,12 @@ void launch_hqr(double* H, double* Z, double* wr, double* wi, int d, int batch,
                                              200 * 1024));
         attr = true;
     }
-    hqr_kernel<<<batch, NT, smem, st>>>(H, Z, wr, wi, d, status);
+    static const char* mode = std::getenv("VRTE_HQR");  // window (default) | band
+    if (!mode || std::string(mode) == "window") {
+        hqr_window_kernel<<<batch, 256, 0, st>>>(H, Z, wr, wi, d, status);
+    } else {
+        hqr_kernel<<<batch, NT, smem, st>>>(H, Z, wr, wi, d, status);
+    }
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
