@@ -1,132 +1,180 @@
 // gemm.cu -- batched fp64 GEMM for the dense contractions of the BRDF path
-// (F*E, eigenvector back-transforms, E*X recoveries, particular Z-projections,
-// boundary trailing updates / triangular-solve updates, tau=0 field products).
+// (F*E, eigenvector back-transforms, 8N residual/refinement products,
+// particular projections, boundary LU trailing updates, tau=0 field products).
 //
-// 64x64 CTA tile, BK=16 k-slab double-buffered in shared memory, 256 threads
-// each owning a 4x4 register micro-tile (rows tx+16i, cols ty+16j so both smem
-// operand reads are bank-conflict free).  DFMA pipe; B200's FP64 tensor rate
-// equals its DFMA rate, so the tensor path buys nothing for fp64 here.
+// FP64 tensor cores: mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4; tcgen05 has no f64
+// kind).  CTA tile 64 x 128 x 16, 8 warps as 2 x 4, each warp a 32 x 32 tile
+// of 4 x 4 DMMA fragments (32 fp64 accumulators per thread).  Operands are
+// streamed global -> shared with cp.async (2-stage double buffer, zero fill at
+// the edges); the shared layout of each operand follows its transpose so the
+// per-lane fragment loads are bank-conflict free:
+//   A not transposed: As[k][m] (ld 72)     A transposed: As[m][k] (ld 20)
+//   B not transposed: Bs[n][k] (ld 20)     B transposed: Bs[k][n] (ld 136)
+// The epilogue stages the C tile through shared memory so global stores are
+// coalesced down the columns of the column-major output.
 #include "common.cuh"
 
 namespace vrte {
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, NT = 256;
+constexpr int BM = 64, BN = 128, BK = 16, NT = 256;
+constexpr int LDA_K = BM + 8;   // k-major A: As[k * LDA_K + m]
+constexpr int LDA_M = BK + 4;   // m-major A: As[m * LDA_M + k]
+constexpr int LDB_N = BK + 4;   // n-major B: Bs[n * LDB_N + k]
+constexpr int LDB_K = BN + 8;   // k-major B: Bs[k * LDB_K + n]
+constexpr int A_STAGE = (BK * LDA_K > BM * LDA_M) ? BK * LDA_K : BM * LDA_M;   // doubles
+constexpr int B_STAGE = (BN * LDB_N > BK * LDB_K) ? BN * LDB_N : BK * LDB_K;
+constexpr int LDC_S = BN + 1;   // epilogue staging Cs[m * LDC_S + n] (aliases the operand buffers)
+constexpr int SMEM_DOUBLES = (2 * (A_STAGE + B_STAGE) > BM * LDC_S) ? 2 * (A_STAGE + B_STAGE) : BM * LDC_S;
+
+__device__ inline void cp_async8(double* smem, const double* gmem, bool valid) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    const int src_size = valid ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_size));
+}
+__device__ inline void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ inline void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+__device__ inline void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
 
 template <bool TA, bool TB>
-__global__ void __launch_bounds__(NT) gemm_kernel(GemmBatch g) {
-    __shared__ double As[2][BK][BM + 1];
-    __shared__ double Bs[2][BK][BN + 1];
+__global__ void __launch_bounds__(NT) dmma_gemm_kernel(GemmBatch g) {
+    extern __shared__ double smem[];
+    double* As0 = smem;
+    double* Bs0 = smem + 2 * A_STAGE;
     const int bz = blockIdx.z;
     const double* A = g.a + bz * g.stride_a;
     const double* B = g.b + bz * g.stride_b;
     double* C = g.c + bz * g.stride_c;
-    const int r0 = blockIdx.x * BM, c0 = blockIdx.y * BN;
-    const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int wm = (warp >> 2) * 32, wn = (warp & 3) * 32;  // warp tile origin in the CTA tile
+    const int gq = lane >> 2, tq = lane & 3;                 // fragment coordinates
 
-    double acc[4][4];
+    auto load_stage = [&](int stage, int k0) {
+        double* As = As0 + stage * A_STAGE;
+        double* Bs = Bs0 + stage * B_STAGE;
+        // A tile: BM x BK = 1024 doubles, 4 per thread
+#pragma unroll
+        for (int q = 0; q < (BM * BK) / NT; ++q) {
+            const int e = t + q * NT;
+            if (!TA) {  // contiguous along m: As[k][m]
+                const int m = e % BM, k = e / BM;
+                const int gm = m0 + m, gk = k0 + k;
+                const bool ok = gm < g.m && gk < g.k;
+                cp_async8(As + k * LDA_K + m, ok ? A + gm + (long long)gk * g.lda : A, ok);
+            } else {    // contiguous along k: As[m][k]
+                const int k = e % BK, m = e / BK;
+                const int gm = m0 + m, gk = k0 + k;
+                const bool ok = gm < g.m && gk < g.k;
+                cp_async8(As + m * LDA_M + k, ok ? A + gk + (long long)gm * g.lda : A, ok);
+            }
+        }
+        // B tile: BK x BN = 2048 doubles, 8 per thread
+#pragma unroll
+        for (int q = 0; q < (BK * BN) / NT; ++q) {
+            const int e = t + q * NT;
+            if (!TB) {  // contiguous along k: Bs[n][k]
+                const int k = e % BK, n = e / BK;
+                const int gn = n0 + n, gk = k0 + k;
+                const bool ok = gn < g.n && gk < g.k;
+                cp_async8(Bs + n * LDB_N + k, ok ? B + gk + (long long)gn * g.ldb : B, ok);
+            } else {    // contiguous along n: Bs[k][n]
+                const int n = e % BN, k = e / BN;
+                const int gn = n0 + n, gk = k0 + k;
+                const bool ok = gn < g.n && gk < g.k;
+                cp_async8(Bs + k * LDB_K + n, ok ? B + gn + (long long)gk * g.ldb : B, ok);
+            }
+        }
+        cp_async_commit();
+    };
+
+    double acc[4][4][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-
-    double ra[4], rb[4];
-    auto load_regs = [&](int k0) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            int i, kk;
-            if (!TA) {
-                i = t & 63;
-                kk = (t >> 6) + 4 * q;
-                const int gr = r0 + i, gk = k0 + kk;
-                ra[q] = (gr < g.m && gk < g.k) ? A[gr + (long long)gk * g.lda] : 0.0;
-            } else {
-                kk = t & 15;
-                i = (t >> 4) + 16 * q;
-                const int gr = r0 + i, gk = k0 + kk;
-                ra[q] = (gr < g.m && gk < g.k) ? A[gk + (long long)gr * g.lda] : 0.0;
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            int j, kk;
-            if (!TB) {
-                kk = t & 15;
-                j = (t >> 4) + 16 * q;
-                const int gc = c0 + j, gk = k0 + kk;
-                rb[q] = (gc < g.n && gk < g.k) ? B[gk + (long long)gc * g.ldb] : 0.0;
-            } else {
-                j = t & 63;
-                kk = (t >> 6) + 4 * q;
-                const int gc = c0 + j, gk = k0 + kk;
-                rb[q] = (gc < g.n && gk < g.k) ? B[gc + (long long)gk * g.ldb] : 0.0;
-            }
-        }
-    };
-    auto store_smem = [&](int buf) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (!TA)
-                As[buf][(t >> 6) + 4 * q][t & 63] = ra[q];
-            else
-                As[buf][t & 15][(t >> 4) + 16 * q] = ra[q];
-            if (!TB)
-                Bs[buf][t & 15][(t >> 4) + 16 * q] = rb[q];
-            else
-                Bs[buf][(t >> 6) + 4 * q][t & 63] = rb[q];
-        }
-    };
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     const int nk = (g.k + BK - 1) / BK;
-    if (nk > 0) {
-        load_regs(0);
-        store_smem(0);
-    }
-    __syncthreads();
+    if (nk > 0) load_stage(0, 0);
     for (int kt = 0; kt < nk; ++kt) {
-        const int buf = kt & 1;
-        if (kt + 1 < nk) load_regs((kt + 1) * BK);
+        cp_async_wait_all();
+        __syncthreads();
+        if (kt + 1 < nk) load_stage((kt + 1) & 1, (kt + 1) * BK);
+        const double* As = As0 + (kt & 1) * A_STAGE;
+        const double* Bs = Bs0 + (kt & 1) * B_STAGE;
 #pragma unroll
-        for (int kk = 0; kk < BK; ++kk) {
-            double a[4], b[4];
+        for (int kk = 0; kk < BK; kk += 4) {
+            double af[4], bf[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = As[buf][kk][tx + 16 * i];
+            for (int i = 0; i < 4; ++i) {
+                const int m = wm + 8 * i + gq, k = kk + tq;
+                af[i] = TA ? As[m * LDA_M + k] : As[k * LDA_K + m];
+            }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = Bs[buf][kk][ty + 16 * j];
+            for (int j = 0; j < 4; ++j) {
+                const int n = wn + 8 * j + gq, k = kk + tq;
+                bf[j] = TB ? Bs[k * LDB_K + n] : Bs[n * LDB_N + k];
+            }
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
-        if (kt + 1 < nk) store_smem(buf ^ 1);
-        __syncthreads();
     }
+    // epilogue: stage through shared memory, then coalesced column stores
+    cp_async_wait_all();
+    __syncthreads();
+    double* Cs = smem;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const int gr = r0 + tx + 16 * i, gc = c0 + ty + 16 * j;
-            if (gr < g.m && gc < g.n) {
-                double* p = C + gr + (long long)gc * g.ldc;
-                const double v = g.alpha * acc[i][j];
-                *p = (g.beta == 0.0) ? v : fma(g.beta, *p, v);
-            }
+            const int m = wm + 8 * i + gq, n = wn + 8 * j + 2 * tq;
+            Cs[m * LDC_S + n] = acc[i][j][0];
+            Cs[m * LDC_S + n + 1] = acc[i][j][1];
         }
+    __syncthreads();
+    for (int e = t; e < BM * BN; e += NT) {
+        const int m = e % BM, n = e / BM;
+        const int gm = m0 + m, gn = n0 + n;
+        if (gm < g.m && gn < g.n) {
+            double* p = C + gm + (long long)gn * g.ldc;
+            const double v = g.alpha * Cs[m * LDC_S + n];
+            *p = (g.beta == 0.0) ? v : fma(g.beta, *p, v);
+        }
+    }
+}
+
+template <bool TA, bool TB>
+void launch(const GemmBatch& g, cudaStream_t stream) {
+    static bool attr = false;
+    const size_t smem = SMEM_DOUBLES * sizeof(double);
+    if (!attr) {
+        VRTE_CUDA_CHECK(cudaFuncSetAttribute(dmma_gemm_kernel<TA, TB>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    dim3 grid((g.m + BM - 1) / BM, (g.n + BN - 1) / BN, g.batch);
+    dmma_gemm_kernel<TA, TB><<<grid, NT, smem, stream>>>(g);
 }
 
 }  // namespace
 
 void gemm_batched(const GemmBatch& g, cudaStream_t stream) {
     if (g.m <= 0 || g.n <= 0 || g.batch <= 0) return;
-    dim3 grid((g.m + BM - 1) / BM, (g.n + BN - 1) / BN, g.batch);
     if (!g.trans_a && !g.trans_b)
-        gemm_kernel<false, false><<<grid, NT, 0, stream>>>(g);
+        launch<false, false>(g, stream);
     else if (g.trans_a && !g.trans_b)
-        gemm_kernel<true, false><<<grid, NT, 0, stream>>>(g);
+        launch<true, false>(g, stream);
     else if (!g.trans_a && g.trans_b)
-        gemm_kernel<false, true><<<grid, NT, 0, stream>>>(g);
+        launch<false, true>(g, stream);
     else
-        gemm_kernel<true, true><<<grid, NT, 0, stream>>>(g);
+        launch<true, true>(g, stream);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 

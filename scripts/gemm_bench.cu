@@ -1,0 +1,106 @@
+// gemm_bench.cu -- standalone check + timing of the DMMA batched GEMM against cuBLAS DGEMM.
+// Build (GPU box): nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a \
+//   -Ipaper_1707_05882_b200/csrc/cuda scripts/gemm_bench.cu -lcublas -o gpurun_out/gemm_bench
+#include <cublas_v2.h>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include "../paper_1707_05882_b200/csrc/cuda/gemm.cu"
+
+namespace vrte {
+[[noreturn]] void cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+    std::fprintf(stderr, "%s:%d %s: %s\n", file, line, what, cudaGetErrorString(e));
+    std::exit(1);
+}
+}  // namespace vrte
+
+static double run(int m, int n, int k, int batch, bool ta, bool tb, double beta, bool timeit) {
+    const long long lda = ta ? k : m, ldb = tb ? n : k, ldc = m;
+    const long long sa = lda * (ta ? m : k), sb = ldb * (tb ? k : n), sc = ldc * n;
+    std::vector<double> ha(sa * batch), hb(sb * batch), hc(sc * batch);
+    srand(1234);
+    for (auto& x : ha) x = rand() / (double)RAND_MAX - 0.5;
+    for (auto& x : hb) x = rand() / (double)RAND_MAX - 0.5;
+    for (auto& x : hc) x = rand() / (double)RAND_MAX - 0.5;
+    double *a, *b, *c, *c2;
+    cudaMalloc(&a, ha.size() * 8);
+    cudaMalloc(&b, hb.size() * 8);
+    cudaMalloc(&c, hc.size() * 8);
+    cudaMalloc(&c2, hc.size() * 8);
+    cudaMemcpy(a, ha.data(), ha.size() * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(b, hb.data(), hb.size() * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(c, hc.data(), hc.size() * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(c2, hc.data(), hc.size() * 8, cudaMemcpyHostToDevice);
+    vrte::GemmBatch g{};
+    g.m = m; g.n = n; g.k = k; g.a = a; g.lda = lda; g.stride_a = sa; g.b = b; g.ldb = ldb; g.stride_b = sb;
+    g.c = c; g.ldc = ldc; g.stride_c = sc; g.batch = batch; g.alpha = 1.25; g.beta = beta;
+    g.trans_a = ta; g.trans_b = tb;
+    vrte::gemm_batched(g, 0);
+    cublasHandle_t h;
+    cublasCreate(&h);
+    const double alpha = 1.25;
+    cublasDgemmStridedBatched(h, ta ? CUBLAS_OP_T : CUBLAS_OP_N, tb ? CUBLAS_OP_T : CUBLAS_OP_N, m, n, k, &alpha, a,
+                              lda, sa, b, ldb, sb, &beta, c2, ldc, sc, batch);
+    cudaDeviceSynchronize();
+    std::vector<double> r1(hc.size()), r2(hc.size());
+    cudaMemcpy(r1.data(), c, r1.size() * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(r2.data(), c2, r2.size() * 8, cudaMemcpyDeviceToHost);
+    double err = 0, mx = 0;
+    for (size_t i = 0; i < r1.size(); ++i) {
+        err = std::fmax(err, std::fabs(r1[i] - r2[i]));
+        mx = std::fmax(mx, std::fabs(r2[i]));
+    }
+    double rel = err / (mx > 0 ? mx : 1);
+    if (timeit) {
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        const int reps = 20;
+        for (int i = 0; i < 3; ++i) vrte::gemm_batched(g, 0);
+        cudaEventRecord(e0);
+        for (int i = 0; i < reps; ++i) vrte::gemm_batched(g, 0);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms1;
+        cudaEventElapsedTime(&ms1, e0, e1);
+        for (int i = 0; i < 3; ++i)
+            cublasDgemmStridedBatched(h, ta ? CUBLAS_OP_T : CUBLAS_OP_N, tb ? CUBLAS_OP_T : CUBLAS_OP_N, m, n, k,
+                                      &alpha, a, lda, sa, b, ldb, sb, &beta, c2, ldc, sc, batch);
+        cudaEventRecord(e0);
+        for (int i = 0; i < reps; ++i)
+            cublasDgemmStridedBatched(h, ta ? CUBLAS_OP_T : CUBLAS_OP_N, tb ? CUBLAS_OP_T : CUBLAS_OP_N, m, n, k,
+                                      &alpha, a, lda, sa, b, ldb, sb, &beta, c2, ldc, sc, batch);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms2;
+        cudaEventElapsedTime(&ms2, e0, e1);
+        const double fl = 2.0 * m * n * k * batch;
+        std::printf("m=%d n=%d k=%d batch=%d ta=%d tb=%d  ours %.3f ms %.2f TF/s   cublas %.3f ms %.2f TF/s  rel %.2e\n",
+                    m, n, k, batch, ta, tb, ms1 / reps, fl / (ms1 / reps * 1e-3) / 1e12, ms2 / reps,
+                    fl / (ms2 / reps * 1e-3) / 1e12, rel);
+    } else {
+        std::printf("m=%d n=%d k=%d batch=%d ta=%d tb=%d beta=%g rel %.2e %s\n", m, n, k, batch, ta, tb, beta, rel,
+                    rel < 1e-14 ? "ok" : "FAIL");
+    }
+    cublasDestroy(h);
+    cudaFree(a); cudaFree(b); cudaFree(c); cudaFree(c2);
+    return rel;
+}
+
+int main() {
+    int fails = 0;
+    const int sizes[][3] = {{37, 53, 29}, {64, 128, 16}, {65, 129, 17}, {1, 1, 1}, {256, 7, 100}, {200, 300, 5}};
+    for (auto& s : sizes)
+        for (int ta = 0; ta < 2; ++ta)
+            for (int tb = 0; tb < 2; ++tb)
+                for (double beta : {0.0, 0.7}) fails += run(s[0], s[1], s[2], 3, ta, tb, beta, false) >= 1e-14;
+    run(256, 256, 256, 128, false, false, 0.0, true);
+    run(256, 512, 256, 128, false, false, 0.0, true);
+    run(256, 512, 256, 128, true, false, 0.0, true);
+    run(256, 256, 512, 64, false, false, 1.0, true);
+    run(512, 512, 512, 64, false, false, 0.0, true);
+    run(4096, 4096, 4096, 1, false, false, 0.0, true);
+    std::printf("fails=%d\n", fails);
+    return fails != 0;
+}
