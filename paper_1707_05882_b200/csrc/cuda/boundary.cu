@@ -496,6 +496,13 @@ void lu_solve_batched(const double* A, int G, int batch, const int* ipiv, double
     }
 }
 
+int lu_launch_count(int G, int ncol) {
+    const int nbf = 16, nbs = 64;
+    const int panels = (G + nbf - 1) / nbf, blocks = (G + nbs - 1) / nbs;
+    (void)ncol;
+    return 3 * panels - 1 + 1 + 4 * blocks - 2;
+}
+
 void launch_copy_zp0(const BndArgs& a, cudaStream_t st) {
     const long long total = (long long)a.p.n_orders * 4 * a.p.n_in * a.d;
     copy_zp0_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(a);

@@ -25,6 +25,8 @@ void launch_bnd_rhs(const BndArgs& a, cudaStream_t st);
 void launch_copy_zp0(const BndArgs& a, cudaStream_t st);
 void lu_factor_batched(double* A, int G, int batch, int* ipiv, DeviceStatus* status,
                        const int* order_index, cudaStream_t st);
+// kernels launched by lu_factor_batched + lu_solve_batched
+int lu_launch_count(int G, int ncol);
 void lu_solve_batched(const double* A, int G, int batch, const int* ipiv, double* B, int ncol,
                       cudaStream_t st);
 

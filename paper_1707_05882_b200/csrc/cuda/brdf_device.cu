@@ -102,7 +102,9 @@ struct vrte_cuda_plan {
     DevBuf<int> medium, order_index, slot_of_order;
     // homogeneous
     DevBuf<double> gsf_n, gsf_b, E, F, T, Z, psi_p, psi_m, tmp1, tmp2, tmp3, tmp4;
-    DevBuf<double> X, AL, BE, FB, W2, UT, EU;
+    DevBuf<double> X, AL, BE, FB, W2, UT, EU, hwork, Vinv;
+    DevBuf<int> ipivV;
+    bool schur_solves = false;  // VRTE_SOLVE=schur: quasi-triangular solves on the Schur form
     DevBuf<double> wr, wi, femax, nu, lam, residual, rho, sigma_m, rshift;
     DevBuf<int> flags, kind_m, sidx;
     // particular
@@ -116,7 +118,7 @@ struct vrte_cuda_plan {
     DeviceStatus* status = nullptr;  // pinned host-mapped would be nicer; device + copy
     DevBuf<DeviceStatus> status_buf;
     cudaEvent_t ev[16] = {};
-    int refine_iters = 3;
+    int refine_iters = 2;
     int part_refine_iters = 2;
     uint64_t launches = 0;
     ~vrte_cuda_plan() {
@@ -207,6 +209,10 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
                     &pl.tmp4, &pl.X})
         b->alloc(B * dd);
     for (auto* b : {&pl.AL, &pl.BE, &pl.FB, &pl.W2, &pl.UT, &pl.EU}) b->alloc(2 * B * dd);
+    pl.hwork.alloc((size_t)B * hessenberg_work_doubles(d));
+    pl.Vinv.alloc(B * dd);
+    pl.ipivV.alloc((size_t)B * d);
+    if (const char* sv = std::getenv("VRTE_SOLVE")) pl.schur_solves = std::string(sv) == "schur";
     pl.rho.alloc((size_t)B * d * 2);
     pl.sigma_m.alloc((size_t)B * d * 4);
     pl.kind_m.alloc((size_t)B * d * 2);
@@ -275,7 +281,14 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     gemm_batched(gemm(d, d, d, pl.F.p, d, dd, false, pl.E.p, d, dd, false, pl.T.p, d, dd, B), st);
     launch_max_abs(pl.T.p, dd, B, pl.femax.p, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[5], st));
-    launch_hessenberg(pl.T.p, pl.Z.p, d, B, st);
+    static const char* hess_mode = std::getenv("VRTE_HESS");  // blocked (default) | unblocked
+    if (hess_mode && std::string(hess_mode) == "unblocked") {
+        launch_hessenberg(pl.T.p, pl.Z.p, d, B, st);
+        nl += 1;
+    } else {
+        launch_hessenberg_blocked(pl.T.p, pl.Z.p, pl.hwork.p, d, B, st);
+        nl += hessenberg_launch_count(d);
+    }
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[6], st));
     launch_hqr(pl.T.p, pl.Z.p, pl.wr.p, pl.wi.p, d, B, pl.status, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[7], st));
@@ -283,6 +296,17 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[8], st));
     gemm_batched(gemm(d, d, d, pl.Z.p, d, dd, false, pl.tmp1.p, d, dd, false, pl.X.p, d, dd, B), st);
     launch_normalize_modes(pl.X.p, pl.wi.p, d, B, st);
+    if (!pl.schur_solves) {
+        // V^-1 of the packed eigenvector matrix: the shifted solves of the
+        // refinement and of the particular stage run in the eigenbasis
+        // (two GEMMs + an independent 1x1/2x2 solve per entry).
+        double* Vlu = pl.hwork.p;  // Hessenberg work is free again
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(Vlu, pl.X.p, sizeof(double) * B * dd, cudaMemcpyDeviceToDevice, st));
+        launch_set_identity(pl.Vinv.p, d, B, st);
+        lu_factor_batched(Vlu, d, B, pl.ipivV.p, pl.status, pl.order_index.p, st);
+        lu_solve_batched(Vlu, d, B, pl.ipivV.p, pl.Vinv.p, d, st);
+        nl += 1 + lu_launch_count(d, d);
+    }
     gemm_batched(gemm(d, d, d, pl.E.p, d, dd, false, pl.X.p, d, dd, false, pl.tmp3.p, d, dd, B), st);
     ModeArgs ma{};
     ma.d = d;
@@ -303,6 +327,20 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     ma.status = pl.status;
     ma.order_index = pl.order_index.p;
     launch_modes(ma, st);
+    // (F E - sigma_c) y_c = r_c for `ncol` columns in place of W = R (ld d):
+    // eigenbasis (default) or Schur form.  `out` = Q y (+ beta out).
+    auto shifted_solve = [&](const double* Rm, double* Wm, int ncol, long long wst, const double* sig,
+                             const int* knd, double* out, double beta) {
+        const double* Lm = pl.schur_solves ? pl.Z.p : pl.Vinv.p;
+        gemm_batched(gemm(d, ncol, d, Lm, d, dd, pl.schur_solves, Rm, d, wst, false, Wm, d, wst, B), st);
+        if (pl.schur_solves)
+            launch_qtri_solve(pl.T.p, d, dd, Wm, ncol, wst, sig, knd, B, nullptr, st);
+        else
+            launch_eig_diag_solve(Wm, d, ncol, wst, pl.wr.p, pl.wi.p, sig, knd, B, st);
+        gemm_batched(gemm(d, ncol, d, pl.schur_solves ? pl.Z.p : pl.X.p, d, dd, false, Wm, d, wst, false,
+                          out, d, wst, B, 1.0, beta),
+                     st);
+    };
     auto residual_gemms = [&]() {
         gemm_batched(gemm(d, d, d, pl.E.p, d, dd, false, pl.tmp1.p, d, dd, false, pl.tmp3.p, d, dd, B), st);
         gemm_batched(gemm(d, d, d, pl.F.p, d, dd, false, pl.tmp4.p, d, dd, false, pl.tmp2.p, d, dd, B), st);
@@ -357,9 +395,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
         launch_refine_setup(rf, st);
         gemm_batched(gemm(d, 2 * d, d, pl.F.p, d, dd, false, pl.BE.p, d, d2, false, pl.FB.p, d, d2, B), st);
         launch_refine_rhs(rf, st);
-        gemm_batched(gemm(d, 2 * d, d, pl.Z.p, d, dd, true, pl.FB.p, d, d2, false, pl.W2.p, d, d2, B), st);
-        launch_qtri_solve(pl.T.p, d, dd, pl.W2.p, 2 * d, d2, pl.sigma_m.p, pl.kind_m.p, B, nullptr, st);
-        gemm_batched(gemm(d, 2 * d, d, pl.Z.p, d, dd, false, pl.W2.p, d, d2, false, pl.UT.p, d, d2, B), st);
+        shifted_solve(pl.FB.p, pl.W2.p, 2 * d, d2, pl.sigma_m.p, pl.kind_m.p, pl.UT.p, 0.0);
         gemm_batched(gemm(d, 2 * d, d, pl.E.p, d, dd, false, pl.UT.p, d, d2, false, pl.EU.p, d, d2, B), st);
         launch_refine_update(rf, st);
         nl += 11;
@@ -398,9 +434,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     launch_dither(pa, st);
     gemm_batched(gemm(d, R, d, pl.F.p, d, dd, false, pl.sp.p, d, dR, false, pl.fsp.p, d, dR, B), st);
     launch_part_rhs(pa, st);
-    gemm_batched(gemm(d, R, d, pl.Z.p, d, dd, true, pl.rhs.p, d, dR, false, pl.W.p, d, dR, B), st);
-    launch_qtri_solve(pl.T.p, d, dd, pl.W.p, R, dR, pl.sigma.p, pl.kind.p, B, nullptr, st);
-    gemm_batched(gemm(d, R, d, pl.Z.p, d, dd, false, pl.W.p, d, dR, false, pl.g.p, d, dR, B), st);
+    shifted_solve(pl.rhs.p, pl.W.p, R, dR, pl.sigma.p, pl.kind.p, pl.g.p, 0.0);
     gemm_batched(gemm(d, R, d, pl.E.p, d, dd, false, pl.g.p, d, dR, false, pl.eg.p, d, dR, B), st);
     gemm_batched(gemm(d, R, d, pl.F.p, d, dd, false, pl.eg.p, d, dR, false, pl.feg.p, d, dR, B), st);
     // Iterative refinement against the true operator F (E g): the Schur form
@@ -408,9 +442,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     // (componentwise-small on this graded matrix) does not.
     for (int it = 0; it < pl.part_refine_iters; ++it) {
         launch_part_refine_residual(pa, pl.fsp.p, st);
-        gemm_batched(gemm(d, R, d, pl.Z.p, d, dd, true, pl.fsp.p, d, dR, false, pl.W.p, d, dR, B), st);
-        launch_qtri_solve(pl.T.p, d, dd, pl.W.p, R, dR, pl.sigma.p, pl.kind.p, B, nullptr, st);
-        gemm_batched(gemm(d, R, d, pl.Z.p, d, dd, false, pl.W.p, d, dR, false, pl.g.p, d, dR, B, 1.0, 1.0), st);
+        shifted_solve(pl.fsp.p, pl.W.p, R, dR, pl.sigma.p, pl.kind.p, pl.g.p, 1.0);
         gemm_batched(gemm(d, R, d, pl.E.p, d, dd, false, pl.g.p, d, dR, false, pl.eg.p, d, dR, B), st);
         gemm_batched(gemm(d, R, d, pl.F.p, d, dd, false, pl.eg.p, d, dR, false, pl.feg.p, d, dR, B), st);
         nl += 6;

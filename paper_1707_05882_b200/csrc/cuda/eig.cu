@@ -1261,6 +1261,55 @@ __global__ void __launch_bounds__(256) qtri_blocked_kernel(const double* Tall, i
     }
 }
 
+// ------------------------------------------------------------------ eigenbasis solves
+// (Lambda - sigma_c) y_c = w_c with Lambda the real-packed eigenvalue matrix of
+// F E = V Lambda V^-1 (trevc packing: real eigenvalue k -> 1x1; complex pair
+// k (wi > 0), k+1 -> block [[a, b], [-b, a]] acting on the Re/Im columns).
+// Together with the GEMMs W = V^-1 R and Y = V W this replaces the blocked
+// quasi-triangular back substitution: every (matrix, column, eigen-block) is
+// independent.  The 2x2 block is diagonalised exactly (eigenvectors [1, +-i])
+// so a shift next to a + ib loses no accuracy to cancellation in its
+// determinant.  Column kinds as for launch_qtri_solve: 0 real, 1 complex pair
+// (c: Re, c+1: Im), 2 skip.
+__global__ void eig_diag_solve_kernel(double* Wall, int d, int ncol, long long w_stride,
+                                      const double* wrall, const double* wiall,
+                                      const double* sigma, const int* kind, int batch) {
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (idx >= (long long)batch * ncol * d) return;
+    const int k = (int)(idx % d);
+    const long long bc = idx / d;
+    const int c = (int)(bc % ncol), b = (int)(bc / ncol);
+    const int kd = kind[(size_t)b * ncol + c];
+    if (kd != 0 && kd != 1) return;
+    const double wik = wiall[(size_t)b * d + k];
+    if (wik < 0.0) return;  // second row of a pair: handled with its leader
+    const bool cx = kd == 1;
+    const cplx sg = cmk(sigma[2 * ((size_t)b * ncol + c)], sigma[2 * ((size_t)b * ncol + c) + 1]);
+    double* wre = Wall + (size_t)b * w_stride + (size_t)c * d;
+    double* wim = wre + d;
+    const double a = wrall[(size_t)b * d + k];
+    if (wik == 0.0) {
+        const cplx x = cdiv(cmk(wre[k], cx ? wim[k] : 0.0), cmk(a, 0.0) - sg);
+        wre[k] = x.re;
+        if (cx) wim[k] = x.im;
+        return;
+    }
+    // pair rows k, k+1: y = alpha [1; i] + beta [1; -i]
+    const cplx w0 = cmk(wre[k], cx ? wim[k] : 0.0);
+    const cplx w1 = cmk(wre[k + 1], cx ? wim[k + 1] : 0.0);
+    const cplx iw1 = cmk(-w1.im, w1.re);
+    const cplx al = cdiv(0.5 * (w0 - iw1), cmk(a, wik) - sg);
+    const cplx be = cdiv(0.5 * (w0 + iw1), cmk(a, -wik) - sg);
+    const cplx y0 = al + be, dif = al - be;
+    const cplx y1 = cmk(-dif.im, dif.re);
+    wre[k] = y0.re;
+    wre[k + 1] = y1.re;
+    if (cx) {
+        wim[k] = y0.im;
+        wim[k + 1] = y1.im;
+    }
+}
+
 }  // namespace
 
 void launch_max_abs(const double* A, long long per, int batch, double* out, cudaStream_t st) {
@@ -1336,6 +1385,31 @@ void launch_qtri_solve(const double* T, int d, long long t_stride, double* W, in
     const int tiles = (ncol + QCT - 1) / QCT;
     qtri_blocked_kernel<<<(unsigned)(batch * tiles), 256, smem, st>>>(T, d, t_stride, W, ncol, w_stride,
                                                                      sigma, kind, t_index);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_eig_diag_solve(double* W, int d, int ncol, long long w_stride, const double* wr,
+                           const double* wi, const double* sigma, const int* kind, int batch,
+                           cudaStream_t st) {
+    const long long total = (long long)batch * ncol * d;
+    if (total == 0) return;
+    eig_diag_solve_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(W, d, ncol, w_stride, wr, wi,
+                                                                          sigma, kind, batch);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+__global__ void set_identity_batched_kernel(double* Z, int d, long long total) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long w = e % ((long long)d * d);
+        Z[e] = (w % d == w / d) ? 1.0 : 0.0;
+    }
+}
+
+void launch_set_identity(double* Z, int d, int batch, cudaStream_t st) {
+    const long long total = (long long)d * d * batch;
+    const long long blocks = (total + 255) / 256;
+    set_identity_batched_kernel<<<(unsigned)(blocks < 8192 ? blocks : 8192), 256, 0, st>>>(Z, d, total);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 

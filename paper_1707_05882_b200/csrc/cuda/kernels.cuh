@@ -38,6 +38,13 @@ void launch_beam_source(const ProblemDev& p, const double* gsf_nodes, const doub
 // eig.cu
 void launch_max_abs(const double* A, long long per, int batch, double* out, cudaStream_t st);
 void launch_hessenberg(double* A, double* Z, int d, int batch, cudaStream_t st);
+// hessenberg.cu: blocked reduction (panel kernel + DMMA trailing updates) and
+// explicit Q in Z; `work` holds hessenberg_work_doubles(d) doubles per matrix.
+int hessenberg_panel_width(int d);
+size_t hessenberg_work_doubles(int d);
+void launch_hessenberg_blocked(double* A, double* Z, double* work, int d, int batch,
+                               cudaStream_t st);
+int hessenberg_launch_count(int d);
 void launch_hqr(double* H, double* Z, double* wr, double* wi, int d, int batch,
                 DeviceStatus* status, cudaStream_t st);
 void launch_trevc(const double* T, const double* wr, const double* wi, double* Y, int d,
@@ -82,5 +89,12 @@ void launch_residual(const ResidualArgs& a, cudaStream_t st);
 void launch_qtri_solve(const double* T, int d, long long t_stride, double* W, int ncol,
                        long long w_stride, const double* sigma, const int* kind, int batch,
                        const int* t_index, cudaStream_t st);
+
+// Same contract as launch_qtri_solve, but in the eigenbasis of F E: W must
+// already hold V^-1 R; on return it holds (Lambda - sigma_c)^-1 V^-1 R.
+void launch_eig_diag_solve(double* W, int d, int ncol, long long w_stride, const double* wr,
+                           const double* wi, const double* sigma, const int* kind, int batch,
+                           cudaStream_t st);
+void launch_set_identity(double* Z, int d, int batch, cudaStream_t st);
 
 }  // namespace vrte
