@@ -106,6 +106,12 @@ VRTE_API int32_t vrte_cuda_synthesize(const vrte_cuda_problem* problem, const do
 
 VRTE_API int32_t vrte_cuda_device_count(void);
 
+/* Kernel-level check of the batched row-major LU (lu.cu) used by the boundary
+ * stage: X[b] = A[b]^-1 B[b] for `batch` row-major G x G systems with `ncol`
+ * right-hand sides (host arrays, row-major).  Returns 0, 3 (singular) or 5. */
+VRTE_API int32_t vrte_cuda_lu_solve(const double* A, int32_t G, int32_t batch, const double* B,
+                                    int32_t ncol, double* X, int32_t device);
+
 #ifdef __cplusplus
 }
 #endif

@@ -135,7 +135,7 @@ EXPORTED = [
     "vrte_cuda_brdf", "vrte_cuda_plan_create", "vrte_cuda_plan_run", "vrte_cuda_plan_fetch",
     "vrte_cuda_plan_fetch_up", "vrte_cuda_plan_fetch_modes", "vrte_cuda_plan_fetch_ef",
     "vrte_cuda_plan_destroy",
-    "vrte_cuda_synthesize", "vrte_cuda_device_count",
+    "vrte_cuda_synthesize", "vrte_cuda_device_count", "vrte_cuda_lu_solve",
 ]
 
 
@@ -176,6 +176,7 @@ def lib():
     L.vrte_cuda_plan_fetch_modes.argtypes = [vp, dp, dp, dp, dp]
     L.vrte_cuda_plan_destroy.argtypes = [vp]
     L.vrte_cuda_plan_fetch_ef.argtypes = [vp, dp, dp]
+    L.vrte_cuda_lu_solve.argtypes = [dp, C.c_int32, C.c_int32, dp, C.c_int32, dp, C.c_int32]
     L.vrte_solve_radiance.argtypes = [vp, C.POINTER(Options), dp, C.c_size_t, C.POINTER(vp)]
     L.vrte_mc_trace.argtypes = [vp, C.POINTER(Options), C.c_uint64, C.c_uint64, C.c_int32,
                                 C.c_int32, C.POINTER(vp)]
@@ -190,6 +191,20 @@ def _check(code: int):
 
 def _dp(a):
     return None if a is None else a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def lu_solve(A, B, device: int = 0) -> np.ndarray:
+    """Batched dense solve through the boundary stage's row-major LU kernels
+    (kernel-level check): A [batch, G, G], B [batch, G, ncol] -> A^-1 B."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    B = np.ascontiguousarray(B, dtype=np.float64)
+    batch, G, _ = A.shape
+    ncol = B.shape[2]
+    X = np.zeros_like(B)
+    code = lib().vrte_cuda_lu_solve(_dp(A), G, batch, _dp(B), ncol, _dp(X), device)
+    if code != 0:
+        raise VrteError(code, "vrte_cuda_lu_solve failed (singular or bad arguments)")
+    return X
 
 
 def version() -> str:

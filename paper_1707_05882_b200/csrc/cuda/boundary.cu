@@ -35,14 +35,15 @@ struct ModeView {
 __device__ inline cplx dflip(cplx v, int i) { return ((i & 3) >= 2) ? cmk(-v.re, -v.im) : v; }
 __device__ inline cplx att_of(double tau, cplx nu) { return cexp_(cdiv(cmk(-tau, 0.0), nu)); }
 
-// Thread per (order mo, layer p, packed column jj, row i).
+// Thread per (order mo, layer p, row i, packed column jj); the system is stored
+// ROW-major (lu.cu), lhs[mo][r * G + c].
 __global__ void assemble_kernel(BndArgs a) {
     const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     const int d = a.d, P = a.p.n_layers, G = 2 * d * P;
     const long long total = (long long)a.p.n_orders * P * d * d;
     if (idx >= total) return;
-    const int i = (int)(idx % d);
-    const int jj = (int)((idx / d) % d);
+    const int jj = (int)(idx % d);
+    const int i = (int)((idx / d) % d);
     const int p = (int)((idx / ((long long)d * d)) % P);
     const int mo = (int)(idx / ((long long)d * d * P));
     const size_t om = (size_t)a.p.medium[p] * a.p.n_orders + mo;
@@ -53,33 +54,34 @@ __global__ void assemble_kernel(BndArgs a) {
     const cplx att = att_of(a.p.tau[p], nu);
     auto pk = [&](cplx v) { return imc ? v.im : v.re; };
     double* A = a.lhs + (size_t)mo * G * G;
-    const size_t ca = (size_t)(2 * d * p + jj) * G;      // column A_p(jj)
-    const size_t cbk = (size_t)(2 * d * p + d + jj) * G;  // column B_p(jj)
+    const int ca = 2 * d * p + jj;       // column A_p(jj)
+    const int cbk = 2 * d * p + d + jj;  // column B_p(jj)
+    auto at = [&](int r, int c) -> double& { return A[(size_t)r * G + c]; };
     if (p == 0) {
-        A[ca + i] = pk(dflip(pm, i));
-        A[cbk + i] = pk(att * dflip(pp, i));
+        at(i, ca) = pk(dflip(pm, i));
+        at(i, cbk) = pk(att * dflip(pp, i));
         double* T0 = a.top0 + (size_t)mo * d * 2 * d;
         T0[(size_t)jj * d + i] = pk(pp);
         T0[(size_t)(d + jj) * d + i] = pk(att * pm);
     }
     if (p < P - 1) {
         const int ru = d + 2 * d * p;
-        A[ca + ru + i] = pk(att * pp);
-        A[ca + ru + d + i] = pk(att * dflip(pm, i));
-        A[cbk + ru + i] = pk(pm);
-        A[cbk + ru + d + i] = pk(dflip(pp, i));
+        at(ru + i, ca) = pk(att * pp);
+        at(ru + d + i, ca) = pk(att * dflip(pm, i));
+        at(ru + i, cbk) = pk(pm);
+        at(ru + d + i, cbk) = pk(dflip(pp, i));
     }
     if (p > 0) {
         const int ru = d + 2 * d * (p - 1);
-        A[ca + ru + i] = -pk(pp);
-        A[ca + ru + d + i] = -pk(dflip(pm, i));
-        A[cbk + ru + i] = -pk(att * pm);
-        A[cbk + ru + d + i] = -pk(att * dflip(pp, i));
+        at(ru + i, ca) = -pk(pp);
+        at(ru + d + i, ca) = -pk(dflip(pm, i));
+        at(ru + i, cbk) = -pk(att * pm);
+        at(ru + d + i, cbk) = -pk(att * dflip(pp, i));
     }
     if (p == P - 1) {
         const int rb = d + 2 * d * (P - 1);
-        A[ca + rb + i] = pk(att * pp);
-        A[cbk + rb + i] = pk(pm);
+        at(rb + i, ca) = pk(att * pp);
+        at(rb + i, cbk) = pk(pm);
     }
 }
 
@@ -134,9 +136,9 @@ __global__ void base_kernel(BndArgs a, int mo) {
     reflect_rows(a.p, v, d, lane, out);
     __syncwarp();
     double* A = a.lhs + (size_t)mo * G * G;
-    const size_t col = (size_t)(2 * d * q + (isb ? d : 0) + jj) * G;
+    const int col = 2 * d * q + (isb ? d : 0) + jj;
     const int rb = d + 2 * d * (P - 1);
-    for (int i = lane; i < d; i += 32) A[col + rb + i] -= out[i];
+    for (int i = lane; i < d; i += 32) A[(size_t)(rb + i) * G + col] -= out[i];
 }
 
 // Right-hand sides: warp per (order mo, column = incident*4 + channel).
@@ -149,7 +151,12 @@ __global__ void rhs_kernel(BndArgs a) {
     const int mo = gw / R, col = gw % R, ii = col / 4, c = col % 4;
     const int m = a.p.order_of(mo);
     const double mu0 = a.p.mu_in[ii];
-    double* B = a.rhs + ((size_t)mo * R + col) * G;
+    // row-major [G][R] per order (lu.cu); B(r) = rhs[mo][r * R + col]
+    struct RowView {
+        double* base;
+        int R;
+        __device__ double& operator[](int r) const { return base[(size_t)r * R]; }
+    } B{a.rhs + (size_t)mo * R * G + col, R};
     auto zp = [&](int p, int i) {
         const size_t om = (size_t)a.p.medium[p] * a.p.n_orders + mo;
         return a.zp[(om * R + col) * d + i];
@@ -193,171 +200,6 @@ __global__ void rhs_kernel(BndArgs a) {
     }
 }
 
-// ---------------------------------------------------------------- batched LU
-// Panel factorization with partial pivoting, panel staged in shared memory.
-__global__ void lu_panel_kernel(double* Aall, int G, int k0, int jb, int* ipiv_all,
-                                DeviceStatus* status, const int* order_index) {
-    extern __shared__ double P[];  // column-major np x jb
-    __shared__ double rv[32];
-    __shared__ int ri[32];
-    __shared__ int s_piv;
-    const int b = blockIdx.x, t = threadIdx.x, nt = blockDim.x;
-    const int np = G - k0;
-    double* A = Aall + (size_t)b * G * G;
-    int* ipiv = ipiv_all + (size_t)b * G;
-    for (int idx = t; idx < np * jb; idx += nt) {
-        const int r = idx % np, c = idx / np;
-        P[idx] = A[(size_t)(k0 + r) + (size_t)(k0 + c) * G];
-    }
-    __syncthreads();
-    for (int j = 0; j < jb; ++j) {
-        // argmax |P[r][j]|, r >= j (first index on ties)
-        double best = -1.0;
-        int bi = j;
-        for (int r = j + t; r < np; r += nt) {
-            const double v = fabs(P[(size_t)j * np + r]);
-            if (v > best) {
-                best = v;
-                bi = r;
-            }
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (ov > best || (ov == best && oi < bi)) {
-                best = ov;
-                bi = oi;
-            }
-        }
-        if ((t & 31) == 0) {
-            rv[t >> 5] = best;
-            ri[t >> 5] = bi;
-        }
-        __syncthreads();
-        if (t == 0) {
-            double bv = rv[0];
-            int bidx = ri[0];
-            for (int w = 1; w < (nt >> 5); ++w)
-                if (rv[w] > bv || (rv[w] == bv && ri[w] < bidx)) {
-                    bv = rv[w];
-                    bidx = ri[w];
-                }
-            s_piv = bidx;
-            ipiv[k0 + j] = k0 + bidx;
-            if (bv == 0.0)
-                report_failure(status, kFailLuSingular, 3, order_index ? order_index[b] : b,
-                               (double)(k0 + j));
-        }
-        __syncthreads();
-        const int pr = s_piv;
-        if (pr != j)
-            for (int c = t; c < jb; c += nt) {
-                const double tmp = P[(size_t)c * np + j];
-                P[(size_t)c * np + j] = P[(size_t)c * np + pr];
-                P[(size_t)c * np + pr] = tmp;
-            }
-        __syncthreads();
-        const double piv = P[(size_t)j * np + j];
-        if (piv != 0.0) {
-            const double rcp = 1.0 / piv;
-            for (int r = j + 1 + t; r < np; r += nt) {
-                const double l = P[(size_t)j * np + r] * rcp;
-                P[(size_t)j * np + r] = l;
-                for (int c = j + 1; c < jb; ++c) P[(size_t)c * np + r] -= l * P[(size_t)c * np + j];
-            }
-        }
-        __syncthreads();
-    }
-    for (int idx = t; idx < np * jb; idx += nt) {
-        const int r = idx % np, c = idx / np;
-        A[(size_t)(k0 + r) + (size_t)(k0 + c) * G] = P[idx];
-    }
-}
-
-// Row interchanges of the panel applied to every other column, then the
-// unit-lower triangular solve for the U12 block row.  Thread per column.
-__global__ void lu_swap_trsm_kernel(double* Aall, int G, int k0, int jb, const int* ipiv_all) {
-    __shared__ double Lt[64 * 64];
-    const int b = blockIdx.y;
-    double* A = Aall + (size_t)b * G * G;
-    const int* ipiv = ipiv_all + (size_t)b * G;
-    for (int idx = threadIdx.x; idx < jb * jb; idx += blockDim.x) {
-        const int r = idx % jb, c = idx / jb;
-        Lt[r * 64 + c] = A[(size_t)(k0 + r) + (size_t)(k0 + c) * G];
-    }
-    __syncthreads();
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= G || (c >= k0 && c < k0 + jb)) return;
-    double* col = A + (size_t)c * G;
-    for (int j = 0; j < jb; ++j) {
-        const int pr = ipiv[k0 + j];
-        if (pr != k0 + j) {
-            const double tmp = col[k0 + j];
-            col[k0 + j] = col[pr];
-            col[pr] = tmp;
-        }
-    }
-    if (c < k0) return;
-    double x[64];
-#pragma unroll 1
-    for (int j = 0; j < jb; ++j) {
-        double v = col[k0 + j];
-        for (int i = 0; i < j; ++i) v -= Lt[j * 64 + i] * x[i];
-        x[j] = v;
-        col[k0 + j] = v;
-    }
-}
-
-// getrs pieces: row interchanges on B, and the diagonal-block triangular
-// solves of the blocked forward/backward substitution.  Thread per column.
-__global__ void laswp_kernel(double* Ball, int G, int ncol, const int* ipiv_all) {
-    const int b = blockIdx.y, c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= ncol) return;
-    double* col = Ball + (size_t)b * G * ncol + (size_t)c * G;
-    const int* ipiv = ipiv_all + (size_t)b * G;
-    for (int i = 0; i < G; ++i) {
-        const int pr = ipiv[i];
-        if (pr != i) {
-            const double tmp = col[i];
-            col[i] = col[pr];
-            col[pr] = tmp;
-        }
-    }
-}
-
-template <bool LOWER>
-__global__ void trsm_diag_kernel(const double* Aall, double* Ball, int G, int ncol, int k0,
-                                 int jb) {
-    __shared__ double Tt[64 * 64];
-    const int b = blockIdx.y;
-    const double* A = Aall + (size_t)b * G * G;
-    for (int idx = threadIdx.x; idx < jb * jb; idx += blockDim.x) {
-        const int r = idx % jb, c = idx / jb;
-        Tt[r * 64 + c] = A[(size_t)(k0 + r) + (size_t)(k0 + c) * G];
-    }
-    __syncthreads();
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= ncol) return;
-    double* col = Ball + (size_t)b * G * ncol + (size_t)c * G + k0;
-    double x[64];
-    if (LOWER) {
-#pragma unroll 1
-        for (int j = 0; j < jb; ++j) {
-            double v = col[j];
-            for (int i = 0; i < j; ++i) v -= Tt[j * 64 + i] * x[i];
-            x[j] = v;
-        }
-    } else {
-#pragma unroll 1
-        for (int j = jb - 1; j >= 0; --j) {
-            double v = col[j];
-            for (int i = j + 1; i < jb; ++i) v -= Tt[j * 64 + i] * x[i];
-            x[j] = v / Tt[j * 64 + j];
-        }
-    }
-    for (int j = 0; j < jb; ++j) col[j] = x[j];
-}
-
 // up = Z+ of the top layer (then += Top0 * coefficients by GEMM).
 __global__ void copy_zp0_kernel(BndArgs a) {
     const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -396,111 +238,6 @@ void launch_bnd_rhs(const BndArgs& a, cudaStream_t st) {
     rhs_kernel<<<(unsigned)((total + warps - 1) / warps), warps * 32,
                  warps * 2 * a.d * sizeof(double), st>>>(a);
     VRTE_CUDA_CHECK(cudaGetLastError());
-}
-
-void lu_factor_batched(double* A, int G, int batch, int* ipiv, DeviceStatus* status,
-                       const int* order_index, cudaStream_t st) {
-    const int nb = 16;
-    static bool attr = false;
-    if (!attr) {
-        VRTE_CUDA_CHECK(cudaFuncSetAttribute(lu_panel_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        attr = true;
-    }
-    for (int k0 = 0; k0 < G; k0 += nb) {
-        const int jb = min(nb, G - k0);
-        const size_t smem = (size_t)(G - k0) * jb * sizeof(double);
-        lu_panel_kernel<<<batch, 256, smem, st>>>(A, G, k0, jb, ipiv, status, order_index);
-        VRTE_CUDA_CHECK(cudaGetLastError());
-        dim3 g2((G + 127) / 128, batch);
-        lu_swap_trsm_kernel<<<g2, 128, 0, st>>>(A, G, k0, jb, ipiv);
-        VRTE_CUDA_CHECK(cudaGetLastError());
-        const int rest = G - k0 - jb;
-        if (rest > 0) {
-            GemmBatch g{};
-            g.m = rest;
-            g.n = rest;
-            g.k = jb;
-            g.a = A + (k0 + jb) + (size_t)k0 * G;
-            g.lda = G;
-            g.stride_a = (long long)G * G;
-            g.b = A + k0 + (size_t)(k0 + jb) * G;
-            g.ldb = G;
-            g.stride_b = (long long)G * G;
-            g.c = A + (k0 + jb) + (size_t)(k0 + jb) * G;
-            g.ldc = G;
-            g.stride_c = (long long)G * G;
-            g.batch = batch;
-            g.alpha = -1.0;
-            g.beta = 1.0;
-            gemm_batched(g, st);
-        }
-    }
-}
-
-void lu_solve_batched(const double* A, int G, int batch, const int* ipiv, double* B, int ncol,
-                      cudaStream_t st) {
-    const int nb = 64;
-    dim3 gc((ncol + 127) / 128, batch);
-    laswp_kernel<<<gc, 128, 0, st>>>(B, G, ncol, ipiv);
-    VRTE_CUDA_CHECK(cudaGetLastError());
-    for (int k0 = 0; k0 < G; k0 += nb) {
-        const int jb = min(nb, G - k0);
-        trsm_diag_kernel<true><<<gc, 128, 0, st>>>(A, B, G, ncol, k0, jb);
-        VRTE_CUDA_CHECK(cudaGetLastError());
-        const int rest = G - k0 - jb;
-        if (rest > 0) {
-            GemmBatch g{};
-            g.m = rest;
-            g.n = ncol;
-            g.k = jb;
-            g.a = A + (k0 + jb) + (size_t)k0 * G;
-            g.lda = G;
-            g.stride_a = (long long)G * G;
-            g.b = B + k0;
-            g.ldb = G;
-            g.stride_b = (long long)G * ncol;
-            g.c = B + k0 + jb;
-            g.ldc = G;
-            g.stride_c = (long long)G * ncol;
-            g.batch = batch;
-            g.alpha = -1.0;
-            g.beta = 1.0;
-            gemm_batched(g, st);
-        }
-    }
-    const int nblk = (G + nb - 1) / nb;
-    for (int bk = nblk - 1; bk >= 0; --bk) {
-        const int k0 = bk * nb, jb = min(nb, G - k0);
-        trsm_diag_kernel<false><<<gc, 128, 0, st>>>(A, B, G, ncol, k0, jb);
-        VRTE_CUDA_CHECK(cudaGetLastError());
-        if (k0 > 0) {
-            GemmBatch g{};
-            g.m = k0;
-            g.n = ncol;
-            g.k = jb;
-            g.a = A + (size_t)k0 * G;
-            g.lda = G;
-            g.stride_a = (long long)G * G;
-            g.b = B + k0;
-            g.ldb = G;
-            g.stride_b = (long long)G * ncol;
-            g.c = B;
-            g.ldc = G;
-            g.stride_c = (long long)G * ncol;
-            g.batch = batch;
-            g.alpha = -1.0;
-            g.beta = 1.0;
-            gemm_batched(g, st);
-        }
-    }
-}
-
-int lu_launch_count(int G, int ncol) {
-    const int nbf = 16, nbs = 64;
-    const int panels = (G + nbf - 1) / nbf, blocks = (G + nbs - 1) / nbs;
-    (void)ncol;
-    return 3 * panels - 1 + 1 + 4 * blocks - 2;
 }
 
 void launch_copy_zp0(const BndArgs& a, cudaStream_t st) {

@@ -14,20 +14,23 @@ struct BndArgs {
     const double* wi;     // [om][d] (pair layout)
     const double* zp;     // [om][R][d]
     const double* zm;
-    double* lhs;          // [mo][G*G]
+    double* lhs;          // [mo][G*G] row-major
     double* top0;         // [mo][d * 2d]
-    double* rhs;          // [mo][R][G]
+    double* rhs;          // [mo][G][R] row-major
     double* up;           // [mo][R][d]
 };
 
 void launch_bnd_assemble(const BndArgs& a, cudaStream_t st);
 void launch_bnd_rhs(const BndArgs& a, cudaStream_t st);
 void launch_copy_zp0(const BndArgs& a, cudaStream_t st);
-void lu_factor_batched(double* A, int G, int batch, int* ipiv, DeviceStatus* status,
-                       const int* order_index, cudaStream_t st);
-// kernels launched by lu_factor_batched + lu_solve_batched
-int lu_launch_count(int G, int ncol);
-void lu_solve_batched(const double* A, int G, int batch, const int* ipiv, double* B, int ncol,
-                      cudaStream_t st);
+// lu.cu: batched LU with partial pivoting on ROW-major G x G matrices.
+// ipiv: [batch][G] absolute pivot rows (LAPACK order); perm: [batch][G] net
+// row permutation (row i of P B = row perm[i] of B).
+void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatus* status,
+                  const int* order_index, cudaStream_t st);
+// X = A^-1 B for row-major B, X ([batch][G][ncol]); B is not modified.
+void lu_solve_rm(const double* A, int G, int batch, const int* perm, const double* B, double* X,
+                 int ncol, cudaStream_t st);
+int lu_rm_launch_count(int G);
 
 }  // namespace vrte

@@ -103,7 +103,7 @@ struct vrte_cuda_plan {
     // homogeneous
     DevBuf<double> gsf_n, gsf_b, E, F, T, Z, psi_p, psi_m, tmp1, tmp2, tmp3, tmp4;
     DevBuf<double> X, AL, BE, FB, W2, UT, EU, hwork, Vinv;
-    DevBuf<int> ipivV;
+    DevBuf<int> ipivV, permV;
     bool schur_solves = false;  // VRTE_SOLVE=schur: quasi-triangular solves on the Schur form
     DevBuf<double> wr, wi, femax, nu, lam, residual, rho, sigma_m, rshift;
     DevBuf<int> flags, kind_m, sidx;
@@ -111,8 +111,8 @@ struct vrte_cuda_plan {
     DevBuf<double> sp, sm, fsp, rhs, W, g, eg, feg, zp, zm, mu_eff, sigma;
     DevBuf<int> kind;
     // boundary
-    DevBuf<double> lhs, top0, rhs_b, up;
-    DevBuf<int> ipiv;
+    DevBuf<double> lhs, top0, rhs_b, rhs_x, up;
+    DevBuf<int> ipiv, perm;
     // synthesis
     DevBuf<double> out;
     DeviceStatus* status = nullptr;  // pinned host-mapped would be nicer; device + copy
@@ -212,6 +212,7 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pl.hwork.alloc((size_t)B * hessenberg_work_doubles(d));
     pl.Vinv.alloc(B * dd);
     pl.ipivV.alloc((size_t)B * d);
+    pl.permV.alloc((size_t)B * d);
     if (const char* sv = std::getenv("VRTE_SOLVE")) pl.schur_solves = std::string(sv) == "schur";
     pl.rho.alloc((size_t)B * d * 2);
     pl.sigma_m.alloc((size_t)B * d * 4);
@@ -234,7 +235,9 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pl.lhs.alloc((size_t)NO * G * G);
     pl.top0.alloc((size_t)NO * d * 2 * d);
     pl.rhs_b.alloc((size_t)NO * R * G);
+    pl.rhs_x.alloc((size_t)NO * R * G);
     pl.ipiv.alloc((size_t)NO * G);
+    pl.perm.alloc((size_t)NO * G);
     pl.up.alloc((size_t)NO * R * d);
     pl.out.alloc((size_t)pl.n_in * N * pl.n_dphi * 16);
     pl.status_buf.alloc(1);
@@ -300,12 +303,14 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
         // V^-1 of the packed eigenvector matrix: the shifted solves of the
         // refinement and of the particular stage run in the eigenbasis
         // (two GEMMs + an independent 1x1/2x2 solve per entry).
+        // The column-major V read row-major is V^T: factor V^T, solve V^T Y = I
+        // row-major, and Y read column-major is V^-1.
         double* Vlu = pl.hwork.p;  // Hessenberg work is free again
         VRTE_CUDA_CHECK(cudaMemcpyAsync(Vlu, pl.X.p, sizeof(double) * B * dd, cudaMemcpyDeviceToDevice, st));
-        launch_set_identity(pl.Vinv.p, d, B, st);
-        lu_factor_batched(Vlu, d, B, pl.ipivV.p, pl.status, pl.order_index.p, st);
-        lu_solve_batched(Vlu, d, B, pl.ipivV.p, pl.Vinv.p, d, st);
-        nl += 1 + lu_launch_count(d, d);
+        launch_set_identity(pl.tmp2.p, d, B, st);
+        lu_factor_rm(Vlu, d, B, pl.ipivV.p, pl.permV.p, pl.status, pl.order_index.p, st);
+        lu_solve_rm(Vlu, d, B, pl.permV.p, pl.tmp2.p, pl.Vinv.p, d, st);
+        nl += 1 + lu_rm_launch_count(d);
     }
     gemm_batched(gemm(d, d, d, pl.E.p, d, dd, false, pl.X.p, d, dd, false, pl.tmp3.p, d, dd, B), st);
     ModeArgs ma{};
@@ -468,19 +473,17 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     launch_bnd_assemble(ba, st);
     launch_bnd_rhs(ba, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[11], st));
-    lu_factor_batched(pl.lhs.p, G, NO, pl.ipiv.p, pl.status, pl.order_index.p, st);
+    lu_factor_rm(pl.lhs.p, G, NO, pl.ipiv.p, pl.perm.p, pl.status, pl.order_index.p, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[12], st));
-    lu_solve_batched(pl.lhs.p, G, NO, pl.ipiv.p, pl.rhs_b.p, R, st);
+    lu_solve_rm(pl.lhs.p, G, NO, pl.perm.p, pl.rhs_b.p, pl.rhs_x.p, R, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[13], st));
     launch_copy_zp0(ba, st);
-    gemm_batched(gemm(d, R, 2 * d, pl.top0.p, d, (long long)d * 2 * d, false, pl.rhs_b.p, G,
-                      (long long)G * R, false, pl.up.p, d, dR, NO, 1.0, 1.0),
+    // up += Top0 [A_0; B_0]: the first 2d rows of the row-major solution, read
+    // column-major as their transpose
+    gemm_batched(gemm(d, R, 2 * d, pl.top0.p, d, (long long)d * 2 * d, false, pl.rhs_x.p, R,
+                      (long long)G * R, true, pl.up.p, d, dR, NO, 1.0, 1.0),
                  st);
-    {
-        const int nbf = 16, nbs = 64;
-        const uint64_t panels = (G + nbf - 1) / nbf, blocks = (G + nbs - 1) / nbs;
-        nl += 2 + (pd.base_type != 0 ? 1 : 0) + 3 * panels + 1 + 4 * blocks + 2;
-    }
+    nl += 2 + (pd.base_type != 0 ? 1 : 0) + lu_rm_launch_count(G) + 2;
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[3], st));
     // ---------------- synthesis
     if (synth) {
@@ -800,6 +803,36 @@ int32_t vrte_cuda_synthesize(const vrte_cuda_problem* problem, const double* up,
         if (result) result->status = 0;
         return 0;
     });
+}
+
+int32_t vrte_cuda_lu_solve(const double* A, int32_t G, int32_t batch, const double* B, int32_t ncol,
+                           double* X, int32_t device) {
+    if (!A || !B || !X || G < 1 || batch < 1 || ncol < 1) return 5;
+    try {
+        if (device >= 0) VRTE_CUDA_CHECK(cudaSetDevice(device));
+        cudaStream_t st;
+        VRTE_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        DevBuf<double> dA, dB, dX;
+        DevBuf<int> ipiv, perm;
+        DevBuf<DeviceStatus> dst;
+        dA.upload(A, (size_t)batch * G * G, st);
+        dB.upload(B, (size_t)batch * G * ncol, st);
+        dX.alloc((size_t)batch * G * ncol);
+        ipiv.alloc((size_t)batch * G);
+        perm.alloc((size_t)batch * G);
+        dst.alloc(1);
+        VRTE_CUDA_CHECK(cudaMemsetAsync(dst.p, 0, sizeof(DeviceStatus), st));
+        lu_factor_rm(dA.p, G, batch, ipiv.p, perm.p, dst.p, nullptr, st);
+        lu_solve_rm(dA.p, G, batch, perm.p, dB.p, dX.p, ncol, st);
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(X, dX.p, sizeof(double) * dX.n, cudaMemcpyDeviceToHost, st));
+        DeviceStatus s{};
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(&s, dst.p, sizeof s, cudaMemcpyDeviceToHost, st));
+        VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
+        cudaStreamDestroy(st);
+        return s.code != 0 ? 3 : 0;
+    } catch (const std::exception&) {
+        return 3;
+    }
 }
 
 }  // extern "C"
