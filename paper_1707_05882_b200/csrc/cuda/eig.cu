@@ -835,6 +835,564 @@ __global__ void __launch_bounds__(256) hqr_window_kernel(double* Hall, double* Z
     }
 }
 
+
+// ------------------------------------------------------------------ multi-bulge Francis QR
+// Small-bulge multishift QR (the dlaqr5 organisation, without aggressive early
+// deflation): while the active block [L, I] is large, one sweep chases a chain
+// of nb double-shift bulges (2 nb shifts = eigenvalues of the trailing
+// 2nb x 2nb block, computed by a warp-level eigenvalue-only QR), spaced three
+// rows apart, in lock step: warp b owns bulge b.  Within a step every bulge
+// first computes its reflector from the state at the start of the step and
+// applies it from the left (disjoint rows), then -- after a named barrier --
+// from the right and to the chunk factor U (disjoint columns); left and right
+// reflections of different bulges commute, so this equals LAPACK's
+// bottom-to-top bulge order.  Chunks of MS steps are chased in a MW x MW
+// shared-memory window; U is applied to the rest of H and to Z by the whole
+// CTA.  Small active blocks and exceptional-shift sweeps use one bulge with
+// the dlahqr shift / start rules (identical to hqr_window_kernel).
+constexpr int MB_MAX = 4;   // bulges per sweep
+constexpr int MS = 16;      // chase steps per chunk
+constexpr int MW = 32;      // window (>= MS + 3 (MB_MAX - 1) + 4)
+constexpr int TQ = 8;       // tiny-matrix leading dimension (2 MB_MAX)
+
+__device__ inline void named_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Eigenvalues of the n x n Hessenberg S (ld TQ, zero padded) by one warp:
+// double-shift QR without vectors (dlahqr, wantt = wantz = false).  Scalar
+// control is computed redundantly by every lane; row/column operations are
+// lane-parallel.
+__device__ void warp_tiny_eig(double* S, int n, double* sr, double* si) {
+    const int lane = threadIdx.x & 31;
+    const double ulp = kUlp, smlnum = kSafeMin * ((double)n / ulp);
+    auto A = [&](int r, int c) -> double& { return S[r + c * TQ]; };
+    int I = n - 1;
+    int kdefl = 0;
+    while (I >= 0) {
+        int L = 0;
+        bool conv = false;
+        for (int its = 0; its <= 40 * n; ++its) {
+            int kb = L;
+            for (int k = I; k > L; --k)
+                if (small_subdiag_g(S, TQ, k, ulp, smlnum)) {
+                    kb = k;
+                    break;
+                }
+            L = kb;
+            __syncwarp();
+            if (L > 0 && lane == 0) A(L, L - 1) = 0.0;
+            __syncwarp();
+            if (L >= I - 1) {
+                conv = true;
+                break;
+            }
+            ++kdefl;
+            double h11, h12, h21, h22;
+            if (kdefl % 20 == 0) {
+                const double s = fabs(A(I, I - 1)) + fabs(A(I - 1, I - 2 >= 0 ? I - 2 : 0));
+                h11 = 0.75 * s + A(I, I);
+                h12 = -0.4375 * s;
+                h21 = s;
+                h22 = h11;
+            } else if (kdefl % 10 == 0) {
+                const double s = fabs(A(L + 1, L)) + fabs(A(L + 2, L + 1));
+                h11 = 0.75 * s + A(L, L);
+                h12 = -0.4375 * s;
+                h21 = s;
+                h22 = h11;
+            } else {
+                h11 = A(I - 1, I - 1);
+                h21 = A(I, I - 1);
+                h12 = A(I - 1, I);
+                h22 = A(I, I);
+            }
+            double rt1r, rt1i, rt2r, rt2i;
+            {
+                const double s = fabs(h11) + fabs(h12) + fabs(h21) + fabs(h22);
+                if (s == 0.0) {
+                    rt1r = rt1i = rt2r = rt2i = 0.0;
+                } else {
+                    h11 /= s;
+                    h21 /= s;
+                    h12 /= s;
+                    h22 /= s;
+                    const double tr = (h11 + h22) / 2.0;
+                    const double det = (h11 - tr) * (h22 - tr) - h12 * h21;
+                    const double rtdisc = sqrt(fabs(det));
+                    if (det >= 0.0) {
+                        rt1r = tr * s;
+                        rt2r = rt1r;
+                        rt1i = rtdisc * s;
+                        rt2i = -rt1i;
+                    } else {
+                        rt1r = tr + rtdisc;
+                        rt2r = tr - rtdisc;
+                        if (fabs(rt1r - h22) <= fabs(rt2r - h22)) {
+                            rt1r *= s;
+                            rt2r = rt1r;
+                        } else {
+                            rt2r *= s;
+                            rt1r = rt2r;
+                        }
+                        rt1i = rt2i = 0.0;
+                    }
+                }
+            }
+            const int M = L;
+            for (int k = M; k <= I - 1; ++k) {
+                const int nr = min(3, I - k + 1);
+                double v1, v2, v3;
+                if (k == M) {
+                    double v[3];
+                    start_vector_g(S, TQ, M, rt1r, rt1i, rt2r, rt2i, v);
+                    v1 = v[0];
+                    v2 = v[1];
+                    v3 = nr == 3 ? v[2] : 0.0;
+                } else {
+                    v1 = A(k, k - 1);
+                    v2 = A(k + 1, k - 1);
+                    v3 = nr == 3 ? A(k + 2, k - 1) : 0.0;
+                }
+                double t1 = 0.0;
+                const double x2 = v2 * v2 + v3 * v3;
+                if (x2 != 0.0) {
+                    const double nv = sqrt(v1 * v1 + x2);
+                    const double beta = -copysign(nv, v1);
+                    t1 = (beta - v1) / beta;
+                    const double sc = 1.0 / (v1 - beta);
+                    v2 *= sc;
+                    v3 *= sc;
+                    v1 = beta;
+                }
+                const double t2 = t1 * v2, t3 = t1 * v3;
+                __syncwarp();
+                const int c = k + lane;
+                if (c <= I) {
+                    const double a0 = A(k, c), a1 = A(k + 1, c), a2 = nr == 3 ? A(k + 2, c) : 0.0;
+                    const double sum = a0 + v2 * a1 + v3 * a2;
+                    A(k, c) = a0 - sum * t1;
+                    A(k + 1, c) = a1 - sum * t2;
+                    if (nr == 3) A(k + 2, c) = a2 - sum * t3;
+                }
+                __syncwarp();
+                if (k > M && lane == 0) {
+                    A(k, k - 1) = v1;
+                    A(k + 1, k - 1) = 0.0;
+                    if (k < I - 1) A(k + 2, k - 1) = 0.0;
+                }
+                const int r = L + lane;
+                if (r <= min(k + 3, I)) {
+                    const double a0 = A(r, k), a1 = A(r, k + 1), a2 = nr == 3 ? A(r, k + 2) : 0.0;
+                    const double sum = a0 + v2 * a1 + v3 * a2;
+                    A(r, k) = a0 - sum * t1;
+                    A(r, k + 1) = a1 - sum * t2;
+                    if (nr == 3) A(r, k + 2) = a2 - sum * t3;
+                }
+                __syncwarp();
+            }
+        }
+        if (!conv) {  // give up gracefully: diagonal entries as shifts
+            for (int q = 0; q <= I; ++q) {
+                sr[q] = A(q, q);
+                si[q] = 0.0;
+            }
+            return;
+        }
+        if (L == I) {
+            sr[I] = A(I, I);
+            si[I] = 0.0;
+        } else {
+            double a = A(I - 1, I - 1), bb = A(I - 1, I), c = A(I, I - 1), dd = A(I, I);
+            double r1r, r1i, r2r, r2i, cs, sn;
+            dlanv2(a, bb, c, dd, r1r, r1i, r2r, r2i, cs, sn);
+            sr[I - 1] = r1r;
+            si[I - 1] = r1i;
+            sr[I] = r2r;
+            si[I] = r2i;
+        }
+        kdefl = 0;
+        I = L - 1;
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(256) hqr_multi_kernel(double* Hall, double* Zall, double* wrall,
+                                                        double* wiall, int d, DeviceStatus* status) {
+    __shared__ double Wn[MW * MW];  // window, column-major Wn[c*MW + r]
+    __shared__ double Us[MW * MW];  // accumulated factor, column-major
+    __shared__ double Sm[TQ * TQ];  // trailing block for the shifts
+    __shared__ double s_sr[TQ], s_si[TQ];
+    __shared__ double s_pr[4 * MB_MAX];  // shift pair per bulge: rt1r rt1i rt2r rt2i
+    __shared__ int s_int;
+    __shared__ int s_nb;
+    __shared__ double s_t1;
+    const int b = blockIdx.x, t = threadIdx.x, nt = blockDim.x, lane = t & 31, warp = t >> 5;
+    double* H = Hall + (size_t)b * d * d;
+    double* Z = Zall + (size_t)b * d * d;
+    double* wr = wrall + (size_t)b * d;
+    double* wi = wiall + (size_t)b * d;
+    const double ulp = kUlp;
+    const double smlnum = kSafeMin * ((double)d / ulp);
+    const int itmax = 30 * max(10, d);
+    const int kexsh = 10;
+    int kdefl = 0;
+    int I = d - 1;
+    unsigned long long nsweep = 0, nstep = 0;
+    unsigned long long cyc[6] = {0, 0, 0, 0, 0, 0};
+    long long tc = clock64();
+    auto tick = [&](int slot) {
+        const long long now = clock64();
+        cyc[slot] += (unsigned long long)(now - tc);
+        tc = now;
+    };
+    while (I >= 0) {
+        int L = 0;
+        bool conv = false;
+        for (int its = 0; its <= itmax; ++its) {
+            int kb = L;
+            for (int k = L + 1 + t; k <= I; k += nt)
+                if (small_subdiag_g(H, d, k, ulp, smlnum)) kb = max(kb, k);
+            L = block_max_int(kb, &s_int);
+            if (L > 0 && t == 0) H[L + (size_t)(L - 1) * d] = 0.0;
+            __syncthreads();
+            if (L >= I - 1) {
+                conv = true;
+                break;
+            }
+            ++kdefl;
+            const int nsize = I - L + 1;
+            int nb = nsize >= 48 ? 4 : (nsize >= 24 ? 2 : 1);
+            if (kdefl % kexsh == 0) nb = 1;
+            int M = L;
+            double v0[3] = {0.0, 0.0, 0.0};
+            if (nb == 1) {
+                double h11, h12, h21, h22;
+                if (kdefl % (2 * kexsh) == 0) {
+                    const double s = fabs(hg(H, d, I, I - 1)) + fabs(hg(H, d, I - 1, I - 2));
+                    h11 = 0.75 * s + hg(H, d, I, I);
+                    h12 = -0.4375 * s;
+                    h21 = s;
+                    h22 = h11;
+                } else if (kdefl % kexsh == 0) {
+                    const double s = fabs(hg(H, d, L + 1, L)) + fabs(hg(H, d, L + 2, L + 1));
+                    h11 = 0.75 * s + hg(H, d, L, L);
+                    h12 = -0.4375 * s;
+                    h21 = s;
+                    h22 = h11;
+                } else {
+                    h11 = hg(H, d, I - 1, I - 1);
+                    h21 = hg(H, d, I, I - 1);
+                    h12 = hg(H, d, I - 1, I);
+                    h22 = hg(H, d, I, I);
+                }
+                double rt1r, rt1i, rt2r, rt2i;
+                {
+                    const double s = fabs(h11) + fabs(h12) + fabs(h21) + fabs(h22);
+                    if (s == 0.0) {
+                        rt1r = rt1i = rt2r = rt2i = 0.0;
+                    } else {
+                        h11 /= s;
+                        h21 /= s;
+                        h12 /= s;
+                        h22 /= s;
+                        const double tr = (h11 + h22) / 2.0;
+                        const double det = (h11 - tr) * (h22 - tr) - h12 * h21;
+                        const double rtdisc = sqrt(fabs(det));
+                        if (det >= 0.0) {
+                            rt1r = tr * s;
+                            rt2r = rt1r;
+                            rt1i = rtdisc * s;
+                            rt2i = -rt1i;
+                        } else {
+                            rt1r = tr + rtdisc;
+                            rt2r = tr - rtdisc;
+                            if (fabs(rt1r - h22) <= fabs(rt2r - h22)) {
+                                rt1r *= s;
+                                rt2r = rt1r;
+                            } else {
+                                rt2r *= s;
+                                rt1r = rt2r;
+                            }
+                            rt1i = rt2i = 0.0;
+                        }
+                    }
+                }
+                int mb = L;
+                for (int mm = L + 1 + t; mm <= I - 2; mm += nt) {
+                    double vv[3];
+                    start_vector_g(H, d, mm, rt1r, rt1i, rt2r, rt2i, vv);
+                    const double h00 = fabs(hg(H, d, mm, mm - 1)) * (fabs(vv[1]) + fabs(vv[2]));
+                    const double h11b = fabs(vv[0]) * (fabs(hg(H, d, mm - 1, mm - 1)) +
+                                                       fabs(hg(H, d, mm, mm)) + fabs(hg(H, d, mm + 1, mm + 1)));
+                    if (h00 <= ulp * h11b) mb = max(mb, mm);
+                }
+                M = block_max_int(mb, &s_int);
+                start_vector_g(H, d, M, rt1r, rt1i, rt2r, rt2i, v0);
+            } else {
+                // 2 nb shifts: eigenvalues of the trailing 2nb x 2nb block
+                const int n2 = 2 * nb, o = I - n2 + 1;
+                if (warp == 0) {
+                    for (int e = lane; e < TQ * TQ; e += 32) {
+                        const int r = e % TQ, c = e / TQ;
+                        Sm[e] = (r < n2 && c < n2 && r <= c + 1) ? hg(H, d, o + r, o + c) : 0.0;
+                    }
+                    __syncwarp();
+                    warp_tiny_eig(Sm, n2, s_sr, s_si);
+                    __syncwarp();
+                    if (lane == 0) {
+                        // sort by decreasing modulus (conjugate pairs stay adjacent), then
+                        // pair: complex pairs as they are, real shifts two at a time
+                        double ar[TQ], ai[TQ];
+                        for (int q = 0; q < n2; ++q) {
+                            ar[q] = s_sr[q];
+                            ai[q] = s_si[q];
+                        }
+                        int nbul = 0;
+                        double rbuf = 0.0;
+                        bool have = false;
+                        for (int q = 0; q < n2; ++q) {
+                            if (ai[q] != 0.0 && q + 1 < n2) {
+                                s_pr[4 * nbul + 0] = ar[q];
+                                s_pr[4 * nbul + 1] = fabs(ai[q]);
+                                s_pr[4 * nbul + 2] = ar[q + 1];
+                                s_pr[4 * nbul + 3] = -fabs(ai[q]);
+                                ++nbul;
+                                ++q;
+                            } else if (have) {
+                                s_pr[4 * nbul + 0] = rbuf;
+                                s_pr[4 * nbul + 1] = 0.0;
+                                s_pr[4 * nbul + 2] = ar[q];
+                                s_pr[4 * nbul + 3] = 0.0;
+                                ++nbul;
+                                have = false;
+                            } else {
+                                rbuf = ar[q];
+                                have = true;
+                            }
+                        }
+                        if (have) {  // odd real count cannot happen with paired complex shifts
+                            s_pr[4 * nbul + 0] = rbuf;
+                            s_pr[4 * nbul + 1] = 0.0;
+                            s_pr[4 * nbul + 2] = rbuf;
+                            s_pr[4 * nbul + 3] = 0.0;
+                            ++nbul;
+                        }
+                        s_nb = max(1, min(nbul, nb));
+                    }
+                }
+                __syncthreads();
+                nb = s_nb;
+            }
+            if (t == 0) s_t1 = 0.0;
+            ++nsweep;
+            const int S_total = (I - M) + 3 * (nb - 1);
+            nstep += (unsigned long long)(I - M) * nb;
+            if (nb > 1) {
+                cyc[4] += 1;
+                cyc[5] += (unsigned long long)(I - M) * nb;
+            }
+            tick(0);
+            for (int s0 = 0; s0 < S_total; s0 += MS) {
+                const int s1 = min(s0 + MS, S_total);
+                const int kmin = max(M, M + s0 - 3 * (nb - 1));
+                const int kmax = min(I - 1, M + s1 - 1);
+                const int wlo = (kmin > M) ? kmin - 1 : M;
+                const int whi = min(kmax + 3, I);
+                const int nw = whi - wlo + 1;
+                for (int idx = t; idx < MW * MW; idx += nt) {
+                    const int r = idx % MW, c = idx / MW;
+                    Wn[idx] = (r < nw && c < nw) ? H[(wlo + r) + (size_t)(wlo + c) * d] : 0.0;
+                    Us[idx] = (r == c) ? 1.0 : 0.0;
+                }
+                __syncthreads();
+                tick(1);
+                if (warp < nb) {
+                    auto W = [&](int r, int c) -> double& { return Wn[(c - wlo) * MW + (r - wlo)]; };
+                    const int bb = warp;
+                    for (int s = s0; s < s1; ++s) {
+                        const int k = M + s - 3 * bb;
+                        const bool active = k >= M && k <= I - 1;
+                        const int nr = active ? min(3, I - k + 1) : 0;
+                        double v2 = 0.0, v3 = 0.0, t1 = 0.0, beta = 0.0;
+                        if (active) {
+                            double v1;
+                            if (k > M) {
+                                v1 = W(k, k - 1);
+                                v2 = W(k + 1, k - 1);
+                                v3 = (nr == 3) ? W(k + 2, k - 1) : 0.0;
+                            } else if (nb == 1) {
+                                v1 = v0[0];
+                                v2 = v0[1];
+                                v3 = (nr == 3) ? v0[2] : 0.0;
+                            } else {
+                                double vv[3];
+                                start_vector_g(Wn, MW, M - wlo, s_pr[4 * bb], s_pr[4 * bb + 1],
+                                               s_pr[4 * bb + 2], s_pr[4 * bb + 3], vv);
+                                v1 = vv[0];
+                                v2 = vv[1];
+                                v3 = (nr == 3) ? vv[2] : 0.0;
+                            }
+                            beta = v1;
+                            const double x2 = fma(v2, v2, v3 * v3);
+                            if (x2 != 0.0) {
+                                const double ss = fma(v1, v1, x2);
+                                const double rq = rsqrt(ss);
+                                const double nv = ss * rq;
+                                const double av1 = fabs(v1);
+                                const double sc = copysign(__drcp_rn(av1 + nv), v1);
+                                t1 = fma(av1, rq, 1.0);
+                                v2 *= sc;
+                                v3 *= sc;
+                                beta = -copysign(nv, v1);
+                            }
+                            const double t2 = t1 * v2, t3 = t1 * v3;
+                            __syncwarp();
+                            for (int c = k + lane; c <= whi; c += 32) {
+                                double& a0 = W(k, c);
+                                double& a1 = W(k + 1, c);
+                                const double a2v = (nr == 3) ? W(k + 2, c) : 0.0;
+                                const double sum = a0 + v2 * a1 + v3 * a2v;
+                                a0 -= sum * t1;
+                                a1 -= sum * t2;
+                                if (nr == 3) W(k + 2, c) = a2v - sum * t3;
+                            }
+                            __syncwarp();
+                            if (lane == 0) {
+                                if (k > M) {
+                                    W(k, k - 1) = beta;
+                                    W(k + 1, k - 1) = 0.0;
+                                    if (k < I - 1) W(k + 2, k - 1) = 0.0;
+                                } else if (nb == 1) {
+                                    s_t1 = t1;  // H(M, M-1) *= (1 - t1) after the chunk
+                                }
+                            }
+                        }
+                        named_bar(1, nb * 32);
+                        if (active) {
+                            const double t2 = t1 * v2, t3 = t1 * v3;
+                            const int rmax = (nr == 3) ? min(k + 3, I) : I;
+                            for (int r = wlo + lane; r <= rmax && r <= whi; r += 32) {
+                                double& a0 = W(r, k);
+                                double& a1 = W(r, k + 1);
+                                const double a2v = (nr == 3) ? W(r, k + 2) : 0.0;
+                                const double sum = a0 + v2 * a1 + v3 * a2v;
+                                a0 -= sum * t1;
+                                a1 -= sum * t2;
+                                if (nr == 3) W(r, k + 2) = a2v - sum * t3;
+                            }
+                            const int c = k - wlo;
+                            for (int r = lane; r < nw; r += 32) {
+                                double* u = Us + r;
+                                const double u0 = u[c * MW], u1 = u[(c + 1) * MW];
+                                const double u2 = (nr == 3) ? u[(c + 2) * MW] : 0.0;
+                                const double sum = u0 + v2 * u1 + v3 * u2;
+                                u[c * MW] = u0 - sum * t1;
+                                u[(c + 1) * MW] = u1 - sum * t2;
+                                if (nr == 3) u[(c + 2) * MW] = u2 - sum * t3;
+                            }
+                        }
+                        named_bar(1, nb * 32);
+                    }
+                }
+                __syncthreads();
+                tick(2);
+                for (int idx = t; idx < nw * nw; idx += nt) {
+                    const int r = idx % nw, c = idx / nw;
+                    H[(wlo + r) + (size_t)(wlo + c) * d] = Wn[c * MW + r];
+                }
+                if (s0 == 0 && nb == 1 && M > L && t == 0) H[M + (size_t)(M - 1) * d] *= (1.0 - s_t1);
+                // off-window updates with U (nw x nw, zero padded to MW)
+                const int n_right = d - 1 - whi, n_above = wlo;
+                for (int task = t; task < n_right + n_above + d; task += nt) {
+                    double x[MW];
+                    if (task < n_right) {  // column right of the window: U^T x
+                        double* col = H + (size_t)(whi + 1 + task) * d + wlo;
+#pragma unroll
+                        for (int q = 0; q < MW; ++q) x[q] = (q < nw) ? col[q] : 0.0;
+                        for (int r = 0; r < nw; ++r) {
+                            double acc = 0.0;
+#pragma unroll
+                            for (int q = 0; q < MW; ++q) acc = fma(Us[r * MW + q], x[q], acc);
+                            col[r] = acc;
+                        }
+                    } else {  // row of H above the window, or of Z: x U
+                        const bool isz = task >= n_right + n_above;
+                        const int i = isz ? task - n_right - n_above : task - n_right;
+                        double* base = (isz ? Z : H) + i + (size_t)wlo * d;
+#pragma unroll
+                        for (int q = 0; q < MW; ++q) x[q] = (q < nw) ? base[(size_t)q * d] : 0.0;
+                        for (int c = 0; c < nw; ++c) {
+                            double acc = 0.0;
+#pragma unroll
+                            for (int q = 0; q < MW; ++q) acc = fma(x[q], Us[c * MW + q], acc);
+                            base[(size_t)c * d] = acc;
+                        }
+                    }
+                }
+                __syncthreads();
+                tick(3);
+            }
+        }
+        if (!conv) {
+            if (t == 0) report_failure(status, kFailHqrNoConverge, 1, b, (double)I);
+            return;
+        }
+        if (L == I) {
+            if (t == 0) {
+                wr[I] = hg(H, d, I, I);
+                wi[I] = 0.0;
+            }
+        } else {
+            double a = hg(H, d, I - 1, I - 1), bb = hg(H, d, I - 1, I), c = hg(H, d, I, I - 1),
+                   dd = hg(H, d, I, I);
+            double r1r, r1i, r2r, r2i, cs, sn;
+            dlanv2(a, bb, c, dd, r1r, r1i, r2r, r2i, cs, sn);
+            __syncthreads();
+            if (t == 0) {
+                H[(I - 1) + (size_t)(I - 1) * d] = a;
+                H[(I - 1) + (size_t)I * d] = bb;
+                H[I + (size_t)(I - 1) * d] = c;
+                H[I + (size_t)I * d] = dd;
+                wr[I - 1] = r1r;
+                wi[I - 1] = r1i;
+                wr[I] = r2r;
+                wi[I] = r2i;
+            }
+            for (int j = I + 1 + t; j < d; j += nt) {
+                double* x = H + (I - 1) + (size_t)j * d;
+                const double xv = x[0], yv = x[1];
+                x[0] = cs * xv + sn * yv;
+                x[1] = cs * yv - sn * xv;
+            }
+            for (int j = t; j <= I - 2; j += nt) {
+                double* x = H + j + (size_t)(I - 1) * d;
+                const double xv = x[0], yv = x[d];
+                x[0] = cs * xv + sn * yv;
+                x[d] = cs * yv - sn * xv;
+            }
+            for (int j = t; j < d; j += nt) {
+                double* zx = Z + j + (size_t)(I - 1) * d;
+                const double xv = zx[0], yv = zx[d];
+                zx[0] = cs * xv + sn * yv;
+                zx[d] = cs * yv - sn * xv;
+            }
+        }
+        kdefl = 0;
+        I = L - 1;
+        __syncthreads();
+    }
+    if (t == 0) {
+        atomicAdd(&status->qr_sweeps, nsweep);
+        atomicAdd(&status->qr_steps, nstep);
+        for (int q = 0; q < 6; ++q) atomicAdd(&status->qr_cycles[q], cyc[q]);
+    }
+    for (int idx = t; idx < d * d; idx += nt) {
+        const int r = idx % d, c = idx / d;
+        if (r > c + 1) H[idx] = 0.0;
+    }
+}
+
 // ------------------------------------------------------------------ 2x2 solves
 // Complete-pivoting 2x2 solve with the dlaln2 small-pivot perturbation smin
 // (smin <= 0 disables the perturbation).
@@ -1331,8 +1889,10 @@ void launch_hqr(double* H, double* Z, double* wr, double* wi, int d, int batch,
                                              200 * 1024));
         attr = true;
     }
-    static const char* mode = std::getenv("VRTE_HQR");  // window (default) | band
-    if (!mode || std::string(mode) == "window") {
+    static const char* mode = std::getenv("VRTE_HQR");  // multi (default) | window | band
+    if (!mode || std::string(mode) == "multi") {
+        hqr_multi_kernel<<<batch, 256, 0, st>>>(H, Z, wr, wi, d, status);
+    } else if (std::string(mode) == "window") {
         hqr_window_kernel<<<batch, 256, 0, st>>>(H, Z, wr, wi, d, status);
     } else {
         hqr_kernel<<<batch, NT, smem, st>>>(H, Z, wr, wi, d, status);

@@ -8,7 +8,10 @@ for cfg in sys.argv[1:] or ["C3"]:
     p = V.Plan(mat, V.options(w.N), nodes, w.n_dphi, device=0)
     p.run(1)
     r = p.last
-    print(cfg, "sweeps", r.qr_sweeps, "steps", r.qr_steps, "t_hqr ms %.2f" % (r.t_hqr * 1e3),
-          "cycles/step/matrix-par %.0f" % (r.t_hqr * 1.9e9 / (r.qr_steps / (2 * w.material.order_count if cfg == "C3" else w.material.order_count))))
-    cyc = list(r.qr_cycles); tot = sum(cyc) or 1
-    print("   phase cycles per step: " + " ".join("%s=%.0f" % (n, c / r.qr_steps) for n, c in zip(("shift+Msearch", "winload", "chase", "writeback+update", "?", "deflation"), cyc)))
+    nmat = 2 * w.material.order_count if cfg in ("C3", "C5") else w.material.order_count
+    cyc = list(r.qr_cycles)
+    print(cfg, "sweeps", r.qr_sweeps, "reflectors", r.qr_steps, "t_hqr ms %.2f" % (r.t_hqr * 1e3),
+          "cycles/reflector/matrix %.0f" % (r.t_hqr * 1.9e9 / (r.qr_steps / nmat)))
+    st = max(r.qr_steps, 1)
+    print("   per reflector (thread-0 clock): defl+shift=%.0f winload=%.0f chase=%.0f update=%.0f" %
+          tuple(c / st for c in cyc[:4]), " multi sweeps %d (%.0f%% of reflectors)" % (cyc[4], 100.0 * cyc[5] / st))
