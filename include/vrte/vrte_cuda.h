@@ -68,7 +68,7 @@ typedef struct vrte_cuda_result {
     uint64_t kernel_launches;
     uint64_t qr_sweeps;     /* Francis sweeps / bulge-chase steps summed over matrices */
     uint64_t qr_steps;
-    uint64_t qr_cycles[6];  /* debug: QR phase cycles summed over matrices */
+    uint64_t qr_cycles[8];  /* debug: QR phase cycles / counters summed over matrices */
     double max_eigen_residual;
     double max_particular_residual;
     int32_t status;         /* 0 ok, 3 numerical, 5 argument */

@@ -110,7 +110,7 @@ class CudaResult(C.Structure):
         ("kernel_launches", C.c_uint64),
         ("qr_sweeps", C.c_uint64),
         ("qr_steps", C.c_uint64),
-        ("qr_cycles", C.c_uint64 * 6),
+        ("qr_cycles", C.c_uint64 * 8),
         ("max_eigen_residual", C.c_double),
         ("max_particular_residual", C.c_double),
         ("status", C.c_int32),

@@ -591,7 +591,7 @@ int finish(vrte_cuda_plan& pl, vrte_cuda_result* r) {
         r->polished = s.polished;
         r->qr_sweeps = s.qr_sweeps;
         r->qr_steps = s.qr_steps;
-        for (int q = 0; q < 6; ++q) r->qr_cycles[q] = s.qr_cycles[q];
+        for (int q = 0; q < 8; ++q) r->qr_cycles[q] = s.qr_cycles[q];
         r->max_eigen_residual = maxres;
         r->max_particular_residual = s.max_particular_residual;
         r->kernel_launches = pl.launches;

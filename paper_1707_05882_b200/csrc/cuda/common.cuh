@@ -38,7 +38,7 @@ struct DeviceStatus {
     double max_boundary_residual;
     unsigned long long qr_sweeps;
     unsigned long long qr_steps;
-    unsigned long long qr_cycles[6];  // debug phase timers (clock64 in thread 0)
+    unsigned long long qr_cycles[8];  // debug phase timers (clock64 in thread 0)
 };
 
 enum FailKind {

@@ -853,7 +853,10 @@ __global__ void __launch_bounds__(256) hqr_window_kernel(double* Hall, double* Z
 constexpr int MB_MAX = 4;   // bulges per sweep
 constexpr int MS = 16;      // chase steps per chunk
 constexpr int MW = 32;      // window (>= MS + 3 (MB_MAX - 1) + 4)
+constexpr int LDW = MW + 1; // leading dimension of the window: row sweeps (lanes over
+                            // columns) hit distinct shared-memory banks
 constexpr int TQ = 8;       // tiny-matrix leading dimension (2 MB_MAX)
+constexpr int AED_NW = 14;  // deflation window (<= MW); measured optimum for d = 256
 
 __device__ inline void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -1017,13 +1020,252 @@ __device__ void warp_tiny_eig(double* S, int n, double* sr, double* si) {
     }
 }
 
-__global__ void __launch_bounds__(256) hqr_multi_kernel(double* Hall, double* Zall, double* wrall,
-                                                        double* wiall, int d, DeviceStatus* status) {
-    __shared__ double Wn[MW * MW];  // window, column-major Wn[c*MW + r]
+
+// Real Schur form T = V S V^T of the n x n Hessenberg T (ld MW, n <= MW) by one
+// warp: double-shift QR with full updates (dlahqr, wantt = wantz = true); V
+// (ld MW) accumulates the transformations (callers pass V = I).  sr/si receive
+// the eigenvalues by diagonal position.  Returns false if it did not converge.
+__device__ bool warp_small_schur(double* T, double* V, int n, double* sr, double* si) {
+    const int lane = threadIdx.x & 31;
+    const double ulp = kUlp, smlnum = kSafeMin * ((double)n / ulp);
+    auto A = [&](int r, int c) -> double& { return T[r + c * LDW]; };
+    int I = n - 1;
+    int kdefl = 0;
+    while (I >= 0) {
+        int L = 0;
+        bool conv = false;
+        for (int its = 0; its <= 30 * max(10, n); ++its) {
+            // largest k in (L, I] with a negligible subdiagonal: lanes test in parallel
+            const int kk = L + 1 + lane;
+            const bool hit = kk <= I && small_subdiag_g(T, LDW, kk, ulp, smlnum);
+            const unsigned m = __ballot_sync(0xffffffffu, hit);
+            if (m) L = L + 1 + (31 - __clz(m));
+            __syncwarp();
+            if (L > 0 && lane == 0) A(L, L - 1) = 0.0;
+            __syncwarp();
+            if (L >= I - 1) {
+                conv = true;
+                break;
+            }
+            ++kdefl;
+            double h11, h12, h21, h22;
+            if (kdefl % 20 == 0) {
+                const double s = fabs(A(I, I - 1)) + fabs(A(I - 1, I >= 2 ? I - 2 : 0));
+                h11 = 0.75 * s + A(I, I);
+                h12 = -0.4375 * s;
+                h21 = s;
+                h22 = h11;
+            } else if (kdefl % 10 == 0) {
+                const double s = fabs(A(L + 1, L)) + fabs(A(L + 2, L + 1));
+                h11 = 0.75 * s + A(L, L);
+                h12 = -0.4375 * s;
+                h21 = s;
+                h22 = h11;
+            } else {
+                h11 = A(I - 1, I - 1);
+                h21 = A(I, I - 1);
+                h12 = A(I - 1, I);
+                h22 = A(I, I);
+            }
+            double rt1r, rt1i, rt2r, rt2i;
+            {
+                const double s = fabs(h11) + fabs(h12) + fabs(h21) + fabs(h22);
+                if (s == 0.0) {
+                    rt1r = rt1i = rt2r = rt2i = 0.0;
+                } else {
+                    h11 /= s;
+                    h21 /= s;
+                    h12 /= s;
+                    h22 /= s;
+                    const double tr = (h11 + h22) / 2.0;
+                    const double det = (h11 - tr) * (h22 - tr) - h12 * h21;
+                    const double rtdisc = sqrt(fabs(det));
+                    if (det >= 0.0) {
+                        rt1r = tr * s;
+                        rt2r = rt1r;
+                        rt1i = rtdisc * s;
+                        rt2i = -rt1i;
+                    } else {
+                        rt1r = tr + rtdisc;
+                        rt2r = tr - rtdisc;
+                        if (fabs(rt1r - h22) <= fabs(rt2r - h22)) {
+                            rt1r *= s;
+                            rt2r = rt1r;
+                        } else {
+                            rt2r *= s;
+                            rt1r = rt2r;
+                        }
+                        rt1i = rt2i = 0.0;
+                    }
+                }
+            }
+            const int M = L;
+            for (int k = M; k <= I - 1; ++k) {
+                const int nr = min(3, I - k + 1);
+                double v1, v2, v3;
+                if (k == M) {
+                    double v[3];
+                    start_vector_g(T, LDW, M, rt1r, rt1i, rt2r, rt2i, v);
+                    v1 = v[0];
+                    v2 = v[1];
+                    v3 = nr == 3 ? v[2] : 0.0;
+                } else {
+                    v1 = A(k, k - 1);
+                    v2 = A(k + 1, k - 1);
+                    v3 = nr == 3 ? A(k + 2, k - 1) : 0.0;
+                }
+                double t1 = 0.0;
+                const double x2 = fma(v2, v2, v3 * v3);
+                if (x2 != 0.0) {
+                    const double ss = fma(v1, v1, x2);
+                    const double rq = rsqrt(ss);
+                    const double nv = ss * rq;
+                    const double av1 = fabs(v1);
+                    const double sc = copysign(__drcp_rn(av1 + nv), v1);
+                    t1 = fma(av1, rq, 1.0);
+                    v2 *= sc;
+                    v3 *= sc;
+                    v1 = -copysign(nv, v1);
+                }
+                const double t2 = t1 * v2, t3 = t1 * v3;
+                __syncwarp();
+                const int c = k + lane;
+                if (c < n) {
+                    const double a0 = A(k, c), a1 = A(k + 1, c), a2 = nr == 3 ? A(k + 2, c) : 0.0;
+                    const double sum = a0 + v2 * a1 + v3 * a2;
+                    A(k, c) = a0 - sum * t1;
+                    A(k + 1, c) = a1 - sum * t2;
+                    if (nr == 3) A(k + 2, c) = a2 - sum * t3;
+                }
+                __syncwarp();
+                if (k > M && lane == 0) {
+                    A(k, k - 1) = v1;
+                    A(k + 1, k - 1) = 0.0;
+                    if (k < I - 1) A(k + 2, k - 1) = 0.0;
+                }
+                const int r = lane;
+                if (r <= min(k + 3, I)) {
+                    const double a0 = A(r, k), a1 = A(r, k + 1), a2 = nr == 3 ? A(r, k + 2) : 0.0;
+                    const double sum = a0 + v2 * a1 + v3 * a2;
+                    A(r, k) = a0 - sum * t1;
+                    A(r, k + 1) = a1 - sum * t2;
+                    if (nr == 3) A(r, k + 2) = a2 - sum * t3;
+                }
+                if (r < n) {
+                    double* vr = V + r;
+                    const double a0 = vr[k * MW], a1 = vr[(k + 1) * MW], a2 = nr == 3 ? vr[(k + 2) * MW] : 0.0;
+                    const double sum = a0 + v2 * a1 + v3 * a2;
+                    vr[k * MW] = a0 - sum * t1;
+                    vr[(k + 1) * MW] = a1 - sum * t2;
+                    if (nr == 3) vr[(k + 2) * MW] = a2 - sum * t3;
+                }
+                __syncwarp();
+            }
+        }
+        if (!conv) return false;
+        if (L == I) {
+            sr[I] = A(I, I);
+            si[I] = 0.0;
+        } else {
+            double a = A(I - 1, I - 1), bb = A(I - 1, I), c = A(I, I - 1), dd = A(I, I);
+            double r1r, r1i, r2r, r2i, cs, sn;
+            dlanv2(a, bb, c, dd, r1r, r1i, r2r, r2i, cs, sn);
+            __syncwarp();
+            if (lane == 0) {
+                A(I - 1, I - 1) = a;
+                A(I - 1, I) = bb;
+                A(I, I - 1) = c;
+                A(I, I) = dd;
+            }
+            sr[I - 1] = r1r;
+            si[I - 1] = r1i;
+            sr[I] = r2r;
+            si[I] = r2i;
+            const int j = I + 1 + lane;
+            if (j < n) {
+                const double xv = A(I - 1, j), yv = A(I, j);
+                A(I - 1, j) = cs * xv + sn * yv;
+                A(I, j) = cs * yv - sn * xv;
+            }
+            if (lane <= I - 2) {
+                const double xv = A(lane, I - 1), yv = A(lane, I);
+                A(lane, I - 1) = cs * xv + sn * yv;
+                A(lane, I) = cs * yv - sn * xv;
+            }
+            if (lane < n) {
+                double* vr = V + lane;
+                const double xv = vr[(I - 1) * MW], yv = vr[I * MW];
+                vr[(I - 1) * MW] = cs * xv + sn * yv;
+                vr[I * MW] = cs * yv - sn * xv;
+            }
+            __syncwarp();
+        }
+        kdefl = 0;
+        I = L - 1;
+        __syncwarp();
+    }
+    return true;
+}
+
+// Householder reflector applied by one warp: x <- (I - tau v v^T) x on rows
+// [r0, r0+len) of the columns [c0, c1) of A (ld MW) -- left -- or on columns
+// [r0, r0+len) of the rows [c0, c1) -- right.  v[0] = 1 implicitly stored.
+__device__ void warp_refl_left(double* A, int ld, const double* v, int len, double tau, int r0, int c0,
+                               int c1) {
+    const int lane = threadIdx.x & 31;
+    for (int c = c0 + lane; c < c1; c += 32) {
+        double w = 0.0;
+        for (int q = 0; q < len; ++q) w = fma(v[q], A[(r0 + q) + c * ld], w);
+        w *= tau;
+        for (int q = 0; q < len; ++q) A[(r0 + q) + c * ld] -= w * v[q];
+    }
+    __syncwarp();
+}
+__device__ void warp_refl_right(double* A, int ld, const double* v, int len, double tau, int r0, int c0,
+                                int c1) {
+    const int lane = threadIdx.x & 31;
+    for (int r = c0 + lane; r < c1; r += 32) {
+        double w = 0.0;
+        for (int q = 0; q < len; ++q) w = fma(A[r + (r0 + q) * ld], v[q], w);
+        w *= tau;
+        for (int q = 0; q < len; ++q) A[r + (r0 + q) * ld] -= w * v[q];
+    }
+    __syncwarp();
+}
+// dlarfg on (alpha, x[0..len-2]) in place in v[0..len-1]: on return v[0] = 1,
+// v[1..] the reflector tail; returns tau, *beta the new alpha.  Lane-redundant.
+__device__ double warp_dlarfg(double* v, int len, double* beta) {
+    const int lane = threadIdx.x & 31;
+    const double alpha = v[0];
+    double xn = 0.0;
+    for (int q = 1; q < len; ++q) xn = fma(v[q], v[q], xn);
+    __syncwarp();
+    if (xn == 0.0) {
+        *beta = alpha;
+        if (lane == 0) v[0] = 1.0;
+        __syncwarp();
+        return 0.0;
+    }
+    const double b = -copysign(sqrt(alpha * alpha + xn), alpha);
+    const double tau = (b - alpha) / b, sc = 1.0 / (alpha - b);
+    for (int q = 1 + lane; q < len; q += 32) v[q] *= sc;
+    __syncwarp();
+    if (lane == 0) v[0] = 1.0;
+    __syncwarp();
+    *beta = b;
+    return tau;
+}
+
+__global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double* Zall, double* wrall,
+                                                        double* wiall, int d, DeviceStatus* status,
+                                                        int aed_nw, int nb4_min, int nb2_min, int nibble) {
+    __shared__ double Wn[MW * LDW];  // window, column-major Wn[c*LDW + r]
     __shared__ double Us[MW * MW];  // accumulated factor, column-major
     __shared__ double Sm[TQ * TQ];  // trailing block for the shifts
     __shared__ double s_sr[TQ], s_si[TQ];
     __shared__ double s_pr[4 * MB_MAX];  // shift pair per bulge: rt1r rt1i rt2r rt2i
+    __shared__ double s_esr[MW], s_esi[MW], s_vec[MW];
+    __shared__ int s_aed[4];             // ok, ndefl, skip-sweep, bulges
     __shared__ int s_int;
     __shared__ int s_nb;
     __shared__ double s_t1;
@@ -1039,12 +1281,43 @@ __global__ void __launch_bounds__(256) hqr_multi_kernel(double* Hall, double* Za
     int kdefl = 0;
     int I = d - 1;
     unsigned long long nsweep = 0, nstep = 0;
-    unsigned long long cyc[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long cyc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long tc = clock64();
     auto tick = [&](int slot) {
         const long long now = clock64();
         cyc[slot] += (unsigned long long)(now - tc);
         tc = now;
+    };
+    // H(:, wlo:whi) <- H U above the window, H(wlo:whi, :) <- U^T H right of it,
+    // Z(:, wlo:whi) <- Z U  (U = Us, nw x nw zero padded to MW)
+    auto apply_u = [&](int wlo, int whi, int nw) {
+        const int n_right = d - 1 - whi, n_above = wlo;
+        for (int task = t; task < n_right + n_above + d; task += nt) {
+            double x[MW];
+            if (task < n_right) {  // column right of the window: U^T x
+                double* col = H + (size_t)(whi + 1 + task) * d + wlo;
+#pragma unroll
+                for (int q = 0; q < MW; ++q) x[q] = (q < nw) ? col[q] : 0.0;
+                for (int r = 0; r < nw; ++r) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int q = 0; q < MW; ++q) acc = fma(Us[r * MW + q], x[q], acc);
+                    col[r] = acc;
+                }
+            } else {  // row of H above the window, or of Z: x U
+                const bool isz = task >= n_right + n_above;
+                const int i = isz ? task - n_right - n_above : task - n_right;
+                double* base = (isz ? Z : H) + i + (size_t)wlo * d;
+#pragma unroll
+                for (int q = 0; q < MW; ++q) x[q] = (q < nw) ? base[(size_t)q * d] : 0.0;
+                for (int c = 0; c < nw; ++c) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int q = 0; q < MW; ++q) acc = fma(x[q], Us[c * MW + q], acc);
+                    base[(size_t)c * d] = acc;
+                }
+            }
+        }
     };
     while (I >= 0) {
         int L = 0;
@@ -1062,7 +1335,7 @@ __global__ void __launch_bounds__(256) hqr_multi_kernel(double* Hall, double* Za
             }
             ++kdefl;
             const int nsize = I - L + 1;
-            int nb = nsize >= 48 ? 4 : (nsize >= 24 ? 2 : 1);
+            int nb = nsize >= nb4_min ? 4 : (nsize >= nb2_min ? 2 : 1);
             if (kdefl % kexsh == 0) nb = 1;
             int M = L;
             double v0[3] = {0.0, 0.0, 0.0};
@@ -1130,68 +1403,188 @@ __global__ void __launch_bounds__(256) hqr_multi_kernel(double* Hall, double* Za
                 M = block_max_int(mb, &s_int);
                 start_vector_g(H, d, M, rt1r, rt1i, rt2r, rt2i, v0);
             } else {
-                // 2 nb shifts: eigenvalues of the trailing 2nb x 2nb block
-                const int n2 = 2 * nb, o = I - n2 + 1;
+                // ---- aggressive early deflation (dlaqr3 without reordering: the
+                // contiguous bottom run of deflatable blocks) on the trailing
+                // nwin x nwin window; its undeflated eigenvalues are the shifts.
+                const int nwin = min(aed_nw, nsize / 2);
+                const int kwtop = I - nwin + 1;
+                const double sspike = hg(H, d, kwtop, kwtop - 1);
+                const long long t_aed = clock64();
                 if (warp == 0) {
-                    for (int e = lane; e < TQ * TQ; e += 32) {
-                        const int r = e % TQ, c = e / TQ;
-                        Sm[e] = (r < n2 && c < n2 && r <= c + 1) ? hg(H, d, o + r, o + c) : 0.0;
+                    for (int e = lane; e < MW * MW; e += 32) {
+                        const int r = e % MW, c = e / MW;
+                        Wn[r + c * LDW] = (r < nwin && c < nwin && r <= c + 1) ? hg(H, d, kwtop + r, kwtop + c) : 0.0;
+                        Us[e] = (r == c) ? 1.0 : 0.0;
                     }
                     __syncwarp();
-                    warp_tiny_eig(Sm, n2, s_sr, s_si);
+                    const bool ok = warp_small_schur(Wn, Us, nwin, s_esr, s_esi);
                     __syncwarp();
-                    if (lane == 0) {
-                        // sort by decreasing modulus (conjugate pairs stay adjacent), then
-                        // pair: complex pairs as they are, real shifts two at a time
-                        double ar[TQ], ai[TQ];
-                        for (int q = 0; q < n2; ++q) {
-                            ar[q] = s_sr[q];
-                            ai[q] = s_si[q];
+                    int ndefl = 0;
+                    if (ok) {
+                        int j = nwin - 1;
+                        while (j >= 0) {
+                            if (j > 0 && Wn[j + (j - 1) * LDW] != 0.0) {
+                                double foo = fabs(Wn[j + j * LDW]) + sqrt(fabs(Wn[j + (j - 1) * LDW])) *
+                                                                       sqrt(fabs(Wn[(j - 1) + j * LDW]));
+                                if (foo == 0.0) foo = fabs(sspike);
+                                const double sp = fmax(fabs(sspike * Us[j * MW]), fabs(sspike * Us[(j - 1) * MW]));
+                                if (sp <= fmax(smlnum, ulp * foo)) {
+                                    ndefl += 2;
+                                    j -= 2;
+                                } else {
+                                    break;
+                                }
+                            } else {
+                                double foo = fabs(Wn[j + j * LDW]);
+                                if (foo == 0.0) foo = fabs(sspike);
+                                if (fabs(sspike * Us[j * MW]) <= fmax(smlnum, ulp * foo)) {
+                                    ndefl += 1;
+                                    j -= 1;
+                                } else {
+                                    break;
+                                }
+                            }
                         }
-                        int nbul = 0;
+                    }
+                    const int nd = nwin - ndefl;
+                    if (ok && ndefl > 0 && nd > 1) {
+                        // collapse the spike of the undeflated part onto its first row
+                        for (int q = lane; q < nd; q += 32) s_vec[q] = Us[q * MW];
+                        __syncwarp();
+                        double beta;
+                        double tau = warp_dlarfg(s_vec, nd, &beta);
+                        if (tau != 0.0) {
+                            warp_refl_left(Wn, LDW, s_vec, nd, tau, 0, 0, nwin);
+                            warp_refl_right(Wn, LDW, s_vec, nd, tau, 0, 0, nd);
+                            warp_refl_right(Us, MW, s_vec, nd, tau, 0, 0, nwin);
+                        }
+                        // back to Hessenberg form (dgehrd on the leading nd x nd block)
+                        for (int j = 0; j + 2 < nd; ++j) {
+                            const int len = nd - j - 1;
+                            for (int q = lane; q < len; q += 32) s_vec[q] = Wn[(j + 1 + q) + j * LDW];
+                            __syncwarp();
+                            tau = warp_dlarfg(s_vec, len, &beta);
+                            if (tau != 0.0) {
+                                warp_refl_left(Wn, LDW, s_vec, len, tau, j + 1, j + 1, nwin);
+                                warp_refl_right(Wn, LDW, s_vec, len, tau, j + 1, 0, nd);
+                                warp_refl_right(Us, MW, s_vec, len, tau, j + 1, 0, nwin);
+                            }
+                            for (int q = lane; q < len; q += 32) Wn[(j + 1 + q) + j * LDW] = (q == 0) ? beta : 0.0;
+                            __syncwarp();
+                        }
+                    }
+                    if (lane == 0) {
+                        s_aed[0] = ok ? 1 : 0;
+                        s_aed[1] = ndefl;
+                        // nibble: many deflations -> deflate them and redo AED before sweeping
+                        s_aed[2] = (ok && (nd < 2 || 100 * ndefl > nibble * nwin)) ? 1 : 0;
+                        // shifts: bottom-most undeflated eigenvalues, conjugate pairs kept together
+                        int nbul = 0, q = nd - 1;
                         double rbuf = 0.0;
                         bool have = false;
-                        for (int q = 0; q < n2; ++q) {
-                            if (ai[q] != 0.0 && q + 1 < n2) {
-                                s_pr[4 * nbul + 0] = ar[q];
-                                s_pr[4 * nbul + 1] = fabs(ai[q]);
-                                s_pr[4 * nbul + 2] = ar[q + 1];
-                                s_pr[4 * nbul + 3] = -fabs(ai[q]);
+                        while (ok && q >= 0 && nbul < nb) {
+                            if (s_esi[q] != 0.0 && q >= 1) {
+                                s_pr[4 * nbul + 0] = s_esr[q];
+                                s_pr[4 * nbul + 1] = fabs(s_esi[q]);
+                                s_pr[4 * nbul + 2] = s_esr[q - 1];
+                                s_pr[4 * nbul + 3] = -fabs(s_esi[q]);
                                 ++nbul;
-                                ++q;
+                                q -= 2;
                             } else if (have) {
                                 s_pr[4 * nbul + 0] = rbuf;
                                 s_pr[4 * nbul + 1] = 0.0;
-                                s_pr[4 * nbul + 2] = ar[q];
+                                s_pr[4 * nbul + 2] = s_esr[q];
                                 s_pr[4 * nbul + 3] = 0.0;
                                 ++nbul;
                                 have = false;
+                                q -= 1;
                             } else {
-                                rbuf = ar[q];
+                                rbuf = s_esr[q];
                                 have = true;
+                                q -= 1;
                             }
                         }
-                        if (have) {  // odd real count cannot happen with paired complex shifts
-                            s_pr[4 * nbul + 0] = rbuf;
-                            s_pr[4 * nbul + 1] = 0.0;
-                            s_pr[4 * nbul + 2] = rbuf;
-                            s_pr[4 * nbul + 3] = 0.0;
-                            ++nbul;
-                        }
-                        s_nb = max(1, min(nbul, nb));
+                        s_aed[3] = nbul;
                     }
                 }
                 __syncthreads();
-                nb = s_nb;
+                cyc[6] += (unsigned long long)(clock64() - t_aed);
+                cyc[7] += 1;
+                if (s_aed[0] && s_aed[1] > 0) {
+                    for (int idx = t; idx < nwin * nwin; idx += nt) {
+                        const int r = idx % nwin, c = idx / nwin;
+                        H[(kwtop + r) + (size_t)(kwtop + c) * d] = (r <= c + 1) ? Wn[c * LDW + r] : 0.0;
+                    }
+                    if (t == 0) H[kwtop + (size_t)(kwtop - 1) * d] = sspike * Us[0];
+                    apply_u(kwtop, I, nwin);
+                    __syncthreads();
+                    cyc[4] += (unsigned long long)s_aed[1];  // AED deflations
+                }
+                if (s_aed[0] && (s_aed[2] || s_aed[3] == 0)) continue;  // deflate first, then AED again
+                if (s_aed[0]) {
+                    nb = s_aed[3];
+                    M = L;
+                } else {
+                    // fallback: 2 nb shifts from the trailing 2nb x 2nb block
+                    const int n2 = 2 * nb, o = I - n2 + 1;
+                    if (warp == 0) {
+                        for (int e = lane; e < TQ * TQ; e += 32) {
+                            const int r = e % TQ, c = e / TQ;
+                            Sm[e] = (r < n2 && c < n2 && r <= c + 1) ? hg(H, d, o + r, o + c) : 0.0;
+                        }
+                        __syncwarp();
+                        warp_tiny_eig(Sm, n2, s_sr, s_si);
+                        __syncwarp();
+                        if (lane == 0) {
+                            // sort by decreasing modulus (conjugate pairs stay adjacent), then
+                            // pair: complex pairs as they are, real shifts two at a time
+                            double ar[TQ], ai[TQ];
+                            for (int q = 0; q < n2; ++q) {
+                                ar[q] = s_sr[q];
+                                ai[q] = s_si[q];
+                            }
+                            int nbul = 0;
+                            double rbuf = 0.0;
+                            bool have = false;
+                            for (int q = 0; q < n2; ++q) {
+                                if (ai[q] != 0.0 && q + 1 < n2) {
+                                    s_pr[4 * nbul + 0] = ar[q];
+                                    s_pr[4 * nbul + 1] = fabs(ai[q]);
+                                    s_pr[4 * nbul + 2] = ar[q + 1];
+                                    s_pr[4 * nbul + 3] = -fabs(ai[q]);
+                                    ++nbul;
+                                    ++q;
+                                } else if (have) {
+                                    s_pr[4 * nbul + 0] = rbuf;
+                                    s_pr[4 * nbul + 1] = 0.0;
+                                    s_pr[4 * nbul + 2] = ar[q];
+                                    s_pr[4 * nbul + 3] = 0.0;
+                                    ++nbul;
+                                    have = false;
+                                } else {
+                                    rbuf = ar[q];
+                                    have = true;
+                                }
+                            }
+                            if (have) {  // odd real count cannot happen with paired complex shifts
+                                s_pr[4 * nbul + 0] = rbuf;
+                                s_pr[4 * nbul + 1] = 0.0;
+                                s_pr[4 * nbul + 2] = rbuf;
+                                s_pr[4 * nbul + 3] = 0.0;
+                                ++nbul;
+                            }
+                            s_nb = max(1, min(nbul, nb));
+                        }
+                    }
+                    __syncthreads();
+                    nb = s_nb;
+                }
             }
             if (t == 0) s_t1 = 0.0;
             ++nsweep;
             const int S_total = (I - M) + 3 * (nb - 1);
             nstep += (unsigned long long)(I - M) * nb;
-            if (nb > 1) {
-                cyc[4] += 1;
-                cyc[5] += (unsigned long long)(I - M) * nb;
-            }
+            if (nb > 1) cyc[5] += (unsigned long long)(I - M) * nb;
             tick(0);
             for (int s0 = 0; s0 < S_total; s0 += MS) {
                 const int s1 = min(s0 + MS, S_total);
@@ -1202,13 +1595,13 @@ __global__ void __launch_bounds__(256) hqr_multi_kernel(double* Hall, double* Za
                 const int nw = whi - wlo + 1;
                 for (int idx = t; idx < MW * MW; idx += nt) {
                     const int r = idx % MW, c = idx / MW;
-                    Wn[idx] = (r < nw && c < nw) ? H[(wlo + r) + (size_t)(wlo + c) * d] : 0.0;
+                    Wn[r + c * LDW] = (r < nw && c < nw) ? H[(wlo + r) + (size_t)(wlo + c) * d] : 0.0;
                     Us[idx] = (r == c) ? 1.0 : 0.0;
                 }
                 __syncthreads();
                 tick(1);
                 if (warp < nb) {
-                    auto W = [&](int r, int c) -> double& { return Wn[(c - wlo) * MW + (r - wlo)]; };
+                    auto W = [&](int r, int c) -> double& { return Wn[(c - wlo) * LDW + (r - wlo)]; };
                     const int bb = warp;
                     for (int s = s0; s < s1; ++s) {
                         const int k = M + s - 3 * bb;
@@ -1227,7 +1620,7 @@ __global__ void __launch_bounds__(256) hqr_multi_kernel(double* Hall, double* Za
                                 v3 = (nr == 3) ? v0[2] : 0.0;
                             } else {
                                 double vv[3];
-                                start_vector_g(Wn, MW, M - wlo, s_pr[4 * bb], s_pr[4 * bb + 1],
+                                start_vector_g(Wn, LDW, M - wlo, s_pr[4 * bb], s_pr[4 * bb + 1],
                                                s_pr[4 * bb + 2], s_pr[4 * bb + 3], vv);
                                 v1 = vv[0];
                                 v2 = vv[1];
@@ -1299,37 +1692,10 @@ __global__ void __launch_bounds__(256) hqr_multi_kernel(double* Hall, double* Za
                 tick(2);
                 for (int idx = t; idx < nw * nw; idx += nt) {
                     const int r = idx % nw, c = idx / nw;
-                    H[(wlo + r) + (size_t)(wlo + c) * d] = Wn[c * MW + r];
+                    H[(wlo + r) + (size_t)(wlo + c) * d] = Wn[c * LDW + r];
                 }
                 if (s0 == 0 && nb == 1 && M > L && t == 0) H[M + (size_t)(M - 1) * d] *= (1.0 - s_t1);
-                // off-window updates with U (nw x nw, zero padded to MW)
-                const int n_right = d - 1 - whi, n_above = wlo;
-                for (int task = t; task < n_right + n_above + d; task += nt) {
-                    double x[MW];
-                    if (task < n_right) {  // column right of the window: U^T x
-                        double* col = H + (size_t)(whi + 1 + task) * d + wlo;
-#pragma unroll
-                        for (int q = 0; q < MW; ++q) x[q] = (q < nw) ? col[q] : 0.0;
-                        for (int r = 0; r < nw; ++r) {
-                            double acc = 0.0;
-#pragma unroll
-                            for (int q = 0; q < MW; ++q) acc = fma(Us[r * MW + q], x[q], acc);
-                            col[r] = acc;
-                        }
-                    } else {  // row of H above the window, or of Z: x U
-                        const bool isz = task >= n_right + n_above;
-                        const int i = isz ? task - n_right - n_above : task - n_right;
-                        double* base = (isz ? Z : H) + i + (size_t)wlo * d;
-#pragma unroll
-                        for (int q = 0; q < MW; ++q) x[q] = (q < nw) ? base[(size_t)q * d] : 0.0;
-                        for (int c = 0; c < nw; ++c) {
-                            double acc = 0.0;
-#pragma unroll
-                            for (int q = 0; q < MW; ++q) acc = fma(x[q], Us[c * MW + q], acc);
-                            base[(size_t)c * d] = acc;
-                        }
-                    }
-                }
+                apply_u(wlo, whi, nw);
                 __syncthreads();
                 tick(3);
             }
@@ -1385,7 +1751,7 @@ __global__ void __launch_bounds__(256) hqr_multi_kernel(double* Hall, double* Za
     if (t == 0) {
         atomicAdd(&status->qr_sweeps, nsweep);
         atomicAdd(&status->qr_steps, nstep);
-        for (int q = 0; q < 6; ++q) atomicAdd(&status->qr_cycles[q], cyc[q]);
+        for (int q = 0; q < 8; ++q) atomicAdd(&status->qr_cycles[q], cyc[q]);
     }
     for (int idx = t; idx < d * d; idx += nt) {
         const int r = idx % d, c = idx / d;
@@ -1891,7 +2257,12 @@ void launch_hqr(double* H, double* Z, double* wr, double* wi, int d, int batch,
     }
     static const char* mode = std::getenv("VRTE_HQR");  // multi (default) | window | band
     if (!mode || std::string(mode) == "multi") {
-        hqr_multi_kernel<<<batch, 256, 0, st>>>(H, Z, wr, wi, d, status);
+        static const int aed_nw = std::getenv("VRTE_AED_NW") ? std::atoi(std::getenv("VRTE_AED_NW")) : AED_NW;
+        static const int nb4 = std::getenv("VRTE_NB4_MIN") ? std::atoi(std::getenv("VRTE_NB4_MIN")) : 48;
+        static const int nb2 = std::getenv("VRTE_NB2_MIN") ? std::atoi(std::getenv("VRTE_NB2_MIN")) : 24;
+        static const int nibble = std::getenv("VRTE_NIBBLE") ? std::atoi(std::getenv("VRTE_NIBBLE")) : 40;
+        hqr_multi_kernel<<<batch, 256, 0, st>>>(H, Z, wr, wi, d, status, min(max(aed_nw, 4), MW), nb4, nb2,
+                                                nibble);
     } else if (std::string(mode) == "window") {
         hqr_window_kernel<<<batch, 256, 0, st>>>(H, Z, wr, wi, d, status);
     } else {

@@ -14,4 +14,5 @@ for cfg in sys.argv[1:] or ["C3"]:
           "cycles/reflector/matrix %.0f" % (r.t_hqr * 1.9e9 / (r.qr_steps / nmat)))
     st = max(r.qr_steps, 1)
     print("   per reflector (thread-0 clock): defl+shift=%.0f winload=%.0f chase=%.0f update=%.0f" %
-          tuple(c / st for c in cyc[:4]), " multi sweeps %d (%.0f%% of reflectors)" % (cyc[4], 100.0 * cyc[5] / st))
+          tuple(c / st for c in cyc[:4]), " AED deflations %d, %.0f%% of reflectors in multi-bulge sweeps" % (cyc[4], 100.0 * cyc[5] / st))
+    print("   AED calls %d, %.0f cycles per call (warp-0 Schur of the window)" % (cyc[7], cyc[6] / max(cyc[7], 1)))
