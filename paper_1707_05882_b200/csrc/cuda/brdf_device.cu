@@ -38,6 +38,8 @@ namespace vrte {
 
 namespace {
 
+constexpr double kRefineTarget = 1e-11;  // per-mode 8N residual after refinement
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
@@ -118,10 +120,14 @@ struct vrte_cuda_plan {
     DeviceStatus* status = nullptr;  // pinned host-mapped would be nicer; device + copy
     DevBuf<DeviceStatus> status_buf;
     cudaEvent_t ev[16] = {};
-    int refine_iters = 2;
-    int part_refine_iters = 2;
+    int refine_iters = 1;
+    int refine_extra = 2;
+    int part_refine_iters = 1;
+    DevBuf<double> resmax;
+    double* resmax_host = nullptr;
     uint64_t launches = 0;
     ~vrte_cuda_plan() {
+        if (resmax_host) cudaFreeHost(resmax_host);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (st) cudaStreamDestroy(st);
@@ -156,6 +162,9 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
         if (!e) VRTE_CUDA_CHECK(cudaEventCreate(&e));
     if (const char* ri = std::getenv("VRTE_REFINE_ITERS")) pl.refine_iters = std::atoi(ri);
     if (const char* pi = std::getenv("VRTE_PART_REFINE_ITERS")) pl.part_refine_iters = std::atoi(pi);
+    if (const char* re = std::getenv("VRTE_REFINE_EXTRA")) pl.refine_extra = std::atoi(re);
+    if (!pl.resmax_host) VRTE_CUDA_CHECK(cudaMallocHost(&pl.resmax_host, sizeof(double)));
+    pl.resmax.alloc(1);
     pl.N = p->N;
     pl.L = p->L;
     pl.Lc = p->L_coeffs > 0 ? p->L_coeffs : p->L;
@@ -394,7 +403,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[9], st));
     launch_nu_rho(rf, true, st);
     launch_refine_shift(rf, st);
-    for (int it = 0; it < pl.refine_iters; ++it) {
+    auto refine_iteration = [&]() {
         launch_refine_normalize(rf, st);
         residual_gemms();
         launch_refine_setup(rf, st);
@@ -404,13 +413,29 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
         gemm_batched(gemm(d, 2 * d, d, pl.E.p, d, dd, false, pl.UT.p, d, d2, false, pl.EU.p, d, d2, B), st);
         launch_refine_update(rf, st);
         nl += 11;
+    };
+    auto final_residual = [&]() {
+        launch_nu_rho(rf, false, st);
+        launch_refine_normalize(rf, st);
+        residual_gemms();
+        launch_residual(ra, st);
+        nl += 6;
+    };
+    for (int it = 0; it < pl.refine_iters; ++it) refine_iteration();
+    final_residual();
+    // Adaptive: one Newton step normally brings every mode below 1e-11 (the
+    // eigenbasis correction is accurate to ~eps |FE| / gap); otherwise refine
+    // again (at most refine_extra times) before the 1e-9 gate in finish().
+    for (int extra = 0; extra < pl.refine_extra; ++extra) {
+        launch_max_abs(pl.residual.p, (long long)B * d, 1, pl.resmax.p, st);
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(pl.resmax_host, pl.resmax.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+        VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
+        nl += 1;
+        if (*pl.resmax_host <= kRefineTarget) break;
+        refine_iteration();
+        final_residual();
     }
-    launch_nu_rho(rf, false, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[10], st));
-    launch_refine_normalize(rf, st);
-    residual_gemms();
-    launch_residual(ra, st);
-    nl += 6;
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[1], st));
     // ---------------- particular
     launch_beam_source(pd, pl.gsf_n.p, pl.gsf_b.p, pl.sp.p, pl.sm.p, st);
