@@ -158,5 +158,6 @@ struct GemmBatch {
     bool trans_a, trans_b;
 };
 void gemm_batched(const GemmBatch& g, cudaStream_t stream);
+void gemm_batched_cfg(const GemmBatch& g, cudaStream_t stream, int bk, int stages, int minb);
 
 }  // namespace vrte

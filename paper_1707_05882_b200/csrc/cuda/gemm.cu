@@ -10,22 +10,26 @@
 // per-lane fragment loads are bank-conflict free:
 //   A not transposed: As[k][m] (ld 72)     A transposed: As[m][k] (ld 20)
 //   B not transposed: Bs[n][k] (ld 20)     B transposed: Bs[k][n] (ld 136)
-// The epilogue stages the C tile through shared memory so global stores are
-// coalesced down the columns of the column-major output.
+// The epilogue stores the accumulator fragments directly; for the beta = 1
+// trailing updates C is preloaded into the accumulators (overlapping the first
+// operand tile) instead of being re-read in the epilogue.
 #include "common.cuh"
 
 namespace vrte {
 namespace {
 
-constexpr int BM = 64, BN = 128, BK = 16, NT = 256;
-constexpr int LDA_K = BM + 8;   // k-major A: As[k * LDA_K + m]
-constexpr int LDA_M = BK + 4;   // m-major A: As[m * LDA_M + k]
-constexpr int LDB_N = BK + 4;   // n-major B: Bs[n * LDB_N + k]
-constexpr int LDB_K = BN + 8;   // k-major B: Bs[k * LDB_K + n]
-constexpr int A_STAGE = (BK * LDA_K > BM * LDA_M) ? BK * LDA_K : BM * LDA_M;   // doubles
-constexpr int B_STAGE = (BN * LDB_N > BK * LDB_K) ? BN * LDB_N : BK * LDB_K;
-constexpr int LDC_S = BN + 1;   // epilogue staging Cs[m * LDC_S + n] (aliases the operand buffers)
-constexpr int SMEM_DOUBLES = (2 * (A_STAGE + B_STAGE) > BM * LDC_S) ? 2 * (A_STAGE + B_STAGE) : BM * LDC_S;
+constexpr int BM = 64, BN = 128, NT = 256;
+
+// shared-memory geometry of one pipeline stage for k-tile depth BK
+template <int BK>
+struct Geo {
+    static constexpr int LDA_K = BM + 8;   // k-major A: As[k * LDA_K + m]
+    static constexpr int LDA_M = BK + 4;   // m-major A: As[m * LDA_M + k]
+    static constexpr int LDB_N = BK + 4;   // n-major B: Bs[n * LDB_N + k]
+    static constexpr int LDB_K = BN + 8;   // k-major B: Bs[k * LDB_K + n]
+    static constexpr int A_STAGE = (BK * LDA_K > BM * LDA_M) ? BK * LDA_K : BM * LDA_M;  // doubles
+    static constexpr int B_STAGE = (BN * LDB_N > BK * LDB_K) ? BN * LDB_N : BK * LDB_K;
+};
 
 __device__ inline void cp_async8(double* smem, const double* gmem, bool valid) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -34,6 +38,8 @@ __device__ inline void cp_async8(double* smem, const double* gmem, bool valid) {
 }
 __device__ inline void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ inline void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+template <int N>
+__device__ inline void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 __device__ inline void dmma(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -41,11 +47,14 @@ __device__ inline void dmma(double& c0, double& c1, double a, double b) {
                  : "d"(a), "d"(b));
 }
 
-template <bool TA, bool TB>
-__global__ void __launch_bounds__(NT) dmma_gemm_kernel(GemmBatch g) {
+template <bool TA, bool TB, int BK, int ST, int MINB>
+__global__ void __launch_bounds__(NT, MINB) dmma_gemm_kernel(GemmBatch g) {
+    using Gm = Geo<BK>;
+    constexpr int LDA_K = Gm::LDA_K, LDA_M = Gm::LDA_M, LDB_N = Gm::LDB_N, LDB_K = Gm::LDB_K;
+    constexpr int A_STAGE = Gm::A_STAGE, B_STAGE = Gm::B_STAGE;
     extern __shared__ double smem[];
     double* As0 = smem;
-    double* Bs0 = smem + 2 * A_STAGE;
+    double* Bs0 = smem + ST * A_STAGE;
     const int bz = blockIdx.z;
     const double* A = g.a + bz * g.stride_a;
     const double* B = g.b + bz * g.stride_b;
@@ -94,19 +103,46 @@ __global__ void __launch_bounds__(NT) dmma_gemm_kernel(GemmBatch g) {
     };
 
     double acc[4][4][2];
+    const int nk = (g.k + BK - 1) / BK;
+    // prologue: ST-1 stages in flight (empty commit groups keep the count uniform)
+#pragma unroll
+    for (int s = 0; s < ST - 1; ++s) {
+        if (s < nk)
+            load_stage(s, s * BK);
+        else
+            cp_async_commit();
+    }
+    // beta = 1, alpha = +-1 (the trailing updates of LU / Hessenberg / refinement):
+    // C is read into the accumulators while the first operand tile is in flight
+    // (acc = alpha C, result = alpha acc), so no epilogue read round trip.
+    const bool preload = g.beta == 1.0 && (g.alpha == 1.0 || g.alpha == -1.0);
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < 4; ++j) {
+            acc[i][j][0] = acc[i][j][1] = 0.0;
+            if (preload) {
+                const int gm = m0 + wm + 8 * i + gq, gn = n0 + wn + 8 * j + 2 * tq;
+                if (gm < g.m) {
+                    const double* p = C + gm + (long long)gn * g.ldc;
+                    if (gn < g.n) acc[i][j][0] = g.alpha * p[0];
+                    if (gn + 1 < g.n) acc[i][j][1] = g.alpha * p[g.ldc];
+                }
+            }
+        }
 
-    const int nk = (g.k + BK - 1) / BK;
-    if (nk > 0) load_stage(0, 0);
     for (int kt = 0; kt < nk; ++kt) {
-        cp_async_wait_all();
+        cp_async_wait<ST - 2>();
         __syncthreads();
-        if (kt + 1 < nk) load_stage((kt + 1) & 1, (kt + 1) * BK);
-        const double* As = As0 + (kt & 1) * A_STAGE;
-        const double* Bs = Bs0 + (kt & 1) * B_STAGE;
+        {
+            const int nx = kt + ST - 1;
+            if (nx < nk)
+                load_stage(nx % ST, nx * BK);
+            else
+                cp_async_commit();
+        }
+        const double* As = As0 + (kt % ST) * A_STAGE;
+        const double* Bs = Bs0 + (kt % ST) * B_STAGE;
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
             double af[4], bf[4];
@@ -126,56 +162,73 @@ __global__ void __launch_bounds__(NT) dmma_gemm_kernel(GemmBatch g) {
                 for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
     }
-    // epilogue: stage through shared memory, then coalesced column stores
-    cp_async_wait_all();
-    __syncthreads();
-    double* Cs = smem;
+    // epilogue: fragments straight to global (each warp store covers 4 x 64-byte
+    // column segments of the column-major C)
+    const bool beta0 = g.beta == 0.0;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const int m = wm + 8 * i + gq, n = wn + 8 * j + 2 * tq;
-            Cs[m * LDC_S + n] = acc[i][j][0];
-            Cs[m * LDC_S + n + 1] = acc[i][j][1];
+            const int gm = m0 + wm + 8 * i + gq, gn = n0 + wn + 8 * j + 2 * tq;
+            if (gm >= g.m) continue;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (gn + h >= g.n) continue;
+                double* p = C + gm + (long long)(gn + h) * g.ldc;
+                const double v = g.alpha * acc[i][j][h];
+                *p = preload ? v : (beta0 ? v : fma(g.beta, *p, v));
+            }
         }
-    __syncthreads();
-    for (int e = t; e < BM * BN; e += NT) {
-        const int m = e % BM, n = e / BM;
-        const int gm = m0 + m, gn = n0 + n;
-        if (gm < g.m && gn < g.n) {
-            double* p = C + gm + (long long)gn * g.ldc;
-            const double v = g.alpha * Cs[m * LDC_S + n];
-            *p = (g.beta == 0.0) ? v : fma(g.beta, *p, v);
-        }
-    }
 }
 
-template <bool TA, bool TB>
+template <bool TA, bool TB, int BK, int ST, int MINB>
 void launch(const GemmBatch& g, cudaStream_t stream) {
     static bool attr = false;
-    const size_t smem = SMEM_DOUBLES * sizeof(double);
+    constexpr size_t smem = (size_t)ST * (Geo<BK>::A_STAGE + Geo<BK>::B_STAGE) * sizeof(double);
     if (!attr) {
-        VRTE_CUDA_CHECK(cudaFuncSetAttribute(dmma_gemm_kernel<TA, TB>,
+        VRTE_CUDA_CHECK(cudaFuncSetAttribute(dmma_gemm_kernel<TA, TB, BK, ST, MINB>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        VRTE_CUDA_CHECK(cudaFuncSetAttribute(dmma_gemm_kernel<TA, TB, BK, ST, MINB>,
+                                             cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         attr = true;
     }
     dim3 grid((g.m + BM - 1) / BM, (g.n + BN - 1) / BN, g.batch);
-    dmma_gemm_kernel<TA, TB><<<grid, NT, smem, stream>>>(g);
+    dmma_gemm_kernel<TA, TB, BK, ST, MINB><<<grid, NT, smem, stream>>>(g);
+}
+
+template <int BK, int ST, int MINB>
+void launch_cfg(const GemmBatch& g, cudaStream_t stream) {
+    if (!g.trans_a && !g.trans_b)
+        launch<false, false, BK, ST, MINB>(g, stream);
+    else if (g.trans_a && !g.trans_b)
+        launch<true, false, BK, ST, MINB>(g, stream);
+    else if (!g.trans_a && g.trans_b)
+        launch<false, true, BK, ST, MINB>(g, stream);
+    else
+        launch<true, true, BK, ST, MINB>(g, stream);
 }
 
 }  // namespace
 
-void gemm_batched(const GemmBatch& g, cudaStream_t stream) {
+// Explicit pipeline configuration (k-tile depth, stages, CTAs per SM) --
+// benchmarking hook; gemm_batched picks the measured best per shape class.
+void gemm_batched_cfg(const GemmBatch& g, cudaStream_t stream, int bk, int stages, int minb) {
     if (g.m <= 0 || g.n <= 0 || g.batch <= 0) return;
-    if (!g.trans_a && !g.trans_b)
-        launch<false, false>(g, stream);
-    else if (g.trans_a && !g.trans_b)
-        launch<true, false>(g, stream);
-    else if (!g.trans_a && g.trans_b)
-        launch<false, true>(g, stream);
-    else
-        launch<true, true>(g, stream);
+    if (bk == 16 && stages == 2 && minb == 3) launch_cfg<16, 2, 3>(g, stream);
+    else if (bk == 16 && stages == 3) launch_cfg<16, 3, 2>(g, stream);
+    else if (bk == 8 && stages == 4) launch_cfg<8, 4, 3>(g, stream);
+    else launch_cfg<16, 2, 2>(g, stream);
     VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+// Short contractions (k <= 96: LU / solve / Hessenberg trailing updates) are
+// bound by per-CTA prologue/epilogue latency -> 3 CTAs per SM; long ones keep
+// the register budget for a 3-stage pipeline (measured, profiles/r01_gemm_*).
+void gemm_batched(const GemmBatch& g, cudaStream_t stream) {
+    if (g.k <= 96)
+        gemm_batched_cfg(g, stream, 16, 2, 3);
+    else
+        gemm_batched_cfg(g, stream, 16, 3, 2);
 }
 
 }  // namespace vrte

@@ -15,6 +15,7 @@ namespace vrte {
 }
 }  // namespace vrte
 
+static int g_bk = 0, g_st = 0, g_mb = 2;
 static double run(int m, int n, int k, int batch, bool ta, bool tb, double beta, bool timeit) {
     const long long lda = ta ? k : m, ldb = tb ? n : k, ldc = m;
     const long long sa = lda * (ta ? m : k), sb = ldb * (tb ? k : n), sc = ldc * n;
@@ -36,7 +37,7 @@ static double run(int m, int n, int k, int batch, bool ta, bool tb, double beta,
     g.m = m; g.n = n; g.k = k; g.a = a; g.lda = lda; g.stride_a = sa; g.b = b; g.ldb = ldb; g.stride_b = sb;
     g.c = c; g.ldc = ldc; g.stride_c = sc; g.batch = batch; g.alpha = 1.25; g.beta = beta;
     g.trans_a = ta; g.trans_b = tb;
-    vrte::gemm_batched(g, 0);
+    (g_bk ? vrte::gemm_batched_cfg(g, 0, g_bk, g_st, g_mb) : vrte::gemm_batched(g, 0));
     cublasHandle_t h;
     cublasCreate(&h);
     const double alpha = 1.25;
@@ -57,9 +58,9 @@ static double run(int m, int n, int k, int batch, bool ta, bool tb, double beta,
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         const int reps = 20;
-        for (int i = 0; i < 3; ++i) vrte::gemm_batched(g, 0);
+        for (int i = 0; i < 3; ++i) (g_bk ? vrte::gemm_batched_cfg(g, 0, g_bk, g_st, g_mb) : vrte::gemm_batched(g, 0));
         cudaEventRecord(e0);
-        for (int i = 0; i < reps; ++i) vrte::gemm_batched(g, 0);
+        for (int i = 0; i < reps; ++i) (g_bk ? vrte::gemm_batched_cfg(g, 0, g_bk, g_st, g_mb) : vrte::gemm_batched(g, 0));
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms1;
@@ -76,8 +77,8 @@ static double run(int m, int n, int k, int batch, bool ta, bool tb, double beta,
         float ms2;
         cudaEventElapsedTime(&ms2, e0, e1);
         const double fl = 2.0 * m * n * k * batch;
-        std::printf("m=%d n=%d k=%d batch=%d ta=%d tb=%d  ours %.3f ms %.2f TF/s   cublas %.3f ms %.2f TF/s  rel %.2e\n",
-                    m, n, k, batch, ta, tb, ms1 / reps, fl / (ms1 / reps * 1e-3) / 1e12, ms2 / reps,
+        std::printf("[bk%d st%d] m=%d n=%d k=%d batch=%d ta=%d tb=%d  ours %.3f ms %.2f TF/s   cublas %.3f ms %.2f TF/s  rel %.2e\n",
+                    g_bk, g_st, m, n, k, batch, ta, tb, ms1 / reps, fl / (ms1 / reps * 1e-3) / 1e12, ms2 / reps,
                     fl / (ms2 / reps * 1e-3) / 1e12, rel);
     } else {
         std::printf("m=%d n=%d k=%d batch=%d ta=%d tb=%d beta=%g rel %.2e %s\n", m, n, k, batch, ta, tb, beta, rel,
@@ -88,19 +89,32 @@ static double run(int m, int n, int k, int batch, bool ta, bool tb, double beta,
     return rel;
 }
 
-int main() {
+int main(int argc, char** argv) {
+    if (argc > 2) {  // explicit config "bk st [minb]"; default: the library's selection
+        g_bk = atoi(argv[1]);
+        g_st = atoi(argv[2]);
+    }
+    if (argc > 3) {  // single timed shape (for ncu): bk st m n k batch beta
+        run(atoi(argv[3]), atoi(argv[4]), atoi(argv[5]), atoi(argv[6]), false, false, atof(argv[7]), true);
+        return 0;
+    }
     int fails = 0;
     const int sizes[][3] = {{37, 53, 29}, {64, 128, 16}, {65, 129, 17}, {1, 1, 1}, {256, 7, 100}, {200, 300, 5}};
     for (auto& s : sizes)
         for (int ta = 0; ta < 2; ++ta)
             for (int tb = 0; tb < 2; ++tb)
-                for (double beta : {0.0, 0.7}) fails += run(s[0], s[1], s[2], 3, ta, tb, beta, false) >= 1e-14;
+                for (double beta : {0.0, 0.7, 1.0}) fails += run(s[0], s[1], s[2], 3, ta, tb, beta, false) >= 1e-14;
     run(256, 256, 256, 128, false, false, 0.0, true);
     run(256, 512, 256, 128, false, false, 0.0, true);
     run(256, 512, 256, 128, true, false, 0.0, true);
     run(256, 256, 512, 64, false, false, 1.0, true);
     run(512, 512, 512, 64, false, false, 0.0, true);
     run(4096, 4096, 4096, 1, false, false, 0.0, true);
+    // LU / solve trailing updates (k = 64, beta = 1)
+    run(960, 960, 64, 64, false, false, 1.0, true);
+    run(256, 960, 64, 64, false, false, 1.0, true);
+    run(448, 448, 64, 64, false, false, 1.0, true);
+    run(256, 224, 32, 128, false, false, 1.0, true);
     std::printf("fails=%d\n", fails);
     return fails != 0;
 }
