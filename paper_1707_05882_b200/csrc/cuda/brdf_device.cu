@@ -38,7 +38,7 @@ namespace vrte {
 
 namespace {
 
-constexpr double kRefineTarget = 1e-11;  // per-mode 8N residual after refinement
+constexpr double kRefineTarget = 5e-11;  // per-mode 8N residual after refinement
 
 template <typename T>
 struct DevBuf {

@@ -1790,6 +1790,35 @@ __device__ void solve2(cplx c00, cplx c01, cplx c10, cplx c11, cplx b0, cplx b1,
     x1 = X[1];
 }
 
+
+// Real version of solve2 (complete pivoting, dlaln2-style smin perturbation).
+__device__ void solve2r(double c00, double c01, double c10, double c11, double b0, double b1, double smin,
+                        double& x0, double& x1) {
+    const double m00 = fabs(c00), m01 = fabs(c01), m10 = fabs(c10), m11 = fabs(c11);
+    int pr = 0, pc = 0;
+    double mx = m00;
+    if (m01 > mx) { mx = m01; pr = 0; pc = 1; }
+    if (m10 > mx) { mx = m10; pr = 1; pc = 0; }
+    if (m11 > mx) { mx = m11; pr = 1; pc = 1; }
+    if (smin > 0.0 && mx < smin) {
+        x0 = b0 / smin;
+        x1 = b1 / smin;
+        return;
+    }
+    const double cpp = pr ? (pc ? c11 : c10) : (pc ? c01 : c00);   // C[pr][pc]
+    const double cqp = pr ? (pc ? c01 : c00) : (pc ? c11 : c10);   // C[qr][pc]
+    const double cpq = pr ? (pc ? c10 : c11) : (pc ? c00 : c01);   // C[pr][qc]
+    const double cqq = pr ? (pc ? c00 : c01) : (pc ? c10 : c11);   // C[qr][qc]
+    const double bp = pr ? b1 : b0, bq = pr ? b0 : b1;
+    const double l = cqp / cpp;
+    double u22 = cqq - l * cpq;
+    if (smin > 0.0 && fabs(u22) < smin) u22 = smin;
+    const double xq = (bq - l * bp) / u22;
+    const double xp = (bp - cpq * xq) / cpp;
+    x0 = pc ? xq : xp;
+    x1 = pc ? xp : xq;
+}
+
 // ------------------------------------------------------------------ eigenvectors
 // dtrevc right eigenvectors of the quasi-triangular T, warp per eigenvalue
 // (complex pairs handled by the first index, packed Re/Im columns).
@@ -1912,6 +1941,183 @@ __global__ void trevc_kernel(const double* Tall, const double* wrall, const doub
             }
         }
         __syncwarp();
+    }
+}
+
+
+// Register-resident dtrevc: warp per eigenvalue (complex pairs by their first
+// index), lane l owns rows l + 32 i of the solution; the solved entry is
+// broadcast by shuffle and the T columns of the NEXT step are loaded while the
+// current one is applied (the serial chain is shuffle + divide + FMA, not an
+// L2 round trip).  Same arithmetic and dlaln2-style smin perturbation as
+// trevc_kernel.  pf[c] = 1 when T(c, c-1) != 0 (second row of a 2x2 block).
+template <int RPL>
+__global__ void __launch_bounds__(256) trevc_reg_kernel(const double* Tall, const double* wrall,
+                                                        const double* wiall, double* Yall, int d) {
+    extern __shared__ unsigned char pf[];
+    const int b = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const double* T = Tall + (size_t)b * d * d;
+    const double* wr = wrall + (size_t)b * d;
+    const double* wi = wiall + (size_t)b * d;
+    double* Y = Yall + (size_t)b * d * d;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) pf[c] = (c > 0 && T[c + (size_t)(c - 1) * d] != 0.0);
+    __syncthreads();
+    const double smlnum = kSafeMin * ((double)d / kUlp);
+    auto Tat = [&](int r, int c) { return T[r + (size_t)c * d]; };
+    // column c of T restricted to rows < lim, this lane's rows
+    auto load_col = [&](double* dst, int c, int lim) {
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+            const int r = lane + 32 * i;
+            dst[i] = (c >= 0 && r < lim) ? T[r + (size_t)c * d] : 0.0;
+        }
+    };
+    auto pick = [&](const double* v, int r) {  // value of row r from its owner lane
+        double x = 0.0;
+#pragma unroll
+        for (int i = 0; i < RPL; ++i)
+            if (i == (r >> 5)) x = v[i];
+        return __shfl_sync(0xffffffffu, x, r & 31);
+    };
+    auto put = [&](double* v, int r, double x) {
+#pragma unroll
+        for (int i = 0; i < RPL; ++i)
+            if (i == (r >> 5) && lane == (r & 31)) v[i] = x;
+    };
+    for (int ki = w; ki < d; ki += nw) {
+        const double wik = wi[ki];
+        if (wik < 0.0) continue;
+        double re[RPL], im[RPL], t1[RPL], t2[RPL], n1[RPL], n2[RPL];
+        const bool cxv = wik != 0.0;
+        int top;  // first row of the eigenvalue's own block
+        cplx lam;
+        double smin;
+        if (!cxv) {
+            top = ki;
+            lam = cmk(wr[ki], 0.0);
+            smin = fmax(kUlp * fabs(lam.re), smlnum);
+            load_col(re, ki, ki);
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) {
+                re[i] = -re[i];
+                im[i] = 0.0;
+                if (lane + 32 * i == ki) re[i] = 1.0;
+            }
+        } else {
+            const int pp = ki, q = ki + 1;
+            top = pp;
+            lam = cmk(wr[pp], wik);
+            smin = fmax(kUlp * (fabs(wr[pp]) + fabs(wik)), smlnum);
+            double xpr, xqi;
+            if (fabs(Tat(pp, q)) >= fabs(Tat(q, pp))) {
+                xpr = 1.0;
+                xqi = wik / Tat(pp, q);
+            } else {
+                xpr = -wik / Tat(q, pp);
+                xqi = 1.0;
+            }
+            load_col(re, pp, pp);
+            load_col(im, q, pp);
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) {
+                const int r = lane + 32 * i;
+                re[i] *= -xpr;
+                im[i] *= -xqi;
+                if (r == pp) {
+                    re[i] = xpr;
+                    im[i] = 0.0;
+                }
+                if (r == q) {
+                    re[i] = 0.0;
+                    im[i] = xqi;
+                }
+            }
+        }
+        int j = top - 1;
+        // prefetch the first step's columns (and, for real eigenvalues, the
+        // reciprocal pivot of a 1x1 step, off the serial chain)
+        bool pair = j > 0 && pf[j];
+        load_col(t1, j, pair ? j - 1 : j);
+        load_col(t2, pair ? j - 1 : -1, j - 1);
+        auto rpiv = [&](int c) {
+            double den = (c >= 0) ? Tat(c, c) - lam.re : 1.0;
+            if (fabs(den) < smin) den = smin;
+            return 1.0 / den;
+        };
+        double rd = (!cxv && !pair && j >= 0) ? rpiv(j) : 0.0;
+        while (j >= 0) {
+            const int jn = j - (pair ? 2 : 1);
+            const bool pairn = jn > 0 && pf[jn];
+            load_col(n1, jn, pairn ? jn - 1 : jn);
+            load_col(n2, pairn ? jn - 1 : -1, jn - 1);
+            const double rdn = (!cxv && !pairn && jn >= 0) ? rpiv(jn) : 0.0;
+            if (!cxv) {
+                if (pair) {
+                    double x0, x1;
+                    solve2r(Tat(j - 1, j - 1) - lam.re, Tat(j - 1, j), Tat(j, j - 1), Tat(j, j) - lam.re,
+                            pick(re, j - 1), pick(re, j), smin, x0, x1);
+#pragma unroll
+                    for (int i = 0; i < RPL; ++i) re[i] = fma(-x0, t2[i], fma(-x1, t1[i], re[i]));
+                    put(re, j - 1, x0);
+                    put(re, j, x1);
+                } else {
+                    const double x = pick(re, j) * rd;
+#pragma unroll
+                    for (int i = 0; i < RPL; ++i) re[i] = fma(-x, t1[i], re[i]);
+                    put(re, j, x);
+                }
+            } else if (pair) {
+                const double ajj = Tat(j - 1, j - 1), aj1 = Tat(j - 1, j), a1j = Tat(j, j - 1), a11 = Tat(j, j);
+                const cplx b0 = cmk(pick(re, j - 1), pick(im, j - 1));
+                const cplx b1 = cmk(pick(re, j), pick(im, j));
+                cplx x0, x1;
+                solve2(cmk(ajj, 0) - lam, cmk(aj1, 0), cmk(a1j, 0), cmk(a11, 0) - lam, b0, b1, smin, x0, x1);
+                // t2 = column j-1, t1 = column j (rows < j-1)
+#pragma unroll
+                for (int i = 0; i < RPL; ++i) {
+                    re[i] = fma(-x0.re, t2[i], fma(-x1.re, t1[i], re[i]));
+                    im[i] = fma(-x0.im, t2[i], fma(-x1.im, t1[i], im[i]));
+                }
+                put(re, j - 1, x0.re);
+                put(re, j, x1.re);
+                put(im, j - 1, x0.im);
+                put(im, j, x1.im);
+            } else {
+                cplx den = cmk(Tat(j, j), 0.0) - lam;
+                if (cabs_(den) < smin) den = cmk(smin, 0.0);
+                const cplx x = cdiv(cmk(pick(re, j), pick(im, j)), den);
+#pragma unroll
+                for (int i = 0; i < RPL; ++i) {
+                    re[i] = fma(-x.re, t1[i], re[i]);
+                    im[i] = fma(-x.im, t1[i], im[i]);
+                }
+                put(re, j, x.re);
+                put(im, j, x.im);
+            }
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) {
+                t1[i] = n1[i];
+                t2[i] = n2[i];
+            }
+            j = jn;
+            pair = pairn;
+            rd = rdn;
+        }
+        const int last = cxv ? ki + 1 : ki;
+        double* yr = Y + (size_t)ki * d;
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+            const int r = lane + 32 * i;
+            if (r < d) yr[r] = (r <= last) ? re[i] : 0.0;
+        }
+        if (cxv) {
+            double* yi = Y + (size_t)(ki + 1) * d;
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) {
+                const int r = lane + 32 * i;
+                if (r < d) yi[r] = (r <= last) ? im[i] : 0.0;
+            }
+        }
     }
 }
 
@@ -2281,7 +2487,22 @@ void launch_trevc(const double* T, const double* wr, const double* wi, double* Y
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    trevc_kernel<<<batch, warps * 32, smem, st>>>(T, wr, wi, Y, d);
+    static const char* tmode = std::getenv("VRTE_TREVC");  // reg (default) | smem
+    if (tmode && std::string(tmode) == "smem") {
+        trevc_kernel<<<batch, warps * 32, smem, st>>>(T, wr, wi, Y, d);
+    } else {
+        const int rpl = (d + 31) / 32;
+        if (rpl <= 2)
+            trevc_reg_kernel<2><<<batch, 256, d, st>>>(T, wr, wi, Y, d);
+        else if (rpl <= 4)
+            trevc_reg_kernel<4><<<batch, 256, d, st>>>(T, wr, wi, Y, d);
+        else if (rpl <= 8)
+            trevc_reg_kernel<8><<<batch, 256, d, st>>>(T, wr, wi, Y, d);
+        else if (rpl <= 16)
+            trevc_reg_kernel<16><<<batch, 256, d, st>>>(T, wr, wi, Y, d);
+        else
+            trevc_reg_kernel<32><<<batch, 256, d, st>>>(T, wr, wi, Y, d);
+    }
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -27,7 +27,7 @@
 namespace vrte {
 namespace {
 
-constexpr int HNT = 512;
+constexpr int HNT = 1024;
 
 __device__ inline double block_sum_h(double v, double* red) { return block_sum(v, red); }
 
@@ -117,40 +117,23 @@ __global__ void __launch_bounds__(HNT) hess_panel_kernel(double* Aall, double* V
             A[r + (size_t)k * d] = a;  // final Hessenberg column k
         }
         __syncthreads();
-        // 4. y = A[:, k+1:] v[k+1:] over the start-of-panel matrix
+        // 4. y = A[:, k+1:] v[k+1:] over the start-of-panel matrix: nsplit column
+        //    slices per row, 8 independent accumulators (8 loads in flight per thread)
         {
             const int cb = k + 1, ncols = d - cb;
-            if (nsplit > 1) {
-                const int r = t % d, s = t / d;
-                if (s < nsplit) {
-                    const int per = (ncols + nsplit - 1) / nsplit;
-                    const int ca = cb + s * per, ce = min(d, ca + per);
-                    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-                    const double* ap = A + r;
-                    int c = ca;
-                    for (; c + 3 < ce; c += 4) {
-                        a0 = fma(ap[(size_t)c * d], vj[c], a0);
-                        a1 = fma(ap[(size_t)(c + 1) * d], vj[c + 1], a1);
-                        a2 = fma(ap[(size_t)(c + 2) * d], vj[c + 2], a2);
-                        a3 = fma(ap[(size_t)(c + 3) * d], vj[c + 3], a3);
-                    }
-                    for (; c < ce; ++c) a0 = fma(ap[(size_t)c * d], vj[c], a0);
-                    part[s * d + r] = (a0 + a1) + (a2 + a3);
+            for (int rr = t; rr < d * nsplit; rr += HNT) {
+                const int r = rr % d, s = rr / d;
+                const int per = (ncols + nsplit - 1) / nsplit;
+                const int ca = cb + s * per, ce = min(d, ca + per);
+                double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                const double* ap = A + r;
+                int c = ca;
+                for (; c + 7 < ce; c += 8) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) a[q] = fma(ap[(size_t)(c + q) * d], vj[c + q], a[q]);
                 }
-            } else {
-                for (int r = t; r < d; r += HNT) {
-                    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-                    const double* ap = A + r;
-                    int c = cb;
-                    for (; c + 3 < d; c += 4) {
-                        a0 = fma(ap[(size_t)c * d], vj[c], a0);
-                        a1 = fma(ap[(size_t)(c + 1) * d], vj[c + 1], a1);
-                        a2 = fma(ap[(size_t)(c + 2) * d], vj[c + 2], a2);
-                        a3 = fma(ap[(size_t)(c + 3) * d], vj[c + 3], a3);
-                    }
-                    for (; c < d; ++c) a0 = fma(ap[(size_t)c * d], vj[c], a0);
-                    part[r] = (a0 + a1) + (a2 + a3);
-                }
+                for (; c < ce; ++c) a[0] = fma(ap[(size_t)c * d], vj[c], a[0]);
+                part[s * d + r] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
             }
         }
         // 5. u = V_j^T v (rows k+1..), T column, Y column
