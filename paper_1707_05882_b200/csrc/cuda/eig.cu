@@ -1153,11 +1153,11 @@ __device__ bool warp_small_schur(double* T, double* V, int n, double* sr, double
                 }
                 if (r < n) {
                     double* vr = V + r;
-                    const double a0 = vr[k * MW], a1 = vr[(k + 1) * MW], a2 = nr == 3 ? vr[(k + 2) * MW] : 0.0;
+                    const double a0 = vr[k * LDW], a1 = vr[(k + 1) * LDW], a2 = nr == 3 ? vr[(k + 2) * LDW] : 0.0;
                     const double sum = a0 + v2 * a1 + v3 * a2;
-                    vr[k * MW] = a0 - sum * t1;
-                    vr[(k + 1) * MW] = a1 - sum * t2;
-                    if (nr == 3) vr[(k + 2) * MW] = a2 - sum * t3;
+                    vr[k * LDW] = a0 - sum * t1;
+                    vr[(k + 1) * LDW] = a1 - sum * t2;
+                    if (nr == 3) vr[(k + 2) * LDW] = a2 - sum * t3;
                 }
                 __syncwarp();
             }
@@ -1194,9 +1194,9 @@ __device__ bool warp_small_schur(double* T, double* V, int n, double* sr, double
             }
             if (lane < n) {
                 double* vr = V + lane;
-                const double xv = vr[(I - 1) * MW], yv = vr[I * MW];
-                vr[(I - 1) * MW] = cs * xv + sn * yv;
-                vr[I * MW] = cs * yv - sn * xv;
+                const double xv = vr[(I - 1) * LDW], yv = vr[I * LDW];
+                vr[(I - 1) * LDW] = cs * xv + sn * yv;
+                vr[I * LDW] = cs * yv - sn * xv;
             }
             __syncwarp();
         }
@@ -1260,7 +1260,7 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
                                                         double* wiall, int d, DeviceStatus* status,
                                                         int aed_nw, int nb4_min, int nb2_min, int nibble) {
     __shared__ double Wn[MW * LDW];  // window, column-major Wn[c*LDW + r]
-    __shared__ double Us[MW * MW];  // accumulated factor, column-major
+    __shared__ double Us[MW * LDW];  // accumulated factor, column-major Us[c*LDW + r]
     __shared__ double Sm[TQ * TQ];  // trailing block for the shifts
     __shared__ double s_sr[TQ], s_si[TQ];
     __shared__ double s_pr[4 * MB_MAX];  // shift pair per bulge: rt1r rt1i rt2r rt2i
@@ -1289,32 +1289,87 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
         tc = now;
     };
     // H(:, wlo:whi) <- H U above the window, H(wlo:whi, :) <- U^T H right of it,
-    // Z(:, wlo:whi) <- Z U  (U = Us, nw x nw zero padded to MW)
+    // Z(:, wlo:whi) <- Z U  (U = Us, nw x nw, identity beyond).  Every target is
+    // a vector v (a column segment right of the window, or a row segment of H
+    // above it / of Z) mapped to v^T U, so tiles of 8 vectors are one
+    // [8 x 32] x [32 x 32] product on the FP64 tensor cores: warp per tile,
+    // U's B fragments held in registers for the whole call (DMMA m8n8k4).
     auto apply_u = [&](int wlo, int whi, int nw) {
         const int n_right = d - 1 - whi, n_above = wlo;
-        for (int task = t; task < n_right + n_above + d; task += nt) {
-            double x[MW];
-            if (task < n_right) {  // column right of the window: U^T x
-                double* col = H + (size_t)(whi + 1 + task) * d + wlo;
+        const int tr = (n_right + 7) / 8, ta = (n_above + 7) / 8, tz = (d + 7) / 8;
+        const int gq = lane >> 2, tq = lane & 3;
+        double bf[8][4];
 #pragma unroll
-                for (int q = 0; q < MW; ++q) x[q] = (q < nw) ? col[q] : 0.0;
-                for (int r = 0; r < nw; ++r) {
-                    double acc = 0.0;
+        for (int ks = 0; ks < 8; ++ks)
 #pragma unroll
-                    for (int q = 0; q < MW; ++q) acc = fma(Us[r * MW + q], x[q], acc);
-                    col[r] = acc;
+            for (int cb = 0; cb < 4; ++cb) bf[ks][cb] = Us[(cb * 8 + gq) * LDW + ks * 4 + tq];
+        // vector gq of a tile: base pointer and element stride
+        auto locate = [&](int tile, double*& base, long long& st) -> bool {
+            if (tile < tr) {
+                const int c = whi + 1 + tile * 8 + gq;
+                base = H + (size_t)min(c, d - 1) * d + wlo;
+                st = 1;
+                return c < d;
+            } else if (tile < tr + ta) {
+                const int r = (tile - tr) * 8 + gq;
+                base = H + min(r, n_above - 1) + (size_t)wlo * d;
+                st = d;
+                return r < n_above;
+            }
+            const int r = (tile - tr - ta) * 8 + gq;
+            base = Z + min(r, d - 1) + (size_t)wlo * d;
+            st = d;
+            return r < d;
+        };
+        const int ntile = tr + ta + tz, wstep = nt / 32;
+        double an[8];
+        double* bnext = H;
+        long long snext = 1;
+        bool oknext = false;
+        if (warp < ntile) {
+            oknext = locate(warp, bnext, snext);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const int q = ks * 4 + tq;
+                an[ks] = (oknext && q < nw) ? bnext[q * snext] : 0.0;
+            }
+        }
+        // software pipeline: the next tile's vector segments are in flight while
+        // the current tile is multiplied and stored
+        for (int tile = warp; tile < ntile; tile += wstep) {
+            double af[8];
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) af[ks] = an[ks];
+            double* base = bnext;
+            const long long st = snext;
+            const bool ok = oknext;
+            if (tile + wstep < ntile) {
+                oknext = locate(tile + wstep, bnext, snext);
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    const int q = ks * 4 + tq;
+                    an[ks] = (oknext && q < nw) ? bnext[q * snext] : 0.0;
                 }
-            } else {  // row of H above the window, or of Z: x U
-                const bool isz = task >= n_right + n_above;
-                const int i = isz ? task - n_right - n_above : task - n_right;
-                double* base = (isz ? Z : H) + i + (size_t)wlo * d;
+            }
+            double acc[4][2];
 #pragma unroll
-                for (int q = 0; q < MW; ++q) x[q] = (q < nw) ? base[(size_t)q * d] : 0.0;
-                for (int c = 0; c < nw; ++c) {
-                    double acc = 0.0;
+            for (int cb = 0; cb < 4; ++cb) acc[cb][0] = acc[cb][1] = 0.0;
 #pragma unroll
-                    for (int q = 0; q < MW; ++q) acc = fma(x[q], Us[c * MW + q], acc);
-                    base[(size_t)c * d] = acc;
+            for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+                for (int cb = 0; cb < 4; ++cb)
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                                 : "+d"(acc[cb][0]), "+d"(acc[cb][1])
+                                 : "d"(af[ks]), "d"(bf[ks][cb]));
+            // D[i][c]: vector i = gq, element c = cb*8 + 2tq (+1); all A loads of
+            // this tile precede its stores (warp-synchronous)
+            __syncwarp();
+            if (ok) {
+#pragma unroll
+                for (int cb = 0; cb < 4; ++cb) {
+                    const int c = cb * 8 + 2 * tq;
+                    if (c < nw) base[c * st] = acc[cb][0];
+                    if (c + 1 < nw) base[(c + 1) * st] = acc[cb][1];
                 }
             }
         }
@@ -1414,7 +1469,7 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
                     for (int e = lane; e < MW * MW; e += 32) {
                         const int r = e % MW, c = e / MW;
                         Wn[r + c * LDW] = (r < nwin && c < nwin && r <= c + 1) ? hg(H, d, kwtop + r, kwtop + c) : 0.0;
-                        Us[e] = (r == c) ? 1.0 : 0.0;
+                        Us[r + c * LDW] = (r == c) ? 1.0 : 0.0;
                     }
                     __syncwarp();
                     const bool ok = warp_small_schur(Wn, Us, nwin, s_esr, s_esi);
@@ -1427,7 +1482,7 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
                                 double foo = fabs(Wn[j + j * LDW]) + sqrt(fabs(Wn[j + (j - 1) * LDW])) *
                                                                        sqrt(fabs(Wn[(j - 1) + j * LDW]));
                                 if (foo == 0.0) foo = fabs(sspike);
-                                const double sp = fmax(fabs(sspike * Us[j * MW]), fabs(sspike * Us[(j - 1) * MW]));
+                                const double sp = fmax(fabs(sspike * Us[j * LDW]), fabs(sspike * Us[(j - 1) * LDW]));
                                 if (sp <= fmax(smlnum, ulp * foo)) {
                                     ndefl += 2;
                                     j -= 2;
@@ -1437,7 +1492,7 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
                             } else {
                                 double foo = fabs(Wn[j + j * LDW]);
                                 if (foo == 0.0) foo = fabs(sspike);
-                                if (fabs(sspike * Us[j * MW]) <= fmax(smlnum, ulp * foo)) {
+                                if (fabs(sspike * Us[j * LDW]) <= fmax(smlnum, ulp * foo)) {
                                     ndefl += 1;
                                     j -= 1;
                                 } else {
@@ -1449,14 +1504,14 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
                     const int nd = nwin - ndefl;
                     if (ok && ndefl > 0 && nd > 1) {
                         // collapse the spike of the undeflated part onto its first row
-                        for (int q = lane; q < nd; q += 32) s_vec[q] = Us[q * MW];
+                        for (int q = lane; q < nd; q += 32) s_vec[q] = Us[q * LDW];
                         __syncwarp();
                         double beta;
                         double tau = warp_dlarfg(s_vec, nd, &beta);
                         if (tau != 0.0) {
                             warp_refl_left(Wn, LDW, s_vec, nd, tau, 0, 0, nwin);
                             warp_refl_right(Wn, LDW, s_vec, nd, tau, 0, 0, nd);
-                            warp_refl_right(Us, MW, s_vec, nd, tau, 0, 0, nwin);
+                            warp_refl_right(Us, LDW, s_vec, nd, tau, 0, 0, nwin);
                         }
                         // back to Hessenberg form (dgehrd on the leading nd x nd block)
                         for (int j = 0; j + 2 < nd; ++j) {
@@ -1467,7 +1522,7 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
                             if (tau != 0.0) {
                                 warp_refl_left(Wn, LDW, s_vec, len, tau, j + 1, j + 1, nwin);
                                 warp_refl_right(Wn, LDW, s_vec, len, tau, j + 1, 0, nd);
-                                warp_refl_right(Us, MW, s_vec, len, tau, j + 1, 0, nwin);
+                                warp_refl_right(Us, LDW, s_vec, len, tau, j + 1, 0, nwin);
                             }
                             for (int q = lane; q < len; q += 32) Wn[(j + 1 + q) + j * LDW] = (q == 0) ? beta : 0.0;
                             __syncwarp();
@@ -1596,7 +1651,7 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
                 for (int idx = t; idx < MW * MW; idx += nt) {
                     const int r = idx % MW, c = idx / MW;
                     Wn[r + c * LDW] = (r < nw && c < nw) ? H[(wlo + r) + (size_t)(wlo + c) * d] : 0.0;
-                    Us[idx] = (r == c) ? 1.0 : 0.0;
+                    Us[r + c * LDW] = (r == c) ? 1.0 : 0.0;
                 }
                 __syncthreads();
                 tick(1);
@@ -1677,12 +1732,12 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
                             const int c = k - wlo;
                             for (int r = lane; r < nw; r += 32) {
                                 double* u = Us + r;
-                                const double u0 = u[c * MW], u1 = u[(c + 1) * MW];
-                                const double u2 = (nr == 3) ? u[(c + 2) * MW] : 0.0;
+                                const double u0 = u[c * LDW], u1 = u[(c + 1) * LDW];
+                                const double u2 = (nr == 3) ? u[(c + 2) * LDW] : 0.0;
                                 const double sum = u0 + v2 * u1 + v3 * u2;
-                                u[c * MW] = u0 - sum * t1;
-                                u[(c + 1) * MW] = u1 - sum * t2;
-                                if (nr == 3) u[(c + 2) * MW] = u2 - sum * t3;
+                                u[c * LDW] = u0 - sum * t1;
+                                u[(c + 1) * LDW] = u1 - sum * t2;
+                                if (nr == 3) u[(c + 2) * LDW] = u2 - sum * t3;
                             }
                         }
                         named_bar(1, nb * 32);
