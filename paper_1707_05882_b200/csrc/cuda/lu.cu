@@ -16,6 +16,7 @@
 // The solve gathers the right-hand sides through the net row permutation,
 // then runs blocked forward / backward substitution (TRSM on 64-row blocks +
 // GEMM updates).
+#include <cstdlib>
 #include <stdexcept>
 
 #include "boundary.cuh"
@@ -370,9 +371,12 @@ void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatu
                   const int* order_index, cudaStream_t st) {
     if (G > 4096) throw std::invalid_argument("vrte_cuda: boundary system larger than 4096 rows");
     const int PB = panel_width(G);
+    // outer block: 128 columns (trailing GEMMs with k = 128), handled by the
+    // 64-row swap / TRSM kernels in two halves; VRTE_LU_NB=64 for A/B runs
+    static const int OB = std::getenv("VRTE_LU_NB") ? std::atoi(std::getenv("VRTE_LU_NB")) : 128;
     const long long gg = (long long)G * G;
-    for (int K0 = 0; K0 < G; K0 += LU_NB) {
-        const int NBk = min(LU_NB, G - K0);
+    for (int K0 = 0; K0 < G; K0 += OB) {
+        const int NBk = min(OB, G - K0);
         for (int k0 = K0; k0 < K0 + NBk; k0 += PB) {
             const int jb = min(PB, K0 + NBk - k0);
             const int np = G - k0;
@@ -397,10 +401,20 @@ void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatu
                             batch, -1.0, 1.0, st);
             }
         }
-        swap_launch(A, G, gg, ipiv, G, K0, NBk, 0, G, K0, K0 + NBk, batch, st);
+        // the block's interchanges on the other columns, in chunks of <= 64 pivots
+        for (int p0 = K0; p0 < K0 + NBk; p0 += LU_NB)
+            swap_launch(A, G, gg, ipiv, G, p0, min(LU_NB, K0 + NBk - p0), 0, G, K0, K0 + NBk, batch, st);
         const int rest = G - K0 - NBk;
         if (rest > 0) {
-            trsm_launch<true>(A, G, A, G, gg, K0, NBk, K0 + NBk, G, batch, st);
+            // U12 = L11^-1 A12, blocked by 64 rows
+            for (int r0 = K0; r0 < K0 + NBk; r0 += LU_NB) {
+                const int rb = min(LU_NB, K0 + NBk - r0);
+                trsm_launch<true>(A, G, A, G, gg, r0, rb, K0 + NBk, G, batch, st);
+                const int below = K0 + NBk - (r0 + rb);
+                if (below > 0)
+                    rm_gemm(below, rest, rb, A + (size_t)(r0 + rb) * G + r0, G, gg, A + (size_t)r0 * G + K0 + NBk,
+                            G, gg, A + (size_t)(r0 + rb) * G + K0 + NBk, G, gg, batch, -1.0, 1.0, st);
+            }
             rm_gemm(rest, rest, NBk, A + (size_t)(K0 + NBk) * G + K0, G, gg, A + (size_t)K0 * G + K0 + NBk,
                     G, gg, A + (size_t)(K0 + NBk) * G + K0 + NBk, G, gg, batch, -1.0, 1.0, st);
         }
@@ -438,16 +452,17 @@ void lu_solve_rm(const double* A, int G, int batch, const int* perm, const doubl
 
 int lu_rm_launch_count(int G) {
     const int PB = panel_width(G);
+    static const int OB = std::getenv("VRTE_LU_NB") ? std::atoi(std::getenv("VRTE_LU_NB")) : 128;
     int n = 0;
-    for (int K0 = 0; K0 < G; K0 += LU_NB) {
-        const int NBk = min(LU_NB, G - K0);
+    for (int K0 = 0; K0 < G; K0 += OB) {
+        const int NBk = min(OB, G - K0);
         for (int k0 = K0; k0 < K0 + NBk; k0 += PB) {
             const int jb = min(PB, K0 + NBk - k0);
-            n += 1 + (NBk > jb ? 1 : 0);
+            n += 2;  // panel + swap
             if (K0 + NBk - (k0 + jb) > 0) n += 1 + (G - k0 - jb > 0 ? 1 : 0);
         }
-        n += 1;
-        if (G - K0 - NBk > 0) n += 2;
+        n += (NBk + LU_NB - 1) / LU_NB;
+        if (G - K0 - NBk > 0) n += 2 * ((NBk + LU_NB - 1) / LU_NB) - 1 + 1;
     }
     n += 1;                                          // perm
     const int nblk = (G + LU_NB - 1) / LU_NB;
