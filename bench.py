@@ -275,30 +275,37 @@ def main():
         return
 
     # ---------------- roofline of the dominant kernel
+    # Algorithmic FP64 flops per launch (SURVEY §8(d) / Golub-Van Loan counts,
+    # DESIGN.md §5); the stage times are CUDA events on the plan's stream.
     d = 4 * N
     B = S * L
-    kern = {"hqr_kernel (Francis QR + Schur vectors)": (res["t_hqr"], B * 20.0 * d ** 3),
-            "boundary LU factor (panel+trsm+gemm)": (res["t_lu_factor"], L * (2.0 / 3.0) * (2 * d * P) ** 3),
-            "eigen refinement (Newton, 8N)": (res["t_refine"], B * 3 * 20.0 * d ** 3),
-            "hessenberg_kernel": (res["t_hessenberg"], B * (10.0 / 3.0 + 4.0 / 3.0) * d ** 3),
-            "trevc_kernel": (res["t_trevc"], B * (1.0 / 3.0) * d ** 3)}
+    G = 2 * d * P
+    kern = {"hqr_multi_kernel (multishift Francis QR + AED + Schur vectors)": (res["t_hqr"], B * 20.0 * d ** 3),
+            "boundary LU factor (panel + swap + trsm + DMMA GEMM)": (res["t_lu_factor"], L * (2.0 / 3.0) * G ** 3),
+            "boundary LU solve (trsm + DMMA GEMM)": (res["t_lu_solve"], L * 2.0 * G ** 2 * 4 * n_in),
+            "eigen refinement (Newton step, 8N residual GEMMs)": (res["t_refine"], B * 24.0 * d ** 3),
+            "blocked Hessenberg + Q": (res["t_hessenberg"], B * (10.0 / 3.0 + 4.0 / 3.0) * d ** 3),
+            "trevc_reg_kernel (eigenvectors)": (res["t_trevc"], B * (1.0 / 3.0) * d ** 3)}
     name = max(kern, key=lambda k: kern[k][0])
     t_k, flops = kern[name]
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_dominant_kernel.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            pj = json.load(open(prof))
+            if name.startswith(pj.get("kernel", "?")):
+                traffic = pj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     achieved = flops / t_k / 1e12 if t_k > 0 else 0.0
     roofline = {"bound": "tensor", "kernel": name, "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": traffic,
                 "peak_source": "measured cuBLAS DGEMM (torch.float64 matmul 8192^3) on this GPU; "
-                               "MEASURED_PEAKS.json has no FP64 entry",
+                               "MEASURED_PEAKS.json has no FP64 entry (B200 FP64 tensor rate = FP64 rate)",
                 "algorithmic_flops_per_launch": flops,
-                "flop_model": "Golub-Van Loan counts: QR with Schur vectors 20 d^3 per (medium,order); "
-                              "LU (2/3) n_b^3; d = 4N, n_b = 2dP"}
+                "flop_model": "QR with Schur vectors 20 d^3 per (medium, order); LU (2/3) G^3 and solve "
+                              "2 G^2 R per order; Hessenberg+Q 14/3 d^3; d = 4N, G = 2dP, R = 4 n_in",
+                "stage_tflops": {k: (f / t / 1e12 if t > 0 else None) for k, (t, f) in kern.items()}}
 
     # ---------------- CPU baseline (rank 0, N = 1 only)
     cpu = None
