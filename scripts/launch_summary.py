@@ -2,7 +2,7 @@
 time of the LAST solve (the list holds warm-up + timed solve)."""
 import csv, collections, sys, json
 path = sys.argv[1]
-nsolves = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+nsolves = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 2
 rows = [r for r in csv.reader(open(path)) if len(r) > 5]
 hdr = rows[0]
 ki, vi, gi, bi = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Grid Size"), hdr.index("Block Size")
