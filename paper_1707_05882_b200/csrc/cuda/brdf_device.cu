@@ -359,7 +359,8 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
         gemm_batched(gemm(d, d, d, pl.E.p, d, dd, false, pl.tmp1.p, d, dd, false, pl.tmp3.p, d, dd, B), st);
         gemm_batched(gemm(d, d, d, pl.F.p, d, dd, false, pl.tmp4.p, d, dd, false, pl.tmp2.p, d, dd, B), st);
     };
-    residual_gemms();
+    // (the 8N residual of the unrefined modes is not needed: every refinement
+    // step starts by recomputing it, and final_residual() feeds the gate)
     ResidualArgs ra{};
     ra.d = d;
     ra.batch = B;
@@ -371,8 +372,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     ra.G2 = pl.tmp2.p;
     ra.mdiag = pl.mdiag.p;
     ra.residual = pl.residual.p;
-    launch_residual(ra, st);
-    nl += 14;
+    nl += 11;
     // ---- eigenpair refinement (replaces the polish of homogeneous.cpp:216-268)
     RefineArgs rf{};
     rf.d = d;
