@@ -54,8 +54,8 @@ __global__ void assemble_kernel(BndArgs a) {
     const cplx att = att_of(a.p.tau[p], nu);
     auto pk = [&](cplx v) { return imc ? v.im : v.re; };
     double* A = a.lhs + (size_t)mo * G * G;
-    const int ca = 2 * d * p + jj;       // column A_p(jj)
-    const int cbk = 2 * d * p + d + jj;  // column B_p(jj)
+    const int ca = bnd_col(p, jj, d, G);       // column A_p(jj)
+    const int cbk = bnd_col(p, d + jj, d, G);  // column B_p(jj)
     auto at = [&](int r, int c) -> double& { return A[(size_t)r * G + c]; };
     if (p == 0) {
         at(i, ca) = pk(dflip(pm, i));
@@ -136,7 +136,7 @@ __global__ void base_kernel(BndArgs a, int mo) {
     reflect_rows(a.p, v, d, lane, out);
     __syncwarp();
     double* A = a.lhs + (size_t)mo * G * G;
-    const int col = 2 * d * q + (isb ? d : 0) + jj;
+    const int col = bnd_col(q, (isb ? d : 0) + jj, d, G);
     const int rb = d + 2 * d * (P - 1);
     for (int i = lane; i < d; i += 32) A[(size_t)(rb + i) * G + col] -= out[i];
 }

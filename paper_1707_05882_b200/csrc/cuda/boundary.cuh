@@ -28,9 +28,14 @@ void launch_copy_zp0(const BndArgs& a, cudaStream_t st);
 // row permutation (row i of P B = row perm[i] of B).
 void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatus* status,
                   const int* order_index, cudaStream_t st);
-// X = A^-1 B for row-major B, X ([batch][G][ncol]); B is not modified.
+// X = A^-1 B for row-major B, X ([batch][G][ncol]); B is not modified.  Only
+// rows >= row_lo (rounded down to the 64-row block) of X are the solution.
 void lu_solve_rm(const double* A, int G, int batch, const int* perm, const double* B, double* X,
-                 int ncol, cudaStream_t st);
+                 int ncol, cudaStream_t st, int row_lo = 0);
+// Column of the boundary system holding layer p's packed column j: layer 0
+// (the only unknowns the tau = 0 field needs) is ordered LAST, so the back
+// substitution stops after its 2d rows.
+__host__ __device__ inline int bnd_col(int p, int j, int d, int G) { return (2 * d * p + j - 2 * d + G) % G; }
 int lu_rm_launch_count(int G);
 
 }  // namespace vrte

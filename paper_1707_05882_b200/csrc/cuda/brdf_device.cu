@@ -500,13 +500,14 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[11], st));
     lu_factor_rm(pl.lhs.p, G, NO, pl.ipiv.p, pl.perm.p, pl.status, pl.order_index.p, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[12], st));
-    lu_solve_rm(pl.lhs.p, G, NO, pl.perm.p, pl.rhs_b.p, pl.rhs_x.p, R, st);
+    lu_solve_rm(pl.lhs.p, G, NO, pl.perm.p, pl.rhs_b.p, pl.rhs_x.p, R, st, G - 2 * d);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[13], st));
     launch_copy_zp0(ba, st);
-    // up += Top0 [A_0; B_0]: the first 2d rows of the row-major solution, read
-    // column-major as their transpose
-    gemm_batched(gemm(d, R, 2 * d, pl.top0.p, d, (long long)d * 2 * d, false, pl.rhs_x.p, R,
-                      (long long)G * R, true, pl.up.p, d, dR, NO, 1.0, 1.0),
+    // up += Top0 [A_0; B_0]: layer 0's unknowns are the last 2d rows of the
+    // row-major solution (bnd_col), read column-major as their transpose
+    gemm_batched(gemm(d, R, 2 * d, pl.top0.p, d, (long long)d * 2 * d, false,
+                      pl.rhs_x.p + (size_t)(G - 2 * d) * R, R, (long long)G * R, true, pl.up.p, d, dR, NO,
+                      1.0, 1.0),
                  st);
     nl += 2 + (pd.base_type != 0 ? 1 : 0) + lu_rm_launch_count(G) + 2;
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[3], st));

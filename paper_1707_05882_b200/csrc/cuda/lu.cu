@@ -424,7 +424,7 @@ void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatu
 }
 
 void lu_solve_rm(const double* A, int G, int batch, const int* perm, const double* Bin, double* X,
-                 int ncol, cudaStream_t st) {
+                 int ncol, cudaStream_t st, int row_lo) {
     const long long gg = (long long)G * G, gn = (long long)G * ncol;
     {
         const long long total = (long long)batch * gn;
@@ -440,13 +440,16 @@ void lu_solve_rm(const double* A, int G, int batch, const int* perm, const doubl
             rm_gemm(G - k0 - jb, ncol, jb, A + (size_t)(k0 + jb) * G + k0, G, gg, X + (size_t)k0 * ncol,
                     ncol, gn, X + (size_t)(k0 + jb) * ncol, ncol, gn, batch, -1.0, 1.0, st);
     }
+    // back substitution only down to row_lo: the unknowns above it are not
+    // wanted (X rows < row_lo are left holding the forward solution)
     const int nblk = (G + LU_NB - 1) / LU_NB;
-    for (int bk = nblk - 1; bk >= 0; --bk) {
+    const int blo = max(0, row_lo) / LU_NB, rl = blo * LU_NB;
+    for (int bk = nblk - 1; bk >= blo; --bk) {
         const int k0 = bk * LU_NB, jb = min(LU_NB, G - k0);
         trsm_launch<false>(A, G, X, ncol, gn, k0, jb, 0, ncol, batch, st);
-        if (k0 > 0)
-            rm_gemm(k0, ncol, jb, A + k0, G, gg, X + (size_t)k0 * ncol, ncol, gn, X, ncol, gn, batch, -1.0,
-                    1.0, st);
+        if (k0 > rl)
+            rm_gemm(k0 - rl, ncol, jb, A + (size_t)rl * G + k0, G, gg, X + (size_t)k0 * ncol, ncol, gn,
+                    X + (size_t)rl * ncol, ncol, gn, batch, -1.0, 1.0, st);
     }
 }
 
@@ -466,7 +469,7 @@ int lu_rm_launch_count(int G) {
     }
     n += 1;                                          // perm
     const int nblk = (G + LU_NB - 1) / LU_NB;
-    n += 1 + 2 * nblk - 1 + 2 * nblk - 1;            // gather + forward + backward
+    n += 1 + 2 * nblk - 1 + 2 * nblk - 1;            // gather + forward + backward (upper bound)
     return n;
 }
 
