@@ -56,7 +56,7 @@ __global__ void assemble_kernel(BndArgs a) {
     double* A = a.lhs + (size_t)mo * G * G;
     const int ca = bnd_col(p, jj, d, G);       // column A_p(jj)
     const int cbk = bnd_col(p, d + jj, d, G);  // column B_p(jj)
-    auto at = [&](int r, int c) -> double& { return A[(size_t)r * G + c]; };
+    auto at = [&](int r, int c) -> double& { return A[(size_t)bnd_row(r, d, G) * G + c]; };
     if (p == 0) {
         at(i, ca) = pk(dflip(pm, i));
         at(i, cbk) = pk(att * dflip(pp, i));
@@ -138,7 +138,7 @@ __global__ void base_kernel(BndArgs a, int mo) {
     double* A = a.lhs + (size_t)mo * G * G;
     const int col = bnd_col(q, (isb ? d : 0) + jj, d, G);
     const int rb = d + 2 * d * (P - 1);
-    for (int i = lane; i < d; i += 32) A[(size_t)(rb + i) * G + col] -= out[i];
+    for (int i = lane; i < d; i += 32) A[(size_t)bnd_row(rb + i, d, G) * G + col] -= out[i];
 }
 
 // Right-hand sides: warp per (order mo, column = incident*4 + channel).
@@ -154,9 +154,9 @@ __global__ void rhs_kernel(BndArgs a) {
     // row-major [G][R] per order (lu.cu); B(r) = rhs[mo][r * R + col]
     struct RowView {
         double* base;
-        int R;
-        __device__ double& operator[](int r) const { return base[(size_t)r * R]; }
-    } B{a.rhs + (size_t)mo * R * G + col, R};
+        int R, d, G;
+        __device__ double& operator[](int r) const { return base[(size_t)bnd_row(r, d, G) * R]; }
+    } B{a.rhs + (size_t)mo * R * G + col, R, d, G};
     auto zp = [&](int p, int i) {
         const size_t om = (size_t)a.p.medium[p] * a.p.n_orders + mo;
         return a.zp[(om * R + col) * d + i];

@@ -26,16 +26,32 @@ void launch_copy_zp0(const BndArgs& a, cudaStream_t st);
 // lu.cu: batched LU with partial pivoting on ROW-major G x G matrices.
 // ipiv: [batch][G] absolute pivot rows (LAPACK order); perm: [batch][G] net
 // row permutation (row i of P B = row perm[i] of B).
+// prof_d / prof_P > 0: the matrix has the boundary-system staircase profile
+// (bnd_row_end); rows past a column block's profile are skipped.
 void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatus* status,
-                  const int* order_index, cudaStream_t st);
+                  const int* order_index, cudaStream_t st, int prof_d = 0, int prof_P = 0);
 // X = A^-1 B for row-major B, X ([batch][G][ncol]); B is not modified.  Only
 // rows >= row_lo (rounded down to the 64-row block) of X are the solution.
 void lu_solve_rm(const double* A, int G, int batch, const int* perm, const double* B, double* X,
-                 int ncol, cudaStream_t st, int row_lo = 0);
+                 int ncol, cudaStream_t st, int row_lo = 0, int prof_d = 0, int prof_P = 0);
 // Column of the boundary system holding layer p's packed column j: layer 0
 // (the only unknowns the tau = 0 field needs) is ordered LAST, so the back
 // substitution stops after its 2d rows.
 __host__ __device__ inline int bnd_col(int p, int j, int d, int G) { return (2 * d * p + j - 2 * d + G) % G; }
+// Row of boundary equation r (boundary.cpp order: top d, interface p 2d each,
+// bottom d): the top rows -- the only ones touching layer 0 besides interface 0
+// -- are ordered LAST, so the system has a staircase profile: the columns of
+// layer p >= 1 (ordered first) are nonzero only in rows < bnd_row_end.
+__host__ __device__ inline int bnd_row(int r, int d, int G) { return (r - d + G) % G; }
+// First row past the nonzero profile of (reordered) column `col`, P layers.
+__host__ __device__ inline int bnd_row_end(int col, int d, int P) {
+    const int G = 2 * d * P;
+    if (P <= 1) return G;
+    const int b = col / (2 * d);  // column block: b < P-1 is layer b+1, b = P-1 is layer 0
+    if (b >= P - 1) return G;
+    const int p = b + 1;
+    return (p <= P - 2) ? 2 * d * (p + 1) : 2 * d * (P - 1) + d;
+}
 int lu_rm_launch_count(int G);
 
 }  // namespace vrte

@@ -498,9 +498,9 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     launch_bnd_assemble(ba, st);
     launch_bnd_rhs(ba, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[11], st));
-    lu_factor_rm(pl.lhs.p, G, NO, pl.ipiv.p, pl.perm.p, pl.status, pl.order_index.p, st);
+    lu_factor_rm(pl.lhs.p, G, NO, pl.ipiv.p, pl.perm.p, pl.status, pl.order_index.p, st, d, pl.P);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[12], st));
-    lu_solve_rm(pl.lhs.p, G, NO, pl.perm.p, pl.rhs_b.p, pl.rhs_x.p, R, st, G - 2 * d);
+    lu_solve_rm(pl.lhs.p, G, NO, pl.perm.p, pl.rhs_b.p, pl.rhs_x.p, R, st, G - 2 * d, d, pl.P);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[13], st));
     launch_copy_zp0(ba, st);
     // up += Top0 [A_0; B_0]: layer 0's unknowns are the last 2d rows of the

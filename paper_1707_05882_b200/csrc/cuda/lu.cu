@@ -30,7 +30,7 @@ constexpr int SW_TILE = 32;
 // ------------------------------------------------------------------ panel
 template <int NT, int RPT, int PB>
 __global__ void __launch_bounds__(NT) lu_panel_rm_kernel(double* Aall, int G, long long strideA, int k0,
-                                                         int jb, int* ipiv_all, DeviceStatus* status,
+                                                         int jb, int rend, int* ipiv_all, DeviceStatus* status,
                                                          const int* order_index) {
     __shared__ double s_val[NT / 32];
     __shared__ int s_idx[NT / 32];
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(NT) lu_panel_rm_kernel(double* Aall, int G, lo
     const int b = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
     double* A = Aall + (size_t)b * strideA;
     int* ipiv = ipiv_all + (size_t)b * G;
-    const int np = G - k0;
+    const int np = rend - k0;  // rows past the profile end are zero in these columns
     double v[RPT][PB];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
@@ -339,9 +339,9 @@ void rm_gemm(int m, int n, int k, const double* A, long long lda, long long sa, 
 }
 
 template <int NT, int RPT, int PB>
-void panel_launch(double* A, int G, int k0, int jb, int* ipiv, DeviceStatus* status,
+void panel_launch(double* A, int G, int k0, int jb, int rend, int* ipiv, DeviceStatus* status,
                   const int* order_index, int batch, cudaStream_t st) {
-    lu_panel_rm_kernel<NT, RPT, PB><<<batch, NT, 0, st>>>(A, G, (long long)G * G, k0, jb, ipiv, status,
+    lu_panel_rm_kernel<NT, RPT, PB><<<batch, NT, 0, st>>>(A, G, (long long)G * G, k0, jb, rend, ipiv, status,
                                                           order_index);
 }
 
@@ -368,35 +368,37 @@ void trsm_launch(const double* A, int G, double* M, int ld, long long strideM, i
 }  // namespace
 
 void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatus* status,
-                  const int* order_index, cudaStream_t st) {
+                  const int* order_index, cudaStream_t st, int prof_d, int prof_P) {
     if (G > 4096) throw std::invalid_argument("vrte_cuda: boundary system larger than 4096 rows");
     const int PB = panel_width(G);
     // outer block: 128 columns (trailing GEMMs with k = 128), handled by the
     // 64-row swap / TRSM kernels in two halves; VRTE_LU_NB=64 for A/B runs
     static const int OB = std::getenv("VRTE_LU_NB") ? std::atoi(std::getenv("VRTE_LU_NB")) : 128;
     const long long gg = (long long)G * G;
+    auto row_end = [&](int col) { return prof_d > 0 ? min(G, bnd_row_end(col, prof_d, prof_P)) : G; };
     for (int K0 = 0; K0 < G; K0 += OB) {
         const int NBk = min(OB, G - K0);
+        const int rend = row_end(K0 + NBk - 1);  // profile is non-decreasing in the column
         for (int k0 = K0; k0 < K0 + NBk; k0 += PB) {
             const int jb = min(PB, K0 + NBk - k0);
-            const int np = G - k0;
+            const int np = rend - k0;
             if (np <= 256)
-                panel_launch<256, 1, 16>(A, G, k0, jb, ipiv, status, order_index, batch, st);
+                panel_launch<256, 1, 16>(A, G, k0, jb, rend, ipiv, status, order_index, batch, st);
             else if (np <= 512)
-                panel_launch<512, 1, 16>(A, G, k0, jb, ipiv, status, order_index, batch, st);
+                panel_launch<512, 1, 16>(A, G, k0, jb, rend, ipiv, status, order_index, batch, st);
             else if (np <= 1024)
-                panel_launch<1024, 1, 16>(A, G, k0, jb, ipiv, status, order_index, batch, st);
+                panel_launch<1024, 1, 16>(A, G, k0, jb, rend, ipiv, status, order_index, batch, st);
             else if (np <= 2048)
-                panel_launch<512, 4, 8>(A, G, k0, jb, ipiv, status, order_index, batch, st);
+                panel_launch<512, 4, 8>(A, G, k0, jb, rend, ipiv, status, order_index, batch, st);
             else
-                panel_launch<512, 8, 4>(A, G, k0, jb, ipiv, status, order_index, batch, st);
+                panel_launch<512, 8, 4>(A, G, k0, jb, rend, ipiv, status, order_index, batch, st);
             VRTE_CUDA_CHECK(cudaGetLastError());
             const int c_end = K0 + NBk, rest_in = c_end - (k0 + jb);
             swap_launch(A, G, gg, ipiv, G, k0, jb, K0, c_end, k0, k0 + jb, batch, st);
             if (rest_in > 0) {
                 trsm_launch<true>(A, G, A, G, gg, k0, jb, k0 + jb, c_end, batch, st);
-                if (G - k0 - jb > 0)
-                    rm_gemm(G - k0 - jb, rest_in, jb, A + (size_t)(k0 + jb) * G + k0, G, gg,
+                if (rend - k0 - jb > 0)
+                    rm_gemm(rend - k0 - jb, rest_in, jb, A + (size_t)(k0 + jb) * G + k0, G, gg,
                             A + (size_t)k0 * G + k0 + jb, G, gg, A + (size_t)(k0 + jb) * G + k0 + jb, G, gg,
                             batch, -1.0, 1.0, st);
             }
@@ -415,8 +417,11 @@ void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatu
                     rm_gemm(below, rest, rb, A + (size_t)(r0 + rb) * G + r0, G, gg, A + (size_t)r0 * G + K0 + NBk,
                             G, gg, A + (size_t)(r0 + rb) * G + K0 + NBk, G, gg, batch, -1.0, 1.0, st);
             }
-            rm_gemm(rest, rest, NBk, A + (size_t)(K0 + NBk) * G + K0, G, gg, A + (size_t)K0 * G + K0 + NBk,
-                    G, gg, A + (size_t)(K0 + NBk) * G + K0 + NBk, G, gg, batch, -1.0, 1.0, st);
+            // trailing update: rows past the profile have zero multipliers
+            if (rend - K0 - NBk > 0)
+                rm_gemm(rend - K0 - NBk, rest, NBk, A + (size_t)(K0 + NBk) * G + K0, G, gg,
+                        A + (size_t)K0 * G + K0 + NBk, G, gg, A + (size_t)(K0 + NBk) * G + K0 + NBk, G, gg,
+                        batch, -1.0, 1.0, st);
         }
     }
     lu_perm_kernel<<<batch, 256, G * sizeof(int), st>>>(ipiv, perm, G);
@@ -424,7 +429,7 @@ void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatu
 }
 
 void lu_solve_rm(const double* A, int G, int batch, const int* perm, const double* Bin, double* X,
-                 int ncol, cudaStream_t st, int row_lo) {
+                 int ncol, cudaStream_t st, int row_lo, int prof_d, int prof_P) {
     const long long gg = (long long)G * G, gn = (long long)G * ncol;
     {
         const long long total = (long long)batch * gn;
@@ -435,6 +440,10 @@ void lu_solve_rm(const double* A, int G, int batch, const int* perm, const doubl
     }
     for (int k0 = 0; k0 < G; k0 += LU_NB) {
         const int jb = min(LU_NB, G - k0);
+        // (no profile here: later row interchanges move multipliers below the
+        // staircase profile of earlier columns, so L itself is dense)
+        (void)prof_d;
+        (void)prof_P;
         trsm_launch<true>(A, G, X, ncol, gn, k0, jb, 0, ncol, batch, st);
         if (G - k0 - jb > 0)
             rm_gemm(G - k0 - jb, ncol, jb, A + (size_t)(k0 + jb) * G + k0, G, gg, X + (size_t)k0 * ncol,
