@@ -15,6 +15,7 @@
 #include <climits>
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "kernels.cuh"
 
@@ -1258,7 +1259,8 @@ __device__ double warp_dlarfg(double* v, int len, double* beta) {
 
 __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double* Zall, double* wrall,
                                                         double* wiall, int d, DeviceStatus* status,
-                                                        int aed_nw, int nb4_min, int nb2_min, int nibble) {
+                                                        int aed_nw, int nb4_min, int nb2_min, int nibble,
+                                                        double* trace) {
     __shared__ double Wn[MW * LDW];  // window, column-major Wn[c*LDW + r]
     __shared__ double Us[MW * LDW];  // accumulated factor, column-major Us[c*LDW + r]
     __shared__ double Sm[TQ * TQ];  // trailing block for the shifts
@@ -1807,6 +1809,17 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
         atomicAdd(&status->qr_sweeps, nsweep);
         atomicAdd(&status->qr_steps, nstep);
         for (int q = 0; q < 8; ++q) atomicAdd(&status->qr_cycles[q], cyc[q]);
+        if (trace) {  // debug (VRTE_QR_TRACE): per-matrix cost profile
+            double* tr = trace + (size_t)b * 8;
+            tr[0] = (double)(cyc[0] + cyc[1] + cyc[2] + cyc[3]);
+            tr[1] = (double)nstep;
+            tr[2] = (double)nsweep;
+            tr[3] = (double)cyc[7];
+            tr[4] = (double)cyc[6];
+            tr[5] = (double)cyc[2];
+            tr[6] = (double)cyc[3];
+            tr[7] = (double)cyc[4];
+        }
     }
     for (int idx = t; idx < d * d; idx += nt) {
         const int r = idx % d, c = idx / d;
@@ -2522,8 +2535,28 @@ void launch_hqr(double* H, double* Z, double* wr, double* wi, int d, int batch,
         static const int nb4 = std::getenv("VRTE_NB4_MIN") ? std::atoi(std::getenv("VRTE_NB4_MIN")) : 48;
         static const int nb2 = std::getenv("VRTE_NB2_MIN") ? std::atoi(std::getenv("VRTE_NB2_MIN")) : 24;
         static const int nibble = std::getenv("VRTE_NIBBLE") ? std::atoi(std::getenv("VRTE_NIBBLE")) : 40;
+        static const char* trace_path = std::getenv("VRTE_QR_TRACE");
+        static double* trace = nullptr;
+        static int trace_n = 0;
+        if (trace_path && trace_n < batch) {
+            if (trace) cudaFree(trace);
+            VRTE_CUDA_CHECK(cudaMalloc(&trace, sizeof(double) * 8 * batch));
+            trace_n = batch;
+        }
         hqr_multi_kernel<<<batch, 256, 0, st>>>(H, Z, wr, wi, d, status, min(max(aed_nw, 4), MW), nb4, nb2,
-                                                nibble);
+                                                nibble, trace_path ? trace : nullptr);
+        if (trace_path) {
+            std::vector<double> h((size_t)8 * batch);
+            VRTE_CUDA_CHECK(cudaMemcpyAsync(h.data(), trace, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
+            VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
+            if (FILE* f = std::fopen(trace_path, "w")) {
+                std::fprintf(f, "matrix,cycles,reflectors,sweeps,aed_calls,aed_cycles,chase_cycles,update_cycles,aed_deflations\n");
+                for (int q = 0; q < batch; ++q)
+                    std::fprintf(f, "%d,%.0f,%.0f,%.0f,%.0f,%.0f,%.0f,%.0f,%.0f\n", q, h[8 * q], h[8 * q + 1], h[8 * q + 2],
+                                 h[8 * q + 3], h[8 * q + 4], h[8 * q + 5], h[8 * q + 6], h[8 * q + 7]);
+                std::fclose(f);
+            }
+        }
     } else if (std::string(mode) == "window") {
         hqr_window_kernel<<<batch, 256, 0, st>>>(H, Z, wr, wi, d, status);
     } else {
