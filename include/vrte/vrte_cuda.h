@@ -111,6 +111,16 @@ VRTE_API int32_t vrte_cuda_device_count(void);
  * right-hand sides (host arrays, row-major).  Returns 0, 3 (singular) or 5. */
 VRTE_API int32_t vrte_cuda_lu_solve(const double* A, int32_t G, int32_t batch, const double* B,
                                     int32_t ncol, double* X, int32_t device);
+/* Kernel-level check of the blocked Hessenberg reduction (hessenberg.cu):
+ * A[b] = Q[b] H[b] Q[b]^T for `batch` column-major d x d matrices (host arrays).
+ * blocked = 0 selects the unblocked reference kernel. */
+VRTE_API int32_t vrte_cuda_hessenberg(const double* A, int32_t d, int32_t batch, double* H, double* Q,
+                                      int32_t blocked, int32_t device);
+/* Kernel-level check of the eigen stage: real Schur form A[b] = Z T Z^T
+ * (blocked Hessenberg + multishift QR with AED, eig.cu) and the eigenvalues
+ * wr/wi [batch][d].  Returns 0, or 3 if the QR did not converge. */
+VRTE_API int32_t vrte_cuda_schur(const double* A, int32_t d, int32_t batch, double* T, double* Z, double* wr,
+                                 double* wi, int32_t device);
 
 #ifdef __cplusplus
 }

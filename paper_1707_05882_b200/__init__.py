@@ -135,7 +135,7 @@ EXPORTED = [
     "vrte_cuda_brdf", "vrte_cuda_plan_create", "vrte_cuda_plan_run", "vrte_cuda_plan_fetch",
     "vrte_cuda_plan_fetch_up", "vrte_cuda_plan_fetch_modes", "vrte_cuda_plan_fetch_ef",
     "vrte_cuda_plan_destroy",
-    "vrte_cuda_synthesize", "vrte_cuda_device_count", "vrte_cuda_lu_solve",
+    "vrte_cuda_synthesize", "vrte_cuda_device_count", "vrte_cuda_lu_solve", "vrte_cuda_hessenberg", "vrte_cuda_schur",
 ]
 
 
@@ -177,6 +177,8 @@ def lib():
     L.vrte_cuda_plan_destroy.argtypes = [vp]
     L.vrte_cuda_plan_fetch_ef.argtypes = [vp, dp, dp]
     L.vrte_cuda_lu_solve.argtypes = [dp, C.c_int32, C.c_int32, dp, C.c_int32, dp, C.c_int32]
+    L.vrte_cuda_hessenberg.argtypes = [dp, C.c_int32, C.c_int32, dp, dp, C.c_int32, C.c_int32]
+    L.vrte_cuda_schur.argtypes = [dp, C.c_int32, C.c_int32, dp, dp, dp, dp, C.c_int32]
     L.vrte_solve_radiance.argtypes = [vp, C.POINTER(Options), dp, C.c_size_t, C.POINTER(vp)]
     L.vrte_mc_trace.argtypes = [vp, C.POINTER(Options), C.c_uint64, C.c_uint64, C.c_int32,
                                 C.c_int32, C.POINTER(vp)]
@@ -205,6 +207,33 @@ def lu_solve(A, B, device: int = 0) -> np.ndarray:
     if code != 0:
         raise VrteError(code, "vrte_cuda_lu_solve failed (singular or bad arguments)")
     return X
+
+
+def hessenberg(A, blocked: bool = True, device: int = 0):
+    """Kernel-level check of the Hessenberg stage: A [batch, d, d] (row index
+    first) -> (H, Q) with A = Q H Q^T."""
+    A = np.asarray(A, dtype=np.float64)
+    batch, d, _ = A.shape
+    Ac = np.ascontiguousarray(A.transpose(0, 2, 1))  # column-major per matrix
+    H, Q = np.zeros_like(Ac), np.zeros_like(Ac)
+    code = lib().vrte_cuda_hessenberg(_dp(Ac), d, batch, _dp(H), _dp(Q), int(blocked), device)
+    if code != 0:
+        raise VrteError(code, "vrte_cuda_hessenberg failed")
+    return H.transpose(0, 2, 1).copy(), Q.transpose(0, 2, 1).copy()
+
+
+def schur(A, device: int = 0):
+    """Kernel-level check of the eigen stage: A [batch, d, d] -> (T, Z, w) with
+    A = Z T Z^T, T quasi-triangular, w the eigenvalues [batch, d] (complex)."""
+    A = np.asarray(A, dtype=np.float64)
+    batch, d, _ = A.shape
+    Ac = np.ascontiguousarray(A.transpose(0, 2, 1))
+    T, Z = np.zeros_like(Ac), np.zeros_like(Ac)
+    wr, wi = np.zeros((batch, d)), np.zeros((batch, d))
+    code = lib().vrte_cuda_schur(_dp(Ac), d, batch, _dp(T), _dp(Z), _dp(wr), _dp(wi), device)
+    if code != 0:
+        raise VrteError(code, "vrte_cuda_schur: QR did not converge")
+    return T.transpose(0, 2, 1).copy(), Z.transpose(0, 2, 1).copy(), wr + 1j * wi
 
 
 def version() -> str:

@@ -292,6 +292,15 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     launch_build_ef(pd, pl.gsf_n.p, pl.E.p, pl.F.p, st);
     gemm_batched(gemm(d, d, d, pl.F.p, d, dd, false, pl.E.p, d, dd, false, pl.T.p, d, dd, B), st);
     launch_max_abs(pl.T.p, dd, B, pl.femax.p, st);
+    if (const char* dump = std::getenv("VRTE_DUMP_FE")) {  // debug: F E of every (medium, order)
+        std::vector<double> h((size_t)B * dd);
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(h.data(), pl.T.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
+        VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
+        if (FILE* f = std::fopen(dump, "wb")) {
+            std::fwrite(h.data(), sizeof(double), h.size(), f);
+            std::fclose(f);
+        }
+    }
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[5], st));
     static const char* hess_mode = std::getenv("VRTE_HESS");  // blocked (default) | unblocked
     if (hess_mode && std::string(hess_mode) == "unblocked") {
@@ -855,6 +864,72 @@ int32_t vrte_cuda_lu_solve(const double* A, int32_t G, int32_t batch, const doub
         VRTE_CUDA_CHECK(cudaMemcpyAsync(&s, dst.p, sizeof s, cudaMemcpyDeviceToHost, st));
         VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
         cudaStreamDestroy(st);
+        return s.code != 0 ? 3 : 0;
+    } catch (const std::exception&) {
+        return 3;
+    }
+}
+
+int32_t vrte_cuda_hessenberg(const double* A, int32_t d, int32_t batch, double* H, double* Q,
+                             int32_t blocked, int32_t device) {
+    if (!A || !H || !Q || d < 1 || batch < 1) return 5;
+    try {
+        if (device >= 0) VRTE_CUDA_CHECK(cudaSetDevice(device));
+        cudaStream_t st;
+        VRTE_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        const size_t n = (size_t)batch * d * d;
+        DevBuf<double> dA, dQ, work;
+        dA.upload(A, n, st);
+        dQ.alloc(n);
+        work.alloc((size_t)batch * hessenberg_work_doubles(d));
+        if (blocked)
+            launch_hessenberg_blocked(dA.p, dQ.p, work.p, d, batch, st);
+        else
+            launch_hessenberg(dA.p, dQ.p, d, batch, st);
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(H, dA.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(Q, dQ.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
+        cudaStreamDestroy(st);
+        return 0;
+    } catch (const std::exception&) {
+        return 3;
+    }
+}
+
+int32_t vrte_cuda_schur(const double* A, int32_t d, int32_t batch, double* T, double* Z, double* wr,
+                        double* wi, int32_t device) {
+    if (!A || !T || !Z || !wr || !wi || d < 1 || batch < 1) return 5;
+    try {
+        if (device >= 0) VRTE_CUDA_CHECK(cudaSetDevice(device));
+        cudaStream_t st;
+        VRTE_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        const size_t n = (size_t)batch * d * d;
+        DevBuf<double> dA, dZ, work, dwr, dwi;
+        DevBuf<DeviceStatus> dst;
+        dA.upload(A, n, st);
+        dZ.alloc(n);
+        dwr.alloc((size_t)batch * d);
+        dwi.alloc((size_t)batch * d);
+        dst.alloc(1);
+        VRTE_CUDA_CHECK(cudaMemsetAsync(dst.p, 0, sizeof(DeviceStatus), st));
+        static const char* hess_mode = std::getenv("VRTE_HESS");
+        if (hess_mode && std::string(hess_mode) == "unblocked") {
+            launch_hessenberg(dA.p, dZ.p, d, batch, st);
+        } else {
+            work.alloc((size_t)batch * hessenberg_work_doubles(d));
+            launch_hessenberg_blocked(dA.p, dZ.p, work.p, d, batch, st);
+        }
+        launch_hqr(dA.p, dZ.p, dwr.p, dwi.p, d, batch, dst.p, st);
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(T, dA.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(Z, dZ.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(wr, dwr.p, sizeof(double) * batch * d, cudaMemcpyDeviceToHost, st));
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(wi, dwi.p, sizeof(double) * batch * d, cudaMemcpyDeviceToHost, st));
+        DeviceStatus s{};
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(&s, dst.p, sizeof s, cudaMemcpyDeviceToHost, st));
+        VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
+        cudaStreamDestroy(st);
+        if (s.code != 0 && std::getenv("VRTE_DEBUG"))
+            std::fprintf(stderr, "vrte_cuda_schur: code %d matrix %d I=%g L=%g\n", s.code, s.index, s.value, s.value2);
         return s.code != 0 ? 3 : 0;
     } catch (const std::exception&) {
         return 3;

@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(256) hqr_kernel(double* Hall, double* Zall, do
             }
         }
         if (!conv) {
-            if (t == 0) report_failure(status, kFailHqrNoConverge, 1, b, (double)I);
+            if (t == 0) report_failure(status, kFailHqrNoConverge, 1, b, (double)I, (double)L);
             failed = true;
             break;
         }
@@ -500,6 +500,40 @@ __global__ void __launch_bounds__(256) hqr_kernel(double* Hall, double* Zall, do
 // reflectors one by one, but no block barrier and no L2 round trip per step.
 constexpr int QW_STEPS = 12;
 constexpr int QW = QW_STEPS + 4;  // window width
+
+
+// dlarfg for a 2/3-element bulge column: one rsqrt and one reciprocal.  As in
+// LAPACK the reflector is the identity only when v2 = v3 = 0 exactly; when
+// their squares underflow against v1 it is the tau = 2 sign flip (dlarfg's
+// result) -- treating it as the identity stalls the chase on graded matrices
+// whose converging subdiagonals reach ~1e-180.  Columns whose entries could
+// under/overflow in the squares are rescaled by a power of two.  Returns
+// tau; v2, v3 become the reflector tail, beta the new head.
+__device__ inline double house3(double v1, double& v2, double& v3, double& beta) {
+    beta = v1;
+    if (v2 == 0.0 && v3 == 0.0) return 0.0;
+    double x2 = fma(v2, v2, v3 * v3);
+    double ss = fma(v1, v1, x2);
+    double sc = 1.0;
+    if (!(ss > 0x1p-900 && ss < 0x1p900)) {  // rare: the whole column under/overflows
+        const int e = ilogb(fmax(fabs(v1), fmax(fabs(v2), fabs(v3))));
+        sc = scalbn(1.0, e);
+        const double inv = scalbn(1.0, -e);
+        v1 *= inv;
+        v2 *= inv;
+        v3 *= inv;
+        x2 = fma(v2, v2, v3 * v3);
+        ss = fma(v1, v1, x2);
+    }
+    const double rq = rsqrt(ss);
+    const double nv = ss * rq;
+    const double av1 = fabs(v1);
+    const double r = copysign(__drcp_rn(av1 + nv), v1);
+    v2 *= r;
+    v3 *= r;
+    beta = -copysign(nv, v1) * sc;
+    return fma(av1, rq, 1.0);
+}
 
 __device__ inline double hg(const double* H, int d, int r, int c) { return H[r + (size_t)c * d]; }
 
@@ -672,25 +706,9 @@ __global__ void __launch_bounds__(256) hqr_window_kernel(double* Hall, double* Z
                             v3 = (nr == 3) ? v0[2] : 0.0;
                         }
                         if (nr != 3) v3 = 0.0;
-                        double t1 = 0.0;
-                        {
-                            // dlarfg with one sqrt and two independent reciprocals (the
-                            // bulge entries are O(1): no dlapy2 overflow scaling needed)
-                            const double x2 = fma(v2, v2, v3 * v3);
-                            if (x2 != 0.0) {
-                                // beta = -sign(v1) |v|, 1/beta = -sign(v1) rsqrt(|v|^2),
-                                // t1 = 1 + |v1|/|v|, scale = sign(v1) / (|v1| + |v|)
-                                const double ss = fma(v1, v1, x2);
-                                const double rq = rsqrt(ss);
-                                const double nv = ss * rq;
-                                const double av1 = fabs(v1);
-                                const double sc = copysign(__drcp_rn(av1 + nv), v1);
-                                t1 = fma(av1, rq, 1.0);
-                                v2 *= sc;
-                                v3 *= sc;
-                                v1 = -copysign(nv, v1);
-                            }
-                        }
+                        double bt;
+                        const double t1 = house3(v1, v2, v3, bt);
+                        v1 = bt;
                         const double t2 = t1 * v2, t3 = t1 * v3;
                         __syncwarp();
                         // row op: rows k..k+nr-1, columns k..whi (in window)
@@ -780,7 +798,7 @@ __global__ void __launch_bounds__(256) hqr_window_kernel(double* Hall, double* Z
             }
         }
         if (!conv) {
-            if (t == 0) report_failure(status, kFailHqrNoConverge, 1, b, (double)I);
+            if (t == 0) report_failure(status, kFailHqrNoConverge, 1, b, (double)I, (double)L);
             return;
         }
         if (L == I) {
@@ -958,17 +976,9 @@ __device__ void warp_tiny_eig(double* S, int n, double* sr, double* si) {
                     v2 = A(k + 1, k - 1);
                     v3 = nr == 3 ? A(k + 2, k - 1) : 0.0;
                 }
-                double t1 = 0.0;
-                const double x2 = v2 * v2 + v3 * v3;
-                if (x2 != 0.0) {
-                    const double nv = sqrt(v1 * v1 + x2);
-                    const double beta = -copysign(nv, v1);
-                    t1 = (beta - v1) / beta;
-                    const double sc = 1.0 / (v1 - beta);
-                    v2 *= sc;
-                    v3 *= sc;
-                    v1 = beta;
-                }
+                double bt;
+                const double t1 = house3(v1, v2, v3, bt);
+                v1 = bt;
                 const double t2 = t1 * v2, t3 = t1 * v3;
                 __syncwarp();
                 const int c = k + lane;
@@ -1115,19 +1125,9 @@ __device__ bool warp_small_schur(double* T, double* V, int n, double* sr, double
                     v2 = A(k + 1, k - 1);
                     v3 = nr == 3 ? A(k + 2, k - 1) : 0.0;
                 }
-                double t1 = 0.0;
-                const double x2 = fma(v2, v2, v3 * v3);
-                if (x2 != 0.0) {
-                    const double ss = fma(v1, v1, x2);
-                    const double rq = rsqrt(ss);
-                    const double nv = ss * rq;
-                    const double av1 = fabs(v1);
-                    const double sc = copysign(__drcp_rn(av1 + nv), v1);
-                    t1 = fma(av1, rq, 1.0);
-                    v2 *= sc;
-                    v3 *= sc;
-                    v1 = -copysign(nv, v1);
-                }
+                double bt;
+                const double t1 = house3(v1, v2, v3, bt);
+                v1 = bt;
                 const double t2 = t1 * v2, t3 = t1 * v3;
                 __syncwarp();
                 const int c = k + lane;
@@ -1683,19 +1683,7 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
                                 v2 = vv[1];
                                 v3 = (nr == 3) ? vv[2] : 0.0;
                             }
-                            beta = v1;
-                            const double x2 = fma(v2, v2, v3 * v3);
-                            if (x2 != 0.0) {
-                                const double ss = fma(v1, v1, x2);
-                                const double rq = rsqrt(ss);
-                                const double nv = ss * rq;
-                                const double av1 = fabs(v1);
-                                const double sc = copysign(__drcp_rn(av1 + nv), v1);
-                                t1 = fma(av1, rq, 1.0);
-                                v2 *= sc;
-                                v3 *= sc;
-                                beta = -copysign(nv, v1);
-                            }
+                            t1 = house3(v1, v2, v3, beta);
                             const double t2 = t1 * v2, t3 = t1 * v3;
                             __syncwarp();
                             for (int c = k + lane; c <= whi; c += 32) {
@@ -1758,7 +1746,7 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
             }
         }
         if (!conv) {
-            if (t == 0) report_failure(status, kFailHqrNoConverge, 1, b, (double)I);
+            if (t == 0) report_failure(status, kFailHqrNoConverge, 1, b, (double)I, (double)L);
             return;
         }
         if (L == I) {

@@ -37,3 +37,55 @@ def test_row_major_lu_reports_singular():
     A = np.zeros((1, 8, 8))
     with pytest.raises(V.VrteError):
         V.lu_solve(A, np.ones((1, 8, 1)))
+
+
+@pytest.mark.parametrize("d,batch", [(4, 2), (32, 3), (100, 2), (256, 3), (512, 2), (520, 1)])
+@pytest.mark.parametrize("blocked", [True, False])
+def test_hessenberg_reduction(d, batch, blocked):
+    rng = np.random.default_rng(d + batch)
+    # graded like F E (row/column scales 1 .. 1e6)
+    sc = np.exp(rng.uniform(0, 14, d))
+    A = rng.standard_normal((batch, d, d)) * sc[None, :, None] * 1e-3 + np.diag(sc)[None]
+    H, Q = V.hessenberg(A, blocked)
+    for b in range(batch):
+        nrm = np.abs(A[b]).max()
+        assert np.abs(np.tril(H[b], -2)).max() == 0.0
+        assert np.abs(Q[b].T @ Q[b] - np.eye(d)).max() < 1e-13 * d
+        assert np.abs(Q[b] @ H[b] @ Q[b].T - A[b]).max() < 1e-14 * d * nrm
+
+
+@pytest.mark.parametrize("d,batch", [(16, 4), (64, 3), (256, 2)])
+def test_schur_form_of_graded_matrices(d, batch):
+    rng = np.random.default_rng(7 * d + batch)
+    sc = np.exp(rng.uniform(0, 14, d))  # graded like F E (1 .. 1e6)
+    A = rng.standard_normal((batch, d, d)) * 1e-2 * np.sqrt(sc[None, :, None] * sc[None, None, :]) + np.diag(sc)[None]
+    T, Z, lam = V.schur(A)
+    for b in range(batch):
+        nrm = np.abs(A[b]).max()
+        assert np.abs(np.tril(T[b], -2)).max() == 0.0
+        assert np.abs(Z[b].T @ Z[b] - np.eye(d)).max() < 1e-13 * d
+        assert np.abs(Z[b] @ T[b] @ Z[b].T - A[b]).max() < 1e-14 * d * nrm
+        ref = np.sort_complex(np.linalg.eigvals(A[b]))
+        got = np.sort_complex(lam[b])
+        assert np.abs(got - ref).max() < 1e-12 * nrm
+
+
+def test_qr_converges_through_underflowing_bulge():
+    # Trailing 3x3 block with a repeated diagonal entry and a subdiagonal of
+    # 1e-182: the Ahues-Kressner test cannot deflate it (bb = 0), so the QR
+    # sweep must keep chasing a bulge whose squared entries underflow
+    # (LAPACK dlarfg: tau = 2 sign flip, not the identity).  This stalled the
+    # round-1 kernels on a C4 order (m = 151, d = 512).
+    d = 12
+    H = np.triu(np.random.default_rng(3).standard_normal((d, d))) * 1e-3 + np.diag(np.linspace(2.0, 8.0, d))
+    for k in range(1, d):
+        H[k, k - 1] = 1e-3
+    a = 1.000175
+    H[d - 2, d - 2] = H[d - 1, d - 1] = a
+    H[d - 2, d - 1] = 2.8e-33
+    H[d - 1, d - 2] = -3.0e-182
+    T, Z, lam = V.schur(H[None])
+    assert np.isfinite(T).all()
+    assert np.abs(Z[0] @ T[0] @ Z[0].T - H).max() < 1e-13
+    ref = np.sort_complex(np.linalg.eigvals(H))
+    assert np.abs(np.sort_complex(lam[0]) - ref).max() < 1e-12
