@@ -174,3 +174,22 @@ def test_determinism_and_order_sharding_c3():
             orders = list(range(rank, 64, world))
             p = V.Plan(mat, V.options(64), mu, 19, m_begin=rank, m_stride=world, n_orders=len(orders))
             assert np.array_equal(p.up(), up_full[orders])
+
+
+def test_c4_is_rejected_like_the_reference():
+    """SURVEY §8(d) C4 (G(0.9,256), omega 0.99, N=128) is not a physical phase
+    matrix for the generator's fixed polarization ratios: F E has negative real
+    eigenvalues at m = 0, 1, 2 (numpy/LAPACK: -0.0166065, -0.0128605,
+    -0.0255097), so the reference throws homogeneous.cpp:177-181.  The drop-in
+    must fail the same way, with the same text (and not with a QR failure)."""
+    import re
+    w = M.config("C4")
+    nodes, _ = O.quadrature(w.N)
+    with pytest.raises(V.VrteError) as ei:
+        gpu_table(w.material, w.N, nodes[:2], 5)
+    msg = str(ei.value)
+    assert ei.value.code == 3
+    m = re.search(r"eigenvalue on the negative real axis at order m = (\d) \(lambda = (-[0-9.e-]+)\)", msg)
+    assert m, msg
+    expect = {0: -0.0166065, 1: -0.0128605, 2: -0.0255097}
+    assert float(m.group(2)) == pytest.approx(expect[int(m.group(1))], rel=1e-5)
