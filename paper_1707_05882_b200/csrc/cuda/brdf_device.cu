@@ -12,6 +12,7 @@
 //                                                every (incident, channel) a RHS
 //   nodal_components/value    pipeline.cpp:201-220 + brdf.cpp:100-117 -> S
 // Everything for one shape lives in a plan whose buffers are reused.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -97,6 +98,7 @@ struct vrte_cuda_plan {
     int Lc = 0;
     int N = 0, L = 0, P = 0, S = 0, n_in = 0, n_dphi = 0, NO = 0, m_begin = 0, m_stride = 1;
     int d = 0, R = 0, G = 0, B = 0;
+    int Be = 0;  // slots [0, Be) run the eigen pipeline, [Be, B) are free-streaming (analytic)
     bool full_orders = true;
     ProblemDev pd{};
     // inputs
@@ -180,6 +182,23 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pl.R = 4 * pl.n_in;
     pl.G = 2 * pl.d * pl.P;
     pl.B = pl.S * pl.NO;
+    {
+        // trailing free-streaming orders of the last medium: zero kernel for
+        // m >= its last nonzero expansion coefficient (or omega = 0)
+        const int s = pl.S - 1;
+        int lc = 0;
+        if (p->omega[s] != 0.0)
+            for (int l = 0; l < pl.Lc; ++l)
+                for (int q = 0; q < 6; ++q)
+                    if (p->greek[((size_t)s * pl.Lc + l) * 6 + q] != 0.0) lc = l + 1;
+        int tail = 0;
+        for (int mo = pl.NO - 1; mo >= 0; --mo) {
+            if (pl.m_begin + mo * pl.m_stride < lc) break;
+            ++tail;
+        }
+        pl.Be = std::max(1, pl.B - tail);  // at least one slot through the pipeline (no empty launches)
+        if (std::getenv("VRTE_NO_FREE_ORDERS")) pl.Be = pl.B;
+    }
     const int N = pl.N, L = pl.L, d = pl.d, R = pl.R, G = pl.G, B = pl.B, NO = pl.NO;
     cudaStream_t st = pl.st;
 
@@ -279,7 +298,8 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
 
 // The device pipeline; returns the number of kernel launches issued.
 uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
-    const int N = pl.N, L = pl.L, d = pl.d, R = pl.R, G = pl.G, B = pl.B, NO = pl.NO;
+    const int N = pl.N, L = pl.L, d = pl.d, R = pl.R, G = pl.G, NO = pl.NO;
+    const int B = pl.Be;  // eigen / particular batch (free-streaming slots filled analytically)
     const long long dd = (long long)d * d, dR = (long long)d * R;
     cudaStream_t st = pl.st;
     const ProblemDev& pd = pl.pd;
@@ -487,6 +507,8 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
         nl += 6;
     }
     launch_zpm(pa, st);
+    launch_free_modes(d, pl.Be, pl.B, pl.mdiag.p, pl.psi_p.p, pl.psi_m.p, pl.nu.p, pl.wr.p, pl.wi.p,
+                      pl.residual.p, pl.zp.p, pl.zm.p, R, st);
     launch_part_residual(pa, st);
     nl += 11;
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[2], st));

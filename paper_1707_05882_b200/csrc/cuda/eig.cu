@@ -2496,6 +2496,43 @@ __global__ void eig_diag_solve_kernel(double* Wall, int d, int ncol, long long w
     }
 }
 
+// Free-streaming orders: for m >= the last coefficient of a medium (or
+// omega = 0) the azimuthal kernel vanishes identically, E = F = M^-1 and
+// F E = M^-2.  Its modes are analytic -- x = e_j, lambda = 1/mu^2, nu = mu,
+// psi+ = (1/2) M^-1 (x - nu E x) = 0, psi- = M^-1 x -- and the beam source (and
+// so the particular solution) is zero (particular.cpp "max|X| = 0").  Slots
+// [b0, b1) are filled directly instead of running the eigen pipeline.
+__global__ void free_modes_kernel(int d, int b0, int b1, const double* mdiag, double* psi_p,
+                                  double* psi_m, double* nu, double* wr, double* wi, double* residual,
+                                  double* zp, double* zm, int R) {
+    const long long per = (long long)d * d;
+    const long long total = (long long)(b1 - b0) * per;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int b = b0 + (int)(e / per);
+        const long long w = e % per;
+        const int i = (int)(w % d), j = (int)(w / d);
+        const size_t o = (size_t)b * per + w;
+        psi_p[o] = 0.0;
+        psi_m[o] = (i == j) ? 1.0 / mdiag[j] : 0.0;
+        if (i == 0) {
+            const size_t vb = (size_t)b * d + j;
+            nu[2 * vb] = mdiag[j];
+            nu[2 * vb + 1] = 0.0;
+            wr[vb] = 1.0 / (mdiag[j] * mdiag[j]);
+            wi[vb] = 0.0;
+            residual[vb] = 0.0;
+        }
+    }
+    const long long tz = (long long)(b1 - b0) * d * R;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tz;
+         e += (long long)gridDim.x * blockDim.x) {
+        const size_t o = (size_t)b0 * d * R + e;
+        zp[o] = 0.0;
+        zm[o] = 0.0;
+    }
+}
+
 }  // namespace
 
 void launch_max_abs(const double* A, long long per, int batch, double* out, cudaStream_t st) {
@@ -2638,6 +2675,17 @@ void launch_set_identity(double* Z, int d, int batch, cudaStream_t st) {
     const long long total = (long long)d * d * batch;
     const long long blocks = (total + 255) / 256;
     set_identity_batched_kernel<<<(unsigned)(blocks < 8192 ? blocks : 8192), 256, 0, st>>>(Z, d, total);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_free_modes(int d, int b0, int b1, const double* mdiag, double* psi_p, double* psi_m,
+                       double* nu, double* wr, double* wi, double* residual, double* zp, double* zm, int R,
+                       cudaStream_t st) {
+    if (b1 <= b0) return;
+    const long long total = (long long)(b1 - b0) * d * d;
+    const long long blocks = (total + 255) / 256;
+    free_modes_kernel<<<(unsigned)(blocks < 8192 ? blocks : 8192), 256, 0, st>>>(d, b0, b1, mdiag, psi_p, psi_m, nu,
+                                                                               wr, wi, residual, zp, zm, R);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
