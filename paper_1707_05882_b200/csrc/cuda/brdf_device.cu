@@ -941,7 +941,12 @@ int32_t vrte_cuda_schur(const double* A, int32_t d, int32_t batch, double* T, do
             work.alloc((size_t)batch * hessenberg_work_doubles(d));
             launch_hessenberg_blocked(dA.p, dZ.p, work.p, d, batch, st);
         }
+        cudaEvent_t e0, e1;
+        VRTE_CUDA_CHECK(cudaEventCreate(&e0));
+        VRTE_CUDA_CHECK(cudaEventCreate(&e1));
+        VRTE_CUDA_CHECK(cudaEventRecord(e0, st));
         launch_hqr(dA.p, dZ.p, dwr.p, dwi.p, d, batch, dst.p, st);
+        VRTE_CUDA_CHECK(cudaEventRecord(e1, st));
         VRTE_CUDA_CHECK(cudaMemcpyAsync(T, dA.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
         VRTE_CUDA_CHECK(cudaMemcpyAsync(Z, dZ.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
         VRTE_CUDA_CHECK(cudaMemcpyAsync(wr, dwr.p, sizeof(double) * batch * d, cudaMemcpyDeviceToHost, st));
@@ -950,6 +955,13 @@ int32_t vrte_cuda_schur(const double* A, int32_t d, int32_t batch, double* T, do
         VRTE_CUDA_CHECK(cudaMemcpyAsync(&s, dst.p, sizeof s, cudaMemcpyDeviceToHost, st));
         VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
         cudaStreamDestroy(st);
+        if (std::getenv("VRTE_DEBUG")) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            std::fprintf(stderr, "vrte_cuda_schur: QR %.3f ms (batch %d, d %d)\n", ms, batch, d);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
         if (s.code != 0 && std::getenv("VRTE_DEBUG"))
             std::fprintf(stderr, "vrte_cuda_schur: code %d matrix %d I=%g L=%g\n", s.code, s.index, s.value, s.value2);
         return s.code != 0 ? 3 : 0;
