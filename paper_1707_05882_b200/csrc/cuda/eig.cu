@@ -1262,7 +1262,8 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
                                                         int aed_nw, int nb4_min, int nb2_min, int nibble,
                                                         double* trace) {
     __shared__ double Wn[MW * LDW];  // window, column-major Wn[c*LDW + r]
-    __shared__ double Us[MW * LDW];  // accumulated factor, column-major Us[c*LDW + r]
+    __shared__ double Us2[2 * MW * LDW];  // chunk factors (double buffered), column-major [c*LDW + r]
+    double* const Us = Us2;               // buffer 0: AED factor / first chunk
     __shared__ double Sm[TQ * TQ];  // trailing block for the shifts
     __shared__ double s_sr[TQ], s_si[TQ];
     __shared__ double s_pr[4 * MB_MAX];  // shift pair per bulge: rt1r rt1i rt2r rt2i
@@ -1296,22 +1297,28 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
     // above it / of Z) mapped to v^T U, so tiles of 8 vectors are one
     // [8 x 32] x [32 x 32] product on the FP64 tensor cores: warp per tile,
     // U's B fragments held in registers for the whole call (DMMA m8n8k4).
-    auto apply_u = [&](int wlo, int whi, int nw) {
-        const int n_right = d - 1 - whi, n_above = wlo;
-        const int tr = (n_right + 7) / 8, ta = (n_above + 7) / 8, tz = (d + 7) / 8;
+    // Apply the chunk factor U (nw x nw, identity beyond) to H columns [c_lo, c_hi)
+    // right of the window (U^T x), and -- if above_z -- to the rows of H above the
+    // window and to Z (x U).  Every target is a vector v mapped to v^T U, so
+    // tiles of 8 vectors are one [8 x 32] x [32 x 32] product on the FP64 tensor
+    // cores: warp per tile (gw-th of gsize warps), U's B fragments in registers.
+    auto apply_part = [&](const double* U, int wlo, int whi, int nw, int c_lo, int c_hi, bool above_z, int gw,
+                          int gsize) {
+        const int n_right = max(0, c_hi - c_lo), n_above = above_z ? wlo : 0;
+        const int tr = (n_right + 7) / 8, ta = (n_above + 7) / 8, tz = above_z ? (d + 7) / 8 : 0;
         const int gq = lane >> 2, tq = lane & 3;
         double bf[8][4];
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
 #pragma unroll
-            for (int cb = 0; cb < 4; ++cb) bf[ks][cb] = Us[(cb * 8 + gq) * LDW + ks * 4 + tq];
+            for (int cb = 0; cb < 4; ++cb) bf[ks][cb] = U[(cb * 8 + gq) * LDW + ks * 4 + tq];
         // vector gq of a tile: base pointer and element stride
         auto locate = [&](int tile, double*& base, long long& st) -> bool {
             if (tile < tr) {
-                const int c = whi + 1 + tile * 8 + gq;
+                const int c = c_lo + tile * 8 + gq;
                 base = H + (size_t)min(c, d - 1) * d + wlo;
                 st = 1;
-                return c < d;
+                return c < c_hi;
             } else if (tile < tr + ta) {
                 const int r = (tile - tr) * 8 + gq;
                 base = H + min(r, n_above - 1) + (size_t)wlo * d;
@@ -1323,13 +1330,13 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
             st = d;
             return r < d;
         };
-        const int ntile = tr + ta + tz, wstep = nt / 32;
+        const int ntile = tr + ta + tz, wstep = gsize;
         double an[8];
         double* bnext = H;
         long long snext = 1;
         bool oknext = false;
-        if (warp < ntile) {
-            oknext = locate(warp, bnext, snext);
+        if (gw < ntile) {
+            oknext = locate(gw, bnext, snext);
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
                 const int q = ks * 4 + tq;
@@ -1338,7 +1345,7 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
         }
         // software pipeline: the next tile's vector segments are in flight while
         // the current tile is multiplied and stored
-        for (int tile = warp; tile < ntile; tile += wstep) {
+        for (int tile = gw; tile < ntile; tile += wstep) {
             double af[8];
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) af[ks] = an[ks];
@@ -1573,7 +1580,7 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
                         H[(kwtop + r) + (size_t)(kwtop + c) * d] = (r <= c + 1) ? Wn[c * LDW + r] : 0.0;
                     }
                     if (t == 0) H[kwtop + (size_t)(kwtop - 1) * d] = sspike * Us[0];
-                    apply_u(kwtop, I, nwin);
+                    apply_part(Us, kwtop, I, nwin, I + 1, d, true, warp, nt / 32);
                     __syncthreads();
                     cyc[4] += (unsigned long long)s_aed[1];  // AED deflations
                 }
@@ -1643,107 +1650,144 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
             nstep += (unsigned long long)(I - M) * nb;
             if (nb > 1) cyc[5] += (unsigned long long)(I - M) * nb;
             tick(0);
-            for (int s0 = 0; s0 < S_total; s0 += MS) {
-                const int s1 = min(s0 + MS, S_total);
+            // Chunks of MS chase steps.  Warps 0-3 ("chasers") load the window, chase
+            // the bulges (warps 0..nb-1), write the window back and apply the chunk
+            // factor U_c to the few columns the NEXT window will read; warps 4-7
+            // ("updaters") apply U_c to the rest of H and to Z while the chasers
+            // already work on chunk c+1.  Named barriers: 1 = U_c published
+            // (chasers arrive, updaters wait), 2 = rest of U_c done (updaters
+            // arrive, chasers wait before touching columns it covers), 3 = chaser
+            // group, 4 = chase steps.  U is double buffered.
+            const int nchunk = (S_total + MS - 1) / MS;
+            auto geom = [&](int c, int& wlo, int& whi) {
+                const int s0 = c * MS, s1 = min(s0 + MS, S_total);
                 const int kmin = max(M, M + s0 - 3 * (nb - 1));
                 const int kmax = min(I - 1, M + s1 - 1);
-                const int wlo = (kmin > M) ? kmin - 1 : M;
-                const int whi = min(kmax + 3, I);
-                const int nw = whi - wlo + 1;
-                for (int idx = t; idx < MW * MW; idx += nt) {
-                    const int r = idx % MW, c = idx / MW;
-                    Wn[r + c * LDW] = (r < nw && c < nw) ? H[(wlo + r) + (size_t)(wlo + c) * d] : 0.0;
-                    Us[r + c * LDW] = (r == c) ? 1.0 : 0.0;
-                }
-                __syncthreads();
-                tick(1);
-                if (warp < nb) {
-                    auto W = [&](int r, int c) -> double& { return Wn[(c - wlo) * LDW + (r - wlo)]; };
-                    const int bb = warp;
-                    for (int s = s0; s < s1; ++s) {
-                        const int k = M + s - 3 * bb;
-                        const bool active = k >= M && k <= I - 1;
-                        const int nr = active ? min(3, I - k + 1) : 0;
-                        double v2 = 0.0, v3 = 0.0, t1 = 0.0, beta = 0.0;
-                        if (active) {
-                            double v1;
-                            if (k > M) {
-                                v1 = W(k, k - 1);
-                                v2 = W(k + 1, k - 1);
-                                v3 = (nr == 3) ? W(k + 2, k - 1) : 0.0;
-                            } else if (nb == 1) {
-                                v1 = v0[0];
-                                v2 = v0[1];
-                                v3 = (nr == 3) ? v0[2] : 0.0;
-                            } else {
-                                double vv[3];
-                                start_vector_g(Wn, LDW, M - wlo, s_pr[4 * bb], s_pr[4 * bb + 1],
-                                               s_pr[4 * bb + 2], s_pr[4 * bb + 3], vv);
-                                v1 = vv[0];
-                                v2 = vv[1];
-                                v3 = (nr == 3) ? vv[2] : 0.0;
-                            }
-                            t1 = house3(v1, v2, v3, beta);
-                            const double t2 = t1 * v2, t3 = t1 * v3;
-                            __syncwarp();
-                            for (int c = k + lane; c <= whi; c += 32) {
-                                double& a0 = W(k, c);
-                                double& a1 = W(k + 1, c);
-                                const double a2v = (nr == 3) ? W(k + 2, c) : 0.0;
-                                const double sum = a0 + v2 * a1 + v3 * a2v;
-                                a0 -= sum * t1;
-                                a1 -= sum * t2;
-                                if (nr == 3) W(k + 2, c) = a2v - sum * t3;
-                            }
-                            __syncwarp();
-                            if (lane == 0) {
+                wlo = (kmin > M) ? kmin - 1 : M;
+                whi = min(kmax + 3, I);
+            };
+            if (warp < 4) {
+                const int tg = t;  // 0..127
+                for (int c = 0; c < nchunk; ++c) {
+                    const int s0 = c * MS, s1 = min(s0 + MS, S_total);
+                    int wlo, whi;
+                    geom(c, wlo, whi);
+                    const int nw = whi - wlo + 1;
+                    double* Uc = Us2 + (c & 1) * (MW * LDW);
+                    for (int idx = tg; idx < MW * MW; idx += 128) {
+                        const int r = idx % MW, cc = idx / MW;
+                        Wn[r + cc * LDW] = (r < nw && cc < nw) ? H[(wlo + r) + (size_t)(wlo + cc) * d] : 0.0;
+                        Uc[r + cc * LDW] = (r == cc) ? 1.0 : 0.0;
+                    }
+                    named_bar(3, 128);
+                    if (t == 0) tick(1);
+                    if (warp < nb) {
+                        auto W = [&](int r, int cc) -> double& { return Wn[(cc - wlo) * LDW + (r - wlo)]; };
+                        const int bb = warp;
+                        for (int s = s0; s < s1; ++s) {
+                            const int k = M + s - 3 * bb;
+                            const bool active = k >= M && k <= I - 1;
+                            const int nr = active ? min(3, I - k + 1) : 0;
+                            double v2 = 0.0, v3 = 0.0, t1 = 0.0, beta = 0.0;
+                            if (active) {
+                                double v1;
                                 if (k > M) {
-                                    W(k, k - 1) = beta;
-                                    W(k + 1, k - 1) = 0.0;
-                                    if (k < I - 1) W(k + 2, k - 1) = 0.0;
+                                    v1 = W(k, k - 1);
+                                    v2 = W(k + 1, k - 1);
+                                    v3 = (nr == 3) ? W(k + 2, k - 1) : 0.0;
                                 } else if (nb == 1) {
-                                    s_t1 = t1;  // H(M, M-1) *= (1 - t1) after the chunk
+                                    v1 = v0[0];
+                                    v2 = v0[1];
+                                    v3 = (nr == 3) ? v0[2] : 0.0;
+                                } else {
+                                    double vv[3];
+                                    start_vector_g(Wn, LDW, M - wlo, s_pr[4 * bb], s_pr[4 * bb + 1],
+                                                   s_pr[4 * bb + 2], s_pr[4 * bb + 3], vv);
+                                    v1 = vv[0];
+                                    v2 = vv[1];
+                                    v3 = (nr == 3) ? vv[2] : 0.0;
+                                }
+                                t1 = house3(v1, v2, v3, beta);
+                                const double t2 = t1 * v2, t3 = t1 * v3;
+                                __syncwarp();
+                                for (int cc = k + lane; cc <= whi; cc += 32) {
+                                    double& a0 = W(k, cc);
+                                    double& a1 = W(k + 1, cc);
+                                    const double a2v = (nr == 3) ? W(k + 2, cc) : 0.0;
+                                    const double sum = a0 + v2 * a1 + v3 * a2v;
+                                    a0 -= sum * t1;
+                                    a1 -= sum * t2;
+                                    if (nr == 3) W(k + 2, cc) = a2v - sum * t3;
+                                }
+                                __syncwarp();
+                                if (lane == 0) {
+                                    if (k > M) {
+                                        W(k, k - 1) = beta;
+                                        W(k + 1, k - 1) = 0.0;
+                                        if (k < I - 1) W(k + 2, k - 1) = 0.0;
+                                    } else if (nb == 1) {
+                                        s_t1 = t1;  // H(M, M-1) *= (1 - t1) after the chunk
+                                    }
                                 }
                             }
-                        }
-                        named_bar(1, nb * 32);
-                        if (active) {
-                            const double t2 = t1 * v2, t3 = t1 * v3;
-                            const int rmax = (nr == 3) ? min(k + 3, I) : I;
-                            for (int r = wlo + lane; r <= rmax && r <= whi; r += 32) {
-                                double& a0 = W(r, k);
-                                double& a1 = W(r, k + 1);
-                                const double a2v = (nr == 3) ? W(r, k + 2) : 0.0;
-                                const double sum = a0 + v2 * a1 + v3 * a2v;
-                                a0 -= sum * t1;
-                                a1 -= sum * t2;
-                                if (nr == 3) W(r, k + 2) = a2v - sum * t3;
+                            named_bar(4, nb * 32);
+                            if (active) {
+                                const double t2 = t1 * v2, t3 = t1 * v3;
+                                const int rmax = (nr == 3) ? min(k + 3, I) : I;
+                                for (int r = wlo + lane; r <= rmax && r <= whi; r += 32) {
+                                    double& a0 = W(r, k);
+                                    double& a1 = W(r, k + 1);
+                                    const double a2v = (nr == 3) ? W(r, k + 2) : 0.0;
+                                    const double sum = a0 + v2 * a1 + v3 * a2v;
+                                    a0 -= sum * t1;
+                                    a1 -= sum * t2;
+                                    if (nr == 3) W(r, k + 2) = a2v - sum * t3;
+                                }
+                                const int cu = k - wlo;
+                                for (int r = lane; r < nw; r += 32) {
+                                    double* u = Uc + r;
+                                    const double u0 = u[cu * LDW], u1 = u[(cu + 1) * LDW];
+                                    const double u2 = (nr == 3) ? u[(cu + 2) * LDW] : 0.0;
+                                    const double sum = u0 + v2 * u1 + v3 * u2;
+                                    u[cu * LDW] = u0 - sum * t1;
+                                    u[(cu + 1) * LDW] = u1 - sum * t2;
+                                    if (nr == 3) u[(cu + 2) * LDW] = u2 - sum * t3;
+                                }
                             }
-                            const int c = k - wlo;
-                            for (int r = lane; r < nw; r += 32) {
-                                double* u = Us + r;
-                                const double u0 = u[c * LDW], u1 = u[(c + 1) * LDW];
-                                const double u2 = (nr == 3) ? u[(c + 2) * LDW] : 0.0;
-                                const double sum = u0 + v2 * u1 + v3 * u2;
-                                u[c * LDW] = u0 - sum * t1;
-                                u[(c + 1) * LDW] = u1 - sum * t2;
-                                if (nr == 3) u[(c + 2) * LDW] = u2 - sum * t3;
-                            }
+                            named_bar(4, nb * 32);
                         }
-                        named_bar(1, nb * 32);
                     }
+                    named_bar(3, 128);
+                    if (t == 0) tick(2);
+                    for (int idx = tg; idx < nw * nw; idx += 128) {
+                        const int r = idx % nw, cc = idx / nw;
+                        H[(wlo + r) + (size_t)(wlo + cc) * d] = Wn[cc * LDW + r];
+                    }
+                    if (c == 0 && nb == 1 && M > L && t == 0) H[M + (size_t)(M - 1) * d] *= (1.0 - s_t1);
+                    // columns the next window reads: wait until the updaters are done
+                    // with U_{c-1} (they cover the same columns), then apply U_c there
+                    int wlo_n = wlo, whi_n = whi;
+                    if (c + 1 < nchunk) geom(c + 1, wlo_n, whi_n);
+                    if (c >= 1) named_bar(2, 256);
+                    if (whi_n > whi) apply_part(Uc, wlo, whi, nw, whi + 1, whi_n + 1, false, warp, 4);
+                    named_bar(3, 128);
+                    asm volatile("bar.arrive 1, 256;" ::: "memory");
+                    if (t == 0) tick(3);
                 }
-                __syncthreads();
-                tick(2);
-                for (int idx = t; idx < nw * nw; idx += nt) {
-                    const int r = idx % nw, c = idx / nw;
-                    H[(wlo + r) + (size_t)(wlo + c) * d] = Wn[c * LDW + r];
+            } else {
+                for (int c = 0; c < nchunk; ++c) {
+                    named_bar(1, 256);
+                    int wlo, whi, wlo_n, whi_n;
+                    geom(c, wlo, whi);
+                    wlo_n = wlo;
+                    whi_n = whi;
+                    if (c + 1 < nchunk) geom(c + 1, wlo_n, whi_n);
+                    const double* Uc = Us2 + (c & 1) * (MW * LDW);
+                    apply_part(Uc, wlo, whi, whi - wlo + 1, max(whi, whi_n) + 1, d, true, warp - 4, 4);
+                    if (c + 1 < nchunk) asm volatile("bar.arrive 2, 256;" ::: "memory");
                 }
-                if (s0 == 0 && nb == 1 && M > L && t == 0) H[M + (size_t)(M - 1) * d] *= (1.0 - s_t1);
-                apply_u(wlo, whi, nw);
-                __syncthreads();
-                tick(3);
             }
+            __syncthreads();
         }
         if (!conv) {
             if (t == 0) report_failure(status, kFailHqrNoConverge, 1, b, (double)I, (double)L);
