@@ -2221,6 +2221,210 @@ __global__ void __launch_bounds__(256) trevc_reg_kernel(const double* Tall, cons
     }
 }
 
+
+// Grouped register-resident dtrevc: a warp back-substitutes G eigenvectors at
+// once (G consecutive eigen-blocks, complex pairs by their first index), so
+// every column of T loaded for a step feeds G independent substitution chains
+// and the L2 latency of the (one step ahead) prefetch is amortised G-fold.
+// Diagonal / super- / subdiagonal of T and the 2x2 flags live in shared
+// memory.  Arithmetic per vector identical to trevc_reg_kernel.
+template <int RPL, int G>
+__global__ void __launch_bounds__(256) trevc_grp_kernel(const double* Tall, const double* wrall,
+                                                        const double* wiall, double* Yall, int d) {
+    extern __shared__ double shm[];
+    double* tdg = shm;
+    double* tup = tdg + d;
+    double* tlo = tup + d;
+    int* lead = reinterpret_cast<int*>(tlo + d);
+    __shared__ int s_nl;
+    const int b = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const double* T = Tall + (size_t)b * d * d;
+    const double* wr = wrall + (size_t)b * d;
+    const double* wi = wiall + (size_t)b * d;
+    double* Y = Yall + (size_t)b * d * d;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        tdg[c] = T[c + (size_t)c * d];
+        tup[c] = (c + 1 < d) ? T[c + (size_t)(c + 1) * d] : 0.0;
+        tlo[c] = (c > 0) ? T[c + (size_t)(c - 1) * d] : 0.0;
+    }
+    if (threadIdx.x == 0) {  // eigen-block leaders in ascending order
+        int n = 0;
+        for (int k = 0; k < d; ++k)
+            if (wi[k] >= 0.0) lead[n++] = k;
+        s_nl = n;
+    }
+    __syncthreads();
+    const int nl = s_nl;
+    const double smlnum = kSafeMin * ((double)d / kUlp);
+    auto load_col = [&](double* dst, int c, int lim) {
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+            const int r = lane + 32 * i;
+            dst[i] = (c >= 0 && r < lim) ? T[r + (size_t)c * d] : 0.0;
+        }
+    };
+    auto pick = [&](const double* v, int r) {
+        double x = 0.0;
+#pragma unroll
+        for (int i = 0; i < RPL; ++i)
+            if (i == (r >> 5)) x = v[i];
+        return __shfl_sync(0xffffffffu, x, r & 31);
+    };
+    auto put = [&](double* v, int r, double x) {
+#pragma unroll
+        for (int i = 0; i < RPL; ++i)
+            if (i == (r >> 5) && lane == (r & 31)) v[i] = x;
+    };
+    for (int g0 = w * G; g0 < nl; g0 += nw * G) {
+        double re[G][RPL], im[G][RPL];
+        int top[G], kid[G];
+        bool cx[G], on[G];
+        double lr[G], li[G], sm[G];
+        int jmax = -1;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            on[g] = g0 + g < nl;
+            const int ki = on[g] ? lead[g0 + g] : 0;
+            kid[g] = ki;
+            const double wik = on[g] ? wi[ki] : 0.0;
+            cx[g] = wik != 0.0;
+            top[g] = on[g] ? ki : -1;
+            lr[g] = on[g] ? wr[ki] : 0.0;
+            li[g] = wik;
+            if (!on[g]) {
+#pragma unroll
+                for (int i = 0; i < RPL; ++i) re[g][i] = im[g][i] = 0.0;
+                sm[g] = 1.0;
+                continue;
+            }
+            if (!cx[g]) {
+                sm[g] = fmax(kUlp * fabs(lr[g]), smlnum);
+                load_col(re[g], ki, ki);
+#pragma unroll
+                for (int i = 0; i < RPL; ++i) {
+                    re[g][i] = -re[g][i];
+                    im[g][i] = 0.0;
+                    if (lane + 32 * i == ki) re[g][i] = 1.0;
+                }
+            } else {
+                const int pp = ki, q = ki + 1;
+                sm[g] = fmax(kUlp * (fabs(lr[g]) + fabs(wik)), smlnum);
+                double xpr, xqi;
+                if (fabs(tup[pp]) >= fabs(tlo[q])) {
+                    xpr = 1.0;
+                    xqi = wik / tup[pp];
+                } else {
+                    xpr = -wik / tlo[q];
+                    xqi = 1.0;
+                }
+                load_col(re[g], pp, pp);
+                load_col(im[g], q, pp);
+#pragma unroll
+                for (int i = 0; i < RPL; ++i) {
+                    const int r = lane + 32 * i;
+                    re[g][i] *= -xpr;
+                    im[g][i] *= -xqi;
+                    if (r == pp) {
+                        re[g][i] = xpr;
+                        im[g][i] = 0.0;
+                    }
+                    if (r == q) {
+                        re[g][i] = 0.0;
+                        im[g][i] = xqi;
+                    }
+                }
+            }
+            jmax = max(jmax, top[g] - 1);
+        }
+        int j = jmax;
+        double t1[RPL], t2[RPL], n1[RPL], n2[RPL];
+        bool pair = j > 0 && tlo[j] != 0.0;
+        load_col(t1, j, pair ? j - 1 : j);
+        load_col(t2, pair ? j - 1 : -1, j - 1);
+        while (j >= 0) {
+            const int jn = j - (pair ? 2 : 1);
+            const bool pairn = jn > 0 && tlo[jn] != 0.0;
+            load_col(n1, jn, pairn ? jn - 1 : jn);
+            load_col(n2, pairn ? jn - 1 : -1, jn - 1);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                if (!on[g] || j >= top[g]) continue;
+                const cplx lam = cmk(lr[g], li[g]);
+                if (!cx[g]) {
+                    if (pair) {
+                        double x0, x1;
+                        solve2r(tdg[j - 1] - lam.re, tup[j - 1], tlo[j], tdg[j] - lam.re, pick(re[g], j - 1),
+                                pick(re[g], j), sm[g], x0, x1);
+#pragma unroll
+                        for (int i = 0; i < RPL; ++i) re[g][i] = fma(-x0, t2[i], fma(-x1, t1[i], re[g][i]));
+                        put(re[g], j - 1, x0);
+                        put(re[g], j, x1);
+                    } else {
+                        double den = tdg[j] - lam.re;
+                        if (fabs(den) < sm[g]) den = sm[g];
+                        const double x = pick(re[g], j) / den;
+#pragma unroll
+                        for (int i = 0; i < RPL; ++i) re[g][i] = fma(-x, t1[i], re[g][i]);
+                        put(re[g], j, x);
+                    }
+                } else if (pair) {
+                    const cplx b0 = cmk(pick(re[g], j - 1), pick(im[g], j - 1));
+                    const cplx b1 = cmk(pick(re[g], j), pick(im[g], j));
+                    cplx x0, x1;
+                    solve2(cmk(tdg[j - 1], 0) - lam, cmk(tup[j - 1], 0), cmk(tlo[j], 0), cmk(tdg[j], 0) - lam, b0,
+                           b1, sm[g], x0, x1);
+#pragma unroll
+                    for (int i = 0; i < RPL; ++i) {
+                        re[g][i] = fma(-x0.re, t2[i], fma(-x1.re, t1[i], re[g][i]));
+                        im[g][i] = fma(-x0.im, t2[i], fma(-x1.im, t1[i], im[g][i]));
+                    }
+                    put(re[g], j - 1, x0.re);
+                    put(re[g], j, x1.re);
+                    put(im[g], j - 1, x0.im);
+                    put(im[g], j, x1.im);
+                } else {
+                    cplx den = cmk(tdg[j], 0.0) - lam;
+                    if (cabs_(den) < sm[g]) den = cmk(sm[g], 0.0);
+                    const cplx x = cdiv(cmk(pick(re[g], j), pick(im[g], j)), den);
+#pragma unroll
+                    for (int i = 0; i < RPL; ++i) {
+                        re[g][i] = fma(-x.re, t1[i], re[g][i]);
+                        im[g][i] = fma(-x.im, t1[i], im[g][i]);
+                    }
+                    put(re[g], j, x.re);
+                    put(im[g], j, x.im);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) {
+                t1[i] = n1[i];
+                t2[i] = n2[i];
+            }
+            j = jn;
+            pair = pairn;
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            if (!on[g]) continue;
+            const int ki = kid[g], last = cx[g] ? ki + 1 : ki;
+            double* yr = Y + (size_t)ki * d;
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) {
+                const int r = lane + 32 * i;
+                if (r < d) yr[r] = (r <= last) ? re[g][i] : 0.0;
+            }
+            if (cx[g]) {
+                double* yi = Y + (size_t)(ki + 1) * d;
+#pragma unroll
+                for (int i = 0; i < RPL; ++i) {
+                    const int r = lane + 32 * i;
+                    if (r < d) yi[r] = (r <= last) ? im[g][i] : 0.0;
+                }
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------ normalization
 __global__ void normalize_modes_kernel(double* Xall, const double* wiall, int d, int batch) {
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -2649,7 +2853,16 @@ void launch_trevc(const double* T, const double* wr, const double* wi, double* Y
         trevc_kernel<<<batch, warps * 32, smem, st>>>(T, wr, wi, Y, d);
     } else {
         const int rpl = (d + 31) / 32;
-        if (rpl <= 2)
+        static const char* grp = std::getenv("VRTE_TREVC_GROUP");  // default on
+        const size_t gsm = 3 * (size_t)d * sizeof(double) + (size_t)d * sizeof(int);
+        if (!(grp && std::string(grp) == "0") && rpl <= 8) {
+            if (rpl <= 2)
+                trevc_grp_kernel<2, 4><<<batch, 256, gsm, st>>>(T, wr, wi, Y, d);
+            else if (rpl <= 4)
+                trevc_grp_kernel<4, 4><<<batch, 256, gsm, st>>>(T, wr, wi, Y, d);
+            else
+                trevc_grp_kernel<8, 4><<<batch, 256, gsm, st>>>(T, wr, wi, Y, d);
+        } else if (rpl <= 2)
             trevc_reg_kernel<2><<<batch, 256, d, st>>>(T, wr, wi, Y, d);
         else if (rpl <= 4)
             trevc_reg_kernel<4><<<batch, 256, d, st>>>(T, wr, wi, Y, d);
