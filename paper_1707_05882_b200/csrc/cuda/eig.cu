@@ -1257,7 +1257,38 @@ __device__ double warp_dlarfg(double* v, int len, double* beta) {
     return tau;
 }
 
-__global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double* Zall, double* wrall,
+
+// ---- thread-block-cluster helpers (the multishift QR runs as a 2-CTA cluster)
+__device__ inline unsigned dsmem_addr(const void* p, unsigned rank) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ inline unsigned ld_acquire_cluster(unsigned addr) {
+    unsigned v;
+    asm volatile("ld.acquire.cluster.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ inline void st_release_cluster(unsigned addr, unsigned v) {
+    asm volatile("st.release.cluster.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ inline int ld_cluster_s32(unsigned addr) {
+    int v;
+    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ inline double ld_cluster_f64(unsigned addr) {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ inline void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+__device__ inline void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double* Zall, double* wrall,
                                                         double* wiall, int d, DeviceStatus* status,
                                                         int aed_nw, int nb4_min, int nb2_min, int nibble,
                                                         double* trace) {
@@ -1272,7 +1303,12 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
     __shared__ int s_int;
     __shared__ int s_nb;
     __shared__ double s_t1;
-    const int b = blockIdx.x, t = threadIdx.x, nt = blockDim.x, lane = t & 31, warp = t >> 5;
+    // cluster job queue (used in rank 0's shared memory): rank 0 posts chunk
+    // factors, rank 1 applies them to the rest of H and to Z
+    __shared__ unsigned s_posted, s_done;
+    __shared__ int s_job[2][8];  // buf, wlo, whi, nw, c_lo, c_hi, above_z, stop
+    const int b = blockIdx.x >> 1, crank = blockIdx.x & 1;
+    const int t = threadIdx.x, nt = blockDim.x, lane = t & 31, warp = t >> 5;
     double* H = Hall + (size_t)b * d * d;
     double* Z = Zall + (size_t)b * d * d;
     double* wr = wrall + (size_t)b * d;
@@ -1303,7 +1339,7 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
     // tiles of 8 vectors are one [8 x 32] x [32 x 32] product on the FP64 tensor
     // cores: warp per tile (gw-th of gsize warps), U's B fragments in registers.
     auto apply_part = [&](const double* U, int wlo, int whi, int nw, int c_lo, int c_hi, bool above_z, int gw,
-                          int gsize) {
+                          int gsize, unsigned u_remote = 0) {
         const int n_right = max(0, c_hi - c_lo), n_above = above_z ? wlo : 0;
         const int tr = (n_right + 7) / 8, ta = (n_above + 7) / 8, tz = above_z ? (d + 7) / 8 : 0;
         const int gq = lane >> 2, tq = lane & 3;
@@ -1311,7 +1347,10 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
 #pragma unroll
-            for (int cb = 0; cb < 4; ++cb) bf[ks][cb] = U[(cb * 8 + gq) * LDW + ks * 4 + tq];
+            for (int cb = 0; cb < 4; ++cb) {
+                const int e = (cb * 8 + gq) * LDW + ks * 4 + tq;
+                bf[ks][cb] = u_remote ? ld_cluster_f64(u_remote + 8u * e) : U[e];
+            }
         // vector gq of a tile: base pointer and element stride
         auto locate = [&](int tile, double*& base, long long& st) -> bool {
             if (tile < tr) {
@@ -1382,6 +1421,51 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
                 }
             }
         }
+    };
+    if (t == 0) {
+        s_posted = 0u;
+        s_done = 0u;
+    }
+    cluster_sync_all();
+    const unsigned a_posted = dsmem_addr(&s_posted, 0), a_done = dsmem_addr(&s_done, 0);
+    if (crank == 1) {
+        // ---- updater CTA: apply posted chunk factors to H and Z, in order
+        for (unsigned next = 0;; ++next) {
+            if (t == 0)
+                while (ld_acquire_cluster(a_posted) <= next) __nanosleep(64);
+            __syncthreads();
+            (void)ld_acquire_cluster(a_posted);
+            const unsigned jb = dsmem_addr(&s_job[next & 1][0], 0);
+            int jd[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) jd[q] = ld_cluster_s32(jb + 4u * q);
+            if (jd[7]) break;
+            const unsigned ua = dsmem_addr(Us2 + (size_t)jd[0] * (MW * LDW), 0);
+            apply_part(nullptr, jd[1], jd[2], jd[3], jd[4], jd[5], jd[6] != 0, warp, nt / 32, ua);
+            fence_cluster();
+            __syncthreads();
+            if (t == 0) st_release_cluster(a_done, next + 1);
+        }
+        cluster_sync_all();
+        return;
+    }
+    unsigned jid = 0;  // jobs posted so far (rank 0)
+    auto post_job = [&](int buf, int wlo, int whi, int nw, int c_lo, int c_hi, int above_z, int stop) {
+        // caller: one thread
+        int* j = s_job[jid & 1];
+        j[0] = buf;
+        j[1] = wlo;
+        j[2] = whi;
+        j[3] = nw;
+        j[4] = c_lo;
+        j[5] = c_hi;
+        j[6] = above_z;
+        j[7] = stop;
+        fence_cluster();
+        st_release_cluster(a_posted, jid + 1);
+    };
+    auto wait_done = [&](unsigned upto) {  // caller: one thread
+        while (ld_acquire_cluster(a_done) < upto) __nanosleep(32);
     };
     while (I >= 0) {
         int L = 0;
@@ -1768,29 +1852,27 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
                     // with U_{c-1} (they cover the same columns), then apply U_c there
                     int wlo_n = wlo, whi_n = whi;
                     if (c + 1 < nchunk) geom(c + 1, wlo_n, whi_n);
-                    if (c >= 1) named_bar(2, 256);
-                    if (whi_n > whi) apply_part(Uc, wlo, whi, nw, whi + 1, whi_n + 1, false, warp, 4);
+                    // the updater CTA must be done with U_{c-1} (it covers these columns)
+                    if (c >= 1 && t == 0) wait_done(jid);
                     named_bar(3, 128);
-                    asm volatile("bar.arrive 1, 256;" ::: "memory");
+                    if (whi_n > whi) apply_part(Uc, wlo, whi, nw, whi + 1, whi_n + 1, false, warp, 4);
+                    fence_cluster();
+                    named_bar(3, 128);
+                    if (t == 0) post_job(c & 1, wlo, whi, nw, max(whi, whi_n) + 1, d, 1, 0);
+                    ++jid;
                     if (t == 0) tick(3);
                 }
-            } else {
-                for (int c = 0; c < nchunk; ++c) {
-                    named_bar(1, 256);
-                    int wlo, whi, wlo_n, whi_n;
-                    geom(c, wlo, whi);
-                    wlo_n = wlo;
-                    whi_n = whi;
-                    if (c + 1 < nchunk) geom(c + 1, wlo_n, whi_n);
-                    const double* Uc = Us2 + (c & 1) * (MW * LDW);
-                    apply_part(Uc, wlo, whi, whi - wlo + 1, max(whi, whi_n) + 1, d, true, warp - 4, 4);
-                    if (c + 1 < nchunk) asm volatile("bar.arrive 2, 256;" ::: "memory");
-                }
             }
+            // end of sweep: every chunk factor applied before the deflation scan / AED
+            if (t == 0) wait_done(jid);  // (jid is only meaningful in thread 0)
             __syncthreads();
         }
         if (!conv) {
-            if (t == 0) report_failure(status, kFailHqrNoConverge, 1, b, (double)I, (double)L);
+            if (t == 0) {
+                report_failure(status, kFailHqrNoConverge, 1, b, (double)I, (double)L);
+                post_job(0, 0, 0, 0, 0, 0, 0, 1);
+            }
+            cluster_sync_all();
             return;
         }
         if (L == I) {
@@ -1857,6 +1939,8 @@ __global__ void __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double*
         const int r = idx % d, c = idx / d;
         if (r > c + 1) H[idx] = 0.0;
     }
+    if (t == 0) post_job(0, 0, 0, 0, 0, 0, 0, 1);  // stop the updater CTA
+    cluster_sync_all();                              // it reads our shared memory until then
 }
 
 // ------------------------------------------------------------------ 2x2 solves
@@ -2816,7 +2900,8 @@ void launch_hqr(double* H, double* Z, double* wr, double* wi, int d, int batch,
             VRTE_CUDA_CHECK(cudaMalloc(&trace, sizeof(double) * 8 * batch));
             trace_n = batch;
         }
-        hqr_multi_kernel<<<batch, 256, 0, st>>>(H, Z, wr, wi, d, status, min(max(aed_nw, 4), MW), nb4, nb2,
+        // 2-CTA clusters: rank 0 chases / deflates, rank 1 applies the chunk factors
+        hqr_multi_kernel<<<2 * batch, 256, 0, st>>>(H, Z, wr, wi, d, status, min(max(aed_nw, 4), MW), nb4, nb2,
                                                 nibble, trace_path ? trace : nullptr);
         if (trace_path) {
             std::vector<double> h((size_t)8 * batch);
