@@ -37,6 +37,19 @@ VRTE_API vrte_status vrte_brdf_from_stacks(const vrte_material* material, const 
                                            const double* basis, const double* up_all_orders,
                                            vrte_brdf** out);
 
+/* Solve `count` independent BRDF requests -- e.g. the 31 spectral bands of a
+ * paint (BASELINE.json config 5, SURVEY.md §8(f) "spectral batch API") -- with
+ * the same options, incident cosines, azimuth count and basis.  The requests
+ * run concurrently (one device plan and CUDA stream each, `concurrency` host
+ * threads; <= 0 picks 2).  out[i] receives request i's handle, or NULL when it
+ * failed; the return value is the first failure (VRTE_OK if none), with its
+ * message in vrte_last_error().  Each table is identical to the one
+ * vrte_compute_brdf returns for that material alone. */
+VRTE_API vrte_status vrte_compute_brdf_batch(const vrte_material* const* materials, size_t count,
+                                             const vrte_options* options, const double* mu_in,
+                                             size_t n_mu_in, int32_t n_dphi, const double* basis,
+                                             int32_t concurrency, vrte_brdf** out);
+
 #ifdef __cplusplus
 }
 #endif

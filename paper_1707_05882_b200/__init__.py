@@ -131,6 +131,7 @@ EXPORTED = [
     "vrte_mc_tally_write_csv", "vrte_mc_tally_free",
     # vrte_ext.h
     "vrte_brdf_device_stats_get", "vrte_brdf_plan_create", "vrte_brdf_from_stacks",
+    "vrte_compute_brdf_batch",
     # vrte_cuda.h
     "vrte_cuda_brdf", "vrte_cuda_plan_create", "vrte_cuda_plan_run", "vrte_cuda_plan_fetch",
     "vrte_cuda_plan_fetch_up", "vrte_cuda_plan_fetch_modes", "vrte_cuda_plan_fetch_ef",
@@ -155,6 +156,8 @@ def lib():
     L.vrte_material_free.argtypes = [vp]
     L.vrte_material_info.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     L.vrte_options_init.argtypes = [C.POINTER(Options)]
+    L.vrte_compute_brdf_batch.argtypes = [C.POINTER(vp), C.c_size_t, C.POINTER(Options), dp, C.c_size_t,
+                                          C.c_int32, dp, C.c_int32, C.POINTER(vp)]
     L.vrte_compute_brdf.argtypes = [vp, C.POINTER(Options), dp, C.c_size_t, C.c_int32, dp,
                                     C.POINTER(vp)]
     L.vrte_brdf_size.argtypes = [vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
@@ -353,6 +356,28 @@ def compute_brdf(material: Material, opts: Options, mu_in, n_dphi: int = 19, bas
     _check(lib().vrte_compute_brdf(material._h, C.byref(opts), _dp(mu), len(mu), n_dphi, _dp(b),
                                    C.byref(h)))
     return Brdf(h)
+
+
+def compute_brdf_batch(materials, opts: Options, mu_in, n_dphi: int = 19, basis=None,
+                       concurrency: int = 2):
+    """vrte_compute_brdf_batch (vrte_ext.h): independent requests (e.g. spectral
+    bands) solved concurrently, one plan / CUDA stream each.  Returns a list of
+    Brdf handles; raises VrteError with the first failure."""
+    mu = np.ascontiguousarray(mu_in, dtype=np.float64)
+    b = None if basis is None else np.ascontiguousarray(basis, dtype=np.float64).reshape(16)
+    n = len(materials)
+    mats = (C.c_void_p * n)(*[m._h for m in materials])
+    outs = (C.c_void_p * n)()
+    code = lib().vrte_compute_brdf_batch(mats, n, C.byref(opts), _dp(mu), len(mu), n_dphi, _dp(b),
+                                         concurrency, outs)
+    handles = [Brdf(C.c_void_p(outs[i])) if outs[i] else None for i in range(n)]
+    if code != VRTE_OK:
+        msg = lib().vrte_last_error().decode(errors="replace")
+        for h in handles:
+            if h is not None:
+                h.close()
+        raise VrteError(code, msg)
+    return handles
 
 
 def brdf_from_stacks(material: Material, opts: Options, mu_in, n_dphi, basis, up_all) -> Brdf:

@@ -138,7 +138,6 @@ struct vrte_cuda_plan {
 
 namespace {
 
-std::mutex g_plan_mutex;
 
 void fill_message(vrte_cuda_result* r, int status, const std::string& msg) {
     if (!r) return;
@@ -790,22 +789,18 @@ void vrte_cuda_plan_destroy(vrte_cuda_plan* pl) { delete pl; }
 int32_t vrte_cuda_brdf(const vrte_cuda_problem* problem, double* table, vrte_cuda_result* result) {
     return guarded(result, [&]() -> int32_t {
         if (!table) throw std::invalid_argument("null table");
-        // Reuse one cached plan per thread-safe slot; shape changes reallocate.
-        static std::unique_ptr<vrte_cuda_plan> cached;
-        std::lock_guard<std::mutex> lk(g_plan_mutex);
+        // One cached plan (device buffers + stream) per host thread: the entry
+        // point is reentrant (vrte.h "every entry point is reentrant") and
+        // concurrent callers run concurrently on their own streams; shape
+        // changes reallocate.
+        thread_local std::unique_ptr<vrte_cuda_plan> cached;
         if (!cached) cached = std::make_unique<vrte_cuda_plan>();
         vrte_cuda_plan& pl = *cached;
-        cudaEvent_t a, b;
         setup_plan(pl, problem);
-        VRTE_CUDA_CHECK(cudaEventCreate(&a));
-        VRTE_CUDA_CHECK(cudaEventCreate(&b));
         pl.launches = run_pipeline(pl, true);
         VRTE_CUDA_CHECK(cudaMemcpyAsync(table, pl.out.p, sizeof(double) * pl.out.n,
                                         cudaMemcpyDeviceToHost, pl.st));
-        const int rc = finish(pl, result);
-        cudaEventDestroy(a);
-        cudaEventDestroy(b);
-        return rc;
+        return finish(pl, result);
     });
 }
 

@@ -8,7 +8,12 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
 
 #include "host.hpp"
 #include "vrte/vrte.h"
@@ -404,6 +409,44 @@ vrte_status vrte_compute_brdf(const vrte_material* material, const vrte_options*
         *out = h.release();
         return VRTE_OK;
     });
+}
+
+vrte_status vrte_compute_brdf_batch(const vrte_material* const* materials, size_t count,
+                                    const vrte_options* options, const double* mu_in, size_t n_mu_in,
+                                    int32_t n_dphi, const double* basis, int32_t concurrency,
+                                    vrte_brdf** out) {
+    if (!materials || !out || !mu_in || n_mu_in == 0) return set_error(VRTE_E_ARGUMENT, "null argument");
+    for (size_t i = 0; i < count; ++i) out[i] = nullptr;
+    const size_t nthreads = std::min<size_t>(count, concurrency > 0 ? (size_t)concurrency : 2);
+    std::atomic<size_t> next{0};
+    std::mutex mtx;
+    vrte_status first = VRTE_OK;
+    size_t first_index = count;
+    std::string first_msg;
+    auto worker = [&] {
+        for (size_t i = next++; i < count; i = next++) {
+            vrte_brdf* h = nullptr;
+            const vrte_status rc = materials[i]
+                                       ? vrte_compute_brdf(materials[i], options, mu_in, n_mu_in, n_dphi, basis, &h)
+                                       : set_error(VRTE_E_ARGUMENT, "null material");
+            if (rc == VRTE_OK) {
+                out[i] = h;
+            } else {
+                std::lock_guard<std::mutex> lk(mtx);
+                if (i < first_index) {
+                    first_index = i;
+                    first = rc;
+                    first_msg = g_last_error;
+                }
+            }
+        }
+    };
+    std::vector<std::thread> pool;
+    for (size_t k = 1; k < nthreads; ++k) pool.emplace_back(worker);
+    worker();
+    for (auto& th : pool) th.join();
+    if (first != VRTE_OK) return set_error(first, first_msg);
+    return VRTE_OK;
 }
 
 vrte_status vrte_brdf_size(const vrte_brdf* brdf, size_t* n_in, size_t* n_out, size_t* n_dphi) {

@@ -78,3 +78,25 @@ def test_negative_intensity_is_reported_not_clamped_silently():
     b = V.compute_brdf(mat, V.options(6), [0.7], 6)
     assert np.all(b.table()[..., 0, 0] >= 0)
     assert b.device_stats()["clamped"] >= 0
+
+
+def test_spectral_batch_matches_individual_solves():
+    """vrte_compute_brdf_batch (spectral bands, BASELINE config 5 shape at small
+    N): every band's table equals the single-request table bit for bit, for any
+    concurrency."""
+    nodes, _ = O.quadrature(8)
+    mats = [product_material(M.config("C5", band=b).material) for b in (0, 15, 30)]
+    single = [V.compute_brdf(m, V.options(8), nodes[:3], 5).table() for m in mats]
+    for conc in (1, 3):
+        out = V.compute_brdf_batch(mats, V.options(8), nodes[:3], 5, concurrency=conc)
+        for b, s in zip(out, single):
+            assert np.array_equal(b.table(), s)
+
+
+def test_batch_reports_first_failure():
+    nodes, _ = O.quadrature(16)
+    ok = product_material(M.config("C1").material)
+    bad = product_material(M.config("C4").material)  # at N=16 the reference rejects m = 0
+    with pytest.raises(V.VrteError) as ei:
+        V.compute_brdf_batch([ok, bad], V.options(16, 24), nodes[:2], 5)
+    assert ei.value.code == 3 and "negative real axis" in ei.value.message
