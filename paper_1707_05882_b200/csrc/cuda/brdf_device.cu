@@ -652,6 +652,10 @@ int finish(vrte_cuda_plan& pl, vrte_cuda_result* r) {
         r->max_particular_residual = s.max_particular_residual;
         r->kernel_launches = pl.launches;
     }
+    if (s.code == kFailNegativeIntensity && s.neg_key != 0) {
+        const unsigned long long idx = ~s.neg_key;  // first offending entry, reference order
+        VRTE_CUDA_CHECK(cudaMemcpy(&s.value, pl.out.p + idx * 16, sizeof(double), cudaMemcpyDeviceToHost));
+    }
     if (s.code != 0) {
         fill_message(r, 3, describe_failure(s, res, pl.d, oi));
         return 3;
@@ -847,6 +851,10 @@ int32_t vrte_cuda_synthesize(const vrte_cuda_problem* problem, const double* up,
         if (result) {
             result->clamped = s.clamped;
             result->kernel_launches = 1;
+        }
+        if (s.code == kFailNegativeIntensity && s.neg_key != 0) {
+            const unsigned long long idx = ~s.neg_key;
+            VRTE_CUDA_CHECK(cudaMemcpy(&s.value, dout.p + idx * 16, sizeof(double), cudaMemcpyDeviceToHost));
         }
         if (s.code != 0) {
             fill_message(result, 3, describe_failure(s, {}, 0, {}));

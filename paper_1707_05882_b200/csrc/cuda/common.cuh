@@ -39,6 +39,7 @@ struct DeviceStatus {
     unsigned long long qr_sweeps;
     unsigned long long qr_steps;
     unsigned long long qr_cycles[8];  // debug phase timers (clock64 in thread 0)
+    unsigned long long neg_key;       // ~(first negative-intensity table index) (atomicMax)
 };
 
 enum FailKind {

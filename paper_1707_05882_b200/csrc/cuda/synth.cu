@@ -50,9 +50,12 @@ __global__ void synth_kernel(SynthArgs a) {
             for (int k = 0; k < 4; ++k) s += e[r][k] * Tm[4 * k + c];
             f[4 * r + c] = s;
         }
-    if (f[0] < 0.0) {
-        if (f[0] < -1e-9)
-            report_failure(a.status, kFailNegativeIntensity, 4, (int)idx, f[0]);
+    if (f[0] < -1e-9) {
+        // brdf.cpp:108-112 throws at the FIRST such entry in (incident, exit,
+        // azimuth) order: keep the value and record the smallest index
+        atomicMax(&a.status->neg_key, ~(unsigned long long)idx);
+        report_failure(a.status, kFailNegativeIntensity, 4, (int)idx, f[0]);
+    } else if (f[0] < 0.0) {
         f[0] = 0.0;
         atomicAdd(&a.status->clamped, 1ull);
     }

@@ -93,9 +93,10 @@ int main(int argc, char** argv) {
     if (argc > 2) {  // explicit config "bk st [minb]"; default: the library's selection
         g_bk = atoi(argv[1]);
         g_st = atoi(argv[2]);
+        if (argc > 3 && argv[3][0] != '-') g_mb = atoi(argv[3]);
     }
-    if (argc > 3) {  // single timed shape (for ncu): bk st m n k batch beta
-        run(atoi(argv[3]), atoi(argv[4]), atoi(argv[5]), atoi(argv[6]), false, false, atof(argv[7]), true);
+    if (argc > 7) {  // single timed shape (for ncu): bk st minb m n k batch beta
+        run(atoi(argv[4]), atoi(argv[5]), atoi(argv[6]), atoi(argv[7]), false, false, atof(argv[8]), true);
         return 0;
     }
     int fails = 0;
