@@ -157,7 +157,14 @@ struct GemmBatch {
     int batch;
     double alpha, beta;
     bool trans_a, trans_b;
+    // optional per-batch index maps (stride map_stride): A column k is A + amap[k]*lda,
+    // B column n is B + bmap[n]*ldb, C column n is C + cmap[n]*ldc (null = identity)
+    const int* amap;
+    const int* bmap;
+    const int* cmap;
+    long long map_stride;
 };
+constexpr int kMaxMapK = 256;
 void gemm_batched(const GemmBatch& g, cudaStream_t stream);
 void gemm_batched_cfg(const GemmBatch& g, cudaStream_t stream, int bk, int stages, int minb);
 

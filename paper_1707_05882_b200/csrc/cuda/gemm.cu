@@ -13,6 +13,8 @@
 // The epilogue stores the accumulator fragments directly; for the beta = 1
 // trailing updates C is preloaded into the accumulators (overlapping the first
 // operand tile) instead of being re-read in the epilogue.
+#include <stdexcept>
+
 #include "common.cuh"
 
 namespace vrte {
@@ -66,6 +68,21 @@ __global__ void __launch_bounds__(2 * BN, MINB) dmma_gemm_kernel(GemmBatch g) {
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int wm = (warp / WN) * 32, wn = (warp % WN) * 32;  // warp tile origin in the CTA tile
     const int gq = lane >> 2, tq = lane & 3;                 // fragment coordinates
+    // optional index maps (lazily pivoted LU, lu.cu): the k index of A, the n
+    // index of B and the n index of C go through per-batch tables
+    __shared__ int s_amap[kMaxMapK], s_bmap[BN], s_cmap[BN];
+    const bool amapped = g.amap != nullptr, bmapped = g.bmap != nullptr, cmapped = g.cmap != nullptr;
+    if (amapped || bmapped || cmapped) {
+        const long long mo = (long long)bz * g.map_stride;
+        if (amapped)
+            for (int i = t; i < g.k; i += NT) s_amap[i] = g.amap[mo + i];
+        for (int n = t; n < BN; n += NT) {
+            const int gn = min(n0 + n, g.n - 1);
+            if (bmapped) s_bmap[n] = g.bmap[mo + gn];
+            if (cmapped) s_cmap[n] = g.cmap[mo + gn];
+        }
+        __syncthreads();
+    }
 
     auto load_stage = [&](int stage, int k0) {
         double* As = As0 + stage * A_STAGE;
@@ -78,7 +95,7 @@ __global__ void __launch_bounds__(2 * BN, MINB) dmma_gemm_kernel(GemmBatch g) {
                 const int m = e % BM, k = e / BM;
                 const int gm = m0 + m, gk = k0 + k;
                 const bool ok = gm < g.m && gk < g.k;
-                cp_async8(As + k * LDA_K + m, ok ? A + gm + (long long)gk * g.lda : A, ok);
+                cp_async8(As + k * LDA_K + m, ok ? A + gm + (long long)(amapped ? s_amap[gk] : gk) * g.lda : A, ok);
             } else {    // contiguous along k: As[m][k]
                 const int k = e % BK, m = e / BK;
                 const int gm = m0 + m, gk = k0 + k;
@@ -94,7 +111,7 @@ __global__ void __launch_bounds__(2 * BN, MINB) dmma_gemm_kernel(GemmBatch g) {
                 const int k = e % BK, n = e / BK;
                 const int gn = n0 + n, gk = k0 + k;
                 const bool ok = gn < g.n && gk < g.k;
-                cp_async8(Bs + n * LDB_N + k, ok ? B + gk + (long long)gn * g.ldb : B, ok);
+                cp_async8(Bs + n * LDB_N + k, ok ? B + gk + (long long)(bmapped ? s_bmap[n] : gn) * g.ldb : B, ok);
             } else {    // contiguous along n: Bs[k][n]
                 const int n = e % BN, k = e / BN;
                 const int gn = n0 + n, gk = k0 + k;
@@ -127,9 +144,10 @@ __global__ void __launch_bounds__(2 * BN, MINB) dmma_gemm_kernel(GemmBatch g) {
             if (preload) {
                 const int gm = m0 + wm + 8 * i + gq, gn = n0 + wn + 8 * j + 2 * tq;
                 if (gm < g.m) {
-                    const double* p = C + gm + (long long)gn * g.ldc;
-                    if (gn < g.n) acc[i][j][0] = g.alpha * p[0];
-                    if (gn + 1 < g.n) acc[i][j][1] = g.alpha * p[g.ldc];
+                    const int nl = wn + 8 * j + 2 * tq;
+                    if (gn < g.n) acc[i][j][0] = g.alpha * C[gm + (long long)(cmapped ? s_cmap[nl] : gn) * g.ldc];
+                    if (gn + 1 < g.n)
+                        acc[i][j][1] = g.alpha * C[gm + (long long)(cmapped ? s_cmap[nl + 1] : gn + 1) * g.ldc];
                 }
             }
         }
@@ -177,7 +195,7 @@ __global__ void __launch_bounds__(2 * BN, MINB) dmma_gemm_kernel(GemmBatch g) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 if (gn + h >= g.n) continue;
-                double* p = C + gm + (long long)(gn + h) * g.ldc;
+                double* p = C + gm + (long long)(cmapped ? s_cmap[wn + 8 * j + 2 * tq + h] : gn + h) * g.ldc;
                 const double v = g.alpha * acc[i][j][h];
                 *p = preload ? v : (beta0 ? v : fma(g.beta, *p, v));
             }
@@ -229,6 +247,8 @@ void gemm_batched_cfg(const GemmBatch& g, cudaStream_t stream, int bk, int stage
 // bound by per-CTA prologue/epilogue latency -> 3 CTAs per SM; long ones keep
 // the register budget for a 3-stage pipeline (measured, profiles/r01_gemm_*).
 void gemm_batched(const GemmBatch& g, cudaStream_t stream) {
+    if ((g.amap && (g.trans_a || g.k > kMaxMapK)) || (g.bmap && g.trans_b))
+        throw std::invalid_argument("gemm_batched: index maps need untransposed operands and k <= 256");
     if (g.k <= 96)
         gemm_batched_cfg(g, stream, 16, 2, 3);
     else

@@ -3,21 +3,26 @@
 // per Fourier order, every (incident, Stokes channel) a right-hand side) and
 // for V^-1 of the eigenvector matrices (eig.cu).
 //
-// Row-major storage makes every row interchange a contiguous copy.  The
-// factorization is blocked twice:
-//   outer blocks of 64 columns: row interchanges of the whole block applied to
-//     the other columns (staged in shared memory, one round trip), U12 by a
-//     warp-parallel unit-lower triangular solve, and the trailing update as a
-//     DMMA GEMM with k = 64;
-//   inner panels of 16 (8, 4 for taller matrices) columns: register-resident
-//     panel factorization (one row per thread, block-wide argmax pivoting with
-//     LAPACK's first-index tie break), then the same swap / TRSM / GEMM steps
-//     restricted to the outer block.
-// The solve gathers the right-hand sides through the net row permutation,
-// then runs blocked forward / backward substitution (TRSM on 64-row blocks +
-// GEMM updates).
+// Lazy pivoting: rows are never moved.  A per-matrix row map (position ->
+// physical row, returned as `perm`) is updated by the pivot search, and every
+// later kernel addresses rows through it (the GEMMs through their index maps,
+// common.cuh), so the row-interchange traffic of dlaswp -- a full HBM pass per
+// pivot block -- disappears.  The factorization is blocked twice:
+//   outer blocks of 128 columns, right-looking: U12 by a warp-parallel
+//     unit-lower triangular solve (64-row halves) and the trailing update as
+//     one DMMA GEMM with k = 128 over the rows inside the staircase profile;
+//   inner panels of 16 (8, 4 for taller matrices) columns, left-looking
+//     (Crout) inside the outer block and fused into ONE kernel per panel: the
+//     panel's U rows (unit-lower solve with the block's L, in shared memory),
+//     the update of its column strip by the block's earlier panels (rows x 16 x
+//     kk from registers), then register-resident factorization with
+//     block-wide argmax pivoting (LAPACK's first-index tie break).
+// The solve gathers the right-hand sides through the row map, then runs
+// blocked forward / backward substitution (TRSM on 64-row blocks + GEMM
+// updates), reading L and U rows through the map.
 #include <cstdlib>
 #include <stdexcept>
+#include <string>
 
 #include "boundary.cuh"
 
@@ -27,108 +32,235 @@ namespace {
 constexpr int LU_NB = 64;  // outer block
 constexpr int SW_TILE = 32;
 
-// ------------------------------------------------------------------ panel
+// ------------------------------------------------------------------ Crout panel (lazy pivoting)
+constexpr int OB_MAX = 128;  // outer block width (bounds the panel kernel's shared memory)
+
+// Panel [k0, k0+jb) of the outer block starting at K0 (kk = k0 - K0 earlier
+// panel columns), positions [k0, rend) active, rows addressed through map.
+// Shared memory: Us [KKMAX][PB] | (Ls [KKMAX][LDL] during the U solve, then
+// Ps [NT*RPT][PSL], the updated strip, one padded row per position).
+__device__ inline void cp_async8(double* smem, const double* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ inline void cp_async_wait_all() { asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::); }
+
 template <int NT, int RPT, int PB>
-__global__ void __launch_bounds__(NT) lu_panel_rm_kernel(double* Aall, int G, long long strideA, int k0,
-                                                         int jb, int rend, int* ipiv_all, DeviceStatus* status,
-                                                         const int* order_index) {
-    __shared__ double s_val[NT / 32];
-    __shared__ int s_idx[NT / 32];
-    __shared__ double prow[PB];
-    __shared__ double srow[PB];
-    __shared__ int s_piv;
+struct PanelGeo {
+    static constexpr int KKMAX = OB_MAX - PB, LDL = KKMAX + 1;
+    static constexpr int PSL = PB + 2;  // 16-byte aligned rows, conflict-free LDS.128 per lane
+    static constexpr int USL = PB <= 8 ? 8 : 24;  // 2*USL = 16 (mod 32): DMMA B-fragment reads 2 wavefronts
+    static constexpr int US = KKMAX * USL;
+    static constexpr int LS = KKMAX * LDL, PS = NT * RPT * PSL;
+    static constexpr size_t bytes = (size_t)(US + (LS > PS ? LS : PS)) * sizeof(double);
+};
+
+template <int NT, int RPT, int PB>
+__global__ void __launch_bounds__(NT) lu_panel_crout_kernel(double* Aall, int G, long long strideA, int* map_all,
+                                                            int* ipiv_all, int K0, int k0, int jb, int rend,
+                                                            DeviceStatus* status, const int* order_index) {
+    using Geo = PanelGeo<NT, RPT, PB>;
+    constexpr int KKMAX = Geo::KKMAX, LDL = Geo::LDL, PSL = Geo::PSL, USL = Geo::USL, KQ = (KKMAX + 3) / 4;
+    constexpr int NTL = (PB + 7) / 8;  // 8-column DMMA tiles of the strip
+    extern __shared__ double dsm[];
+    double* Us = dsm;             // [kk][USL]: U rows of this panel's columns
+    double* Ls = dsm + Geo::US;   // [kk][LDL]: strictly lower part of the block's L (positions K0..k0)
+    double* Ps = dsm + Geo::US;   // [np][PSL]: the updated strip (after the U solve)
+    __shared__ int s_map[NT * RPT];
+    __shared__ int s_mapu[KKMAX];
+    __shared__ unsigned s_kh[2][NT / 32], s_kl[2][NT / 32];
+    __shared__ int s_kp[2][NT / 32];
+    __shared__ __align__(16) double s_cand[2][NT / 32][PB];
     const int b = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int gq = lane >> 2, tq = lane & 3;
+    constexpr int NW = NT / 32;
     double* A = Aall + (size_t)b * strideA;
+    int* map = map_all + (size_t)b * G;
     int* ipiv = ipiv_all + (size_t)b * G;
-    const int np = rend - k0;  // rows past the profile end are zero in these columns
+    const int kk = k0 - K0, np = rend - k0;
+#ifdef VRTE_LU_TRACE
+    long long tr[6];
+    tr[0] = clock64();
+#define LU_STAMP(i) tr[i] = clock64()
+#else
+#define LU_STAMP(i)
+#endif
+    for (int r = t; r < np; r += NT) s_map[r] = map[k0 + r];
+    for (int q = t; q < kk; q += NT) s_mapu[q] = map[K0 + q];
+    __syncthreads();
+    if (kk > 0) {
+        // U(K0:k0, panel) = L11^-1 A(K0:k0, panel), L11 unit lower (the block's
+        // earlier panels): async copies of L11 / the U rows, warp per column to solve
+        for (int q = w; q < kk; q += NW) {
+            const double* src = A + (size_t)s_mapu[q] * G;
+            for (int c = lane; c < q; c += 32) cp_async8(Ls + q * LDL + c, src + K0 + c);
+            if (lane < jb) cp_async8(Us + q * USL + lane, src + k0 + lane);
+            else if (lane < PB) Us[q * USL + lane] = 0.0;
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        for (int c = w; c < jb; c += NW) {
+            double x[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int q = lane + 32 * i;
+                x[i] = q < kk ? Us[q * USL + c] : 0.0;
+            }
+#pragma unroll
+            for (int ci = 0; ci < 4; ++ci) {
+                const int s1 = min(kk, 32 * ci + 32);
+                for (int s2 = 32 * ci; s2 < s1; ++s2) {
+                    const double xs = __shfl_sync(0xffffffffu, x[ci], s2 & 31);
+#pragma unroll
+                    for (int i = ci; i < 4; ++i) {
+                        const int q = lane + 32 * i;
+                        if (q > s2 && q < kk) x[i] = fma(-Ls[q * LDL + s2], xs, x[i]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int q = lane + 32 * i;
+                if (q < kk) {
+                    Us[q * USL + c] = x[i];
+                    A[(size_t)s_mapu[q] * G + k0 + c] = x[i];
+                }
+            }
+        }
+        __syncthreads();  // Ls is dead from here on (Ps aliases it)
+    }
+    LU_STAMP(1);
+    // The panel strip, updated by the block's earlier panels, Ps = A - L(:, K0:k0) U,
+    // on the FP64 tensor cores: warp per 8-row tile, the tile's whole L segment
+    // (one 32-byte sector per row and k-step) requested before the first DMMA;
+    // each fragment register is refilled with the next tile's value as soon as
+    // its DMMA has issued, so the next tile's loads overlap this tile's math.
+    {
+        const int ntiles = (np + 7) / 8;
+        auto row_of = [&](int tile) -> const double* {
+            const int r = tile * 8 + gq;
+            return (tile < ntiles && r < np) ? A + (size_t)s_map[r] * G : nullptr;
+        };
+        double a[KQ];
+        const double* row = row_of(w);
+#pragma unroll
+        for (int q = 0; q < KQ; ++q) a[q] = (row && 4 * q < kk) ? row[K0 + 4 * q + tq] : 0.0;
+        for (int tile = w; tile < ntiles; tile += NW) {
+            double c[NTL][2];
+#pragma unroll
+            for (int nt = 0; nt < NTL; ++nt) {
+                const int cc = 8 * nt + 2 * tq;
+                c[nt][0] = (row && cc < jb) ? row[k0 + cc] : 0.0;
+                c[nt][1] = (row && cc + 1 < jb) ? row[k0 + cc + 1] : 0.0;
+            }
+            const double* nrow = row_of(tile + NW);
+#pragma unroll
+            for (int q = 0; q < KQ; ++q) {
+                if (4 * q >= kk) break;
+#pragma unroll
+                for (int nt = 0; nt < NTL; ++nt) {
+                    const int n = 8 * nt + gq;
+                    const double bu = n < PB ? Us[(4 * q + tq) * USL + n] : 0.0;
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                                 : "+d"(c[nt][0]), "+d"(c[nt][1])
+                                 : "d"(-a[q]), "d"(bu));
+                }
+                a[q] = nrow ? nrow[K0 + 4 * q + tq] : 0.0;
+            }
+            const int r = tile * 8 + gq;
+            if (row) {
+#pragma unroll
+                for (int nt = 0; nt < NTL; ++nt) {
+                    const int cc = 8 * nt + 2 * tq;
+                    if (cc < PB) *reinterpret_cast<double2*>(Ps + r * PSL + cc) = make_double2(c[nt][0], c[nt][1]);
+                }
+            }
+            row = nrow;
+        }
+    }
+    __syncthreads();
+    LU_STAMP(2);
     double v[RPT][PB];
+    const double* src[RPT];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
         const int r = t + i * NT;
-        const double* src = A + (size_t)(k0 + r) * G + k0;
+        src[i] = r < np ? A + (size_t)s_map[r] * G : nullptr;
 #pragma unroll
-        for (int c = 0; c < PB; ++c) v[i][c] = (r < np && c < jb) ? src[c] : 0.0;
+        for (int c2 = 0; c2 < PB / 2; ++c2) {
+            const double2 x = src[i] ? *reinterpret_cast<const double2*>(Ps + r * PSL + 2 * c2) : make_double2(0.0, 0.0);
+            v[i][2 * c2] = x.x;
+            v[i][2 * c2 + 1] = x.y;
+        }
     }
+    // Factor the strip.  Rows never move between threads: each row carries its
+    // current position (LAPACK's interchange of positions j and pr is a swap of
+    // two position labels).  One barrier per column: every warp publishes its
+    // best candidate (key = |a| bits, then the smallest position) together with
+    // the candidate's row, double buffered by column parity; after the barrier
+    // every warp reduces the NW keys itself and reads the winner's row.
+    int pos[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) pos[i] = src[i] ? t + i * NT : 0x7fffffff;
 #pragma unroll
     for (int j = 0; j < PB; ++j) {
         if (j >= jb) break;
-        // argmax |v[r][j]| over rows r >= j (first index on ties)
-        double best = -1.0;
-        int bi = 0x7fffffff;
+        const int buf = j & 1;
+        // argmax |v| over positions >= j (first position on ties, idamax)
+        unsigned long long kb = 0ull;
+        int kp = 0x7fffffff;
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
-            const int r = t + i * NT;
-            if (r >= j && r < np) {
-                const double a = fabs(v[i][j]);
-                if (a > best) {
-                    best = a;
-                    bi = r;
-                }
+            const unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(v[i][j]));
+            if (pos[i] >= j && pos[i] != 0x7fffffff && (bits > kb || (bits == kb && pos[i] < kp))) {
+                kb = bits;
+                kp = pos[i];
             }
         }
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (ov > best || (ov == best && oi < bi)) {
-                best = ov;
-                bi = oi;
-            }
-        }
-        if (lane == 0) {
-            s_val[w] = best;
-            s_idx[w] = bi;
-        }
-        __syncthreads();
-        if (w == 0) {
-            best = lane < NT / 32 ? s_val[lane] : -1.0;
-            bi = lane < NT / 32 ? s_idx[lane] : 0x7fffffff;
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                if (ov > best || (ov == best && oi < bi)) {
-                    best = ov;
-                    bi = oi;
-                }
-            }
+        const unsigned hi = (unsigned)(kb >> 32), lo = (unsigned)kb;
+        const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+        const int mp = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? kp : 0x7fffffff);
+        if (mp == 0x7fffffff) {
             if (lane == 0) {
-                s_piv = bi;
-                ipiv[k0 + j] = k0 + bi;
-                if (!(best > 0.0))
-                    report_failure(status, kFailLuSingular, 3, order_index ? order_index[b] : b,
-                                   (double)(k0 + j));
+                s_kh[buf][w] = 0u;
+                s_kl[buf][w] = 0u;
+                s_kp[buf][w] = 0x7fffffff;
             }
+        } else {
+#pragma unroll
+            for (int i = 0; i < RPT; ++i)
+                if (pos[i] == mp) {
+                    s_kh[buf][w] = mh;
+                    s_kl[buf][w] = ml;
+                    s_kp[buf][w] = mp;
+#pragma unroll
+                    for (int c = j; c < PB; ++c) s_cand[buf][w][c] = v[i][c];
+                }
         }
         __syncthreads();
-        const int pr = s_piv;
-        // exchange rows j and pr through shared memory
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-            const int r = t + i * NT;
-            if (r == pr) {
-#pragma unroll
-                for (int c = 0; c < PB; ++c) prow[c] = v[i][c];
-            }
-            if (r == j && pr != j) {
-#pragma unroll
-                for (int c = 0; c < PB; ++c) srow[c] = v[i][c];
-            }
+        const unsigned h2 = lane < NW ? s_kh[buf][lane] : 0u;
+        const unsigned l2 = lane < NW ? s_kl[buf][lane] : 0u;
+        const int p2 = lane < NW ? s_kp[buf][lane] : 0x7fffffff;
+        const unsigned gh = __reduce_max_sync(0xffffffffu, h2);
+        const unsigned gl = __reduce_max_sync(0xffffffffu, h2 == gh ? l2 : 0u);
+        const int pr = __reduce_min_sync(0xffffffffu, (h2 == gh && l2 == gl) ? p2 : 0x7fffffff);
+        const int ww = __ffs(__ballot_sync(0xffffffffu, lane < NW && p2 == pr)) - 1;
+        const double* prow = s_cand[buf][ww >= 0 ? ww : 0];
+        if (t == 0) {
+            ipiv[k0 + j] = ww >= 0 ? k0 + pr : k0 + j;
+            if (!(gh != 0u || gl != 0u))
+                report_failure(status, kFailLuSingular, 3, order_index ? order_index[b] : b, (double)(k0 + j));
         }
-        __syncthreads();
-        const double piv = prow[j];
+        const double piv = ww >= 0 ? prow[j] : 0.0;
         const double rcp = piv != 0.0 ? 1.0 / piv : 0.0;
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
-            const int r = t + i * NT;
-            if (pr != j) {
-                if (r == j) {
-#pragma unroll
-                    for (int c = 0; c < PB; ++c) v[i][c] = prow[c];
-                } else if (r == pr) {
-#pragma unroll
-                    for (int c = 0; c < PB; ++c) v[i][c] = srow[c];
-                }
-            }
-            if (r > j && r < np && piv != 0.0) {
+            if (pos[i] == pr)
+                pos[i] = j;
+            else if (pos[i] == j)
+                pos[i] = pr;
+            if (pos[i] > j && pos[i] != 0x7fffffff && piv != 0.0) {
                 const double l = v[i][j] * rcp;
                 v[i][j] = l;
 #pragma unroll
@@ -136,81 +268,46 @@ __global__ void __launch_bounds__(NT) lu_panel_rm_kernel(double* Aall, int G, lo
             }
         }
     }
+    LU_STAMP(3);
+    // every row goes back to its own physical row (staged through Ps, then whole
+    // rows per 16-byte lane group); the map records its position
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
         const int r = t + i * NT;
-        if (r < np) {
-            double* dst = A + (size_t)(k0 + r) * G + k0;
+        if (src[i]) {
 #pragma unroll
-            for (int c = 0; c < PB; ++c)
-                if (c < jb) dst[c] = v[i][c];
+            for (int c2 = 0; c2 < PB / 2; ++c2)
+                *reinterpret_cast<double2*>(Ps + r * PSL + 2 * c2) = make_double2(v[i][2 * c2], v[i][2 * c2 + 1]);
+            map[k0 + pos[i]] = s_map[r];
         }
     }
+    __syncthreads();
+    if (jb == PB) {
+        constexpr int LPR = PB / 2;  // lanes per row (16 bytes each)
+        for (int e = t; e < np * LPR; e += NT) {
+            const int r = e / LPR, c2 = e - r * LPR;
+            *reinterpret_cast<double2*>(A + (size_t)s_map[r] * G + k0 + 2 * c2) =
+                *reinterpret_cast<const double2*>(Ps + r * PSL + 2 * c2);
+        }
+    } else {
+        for (int e = t; e < np * jb; e += NT) {
+            const int r = e / jb, c = e - r * jb;
+            A[(size_t)s_map[r] * G + k0 + c] = Ps[r * PSL + c];
+        }
+    }
+#ifdef VRTE_LU_TRACE
+    __syncthreads();
+    LU_STAMP(4);
+    if (t == 0 && b == 0)
+        printf("panel NT=%d K0=%4d k0=%4d np=%4d kk=%3d | setup+U %6lld  strip %6lld  factor %6lld  store %6lld cycles\n", NT, K0,
+               k0, np, kk, tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2], tr[4] - tr[3]);
+#endif
 }
 
-// ------------------------------------------------------------------ row interchanges
-// Pivots ipiv[k0 .. k0+npiv) (absolute rows, applied in order) on the columns
-// [c_lo, c_hi) \ [s_lo, s_hi) of M (row-major, ld).  The npiv "top" rows and the
-// distinct far rows of a 32-column tile are staged in shared memory, permuted
-// there, and written back: one global round trip per tile.
-__global__ void __launch_bounds__(256) lu_swap_rm_kernel(double* Mall, int ld, long long strideM,
-                                                         const int* ipiv_all, int G, int k0, int npiv,
-                                                         int c_lo, int c_hi, int s_lo, int s_hi) {
-    __shared__ double top[LU_NB][SW_TILE + 1];
-    __shared__ double far[LU_NB][SW_TILE + 1];
-    __shared__ int prs[LU_NB];
-    __shared__ int slot[LU_NB];
-    const int b = blockIdx.y, t = threadIdx.x;
-    const int col0 = c_lo + blockIdx.x * SW_TILE;
-    if (col0 >= c_hi) return;
-    if (col0 >= s_lo && col0 + SW_TILE <= s_hi) return;  // tile entirely inside the skipped panel
-    double* M = Mall + (size_t)b * strideM;
-    const int* ipiv = ipiv_all + (size_t)b * G;
-    if (t < npiv) prs[t] = ipiv[k0 + t];
-    __syncthreads();
-    if (t < 32) {
-        for (int j = t; j < npiv; j += 32) {
-            const int pr = prs[j];
-            int s = -1;
-            if (pr >= k0 + npiv) {
-                s = j;
-                for (int q = 0; q < j; ++q)
-                    if (prs[q] == pr) {
-                        s = q;
-                        break;
-                    }
-            }
-            slot[j] = s;
-        }
-    }
-    __syncthreads();
-    const int c = t & 31;
-    const int col = col0 + c;
-    const bool live = col < c_hi && !(col >= s_lo && col < s_hi);
-    for (int r = t >> 5; r < npiv; r += 8) {
-        if (live) {
-            top[r][c] = M[(size_t)(k0 + r) * ld + col];
-            if (slot[r] == r) far[r][c] = M[(size_t)prs[r] * ld + col];
-        }
-    }
-    __syncthreads();
-    if (t < 32 && live) {
-        for (int j = 0; j < npiv; ++j) {
-            const int pr = prs[j];
-            if (pr == k0 + j) continue;
-            double* y = (pr < k0 + npiv) ? &top[pr - k0][c] : &far[slot[j]][c];
-            const double tmp = top[j][c];
-            top[j][c] = *y;
-            *y = tmp;
-        }
-    }
-    __syncthreads();
-    for (int r = t >> 5; r < npiv; r += 8) {
-        if (live) {
-            M[(size_t)(k0 + r) * ld + col] = top[r][c];
-            if (slot[r] == r) M[(size_t)prs[r] * ld + col] = far[r][c];
-        }
-    }
+__global__ void lu_map_init_kernel(int* map, long long total, int G) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x)
+        map[e] = (int)(e % G);
 }
 
 // ------------------------------------------------------------------ triangular block solves
@@ -221,28 +318,45 @@ __global__ void __launch_bounds__(256) lu_swap_rm_kernel(double* Mall, int ld, l
 template <bool LOWER>
 __global__ void __launch_bounds__(256) lu_trsm_rm_kernel(const double* Aall, int G, long long strideA,
                                                          double* Mall, int ld, long long strideM, int k0,
-                                                         int jb, int c_lo, int c_hi) {
+                                                         int jb, int c_lo, int c_hi, const int* tmap_all,
+                                                         const int* mmap_all) {
     __shared__ double Ts[LU_NB][LU_NB + 1];
+    __shared__ int s_mrow[LU_NB];
     const int b = blockIdx.y, t = threadIdx.x, lane = t & 31, w = t >> 5;
     const int col0 = c_lo + blockIdx.x * SW_TILE;
     if (col0 >= c_hi) return;
     const double* A = Aall + (size_t)b * strideA;
     double* M = Mall + (size_t)b * strideM;
-    for (int e = t; e < jb * jb; e += 256) {
-        const int r = e / jb, cc = e % jb;
-        Ts[r][cc] = A[(size_t)(k0 + r) * G + k0 + cc];
+    // T rows (positions k0..k0+jb of A) and M rows, through the row maps if given
+    const int* tmap = tmap_all ? tmap_all + (size_t)b * G : nullptr;
+    const int* mmap = mmap_all ? mmap_all + (size_t)b * G : nullptr;
+#ifdef VRTE_LU_TRACE
+    long long tr[5];
+    tr[0] = clock64();
+#endif
+    for (int r = w; r < jb; r += 8) {
+        const double* src = A + (size_t)(tmap ? tmap[k0 + r] : k0 + r) * G + k0;
+        for (int cc = lane; cc < jb; cc += 32) Ts[r][cc] = src[cc];
+        if (lane == 0) s_mrow[r] = mmap ? mmap[k0 + r] : k0 + r;
     }
     __syncthreads();
+#ifdef VRTE_LU_TRACE
+    tr[1] = clock64();
+#endif
     // lane rows r0, r1; the warp's 4 consecutive columns (one 32-byte sector per row)
     const int r0 = lane, r1 = lane + 32, cw = col0 + w * 4;
     double x0[4], x1[4];
     bool lv[4];
+    const size_t m0 = r0 < jb ? (size_t)s_mrow[r0] * ld : 0, m1 = r1 < jb ? (size_t)s_mrow[r1] * ld : 0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         lv[q] = cw + q < c_hi;
-        x0[q] = (r0 < jb && lv[q]) ? M[(size_t)(k0 + r0) * ld + cw + q] : 0.0;
-        x1[q] = (r1 < jb && lv[q]) ? M[(size_t)(k0 + r1) * ld + cw + q] : 0.0;
+        x0[q] = (r0 < jb && lv[q]) ? M[m0 + cw + q] : 0.0;
+        x1[q] = (r1 < jb && lv[q]) ? M[m1 + cw + q] : 0.0;
     }
+#ifdef VRTE_LU_TRACE
+    tr[2] = clock64();
+#endif
     if (LOWER) {
         for (int j = 0; j < jb; ++j) {
             const int src = j & 31;
@@ -271,31 +385,21 @@ __global__ void __launch_bounds__(256) lu_trsm_rm_kernel(const double* Aall, int
             }
         }
     }
+#ifdef VRTE_LU_TRACE
+    tr[3] = clock64();
+#endif
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        if (r0 < jb && lv[q]) M[(size_t)(k0 + r0) * ld + cw + q] = x0[q];
-        if (r1 < jb && lv[q]) M[(size_t)(k0 + r1) * ld + cw + q] = x1[q];
+        if (r0 < jb && lv[q]) M[m0 + cw + q] = x0[q];
+        if (r1 < jb && lv[q]) M[m1 + cw + q] = x1[q];
     }
-}
-
-// Net row permutation of the pivot sequence: out row i <- in row perm[i].
-__global__ void lu_perm_kernel(const int* ipiv_all, int* perm_all, int G) {
-    extern __shared__ int pm[];
-    const int b = blockIdx.x;
-    const int* ipiv = ipiv_all + (size_t)b * G;
-    for (int i = threadIdx.x; i < G; i += blockDim.x) pm[i] = i;
+#ifdef VRTE_LU_TRACE
     __syncthreads();
-    if (threadIdx.x == 0)
-        for (int j = 0; j < G; ++j) {
-            const int p = ipiv[j];
-            if (p != j) {
-                const int tmp = pm[j];
-                pm[j] = pm[p];
-                pm[p] = tmp;
-            }
-        }
-    __syncthreads();
-    for (int i = threadIdx.x; i < G; i += blockDim.x) perm_all[(size_t)b * G + i] = pm[i];
+    tr[4] = clock64();
+    if (t == 0 && b == 0 && blockIdx.x == 0)
+        printf("trsm%d k0=%4d jb=%2d cols=%4d | Ts %6lld  M %6lld  solve %6lld  store %6lld cycles\n", (int)LOWER, k0, jb,
+               c_hi - c_lo, tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2], tr[4] - tr[3]);
+#endif
 }
 
 __global__ void lu_gather_rows_kernel(const double* In, long long strideIn, double* Out,
@@ -313,10 +417,13 @@ __global__ void lu_gather_rows_kernel(const double* In, long long strideIn, doub
 }
 
 // C (m x n) = alpha A (m x k) B (k x n) + beta C, all row-major: the col-major
-// GEMM on the transposed views, C^T = B^T A^T.
+// GEMM on the transposed views, C^T = B^T A^T.  Optional row maps (per batch,
+// stride map_stride): row i of A is A + arow[i]*lda, row k of B is B + brow[k]*ldb,
+// row i of C is C + crow[i]*ldc (the pointers then carry only the column offset).
 void rm_gemm(int m, int n, int k, const double* A, long long lda, long long sa, const double* B,
              long long ldb, long long sb, double* C, long long ldc, long long sc, int batch,
-             double alpha, double beta, cudaStream_t st) {
+             double alpha, double beta, cudaStream_t st, const int* arow = nullptr, const int* brow = nullptr,
+             const int* crow = nullptr, long long map_stride = 0) {
     GemmBatch g{};
     g.m = n;
     g.n = m;
@@ -335,34 +442,66 @@ void rm_gemm(int m, int n, int k, const double* A, long long lda, long long sa, 
     g.batch = batch;
     g.alpha = alpha;
     g.beta = beta;
+    g.amap = brow;
+    g.bmap = arow;
+    g.cmap = crow;
+    g.map_stride = map_stride;
     gemm_batched(g, st);
 }
 
 template <int NT, int RPT, int PB>
-void panel_launch(double* A, int G, int k0, int jb, int rend, int* ipiv, DeviceStatus* status,
+void panel_launch(double* A, int G, int* map, int* ipiv, int K0, int k0, int jb, int rend, DeviceStatus* status,
                   const int* order_index, int batch, cudaStream_t st) {
-    lu_panel_rm_kernel<NT, RPT, PB><<<batch, NT, 0, st>>>(A, G, (long long)G * G, k0, jb, rend, ipiv, status,
-                                                          order_index);
+    constexpr size_t smem = PanelGeo<NT, RPT, PB>::bytes;
+    static bool attr = false;
+    if (!attr) {
+        VRTE_CUDA_CHECK(cudaFuncSetAttribute(lu_panel_crout_kernel<NT, RPT, PB>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    lu_panel_crout_kernel<NT, RPT, PB><<<batch, NT, smem, st>>>(A, G, (long long)G * G, map, ipiv, K0, k0, jb,
+                                                                rend, status, order_index);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+// the kernel's PB must be the driver's panel width (it sizes the block's L in
+// shared memory); rows per thread grow with the active height
+template <int PB>
+void panel_dispatch(int np, double* A, int G, int* map, int* ipiv, int K0, int k0, int jb, int rend,
+                    DeviceStatus* status, const int* order_index, int batch, cudaStream_t st) {
+    if (np <= 256)
+        panel_launch<256, 1, PB>(A, G, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
+    else if (np <= 512)
+        panel_launch<512, 1, PB>(A, G, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
+    else if (np <= 1024)
+        panel_launch<512, 2, PB>(A, G, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
+    else if constexpr (PB <= 8) {
+        if (np <= 2048)
+            panel_launch<512, 4, PB>(A, G, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
+        else if constexpr (PB <= 4)
+            panel_launch<512, 8, PB>(A, G, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
+        else
+            throw std::invalid_argument("lu: panel height exceeds the panel kernel");
+    } else {
+        throw std::invalid_argument("lu: panel height exceeds the panel kernel");
+    }
 }
 
 int panel_width(int G) { return G <= 1024 ? 16 : (G <= 2048 ? 8 : 4); }
 
-void swap_launch(double* M, int ld, long long strideM, const int* ipiv, int G, int k0, int npiv,
-                 int c_lo, int c_hi, int s_lo, int s_hi, int batch, cudaStream_t st) {
-    if (npiv <= 0 || c_hi <= c_lo) return;
+template <bool LOWER>
+void trsm_launch(const double* A, int G, double* M, int ld, long long strideM, int k0, int jb, int c_lo,
+                 int c_hi, int batch, cudaStream_t st, const int* tmap, const int* mmap) {
+    if (jb <= 0 || c_hi <= c_lo) return;
     dim3 grid((c_hi - c_lo + SW_TILE - 1) / SW_TILE, batch);
-    lu_swap_rm_kernel<<<grid, 256, 0, st>>>(M, ld, strideM, ipiv, G, k0, npiv, c_lo, c_hi, s_lo, s_hi);
+    lu_trsm_rm_kernel<LOWER><<<grid, 256, 0, st>>>(A, G, (long long)G * G, M, ld, strideM, k0, jb, c_lo, c_hi, tmap,
+                                                   mmap);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
-template <bool LOWER>
-void trsm_launch(const double* A, int G, double* M, int ld, long long strideM, int k0, int jb, int c_lo,
-                 int c_hi, int batch, cudaStream_t st) {
-    if (jb <= 0 || c_hi <= c_lo) return;
-    dim3 grid((c_hi - c_lo + SW_TILE - 1) / SW_TILE, batch);
-    lu_trsm_rm_kernel<LOWER><<<grid, 256, 0, st>>>(A, G, (long long)G * G, M, ld, strideM, k0, jb, c_lo,
-                                                   c_hi);
-    VRTE_CUDA_CHECK(cudaGetLastError());
+int outer_block() {
+    static const int ob = std::getenv("VRTE_LU_NB") ? std::atoi(std::getenv("VRTE_LU_NB")) : OB_MAX;
+    return ob == 64 ? 64 : OB_MAX;
 }
 
 }  // namespace
@@ -370,11 +509,14 @@ void trsm_launch(const double* A, int G, double* M, int ld, long long strideM, i
 void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatus* status,
                   const int* order_index, cudaStream_t st, int prof_d, int prof_P) {
     if (G > 4096) throw std::invalid_argument("vrte_cuda: boundary system larger than 4096 rows");
-    const int PB = panel_width(G);
-    // outer block: 128 columns (trailing GEMMs with k = 128), handled by the
-    // 64-row swap / TRSM kernels in two halves; VRTE_LU_NB=64 for A/B runs
-    static const int OB = std::getenv("VRTE_LU_NB") ? std::atoi(std::getenv("VRTE_LU_NB")) : 128;
+    const int PB = panel_width(G), OB = outer_block();
     const long long gg = (long long)G * G;
+    int* map = perm;  // the row map IS the net permutation: row i of P A = row perm[i] of A
+    {
+        const long long total = (long long)batch * G;
+        lu_map_init_kernel<<<(unsigned)min(4096LL, (total + 255) / 256), 256, 0, st>>>(map, total, G);
+        VRTE_CUDA_CHECK(cudaGetLastError());
+    }
     auto row_end = [&](int col) { return prof_d > 0 ? min(G, bnd_row_end(col, prof_d, prof_P)) : G; };
     for (int K0 = 0; K0 < G; K0 += OB) {
         const int NBk = min(OB, G - K0);
@@ -382,50 +524,30 @@ void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatu
         for (int k0 = K0; k0 < K0 + NBk; k0 += PB) {
             const int jb = min(PB, K0 + NBk - k0);
             const int np = rend - k0;
-            if (np <= 256)
-                panel_launch<256, 1, 16>(A, G, k0, jb, rend, ipiv, status, order_index, batch, st);
-            else if (np <= 512)
-                panel_launch<512, 1, 16>(A, G, k0, jb, rend, ipiv, status, order_index, batch, st);
-            else if (np <= 1024)
-                panel_launch<1024, 1, 16>(A, G, k0, jb, rend, ipiv, status, order_index, batch, st);
-            else if (np <= 2048)
-                panel_launch<512, 4, 8>(A, G, k0, jb, rend, ipiv, status, order_index, batch, st);
+            if (PB == 16)
+                panel_dispatch<16>(np, A, G, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
+            else if (PB == 8)
+                panel_dispatch<8>(np, A, G, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
             else
-                panel_launch<512, 8, 4>(A, G, k0, jb, rend, ipiv, status, order_index, batch, st);
-            VRTE_CUDA_CHECK(cudaGetLastError());
-            const int c_end = K0 + NBk, rest_in = c_end - (k0 + jb);
-            swap_launch(A, G, gg, ipiv, G, k0, jb, K0, c_end, k0, k0 + jb, batch, st);
-            if (rest_in > 0) {
-                trsm_launch<true>(A, G, A, G, gg, k0, jb, k0 + jb, c_end, batch, st);
-                if (rend - k0 - jb > 0)
-                    rm_gemm(rend - k0 - jb, rest_in, jb, A + (size_t)(k0 + jb) * G + k0, G, gg,
-                            A + (size_t)k0 * G + k0 + jb, G, gg, A + (size_t)(k0 + jb) * G + k0 + jb, G, gg,
-                            batch, -1.0, 1.0, st);
-            }
+                panel_dispatch<4>(np, A, G, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
         }
-        // the block's interchanges on the other columns, in chunks of <= 64 pivots
-        for (int p0 = K0; p0 < K0 + NBk; p0 += LU_NB)
-            swap_launch(A, G, gg, ipiv, G, p0, min(LU_NB, K0 + NBk - p0), 0, G, K0, K0 + NBk, batch, st);
         const int rest = G - K0 - NBk;
         if (rest > 0) {
-            // U12 = L11^-1 A12, blocked by 64 rows
+            // U12 = L11^-1 A12 on the block's pivot rows, by 64-row halves
             for (int r0 = K0; r0 < K0 + NBk; r0 += LU_NB) {
                 const int rb = min(LU_NB, K0 + NBk - r0);
-                trsm_launch<true>(A, G, A, G, gg, r0, rb, K0 + NBk, G, batch, st);
+                trsm_launch<true>(A, G, A, G, gg, r0, rb, K0 + NBk, G, batch, st, map, map);
                 const int below = K0 + NBk - (r0 + rb);
                 if (below > 0)
-                    rm_gemm(below, rest, rb, A + (size_t)(r0 + rb) * G + r0, G, gg, A + (size_t)r0 * G + K0 + NBk,
-                            G, gg, A + (size_t)(r0 + rb) * G + K0 + NBk, G, gg, batch, -1.0, 1.0, st);
+                    rm_gemm(below, rest, rb, A + r0, G, gg, A + K0 + NBk, G, gg, A + K0 + NBk, G, gg, batch, -1.0,
+                            1.0, st, map + r0 + rb, map + r0, map + r0 + rb, G);
             }
             // trailing update: rows past the profile have zero multipliers
             if (rend - K0 - NBk > 0)
-                rm_gemm(rend - K0 - NBk, rest, NBk, A + (size_t)(K0 + NBk) * G + K0, G, gg,
-                        A + (size_t)K0 * G + K0 + NBk, G, gg, A + (size_t)(K0 + NBk) * G + K0 + NBk, G, gg,
-                        batch, -1.0, 1.0, st);
+                rm_gemm(rend - K0 - NBk, rest, NBk, A + K0, G, gg, A + K0 + NBk, G, gg, A + K0 + NBk, G, gg, batch,
+                        -1.0, 1.0, st, map + K0 + NBk, map + K0, map + K0 + NBk, G);
         }
     }
-    lu_perm_kernel<<<batch, 256, G * sizeof(int), st>>>(ipiv, perm, G);
-    VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
 void lu_solve_rm(const double* A, int G, int batch, const int* perm, const double* Bin, double* X,
@@ -438,16 +560,15 @@ void lu_solve_rm(const double* A, int G, int batch, const int* perm, const doubl
             Bin, gn, X, gn, perm, G, ncol, batch);
         VRTE_CUDA_CHECK(cudaGetLastError());
     }
+    // L and U rows are read through the row map (perm)
     for (int k0 = 0; k0 < G; k0 += LU_NB) {
         const int jb = min(LU_NB, G - k0);
-        // (no profile here: later row interchanges move multipliers below the
-        // staircase profile of earlier columns, so L itself is dense)
         (void)prof_d;
         (void)prof_P;
-        trsm_launch<true>(A, G, X, ncol, gn, k0, jb, 0, ncol, batch, st);
+        trsm_launch<true>(A, G, X, ncol, gn, k0, jb, 0, ncol, batch, st, perm, nullptr);
         if (G - k0 - jb > 0)
-            rm_gemm(G - k0 - jb, ncol, jb, A + (size_t)(k0 + jb) * G + k0, G, gg, X + (size_t)k0 * ncol,
-                    ncol, gn, X + (size_t)(k0 + jb) * ncol, ncol, gn, batch, -1.0, 1.0, st);
+            rm_gemm(G - k0 - jb, ncol, jb, A + k0, G, gg, X + (size_t)k0 * ncol, ncol, gn,
+                    X + (size_t)(k0 + jb) * ncol, ncol, gn, batch, -1.0, 1.0, st, perm + k0 + jb, nullptr, nullptr, G);
     }
     // back substitution only down to row_lo: the unknowns above it are not
     // wanted (X rows < row_lo are left holding the forward solution)
@@ -455,30 +576,23 @@ void lu_solve_rm(const double* A, int G, int batch, const int* perm, const doubl
     const int blo = max(0, row_lo) / LU_NB, rl = blo * LU_NB;
     for (int bk = nblk - 1; bk >= blo; --bk) {
         const int k0 = bk * LU_NB, jb = min(LU_NB, G - k0);
-        trsm_launch<false>(A, G, X, ncol, gn, k0, jb, 0, ncol, batch, st);
+        trsm_launch<false>(A, G, X, ncol, gn, k0, jb, 0, ncol, batch, st, perm, nullptr);
         if (k0 > rl)
-            rm_gemm(k0 - rl, ncol, jb, A + (size_t)rl * G + k0, G, gg, X + (size_t)k0 * ncol, ncol, gn,
-                    X + (size_t)rl * ncol, ncol, gn, batch, -1.0, 1.0, st);
+            rm_gemm(k0 - rl, ncol, jb, A + k0, G, gg, X + (size_t)k0 * ncol, ncol, gn, X + (size_t)rl * ncol, ncol,
+                    gn, batch, -1.0, 1.0, st, perm + rl, nullptr, nullptr, G);
     }
 }
 
 int lu_rm_launch_count(int G) {
-    const int PB = panel_width(G);
-    static const int OB = std::getenv("VRTE_LU_NB") ? std::atoi(std::getenv("VRTE_LU_NB")) : 128;
-    int n = 0;
+    const int PB = panel_width(G), OB = outer_block();
+    int n = 1;  // row map init
     for (int K0 = 0; K0 < G; K0 += OB) {
         const int NBk = min(OB, G - K0);
-        for (int k0 = K0; k0 < K0 + NBk; k0 += PB) {
-            const int jb = min(PB, K0 + NBk - k0);
-            n += 2;  // panel + swap
-            if (K0 + NBk - (k0 + jb) > 0) n += 1 + (G - k0 - jb > 0 ? 1 : 0);
-        }
-        n += (NBk + LU_NB - 1) / LU_NB;
+        n += (NBk + PB - 1) / PB;  // fused Crout panels
         if (G - K0 - NBk > 0) n += 2 * ((NBk + LU_NB - 1) / LU_NB) - 1 + 1;
     }
-    n += 1;                                          // perm
     const int nblk = (G + LU_NB - 1) / LU_NB;
-    n += 1 + 2 * nblk - 1 + 2 * nblk - 1;            // gather + forward + backward (upper bound)
+    n += 1 + 2 * nblk - 1 + 2 * nblk - 1;  // gather + forward + backward (upper bound)
     return n;
 }
 
