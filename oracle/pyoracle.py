@@ -220,3 +220,28 @@ def brdf(mat: Material, N, mu_in, n_dphi=19, basis=None, order_cap=0, threads=0,
         cc = comps[0::2] + 1j * comps[1::2]
         return out, t, cc.reshape(len(mu), 4, L, 2, 4 * N)
     return out, t
+
+
+def radiance(mat: Material, N, mu0, phi0, stokes, taus=(0.0,), zenith=11, azimuth=19, mus=None,
+             phis=None, nodal=False, order_cap=0, threads=0):
+    """capi.cpp:138-174 restated: (values [n_tau, n_mu, n_phi, 4], mus, phis,
+    reflectance[4]).  nodal=True: discrete-ordinate stacks at +nodes, -nodes."""
+    tv = np.ascontiguousarray(taus, np.float64)
+    st = np.ascontiguousarray(stokes, np.float64)
+    mu_in = None if mus is None else np.ascontiguousarray(mus, np.float64)
+    ph_in = None if phis is None else np.ascontiguousarray(phis, np.float64)
+    n_mu = 2 * N if nodal else (len(mu_in) if mu_in is not None else 2 * zenith)
+    n_ph = len(ph_in) if ph_in is not None else azimuth
+    vals = np.zeros((max(1, len(tv)), n_mu, n_ph, 4))
+    mo = np.zeros(n_mu)
+    po = np.zeros(n_ph)
+    refl = np.zeros(4)
+    tm = OracleTimings()
+    cm = mat.c()
+    lib().oracle_radiance_at.argtypes = None
+    _check(lib().oracle_radiance_at(C.byref(cm), N, order_cap, threads, C.c_double(mu0), C.c_double(phi0),
+                                    _dp(st), _dp(tv), C.c_size_t(len(tv)), zenith, azimuth, _dp(mu_in),
+                                    C.c_size_t(0 if mu_in is None else len(mu_in)), _dp(ph_in),
+                                    C.c_size_t(0 if ph_in is None else len(ph_in)), 1 if nodal else 0,
+                                    _dp(mo), _dp(po), _dp(vals), _dp(refl), C.byref(tm)))
+    return vals, mo, po, refl

@@ -310,6 +310,29 @@ static KColumn beam_column(int m, const Layer& layer, const Quad& q, double mu_b
     return c;
 }
 
+struct KRow {
+    std::vector<M4> plus, minus;
+};
+// kernel.cpp:67-87: A^m(mu, +mu_j) and A^m(mu, -mu_j) for an arbitrary signed mu
+static KRow kernel_row(int m, const Layer& layer, const Quad& q, double mu) {
+    const int n = q.n, L = layer.order_count();
+    KRow row;
+    row.plus.assign(n, M4{});
+    row.minus.assign(n, M4{});
+    if (m >= L) return row;
+    const Gsf g = gsf_seq(m, L - 1, mu);
+    std::vector<Gsf> tab(n);
+    for (int j = 0; j < n; ++j) tab[j] = gsf_seq(m, L - 1, q.nodes[j]);
+    for (int j = 0; j < n; ++j)
+        for (int l = m; l < L; ++l) {
+            const M4 left = mul(gsf_matrix(g, l, false), layer.coeffs[l]);
+            const double sgn = ((l - m) & 1) ? -1.0 : 1.0;
+            axpy4(row.plus[j], 1.0, mul(left, gsf_matrix(tab[j], l, false)));
+            axpy4(row.minus[j], sgn, mul(left, gsf_matrix(tab[j], l, true)));
+        }
+    return row;
+}
+
 // ---------------------------------------------------------------- dense helpers (col-major)
 static void dgemm(char ta, char tb, int m, int n, int k, double alpha, const double* a, int lda,
                   const double* b, int ldb, double beta, double* c, int ldc) {
@@ -1091,6 +1114,233 @@ static double now_s() {
         .count();
 }
 
+// ---------------------------------------------------------------- radiance reconstruction
+// reconstruction.cpp:28-199: source-function integration along an arbitrary
+// direction, per (order, k) chain of layers.
+using V4c = std::array<cd, 4>;
+struct SrcCoeffs {
+    std::vector<std::pair<cd, V4c>> from_top, from_bottom;
+    V4c beam{};
+    double mu0 = 1.0, thickness = 0.0;
+};
+static void add4(V4c& a, cd s, const V4c& x) {
+    for (int c = 0; c < 4; ++c) a[c] += s * x[c];
+}
+static V4c mat4v(const M4& a, const cd* x) {  // A (real 4x4) * complex 4-vector
+    V4c o{};
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c) o[r] += a(r, c) * x[c];
+    return o;
+}
+struct ChainEntry {
+    const Layer* layer;
+    const ModeSet* modes;
+    const Part* part;
+    std::vector<cd> coef_a, coef_b;
+    double tau_top, thickness, beam_top;
+};
+// reconstruction.cpp:28-72
+static SrcCoeffs source_coefficients(const ChainEntry& e, const Quad& q, int k, double mu0, const double* stokes,
+                                     const KRow& row, const M4& beam_block) {
+    const int n = q.n;
+    const double half_omega = 0.5 * e.layer->omega;
+    SrcCoeffs out;
+    out.mu0 = mu0;
+    out.thickness = e.thickness;
+    std::vector<M4> wp(n), wm(n);
+    for (int i = 0; i < n; ++i) {
+        axpy4(wp[i], q.weights[i], row.plus[i]);
+        axpy4(wm[i], q.weights[i], row.minus[i]);
+    }
+    for (size_t j = 0; j < e.modes->modes.size(); ++j) {
+        const Mode& md = e.modes->modes[j];
+        const auto down_a = block_parity(md.psi_minus), down_b = block_parity(md.psi_plus);
+        V4c aa{}, ab{};
+        for (int i = 0; i < n; ++i) {
+            const V4c t1 = mat4v(wp[i], &md.psi_plus[4 * i]), t2 = mat4v(wm[i], &down_a[4 * i]);
+            const V4c t3 = mat4v(wp[i], &md.psi_minus[4 * i]), t4 = mat4v(wm[i], &down_b[4 * i]);
+            for (int c = 0; c < 4; ++c) {
+                aa[c] += t1[c] + t2[c];
+                ab[c] += t3[c] + t4[c];
+            }
+        }
+        V4c ta{}, tb{};
+        add4(ta, half_omega * e.coef_a[j], aa);
+        add4(tb, half_omega * e.coef_b[j], ab);
+        out.from_top.emplace_back(md.nu, ta);
+        out.from_bottom.emplace_back(md.nu, tb);
+    }
+    V4c beam{};
+    for (int i = 0; i < n; ++i) {
+        cd zp[4], zm[4];
+        for (int c = 0; c < 4; ++c) {
+            zp[c] = e.part->zp[4 * i + c];
+            zm[c] = e.part->zm[4 * i + c];
+        }
+        const V4c t1 = mat4v(wp[i], zp), t2 = mat4v(wm[i], zm);
+        for (int c = 0; c < 4; ++c) beam[c] += t1[c] + t2[c];
+    }
+    for (auto& b : beam) b *= half_omega;
+    cd sel[4];
+    for (int c = 0; c < 4; ++c) sel[c] = ((k == 1) == (c < 2)) ? stokes[c] : 0.0;  // kernel.cpp:124-128
+    const V4c bb = mat4v(beam_block, sel);
+    add4(beam, e.layer->omega / (2.0 * kPi), bb);
+    for (int c = 0; c < 4; ++c) out.beam[c] = e.beam_top * beam[c];
+    return out;
+}
+constexpr double kDegenerateRate = 1e-9;  // reconstruction.cpp:85
+// reconstruction.cpp:87-121
+static V4c up_top(cd a, const V4c& c, double mu, double t, double d) {
+    const cd f = (std::exp(-t / a) - std::exp(-d / a) * std::exp(-(d - t) / mu)) / (1.0 + mu / a);
+    V4c o;
+    for (int q = 0; q < 4; ++q) o[q] = c[q] * f;
+    return o;
+}
+static V4c up_bottom(cd b, const V4c& c, double mu, double t, double d) {
+    cd f;
+    if (std::abs(1.0 / mu - 1.0 / b) < kDegenerateRate)
+        f = std::exp(-(d - t) / mu) * ((d - t) / mu);
+    else
+        f = (std::exp(-(d - t) / b) - std::exp(-(d - t) / mu)) / (1.0 - mu / b);
+    V4c o;
+    for (int q = 0; q < 4; ++q) o[q] = c[q] * f;
+    return o;
+}
+static V4c down_top(cd a, const V4c& c, double mu, double t) {
+    cd f;
+    if (std::abs(1.0 / mu - 1.0 / a) < kDegenerateRate)
+        f = std::exp(-t / mu) * (t / mu);
+    else
+        f = (std::exp(-t / a) - std::exp(-t / mu)) / (1.0 - mu / a);
+    V4c o;
+    for (int q = 0; q < 4; ++q) o[q] = c[q] * f;
+    return o;
+}
+static V4c down_bottom(cd b, const V4c& c, double mu, double t, double d) {
+    const cd f = (std::exp(-(d - t) / b) - std::exp(-d / b) * std::exp(-t / mu)) / (1.0 + mu / b);
+    V4c o;
+    for (int q = 0; q < 4; ++q) o[q] = c[q] * f;
+    return o;
+}
+// reconstruction.cpp:123-149
+static V4c integrate_up(const SrcCoeffs& s, double mu, double t, const V4c& ib) {
+    const double d = s.thickness;
+    V4c v;
+    for (int q = 0; q < 4; ++q) v[q] = ib[q] * std::exp(-(d - t) / mu);
+    for (const auto& [a, c] : s.from_top) add4(v, 1.0, up_top(a, c, mu, t, d));
+    for (const auto& [b, c] : s.from_bottom) add4(v, 1.0, up_bottom(b, c, mu, t, d));
+    add4(v, 1.0, up_top(cd(s.mu0, 0.0), s.beam, mu, t, d));
+    return v;
+}
+static V4c integrate_down(const SrcCoeffs& s, double mu, double t, const V4c& it) {
+    const double d = s.thickness;
+    V4c v;
+    for (int q = 0; q < 4; ++q) v[q] = it[q] * std::exp(-t / mu);
+    for (const auto& [a, c] : s.from_top) add4(v, 1.0, down_top(a, c, mu, t));
+    for (const auto& [b, c] : s.from_bottom) add4(v, 1.0, down_bottom(b, c, mu, t, d));
+    add4(v, 1.0, down_top(cd(s.mu0, 0.0), s.beam, mu, t));
+    return v;
+}
+// boundary.cpp:20-35 (chain_stacks): up/down nodal stacks of one chain entry at local depth t
+static void chain_stacks(const ChainEntry& e, double mu0, double t, std::vector<cd>& up, std::vector<cd>& down) {
+    const int d = (int)e.part->zp.size();
+    up.assign(d, 0.0);
+    down.assign(d, 0.0);
+    for (size_t j = 0; j < e.modes->modes.size(); ++j) {
+        const Mode& md = e.modes->modes[j];
+        const cd ea = e.coef_a[j] * std::exp(-t / md.nu);
+        const cd eb = e.coef_b[j] * std::exp(-(e.thickness - t) / md.nu);
+        const auto dm = block_parity(md.psi_minus), dp = block_parity(md.psi_plus);
+        for (int i = 0; i < d; ++i) {
+            up[i] += ea * md.psi_plus[i] + eb * md.psi_minus[i];
+            down[i] += ea * dm[i] + eb * dp[i];
+        }
+    }
+    const double beam = e.beam_top * std::exp(-t / mu0);
+    for (int i = 0; i < d; ++i) {
+        up[i] += beam * e.part->zp[i];
+        down[i] += beam * e.part->zm[i];
+    }
+}
+// reconstruction.cpp:151-199
+static std::vector<V4c> reconstruct_component(const std::vector<ChainEntry>& chain, const Quad& q, int m, int k,
+                                              double mu0, const double* stokes, const Base& base, double mu_signed,
+                                              const std::vector<double>& taus, const std::vector<KRow>& rows,
+                                              const std::vector<M4>& beam_blocks) {
+    const int P = (int)chain.size();
+    const double mu = std::abs(mu_signed);
+    std::vector<SrcCoeffs> co(P);
+    for (int p = 0; p < P; ++p) co[p] = source_coefficients(chain[p], q, k, mu0, stokes, rows[p], beam_blocks[p]);
+    std::vector<std::pair<int, double>> tg(taus.size());
+    for (size_t it = 0; it < taus.size(); ++it) {  // reconstruction.cpp:12-19 locate_layer
+        int p = 0;
+        while (p + 1 < P && taus[it] >= chain[p].tau_top + chain[p].thickness) ++p;
+        tg[it] = {p, std::clamp(taus[it] - chain[p].tau_top, 0.0, chain[p].thickness)};
+    }
+    std::vector<V4c> out(taus.size(), V4c{});
+    V4c bnd{};
+    if (mu_signed <= 0.0) {
+        for (int p = 0; p < P; ++p) {
+            for (size_t it = 0; it < taus.size(); ++it)
+                if (tg[it].first == p) out[it] = integrate_down(co[p], mu, tg[it].second, bnd);
+            bnd = integrate_down(co[p], mu, chain[p].thickness, bnd);
+        }
+        return out;
+    }
+    if (m == 0 && base.type != 0) {
+        const ChainEntry& last = chain.back();
+        const double tau_total = last.tau_top + last.thickness;
+        std::vector<cd> upn, dnn;
+        chain_stacks(last, mu0, last.thickness, upn, dnn);
+        for (int j = 0; j < q.n; ++j) {
+            const M4 r = base_row_at(base, q, mu, q.nodes[j]);
+            const V4c v = mat4v(r, &dnn[4 * j]);
+            add4(bnd, q.weights[j] * q.nodes[j], v);
+        }
+        const M4 rb = base_row_at(base, q, mu, mu0);
+        double sv[4] = {0, 0, 0, 0};
+        for (int r = 0; r < 4; ++r)
+            for (int c = 0; c < 4; ++c) sv[r] += rb(r, c) * stokes[c];
+        const double f = (mu0 / kPi) * std::exp(-tau_total / mu0);
+        for (int c = 0; c < 4; ++c)
+            if ((k == 1) == (c < 2)) bnd[c] += f * sv[c];
+    }
+    for (int p = P - 1; p >= 0; --p) {
+        for (size_t it = 0; it < taus.size(); ++it)
+            if (tg[it].first == p) out[it] = integrate_up(co[p], mu, tg[it].second, bnd);
+        bnd = integrate_up(co[p], mu, 0.0, bnd);
+    }
+    return out;
+}
+// reconstruction.cpp:201-227
+static void assemble_field(const std::vector<std::array<V4c, 2>>& comps, double dphi, double out[4]) {
+    const double x = -dphi;
+    cd tot[4] = {0, 0, 0, 0};
+    double scale = 0.0, imag = 0.0;
+    for (size_t m = 0; m < comps.size(); ++m) {
+        const double sc = (m == 0) ? 1.0 : 2.0, c = std::cos(m * x), s = std::sin(m * x);
+        const double p1[4] = {sc * c, sc * c, sc * s, sc * s}, p2[4] = {-sc * s, -sc * s, sc * c, sc * c};
+        for (int q = 0; q < 4; ++q) {
+            tot[q] += 0.5 * (p1[q] * comps[m][0][q] + p2[q] * comps[m][1][q]);
+            scale = std::max({scale, std::abs(comps[m][0][q]), std::abs(comps[m][1][q])});
+        }
+    }
+    for (int q = 0; q < 4; ++q) imag = std::max(imag, std::abs(tot[q].imag()));
+    if (imag > 1e-9 * scale + 1e-300) {
+        char buf[200];
+        std::snprintf(buf, sizeof buf,
+                      "imaginary residue %g exceeds tolerance (scale %g); conjugate mode pairing is broken", imag,
+                      scale);
+        throw NumericalError(buf);
+    }
+    for (int q = 0; q < 4; ++q) out[q] = tot[q].real();
+}
+static double reduce_azimuth(double phi) {  // types.cpp:7-12
+    double r = std::fmod(phi, kTwoPi);
+    if (r < 0.0) r += kTwoPi;
+    return r;
+}
+
 struct OrderState {
     Kernel kernel;
     Reduced ops;
@@ -1234,6 +1484,160 @@ class Solver {
             t.boundary += now_s() - t0;
         }
         return up;
+    }
+
+    // pipeline.cpp:253-309 (radiance_field) on the solve_incident chains
+    // (pipeline.cpp:95-199), brdf.cpp:142-160 (field reflectance).
+    // values [n_tau][n_mu][n_phi][4]
+    void radiance(double mu0, double phi0, const double* stokes, const std::vector<double>& taus,
+                  const std::vector<double>& mus, const std::vector<double>& phis, double* values,
+                  double* reflectance, bool nodal = false) {
+        prepare_homogeneous();
+        if (!(mu0 > 0.0 && mu0 <= 1.0)) throw ValidationError("incident mu0 must lie in (0,1]");
+        const int P = (int)spec_.layers.size(), S = (int)rep_.size();
+        const double t0 = now_s();
+        std::vector<Part> parts((size_t)L_ * 2 * S);
+        std::vector<std::string> fail(std::max(parts.size(), (size_t)L_));
+        parallel_for(threads_, parts.size(), [&](size_t idx) {
+            const int m = (int)(idx / (2 * S)), k = (int)((idx / S) % 2) + 1, s = (int)(idx % S);
+            try {
+                const Layer& layer = spec_.layers[rep_[s]];
+                const auto& st = states_[s][m];
+                parts[idx] = solve_particular(st.ops, build_source(m, k, layer, mu0, stokes, quad_), st.modes,
+                                              st.kernel);
+            } catch (const std::exception& e) {
+                fail[idx] = e.what();
+            }
+        });
+        for (const auto& f : fail)
+            if (!f.empty()) throw NumericalError(f);
+        std::vector<double> tau_top(P, 0.0);
+        for (int p = 1; p < P; ++p) tau_top[p] = tau_top[p - 1] + spec_.layers[p - 1].tau;
+        // chains[m][k][p]
+        std::vector<std::array<std::vector<ChainEntry>, 2>> chains(L_);
+        parallel_for(threads_, (size_t)L_, [&](size_t mi) {
+            const int m = (int)mi;
+            try {
+                std::vector<const ModeSet*> ms(P);
+                std::vector<const Part*> pk[2];
+                pk[0].resize(P);
+                pk[1].resize(P);
+                for (int p = 0; p < P; ++p) {
+                    ms[p] = &states_[sig_[p]][m].modes;
+                    pk[0][p] = &parts[((size_t)m * 2 + 0) * S + sig_[p]];
+                    pk[1][p] = &parts[((size_t)m * 2 + 1) * S + sig_[p]];
+                }
+                const OrderBoundary ob = solve_boundary(spec_, mu0, stokes, quad_, m, ms, pk);
+                for (int k = 0; k < 2; ++k) {
+                    auto& ch = chains[m][k];
+                    ch.resize(P);
+                    for (int p = 0; p < P; ++p) {
+                        ch[p].layer = &spec_.layers[p];
+                        ch[p].modes = ms[p];
+                        ch[p].part = pk[k][p];
+                        ch[p].coef_a = ob.coef[k][p].a;
+                        ch[p].coef_b = ob.coef[k][p].b;
+                        ch[p].tau_top = tau_top[p];
+                        ch[p].thickness = spec_.layers[p].tau;
+                        ch[p].beam_top = std::exp(-tau_top[p] / mu0);
+                    }
+                }
+            } catch (const std::exception& e) {
+                fail[m] = e.what();
+            }
+        });
+        for (const auto& f : fail)
+            if (!f.empty()) throw NumericalError(f);
+        t.boundary_solves += L_;
+        const size_t nt = taus.size(), nm = mus.size(), nph = phis.size();
+        if (nodal) {
+            // discrete-ordinate stacks at the nodes (reconstruction.cpp:20-26 nodal_stacks):
+            // mus = +nodes then -nodes
+            const int N = quad_.n;
+            for (size_t it = 0; it < nt; ++it) {
+                std::vector<std::array<std::vector<cd>, 2>> up(L_), dn(L_);
+                for (int m = 0; m < L_; ++m)
+                    for (int k = 0; k < 2; ++k) {
+                        const auto& ch = chains[m][k];
+                        int p = 0;
+                        while (p + 1 < P && taus[it] >= ch[p].tau_top + ch[p].thickness) ++p;
+                        const double tl = std::clamp(taus[it] - ch[p].tau_top, 0.0, ch[p].thickness);
+                        chain_stacks(ch[p], mu0, tl, up[m][k], dn[m][k]);
+                    }
+                for (int sgn = 0; sgn < 2; ++sgn)
+                    for (int i = 0; i < N; ++i) {
+                        std::vector<std::array<V4c, 2>> comps(L_);
+                        for (int m = 0; m < L_; ++m)
+                            for (int k = 0; k < 2; ++k)
+                                for (int c = 0; c < 4; ++c)
+                                    comps[m][k][c] = (sgn == 0 ? up : dn)[m][k][4 * i + c];
+                        for (size_t ip = 0; ip < nph; ++ip)
+                            assemble_field(comps, phis[ip] - phi0,
+                                           values + ((it * (2 * N) + sgn * N + i) * nph + ip) * 4);
+                    }
+            }
+            return;
+        }
+        std::vector<std::string> fail2(nm);
+        parallel_for(threads_, nm, [&](size_t imu) {
+            try {
+                const double mu = mus[imu];
+                std::vector<std::vector<std::array<V4c, 2>>> per_tau(nt, std::vector<std::array<V4c, 2>>(L_));
+                for (int m = 0; m < L_; ++m) {
+                    std::vector<KRow> rows(P);
+                    std::vector<M4> bb(P);
+                    for (int p = 0; p < P; ++p) {  // pipeline.cpp:237-258 direction_kernels
+                        const Layer& layer = spec_.layers[p];
+                        rows[p] = kernel_row(m, layer, quad_, mu);
+                        if (m < layer.order_count()) {
+                            const Gsf go = gsf_seq(m, layer.order_count() - 1, mu),
+                                      gi = gsf_seq(m, layer.order_count() - 1, -mu0);
+                            for (int l = m; l < layer.order_count(); ++l)
+                                axpy4(bb[p], 1.0,
+                                      mul(mul(gsf_matrix(go, l, false), layer.coeffs[l]), gsf_matrix(gi, l, false)));
+                        }
+                    }
+                    for (int k = 0; k < 2; ++k) {
+                        const auto v = reconstruct_component(chains[m][k], quad_, m, k + 1, mu0, stokes, spec_.base, mu,
+                                                             taus, rows, bb);
+                        for (size_t it = 0; it < nt; ++it) per_tau[it][m][k] = v[it];
+                    }
+                }
+                for (size_t it = 0; it < nt; ++it)
+                    for (size_t ip = 0; ip < nph; ++ip)
+                        assemble_field(per_tau[it], phis[ip] - phi0, values + ((it * nm + imu) * nph + ip) * 4);
+            } catch (const std::exception& e) {
+                fail2[imu] = e.what();
+            }
+        });
+        for (const auto& f : fail2)
+            if (!f.empty()) throw NumericalError(f);
+        t.reconstruction_items += nm * nt;
+        if (reflectance) {
+            // nodal components at tau = 0 (layer 0, t = 0), 19 azimuths (brdf.hpp:46-48)
+            const int n_phi = 19, N = quad_.n;
+            std::vector<std::array<std::vector<cd>, 2>> up(L_);
+            for (int m = 0; m < L_; ++m)
+                for (int k = 0; k < 2; ++k) {
+                    std::vector<cd> dn;
+                    chain_stacks(chains[m][k][0], mu0, 0.0, up[m][k], dn);
+                }
+            double flux[4] = {0, 0, 0, 0};
+            for (int i = 0; i < N; ++i)
+                for (int j = 0; j < n_phi; ++j) {
+                    std::vector<std::array<V4c, 2>> comps(L_);
+                    for (int m = 0; m < L_; ++m)
+                        for (int k = 0; k < 2; ++k)
+                            for (int c = 0; c < 4; ++c) comps[m][k][c] = up[m][k][4 * i + c];
+                    double sv[4];
+                    assemble_field(comps, kTwoPi * j / n_phi, sv);
+                    const double w = quad_.weights[i] * quad_.nodes[i] * (kTwoPi / n_phi);
+                    for (int c = 0; c < 4; ++c) flux[c] += w * sv[c];
+                }
+            const double inc = std::max(mu0 * stokes[0], 1e-300);
+            for (int c = 0; c < 4; ++c) reflectance[c] = flux[c] / inc;
+        }
+        t.reconstruction += now_s() - t0;
     }
 
   private:
@@ -1547,6 +1951,62 @@ int32_t oracle_brdf(const oracle_material* cm, int32_t quad_n, int32_t order_cap
         const auto mat = vo::from_c(cm);
         vo::compute_brdf(mat, quad_n, order_cap, th, mu_in, n_in, n_dphi > 0 ? n_dphi : 19, basis,
                          out, timings, up_components);
+    });
+}
+
+
+// capi.cpp:138-174 (vrte_solve_radiance) restated: grids from pipeline.cpp:358-390.
+int32_t oracle_radiance_at(const oracle_material* cm, int32_t quad_n, int32_t order_cap, int32_t threads,
+                           double mu0, double phi0, const double* stokes, const double* taus, size_t n_tau,
+                           int32_t zenith, int32_t azimuth, const double* mus_in, size_t n_mu_in,
+                           const double* phis_in, size_t n_phi_in, int32_t nodal, double* mus_out,
+                           double* phis_out, double* values, double* reflectance, oracle_timings* timings);
+int32_t oracle_radiance(const oracle_material* cm, int32_t quad_n, int32_t order_cap, int32_t threads, double mu0,
+                        double phi0, const double* stokes, const double* taus, size_t n_tau, int32_t zenith,
+                        int32_t azimuth, double* mus_out, double* phis_out, double* values, double* reflectance,
+                        oracle_timings* timings) {
+    return oracle_radiance_at(cm, quad_n, order_cap, threads, mu0, phi0, stokes, taus, n_tau, zenith, azimuth,
+                              nullptr, 0, nullptr, 0, 0, mus_out, phis_out, values, reflectance, timings);
+}
+
+int32_t oracle_radiance_at(const oracle_material* cm, int32_t quad_n, int32_t order_cap, int32_t threads,
+                           double mu0, double phi0, const double* stokes, const double* taus, size_t n_tau,
+                           int32_t zenith, int32_t azimuth, const double* mus_in, size_t n_mu_in,
+                           const double* phis_in, size_t n_phi_in, int32_t nodal, double* mus_out,
+                           double* phis_out, double* values, double* reflectance, oracle_timings* timings) {
+    if (!cm || !stokes || !values || (n_tau > 0 && !taus) || zenith < 1 || azimuth < 1) {
+        g_err = "null argument";
+        return 5;
+    }
+    return guarded([&] {
+        int th = threads;
+        if (th <= 0) th = (int)std::max(1u, std::thread::hardware_concurrency());
+        const auto mat = vo::from_c(cm);
+        vo::Solver solver(mat, quad_n, order_cap, th);
+        std::vector<double> tv(taus, taus + n_tau);
+        if (tv.empty()) tv.push_back(0.0);
+        std::vector<double> up(zenith);
+        for (int i = 0; i < zenith; ++i)
+            up[i] = zenith == 1 ? 1.0 : std::clamp((double)i / (zenith - 1), 1e-6, 1.0);  // clamp_mu, kMinMu
+        std::vector<double> mus;
+        for (double m : up) mus.push_back(m);
+        for (double m : up) mus.push_back(-m);
+        std::vector<double> phis(azimuth);
+        const double p0 = vo::reduce_azimuth(phi0);
+        for (int j = 0; j < azimuth; ++j)
+            phis[j] = azimuth == 1 ? p0 : vo::reduce_azimuth(p0 + vo::kPi * j / (azimuth - 1));
+        if (mus_in && n_mu_in) mus.assign(mus_in, mus_in + n_mu_in);
+        if (phis_in && n_phi_in) phis.assign(phis_in, phis_in + n_phi_in);
+        if (nodal) {  // +nodes then -nodes
+            const auto& q = solver.quad();
+            mus.clear();
+            for (int i = 0; i < q.n; ++i) mus.push_back(q.nodes[i]);
+            for (int i = 0; i < q.n; ++i) mus.push_back(-q.nodes[i]);
+        }
+        solver.radiance(mu0, p0, stokes, tv, mus, phis, values, reflectance, nodal != 0);
+        if (mus_out) std::copy(mus.begin(), mus.end(), mus_out);
+        if (phis_out) std::copy(phis.begin(), phis.end(), phis_out);
+        if (timings) *timings = solver.t;
     });
 }
 

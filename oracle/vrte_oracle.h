@@ -87,6 +87,23 @@ int32_t oracle_brdf(const oracle_material* mat, int32_t quad_n, int32_t order_ca
                     const double* mu_in, size_t n_in, int32_t n_dphi, const double* basis,
                     double* out, oracle_timings* timings, double* up_components);
 
+/* capi.cpp:138-174 vrte_solve_radiance: field at optical depths taus (n_tau = 0
+ * -> {0}) on the signed zenith grid (2*zenith) x azimuth grid, from the beam
+ * (mu0, phi0, stokes).  values [n_tau][2*zenith][azimuth][4]; reflectance [4]
+ * (brdf.cpp:142-160); mus_out [2*zenith], phis_out [azimuth] may be NULL. */
+int32_t oracle_radiance(const oracle_material* mat, int32_t quad_n, int32_t order_cap, int32_t threads, double mu0,
+                        double phi0, const double* stokes, const double* taus, size_t n_tau, int32_t zenith,
+                        int32_t azimuth, double* mus_out, double* phis_out, double* values, double* reflectance,
+                        oracle_timings* timings);
+/* Same with explicit signed directions / azimuths (NULL/0 -> grids); nodal = 1
+ * returns the discrete-ordinate stacks at +nodes then -nodes (reconstruction.cpp:20-26)
+ * instead of the source-function integration (values [n_tau][2N][n_phi][4]). */
+int32_t oracle_radiance_at(const oracle_material* mat, int32_t quad_n, int32_t order_cap, int32_t threads,
+                           double mu0, double phi0, const double* stokes, const double* taus, size_t n_tau,
+                           int32_t zenith, int32_t azimuth, const double* mus_in, size_t n_mu_in,
+                           const double* phis_in, size_t n_phi_in, int32_t nodal, double* mus_out,
+                           double* phis_out, double* values, double* reflectance, oracle_timings* timings);
+
 #ifdef __cplusplus
 }
 #endif
