@@ -75,6 +75,24 @@ typedef struct vrte_cuda_result {
     char message[512];
 } vrte_cuda_result;
 
+/* Radiance field (capi.cpp:138-174 / reconstruction.cpp:28-227):
+ * the problem carries ONE incident (n_in = 1, mu_in[0] = the beam's mu0); the
+ * field is evaluated at every (tau, signed mu, phi) of the grid. */
+typedef struct vrte_cuda_radiance {
+    int32_t n_tau, n_mu, n_phi;
+    const double* taus;       /* [n_tau] optical depths */
+    const double* mus;        /* [n_mu] signed output cosines (> 0 upward) */
+    const double* phis;       /* [n_phi] azimuths */
+    double phi0;              /* beam azimuth */
+    double stokes[4];         /* beam I0 */
+    const double* base_out;   /* [n_mu][N][16] base_row_at(|mu_o|, node_j) (m = 0, non-black base) */
+    const double* base_beam;  /* [n_mu][16] base_row_at(|mu_o|, mu0) */
+} vrte_cuda_radiance;
+
+/* values [n_tau][n_mu][n_phi][4] (host), reflectance [4] (brdf.cpp:142-160). */
+VRTE_API int32_t vrte_cuda_radiance_field(const vrte_cuda_problem* problem, const vrte_cuda_radiance* rad,
+                                          double* values, double* reflectance, vrte_cuda_result* result);
+
 /* Full solve: host inputs -> host table [n_in][N][n_dphi][16]. */
 VRTE_API int32_t vrte_cuda_brdf(const vrte_cuda_problem* problem, double* table,
                                 vrte_cuda_result* result);

@@ -137,6 +137,7 @@ EXPORTED = [
     "vrte_cuda_plan_fetch_up", "vrte_cuda_plan_fetch_modes", "vrte_cuda_plan_fetch_ef",
     "vrte_cuda_plan_destroy",
     "vrte_cuda_synthesize", "vrte_cuda_device_count", "vrte_cuda_lu_solve", "vrte_cuda_hessenberg", "vrte_cuda_schur",
+    "vrte_cuda_radiance_field",
 ]
 
 
@@ -183,6 +184,12 @@ def lib():
     L.vrte_cuda_hessenberg.argtypes = [dp, C.c_int32, C.c_int32, dp, dp, C.c_int32, C.c_int32]
     L.vrte_cuda_schur.argtypes = [dp, C.c_int32, C.c_int32, dp, dp, dp, dp, C.c_int32]
     L.vrte_solve_radiance.argtypes = [vp, C.POINTER(Options), dp, C.c_size_t, C.POINTER(vp)]
+    L.vrte_field_size.argtypes = [vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]
+    L.vrte_field_row.argtypes = [vp, C.c_size_t, C.c_size_t, C.c_size_t, dp]
+    L.vrte_field_write_csv.argtypes = [vp, C.c_char_p]
+    L.vrte_field_timings.argtypes = [vp, C.POINTER(Timings)]
+    L.vrte_field_reflectance.argtypes = [vp, dp]
+    L.vrte_field_free.argtypes = [vp]
     L.vrte_mc_trace.argtypes = [vp, C.POINTER(Options), C.c_uint64, C.c_uint64, C.c_int32,
                                 C.c_int32, C.POINTER(vp)]
     _lib = L
@@ -356,6 +363,68 @@ def compute_brdf(material: Material, opts: Options, mu_in, n_dphi: int = 19, bas
     _check(lib().vrte_compute_brdf(material._h, C.byref(opts), _dp(mu), len(mu), n_dphi, _dp(b),
                                    C.byref(h)))
     return Brdf(h)
+
+
+class Field:
+    """Opaque vrte_field handle (vrte.h:87-98): radiance on the (tau, signed mu, phi) grid."""
+
+    def __init__(self, handle):
+        self._h = handle
+        nt, nm, npd = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        _check(lib().vrte_field_size(handle, C.byref(nt), C.byref(nm), C.byref(npd)))
+        self.shape = (nt.value, nm.value, npd.value)
+
+    def row(self, it, imu, ip) -> np.ndarray:
+        r = np.zeros(7)
+        _check(lib().vrte_field_row(self._h, it, imu, ip, _dp(r)))
+        return r
+
+    def values(self):
+        """(taus, mus, phis, stokes [n_tau, n_mu, n_phi, 4]) via vrte_field_row."""
+        nt, nm, npd = self.shape
+        out = np.zeros((nt, nm, npd, 4))
+        taus, mus, phis = np.zeros(nt), np.zeros(nm), np.zeros(npd)
+        r = np.zeros(7)
+        for it in range(nt):
+            for im in range(nm):
+                for ip in range(npd):
+                    _check(lib().vrte_field_row(self._h, it, im, ip, _dp(r)))
+                    out[it, im, ip] = r[3:]
+                    taus[it], mus[im], phis[ip] = r[0], r[1], r[2]
+        return taus, mus, phis, out
+
+    def reflectance(self) -> np.ndarray:
+        r = np.zeros(4)
+        _check(lib().vrte_field_reflectance(self._h, _dp(r)))
+        return r
+
+    def timings(self) -> Timings:
+        t = Timings()
+        _check(lib().vrte_field_timings(self._h, C.byref(t)))
+        return t
+
+    def write_csv(self, path: str):
+        _check(lib().vrte_field_write_csv(self._h, path.encode()))
+
+    def close(self):
+        if self._h:
+            lib().vrte_field_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def solve_radiance(material: Material, opts: Options, taus=()) -> Field:
+    """vrte_solve_radiance (vrte.h:87-89) on the sm_100a pipeline + radiance.cu."""
+    t = np.ascontiguousarray(taus, dtype=np.float64)
+    h = C.c_void_p()
+    _check(lib().vrte_solve_radiance(material._h, C.byref(opts), _dp(t) if len(t) else None, len(t),
+                                     C.byref(h)))
+    return Field(h)
 
 
 def compute_brdf_batch(materials, opts: Options, mu_in, n_dphi: int = 19, basis=None,

@@ -13,6 +13,7 @@
 //   nodal_components/value    pipeline.cpp:201-220 + brdf.cpp:100-117 -> S
 // Everything for one shape lives in a plan whose buffers are reused.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -100,6 +101,7 @@ struct vrte_cuda_plan {
     int d = 0, R = 0, G = 0, B = 0;
     int Be = 0;  // slots [0, Be) run the eigen pipeline, [Be, B) are free-streaming (analytic)
     bool full_orders = true;
+    bool full_solution = false;  // radiance path: back substitution through every layer
     ProblemDev pd{};
     // inputs
     DevBuf<double> nodes, weights, mdiag, omega, greek, tau, mu_in, table, beam_rows, post, trig;
@@ -530,7 +532,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[11], st));
     lu_factor_rm(pl.lhs.p, G, NO, pl.ipiv.p, pl.perm.p, pl.status, pl.order_index.p, st, d, pl.P);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[12], st));
-    lu_solve_rm(pl.lhs.p, G, NO, pl.perm.p, pl.rhs_b.p, pl.rhs_x.p, R, st, G - 2 * d, d, pl.P);
+    lu_solve_rm(pl.lhs.p, G, NO, pl.perm.p, pl.rhs_b.p, pl.rhs_x.p, R, st, pl.full_solution ? 0 : G - 2 * d, d, pl.P);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[13], st));
     launch_copy_zp0(ba, st);
     // up += Top0 [A_0; B_0]: layer 0's unknowns are the last 2d rows of the
@@ -805,6 +807,101 @@ int32_t vrte_cuda_brdf(const vrte_cuda_problem* problem, double* table, vrte_cud
         VRTE_CUDA_CHECK(cudaMemcpyAsync(table, pl.out.p, sizeof(double) * pl.out.n,
                                         cudaMemcpyDeviceToHost, pl.st));
         return finish(pl, result);
+    });
+}
+
+int32_t vrte_cuda_radiance_field(const vrte_cuda_problem* problem, const vrte_cuda_radiance* rad, double* values,
+                                 double* reflectance, vrte_cuda_result* result) {
+    return guarded(result, [&]() -> int32_t {
+        if (!rad || !values || !reflectance) throw std::invalid_argument("null buffer");
+        if (problem->n_in != 1) throw std::invalid_argument("vrte_cuda: the radiance path solves one beam");
+        if (rad->n_tau < 1 || rad->n_mu < 1 || rad->n_phi < 1 || !rad->taus || !rad->mus || !rad->phis)
+            throw std::invalid_argument("vrte_cuda: empty radiance grid");
+        thread_local std::unique_ptr<vrte_cuda_plan> cached;
+        if (!cached) cached = std::make_unique<vrte_cuda_plan>();
+        vrte_cuda_plan& pl = *cached;
+        setup_plan(pl, problem);
+        pl.full_solution = true;
+        pl.launches = run_pipeline(pl, false);
+        const int code = finish(pl, result);
+        if (code != 0) return code;
+        // ---- source-function reconstruction (radiance.cu)
+        cudaStream_t st = pl.st;
+        const int N = pl.N, d = pl.d, P = pl.P, NO = pl.NO, B = pl.B, nmu = rad->n_mu;
+        const size_t ld = 4 * (size_t)nmu;
+        const double mu0 = problem->mu_in[0];
+        std::vector<double> tau_top(P, 0.0), beam_top(P);
+        for (int q = 1; q < P; ++q) tau_top[q] = tau_top[q - 1] + problem->tau[q - 1];
+        for (int q = 0; q < P; ++q) beam_top[q] = std::exp(-tau_top[q] / mu0);
+        DevBuf<double> taus, mus, phis, dtop, dbeam, gsf_o, wp, wm, bb, acc_a, acc_b, bsrc, bout, bbeam, down, bval,
+            comp, field, refl;
+        taus.upload(rad->taus, rad->n_tau, st);
+        mus.upload(rad->mus, nmu, st);
+        phis.upload(rad->phis, rad->n_phi, st);
+        dtop.upload(tau_top.data(), P, st);
+        dbeam.upload(beam_top.data(), P, st);
+        gsf_o.alloc((size_t)pl.L * pl.Lc * 3 * nmu);
+        for (auto* b : {&wp, &wm, &acc_a, &acc_b}) b->alloc((size_t)B * ld * d);
+        bb.alloc((size_t)B * nmu * 16);
+        bsrc.alloc((size_t)P * NO * nmu * 16);
+        comp.alloc((size_t)NO * 16 * rad->n_tau * nmu);
+        field.alloc((size_t)rad->n_tau * nmu * rad->n_phi * 4);
+        refl.alloc(4);
+        RadArgs a{};
+        a.p = pl.pd;
+        a.R = pl.R;
+        a.n_tau = rad->n_tau;
+        a.n_mu = nmu;
+        a.n_phi = rad->n_phi;
+        a.mu0 = mu0;
+        a.phi0 = rad->phi0;
+        a.tau_total = tau_top[P - 1] + problem->tau[P - 1];
+        for (int c = 0; c < 4; ++c) a.stokes[c] = rad->stokes[c];
+        a.taus = taus.p;
+        a.mus = mus.p;
+        a.phis = phis.p;
+        a.tau_top = dtop.p;
+        a.beam_top = dbeam.p;
+        a.gsf_n = pl.gsf_n.p;
+        a.gsf_b = pl.gsf_b.p;
+        a.gsf_o = gsf_o.p;
+        a.wp = wp.p;
+        a.wm = wm.p;
+        a.bb = bb.p;
+        a.acc_a = acc_a.p;
+        a.acc_b = acc_b.p;
+        a.beam_src = bsrc.p;
+        a.psi_p = pl.psi_p.p;
+        a.psi_m = pl.psi_m.p;
+        a.nu = pl.nu.p;
+        a.wi = pl.wi.p;
+        a.zp = pl.zp.p;
+        a.zm = pl.zm.p;
+        a.rhs_x = pl.rhs_x.p;
+        a.comp = comp.p;
+        a.field = field.p;
+        a.up = pl.up.p;
+        a.refl = refl.p;
+        a.slot0 = -1;
+        for (int mo = 0; mo < NO; ++mo)
+            if (pl.m_begin + mo * pl.m_stride == 0) a.slot0 = mo;
+        if (problem->base_type != 0 && a.slot0 >= 0) {
+            if (!rad->base_out || !rad->base_beam) throw std::invalid_argument("vrte_cuda: missing base rows");
+            bout.upload(rad->base_out, (size_t)nmu * N * 16, st);
+            bbeam.upload(rad->base_beam, (size_t)nmu * 16, st);
+            down.alloc(4 * (size_t)d);
+            bval.alloc(16 * (size_t)nmu);
+            a.base_out = bout.p;
+            a.base_beam = bbeam.p;
+            a.down_bot = down.p;
+            a.base_val = bval.p;
+        }
+        pl.launches += launch_radiance(a, st);
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(values, field.p, sizeof(double) * field.n, cudaMemcpyDeviceToHost, st));
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(reflectance, refl.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, st));
+        VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
+        if (result) result->kernel_launches = pl.launches;
+        return 0;
     });
 }
 

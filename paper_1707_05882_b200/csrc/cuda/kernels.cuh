@@ -102,4 +102,45 @@ void launch_free_modes(int d, int b0, int b1, const double* mdiag, double* psi_p
                        double* nu, double* wr, double* wi, double* residual, double* zp, double* zm, int R,
                        cudaStream_t st);
 
+
+// radiance.cu: source-function reconstruction of the radiance field
+// (reconstruction.cpp:28-227) on one solve's device state.  All pointers are
+// device pointers; p.n_in = 1 (the beam), R = 4 channels.
+struct RadArgs {
+    ProblemDev p;
+    int R, n_tau, n_mu, n_phi, slot0;  // slot0: mo of order 0 (base term) when base_val != nullptr
+    double mu0, phi0, tau_total;
+    double stokes[4];
+    const double* taus;       // [n_tau]
+    const double* mus;        // [n_mu] signed output cosines
+    const double* phis;       // [n_phi]
+    const double* tau_top;    // [n_layers]
+    const double* beam_top;   // [n_layers] exp(-tau_top / mu0)
+    const double* gsf_n;      // [L][Lc][3][N]   (nodes)
+    const double* gsf_b;      // [L][Lc][3][1]   (-mu0)
+    double* gsf_o;            // [L][Lc][3][n_mu]
+    double* wp;               // [B][4 n_mu][d] weighted kernel rows (col-major)
+    double* wm;
+    double* bb;               // [B][n_mu][16]  beam blocks A^m(mu_o, -mu0)
+    double* acc_a;            // [B][4 n_mu][d] source-coefficient contractions
+    double* acc_b;
+    double* beam_src;         // [P][NO][n_mu][4 ch][4]
+    const double* psi_p;      // [B][d][d] packed modes
+    const double* psi_m;
+    const double* nu;         // [B][d][2]
+    const double* wi;         // [B][d]
+    const double* zp;         // [B][R][d]
+    const double* zm;
+    const double* rhs_x;      // [NO][G][R] boundary solution (all layers)
+    const double* base_out;   // [n_mu][N][16] base_row_at(|mu_o|, mu_j)
+    const double* base_beam;  // [n_mu][16]    base_row_at(|mu_o|, mu0)
+    double* down_bot;         // [4][d]
+    double* base_val;         // [4][n_mu][4] (nullptr: no base term)
+    double* comp;             // [NO][4][n_tau][n_mu][4]
+    double* field;            // [n_tau][n_mu][n_phi][4]
+    const double* up;         // [NO][R][d] tau = 0 stacks
+    double* refl;             // [4]
+};
+int launch_radiance(RadArgs a, cudaStream_t st);
+
 }  // namespace vrte

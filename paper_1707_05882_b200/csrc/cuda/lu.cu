@@ -99,33 +99,38 @@ __global__ void __launch_bounds__(NT) lu_panel_crout_kernel(double* Aall, int G,
         }
         cp_async_wait_all();
         __syncthreads();
-        for (int c = w; c < jb; c += NW) {
-            double x[4];
+        // blocked by the earlier panels (PB rows each): solve the PB x PB unit-lower
+        // diagonal block (lane group of PB per column, shuffles within the group),
+        // then update the rows below it from shared memory -- PB-step chains
+        // instead of one kk-step shuffle chain per column
+        constexpr int NG = NT / PB;
+        const int grp = t / PB, gl = t % PB;
+        for (int r0 = 0; r0 < kk; r0 += PB) {
+            for (int cb = 0; cb < jb; cb += NG) {
+                const int c = cb + grp;
+                const bool act = c < jb;
+                double x = act ? Us[(r0 + gl) * USL + c] : 0.0;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int q = lane + 32 * i;
-                x[i] = q < kk ? Us[q * USL + c] : 0.0;
-            }
-#pragma unroll
-            for (int ci = 0; ci < 4; ++ci) {
-                const int s1 = min(kk, 32 * ci + 32);
-                for (int s2 = 32 * ci; s2 < s1; ++s2) {
-                    const double xs = __shfl_sync(0xffffffffu, x[ci], s2 & 31);
-#pragma unroll
-                    for (int i = ci; i < 4; ++i) {
-                        const int q = lane + 32 * i;
-                        if (q > s2 && q < kk) x[i] = fma(-Ls[q * LDL + s2], xs, x[i]);
-                    }
+                for (int s2 = 0; s2 < PB - 1; ++s2) {
+                    const double xs = __shfl_sync(0xffffffffu, x, s2, PB);
+                    if (gl > s2) x = fma(-Ls[(r0 + gl) * LDL + r0 + s2], xs, x);
                 }
+                if (act) Us[(r0 + gl) * USL + c] = x;
             }
+            __syncthreads();
+            const int below = kk - r0 - PB;
+            for (int e = t; e < below * jb; e += NT) {
+                const int r = r0 + PB + e / jb, c = e - (e / jb) * jb;
+                double acc = Us[r * USL + c];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int q = lane + 32 * i;
-                if (q < kk) {
-                    Us[q * USL + c] = x[i];
-                    A[(size_t)s_mapu[q] * G + k0 + c] = x[i];
-                }
+                for (int s2 = 0; s2 < PB; ++s2) acc = fma(-Ls[r * LDL + r0 + s2], Us[(r0 + s2) * USL + c], acc);
+                Us[r * USL + c] = acc;
             }
+            __syncthreads();
+        }
+        for (int e = t; e < kk * jb; e += NT) {
+            const int q = e / jb, c = e - q * jb;
+            A[(size_t)s_mapu[q] * G + k0 + c] = Us[q * USL + c];
         }
         __syncthreads();  // Ls is dead from here on (Ps aliases it)
     }

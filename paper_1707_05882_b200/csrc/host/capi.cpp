@@ -268,6 +268,12 @@ struct vrte_material {
     MaterialSpec spec;
 };
 
+struct vrte_field {  // capi.cpp:69-74
+    RadianceField field;
+    vrte_timings timings{};
+    double reflectance[4] = {0, 0, 0, 0};
+};
+
 struct vrte_brdf {
     BrdfTable table;
     Quadrature quadrature;
@@ -326,27 +332,121 @@ static vrte_status not_built(const char* what) {
                                           "see DESIGN.md)");
 }
 
-vrte_status vrte_solve_radiance(const vrte_material*, const vrte_options*, const double*, size_t,
-                                vrte_field** out) {
-    if (out) *out = nullptr;
-    return not_built("vrte_solve_radiance");
+// ---------------------------------------------------------------- radiance
+// capi.cpp:138-232: solve one beam (the material's source, or the options'
+// override), reconstruct the field on the signed zenith x azimuth grid at the
+// requested depths on the device (radiance.cu), field reflectance brdf.cpp:142-160.
+vrte_status vrte_solve_radiance(const vrte_material* material, const vrte_options* options,
+                                const double* tau_levels, size_t n_tau, vrte_field** out) {
+    if (!material || !out || (n_tau > 0 && !tau_levels)) return set_error(VRTE_E_ARGUMENT, "null argument");
+    return guarded([&] {
+        const double t0 = wall_now();
+        auto h = std::make_unique<vrte_field>();
+        BeamSource beam = material->spec.source;
+        if (options && options->incident_override) {
+            beam.mu0 = options->incident_mu0;
+            beam.phi0 = options->incident_phi0;
+        }
+        if (!(beam.mu0 > 0.0 && beam.mu0 <= 1.0))  // pipeline.cpp:97-98
+            throw ValidationError("incident mu0 must lie in (0,1]");
+        BrdfSetup s;
+        const double mu0 = beam.mu0;
+        build_setup(s, material->spec, options, &mu0, 1, 1, nullptr);
+        // grids (pipeline.cpp:358-390)
+        const int zen = options ? options->out_zenith : 11, azi = options ? options->out_azimuth : 19;
+        if (zen < 1 || azi < 1) throw ValidationError("radiance: output grid must have at least one point");
+        std::vector<double> up(zen);
+        for (int i = 0; i < zen; ++i) {
+            const double m = zen == 1 ? 1.0 : (double)i / (zen - 1);
+            up[i] = std::fabs(m) >= 1e-6 ? m : (m < 0.0 ? -1e-6 : 1e-6);  // clamp_mu, kMinMu
+        }
+        RadianceField& f = h->field;
+        f.taus.assign(tau_levels, tau_levels + n_tau);
+        if (f.taus.empty()) f.taus.push_back(0.0);
+        for (double m : up) f.mus.push_back(m);
+        for (double m : up) f.mus.push_back(-m);
+        const double p0 = reduce_azimuth(beam.phi0);
+        f.phis.resize(azi);
+        for (int j = 0; j < azi; ++j) f.phis[j] = azi == 1 ? p0 : reduce_azimuth(p0 + kPi * j / (azi - 1));
+        const int N = s.quad.n, nmu = (int)f.mus.size();
+        std::vector<double> base_out((size_t)nmu * N * 16), base_beam((size_t)nmu * 16);
+        for (int o = 0; o < nmu; ++o) {
+            const double mu = std::fabs(f.mus[o]);
+            for (int j = 0; j < N; ++j) {
+                const Mat4 r = base_row_at(s.spec.base, s.quad, mu, s.quad.nodes[j]);
+                std::memcpy(&base_out[((size_t)o * N + j) * 16], r.data(), 128);
+            }
+            const Mat4 rb = base_row_at(s.spec.base, s.quad, mu, mu0);
+            std::memcpy(&base_beam[(size_t)o * 16], rb.data(), 128);
+        }
+        vrte_cuda_radiance rad{};
+        rad.n_tau = (int32_t)f.taus.size();
+        rad.n_mu = nmu;
+        rad.n_phi = azi;
+        rad.taus = f.taus.data();
+        rad.mus = f.mus.data();
+        rad.phis = f.phis.data();
+        rad.phi0 = p0;
+        for (int c = 0; c < 4; ++c) rad.stokes[c] = beam.stokes[c];
+        rad.base_out = base_out.data();
+        rad.base_beam = base_beam.data();
+        f.values.assign((size_t)rad.n_tau * nmu * azi * 4, 0.0);
+        vrte_cuda_result r{};
+        const int32_t rc = vrte_cuda_radiance_field(&s.prob, &rad, f.values.data(), h->reflectance, &r);
+        if (rc == 5) throw std::invalid_argument(r.message);
+        if (rc != 0) throw NumericalError(r.message);
+        const uint64_t S = s.rep.size(), L = s.L;
+        h->timings.homogeneous = r.t_homogeneous;
+        h->timings.particular = r.t_particular;
+        h->timings.boundary = r.t_boundary;
+        h->timings.homogeneous_solves = S * L;
+        h->timings.particular_solves = 2 * L * S;
+        h->timings.boundary_solves = L;
+        h->timings.reconstruction_items = (uint64_t)nmu * f.taus.size();
+        h->timings.total_wall = wall_now() - t0;
+        h->timings.reconstruction = h->timings.total_wall - r.t_device;
+        *out = h.release();
+        return VRTE_OK;
+    });
 }
-vrte_status vrte_field_size(const vrte_field*, size_t*, size_t*, size_t*) {
-    return not_built("vrte_field_size");
+vrte_status vrte_field_size(const vrte_field* field, size_t* n_tau, size_t* n_mu, size_t* n_phi) {
+    if (!field) return set_error(VRTE_E_ARGUMENT, "null field");
+    if (n_tau) *n_tau = field->field.taus.size();
+    if (n_mu) *n_mu = field->field.mus.size();
+    if (n_phi) *n_phi = field->field.phis.size();
+    return VRTE_OK;
 }
-vrte_status vrte_field_row(const vrte_field*, size_t, size_t, size_t, double*) {
-    return not_built("vrte_field_row");
+vrte_status vrte_field_row(const vrte_field* field, size_t tau_index, size_t mu_index, size_t phi_index,
+                           double row[7]) {
+    if (!field || !row) return set_error(VRTE_E_ARGUMENT, "null argument");
+    const RadianceField& f = field->field;
+    if (tau_index >= f.taus.size() || mu_index >= f.mus.size() || phi_index >= f.phis.size())
+        return set_error(VRTE_E_ARGUMENT, "field index out of range");
+    const double* s = &f.values[((tau_index * f.mus.size() + mu_index) * f.phis.size() + phi_index) * 4];
+    row[0] = f.taus[tau_index];
+    row[1] = f.mus[mu_index];
+    row[2] = f.phis[phi_index];
+    for (int c = 0; c < 4; ++c) row[3 + c] = s[c];
+    return VRTE_OK;
 }
-vrte_status vrte_field_write_csv(const vrte_field*, const char*) {
-    return not_built("vrte_field_write_csv");
+vrte_status vrte_field_write_csv(const vrte_field* field, const char* path) {
+    if (!field || !path) return set_error(VRTE_E_ARGUMENT, "null argument");
+    return guarded([&] {
+        write_radiance_csv(path, field->field);
+        return VRTE_OK;
+    });
 }
-vrte_status vrte_field_timings(const vrte_field*, vrte_timings*) {
-    return not_built("vrte_field_timings");
+vrte_status vrte_field_timings(const vrte_field* field, vrte_timings* out) {
+    if (!field || !out) return set_error(VRTE_E_ARGUMENT, "null argument");
+    *out = field->timings;
+    return VRTE_OK;
 }
-vrte_status vrte_field_reflectance(const vrte_field*, double*) {
-    return not_built("vrte_field_reflectance");
+vrte_status vrte_field_reflectance(const vrte_field* field, double out[4]) {
+    if (!field || !out) return set_error(VRTE_E_ARGUMENT, "null argument");
+    for (int c = 0; c < 4; ++c) out[c] = field->reflectance[c];
+    return VRTE_OK;
 }
-void vrte_field_free(vrte_field*) {}
+void vrte_field_free(vrte_field* field) { delete field; }
 
 vrte_status vrte_mc_trace(const vrte_material*, const vrte_options*, uint64_t, uint64_t, int32_t,
                           int32_t, vrte_mc_tally** out) {

@@ -75,6 +75,11 @@ struct BrdfTable {  // brdf.hpp:9-24
 };
 
 void write_brdf_csv(const std::string& path, const BrdfTable& t);     // csv.cpp:111-129
+// pipeline.hpp RadianceField: values [tau][mu][phi][4]
+struct RadianceField {
+    std::vector<double> taus, mus, phis, values;
+};
+void write_radiance_csv(const std::string& path, const RadianceField& f);  // csv.cpp:28-40
 void write_brdf_binary(const std::string& path, const BrdfTable& t);  // csv.cpp:147-168
 
 }  // namespace vrte::host

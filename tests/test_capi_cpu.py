@@ -145,16 +145,29 @@ def test_out_of_path_symbols_are_not_built():
     mat = V.Material.load(write_rayleigh_slab(d))
     lib = V.lib()
     h = C.c_void_p(1)
-    taus = np.zeros(1)
-    rc = lib.vrte_solve_radiance(mat._h, C.byref(V.options(4)), taus.ctypes.data_as(C.POINTER(C.c_double)),
-                                 1, C.byref(h))
-    assert rc == V.VRTE_E_ARGUMENT and h.value is None
-    assert "not built" in lib.vrte_last_error().decode()
     assert lib.vrte_mc_trace(mat._h, C.byref(V.options(4)), 100, 7, 4, 4, C.byref(h)) == V.VRTE_E_ARGUMENT
+    assert "not built" in lib.vrte_last_error().decode()
     lib.vrte_field_free(None)
     lib.vrte_mc_tally_free(None)
     lib.vrte_brdf_free(None)
     lib.vrte_material_free(None)
+
+
+def test_radiance_argument_checks_before_any_device_work():
+    # capi.cpp:138-140 null checks (5), pipeline.cpp:97-98 incident validation (2)
+    d = tempfile.mkdtemp()
+    mat = V.Material.load(write_rayleigh_slab(d))
+    lib = V.lib()
+    h = C.c_void_p()
+    assert lib.vrte_solve_radiance(None, C.byref(V.options(4)), None, 0, C.byref(h)) == V.VRTE_E_ARGUMENT
+    assert lib.vrte_solve_radiance(mat._h, C.byref(V.options(4)), None, 1, C.byref(h)) == V.VRTE_E_ARGUMENT
+    o = V.options(4, incident_override=1, incident_mu0=1.5)
+    with pytest.raises(V.VrteError) as e:
+        V.solve_radiance(mat, o, [0.0])
+    assert e.value.code == V.VRTE_E_VALIDATION and "incident mu0 must lie in (0,1]" in e.value.message
+    row = np.zeros(7)
+    assert lib.vrte_field_row(None, 0, 0, 0, row.ctypes.data_as(C.POINTER(C.c_double))) == V.VRTE_E_ARGUMENT
+    assert lib.vrte_field_size(None, None, None, None) == V.VRTE_E_ARGUMENT
 
 
 def test_last_error_is_thread_local():
