@@ -319,12 +319,70 @@ def run_c5(args):
         dist.destroy_process_group()
 
 
+def run_radiance(args):
+    """vrte_solve_radiance on the C3 paint (its beam source,
+    mu0 = 0.6), field at tau = 0, the layer interface and the bottom on the
+    standard 11 x 19 signed grid.  One step = one full call through the public
+    C ABI (host in, host out: the solve, the reconstruction, the field copy).
+    The CPU baseline runs the oracle restatement of the same call in full."""
+    import numpy as np
+    import torch
+    import paper_1707_05882_b200 as V
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    os.environ["VRTE_DEVICE"] = str(local)
+    w = workload("C3")
+    tmp = tempfile.mkdtemp(prefix=f"vrte_rad_{rank}_")
+    mat = V.Material.load(w.material.write(tmp, "m"))
+    opts = V.options(w.N)
+    tot = sum(l.tau for l in w.material.layers)
+    taus = [0.0, w.material.layers[0].tau, tot]
+    for _ in range(max(1, args.warmup)):
+        f = V.solve_radiance(mat, opts, taus)
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        f = V.solve_radiance(mat, opts, taus)
+        times.append(time.perf_counter() - t0)
+    tm = f.timings()
+    t = statistics.median(times)
+    line = {"metric": "radiance fields/s (C3 paint, 3 depths x 22 x 19 directions)", "value": 1.0 / t,
+            "unit": "fields/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SURVEY §8(d) generator)",
+            "config": {"workload": "R3: C3 paint radiance field (vrte_solve_radiance)", "N": w.N,
+                       "L": w.material.order_count, "taus": taus, "out_zenith": 11, "out_azimuth": 19},
+            "e2e": {"value": 1.0 / t, "unit": "fields/s", "h2d_bytes_per_step": None, "d2h_bytes_per_step":
+                    3 * 22 * 19 * 4 * 8},
+            "stages_s": {"homogeneous": tm.homogeneous, "particular": tm.particular, "boundary": tm.boundary,
+                         "reconstruction_and_host": tm.reconstruction, "total_wall": tm.total_wall}}
+    if not args.no_cpu_baseline and rank == 0:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import pyoracle as O
+        d = w.material
+        bt = {"black": 0, "lambertian": 1, "mueller_table": 2}[d.base]
+        om = O.Material(np.array([l.omega for l in d.layers]), np.array([l.tau for l in d.layers]),
+                        d.padded_coeffs(), bt, d.albedo, d.table)
+        threads = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        ref, *_ = O.radiance(om, w.N, d.mu0, d.phi0, d.stokes, taus, zenith=11, azimuth=19, threads=threads)
+        tc = time.perf_counter() - t0
+        _, _, _, g = f.values()
+        line["cpu_baseline"] = {"value": 1.0 / tc, "unit": "fields/s", "cores": threads, "kind": "port",
+                                "sample": "oracle restatement of the full vrte_solve_radiance call (not sampled)"}
+        line["parity_vs_oracle"] = float(np.abs(g - ref).max() / np.abs(ref).max())
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
     if args.config == "C5":
         return run_c5(args)
+    if args.config == "R3":
+        return run_radiance(args)
     import numpy as np
     import torch
     import paper_1707_05882_b200 as V
