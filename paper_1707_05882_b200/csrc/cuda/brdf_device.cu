@@ -102,6 +102,10 @@ struct vrte_cuda_plan {
     int Be = 0;  // slots [0, Be) run the eigen pipeline, [Be, B) are free-streaming (analytic)
     bool full_orders = true;
     bool full_solution = false;  // radiance path: back substitution through every layer
+    struct RadBufs {             // radiance.cu scratch, persistent across calls
+        DevBuf<double> taus, mus, phis, dtop, dbeam, gsf_o, wp, wm, bb, acc_a, acc_b, bsrc, bout, bbeam, down, bval,
+            comp, field, refl;
+    } rad;
     ProblemDev pd{};
     // inputs
     DevBuf<double> nodes, weights, mdiag, omega, greek, tau, mu_in, table, beam_rows, post, trig;
@@ -833,8 +837,11 @@ int32_t vrte_cuda_radiance_field(const vrte_cuda_problem* problem, const vrte_cu
         std::vector<double> tau_top(P, 0.0), beam_top(P);
         for (int q = 1; q < P; ++q) tau_top[q] = tau_top[q - 1] + problem->tau[q - 1];
         for (int q = 0; q < P; ++q) beam_top[q] = std::exp(-tau_top[q] / mu0);
-        DevBuf<double> taus, mus, phis, dtop, dbeam, gsf_o, wp, wm, bb, acc_a, acc_b, bsrc, bout, bbeam, down, bval,
-            comp, field, refl;
+        auto& rb = pl.rad;
+        auto &taus = rb.taus, &mus = rb.mus, &phis = rb.phis, &dtop = rb.dtop, &dbeam = rb.dbeam, &gsf_o = rb.gsf_o;
+        auto &wp = rb.wp, &wm = rb.wm, &bb = rb.bb, &acc_a = rb.acc_a, &acc_b = rb.acc_b, &bsrc = rb.bsrc;
+        auto &bout = rb.bout, &bbeam = rb.bbeam, &down = rb.down, &bval = rb.bval, &comp = rb.comp;
+        auto &field = rb.field, &refl = rb.refl;
         taus.upload(rad->taus, rad->n_tau, st);
         mus.upload(rad->mus, nmu, st);
         phis.upload(rad->phis, rad->n_phi, st);
@@ -882,6 +889,8 @@ int32_t vrte_cuda_radiance_field(const vrte_cuda_problem* problem, const vrte_cu
         a.field = field.p;
         a.up = pl.up.p;
         a.refl = refl.p;
+        down.alloc(4 * (size_t)d + 4 * (size_t)N);  // base-term stack + reflectance partials
+        a.down_bot = down.p;
         a.slot0 = -1;
         for (int mo = 0; mo < NO; ++mo)
             if (pl.m_begin + mo * pl.m_stride == 0) a.slot0 = mo;
@@ -889,11 +898,9 @@ int32_t vrte_cuda_radiance_field(const vrte_cuda_problem* problem, const vrte_cu
             if (!rad->base_out || !rad->base_beam) throw std::invalid_argument("vrte_cuda: missing base rows");
             bout.upload(rad->base_out, (size_t)nmu * N * 16, st);
             bbeam.upload(rad->base_beam, (size_t)nmu * 16, st);
-            down.alloc(4 * (size_t)d);
             bval.alloc(16 * (size_t)nmu);
             a.base_out = bout.p;
             a.base_beam = bbeam.p;
-            a.down_bot = down.p;
             a.base_val = bval.p;
         }
         pl.launches += launch_radiance(a, st);

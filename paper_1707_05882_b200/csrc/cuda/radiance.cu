@@ -178,15 +178,15 @@ struct LayerCtx {
 __device__ inline cplx cexpd(cplx z) { return cexp_(z); }
 
 // sum over the packed mode columns of the layer integrals (reconstruction.cpp:87-149)
+// warp-cooperative: lanes split the mode columns, fixed-order butterfly sum
 __device__ void layer_integral(const RadArgs& a, const LayerCtx& L, int o, int p, bool up, double mu, double t,
-                               const double ib[4], double out[4]) {
+                               const double ib[4], double out[4], int lane) {
     const int d = 4 * a.p.N, ld = 4 * a.n_mu, G = 2 * d * a.p.n_layers;
     const double dth = L.thick;
     const double eb = up ? exp(-(dth - t) / mu) : exp(-t / mu);
-#pragma unroll
-    for (int r = 0; r < 4; ++r) out[r] = ib[r] * eb;
+    double ms[4] = {0.0, 0.0, 0.0, 0.0};
     const double emu_dt = exp(-(dth - t) / mu), emu_t = exp(-t / mu);
-    for (int jj = 0; jj < d; ++jj) {
+    for (int jj = lane; jj < d; jj += 32) {
         const double w = L.wi[jj];
         const int j = (w < 0.0) ? jj - 1 : jj;
         const bool pair = w != 0.0, imc = w < 0.0;
@@ -228,9 +228,11 @@ __device__ void layer_integral(const RadArgs& a, const LayerCtx& L, int o, int p
             const cplx va = cmk(L.half_omega * ca[r], pair ? L.half_omega * ca2[r] : 0.0);
             const cplx vb = cmk(L.half_omega * cb[r], pair ? L.half_omega * cb2[r] : 0.0);
             const cplx ta = ft * va, tb = fb * vb;
-            out[r] += xa * (imc ? ta.im : ta.re) + xb * (imc ? tb.im : tb.re);
+            ms[r] += xa * (imc ? ta.im : ta.re) + xb * (imc ? tb.im : tb.re);
         }
     }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) out[r] = ib[r] * eb + warp_sum(ms[r]);
     // beam term at the real rate mu0 (up_term_top / down_term_top with a = mu0)
     const double mu0 = a.mu0;
     double f;
@@ -248,7 +250,7 @@ __device__ void layer_integral(const RadArgs& a, const LayerCtx& L, int o, int p
 
 // Components per (order mo, channel c, depth it, output o): reconstruction.cpp:151-199.
 __global__ void rad_integrate_kernel(RadArgs a) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int idx = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     const ProblemDev& p = a.p;
     const int nmu = a.n_mu, NO = p.n_orders, P = p.n_layers, d = 4 * p.N, ld = 4 * nmu, G = 2 * d * P;
     if (idx >= NO * 4 * a.n_tau * nmu) return;
@@ -281,29 +283,28 @@ __global__ void rad_integrate_kernel(RadArgs a) {
             for (int r = 0; r < 4; ++r) bnd[r] = a.base_val[((size_t)c * nmu + o) * 4 + r];
         }
         for (int pl = P - 1; pl > pt; --pl) {
-            layer_integral(a, ctx(pl), o, pl, true, mu, 0.0, bnd, val);
+            layer_integral(a, ctx(pl), o, pl, true, mu, 0.0, bnd, val, lane);
 #pragma unroll
             for (int r = 0; r < 4; ++r) bnd[r] = val[r];
         }
-        layer_integral(a, ctx(pt), o, pt, true, mu, tl, bnd, val);
+        layer_integral(a, ctx(pt), o, pt, true, mu, tl, bnd, val, lane);
     } else {
         for (int pl = 0; pl < pt; ++pl) {
-            layer_integral(a, ctx(pl), o, pl, false, mu, p.tau[pl], bnd, val);
+            layer_integral(a, ctx(pl), o, pl, false, mu, p.tau[pl], bnd, val, lane);
 #pragma unroll
             for (int r = 0; r < 4; ++r) bnd[r] = val[r];
         }
-        layer_integral(a, ctx(pt), o, pt, false, mu, tl, bnd, val);
+        layer_integral(a, ctx(pt), o, pt, false, mu, tl, bnd, val, lane);
     }
     double* out = a.comp + ((((size_t)mo * 4 + c) * a.n_tau + it) * nmu + o) * 4;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) out[r] = val[r];
+    if (lane < 4) out[lane] = val[lane];
 }
 
 // m = 0 base reflection start value (reconstruction.cpp:176-192): the downward
 // nodal stack at the bottom of the last layer per channel, then its reflection
 // along every output direction plus the reflected attenuated beam.
 __global__ void rad_base_down_kernel(RadArgs a, int mo) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int idx = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     const ProblemDev& p = a.p;
     const int d = 4 * p.N, NO = p.n_orders, P = p.n_layers, G = 2 * d * P;
     if (idx >= 4 * d) return;
@@ -314,7 +315,7 @@ __global__ void rad_base_down_kernel(RadArgs a, int mo) {
     const double* psm = a.psi_m + (size_t)om * d * d;
     const double* x = a.rhs_x + (size_t)mo * G * a.R + c;
     double v = 0.0;
-    for (int jj = 0; jj < d; ++jj) {
+    for (int jj = lane; jj < d; jj += 32) {
         const double w = a.wi[(size_t)om * d + jj];
         const int j = (w < 0.0) ? jj - 1 : jj;
         const bool pair = w != 0.0, imc = w < 0.0;
@@ -329,8 +330,8 @@ __global__ void rad_base_down_kernel(RadArgs a, int mo) {
         v += x[(size_t)bnd_col(q, jj, d, G) * a.R] * (imc ? ta.im : ta.re) +
              x[(size_t)bnd_col(q, d + jj, d, G) * a.R] * (imc ? tb.im : tb.re);
     }
-    v += a.beam_top[q] * exp(-th / a.mu0) * a.zm[((size_t)om * a.R + c) * d + i];
-    a.down_bot[(size_t)c * d + i] = v;
+    v = warp_sum(v) + a.beam_top[q] * exp(-th / a.mu0) * a.zm[((size_t)om * a.R + c) * d + i];
+    if (lane == 0) a.down_bot[(size_t)c * d + i] = v;
 }
 
 __global__ void rad_base_val_kernel(RadArgs a) {
@@ -380,15 +381,12 @@ __global__ void rad_assemble_kernel(RadArgs a) {
 }
 
 // field reflectance (brdf.cpp:142-160): exiting nodal flux at tau = 0 over 19
-// azimuths, divided by mu0 I0.  One CTA; fixed-order reduction.
-__global__ void rad_reflectance_kernel(RadArgs a) {
-    __shared__ double red[4][256];
-    const int t = threadIdx.x, N = a.p.N, d = 4 * N, nph = 19;
-    double f[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int e = t; e < N * nph; e += blockDim.x) {
-        const int i = e / nph, j = e % nph;
+// azimuths, divided by mu0 I0.  CTA (one warp) per node, then a fixed-order sum.
+__global__ void rad_refl_node_kernel(RadArgs a, double* part) {
+    const int i = blockIdx.x, j = threadIdx.x, N = a.p.N, d = 4 * N, nph = 19;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    if (j < nph) {
         const double x = -(2.0 * kPi * j / nph);
-        double s[4] = {0.0, 0.0, 0.0, 0.0};
         for (int mo = 0; mo < a.p.n_orders; ++mo) {
             const int m = a.p.order_of(mo);
             const double sc = (m == 0) ? 1.0 : 2.0;
@@ -405,16 +403,19 @@ __global__ void rad_reflectance_kernel(RadArgs a) {
             s[2] += 0.5 * sc * (sn * k1[2] + cs * k2[2]);
             s[3] += 0.5 * sc * (sn * k1[3] + cs * k2[3]);
         }
-        const double w = a.p.weights[i] * a.p.nodes[i] * (2.0 * kPi / nph);
-        for (int r = 0; r < 4; ++r) f[r] += w * s[r];
     }
-    for (int r = 0; r < 4; ++r) red[r][t] = f[r];
-    __syncthreads();
-    if (t < 4) {
-        double acc = 0.0;
-        for (int q = 0; q < (int)blockDim.x; ++q) acc += red[t][q];
-        a.refl[t] = acc / fmax(a.mu0 * a.stokes[0], 1e-300);
+    const double w = a.p.weights[i] * a.p.nodes[i] * (2.0 * kPi / nph);
+    for (int r = 0; r < 4; ++r) {
+        const double v = warp_sum(w * s[r]);
+        if (j == 0) part[4 * i + r] = v;
     }
+}
+__global__ void rad_refl_sum_kernel(RadArgs a, const double* part) {
+    const int r = threadIdx.x;
+    if (r >= 4) return;
+    double acc = 0.0;
+    for (int i = 0; i < a.p.N; ++i) acc += part[4 * i + r];
+    a.refl[r] = acc / fmax(a.mu0 * a.stokes[0], 1e-300);
 }
 
 }  // namespace
@@ -464,19 +465,20 @@ int launch_radiance(RadArgs a, cudaStream_t st) {
         ++nl;
     }
     if (a.base_val) {
-        rad_base_down_kernel<<<(4 * d + 127) / 128, 128, 0, st>>>(a, a.slot0);
+        rad_base_down_kernel<<<(4 * d * 32 + 255) / 256, 256, 0, st>>>(a, a.slot0);
         rad_base_val_kernel<<<(16 * nmu + 127) / 128, 128, 0, st>>>(a);
         VRTE_CUDA_CHECK(cudaGetLastError());
         nl += 2;
     }
     {
-        const int total = p.n_orders * 4 * a.n_tau * nmu;
-        rad_integrate_kernel<<<(total + 63) / 64, 64, 0, st>>>(a);
+        const long long total = (long long)p.n_orders * 4 * a.n_tau * nmu * 32;  // warp per item
+        rad_integrate_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(a);
         const int tf = a.n_tau * nmu * a.n_phi;
         rad_assemble_kernel<<<(tf + 127) / 128, 128, 0, st>>>(a);
-        rad_reflectance_kernel<<<1, 256, 0, st>>>(a);
+        rad_refl_node_kernel<<<N, 32, 0, st>>>(a, a.down_bot + 4 * (size_t)d);  // scratch after down_bot
+        rad_refl_sum_kernel<<<1, 32, 0, st>>>(a, a.down_bot + 4 * (size_t)d);
         VRTE_CUDA_CHECK(cudaGetLastError());
-        nl += 3;
+        nl += 4;
     }
     return nl;
 }
