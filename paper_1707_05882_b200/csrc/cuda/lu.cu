@@ -407,6 +407,83 @@ __global__ void __launch_bounds__(256) lu_trsm_rm_kernel(const double* Aall, int
 #endif
 }
 
+// Column-per-lane substitution: lane = one column of M, the jb-row column in
+// registers, the triangle in shared memory read as warp-wide broadcasts (LDS.128 =
+// two entries), four partial sums per row to shorten the FMA chains.  Every
+// global access of the prologue is issued before the first is consumed (row
+// indices, then the triangle by cp.async, then the column), so a CTA pays two
+// L2 round trips instead of one per row -- and no shuffles: the lane-over-rows
+// variant above is bound by 8 SHFL per 8 FMA on the MIO pipe.  CTA = 2 warps.
+template <bool LOWER>
+__global__ void __launch_bounds__(64, 6) lu_trsm_col_kernel(const double* Aall, int G, long long strideA,
+                                                            double* Mall, int ld, long long strideM, int k0, int jb,
+                                                            int c_lo, int c_hi, const int* tmap_all,
+                                                            const int* mmap_all) {
+    __shared__ __align__(16) double Ts[LU_NB * LU_NB];
+    __shared__ double s_rd[LU_NB];
+    __shared__ int s_trow[LU_NB], s_mrow[LU_NB];
+    const int b = blockIdx.y, t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const double* A = Aall + (size_t)b * strideA;
+    double* M = Mall + (size_t)b * strideM;
+    const int* tmap = tmap_all ? tmap_all + (size_t)b * G : nullptr;
+    const int* mmap = mmap_all ? mmap_all + (size_t)b * G : nullptr;
+    for (int q = t; q < jb; q += 64) {
+        s_trow[q] = tmap ? tmap[k0 + q] : k0 + q;
+        s_mrow[q] = mmap ? mmap[k0 + q] : k0 + q;
+    }
+    __syncthreads();
+    for (int r = w; r < jb; r += 2) {
+        const double* src = A + (size_t)s_trow[r] * G + k0;
+        if (LOWER) {
+            for (int c = lane; c < r; c += 32) cp_async8(Ts + r * LU_NB + c, src + c);
+        } else {
+            for (int c = r + lane; c < jb; c += 32) cp_async8(Ts + r * LU_NB + c, src + c);
+        }
+    }
+    cp_async_wait_all();
+    const int col = c_lo + blockIdx.x * 64 + w * 32 + lane;
+    const bool live = col < c_hi;
+    double x[LU_NB];
+#pragma unroll
+    for (int r = 0; r < LU_NB; ++r) x[r] = (live && r < jb) ? M[(size_t)s_mrow[r] * ld + col] : 0.0;
+    __syncthreads();
+    if (!LOWER)
+        for (int q = t; q < jb; q += 64) s_rd[q] = 1.0 / Ts[q * LU_NB + q];
+    __syncthreads();
+    if (LOWER) {
+#pragma unroll
+        for (int r = 1; r < LU_NB; ++r) {
+            if (r >= jb) break;
+            const double2* Lr = reinterpret_cast<const double2*>(Ts + r * LU_NB);
+            double acc[4] = {x[r], 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int s2 = 0; s2 < r / 2; ++s2) {
+                const double2 l = Lr[s2];
+                acc[(2 * s2) & 3] = fma(-l.x, x[2 * s2], acc[(2 * s2) & 3]);
+                acc[(2 * s2 + 1) & 3] = fma(-l.y, x[2 * s2 + 1], acc[(2 * s2 + 1) & 3]);
+            }
+            if (r & 1) acc[(r - 1) & 3] = fma(-Ts[r * LU_NB + r - 1], x[r - 1], acc[(r - 1) & 3]);
+            x[r] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        }
+    } else {
+#pragma unroll
+        for (int r = LU_NB - 1; r >= 0; --r) {
+            if (r < jb) {
+                double acc[4] = {x[r], 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int s = r + 1; s < LU_NB; ++s)
+                    if (s < jb) acc[s & 3] = fma(-Ts[r * LU_NB + s], x[s], acc[s & 3]);
+                x[r] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) * s_rd[r];
+            }
+        }
+    }
+    if (live) {
+#pragma unroll
+        for (int r = 0; r < LU_NB; ++r)
+            if (r < jb) M[(size_t)s_mrow[r] * ld + col] = x[r];
+    }
+}
+
 __global__ void lu_gather_rows_kernel(const double* In, long long strideIn, double* Out,
                                       long long strideOut, const int* perm_all, int G, int ncol,
                                       int batch) {
@@ -498,9 +575,19 @@ template <bool LOWER>
 void trsm_launch(const double* A, int G, double* M, int ld, long long strideM, int k0, int jb, int c_lo,
                  int c_hi, int batch, cudaStream_t st, const int* tmap, const int* mmap) {
     if (jb <= 0 || c_hi <= c_lo) return;
-    dim3 grid((c_hi - c_lo + SW_TILE - 1) / SW_TILE, batch);
-    lu_trsm_rm_kernel<LOWER><<<grid, 256, 0, st>>>(A, G, (long long)G * G, M, ld, strideM, k0, jb, c_lo, c_hi, tmap,
-                                                   mmap);
+    // wide right-hand sides (the factorization's U12 blocks): column-per-lane;
+    // narrow ones (the 256-column solves) keep enough CTAs with lanes over rows
+    static const char* mode = std::getenv("VRTE_TRSM");  // shfl | col | (auto)
+    const bool shfl = mode ? std::string(mode) == "shfl" : (c_hi - c_lo) < 512;
+    if (shfl) {
+        dim3 grid((c_hi - c_lo + SW_TILE - 1) / SW_TILE, batch);
+        lu_trsm_rm_kernel<LOWER><<<grid, 256, 0, st>>>(A, G, (long long)G * G, M, ld, strideM, k0, jb, c_lo, c_hi,
+                                                       tmap, mmap);
+    } else {
+        dim3 grid((c_hi - c_lo + 63) / 64, batch);
+        lu_trsm_col_kernel<LOWER><<<grid, 64, 0, st>>>(A, G, (long long)G * G, M, ld, strideM, k0, jb, c_lo, c_hi,
+                                                       tmap, mmap);
+    }
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
