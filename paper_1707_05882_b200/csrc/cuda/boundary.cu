@@ -53,10 +53,10 @@ __global__ void assemble_kernel(BndArgs a) {
     mv.load(om, jj, i, pp, pm, nu, imc);
     const cplx att = att_of(a.p.tau[p], nu);
     auto pk = [&](cplx v) { return imc ? v.im : v.re; };
-    double* A = a.lhs + (size_t)mo * G * G;
+    double* A = a.lhs + (size_t)mo * a.sl;
     const int ca = bnd_col(p, jj, d, G);       // column A_p(jj)
     const int cbk = bnd_col(p, d + jj, d, G);  // column B_p(jj)
-    auto at = [&](int r, int c) -> double& { return A[(size_t)bnd_row(r, d, G) * G + c]; };
+    auto at = [&](int r, int c) -> double& { return A[(size_t)bnd_row(r, d, G) * a.ldl + c]; };
     if (p == 0) {
         at(i, ca) = pk(dflip(pm, i));
         at(i, cbk) = pk(att * dflip(pp, i));
@@ -135,10 +135,10 @@ __global__ void base_kernel(BndArgs a, int mo) {
     __syncwarp();
     reflect_rows(a.p, v, d, lane, out);
     __syncwarp();
-    double* A = a.lhs + (size_t)mo * G * G;
+    double* A = a.lhs + (size_t)mo * a.sl;
     const int col = bnd_col(q, (isb ? d : 0) + jj, d, G);
     const int rb = d + 2 * d * (P - 1);
-    for (int i = lane; i < d; i += 32) A[(size_t)bnd_row(rb + i, d, G) * G + col] -= out[i];
+    for (int i = lane; i < d; i += 32) A[(size_t)bnd_row(rb + i, d, G) * a.ldl + col] -= out[i];
 }
 
 // Right-hand sides: warp per (order mo, column = incident*4 + channel).
@@ -156,7 +156,7 @@ __global__ void rhs_kernel(BndArgs a) {
         double* base;
         int R, d, G;
         __device__ double& operator[](int r) const { return base[(size_t)bnd_row(r, d, G) * R]; }
-    } B{a.rhs + (size_t)mo * R * G + col, R, d, G};
+    } B{a.rhs + (size_t)mo * a.sr + col, a.ldr, d, G};
     auto zp = [&](int p, int i) {
         const size_t om = (size_t)a.p.medium[p] * a.p.n_orders + mo;
         return a.zp[(om * R + col) * d + i];
@@ -216,7 +216,7 @@ __global__ void copy_zp0_kernel(BndArgs a) {
 
 void launch_bnd_assemble(const BndArgs& a, cudaStream_t st) {
     const int d = a.d, P = a.p.n_layers, G = 2 * d * P;
-    VRTE_CUDA_CHECK(cudaMemsetAsync(a.lhs, 0, sizeof(double) * (size_t)a.p.n_orders * G * G, st));
+    VRTE_CUDA_CHECK(cudaMemsetAsync(a.lhs, 0, sizeof(double) * (size_t)a.p.n_orders * a.sl, st));
     const long long total = (long long)a.p.n_orders * P * d * d;
     assemble_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(a);
     VRTE_CUDA_CHECK(cudaGetLastError());

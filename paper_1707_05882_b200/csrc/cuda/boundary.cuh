@@ -14,9 +14,11 @@ struct BndArgs {
     const double* wi;     // [om][d] (pair layout)
     const double* zp;     // [om][R][d]
     const double* zm;
-    double* lhs;          // [mo][G*G] row-major
+    double* lhs;          // [mo] row-major G x ldl (ldl = G + R: augmented with the right-hand sides)
     double* top0;         // [mo][d * 2d]
-    double* rhs;          // [mo][G][R] row-major
+    double* rhs;          // [mo] row-major G x ldr (into the augmented lhs: lhs + G, ldr = ldl)
+    int ldl, ldr;
+    long long sl, sr;     // per-order strides of lhs and rhs
     double* up;           // [mo][R][d]
 };
 
@@ -28,8 +30,15 @@ void launch_copy_zp0(const BndArgs& a, cudaStream_t st);
 // row permutation (row i of P B = row perm[i] of B).
 // prof_d / prof_P > 0: the matrix has the boundary-system staircase profile
 // (bnd_row_end); rows past a column block's profile are skipped.
+// lda: row stride (0 = G); ncols > G: the columns past G (right-hand sides of
+// an augmented system [A | B]) are carried through the elimination.
 void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatus* status,
-                  const int* order_index, cudaStream_t st, int prof_d = 0, int prof_P = 0);
+                  const int* order_index, cudaStream_t st, int prof_d = 0, int prof_P = 0, int lda = 0,
+                  int ncols = 0);
+// Back substitution of an augmented factorization (ncols = G + R) in place, down
+// to row_lo (rounded down to a 64-row block); X [batch][G][R] receives rows >= that.
+void lu_backsolve_aug(double* A, int G, int lda, int R, int batch, const int* perm, double* X, int row_lo,
+                      cudaStream_t st);
 // X = A^-1 B for row-major B, X ([batch][G][ncol]); B is not modified.  Only
 // rows >= row_lo (rounded down to the 64-row block) of X are the solution.
 void lu_solve_rm(const double* A, int G, int batch, const int* perm, const double* B, double* X,
@@ -53,5 +62,6 @@ __host__ __device__ inline int bnd_row_end(int col, int d, int P) {
     return (p <= P - 2) ? 2 * d * (p + 1) : 2 * d * (P - 1) + d;
 }
 int lu_rm_launch_count(int G);
+int lu_aug_launch_count(int G, int R, int row_lo);
 
 }  // namespace vrte

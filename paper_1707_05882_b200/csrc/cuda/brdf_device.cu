@@ -265,9 +265,8 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pl.mu_eff.alloc((size_t)B * pl.n_in);
     pl.sigma.alloc((size_t)B * R * 2);
     pl.kind.alloc((size_t)B * R);
-    pl.lhs.alloc((size_t)NO * G * G);
+    pl.lhs.alloc((size_t)NO * G * (G + R));  // augmented [A | B] per order, row-major
     pl.top0.alloc((size_t)NO * d * 2 * d);
-    pl.rhs_b.alloc((size_t)NO * R * G);
     pl.rhs_x.alloc((size_t)NO * R * G);
     pl.ipiv.alloc((size_t)NO * G);
     pl.perm.alloc((size_t)NO * G);
@@ -529,14 +528,16 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     ba.zm = pl.zm.p;
     ba.lhs = pl.lhs.p;
     ba.top0 = pl.top0.p;
-    ba.rhs = pl.rhs_b.p;
+    ba.ldl = ba.ldr = G + R;  // the right-hand sides ride in the LU as columns G .. G+R
+    ba.sl = ba.sr = (long long)G * (G + R);
+    ba.rhs = pl.lhs.p + G;
     ba.up = pl.up.p;
     launch_bnd_assemble(ba, st);
     launch_bnd_rhs(ba, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[11], st));
-    lu_factor_rm(pl.lhs.p, G, NO, pl.ipiv.p, pl.perm.p, pl.status, pl.order_index.p, st, d, pl.P);
+    lu_factor_rm(pl.lhs.p, G, NO, pl.ipiv.p, pl.perm.p, pl.status, pl.order_index.p, st, d, pl.P, G + R, G + R);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[12], st));
-    lu_solve_rm(pl.lhs.p, G, NO, pl.perm.p, pl.rhs_b.p, pl.rhs_x.p, R, st, pl.full_solution ? 0 : G - 2 * d, d, pl.P);
+    lu_backsolve_aug(pl.lhs.p, G, G + R, R, NO, pl.perm.p, pl.rhs_x.p, pl.full_solution ? 0 : G - 2 * d, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[13], st));
     launch_copy_zp0(ba, st);
     // up += Top0 [A_0; B_0]: layer 0's unknowns are the last 2d rows of the
@@ -545,7 +546,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
                       pl.rhs_x.p + (size_t)(G - 2 * d) * R, R, (long long)G * R, true, pl.up.p, d, dR, NO,
                       1.0, 1.0),
                  st);
-    nl += 2 + (pd.base_type != 0 ? 1 : 0) + lu_rm_launch_count(G) + 2;
+    nl += 2 + (pd.base_type != 0 ? 1 : 0) + lu_aug_launch_count(G, R, pl.full_solution ? 0 : G - 2 * d) + 2;
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[3], st));
     // ---------------- synthesis
     if (synth) {

@@ -56,7 +56,7 @@ struct PanelGeo {
 };
 
 template <int NT, int RPT, int PB>
-__global__ void __launch_bounds__(NT) lu_panel_crout_kernel(double* Aall, int G, long long strideA, int* map_all,
+__global__ void __launch_bounds__(NT) lu_panel_crout_kernel(double* Aall, int G, int lda, long long strideA, int* map_all,
                                                             int* ipiv_all, int K0, int k0, int jb, int rend,
                                                             DeviceStatus* status, const int* order_index) {
     using Geo = PanelGeo<NT, RPT, PB>;
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(NT) lu_panel_crout_kernel(double* Aall, int G,
         // U(K0:k0, panel) = L11^-1 A(K0:k0, panel), L11 unit lower (the block's
         // earlier panels): async copies of L11 / the U rows, warp per column to solve
         for (int q = w; q < kk; q += NW) {
-            const double* src = A + (size_t)s_mapu[q] * G;
+            const double* src = A + (size_t)s_mapu[q] * lda;
             for (int c = lane; c < q; c += 32) cp_async8(Ls + q * LDL + c, src + K0 + c);
             if (lane < jb) cp_async8(Us + q * USL + lane, src + k0 + lane);
             else if (lane < PB) Us[q * USL + lane] = 0.0;
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(NT) lu_panel_crout_kernel(double* Aall, int G,
         }
         for (int e = t; e < kk * jb; e += NT) {
             const int q = e / jb, c = e - q * jb;
-            A[(size_t)s_mapu[q] * G + k0 + c] = Us[q * USL + c];
+            A[(size_t)s_mapu[q] * lda + k0 + c] = Us[q * USL + c];
         }
         __syncthreads();  // Ls is dead from here on (Ps aliases it)
     }
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(NT) lu_panel_crout_kernel(double* Aall, int G,
         const int ntiles = (np + 7) / 8;
         auto row_of = [&](int tile) -> const double* {
             const int r = tile * 8 + gq;
-            return (tile < ntiles && r < np) ? A + (size_t)s_map[r] * G : nullptr;
+            return (tile < ntiles && r < np) ? A + (size_t)s_map[r] * lda : nullptr;
         };
         double a[KQ];
         const double* row = row_of(w);
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(NT) lu_panel_crout_kernel(double* Aall, int G,
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
         const int r = t + i * NT;
-        src[i] = r < np ? A + (size_t)s_map[r] * G : nullptr;
+        src[i] = r < np ? A + (size_t)s_map[r] * lda : nullptr;
 #pragma unroll
         for (int c2 = 0; c2 < PB / 2; ++c2) {
             const double2 x = src[i] ? *reinterpret_cast<const double2*>(Ps + r * PSL + 2 * c2) : make_double2(0.0, 0.0);
@@ -291,13 +291,13 @@ __global__ void __launch_bounds__(NT) lu_panel_crout_kernel(double* Aall, int G,
         constexpr int LPR = PB / 2;  // lanes per row (16 bytes each)
         for (int e = t; e < np * LPR; e += NT) {
             const int r = e / LPR, c2 = e - r * LPR;
-            *reinterpret_cast<double2*>(A + (size_t)s_map[r] * G + k0 + 2 * c2) =
+            *reinterpret_cast<double2*>(A + (size_t)s_map[r] * lda + k0 + 2 * c2) =
                 *reinterpret_cast<const double2*>(Ps + r * PSL + 2 * c2);
         }
     } else {
         for (int e = t; e < np * jb; e += NT) {
             const int r = e / jb, c = e - r * jb;
-            A[(size_t)s_map[r] * G + k0 + c] = Ps[r * PSL + c];
+            A[(size_t)s_map[r] * lda + k0 + c] = Ps[r * PSL + c];
         }
     }
 #ifdef VRTE_LU_TRACE
@@ -321,7 +321,7 @@ __global__ void lu_map_init_kernel(int* map, long long total, int G) {
 // columns, lanes over rows (two rows per lane), the solved entry broadcast by
 // shuffle -- substitution, not an explicit inverse.
 template <bool LOWER>
-__global__ void __launch_bounds__(256) lu_trsm_rm_kernel(const double* Aall, int G, long long strideA,
+__global__ void __launch_bounds__(256) lu_trsm_rm_kernel(const double* Aall, int G, int lda, long long strideA,
                                                          double* Mall, int ld, long long strideM, int k0,
                                                          int jb, int c_lo, int c_hi, const int* tmap_all,
                                                          const int* mmap_all) {
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(256) lu_trsm_rm_kernel(const double* Aall, int
     tr[0] = clock64();
 #endif
     for (int r = w; r < jb; r += 8) {
-        const double* src = A + (size_t)(tmap ? tmap[k0 + r] : k0 + r) * G + k0;
+        const double* src = A + (size_t)(tmap ? tmap[k0 + r] : k0 + r) * lda + k0;
         for (int cc = lane; cc < jb; cc += 32) Ts[r][cc] = src[cc];
         if (lane == 0) s_mrow[r] = mmap ? mmap[k0 + r] : k0 + r;
     }
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(256) lu_trsm_rm_kernel(const double* Aall, int
 // L2 round trips instead of one per row -- and no shuffles: the lane-over-rows
 // variant above is bound by 8 SHFL per 8 FMA on the MIO pipe.  CTA = 2 warps.
 template <bool LOWER>
-__global__ void __launch_bounds__(64, 6) lu_trsm_col_kernel(const double* Aall, int G, long long strideA,
+__global__ void __launch_bounds__(64, 6) lu_trsm_col_kernel(const double* Aall, int G, int lda, long long strideA,
                                                             double* Mall, int ld, long long strideM, int k0, int jb,
                                                             int c_lo, int c_hi, const int* tmap_all,
                                                             const int* mmap_all) {
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(64, 6) lu_trsm_col_kernel(const double* Aall, 
     }
     __syncthreads();
     for (int r = w; r < jb; r += 2) {
-        const double* src = A + (size_t)s_trow[r] * G + k0;
+        const double* src = A + (size_t)s_trow[r] * lda + k0;
         if (LOWER) {
             for (int c = lane; c < r; c += 32) cp_async8(Ts + r * LU_NB + c, src + c);
         } else {
@@ -532,8 +532,8 @@ void rm_gemm(int m, int n, int k, const double* A, long long lda, long long sa, 
 }
 
 template <int NT, int RPT, int PB>
-void panel_launch(double* A, int G, int* map, int* ipiv, int K0, int k0, int jb, int rend, DeviceStatus* status,
-                  const int* order_index, int batch, cudaStream_t st) {
+void panel_launch(double* A, int G, int lda, int* map, int* ipiv, int K0, int k0, int jb, int rend,
+                  DeviceStatus* status, const int* order_index, int batch, cudaStream_t st) {
     constexpr size_t smem = PanelGeo<NT, RPT, PB>::bytes;
     static bool attr = false;
     if (!attr) {
@@ -541,27 +541,27 @@ void panel_launch(double* A, int G, int* map, int* ipiv, int K0, int k0, int jb,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    lu_panel_crout_kernel<NT, RPT, PB><<<batch, NT, smem, st>>>(A, G, (long long)G * G, map, ipiv, K0, k0, jb,
-                                                                rend, status, order_index);
+    lu_panel_crout_kernel<NT, RPT, PB><<<batch, NT, smem, st>>>(A, G, lda, (long long)G * lda, map, ipiv, K0, k0,
+                                                                jb, rend, status, order_index);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
 // the kernel's PB must be the driver's panel width (it sizes the block's L in
 // shared memory); rows per thread grow with the active height
 template <int PB>
-void panel_dispatch(int np, double* A, int G, int* map, int* ipiv, int K0, int k0, int jb, int rend,
+void panel_dispatch(int np, double* A, int G, int lda, int* map, int* ipiv, int K0, int k0, int jb, int rend,
                     DeviceStatus* status, const int* order_index, int batch, cudaStream_t st) {
     if (np <= 256)
-        panel_launch<256, 1, PB>(A, G, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
+        panel_launch<256, 1, PB>(A, G, lda, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
     else if (np <= 512)
-        panel_launch<512, 1, PB>(A, G, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
+        panel_launch<512, 1, PB>(A, G, lda, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
     else if (np <= 1024)
-        panel_launch<512, 2, PB>(A, G, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
+        panel_launch<512, 2, PB>(A, G, lda, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
     else if constexpr (PB <= 8) {
         if (np <= 2048)
-            panel_launch<512, 4, PB>(A, G, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
+            panel_launch<512, 4, PB>(A, G, lda, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
         else if constexpr (PB <= 4)
-            panel_launch<512, 8, PB>(A, G, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
+            panel_launch<512, 8, PB>(A, G, lda, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
         else
             throw std::invalid_argument("lu: panel height exceeds the panel kernel");
     } else {
@@ -572,7 +572,7 @@ void panel_dispatch(int np, double* A, int G, int* map, int* ipiv, int K0, int k
 int panel_width(int G) { return G <= 1024 ? 16 : (G <= 2048 ? 8 : 4); }
 
 template <bool LOWER>
-void trsm_launch(const double* A, int G, double* M, int ld, long long strideM, int k0, int jb, int c_lo,
+void trsm_launch(const double* A, int G, int lda, double* M, int ld, long long strideM, int k0, int jb, int c_lo,
                  int c_hi, int batch, cudaStream_t st, const int* tmap, const int* mmap) {
     if (jb <= 0 || c_hi <= c_lo) return;
     // wide right-hand sides (the factorization's U12 blocks): column-per-lane;
@@ -581,12 +581,12 @@ void trsm_launch(const double* A, int G, double* M, int ld, long long strideM, i
     const bool shfl = mode ? std::string(mode) == "shfl" : (c_hi - c_lo) < 512;
     if (shfl) {
         dim3 grid((c_hi - c_lo + SW_TILE - 1) / SW_TILE, batch);
-        lu_trsm_rm_kernel<LOWER><<<grid, 256, 0, st>>>(A, G, (long long)G * G, M, ld, strideM, k0, jb, c_lo, c_hi,
-                                                       tmap, mmap);
+        lu_trsm_rm_kernel<LOWER><<<grid, 256, 0, st>>>(A, G, lda, (long long)G * lda, M, ld, strideM, k0, jb, c_lo,
+                                                       c_hi, tmap, mmap);
     } else {
         dim3 grid((c_hi - c_lo + 63) / 64, batch);
-        lu_trsm_col_kernel<LOWER><<<grid, 64, 0, st>>>(A, G, (long long)G * G, M, ld, strideM, k0, jb, c_lo, c_hi,
-                                                       tmap, mmap);
+        lu_trsm_col_kernel<LOWER><<<grid, 64, 0, st>>>(A, G, lda, (long long)G * lda, M, ld, strideM, k0, jb, c_lo,
+                                                       c_hi, tmap, mmap);
     }
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
@@ -599,10 +599,12 @@ int outer_block() {
 }  // namespace
 
 void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatus* status,
-                  const int* order_index, cudaStream_t st, int prof_d, int prof_P) {
+                  const int* order_index, cudaStream_t st, int prof_d, int prof_P, int lda, int ncols) {
     if (G > 4096) throw std::invalid_argument("vrte_cuda: boundary system larger than 4096 rows");
+    if (lda <= 0) lda = G;
+    if (ncols <= 0) ncols = G;  // columns past G: right-hand sides eliminated along (augmented system)
     const int PB = panel_width(G), OB = outer_block();
-    const long long gg = (long long)G * G;
+    const long long gg = (long long)G * lda;
     int* map = perm;  // the row map IS the net permutation: row i of P A = row perm[i] of A
     {
         const long long total = (long long)batch * G;
@@ -617,29 +619,64 @@ void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatu
             const int jb = min(PB, K0 + NBk - k0);
             const int np = rend - k0;
             if (PB == 16)
-                panel_dispatch<16>(np, A, G, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
+                panel_dispatch<16>(np, A, G, lda, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
             else if (PB == 8)
-                panel_dispatch<8>(np, A, G, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
+                panel_dispatch<8>(np, A, G, lda, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
             else
-                panel_dispatch<4>(np, A, G, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
+                panel_dispatch<4>(np, A, G, lda, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
         }
-        const int rest = G - K0 - NBk;
+        const int rest = ncols - K0 - NBk;
         if (rest > 0) {
             // U12 = L11^-1 A12 on the block's pivot rows, by 64-row halves
             for (int r0 = K0; r0 < K0 + NBk; r0 += LU_NB) {
                 const int rb = min(LU_NB, K0 + NBk - r0);
-                trsm_launch<true>(A, G, A, G, gg, r0, rb, K0 + NBk, G, batch, st, map, map);
+                trsm_launch<true>(A, G, lda, A, lda, gg, r0, rb, K0 + NBk, ncols, batch, st, map, map);
                 const int below = K0 + NBk - (r0 + rb);
                 if (below > 0)
-                    rm_gemm(below, rest, rb, A + r0, G, gg, A + K0 + NBk, G, gg, A + K0 + NBk, G, gg, batch, -1.0,
-                            1.0, st, map + r0 + rb, map + r0, map + r0 + rb, G);
+                    rm_gemm(below, rest, rb, A + r0, lda, gg, A + K0 + NBk, lda, gg, A + K0 + NBk, lda, gg, batch,
+                            -1.0, 1.0, st, map + r0 + rb, map + r0, map + r0 + rb, G);
             }
             // trailing update: rows past the profile have zero multipliers
             if (rend - K0 - NBk > 0)
-                rm_gemm(rend - K0 - NBk, rest, NBk, A + K0, G, gg, A + K0 + NBk, G, gg, A + K0 + NBk, G, gg, batch,
-                        -1.0, 1.0, st, map + K0 + NBk, map + K0, map + K0 + NBk, G);
+                rm_gemm(rend - K0 - NBk, rest, NBk, A + K0, lda, gg, A + K0 + NBk, lda, gg, A + K0 + NBk, lda, gg,
+                        batch, -1.0, 1.0, st, map + K0 + NBk, map + K0, map + K0 + NBk, G);
         }
     }
+}
+
+// Back substitution on an augmented factorization ([A | B] factored with
+// ncols = G + R: the columns past G already hold L^-1 P B), in place through
+// the row map, down to row_lo; then the solution rows [row_lo, G) are
+// gathered in unknown order into X [batch][G][R].
+__global__ void lu_gather_aug_kernel(const double* Aall, int G, int lda, int R, const int* perm_all, int row_lo,
+                                     double* X, int batch) {
+    const long long total = (long long)batch * (G - row_lo) * R;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(e % R);
+        const long long rb = e / R;
+        const int i = row_lo + (int)(rb % (G - row_lo)), b = (int)(rb / (G - row_lo));
+        X[((size_t)b * G + i) * R + c] =
+            Aall[(size_t)b * G * lda + (size_t)perm_all[(size_t)b * G + i] * lda + G + c];
+    }
+}
+
+void lu_backsolve_aug(double* A, int G, int lda, int R, int batch, const int* perm, double* X, int row_lo,
+                      cudaStream_t st) {
+    const long long gg = (long long)G * lda;
+    const int nblk = (G + LU_NB - 1) / LU_NB;
+    const int blo = max(0, row_lo) / LU_NB, rl = blo * LU_NB;
+    for (int bk = nblk - 1; bk >= blo; --bk) {
+        const int k0 = bk * LU_NB, jb = min(LU_NB, G - k0);
+        trsm_launch<false>(A, G, lda, A + G, lda, gg, k0, jb, 0, R, batch, st, perm, perm);
+        if (k0 > rl)
+            rm_gemm(k0 - rl, R, jb, A + k0, lda, gg, A + G, lda, gg, A + G, lda, gg, batch, -1.0, 1.0, st, perm + rl,
+                    perm + k0, perm + rl, G);
+    }
+    const long long total = (long long)batch * (G - rl) * R;
+    lu_gather_aug_kernel<<<(unsigned)min(16384LL, (total + 255) / 256), 256, 0, st>>>(A, G, lda, R, perm, rl, X,
+                                                                                     batch);
+    VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
 void lu_solve_rm(const double* A, int G, int batch, const int* perm, const double* Bin, double* X,
@@ -657,7 +694,7 @@ void lu_solve_rm(const double* A, int G, int batch, const int* perm, const doubl
         const int jb = min(LU_NB, G - k0);
         (void)prof_d;
         (void)prof_P;
-        trsm_launch<true>(A, G, X, ncol, gn, k0, jb, 0, ncol, batch, st, perm, nullptr);
+        trsm_launch<true>(A, G, G, X, ncol, gn, k0, jb, 0, ncol, batch, st, perm, nullptr);
         if (G - k0 - jb > 0)
             rm_gemm(G - k0 - jb, ncol, jb, A + k0, G, gg, X + (size_t)k0 * ncol, ncol, gn,
                     X + (size_t)(k0 + jb) * ncol, ncol, gn, batch, -1.0, 1.0, st, perm + k0 + jb, nullptr, nullptr, G);
@@ -668,11 +705,24 @@ void lu_solve_rm(const double* A, int G, int batch, const int* perm, const doubl
     const int blo = max(0, row_lo) / LU_NB, rl = blo * LU_NB;
     for (int bk = nblk - 1; bk >= blo; --bk) {
         const int k0 = bk * LU_NB, jb = min(LU_NB, G - k0);
-        trsm_launch<false>(A, G, X, ncol, gn, k0, jb, 0, ncol, batch, st, perm, nullptr);
+        trsm_launch<false>(A, G, G, X, ncol, gn, k0, jb, 0, ncol, batch, st, perm, nullptr);
         if (k0 > rl)
             rm_gemm(k0 - rl, ncol, jb, A + k0, G, gg, X + (size_t)k0 * ncol, ncol, gn, X + (size_t)rl * ncol, ncol,
                     gn, batch, -1.0, 1.0, st, perm + rl, nullptr, nullptr, G);
     }
+}
+
+int lu_aug_launch_count(int G, int R, int row_lo) {
+    const int PB = panel_width(G), OB = outer_block();
+    int n = 1;  // row map init
+    for (int K0 = 0; K0 < G; K0 += OB) {
+        const int NBk = min(OB, G - K0);
+        n += (NBk + PB - 1) / PB;
+        if (G + R - K0 - NBk > 0) n += 2 * ((NBk + LU_NB - 1) / LU_NB) - 1 + 1;
+    }
+    const int nblk = (G + LU_NB - 1) / LU_NB, blo = max(0, row_lo) / LU_NB;
+    n += 2 * (nblk - blo) - 1 + 1;  // backward TRSM + GEMM per block, gather
+    return n;
 }
 
 int lu_rm_launch_count(int G) {
