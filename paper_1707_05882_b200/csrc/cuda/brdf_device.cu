@@ -696,6 +696,41 @@ int32_t guarded(vrte_cuda_result* r, Fn&& fn) {
 
 }  // namespace
 
+namespace {
+// Plan pool: every concurrent caller leases its own plan (device buffers +
+// stream), so the entry points stay reentrant, and plans outlive the calling
+// thread -- a batch's short-lived worker threads reuse them instead of
+// re-allocating gigabytes per call (a thread_local cache dies with its thread).
+std::mutex g_pool_mu;
+std::vector<std::unique_ptr<vrte_cuda_plan>> g_pool;
+std::vector<int> g_pool_dev;
+
+struct PlanLease {
+    std::unique_ptr<vrte_cuda_plan> p;
+    int dev = 0;
+    explicit PlanLease(int device) {
+        dev = device;
+        if (dev < 0) VRTE_CUDA_CHECK(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        for (size_t i = g_pool.size(); i-- > 0;)
+            if (g_pool_dev[i] == dev) {
+                p = std::move(g_pool[i]);
+                g_pool.erase(g_pool.begin() + i);
+                g_pool_dev.erase(g_pool_dev.begin() + i);
+                return;
+            }
+        p = std::make_unique<vrte_cuda_plan>();
+    }
+    ~PlanLease() {
+        if (!p) return;
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        g_pool.push_back(std::move(p));
+        g_pool_dev.push_back(dev);
+    }
+    vrte_cuda_plan& operator*() { return *p; }
+};
+}  // namespace
+
 extern "C" {
 
 int32_t vrte_cuda_device_count(void) {
@@ -800,14 +835,14 @@ void vrte_cuda_plan_destroy(vrte_cuda_plan* pl) { delete pl; }
 int32_t vrte_cuda_brdf(const vrte_cuda_problem* problem, double* table, vrte_cuda_result* result) {
     return guarded(result, [&]() -> int32_t {
         if (!table) throw std::invalid_argument("null table");
-        // One cached plan (device buffers + stream) per host thread: the entry
-        // point is reentrant (vrte.h "every entry point is reentrant") and
-        // concurrent callers run concurrently on their own streams; shape
-        // changes reallocate.
-        thread_local std::unique_ptr<vrte_cuda_plan> cached;
-        if (!cached) cached = std::make_unique<vrte_cuda_plan>();
-        vrte_cuda_plan& pl = *cached;
+        // A leased plan (device buffers + stream): the entry point is reentrant
+        // (vrte.h "every entry point is reentrant") and concurrent callers run
+        // concurrently on their own streams; shape changes reallocate.
+        if (!problem) throw std::invalid_argument("null problem");
+        PlanLease lease(problem->device);
+        vrte_cuda_plan& pl = *lease;
         setup_plan(pl, problem);
+        pl.full_solution = false;
         pl.launches = run_pipeline(pl, true);
         VRTE_CUDA_CHECK(cudaMemcpyAsync(table, pl.out.p, sizeof(double) * pl.out.n,
                                         cudaMemcpyDeviceToHost, pl.st));
@@ -818,13 +853,12 @@ int32_t vrte_cuda_brdf(const vrte_cuda_problem* problem, double* table, vrte_cud
 int32_t vrte_cuda_radiance_field(const vrte_cuda_problem* problem, const vrte_cuda_radiance* rad, double* values,
                                  double* reflectance, vrte_cuda_result* result) {
     return guarded(result, [&]() -> int32_t {
-        if (!rad || !values || !reflectance) throw std::invalid_argument("null buffer");
+        if (!problem || !rad || !values || !reflectance) throw std::invalid_argument("null buffer");
         if (problem->n_in != 1) throw std::invalid_argument("vrte_cuda: the radiance path solves one beam");
         if (rad->n_tau < 1 || rad->n_mu < 1 || rad->n_phi < 1 || !rad->taus || !rad->mus || !rad->phis)
             throw std::invalid_argument("vrte_cuda: empty radiance grid");
-        thread_local std::unique_ptr<vrte_cuda_plan> cached;
-        if (!cached) cached = std::make_unique<vrte_cuda_plan>();
-        vrte_cuda_plan& pl = *cached;
+        PlanLease lease(problem->device);
+        vrte_cuda_plan& pl = *lease;
         setup_plan(pl, problem);
         pl.full_solution = true;
         pl.launches = run_pipeline(pl, false);
