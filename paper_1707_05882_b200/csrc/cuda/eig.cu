@@ -2340,26 +2340,28 @@ __global__ void __launch_bounds__(256) trevc_grp_kernel(const double* Tall, cons
     __syncthreads();
     const int nl = s_nl;
     const double smlnum = kSafeMin * ((double)d / kUlp);
-    auto load_col = [&](double* dst, int c, int lim) {
+    auto load_col = [&](double (&dst)[RPL], int c, int lim) {
 #pragma unroll
         for (int i = 0; i < RPL; ++i) {
             const int r = lane + 32 * i;
             dst[i] = (c >= 0 && r < lim) ? T[r + (size_t)c * d] : 0.0;
         }
     };
-    auto pick = [&](const double* v, int r) {
+    auto pick = [&](const double (&v)[RPL], int r) {
         double x = 0.0;
 #pragma unroll
         for (int i = 0; i < RPL; ++i)
             if (i == (r >> 5)) x = v[i];
         return __shfl_sync(0xffffffffu, x, r & 31);
     };
-    auto put = [&](double* v, int r, double x) {
+    auto put = [&](double (&v)[RPL], int r, double x) {
 #pragma unroll
         for (int i = 0; i < RPL; ++i)
             if (i == (r >> 5) && lane == (r & 31)) v[i] = x;
     };
-    for (int g0 = w * G; g0 < nl; g0 += nw * G) {
+    // eigen-block groups spread over the CTAs of this matrix (blockIdx.y) and
+    // interleaved so every CTA mixes short and long back substitutions
+    for (int g0 = (w * gridDim.y + blockIdx.y) * G; g0 < nl; g0 += nw * gridDim.y * G) {
         double re[G][RPL], im[G][RPL];
         int top[G], kid[G];
         bool cx[G], on[G];
@@ -2942,11 +2944,11 @@ void launch_trevc(const double* T, const double* wr, const double* wi, double* Y
         const size_t gsm = 3 * (size_t)d * sizeof(double) + (size_t)d * sizeof(int);
         if (!(grp && std::string(grp) == "0") && rpl <= 8) {
             if (rpl <= 2)
-                trevc_grp_kernel<2, 4><<<batch, 256, gsm, st>>>(T, wr, wi, Y, d);
+                trevc_grp_kernel<2, 4><<<dim3(batch, (d + 15) / 16), 128, gsm, st>>>(T, wr, wi, Y, d);
             else if (rpl <= 4)
-                trevc_grp_kernel<4, 4><<<batch, 256, gsm, st>>>(T, wr, wi, Y, d);
+                trevc_grp_kernel<4, 4><<<dim3(batch, (d + 15) / 16), 128, gsm, st>>>(T, wr, wi, Y, d);
             else
-                trevc_grp_kernel<8, 4><<<batch, 256, gsm, st>>>(T, wr, wi, Y, d);
+                trevc_grp_kernel<8, 4><<<dim3(batch, (d + 15) / 16), 128, gsm, st>>>(T, wr, wi, Y, d);
         } else if (rpl <= 2)
             trevc_reg_kernel<2><<<batch, 256, d, st>>>(T, wr, wi, Y, d);
         else if (rpl <= 4)
