@@ -80,3 +80,29 @@ def test_incident_override_and_isotropy():
     r, *_ = O.radiance(oracle_material(d), N, 0.33, 2.0, d.stokes, [0.0, 0.5], zenith=4, azimuth=8)
     assert np.abs(g - r).max() < 1e-9 * np.abs(r).max()
     assert np.abs(g[..., 0] - g[..., :1, 0]).max() < 1e-12 * np.abs(g[..., 0]).max()
+
+
+def table_base(N, rho=0.2):
+    # smooth, partially polarizing Mueller table on the quadrature nodes (boundary.cpp:37-71)
+    nodes, _ = O.quadrature(N)
+    t = np.zeros((N, N, 4, 4))
+    for i, a in enumerate(nodes):
+        for j, b in enumerate(nodes):
+            f = 2 * rho * (1.0 + 0.3 * (a - b))
+            t[i, j] = f * np.array([[1, 0.1 * (a - b), 0, 0], [0.1 * (a - b), 0.5, 0, 0],
+                                    [0, 0, 0.3, 0.05], [0, 0, -0.05, 0.3]])
+    return t
+
+
+def test_mueller_table_base_brdf_and_radiance_match_oracle():
+    # the bilinear Mueller-table base (base_type 2) through both product paths
+    N = 8
+    d = desc([(M.RAYLEIGH, 0.9, 1.5)], "mueller_table", mu0=0.55, phi0=0.4, stokes=(1.0, 0.2, 0.1, -0.1))
+    d.table = table_base(N)
+    nodes, _ = O.quadrature(N)
+    g = V.compute_brdf(product_material(d), V.options(N), nodes, 7).table()
+    r, _ = O.brdf(oracle_material(d), N, nodes, 7)
+    assert np.abs(g - r).max() < 1e-9 * np.abs(r).max()
+    f, (t, mus, phis, gf), (omu, ophi, rf, orefl) = run_pair(d, N, [0.0, 0.7, 1.5], zen=5, azi=6)
+    assert np.abs(gf - rf).max() < 1e-9 * np.abs(rf).max()
+    assert np.allclose(f.reflectance(), orefl, rtol=1e-10, atol=1e-13)
