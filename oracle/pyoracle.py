@@ -245,3 +245,37 @@ def radiance(mat: Material, N, mu0, phi0, stokes, taus=(0.0,), zenith=11, azimut
                                     C.c_size_t(0 if ph_in is None else len(ph_in)), 1 if nodal else 0,
                                     _dp(mo), _dp(po), _dp(vals), _dp(refl), C.byref(tm)))
     return vals, mo, po, refl
+
+
+class McTally:
+    """mc.hpp TallyGrid: raw sums [2, zb, ab, 4], hits [2, zb, ab] and the flux-weighted
+    bin-average radiance / standard error of mc.cpp:233-253."""
+
+    def __init__(self, s, sq, hits, photons, mu0, zb, ab):
+        self.sum, self.sum_sq, self.hits = s, sq, hits
+        self.photons, self.mu0, self.zb, self.ab = photons, mu0, zb, ab
+
+    def bin_flux_measure(self, iz):
+        lo, hi = iz / self.zb, (iz + 1) / self.zb
+        return 0.5 * (hi * hi - lo * lo) * (2 * np.pi / self.ab)
+
+    def radiance(self, hemi, iz, ia):
+        return self.sum[hemi, iz, ia] * self.mu0 / (self.photons * self.bin_flux_measure(iz))
+
+    def std_error(self, hemi, iz, ia):
+        n = float(self.photons)
+        mean = self.sum[hemi, iz, ia] / n
+        var = np.maximum(0.0, self.sum_sq[hemi, iz, ia] / n - mean * mean)
+        return self.mu0 / self.bin_flux_measure(iz) * np.sqrt(var / max(1.0, n - 1.0))
+
+
+def mc_trace(mat: Material, mu0, phi0, stokes, photons, seed, zb, ab, threads=0) -> McTally:
+    s = np.zeros((2, zb, ab, 4))
+    sq = np.zeros((2, zb, ab, 4))
+    h = np.zeros((2, zb, ab), dtype=np.uint64)
+    st = np.ascontiguousarray(stokes, np.float64)
+    cm = mat.c()
+    _check(lib().oracle_mc_trace(C.byref(cm), C.c_double(mu0), C.c_double(phi0), _dp(st), C.c_uint64(photons),
+                                 C.c_uint64(seed), zb, ab, threads, _dp(s), _dp(sq),
+                                 h.ctypes.data_as(C.POINTER(C.c_uint64))))
+    return McTally(s, sq, h, photons, mu0, zb, ab)

@@ -1341,6 +1341,317 @@ static double reduce_azimuth(double phi) {  // types.cpp:7-12
     return r;
 }
 
+// ---------------------------------------------------------------- Monte Carlo (mc.cpp:1-315)
+// Polarized photon tracer restated for the statistical cross-checks of
+// SURVEY §8(f) rank 4.  Per-photon xoshiro256++ streams, tabulated inverse CDF
+// of the intensity phase function, meridian-frame Stokes rotations, fixed
+// 16384-photon blocks merged in order (thread-count independent).
+struct McRng {  // mc.cpp:11-45
+    uint64_t s[4];
+    static uint64_t splitmix(uint64_t& x) {
+        x += 0x9e3779b97f4a7c15ull;
+        uint64_t z = x;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        return z ^ (z >> 31);
+    }
+    McRng(uint64_t seed, uint64_t stream) {
+        uint64_t x = seed ^ (0x9e3779b97f4a7c15ull * (stream + 1));
+        for (auto& w : s) w = splitmix(x);
+    }
+    static uint64_t rotl(uint64_t v, int k) { return (v << k) | (v >> (64 - k)); }
+    uint64_t next() {
+        const uint64_t result = rotl(s[0] + s[3], 23) + s[0];
+        const uint64_t t = s[1] << 17;
+        s[2] ^= s[0];
+        s[3] ^= s[1];
+        s[1] ^= s[2];
+        s[0] ^= s[3];
+        s[2] ^= t;
+        s[3] = rotl(s[3], 45);
+        return result;
+    }
+    double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+};
+static double scalar_phase(const Layer& layer, double x) {  // kernel.cpp:179-186
+    const int lmax = layer.order_count() - 1;
+    const auto d00 = wigner_seq(0, 0, lmax, x);
+    double a1 = 0.0;
+    for (int l = 0; l <= lmax; ++l) a1 += layer.coeffs[l](0, 0) * d00[l];
+    return a1;
+}
+struct McPdf {  // mc.cpp:47-88
+    static constexpr int kCells = 2048;
+    std::vector<double> cdf, density;
+    explicit McPdf(const Layer& layer) {
+        cdf.assign(kCells + 1, 0.0);
+        density.assign(kCells, 0.0);
+        const double dx = 2.0 / kCells;
+        double prev = std::max(0.0, scalar_phase(layer, -1.0)), total = 0.0;
+        for (int i = 0; i < kCells; ++i) {
+            const double x1 = std::min(-1.0 + dx * (i + 1), 1.0);
+            const double cur = std::max(0.0, scalar_phase(layer, x1));
+            total += 0.5 * (prev + cur) * dx;
+            cdf[i + 1] = total;
+            prev = cur;
+        }
+        if (total <= 0.0) throw ValidationError("mc: intensity phase function has no positive mass");
+        for (auto& c : cdf) c /= total;
+        for (int i = 0; i < kCells; ++i) density[i] = (cdf[i + 1] - cdf[i]) / dx;
+    }
+    std::pair<double, double> sample(double u) const {
+        int lo = 0, hi = kCells;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) / 2;
+            (cdf[mid] <= u ? lo : hi) = mid;
+        }
+        const double mass = cdf[lo + 1] - cdf[lo];
+        const double frac = mass > 0.0 ? (u - cdf[lo]) / mass : 0.5;
+        const double dx = 2.0 / kCells;
+        const double x = std::clamp(-1.0 + dx * (lo + frac), -1.0, 1.0);
+        return {x, std::max(density[lo], 1e-300)};
+    }
+};
+using V3 = std::array<double, 3>;
+static V3 v3norm(V3 a) {
+    const double n = std::sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+    return {a[0] / n, a[1] / n, a[2] / n};
+}
+static V3 cross(const V3& a, const V3& b) {
+    return {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]};
+}
+static double dot(const V3& a, const V3& b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+static V3 unit_dir(double mu, double phi) {  // types.hpp:94-97
+    const double sn = std::sqrt(std::max(0.0, 1.0 - mu * mu));
+    return {sn * std::cos(phi), sn * std::sin(phi), mu};
+}
+static V3 rotate_direction(const V3& d, double ct, double psi) {  // mc.cpp:107-114
+    const double st = std::sqrt(std::max(0.0, 1.0 - ct * ct));
+    const V3 a = std::abs(d[2]) < 0.99 ? V3{0, 0, 1} : V3{1, 0, 0};
+    const V3 t1 = v3norm(cross(d, a)), t2 = cross(d, t1);
+    const double c = std::cos(psi), sn = std::sin(psi);
+    return v3norm({ct * d[0] + st * (c * t1[0] + sn * t2[0]), ct * d[1] + st * (c * t1[1] + sn * t2[1]),
+                   ct * d[2] + st * (c * t1[2] + sn * t2[2])});
+}
+static V3 nudge_off_pole(V3 d) {  // rotation.cpp:9-15
+    if (1.0 - std::abs(d[2]) < 1e-12) {
+        d[0] += 1e-9;
+        d = v3norm(d);
+    }
+    return d;
+}
+static void meridian_basis(const V3& dir, V3& l, V3& r) {  // rotation.cpp:19-29
+    const V3 d = nudge_off_pole(dir);
+    const double sxy = std::sqrt(std::max(1e-300, d[0] * d[0] + d[1] * d[1]));
+    const double cphi = d[0] / sxy, sphi = d[1] / sxy;
+    l = {d[2] * cphi, d[2] * sphi, -sxy};
+    r = {-sphi, cphi, 0.0};
+}
+static void scatter_geometry(const V3& din_raw, const V3& dout_raw, double& ct, double& eta_in, double& eta_out) {
+    V3 din = nudge_off_pole(din_raw), dout = nudge_off_pole(dout_raw);  // rotation.cpp:42-68
+    double c = std::clamp(dot(din, dout), -1.0, 1.0);
+    if (1.0 - std::abs(c) < 1e-12) {
+        const V3 probe = std::abs(dout[2]) < 0.9 ? V3{0, 0, 1} : V3{1, 0, 0};
+        dout = v3norm({dout[0] + 1e-9 * probe[0], dout[1] + 1e-9 * probe[1], dout[2] + 1e-9 * probe[2]});
+        c = std::clamp(dot(din, dout), -1.0, 1.0);
+    }
+    const V3 lin = v3norm({dout[0] - c * din[0], dout[1] - c * din[1], dout[2] - c * din[2]});
+    const V3 lout = v3norm({c * dout[0] - din[0], c * dout[1] - din[1], c * dout[2] - din[2]});
+    const V3 rout = cross(dout, lout);
+    V3 il, ir, ol, orr;
+    meridian_basis(din, il, ir);
+    meridian_basis(dout, ol, orr);
+    ct = c;
+    eta_in = std::atan2(dot(lin, ir), dot(lin, il));
+    eta_out = std::atan2(dot(ol, rout), dot(ol, lout));
+}
+static M4 stokes_rot(double eta) {  // rotation.cpp:31-40
+    M4 l;
+    l(0, 0) = l(3, 3) = 1.0;
+    const double c = std::cos(2.0 * eta), sn = std::sin(2.0 * eta);
+    l(1, 1) = c;
+    l(1, 2) = sn;
+    l(2, 1) = -sn;
+    l(2, 2) = c;
+    return l;
+}
+static M4 scatter_matrix(const Layer& layer, double ct) {  // kernel.cpp:147-177
+    const int lmax = layer.order_count() - 1;
+    const auto d00 = wigner_seq(0, 0, lmax, ct), d02 = wigner_seq(0, 2, lmax, ct), d22 = wigner_seq(2, 2, lmax, ct),
+               d2m2 = wigner_seq(2, -2, lmax, ct);
+    double a1 = 0, a4 = 0, b1 = 0, b2 = 0, apc = 0, amc = 0;
+    for (int l = 0; l <= lmax; ++l) {
+        const M4& b = layer.coeffs[l];  // greek_of: beta, alpha, gamma, delta, eps, zeta
+        a1 += b(0, 0) * d00[l];
+        a4 += b(3, 3) * d00[l];
+        b1 += b(0, 1) * d02[l];
+        b2 -= b(3, 2) * d02[l];
+        apc += (b(1, 1) + b(2, 2)) * d22[l];
+        amc += (b(1, 1) - b(2, 2)) * d2m2[l];
+    }
+    M4 f;
+    f(0, 0) = a1;
+    f(0, 1) = f(1, 0) = b1;
+    f(1, 1) = 0.5 * (apc + amc);
+    f(2, 2) = 0.5 * (apc - amc);
+    f(2, 3) = b2;
+    f(3, 2) = -b2;
+    f(3, 3) = a4;
+    return f;
+}
+struct McGrid {
+    int zb = 0, ab = 0;
+    std::vector<double> sum, sum_sq;  // [2][zb][ab][4]
+    std::vector<uint64_t> hits;
+};
+struct McTracer {  // mc.cpp:119-231
+    const Material& spec;
+    double mu0, phi0;
+    const double* stokes;
+    const std::vector<double>& tops;
+    double total;
+    const std::vector<McPdf>& pdfs;
+    const Quad* base_quad;
+    McGrid& g;
+    int layer_at(double tau) const {  // mc.cpp:100-105
+        int p = (int)tops.size() - 1;
+        while (p > 0 && tau < tops[p]) --p;
+        return p;
+    }
+    void tally(const V3& dir, const double w[4], bool top) {
+        const double mu = std::abs(dir[2]);
+        if (mu <= 0.0) return;
+        const double phi = reduce_azimuth(std::atan2(dir[1], dir[0]));
+        const int iz = std::min((int)(mu * g.zb), g.zb - 1);
+        const int ia = std::min((int)(phi / kTwoPi * g.ab), g.ab - 1);
+        const size_t idx = ((size_t)(top ? 0 : 1) * g.zb + iz) * g.ab + ia;
+        for (int c = 0; c < 4; ++c) {
+            g.sum[idx * 4 + c] += w[c];
+            g.sum_sq[idx * 4 + c] += w[c] * w[c];
+        }
+        g.hits[idx] += 1;
+    }
+    void trace(McRng& rng) {
+        double tau = 0.0;
+        V3 dir = unit_dir(-mu0, phi0);
+        double w[4] = {stokes[0], stokes[1], stokes[2], stokes[3]};
+        int events = 0;
+        for (int bounce = 0; bounce < 100000; ++bounce) {
+            const double step = -std::log(std::max(1e-300, 1.0 - rng.uniform()));
+            const double mu = dir[2];
+            if (mu == 0.0) return;
+            const double dtau = -mu * step;
+            if (mu > 0.0 && tau + dtau < 0.0) {
+                if (events > 0) tally(dir, w, true);
+                return;
+            }
+            if (mu < 0.0 && tau + dtau > total) {
+                if (spec.base.type == 0) {
+                    if (events > 0) tally(dir, w, false);
+                    return;
+                }
+                tau = total;
+                if (spec.base.type == 1) {
+                    const double refl = spec.base.rho * w[0];
+                    if (refl <= 0.0) return;
+                    w[0] = refl;
+                    w[1] = w[2] = w[3] = 0.0;
+                } else {
+                    const double mu_in = -dir[2];
+                    const double mu_up = std::sqrt(std::max(rng.uniform(), 1e-300));
+                    const double phi = kTwoPi * rng.uniform();
+                    const M4 r = base_row_at(spec.base, *base_quad, mu_up, mu_in);
+                    double nw[4];
+                    for (int a = 0; a < 4; ++a) {
+                        nw[a] = 0.0;
+                        for (int b = 0; b < 4; ++b) nw[a] += r(a, b) * w[b];
+                        nw[a] *= 0.5;
+                    }
+                    std::copy(nw, nw + 4, w);
+                    if (w[0] <= 0.0) return;
+                    dir = unit_dir(std::max(mu_up, 1e-9), reduce_azimuth(phi));
+                    ++events;
+                    continue;
+                }
+                const double mu_up = std::sqrt(std::max(rng.uniform(), 1e-300));
+                const double phi = kTwoPi * rng.uniform();
+                dir = unit_dir(std::max(mu_up, 1e-9), reduce_azimuth(phi));
+                ++events;
+                continue;
+            }
+            tau += dtau;
+            const int li = layer_at(tau);
+            const Layer& layer = spec.layers[li];
+            if (layer.omega <= 0.0) return;
+            const auto [ct, pdf] = pdfs[li].sample(rng.uniform());
+            const double psi = kTwoPi * rng.uniform();
+            const V3 nd = rotate_direction(dir, ct, psi);
+            double c2, ein, eout;
+            scatter_geometry(dir, nd, c2, ein, eout);
+            const M4 z = mul(mul(stokes_rot(eout), scatter_matrix(layer, c2)), stokes_rot(ein));
+            double nw[4];
+            const double f = layer.omega / (2.0 * pdf);
+            for (int a = 0; a < 4; ++a) {
+                nw[a] = 0.0;
+                for (int b = 0; b < 4; ++b) nw[a] += z(a, b) * w[b];
+                nw[a] *= f;
+            }
+            std::copy(nw, nw + 4, w);
+            dir = nd;
+            ++events;
+            if (w[0] <= 0.0) return;
+            if (w[0] < 1e-4 * stokes[0]) {  // kRouletteThreshold, kRouletteBoost (mc.cpp:116-117)
+                if (rng.uniform() * 10.0 > 1.0) return;
+                for (auto& x : w) x *= 10.0;
+            }
+        }
+    }
+};
+// mc.cpp:256-312
+static McGrid mc_trace(const Material& spec, double mu0, double phi0, const double* stokes, uint64_t photons,
+                       uint64_t seed, int zb, int ab, int threads) {
+    if (photons < 1) throw ValidationError("mc: photon count must be positive");
+    if (zb < 1 || ab < 1) throw ValidationError("mc: bin counts must be positive");
+    const int P = (int)spec.layers.size();
+    std::vector<double> tops(P, 0.0);
+    for (int p = 1; p < P; ++p) tops[p] = tops[p - 1] + spec.layers[p - 1].tau;
+    const double total = tops.back() + spec.layers.back().tau;
+    std::vector<McPdf> pdfs;
+    for (const auto& l : spec.layers) pdfs.emplace_back(l);
+    Quad bq;
+    if (spec.base.type == 2) bq = build_quadrature(spec.base.n);
+    auto make = [&] {
+        McGrid g;
+        g.zb = zb;
+        g.ab = ab;
+        g.sum.assign((size_t)2 * zb * ab * 4, 0.0);
+        g.sum_sq.assign((size_t)2 * zb * ab * 4, 0.0);
+        g.hits.assign((size_t)2 * zb * ab, 0);
+        return g;
+    };
+    McGrid tot = make();
+    const uint64_t kBlock = 16384, nblk = (photons + kBlock - 1) / kBlock, kChunk = 256;
+    for (uint64_t c0 = 0; c0 < nblk; c0 += kChunk) {
+        const uint64_t chunk = std::min(kChunk, nblk - c0);
+        std::vector<McGrid> gs(chunk, make());
+        parallel_for(threads, chunk, [&](size_t b) {
+            const uint64_t blk = c0 + b, begin = blk * kBlock, end = std::min(begin + kBlock, photons);
+            McTracer tr{spec, mu0, phi0, stokes, tops, total, pdfs, spec.base.type == 2 ? &bq : nullptr, gs[b]};
+            for (uint64_t ph = begin; ph < end; ++ph) {
+                McRng rng(seed, ph);
+                tr.trace(rng);
+            }
+        });
+        for (uint64_t b = 0; b < chunk; ++b)
+            for (size_t i = 0; i < tot.sum.size(); ++i) {
+                tot.sum[i] += gs[b].sum[i];
+                tot.sum_sq[i] += gs[b].sum_sq[i];
+                if (i % 4 == 0) tot.hits[i / 4] += gs[b].hits[i / 4];
+            }
+    }
+    return tot;
+}
+
 struct OrderState {
     Kernel kernel;
     Reduced ops;
@@ -2007,6 +2318,27 @@ int32_t oracle_radiance_at(const oracle_material* cm, int32_t quad_n, int32_t or
         if (mus_out) std::copy(mus.begin(), mus.end(), mus_out);
         if (phis_out) std::copy(phis.begin(), phis.end(), phis_out);
         if (timings) *timings = solver.t;
+    });
+}
+
+
+// mc.cpp:256-312 (vrte_mc_trace, capi.cpp:328-346): raw tallies sum/sum_sq [2][zb][ab][4], hits [2][zb][ab]
+int32_t oracle_mc_trace(const oracle_material* cm, double mu0, double phi0, const double* stokes, uint64_t photons,
+                        uint64_t seed, int32_t zenith_bins, int32_t azimuth_bins, int32_t threads, double* sum,
+                        double* sum_sq, uint64_t* hits) {
+    if (!cm || !stokes || !sum || !sum_sq || !hits) {
+        g_err = "null argument";
+        return 5;
+    }
+    return guarded([&] {
+        int th = threads;
+        if (th <= 0) th = (int)std::max(1u, std::thread::hardware_concurrency());
+        const auto mat = vo::from_c(cm);
+        const auto g = vo::mc_trace(mat, mu0, vo::reduce_azimuth(phi0), stokes, photons, seed, zenith_bins,
+                                    azimuth_bins, th);
+        std::copy(g.sum.begin(), g.sum.end(), sum);
+        std::copy(g.sum_sq.begin(), g.sum_sq.end(), sum_sq);
+        std::copy(g.hits.begin(), g.hits.end(), hits);
     });
 }
 

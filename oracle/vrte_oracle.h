@@ -104,6 +104,11 @@ int32_t oracle_radiance_at(const oracle_material* mat, int32_t quad_n, int32_t o
                            const double* phis_in, size_t n_phi_in, int32_t nodal, double* mus_out,
                            double* phis_out, double* values, double* reflectance, oracle_timings* timings);
 
+/* mc.cpp:1-315: raw Monte Carlo tallies (sum, sum_sq [2][zb][ab][4]; hits [2][zb][ab]). */
+int32_t oracle_mc_trace(const oracle_material* mat, double mu0, double phi0, const double* stokes, uint64_t photons,
+                        uint64_t seed, int32_t zenith_bins, int32_t azimuth_bins, int32_t threads, double* sum,
+                        double* sum_sq, uint64_t* hits);
+
 #ifdef __cplusplus
 }
 #endif
