@@ -93,6 +93,24 @@ typedef struct vrte_cuda_radiance {
 VRTE_API int32_t vrte_cuda_radiance_field(const vrte_cuda_problem* problem, const vrte_cuda_radiance* rad,
                                           double* values, double* reflectance, vrte_cuda_result* result);
 
+/* Polarized Monte Carlo tracer (mc.cpp:1-315): raw tallies
+ * sum / sum_sq [2][zb][ab][4] and hits [2][zb][ab] (host arrays).  Layers top
+ * first; greek rows beta alpha gamma delta eps zeta. */
+typedef struct vrte_cuda_mc {
+    int32_t n_layers, Lc, base_type, table_n, zb, ab;
+    uint64_t photons, seed;
+    double mu0, phi0, rho, total;
+    double stokes[4];
+    const double* greek;        /* [n_layers][Lc][6] */
+    const double* omega;        /* [n_layers] */
+    const double* tops;         /* [n_layers] */
+    const double* table;        /* [table_n^2][16] (base_type 2) */
+    const double* table_nodes;  /* [table_n] */
+    int32_t device;
+} vrte_cuda_mc;
+VRTE_API int32_t vrte_cuda_mc_trace(const vrte_cuda_mc* mc, double* sum, double* sum_sq, uint64_t* hits,
+                                    vrte_cuda_result* result);
+
 /* Full solve: host inputs -> host table [n_in][N][n_dphi][16]. */
 VRTE_API int32_t vrte_cuda_brdf(const vrte_cuda_problem* problem, double* table,
                                 vrte_cuda_result* result);

@@ -137,7 +137,7 @@ EXPORTED = [
     "vrte_cuda_plan_fetch_up", "vrte_cuda_plan_fetch_modes", "vrte_cuda_plan_fetch_ef",
     "vrte_cuda_plan_destroy",
     "vrte_cuda_synthesize", "vrte_cuda_device_count", "vrte_cuda_lu_solve", "vrte_cuda_hessenberg", "vrte_cuda_schur",
-    "vrte_cuda_radiance_field",
+    "vrte_cuda_radiance_field", "vrte_cuda_mc_trace",
 ]
 
 
@@ -192,6 +192,9 @@ def lib():
     L.vrte_field_free.argtypes = [vp]
     L.vrte_mc_trace.argtypes = [vp, C.POINTER(Options), C.c_uint64, C.c_uint64, C.c_int32,
                                 C.c_int32, C.POINTER(vp)]
+    L.vrte_mc_tally_row.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, dp]
+    L.vrte_mc_tally_write_csv.argtypes = [vp, C.c_char_p]
+    L.vrte_mc_tally_free.argtypes = [vp]
     _lib = L
     return L
 
@@ -425,6 +428,44 @@ def solve_radiance(material: Material, opts: Options, taus=()) -> Field:
     _check(lib().vrte_solve_radiance(material._h, C.byref(opts), _dp(t) if len(t) else None, len(t),
                                      C.byref(h)))
     return Field(h)
+
+
+class McTally:
+    """Opaque vrte_mc_tally handle (vrte.h:119-129): binned exiting radiance of the tracer."""
+
+    def __init__(self, handle, zb, ab):
+        self._h, self.zb, self.ab = handle, zb, ab
+
+    def row(self, hemisphere, iz, ia) -> np.ndarray:
+        """(mu center, phi center, I, Q, U, V, se_I, se_Q, se_U, se_V)"""
+        r = np.zeros(10)
+        _check(lib().vrte_mc_tally_row(self._h, hemisphere, iz, ia, _dp(r)))
+        return r
+
+    def rows(self) -> np.ndarray:
+        return np.array([[[self.row(h, iz, ia) for ia in range(self.ab)] for iz in range(self.zb)] for h in (0, 1)])
+
+    def write_csv(self, path: str):
+        _check(lib().vrte_mc_tally_write_csv(self._h, path.encode()))
+
+    def close(self):
+        if self._h:
+            lib().vrte_mc_tally_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def mc_trace(material: Material, opts: Options, photons: int, seed: int, zenith_bins: int,
+             azimuth_bins: int) -> McTally:
+    """vrte_mc_trace (vrte.h:123-125) on the GPU tracer (mc.cu)."""
+    h = C.c_void_p()
+    _check(lib().vrte_mc_trace(material._h, C.byref(opts), photons, seed, zenith_bins, azimuth_bins, C.byref(h)))
+    return McTally(h, zenith_bins, azimuth_bins)
 
 
 def compute_brdf_batch(materials, opts: Options, mu_in, n_dphi: int = 19, basis=None,

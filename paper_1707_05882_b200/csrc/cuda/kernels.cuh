@@ -143,4 +143,28 @@ struct RadArgs {
 };
 int launch_radiance(RadArgs a, cudaStream_t st);
 
+
+// mc.cu: polarized Monte Carlo tracer (mc.cpp).  Device pointers except the scalars.
+struct McArgs {
+    uint64_t photons, seed, ph0;  // ph0: first photon of this launch (chunked)
+    int zb, ab, n_layers, Lc, base_type, table_n;
+    double mu0, phi0, rho, total;
+    double stokes[4];
+    const double* greek;        // [n_layers][Lc][6] beta alpha gamma delta eps zeta
+    const int* medium;          // [n_layers] -> greek/omega row
+    const double* omega;        // [n_layers]
+    const double* tops;         // [n_layers] optical depth of each layer top
+    const double* table;        // [table_n^2][16] Mueller-table base
+    const double* table_nodes;  // [table_n] Gauss nodes of the table
+    double* cdf;                // [n_layers][2049]
+    double* density;            // [n_layers][2048]
+    int* fail;
+    double* cta_grid;           // [n_cta][2 zb ab][9]
+    double* out;                // [2 zb ab][9]: sum[4], sum_sq[4], hits
+};
+int mc_photons_per_cta();
+// tabulates the phase functions, then traces photons [ph0, ph0 + n) into out (accumulated)
+int launch_mc_tables(McArgs a, double* edge_scratch, cudaStream_t st);
+int launch_mc_chunk(McArgs a, uint64_t n, cudaStream_t st);
+
 }  // namespace vrte

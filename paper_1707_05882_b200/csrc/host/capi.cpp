@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <atomic>
 #include <memory>
 #include <mutex>
@@ -268,6 +269,14 @@ struct vrte_material {
     MaterialSpec spec;
 };
 
+struct vrte_mc_tally {  // capi.cpp:83-86 (mc.hpp TallyGrid)
+    std::vector<double> sum, sum_sq;  // [2][zb][ab][4]
+    std::vector<uint64_t> hits;       // [2][zb][ab]
+    int zb = 0, ab = 0;
+    uint64_t photons = 0;
+    double mu0 = 1.0, tau_bottom = 0.0;
+};
+
 struct vrte_field {  // capi.cpp:69-74
     RadianceField field;
     vrte_timings timings{};
@@ -448,18 +457,148 @@ vrte_status vrte_field_reflectance(const vrte_field* field, double out[4]) {
 }
 void vrte_field_free(vrte_field* field) { delete field; }
 
-vrte_status vrte_mc_trace(const vrte_material*, const vrte_options*, uint64_t, uint64_t, int32_t,
-                          int32_t, vrte_mc_tally** out) {
-    if (out) *out = nullptr;
-    return not_built("vrte_mc_trace");
+// ---------------------------------------------------------------- Monte Carlo
+// capi.cpp:328-378 / mc.cpp: the tracer runs on the GPU (mc.cu), photon per thread.
+vrte_status vrte_mc_trace(const vrte_material* material, const vrte_options* options, uint64_t photons,
+                          uint64_t seed, int32_t zenith_bins, int32_t azimuth_bins, vrte_mc_tally** out) {
+    if (!material || !out) return set_error(VRTE_E_ARGUMENT, "null argument");
+    return guarded([&] {
+        auto h = std::make_unique<vrte_mc_tally>();
+        MaterialSpec spec = material->spec;
+        if (options && options->incident_override) {
+            spec.source.mu0 = options->incident_mu0;
+            spec.source.phi0 = options->incident_phi0;
+        }
+        if (photons < 1) throw ValidationError("mc: photon count must be positive");
+        if (zenith_bins < 1 || azimuth_bins < 1) throw ValidationError("mc: bin counts must be positive");
+        const int P = (int)spec.layers.size(), Lc = spec.order_count();
+        std::vector<double> greek((size_t)P * Lc * 6, 0.0), omega(P), tops(P, 0.0);
+        for (int p = 0; p < P; ++p) {
+            const auto& layer = spec.layers[p];
+            omega[p] = layer.omega;
+            if (p > 0) tops[p] = tops[p - 1] + spec.layers[p - 1].tau;
+            for (int l = 0; l < layer.order_count() && l < Lc; ++l) {
+                const Mat4& bm = layer.coeffs[l];  // greek_of, kernel.cpp:14-16
+                double* g = &greek[((size_t)p * Lc + l) * 6];
+                g[0] = at(bm, 0, 0);
+                g[1] = at(bm, 1, 1);
+                g[2] = at(bm, 0, 1);
+                g[3] = at(bm, 3, 3);
+                g[4] = at(bm, 3, 2);
+                g[5] = at(bm, 2, 2);
+            }
+        }
+        vrte_cuda_mc mc{};
+        mc.n_layers = P;
+        mc.Lc = Lc;
+        mc.zb = zenith_bins;
+        mc.ab = azimuth_bins;
+        mc.photons = photons;
+        mc.seed = seed;
+        mc.mu0 = spec.source.mu0;
+        mc.phi0 = reduce_azimuth(spec.source.phi0);
+        for (int c = 0; c < 4; ++c) mc.stokes[c] = spec.source.stokes[c];
+        mc.total = tops[P - 1] + spec.layers[P - 1].tau;
+        mc.greek = greek.data();
+        mc.omega = omega.data();
+        mc.tops = tops.data();
+        std::vector<double> table_flat, table_nodes;
+        if (const auto* lam = std::get_if<LambertianBase>(&spec.base)) {
+            mc.base_type = 1;
+            mc.rho = lam->rho;
+        } else if (const auto* tab = std::get_if<MuellerTableBase>(&spec.base)) {
+            mc.base_type = 2;
+            mc.table_n = tab->n;
+            table_flat.resize((size_t)tab->n * tab->n * 16);
+            for (size_t e = 0; e < tab->table.size(); ++e) std::memcpy(&table_flat[e * 16], tab->table[e].data(), 128);
+            table_nodes = build_double_gauss_quadrature(tab->n).nodes;  // mc.cpp:274-276
+            mc.table = table_flat.data();
+            mc.table_nodes = table_nodes.data();
+        }
+        const char* dev = std::getenv("VRTE_DEVICE");
+        mc.device = dev ? std::atoi(dev) : -1;
+        const size_t bins = 2 * (size_t)zenith_bins * azimuth_bins;
+        h->sum.assign(bins * 4, 0.0);
+        h->sum_sq.assign(bins * 4, 0.0);
+        h->hits.assign(bins, 0);
+        vrte_cuda_result r{};
+        const int32_t rc = vrte_cuda_mc_trace(&mc, h->sum.data(), h->sum_sq.data(), h->hits.data(), &r);
+        if (rc == 2) throw ValidationError(r.message);
+        if (rc == 5) throw std::invalid_argument(r.message);
+        if (rc != 0) throw NumericalError(r.message);
+        h->zb = zenith_bins;
+        h->ab = azimuth_bins;
+        h->photons = photons;
+        h->mu0 = spec.source.mu0;
+        h->tau_bottom = mc.total;
+        *out = h.release();
+        return VRTE_OK;
+    });
 }
-vrte_status vrte_mc_tally_row(const vrte_mc_tally*, int32_t, int32_t, int32_t, double*) {
-    return not_built("vrte_mc_tally_row");
+
+namespace {
+// mc.cpp:235-253: flux-weighted bin average and its standard error
+double mc_bin_flux_measure(const vrte_mc_tally& t, int iz) {
+    const double lo = (double)iz / t.zb, hi = (double)(iz + 1) / t.zb;
+    return 0.5 * (hi * hi - lo * lo) * (kTwoPi / t.ab);
 }
-vrte_status vrte_mc_tally_write_csv(const vrte_mc_tally*, const char*) {
-    return not_built("vrte_mc_tally_write_csv");
+void mc_radiance(const vrte_mc_tally& t, int hemi, int iz, int ia, double s[4], double se[4]) {
+    const size_t idx = ((size_t)hemi * t.zb + iz) * t.ab + ia;
+    const double n = (double)t.photons, meas = mc_bin_flux_measure(t, iz);
+    for (int c = 0; c < 4; ++c) {
+        s[c] = t.sum[idx * 4 + c] * (t.mu0 / (n * meas));
+        const double mean = t.sum[idx * 4 + c] / n;
+        const double var = std::max(0.0, t.sum_sq[idx * 4 + c] / n - mean * mean);
+        se[c] = (t.mu0 / meas) * std::sqrt(var / std::max(1.0, n - 1.0));
+    }
 }
-void vrte_mc_tally_free(vrte_mc_tally*) {}
+}  // namespace
+
+vrte_status vrte_mc_tally_row(const vrte_mc_tally* tally, int32_t hemisphere, int32_t zenith_bin,
+                              int32_t azimuth_bin, double row[10]) {
+    if (!tally || !row) return set_error(VRTE_E_ARGUMENT, "null argument");
+    const auto& t = *tally;
+    if (hemisphere < 0 || hemisphere > 1 || zenith_bin < 0 || zenith_bin >= t.zb || azimuth_bin < 0 ||
+        azimuth_bin >= t.ab)
+        return set_error(VRTE_E_ARGUMENT, "tally index out of range");
+    double s[4], se[4];
+    mc_radiance(t, hemisphere, zenith_bin, azimuth_bin, s, se);
+    row[0] = (zenith_bin + 0.5) / t.zb;
+    row[1] = kTwoPi * (azimuth_bin + 0.5) / t.ab;
+    for (int c = 0; c < 4; ++c) {
+        row[2 + c] = s[c];
+        row[6 + c] = se[c];
+    }
+    return VRTE_OK;
+}
+vrte_status vrte_mc_tally_write_csv(const vrte_mc_tally* tally, const char* path) {
+    if (!tally || !path) return set_error(VRTE_E_ARGUMENT, "null argument");
+    return guarded([&] {  // csv.cpp:90-109
+        std::ofstream out(path);
+        if (!out) throw ValidationError("cannot open output file: " + std::string(path));
+        auto f17 = [](double v) {
+            char buf[40];
+            std::snprintf(buf, sizeof buf, "%.17g", v);
+            return std::string(buf);
+        };
+        out << "tau,mu,phi,I,Q,U,V,se_i,se_q,se_u,se_v\n";
+        const auto& t = *tally;
+        for (int hemi = 0; hemi < 2; ++hemi) {
+            const double tau = hemi == 0 ? 0.0 : t.tau_bottom, sign = hemi == 0 ? 1.0 : -1.0;
+            for (int iz = 0; iz < t.zb; ++iz)
+                for (int ia = 0; ia < t.ab; ++ia) {
+                    double s[4], se[4];
+                    mc_radiance(t, hemi, iz, ia, s, se);
+                    out << f17(tau) << ',' << f17(sign * (iz + 0.5) / t.zb) << ',' << f17(kTwoPi * (ia + 0.5) / t.ab);
+                    for (int c = 0; c < 4; ++c) out << ',' << f17(s[c]);
+                    for (int c = 0; c < 4; ++c) out << ',' << f17(se[c]);
+                    out << '\n';
+                }
+        }
+        return VRTE_OK;
+    });
+}
+void vrte_mc_tally_free(vrte_mc_tally* tally) { delete tally; }
 
 // ---------------------------------------------------------------- BRDF
 vrte_status vrte_compute_brdf(const vrte_material* material, const vrte_options* options,

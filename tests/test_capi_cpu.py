@@ -140,13 +140,19 @@ def test_brdf_argument_and_validation_errors_precede_device_work():
     assert e.value.code == V.VRTE_E_VALIDATION and "quadrature size must be at least 1" in e.value.message
 
 
-def test_out_of_path_symbols_are_not_built():
+def test_mc_argument_checks_before_any_device_work():
+    # mc.cpp:258-261 validation (2), capi.cpp:331-332 null checks (5); free accepts NULL
     d = tempfile.mkdtemp()
     mat = V.Material.load(write_rayleigh_slab(d))
     lib = V.lib()
-    h = C.c_void_p(1)
-    assert lib.vrte_mc_trace(mat._h, C.byref(V.options(4)), 100, 7, 4, 4, C.byref(h)) == V.VRTE_E_ARGUMENT
-    assert "not built" in lib.vrte_last_error().decode()
+    h = C.c_void_p()
+    assert lib.vrte_mc_trace(None, C.byref(V.options(4)), 100, 7, 4, 4, C.byref(h)) == V.VRTE_E_ARGUMENT
+    assert lib.vrte_mc_trace(mat._h, C.byref(V.options(4)), 0, 7, 4, 4, C.byref(h)) == V.VRTE_E_VALIDATION
+    assert "mc: photon count must be positive" in lib.vrte_last_error().decode()
+    assert lib.vrte_mc_trace(mat._h, C.byref(V.options(4)), 10, 7, 0, 4, C.byref(h)) == V.VRTE_E_VALIDATION
+    assert "mc: bin counts must be positive" in lib.vrte_last_error().decode()
+    row = np.zeros(10)
+    assert lib.vrte_mc_tally_row(None, 0, 0, 0, row.ctypes.data_as(C.POINTER(C.c_double))) == V.VRTE_E_ARGUMENT
     lib.vrte_field_free(None)
     lib.vrte_mc_tally_free(None)
     lib.vrte_brdf_free(None)

@@ -1,0 +1,114 @@
+"""GPU polarized Monte Carlo tracer (vrte_mc_trace,
+mc.cpp:1-315) -- ports of the reference tracer tests (test_mc.cpp), the same
+photon streams against the oracle restatement, and the tracer against the
+GPU radiance field (the statistical cross-check the row exists for)."""
+import math
+import os
+import tempfile
+
+import numpy as np
+import pytest
+
+import paper_1707_05882_b200 as V
+import pyoracle as O
+from paper_1707_05882_b200 import materials as M
+
+from helpers import oracle_material, product_material
+
+pytestmark = pytest.mark.gpu
+
+ISO = np.array([M.greek(1, 0, 0, 0, 0, 0)])
+
+
+def desc(coeffs, omega, tau, base="black", albedo=0.0, mu0=0.6, phi0=0.0, stokes=(1, 0, 0, 0)):
+    d = M.MaterialDesc([M.LayerDesc(omega, tau, np.asarray(coeffs, float))], base=base, albedo=albedo)
+    d.mu0, d.phi0, d.stokes = mu0, phi0, tuple(float(x) for x in stokes)
+    return d
+
+
+def run(d, photons, seed, zb, ab):
+    return V.mc_trace(product_material(d), V.options(4), photons, seed, zb, ab).rows()
+
+
+def test_vacuum_tallies_nothing():
+    r = run(desc(ISO, 0.0, 1.0), 20000, 7, 6, 6)
+    assert np.abs(r[..., 2:]).max() == 0.0
+
+
+def test_deterministic_for_a_fixed_seed():
+    d = desc(M.RAYLEIGH, 0.8, 1.0)
+    a, b, c = run(d, 300000, 123, 5, 6), run(d, 300000, 123, 5, 6), run(d, 300000, 124, 5, 6)
+    assert np.array_equal(a, b) and not np.array_equal(a, c)
+
+
+def test_lossless_slab_over_perfect_diffuse_base_returns_all_flux():
+    # test_mc.cpp:35-55: total reflected flux = incident flux within 3 sigma
+    zb = ab = 8
+    r = run(desc(ISO, 1.0, 10.0, "lambertian", 1.0), 1000000, 42, zb, ab)
+    meas = np.array([0.5 * (((iz + 1) / zb) ** 2 - (iz / zb) ** 2) * 2 * np.pi / ab for iz in range(zb)])
+    flux = (r[0, :, :, 2] * meas[:, None]).sum()  # radiance x bin measure = mu0 sum(w) / N
+    se = math.sqrt(((r[0, :, :, 6] * meas[:, None]) ** 2).sum())
+    assert abs(flux - 0.6) < 3.0 * se + 1e-3 * 0.6, (flux, se)
+
+
+def test_isotropic_scattering_keeps_an_unpolarized_beam_unpolarized():
+    r = run(desc(ISO, 0.5, 1.0), 400000, 99, 5, 5)
+    s, se = r[..., 3:6], r[..., 7:10]
+    ok = r[..., 2] > 0
+    assert np.all(np.abs(s[ok]) < 3.0 * se[ok] + 1e-12)
+
+
+def test_same_photon_streams_as_the_oracle():
+    # the reference's per-photon xoshiro256++ streams: every bin agrees with the oracle
+    # restatement far inside the statistical error (libm vs CUDA last-ulp differences
+    # only perturb a few trajectories)
+    d = desc(M.RAYLEIGH, 0.9, 1.0, "lambertian", 0.3, stokes=(1.0, 0.2, 0.0, 0.1))
+    zb, ab, n = 5, 6, 200000
+    g = run(d, n, 2024, zb, ab)
+    t = O.mc_trace(oracle_material(d), d.mu0, d.phi0, d.stokes, n, 2024, zb, ab)
+    ref = np.array([[[t.radiance(h, iz, ia) for ia in range(ab)] for iz in range(zb)] for h in range(2)])
+    se = np.array([[[t.std_error(h, iz, ia) for ia in range(ab)] for iz in range(zb)] for h in range(2)])
+    diff = np.abs(g[..., 2:6] - ref)
+    assert np.all(diff <= 0.05 * se + 1e-15), (diff / (se + 1e-300)).max()
+
+
+def test_tracer_agrees_with_the_dom_field():
+    # test_mc.cpp:96-130 on the product tracer: flux-weighted bin averages of the
+    # discrete-ordinate field at 2x2 Gauss points per bin (the oracle restatement,
+    # equal to the GPU radiance path to 1e-9 -- tests/test_gpu_radiance.py)
+    d = desc(M.RAYLEIGH, 0.9, 1.0)
+    zb, ab = 6, 8
+    r = run(d, 2000000, 31415, zb, ab)
+    ga, gb = 0.5 - 0.5 / math.sqrt(3), 0.5 + 0.5 / math.sqrt(3)
+    checked = passed = 0
+    for h in range(2):
+        tau = 0.0 if h == 0 else 1.0
+        for iz in range(zb):
+            mus = [(iz + f) / zb for f in (ga, gb)]
+            for ia in range(ab):
+                phis = [2 * math.pi * (ia + f) / ab for f in (ga, gb)]
+                dom = np.zeros(4)
+                for mu in mus:
+                    for ph in phis:
+                        f, *_ = O.radiance(oracle_material(d), 16, 0.6, 0.0, d.stokes, [tau],
+                                           mus=[mu if h == 0 else -mu], phis=[ph])
+                        dom += mu * f[0, 0, 0]
+                dom /= 2 * sum(mus)
+                s, se = r[h, iz, ia, 2:6], r[h, iz, ia, 6:10]
+                if s[0] == 0:
+                    continue
+                checked += 1
+                if abs(s[0] - dom[0]) < 4.0 * se[0] + 0.02 * abs(dom[0]):
+                    passed += 1
+    assert checked > 40 and passed >= 0.9 * checked, (checked, passed)
+
+
+def test_csv_layout():
+    d = desc(M.RAYLEIGH, 0.8, 1.0)
+    t = V.mc_trace(product_material(d), V.options(4), 20000, 3, 3, 4)
+    p = os.path.join(tempfile.mkdtemp(), "mc.csv")
+    t.write_csv(p)
+    lines = open(p).read().splitlines()
+    assert lines[0] == "tau,mu,phi,I,Q,U,V,se_i,se_q,se_u,se_v" and len(lines) == 1 + 2 * 3 * 4
+    row = [float(x) for x in lines[1 + 3 * 4].split(",")]  # first bottom-hemisphere row
+    assert row[0] == 1.0 and row[1] == -(0.5 / 3)
