@@ -375,6 +375,100 @@ def run_radiance(args):
     print(json.dumps(line), flush=True)
 
 
+def run_mc7(args):
+    """the reference's acceptance criterion 7 (acceptance_main.cpp:
+    316-400) on the GPU tracer -- 16 single-layer configs (isotropic/Rayleigh x omega
+    {0.5, 0.9} x tau {1, 10} x mu0 {0.6, 1}), 1e7 photons each, 8 x 8 bins per
+    hemisphere, every bin against the discrete-ordinate field (2 x 2 Gauss points,
+    flux weighted; 3 sigma).  value = photons/s through vrte_mc_trace."""
+    import math
+    import numpy as np
+    import torch
+    import paper_1707_05882_b200 as V
+    from paper_1707_05882_b200 import materials as M
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as O
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    os.environ["VRTE_DEVICE"] = str(local)
+    photons, zb, ab = 10_000_000, 8, 8
+    iso = np.array([M.greek(1, 0, 0, 0, 0, 0)])
+    cfgs = []
+    for ray in (False, True):
+        for om in (0.5, 0.9):
+            for t0 in (1.0, 10.0):
+                for mu0 in (0.6, 1.0):
+                    cfgs.append((ray, om, t0, mu0))
+    tmp = tempfile.mkdtemp(prefix="vrte_mc7_")
+    mats, descs = [], []
+    for k, (ray, om, t0, mu0) in enumerate(cfgs):
+        d = M.MaterialDesc([M.LayerDesc(om, t0, M.RAYLEIGH if ray else iso)])
+        d.mu0 = mu0
+        descs.append(d)
+        mats.append(V.Material.load(d.write(tmp, f"m{k}")))
+    V.mc_trace(mats[0], V.options(4), 100000, 1, zb, ab)  # warm-up
+    torch.cuda.synchronize()
+    t0w = time.perf_counter()
+    tallies = [V.mc_trace(m, V.options(4), photons, 1001 + k, zb, ab) for k, m in enumerate(mats)]
+    t = time.perf_counter() - t0w
+    rows = [tl.rows() for tl in tallies]
+    hits = [tl.hits() for tl in tallies]
+    # acceptance: every bin with >= 50 hits (hit counts are not exposed; use I > 0) vs the DOM field
+    g0, g1 = 0.5 - 0.5 / math.sqrt(3.0), 0.5 + 0.5 / math.sqrt(3.0)
+    total = passed = 0
+    worst = (1.0, "")
+    for (ray, om, t0_, mu0_), d, r, hc in zip(cfgs, descs, rows, hits):
+        c_tot = c_pass = 0
+        om_ = O.Material(np.array([d.layers[0].omega]), np.array([d.layers[0].tau]), d.padded_coeffs(), 0, 0.0, None)
+        for h in range(2):
+            tau = 0.0 if h == 0 else d.layers[0].tau
+            mus = [(iz + g) / zb for iz in range(zb) for g in (g0, g1)]
+            phis = [2 * math.pi * (ia + g) / ab for ia in range(ab) for g in (g0, g1)]
+            f, *_ = O.radiance(om_, 16, d.mu0, 0.0, [1, 0, 0, 0], [tau], mus=[m if h == 0 else -m for m in mus],
+                               phis=phis)
+            for iz in range(zb):
+                for ia in range(ab):
+                    s, se = r[h, iz, ia, 2:6], r[h, iz, ia, 6:10]
+                    if hc[h, iz, ia] < 50:  # acceptance_main.cpp:360
+                        continue
+                    dom = np.zeros(4)
+                    ws = 0.0
+                    for gm in range(2):
+                        for gp in range(2):
+                            mu = mus[2 * iz + gm]
+                            dom += mu * f[0, 2 * iz + gm, 2 * ia + gp]
+                            ws += mu
+                    dom /= ws
+                    ok = int(np.all(np.abs(s - dom) <= 3.0 * se + 1e-9))
+                    total += 1
+                    passed += ok
+                    c_tot += 1
+                    c_pass += ok
+        frac = c_pass / c_tot if c_tot else 1.0
+        if frac < worst[0]:
+            worst = (frac, f"{'rayleigh' if ray else 'isotropic'} omega={om} tau0={t0_} mu0={mu0_}")
+    line = {"metric": "Monte Carlo photons/s (acceptance 7: 16 configs x 1e7 photons)", "value": 16 * photons / t,
+            "unit": "photons/s", "n_gpus": 1, "steps": 1, "warmup": 1, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (acceptance_main.cpp:316-400 configs)",
+            "config": {"workload": "MC7: reference acceptance criterion 7 on vrte_mc_trace", "photons": photons,
+                       "configs": 16, "bins": [zb, ab]},
+            "acceptance_bins_within_3sigma": [passed, total],
+            "acceptance_worst_config": {"fraction": worst[0], "config": worst[1], "pass_threshold": 0.95},
+            "reference_acceptance_7_seconds": 432.41}
+    if not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        d = descs[-1]
+        om_ = O.Material(np.array([d.layers[0].omega]), np.array([d.layers[0].tau]), d.padded_coeffs(), 0, 0.0, None)
+        n_s = 400_000
+        t1 = time.perf_counter()
+        O.mc_trace(om_, d.mu0, 0.0, [1, 0, 0, 0], n_s, 1016, zb, ab, threads=threads)
+        tc = time.perf_counter() - t1
+        line["cpu_baseline"] = {"value": n_s / tc, "unit": "photons/s", "cores": threads, "kind": "port",
+                                "sample": f"oracle tracer, {n_s} photons of the last config (rayleigh w=0.9 tau=10 mu0=1)"}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -383,6 +477,8 @@ def main():
         return run_c5(args)
     if args.config == "R3":
         return run_radiance(args)
+    if args.config == "MC7":
+        return run_mc7(args)
     import numpy as np
     import torch
     import paper_1707_05882_b200 as V

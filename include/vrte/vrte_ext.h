@@ -50,6 +50,11 @@ VRTE_API vrte_status vrte_compute_brdf_batch(const vrte_material* const* materia
                                              size_t n_mu_in, int32_t n_dphi, const double* basis,
                                              int32_t concurrency, vrte_brdf** out);
 
+/* Photon count of one tally bin (mc.hpp TallyGrid::hits; the reference keeps it
+ * internal, its acceptance test skips bins with < 50 hits). */
+VRTE_API vrte_status vrte_mc_tally_hits(const vrte_mc_tally* tally, int32_t hemisphere, int32_t zenith_bin,
+                                        int32_t azimuth_bin, uint64_t* hits);
+
 #ifdef __cplusplus
 }
 #endif

@@ -131,7 +131,7 @@ EXPORTED = [
     "vrte_mc_tally_write_csv", "vrte_mc_tally_free",
     # vrte_ext.h
     "vrte_brdf_device_stats_get", "vrte_brdf_plan_create", "vrte_brdf_from_stacks",
-    "vrte_compute_brdf_batch",
+    "vrte_compute_brdf_batch", "vrte_mc_tally_hits",
     # vrte_cuda.h
     "vrte_cuda_brdf", "vrte_cuda_plan_create", "vrte_cuda_plan_run", "vrte_cuda_plan_fetch",
     "vrte_cuda_plan_fetch_up", "vrte_cuda_plan_fetch_modes", "vrte_cuda_plan_fetch_ef",
@@ -195,6 +195,7 @@ def lib():
     L.vrte_mc_tally_row.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, dp]
     L.vrte_mc_tally_write_csv.argtypes = [vp, C.c_char_p]
     L.vrte_mc_tally_free.argtypes = [vp]
+    L.vrte_mc_tally_hits.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_uint64)]
     _lib = L
     return L
 
@@ -444,6 +445,17 @@ class McTally:
 
     def rows(self) -> np.ndarray:
         return np.array([[[self.row(h, iz, ia) for ia in range(self.ab)] for iz in range(self.zb)] for h in (0, 1)])
+
+    def hits(self) -> np.ndarray:
+        """[2, zb, ab] photon counts (vrte_mc_tally_hits, vrte_ext.h)"""
+        out = np.zeros((2, self.zb, self.ab), dtype=np.int64)
+        v = C.c_uint64()
+        for h in (0, 1):
+            for iz in range(self.zb):
+                for ia in range(self.ab):
+                    _check(lib().vrte_mc_tally_hits(self._h, h, iz, ia, C.byref(v)))
+                    out[h, iz, ia] = v.value
+        return out
 
     def write_csv(self, path: str):
         _check(lib().vrte_mc_tally_write_csv(self._h, path.encode()))

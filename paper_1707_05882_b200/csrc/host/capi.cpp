@@ -600,6 +600,17 @@ vrte_status vrte_mc_tally_write_csv(const vrte_mc_tally* tally, const char* path
 }
 void vrte_mc_tally_free(vrte_mc_tally* tally) { delete tally; }
 
+vrte_status vrte_mc_tally_hits(const vrte_mc_tally* tally, int32_t hemisphere, int32_t zenith_bin,
+                               int32_t azimuth_bin, uint64_t* hits) {
+    if (!tally || !hits) return set_error(VRTE_E_ARGUMENT, "null argument");
+    const auto& t = *tally;
+    if (hemisphere < 0 || hemisphere > 1 || zenith_bin < 0 || zenith_bin >= t.zb || azimuth_bin < 0 ||
+        azimuth_bin >= t.ab)
+        return set_error(VRTE_E_ARGUMENT, "tally index out of range");
+    *hits = t.hits[((size_t)hemisphere * t.zb + zenith_bin) * t.ab + azimuth_bin];
+    return VRTE_OK;
+}
+
 // ---------------------------------------------------------------- BRDF
 vrte_status vrte_compute_brdf(const vrte_material* material, const vrte_options* options,
                               const double* mu_in, size_t n_mu_in, int32_t n_dphi,
