@@ -111,6 +111,11 @@ typedef struct vrte_cuda_mc {
 VRTE_API int32_t vrte_cuda_mc_trace(const vrte_cuda_mc* mc, double* sum, double* sum_sq, uint64_t* hits,
                                     vrte_cuda_result* result);
 
+/* Recycled page-locked host buffers (per-size free list) for result tables;
+ * falls back to the heap when pinning is unavailable. */
+VRTE_API void* vrte_cuda_host_alloc(size_t bytes);
+VRTE_API void vrte_cuda_host_free(void* p, size_t bytes);
+
 /* Full solve: host inputs -> host table [n_in][N][n_dphi][16]. */
 VRTE_API int32_t vrte_cuda_brdf(const vrte_cuda_problem* problem, double* table,
                                 vrte_cuda_result* result);

@@ -137,7 +137,7 @@ EXPORTED = [
     "vrte_cuda_plan_fetch_up", "vrte_cuda_plan_fetch_modes", "vrte_cuda_plan_fetch_ef",
     "vrte_cuda_plan_destroy",
     "vrte_cuda_synthesize", "vrte_cuda_device_count", "vrte_cuda_lu_solve", "vrte_cuda_hessenberg", "vrte_cuda_schur",
-    "vrte_cuda_radiance_field", "vrte_cuda_mc_trace",
+    "vrte_cuda_radiance_field", "vrte_cuda_mc_trace", "vrte_cuda_host_alloc", "vrte_cuda_host_free",
 ]
 
 

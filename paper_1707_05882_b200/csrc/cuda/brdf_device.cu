@@ -731,7 +731,52 @@ struct PlanLease {
 };
 }  // namespace
 
+namespace {
+std::mutex g_host_mu;
+std::vector<std::pair<size_t, void*>> g_host_free;  // (bytes, pinned block)
+std::vector<void*> g_heap_blocks;                    // blocks that fell back to the heap
+}  // namespace
+
 extern "C" {
+
+void* vrte_cuda_host_alloc(size_t bytes) {
+    if (bytes == 0) bytes = 8;
+    {
+        std::lock_guard<std::mutex> lk(g_host_mu);
+        for (size_t i = g_host_free.size(); i-- > 0;)
+            if (g_host_free[i].first == bytes) {
+                void* p = g_host_free[i].second;
+                g_host_free.erase(g_host_free.begin() + i);
+                return p;
+            }
+    }
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();  // clear; no device: plain heap memory
+        p = std::malloc(bytes);
+        if (!p) throw std::bad_alloc();
+        std::lock_guard<std::mutex> lk(g_host_mu);
+        g_heap_blocks.push_back(p);
+    }
+    return p;
+}
+
+void vrte_cuda_host_free(void* p, size_t bytes) {
+    if (!p) return;
+    if (bytes == 0) bytes = 8;
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    for (size_t i = 0; i < g_heap_blocks.size(); ++i)
+        if (g_heap_blocks[i] == p) {
+            g_heap_blocks.erase(g_heap_blocks.begin() + i);
+            std::free(p);
+            return;
+        }
+    if (g_host_free.size() >= 64) {  // bound the cache
+        cudaFreeHost(g_host_free.front().second);
+        g_host_free.erase(g_host_free.begin());
+    }
+    g_host_free.emplace_back(bytes, p);
+}
 
 int32_t vrte_cuda_device_count(void) {
     int n = 0;

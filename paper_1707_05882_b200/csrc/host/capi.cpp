@@ -629,7 +629,7 @@ vrte_status vrte_compute_brdf(const vrte_material* material, const vrte_options*
         t.quadrature_n = N;
         t.order_count = s.L;
         t.material_hash = material_hash(s.spec);
-        t.entries.assign(n_mu_in * (size_t)N * np * 16, 0.0);
+        t.entries.resize(n_mu_in * (size_t)N * np * 16);  // overwritten by the device result
         vrte_cuda_result r{};
         const int32_t rc = vrte_cuda_brdf(&s.prob, t.entries.data(), &r);
         if (rc == 5) throw std::invalid_argument(r.message);
@@ -805,7 +805,7 @@ vrte_status vrte_brdf_from_stacks(const vrte_material* material, const vrte_opti
         t.quadrature_n = N;
         t.order_count = s.L;
         t.material_hash = material_hash(s.spec);
-        t.entries.assign(n_mu_in * (size_t)N * np * 16, 0.0);
+        t.entries.resize(n_mu_in * (size_t)N * np * 16);
         vrte_cuda_result r{};
         const int32_t rc = vrte_cuda_synthesize(&s.prob, up_all_orders, t.entries.data(), &r);
         if (rc == 5) throw std::invalid_argument(r.message);

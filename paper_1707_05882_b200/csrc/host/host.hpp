@@ -3,7 +3,10 @@
 // (core/types.*, core/material.*, brdf/brdf.hpp) without Eigen.
 #pragma once
 
+#include "vrte/vrte_cuda.h"
 #include <array>
+#include <new>
+#include <utility>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -67,9 +70,35 @@ double reduce_azimuth(double phi);
 Mat4 base_row_at(const BaseReflector& base, const Quadrature& quad, double mu_out, double mu_in);
 uint64_t material_hash(const MaterialSpec& spec);  // brdf.cpp:11-41
 
+// Page-locked, recycled host storage for the BRDF table: the device result lands
+// by DMA at full PCIe/C2C speed, and elements are default-initialized (no
+// zero-fill pass over 10 MB before the copy overwrites it).  vrte_cuda_host_*
+// (brdf_device.cu) keep a per-size free list; plain heap memory if pinning fails.
+template <typename T>
+struct PinnedAlloc {
+    using value_type = T;
+    PinnedAlloc() = default;
+    template <typename U>
+    PinnedAlloc(const PinnedAlloc<U>&) {}
+    T* allocate(size_t n) { return static_cast<T*>(vrte_cuda_host_alloc(n * sizeof(T))); }
+    void deallocate(T* p, size_t n) { vrte_cuda_host_free(p, n * sizeof(T)); }
+    template <typename U>
+    void construct(U* p) {
+        ::new (static_cast<void*>(p)) U;  // default-init
+    }
+    template <typename U, typename... A>
+    void construct(U* p, A&&... a) {
+        ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+    }
+    template <typename U>
+    bool operator==(const PinnedAlloc<U>&) const { return true; }
+    template <typename U>
+    bool operator!=(const PinnedAlloc<U>&) const { return false; }
+};
+
 struct BrdfTable {  // brdf.hpp:9-24
     std::vector<double> mu_in, mu_out, dphi;
-    std::vector<double> entries;  // [in][out][dphi][16] row-major Mueller
+    std::vector<double, PinnedAlloc<double>> entries;  // [in][out][dphi][16] row-major Mueller
     int quadrature_n = 0, order_count = 0;
     uint64_t material_hash = 0;
 };
