@@ -51,7 +51,7 @@ __device__ inline void dmma(double& c0, double& c1, double a, double b) {
 
 // CTA tile BM x BN with NT = 2 BN threads: warps laid out (BM/32) x (BN/32),
 // each a 32 x 32 tile of 4 x 4 DMMA fragments.
-template <bool TA, bool TB, int BK, int ST, int MINB, int BN>
+template <bool TA, bool TB, int BK, int ST, int MINB, int BN, bool MAP>
 __global__ void __launch_bounds__(2 * BN, MINB) dmma_gemm_kernel(GemmBatch g) {
     constexpr int NT = 2 * BN, WN = BN / 32;
     using Gm = Geo<BK, BN>;
@@ -70,9 +70,11 @@ __global__ void __launch_bounds__(2 * BN, MINB) dmma_gemm_kernel(GemmBatch g) {
     const int gq = lane >> 2, tq = lane & 3;                 // fragment coordinates
     // optional index maps (lazily pivoted LU, lu.cu): the k index of A, the n
     // index of B and the n index of C go through per-batch tables
-    __shared__ int s_amap[kMaxMapK], s_bmap[BN], s_cmap[BN];
-    const bool amapped = g.amap != nullptr, bmapped = g.bmap != nullptr, cmapped = g.cmap != nullptr;
-    if (amapped || bmapped || cmapped) {
+    // (MAP = false: the plain kernel, no map state in registers)
+    __shared__ int s_amap[MAP ? kMaxMapK : 1], s_bmap[MAP ? BN : 1], s_cmap[MAP ? BN : 1];
+    const bool amapped = MAP && g.amap != nullptr, bmapped = MAP && g.bmap != nullptr,
+               cmapped = MAP && g.cmap != nullptr;
+    if (MAP) {
         const long long mo = (long long)bz * g.map_stride;
         if (amapped)
             for (int i = t; i < g.k; i += NT) s_amap[i] = g.amap[mo + i];
@@ -84,6 +86,15 @@ __global__ void __launch_bounds__(2 * BN, MINB) dmma_gemm_kernel(GemmBatch g) {
         __syncthreads();
     }
 
+    // mapped B rows: the per-thread row offsets are fixed over the k loop
+    long long boff[MAP && !TB ? (BK * BN) / NT : 1];
+    if (MAP && !TB) {
+#pragma unroll
+        for (int q = 0; q < (MAP && !TB ? (BK * BN) / NT : 1); ++q) {
+            const int n = (t + q * NT) / BK;
+            boff[q] = (long long)(bmapped ? s_bmap[n] : n0 + n) * g.ldb;
+        }
+    }
     auto load_stage = [&](int stage, int k0) {
         double* As = As0 + stage * A_STAGE;
         double* Bs = Bs0 + stage * B_STAGE;
@@ -111,7 +122,7 @@ __global__ void __launch_bounds__(2 * BN, MINB) dmma_gemm_kernel(GemmBatch g) {
                 const int k = e % BK, n = e / BK;
                 const int gn = n0 + n, gk = k0 + k;
                 const bool ok = gn < g.n && gk < g.k;
-                cp_async8(Bs + n * LDB_N + k, ok ? B + gk + (long long)(bmapped ? s_bmap[n] : gn) * g.ldb : B, ok);
+                cp_async8(Bs + n * LDB_N + k, ok ? B + gk + (MAP ? boff[q] : (long long)gn * g.ldb) : B, ok);
             } else {    // contiguous along n: Bs[k][n]
                 const int n = e % BN, k = e / BN;
                 const int gn = n0 + n, gk = k0 + k;
@@ -202,24 +213,26 @@ __global__ void __launch_bounds__(2 * BN, MINB) dmma_gemm_kernel(GemmBatch g) {
         }
 }
 
-template <bool TA, bool TB, int BK, int ST, int MINB, int BN>
+template <bool TA, bool TB, int BK, int ST, int MINB, int BN, bool MAP = false>
 void launch(const GemmBatch& g, cudaStream_t stream) {
     static bool attr = false;
     constexpr size_t smem = (size_t)ST * (Geo<BK, BN>::A_STAGE + Geo<BK, BN>::B_STAGE) * sizeof(double);
     if (!attr) {
-        VRTE_CUDA_CHECK(cudaFuncSetAttribute(dmma_gemm_kernel<TA, TB, BK, ST, MINB, BN>,
+        VRTE_CUDA_CHECK(cudaFuncSetAttribute(dmma_gemm_kernel<TA, TB, BK, ST, MINB, BN, MAP>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        VRTE_CUDA_CHECK(cudaFuncSetAttribute(dmma_gemm_kernel<TA, TB, BK, ST, MINB, BN>,
+        VRTE_CUDA_CHECK(cudaFuncSetAttribute(dmma_gemm_kernel<TA, TB, BK, ST, MINB, BN, MAP>,
                                              cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         attr = true;
     }
     dim3 grid((g.m + BM - 1) / BM, (g.n + BN - 1) / BN, g.batch);
-    dmma_gemm_kernel<TA, TB, BK, ST, MINB, BN><<<grid, 2 * BN, smem, stream>>>(g);
+    dmma_gemm_kernel<TA, TB, BK, ST, MINB, BN, MAP><<<grid, 2 * BN, smem, stream>>>(g);
 }
 
 template <int BK, int ST, int MINB, int BN = 128>
 void launch_cfg(const GemmBatch& g, cudaStream_t stream) {
-    if (!g.trans_a && !g.trans_b)
+    if (!g.trans_a && !g.trans_b && (g.amap || g.bmap || g.cmap))
+        launch<false, false, BK, ST, MINB, BN, true>(g, stream);
+    else if (!g.trans_a && !g.trans_b)
         launch<false, false, BK, ST, MINB, BN>(g, stream);
     else if (g.trans_a && !g.trans_b)
         launch<true, false, BK, ST, MINB, BN>(g, stream);
@@ -249,8 +262,9 @@ void gemm_batched_cfg(const GemmBatch& g, cudaStream_t stream, int bk, int stage
 void gemm_batched(const GemmBatch& g, cudaStream_t stream) {
     if ((g.amap && (g.trans_a || g.k > kMaxMapK)) || (g.bmap && g.trans_b))
         throw std::invalid_argument("gemm_batched: index maps need untransposed operands and k <= 256");
+    const bool mapped = g.amap || g.bmap || g.cmap;
     if (g.k <= 96)
-        gemm_batched_cfg(g, stream, 16, 2, 3);
+        gemm_batched_cfg(g, stream, 16, 2, mapped ? 2 : 3);  // the mapped kernel needs the register budget
     else
         gemm_batched_cfg(g, stream, 16, 3, 2);
 }
