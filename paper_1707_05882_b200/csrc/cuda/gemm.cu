@@ -13,6 +13,7 @@
 // The epilogue stores the accumulator fragments directly; for the beta = 1
 // trailing updates C is preloaded into the accumulators (overlapping the first
 // operand tile) instead of being re-read in the epilogue.
+#include <cstdlib>
 #include <stdexcept>
 
 #include "common.cuh"
@@ -263,8 +264,9 @@ void gemm_batched(const GemmBatch& g, cudaStream_t stream) {
     if ((g.amap && (g.trans_a || g.k > kMaxMapK)) || (g.bmap && g.trans_b))
         throw std::invalid_argument("gemm_batched: index maps need untransposed operands and k <= 256");
     const bool mapped = g.amap || g.bmap || g.cmap;
+    static const int small_minb = std::getenv("VRTE_GEMM_SMALL_MINB") ? std::atoi(std::getenv("VRTE_GEMM_SMALL_MINB")) : 3;
     if (g.k <= 96)
-        gemm_batched_cfg(g, stream, 16, 2, mapped ? 2 : 3);  // the mapped kernel needs the register budget
+        gemm_batched_cfg(g, stream, 16, 2, mapped ? 2 : small_minb);  // the mapped kernel needs the register budget
     else
         gemm_batched_cfg(g, stream, 16, 3, 2);
 }
