@@ -112,3 +112,22 @@ def test_csv_layout():
     assert lines[0] == "tau,mu,phi,I,Q,U,V,se_i,se_q,se_u,se_v" and len(lines) == 1 + 2 * 3 * 4
     row = [float(x) for x in lines[1 + 3 * 4].split(",")]  # first bottom-hemisphere row
     assert row[0] == 1.0 and row[1] == -(0.5 / 3)
+
+
+def test_mueller_table_base_matches_the_oracle_tracer():
+    # the table base branch (mc.cpp:166-180) on the same photon streams
+    N = 6
+    nodes, _ = O.quadrature(N)
+    tab = np.zeros((N, N, 4, 4))
+    for i, a in enumerate(nodes):
+        for j, b in enumerate(nodes):
+            tab[i, j] = 0.4 * (1 + 0.2 * (a - b)) * np.array([[1, 0.1, 0, 0], [0.1, 0.6, 0, 0],
+                                                              [0, 0, 0.4, 0.05], [0, 0, -0.05, 0.4]])
+    d = desc(M.RAYLEIGH, 0.7, 0.8, "mueller_table", stokes=(1.0, 0.1, 0.0, 0.0))
+    d.table = tab
+    zb, ab, n = 4, 5, 200000
+    g = run(d, n, 77, zb, ab)
+    t = O.mc_trace(oracle_material(d), d.mu0, d.phi0, d.stokes, n, 77, zb, ab)
+    ref = np.array([[[t.radiance(h, iz, ia) for ia in range(ab)] for iz in range(zb)] for h in range(2)])
+    se = np.array([[[t.std_error(h, iz, ia) for ia in range(ab)] for iz in range(zb)] for h in range(2)])
+    assert np.all(np.abs(g[..., 2:6] - ref) <= 0.05 * se + 1e-15)

@@ -106,3 +106,13 @@ def test_mueller_table_base_brdf_and_radiance_match_oracle():
     f, (t, mus, phis, gf), (omu, ophi, rf, orefl) = run_pair(d, N, [0.0, 0.7, 1.5], zen=5, azi=6)
     assert np.abs(gf - rf).max() < 1e-9 * np.abs(rf).max()
     assert np.allclose(f.reflectance(), orefl, rtol=1e-10, atol=1e-13)
+
+
+def test_degenerate_grids_and_many_depths():
+    # out_zenith = 1 -> mu = {1, -1}; out_azimuth = 1 -> phi = {phi0} (pipeline.cpp:358-390);
+    # depths outside [0, tau_total] clamp into the stack (reconstruction.cpp:12-19)
+    d, N = CASES["two_layer"]
+    taus = [-0.5, 0.0, 0.2, 1.0, 1.0000001, 1.3, 1.5, 9.0]
+    f, (t, mus, phis, g), (omu, ophi, r, orefl) = run_pair(d, N, taus, zen=1, azi=1)
+    assert list(mus) == [1.0, -1.0] and len(phis) == 1
+    assert np.abs(g - r).max() < 1e-9 * np.abs(r).max()
