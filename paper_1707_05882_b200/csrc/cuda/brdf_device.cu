@@ -128,6 +128,8 @@ struct vrte_cuda_plan {
     DeviceStatus* status = nullptr;  // pinned host-mapped would be nicer; device + copy
     DevBuf<DeviceStatus> status_buf;
     cudaEvent_t ev[16] = {};
+    cudaStream_t st2 = nullptr;          // side stream: independent work overlapped with the main chain
+    cudaEvent_t fork[4] = {}, join[4] = {};
     int refine_iters = 1;
     int refine_extra = 2;
     int part_refine_iters = 1;
@@ -138,6 +140,10 @@ struct vrte_cuda_plan {
         if (resmax_host) cudaFreeHost(resmax_host);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
+        for (auto* es : {fork, join})
+            for (int i = 0; i < 4; ++i)
+                if (es[i]) cudaEventDestroy(es[i]);
+        if (st2) cudaStreamDestroy(st2);
         if (st) cudaStreamDestroy(st);
     }
 };
@@ -167,6 +173,10 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     if (!pl.st) VRTE_CUDA_CHECK(cudaStreamCreateWithFlags(&pl.st, cudaStreamNonBlocking));
     for (auto& e : pl.ev)
         if (!e) VRTE_CUDA_CHECK(cudaEventCreate(&e));
+    if (!pl.st2) VRTE_CUDA_CHECK(cudaStreamCreateWithFlags(&pl.st2, cudaStreamNonBlocking));
+    for (auto* es : {pl.fork, pl.join})
+        for (int i = 0; i < 4; ++i)
+            if (!es[i]) VRTE_CUDA_CHECK(cudaEventCreateWithFlags(&es[i], cudaEventDisableTiming));
     if (const char* ri = std::getenv("VRTE_REFINE_ITERS")) pl.refine_iters = std::atoi(ri);
     if (const char* pi = std::getenv("VRTE_PART_REFINE_ITERS")) pl.part_refine_iters = std::atoi(pi);
     if (const char* re = std::getenv("VRTE_REFINE_EXTRA")) pl.refine_extra = std::atoi(re);
@@ -313,6 +323,13 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     // ---------------- homogeneous
     launch_gsf(pd, pl.nodes.p, N, 1.0, pl.gsf_n.p, st);
     launch_gsf(pd, pl.mu_in.p, pl.n_in, -1.0, pl.gsf_b.p, st);
+    // the beam source terms (particular.cpp:7-25) need only the GSF tables: side stream,
+    // overlapped with the homogeneous stage
+    cudaStream_t st2 = pl.st2;
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.fork[0], st));
+    VRTE_CUDA_CHECK(cudaStreamWaitEvent(st2, pl.fork[0], 0));
+    launch_beam_source(pd, pl.gsf_n.p, pl.gsf_b.p, pl.sp.p, pl.sm.p, st2);
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.join[0], st2));
     launch_build_ef(pd, pl.gsf_n.p, pl.E.p, pl.F.p, st);
     gemm_batched(gemm(d, d, d, pl.F.p, d, dd, false, pl.E.p, d, dd, false, pl.T.p, d, dd, B), st);
     launch_max_abs(pl.T.p, dd, B, pl.femax.p, st);
@@ -347,11 +364,17 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
         // (two GEMMs + an independent 1x1/2x2 solve per entry).
         // The column-major V read row-major is V^T: factor V^T, solve V^T Y = I
         // row-major, and Y read column-major is V^-1.
+        // Side stream: overlapped with E X, the mode recovery and the refinement set-up
+        // (they touch neither Vlu = hwork, tmp2, Vinv nor the V pivots); joined before
+        // the first eigenbasis solve.
         double* Vlu = pl.hwork.p;  // Hessenberg work is free again
-        VRTE_CUDA_CHECK(cudaMemcpyAsync(Vlu, pl.X.p, sizeof(double) * B * dd, cudaMemcpyDeviceToDevice, st));
-        launch_set_identity(pl.tmp2.p, d, B, st);
-        lu_factor_rm(Vlu, d, B, pl.ipivV.p, pl.permV.p, pl.status, pl.order_index.p, st);
-        lu_solve_rm(Vlu, d, B, pl.permV.p, pl.tmp2.p, pl.Vinv.p, d, st);
+        VRTE_CUDA_CHECK(cudaEventRecord(pl.fork[1], st));
+        VRTE_CUDA_CHECK(cudaStreamWaitEvent(st2, pl.fork[1], 0));
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(Vlu, pl.X.p, sizeof(double) * B * dd, cudaMemcpyDeviceToDevice, st2));
+        launch_set_identity(pl.tmp2.p, d, B, st2);
+        lu_factor_rm(Vlu, d, B, pl.ipivV.p, pl.permV.p, pl.status, pl.order_index.p, st2);
+        lu_solve_rm(Vlu, d, B, pl.permV.p, pl.tmp2.p, pl.Vinv.p, d, st2);
+        VRTE_CUDA_CHECK(cudaEventRecord(pl.join[1], st2));
         nl += 1 + lu_rm_launch_count(d);
     }
     gemm_batched(gemm(d, d, d, pl.E.p, d, dd, false, pl.X.p, d, dd, false, pl.tmp3.p, d, dd, B), st);
@@ -454,6 +477,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
         launch_residual(ra, st);
         nl += 6;
     };
+    if (!pl.schur_solves) VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[1], 0));  // V^-1 (side stream)
     for (int it = 0; it < pl.refine_iters; ++it) refine_iteration();
     final_residual();
     // Adaptive: one Newton step normally brings every mode below 1e-11 (the
@@ -471,7 +495,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[10], st));
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[1], st));
     // ---------------- particular
-    launch_beam_source(pd, pl.gsf_n.p, pl.gsf_b.p, pl.sp.p, pl.sm.p, st);
+    VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[0], 0));  // beam source (side stream)
     PartArgs pa{};
     pa.d = d;
     pa.batch = B;
