@@ -870,7 +870,7 @@ __global__ void __launch_bounds__(256) hqr_window_kernel(double* Hall, double* Z
 // CTA.  Small active blocks and exceptional-shift sweeps use one bulge with
 // the dlahqr shift / start rules (identical to hqr_window_kernel).
 constexpr int MB_MAX = 4;   // bulges per sweep
-constexpr int MS = 16;      // chase steps per chunk
+constexpr int MS = 19;      // chase steps per chunk with MB_MAX bulges (MW - 3 (nb - 1) - 4 for nb)
 constexpr int MW = 32;      // window (>= MS + 3 (MB_MAX - 1) + 4)
 constexpr int LDW = MW + 1; // leading dimension of the window: row sweeps (lanes over
                             // columns) hit distinct shared-memory banks
@@ -1742,9 +1742,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) hqr_multi_ke
             // (chasers arrive, updaters wait), 2 = rest of U_c done (updaters
             // arrive, chasers wait before touching columns it covers), 3 = chaser
             // group, 4 = chase steps.  U is double buffered.
-            const int nchunk = (S_total + MS - 1) / MS;
+            // chunk length: as many steps as the MW window holds for this bulge count
+            const int ms = MW - 3 * (nb - 1) - 4;
+            const int nchunk = (S_total + ms - 1) / ms;
             auto geom = [&](int c, int& wlo, int& whi) {
-                const int s0 = c * MS, s1 = min(s0 + MS, S_total);
+                const int s0 = c * ms, s1 = min(s0 + ms, S_total);
                 const int kmin = max(M, M + s0 - 3 * (nb - 1));
                 const int kmax = min(I - 1, M + s1 - 1);
                 wlo = (kmin > M) ? kmin - 1 : M;
@@ -1753,7 +1755,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) hqr_multi_ke
             if (warp < 4) {
                 const int tg = t;  // 0..127
                 for (int c = 0; c < nchunk; ++c) {
-                    const int s0 = c * MS, s1 = min(s0 + MS, S_total);
+                    const int s0 = c * ms, s1 = min(s0 + ms, S_total);
                     int wlo, whi;
                     geom(c, wlo, whi);
                     const int nw = whi - wlo + 1;
