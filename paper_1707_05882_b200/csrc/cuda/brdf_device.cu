@@ -364,16 +364,17 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
         // (two GEMMs + an independent 1x1/2x2 solve per entry).
         // The column-major V read row-major is V^T: factor V^T, solve V^T Y = I
         // row-major, and Y read column-major is V^-1.
-        // Side stream: overlapped with E X, the mode recovery and the refinement set-up
-        // (they touch neither Vlu = hwork, tmp2, Vinv nor the V pivots); joined before
-        // the first eigenbasis solve.
+        // Side stream: overlapped with E X, the mode recovery and the first refinement
+        // GEMMs (they touch neither the Hessenberg work (Vlu, identity), Vinv nor the V
+        // pivots); joined at the first eigenbasis solve.
         double* Vlu = pl.hwork.p;  // Hessenberg work is free again
         VRTE_CUDA_CHECK(cudaEventRecord(pl.fork[1], st));
         VRTE_CUDA_CHECK(cudaStreamWaitEvent(st2, pl.fork[1], 0));
         VRTE_CUDA_CHECK(cudaMemcpyAsync(Vlu, pl.X.p, sizeof(double) * B * dd, cudaMemcpyDeviceToDevice, st2));
-        launch_set_identity(pl.tmp2.p, d, B, st2);
+        double* Ident = pl.hwork.p + (size_t)B * dd;  // second half of the Hessenberg work (>= 2 d^2 per slot)
+        launch_set_identity(Ident, d, B, st2);
         lu_factor_rm(Vlu, d, B, pl.ipivV.p, pl.permV.p, pl.status, pl.order_index.p, st2);
-        lu_solve_rm(Vlu, d, B, pl.permV.p, pl.tmp2.p, pl.Vinv.p, d, st2);
+        lu_solve_rm(Vlu, d, B, pl.permV.p, Ident, pl.Vinv.p, d, st2);
         VRTE_CUDA_CHECK(cudaEventRecord(pl.join[1], st2));
         nl += 1 + lu_rm_launch_count(d);
     }
@@ -399,8 +400,13 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     launch_modes(ma, st);
     // (F E - sigma_c) y_c = r_c for `ncol` columns in place of W = R (ld d):
     // eigenbasis (default) or Schur form.  `out` = Q y (+ beta out).
+    bool vinv_joined = pl.schur_solves;
     auto shifted_solve = [&](const double* Rm, double* Wm, int ncol, long long wst, const double* sig,
                              const int* knd, double* out, double beta) {
+        if (!vinv_joined) {  // V^-1 comes from the side stream: join at its first use
+            VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[1], 0));
+            vinv_joined = true;
+        }
         const double* Lm = pl.schur_solves ? pl.Z.p : pl.Vinv.p;
         gemm_batched(gemm(d, ncol, d, Lm, d, dd, pl.schur_solves, Rm, d, wst, false, Wm, d, wst, B), st);
         if (pl.schur_solves)
@@ -477,7 +483,6 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
         launch_residual(ra, st);
         nl += 6;
     };
-    if (!pl.schur_solves) VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[1], 0));  // V^-1 (side stream)
     for (int it = 0; it < pl.refine_iters; ++it) refine_iteration();
     final_residual();
     // Adaptive: one Newton step normally brings every mode below 1e-11 (the
