@@ -115,7 +115,7 @@ struct vrte_cuda_plan {
     DevBuf<double> X, AL, BE, FB, W2, UT, EU, hwork, Vinv;
     DevBuf<int> ipivV, permV;
     bool schur_solves = false;  // VRTE_SOLVE=schur: quasi-triangular solves on the Schur form
-    DevBuf<double> wr, wi, femax, nu, lam, residual, rho, sigma_m, rshift;
+    DevBuf<double> wr, wi, femax, nu, nu0, lam, residual, rho, sigma_m, rshift;
     DevBuf<int> flags, kind_m, sidx;
     // particular
     DevBuf<double> sp, sm, fsp, rhs, W, g, eg, feg, zp, zm, mu_eff, sigma;
@@ -266,6 +266,7 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pl.wi.alloc((size_t)B * d);
     pl.femax.alloc(B);
     pl.nu.alloc((size_t)B * d * 2);
+    pl.nu0.alloc((size_t)B * d * 2);
     pl.lam.alloc((size_t)B * d * 2);
     pl.residual.alloc((size_t)B * d);
     pl.flags.alloc((size_t)B * d);
@@ -402,25 +403,77 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     // eigenbasis (default) or Schur form.  `out` = Q y (+ beta out).
     bool vinv_joined = pl.schur_solves;
     auto shifted_solve = [&](const double* Rm, double* Wm, int ncol, long long wst, const double* sig,
-                             const int* knd, double* out, double beta) {
-        if (!vinv_joined) {  // V^-1 comes from the side stream: join at its first use
+                             const int* knd, double* out, double beta, cudaStream_t ss) {
+        if (ss == st && !vinv_joined) {  // V^-1 comes from the side stream: join at its first use
             VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[1], 0));
             vinv_joined = true;
         }
         const double* Lm = pl.schur_solves ? pl.Z.p : pl.Vinv.p;
-        gemm_batched(gemm(d, ncol, d, Lm, d, dd, pl.schur_solves, Rm, d, wst, false, Wm, d, wst, B), st);
+        gemm_batched(gemm(d, ncol, d, Lm, d, dd, pl.schur_solves, Rm, d, wst, false, Wm, d, wst, B), ss);
         if (pl.schur_solves)
-            launch_qtri_solve(pl.T.p, d, dd, Wm, ncol, wst, sig, knd, B, nullptr, st);
+            launch_qtri_solve(pl.T.p, d, dd, Wm, ncol, wst, sig, knd, B, nullptr, ss);
         else
-            launch_eig_diag_solve(Wm, d, ncol, wst, pl.wr.p, pl.wi.p, sig, knd, B, st);
+            launch_eig_diag_solve(Wm, d, ncol, wst, pl.wr.p, pl.wi.p, sig, knd, B, ss);
         gemm_batched(gemm(d, ncol, d, pl.schur_solves ? pl.Z.p : pl.X.p, d, dd, false, Wm, d, wst, false,
                           out, d, wst, B, 1.0, beta),
-                     st);
+                     ss);
     };
     auto residual_gemms = [&]() {
         gemm_batched(gemm(d, d, d, pl.E.p, d, dd, false, pl.tmp1.p, d, dd, false, pl.tmp3.p, d, dd, B), st);
         gemm_batched(gemm(d, d, d, pl.F.p, d, dd, false, pl.tmp4.p, d, dd, false, pl.tmp2.p, d, dd, B), st);
     };
+    // ---------------- particular (particular.cpp:27-107) on the side stream: it needs
+    // V^-1 (queued before it there), the beam source and the modes' nu, none of which
+    // the refinement below touches except nu -- snapshotted here.  Joined before the
+    // boundary stage.
+    VRTE_CUDA_CHECK(cudaMemcpyAsync(pl.nu0.p, pl.nu.p, sizeof(double) * 2 * (size_t)B * d, cudaMemcpyDeviceToDevice,
+                                    st));
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.fork[2], st));
+    VRTE_CUDA_CHECK(cudaStreamWaitEvent(st2, pl.fork[2], 0));
+    PartArgs pa{};
+    pa.d = d;
+    pa.batch = B;
+    pa.n_in = pl.n_in;
+    pa.mu_in = pl.mu_in.p;
+    pa.nu = pl.nu0.p;  // the modes' nu before refinement (the refinement updates nu concurrently)
+    pa.femax = pl.femax.p;
+    pa.mdiag = pl.mdiag.p;
+    pa.order_index = pl.order_index.p;
+    pa.mu_eff = pl.mu_eff.p;
+    pa.sigma = pl.sigma.p;
+    pa.kind = pl.kind.p;
+    pa.fsp = pl.fsp.p;
+    pa.sp = pl.sp.p;
+    pa.sm = pl.sm.p;
+    pa.rhs = pl.rhs.p;
+    pa.g = pl.g.p;
+    pa.eg = pl.eg.p;
+    pa.feg = pl.feg.p;
+    pa.zp = pl.zp.p;
+    pa.zm = pl.zm.p;
+    pa.status = pl.status;
+    launch_dither(pa, st2);
+    gemm_batched(gemm(d, R, d, pl.F.p, d, dd, false, pl.sp.p, d, dR, false, pl.fsp.p, d, dR, B), st2);
+    launch_part_rhs(pa, st2);
+    shifted_solve(pl.rhs.p, pl.W.p, R, dR, pl.sigma.p, pl.kind.p, pl.g.p, 0.0, st2);
+    gemm_batched(gemm(d, R, d, pl.E.p, d, dd, false, pl.g.p, d, dR, false, pl.eg.p, d, dR, B), st2);
+    gemm_batched(gemm(d, R, d, pl.F.p, d, dd, false, pl.eg.p, d, dR, false, pl.feg.p, d, dR, B), st2);
+    // Iterative refinement against the true operator F (E g): the Schur form
+    // carries a normwise backward error ~eps|FE| that the reference's dense LU
+    // (componentwise-small on this graded matrix) does not.
+    for (int it = 0; it < pl.part_refine_iters; ++it) {
+        launch_part_refine_residual(pa, pl.fsp.p, st2);
+        shifted_solve(pl.fsp.p, pl.W.p, R, dR, pl.sigma.p, pl.kind.p, pl.g.p, 1.0, st2);
+        gemm_batched(gemm(d, R, d, pl.E.p, d, dd, false, pl.g.p, d, dR, false, pl.eg.p, d, dR, B), st2);
+        gemm_batched(gemm(d, R, d, pl.F.p, d, dd, false, pl.eg.p, d, dR, false, pl.feg.p, d, dR, B), st2);
+        nl += 6;
+    }
+    launch_zpm(pa, st2);
+    launch_free_modes(d, pl.Be, pl.B, pl.mdiag.p, pl.psi_p.p, pl.psi_m.p, pl.nu.p, pl.wr.p, pl.wi.p,
+                      pl.residual.p, pl.zp.p, pl.zm.p, R, st2);
+    launch_part_residual(pa, st2);
+    nl += 11;
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.join[2], st2));
     // (the 8N residual of the unrefined modes is not needed: every refinement
     // step starts by recomputing it, and final_residual() feeds the gate)
     ResidualArgs ra{};
@@ -471,7 +524,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
         launch_refine_setup(rf, st);
         gemm_batched(gemm(d, 2 * d, d, pl.F.p, d, dd, false, pl.BE.p, d, d2, false, pl.FB.p, d, d2, B), st);
         launch_refine_rhs(rf, st);
-        shifted_solve(pl.FB.p, pl.W2.p, 2 * d, d2, pl.sigma_m.p, pl.kind_m.p, pl.UT.p, 0.0);
+        shifted_solve(pl.FB.p, pl.W2.p, 2 * d, d2, pl.sigma_m.p, pl.kind_m.p, pl.UT.p, 0.0, st);
         gemm_batched(gemm(d, 2 * d, d, pl.E.p, d, dd, false, pl.UT.p, d, d2, false, pl.EU.p, d, d2, B), st);
         launch_refine_update(rf, st);
         nl += 11;
@@ -499,51 +552,8 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     }
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[10], st));
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[1], st));
-    // ---------------- particular
-    VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[0], 0));  // beam source (side stream)
-    PartArgs pa{};
-    pa.d = d;
-    pa.batch = B;
-    pa.n_in = pl.n_in;
-    pa.mu_in = pl.mu_in.p;
-    pa.nu = pl.nu.p;
-    pa.femax = pl.femax.p;
-    pa.mdiag = pl.mdiag.p;
-    pa.order_index = pl.order_index.p;
-    pa.mu_eff = pl.mu_eff.p;
-    pa.sigma = pl.sigma.p;
-    pa.kind = pl.kind.p;
-    pa.fsp = pl.fsp.p;
-    pa.sp = pl.sp.p;
-    pa.sm = pl.sm.p;
-    pa.rhs = pl.rhs.p;
-    pa.g = pl.g.p;
-    pa.eg = pl.eg.p;
-    pa.feg = pl.feg.p;
-    pa.zp = pl.zp.p;
-    pa.zm = pl.zm.p;
-    pa.status = pl.status;
-    launch_dither(pa, st);
-    gemm_batched(gemm(d, R, d, pl.F.p, d, dd, false, pl.sp.p, d, dR, false, pl.fsp.p, d, dR, B), st);
-    launch_part_rhs(pa, st);
-    shifted_solve(pl.rhs.p, pl.W.p, R, dR, pl.sigma.p, pl.kind.p, pl.g.p, 0.0);
-    gemm_batched(gemm(d, R, d, pl.E.p, d, dd, false, pl.g.p, d, dR, false, pl.eg.p, d, dR, B), st);
-    gemm_batched(gemm(d, R, d, pl.F.p, d, dd, false, pl.eg.p, d, dR, false, pl.feg.p, d, dR, B), st);
-    // Iterative refinement against the true operator F (E g): the Schur form
-    // carries a normwise backward error ~eps|FE| that the reference's dense LU
-    // (componentwise-small on this graded matrix) does not.
-    for (int it = 0; it < pl.part_refine_iters; ++it) {
-        launch_part_refine_residual(pa, pl.fsp.p, st);
-        shifted_solve(pl.fsp.p, pl.W.p, R, dR, pl.sigma.p, pl.kind.p, pl.g.p, 1.0);
-        gemm_batched(gemm(d, R, d, pl.E.p, d, dd, false, pl.g.p, d, dR, false, pl.eg.p, d, dR, B), st);
-        gemm_batched(gemm(d, R, d, pl.F.p, d, dd, false, pl.eg.p, d, dR, false, pl.feg.p, d, dR, B), st);
-        nl += 6;
-    }
-    launch_zpm(pa, st);
-    launch_free_modes(d, pl.Be, pl.B, pl.mdiag.p, pl.psi_p.p, pl.psi_m.p, pl.nu.p, pl.wr.p, pl.wi.p,
-                      pl.residual.p, pl.zp.p, pl.zm.p, R, st);
-    launch_part_residual(pa, st);
-    nl += 11;
+    // ---------------- particular: ran on the side stream, concurrent with the refinement
+    VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[2], 0));
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[2], st));
     // ---------------- boundary
     BndArgs ba{};
