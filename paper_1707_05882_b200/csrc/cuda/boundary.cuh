@@ -34,7 +34,7 @@ void launch_copy_zp0(const BndArgs& a, cudaStream_t st);
 // an augmented system [A | B]) are carried through the elimination.
 void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatus* status,
                   const int* order_index, cudaStream_t st, int prof_d = 0, int prof_P = 0, int lda = 0,
-                  int ncols = 0);
+                  int ncols = 0, cudaEvent_t cols_ready = nullptr);
 // Back substitution of an augmented factorization (ncols = G + R) in place, down
 // to row_lo (rounded down to a 64-row block); X [batch][G][R] receives rows >= that.
 void lu_backsolve_aug(double* A, int G, int lda, int R, int batch, const int* perm, double* X, int row_lo,

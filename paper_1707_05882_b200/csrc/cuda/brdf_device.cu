@@ -469,8 +469,6 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
         nl += 6;
     }
     launch_zpm(pa, st2);
-    launch_free_modes(d, pl.Be, pl.B, pl.mdiag.p, pl.psi_p.p, pl.psi_m.p, pl.nu.p, pl.wr.p, pl.wi.p,
-                      pl.residual.p, pl.zp.p, pl.zm.p, R, st2);
     launch_part_residual(pa, st2);
     nl += 11;
     VRTE_CUDA_CHECK(cudaEventRecord(pl.join[2], st2));
@@ -552,8 +550,10 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     }
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[10], st));
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[1], st));
-    // ---------------- particular: ran on the side stream, concurrent with the refinement
-    VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[2], 0));
+    // ---------------- particular: runs on the side stream, concurrent with the refinement;
+    // the free-streaming slots' analytic modes and (zero) particular vectors here
+    launch_free_modes(d, pl.Be, pl.B, pl.mdiag.p, pl.psi_p.p, pl.psi_m.p, pl.nu.p, pl.wr.p, pl.wi.p,
+                      pl.residual.p, pl.zp.p, pl.zm.p, R, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[2], st));
     // ---------------- boundary
     BndArgs ba{};
@@ -572,9 +572,15 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     ba.rhs = pl.lhs.p + G;
     ba.up = pl.up.p;
     launch_bnd_assemble(ba, st);
-    launch_bnd_rhs(ba, st);
+    // right-hand sides on the side stream once the particular vectors are there; the
+    // factorization waits for them only before its first update of those columns
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.fork[3], st));
+    VRTE_CUDA_CHECK(cudaStreamWaitEvent(st2, pl.fork[3], 0));
+    launch_bnd_rhs(ba, st2);
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.join[3], st2));
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[11], st));
-    lu_factor_rm(pl.lhs.p, G, NO, pl.ipiv.p, pl.perm.p, pl.status, pl.order_index.p, st, d, pl.P, G + R, G + R);
+    lu_factor_rm(pl.lhs.p, G, NO, pl.ipiv.p, pl.perm.p, pl.status, pl.order_index.p, st, d, pl.P, G + R, G + R,
+                 pl.join[3]);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[12], st));
     lu_backsolve_aug(pl.lhs.p, G, G + R, R, NO, pl.perm.p, pl.rhs_x.p, pl.full_solution ? 0 : G - 2 * d, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[13], st));

@@ -599,7 +599,8 @@ int outer_block() {
 }  // namespace
 
 void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatus* status,
-                  const int* order_index, cudaStream_t st, int prof_d, int prof_P, int lda, int ncols) {
+                  const int* order_index, cudaStream_t st, int prof_d, int prof_P, int lda, int ncols,
+                  cudaEvent_t cols_ready) {
     if (G > 4096) throw std::invalid_argument("vrte_cuda: boundary system larger than 4096 rows");
     if (lda <= 0) lda = G;
     if (ncols <= 0) ncols = G;  // columns past G: right-hand sides eliminated along (augmented system)
@@ -626,6 +627,10 @@ void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatu
                 panel_dispatch<4>(np, A, G, lda, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
         }
         const int rest = ncols - K0 - NBk;
+        if (cols_ready) {  // the columns past G (right-hand sides) are written by another stream
+            VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, cols_ready, 0));
+            cols_ready = nullptr;
+        }
         if (rest > 0) {
             // U12 = L11^-1 A12 on the block's pivot rows, by 64-row halves
             for (int r0 = K0; r0 < K0 + NBk; r0 += LU_NB) {
