@@ -334,13 +334,6 @@ void vrte_options_init(vrte_options* options) {
     options->out_azimuth = 19;
 }
 
-// ---------------------------------------------------------------- out-of-path
-static vrte_status not_built(const char* what) {
-    return set_error(VRTE_E_ARGUMENT, std::string(what) +
-                                          ": not built (this library is the BRDF-path drop-in; "
-                                          "see DESIGN.md)");
-}
-
 // ---------------------------------------------------------------- radiance
 // capi.cpp:138-232: solve one beam (the material's source, or the options'
 // override), reconstruct the field on the signed zenith x azimuth grid at the
