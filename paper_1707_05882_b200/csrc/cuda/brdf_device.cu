@@ -20,6 +20,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "boundary.cuh"
@@ -135,9 +136,12 @@ struct vrte_cuda_plan {
     int part_refine_iters = 1;
     DevBuf<double> resmax;
     double* resmax_host = nullptr;
+    char* stage = nullptr;  // page-locked staging for the per-call inputs (one async copy each)
+    size_t stage_bytes = 0;
     uint64_t launches = 0;
     ~vrte_cuda_plan() {
         if (resmax_host) cudaFreeHost(resmax_host);
+        if (stage) cudaFreeHost(stage);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         for (auto* es : {fork, join})
@@ -227,23 +231,45 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
         const int m = pl.m_begin + mo * pl.m_stride;
         if (m < L) slot[m] = mo;
     }
-    pl.nodes.upload(p->nodes, N, st);
-    pl.weights.upload(p->weights, N, st);
-    pl.mdiag.upload(mdiag.data(), d, st);
-    pl.omega.upload(p->omega, pl.S, st);
-    pl.greek.upload(p->greek, (size_t)pl.S * pl.Lc * 6, st);
-    pl.tau.upload(p->tau, pl.P, st);
-    pl.medium.upload(medium.data(), pl.P, st);
-    pl.mu_in.upload(p->mu_in, pl.n_in, st);
+    // inputs through a page-locked staging area: every H2D copy is truly asynchronous
+    // (pageable sources would be staged by the driver one copy at a time)
+    {
+        const size_t tab_n = p->base_type == 2 ? (size_t)p->table_n * p->table_n * 16 : 16;
+        const size_t need_d = 2 * (size_t)N + d + pl.S + (size_t)pl.S * pl.Lc * 6 + pl.P + pl.n_in + tab_n +
+                              (size_t)pl.n_in * N * 16 + (size_t)pl.n_in * 16 + (size_t)L * pl.n_dphi * 2;
+        const size_t need = need_d * sizeof(double) + ((size_t)pl.P + B + L) * sizeof(int) + 32 * 256;
+        if (pl.stage_bytes < need) {
+            if (pl.stage) cudaFreeHost(pl.stage);
+            VRTE_CUDA_CHECK(cudaMallocHost(reinterpret_cast<void**>(&pl.stage), need));
+            pl.stage_bytes = need;
+        }
+    }
+    size_t off = 0;
+    auto put = [&](auto& buf, const auto* h, size_t n) {
+        using T = std::remove_pointer_t<decltype(buf.p)>;
+        buf.alloc(n);
+        if (!n) return;
+        std::memcpy(pl.stage + off, h, sizeof(T) * n);
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(buf.p, pl.stage + off, sizeof(T) * n, cudaMemcpyHostToDevice, st));
+        off += (sizeof(T) * n + 255) & ~size_t(255);
+    };
+    put(pl.nodes, p->nodes, N);
+    put(pl.weights, p->weights, N);
+    put(pl.mdiag, mdiag.data(), d);
+    put(pl.omega, p->omega, pl.S);
+    put(pl.greek, p->greek, (size_t)pl.S * pl.Lc * 6);
+    put(pl.tau, p->tau, pl.P);
+    put(pl.medium, medium.data(), pl.P);
+    put(pl.mu_in, p->mu_in, pl.n_in);
     if (p->base_type == 2)
-        pl.table.upload(p->table, (size_t)p->table_n * p->table_n * 16, st);
+        put(pl.table, p->table, (size_t)p->table_n * p->table_n * 16);
     else
         pl.table.alloc(16);
-    pl.beam_rows.upload(p->beam_rows, (size_t)pl.n_in * N * 16, st);
-    pl.post.upload(p->post, (size_t)pl.n_in * 16, st);
-    pl.trig.upload(p->trig, (size_t)L * pl.n_dphi * 2, st);
-    pl.order_index.upload(order_index.data(), B, st);
-    pl.slot_of_order.upload(slot.data(), L, st);
+    put(pl.beam_rows, p->beam_rows, (size_t)pl.n_in * N * 16);
+    put(pl.post, p->post, (size_t)pl.n_in * 16);
+    put(pl.trig, p->trig, (size_t)L * pl.n_dphi * 2);
+    put(pl.order_index, order_index.data(), B);
+    put(pl.slot_of_order, slot.data(), L);
 
     const size_t dd = (size_t)d * d;
     pl.gsf_n.alloc((size_t)L * pl.Lc * 3 * N);
