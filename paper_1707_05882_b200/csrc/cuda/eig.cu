@@ -1760,10 +1760,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) hqr_multi_ke
                     geom(c, wlo, whi);
                     const int nw = whi - wlo + 1;
                     double* Uc = Us2 + (c & 1) * (MW * LDW);
-                    for (int idx = tg; idx < MW * MW; idx += 128) {
-                        const int r = idx % MW, cc = idx / MW;
-                        Wn[r + cc * LDW] = (r < nw && cc < nw) ? H[(wlo + r) + (size_t)(wlo + cc) * d] : 0.0;
-                        Uc[r + cc * LDW] = (r == cc) ? 1.0 : 0.0;
+                    {
+                        // all loads in flight before the first shared store (a generic H
+                        // may alias shared memory, so interleaving would serialise them)
+                        static_assert((MW * MW) % 128 == 0, "window tiling");
+                        double wv[MW * MW / 128];
+#pragma unroll
+                        for (int q = 0; q < MW * MW / 128; ++q) {
+                            const int idx = tg + 128 * q, r = idx % MW, cc = idx / MW;
+                            wv[q] = (r < nw && cc < nw) ? H[(wlo + r) + (size_t)(wlo + cc) * d] : 0.0;
+                        }
+#pragma unroll
+                        for (int q = 0; q < MW * MW / 128; ++q) {
+                            const int idx = tg + 128 * q, r = idx % MW, cc = idx / MW;
+                            Wn[r + cc * LDW] = wv[q];
+                            Uc[r + cc * LDW] = (r == cc) ? 1.0 : 0.0;
+                        }
                     }
                     named_bar(3, 128);
                     if (t == 0) tick(1);
