@@ -89,3 +89,23 @@ def test_empty_layer_is_rejected_like_the_reference():
     with pytest.raises(V.VrteError) as ei:
         product_material(M.MaterialDesc([top, bottom], base="lambertian", albedo=0.1))
     assert ei.value.code == 2 and "optical thickness must be positive" in ei.value.message
+
+
+@pytest.mark.parametrize("which", ["N128_one_layer", "N100_two_layers"])
+def test_large_and_ragged_quadratures(which):
+    # d = 4N = 512 (the largest eigen / LU shapes of the fused kernels: G = 1024)
+    # and d = 400, G = 1600 (no dimension a multiple of the 32/64/128 tiles)
+    if which == "N128_one_layer":
+        desc = slab(M.RAYLEIGH, 0.95, 1.3, "lambertian", 0.25)
+        N = 128
+    else:
+        desc = M.MaterialDesc([M.LayerDesc(0.9, 0.6, np.asarray(M.FULL, float)),
+                               M.LayerDesc(0.8, 1.1, np.asarray(M.generator_G(0.6, 6), float))], base="black")
+        N = 100
+    mu = np.array([0.3, 0.77])
+    b = V.compute_brdf(product_material(desc), V.options(N), mu, 5)
+    g = b.table()
+    r, tm = O.brdf(oracle_material(desc), N, mu, 5)  # the reference as written (own error ~3e-12 here)
+    assert g.shape == r.shape == (2, N, 5, 4, 4)
+    assert matrix_metric(g, r) < 1e-9, matrix_metric(g, r)
+    assert b.device_stats()["max_eigen_residual"] < 1e-10
