@@ -2,16 +2,23 @@
 // homogeneous problem (F E) x = x / nu^2 of every (medium, order), and the
 // mode recovery / residual machinery of homogeneous.cpp:131-287.
 //
-// Reference uses Eigen::EigenSolver (real Schur + eigenvectors).  Here:
-//   hessenberg_kernel : Householder reduction, Q accumulated into Z
-//   hqr_kernel        : Francis double-shift QR with Schur vectors (the
-//                       dlahqr algorithm; Ahues-Kressner deflation, exceptional
-//                       shifts every 10 iterations, dlanv2 standardization)
-//   trevc_kernel      : eigenvectors of the quasi-triangular Schur factor by
-//                       back substitution (dtrevc), back-transformed by a GEMM
-// One CTA per matrix; the near-diagonal band of H (offsets -3..+8) lives in
-// shared memory as its only copy so the sequential control path (reflector,
-// deflation tests, shifts) never touches L2.
+// Reference uses Eigen::EigenSolver (real Schur + eigenvectors).  Here
+// (defaults; the other kernels stay selectable for A/B runs and tests):
+//   hessenberg.cu        : blocked Householder reduction (dlahr2 panels + DMMA
+//                          trailing updates), Q formed into Z
+//   hqr_multi_kernel     : small-bulge multishift Francis QR with aggressive
+//                          early deflation (dlaqr0/3/5 organisation) on a 2-CTA
+//                          cluster per matrix: rank 0 chases up to 4 bulges in a
+//                          32 x 32 shared-memory window and runs the AED window
+//                          Schur, rank 1 applies each chunk's orthogonal factor to
+//                          the rest of H and to Z on the FP64 tensor cores;
+//                          dlahqr rules (Ahues-Kressner deflation, exceptional
+//                          shifts, dlanv2 standardization) for small blocks
+//   trevc_grp_kernel     : eigenvectors of the quasi-triangular Schur factor by
+//                          register-resident back substitution (dtrevc), 4 per
+//                          warp, back-transformed by a GEMM
+//   hqr_kernel / hqr_window_kernel / trevc_kernel: the single-CTA predecessors
+//                          (VRTE_HQR=band|window, VRTE_TREVC=smem)
 #include <climits>
 #include <cstdlib>
 #include <string>
