@@ -100,3 +100,22 @@ def test_batch_reports_first_failure():
     with pytest.raises(V.VrteError) as ei:
         V.compute_brdf_batch([ok, bad], V.options(16, 24), nodes[:2], 5)
     assert ei.value.code == 3 and "negative real axis" in ei.value.message
+
+
+def test_pinned_host_buffers_are_recycled_per_size():
+    import ctypes as C
+    L = V.lib()
+    L.vrte_cuda_host_alloc.restype = C.c_void_p
+    L.vrte_cuda_host_alloc.argtypes = [C.c_size_t]
+    L.vrte_cuda_host_free.argtypes = [C.c_void_p, C.c_size_t]
+    n = 1 << 20
+    p = L.vrte_cuda_host_alloc(n)
+    assert p
+    buf = (C.c_ubyte * n).from_address(p)
+    buf[0], buf[n - 1] = 7, 9
+    assert buf[0] == 7 and buf[n - 1] == 9
+    L.vrte_cuda_host_free(p, n)
+    q = L.vrte_cuda_host_alloc(n)  # the freed buffer of the same size comes back
+    assert q == p
+    L.vrte_cuda_host_free(q, n)
+    L.vrte_cuda_host_free(None, 0)  # null is a no-op
