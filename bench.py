@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-incidents", type=int, default=1,
+    ap.add_argument("--cpu-incidents", type=int, default=2,
                     help="incidents in the bounded CPU sample (x4 basis vectors)")
     ap.add_argument("--concurrency", type=int, default=4,
                     help="C5 spectral batch: bands solved concurrently (plans / streams)")
@@ -170,11 +170,49 @@ def oracle_sample(w, mu_nodes, n_inc, threads):
     om = O.Material(np.array([l.omega for l in desc.layers]), np.array([l.tau for l in desc.layers]),
                     desc.padded_coeffs(), bt, desc.albedo, desc.table)
     pick = np.linspace(0, len(mu_nodes) - 1, n_inc).round().astype(int)
-    _, tm = O.brdf(om, w.N, mu_nodes[pick], w.n_dphi, threads=threads)
+    table, tm = O.brdf(om, w.N, mu_nodes[pick], w.n_dphi, threads=threads)
     t_hom = tm["homogeneous"]
     t_inc = tm["total_wall"] - t_hom
     full = t_hom + len(mu_nodes) / n_inc * t_inc
+    oracle_sample.last = (pick, table)
     return full, tm, [float(x) for x in mu_nodes[pick]]
+
+
+def cpu_model():
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def parity_record(gpu_table):
+    """Parity carried on the bench line: live, the GPU table at the CPU sample's
+    incidents vs the oracle as written (the same run); and the full-table
+    numbers of profiles/parity_r02.json (GPU vs the oracle as written and in
+    accurate mode, every incident, SURVEY §8(d) metric)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from helpers import matrix_metric, survey_metric
+    out = {"metric": "SURVEY §8(d): per Mueller matrix max_rc |G-R| / max(|R_rc|, 1e-3 |R_00|)"}
+    last = getattr(oracle_sample, "last", None)
+    if last is not None and gpu_table is not None:
+        pick, r = last
+        g = gpu_table[pick]
+        out["live_vs_reference_as_written"] = {"incidents": [int(i) for i in pick], "survey": survey_metric(g, r),
+                                               "matrix": matrix_metric(g, r)}
+    prof = os.path.join(ROOT, "profiles", "parity_r02.json")
+    if os.path.exists(prof):
+        try:
+            pj = json.load(open(prof))
+            out["full_table"] = {c["workload"]: {k: c[k] for k in ("gpu_vs_accurate_survey", "gpu_vs_ref_survey",
+                                                                   "ref_vs_accurate_survey", "gpu_vs_accurate_matrix")}
+                                 for c in pj.get("cases", [])}
+            out["full_table_source"] = "profiles/parity_r02.json (scripts/parity_full.py on the B200)"
+        except Exception:
+            pass
+    return out
 
 
 def run_reference(args):
@@ -184,12 +222,14 @@ def run_reference(args):
     w = workload(args.config)
     nodes = quad_nodes(w.N)
     threads = os.cpu_count() or 1
-    vals = []
+    vals, walls = [], []
     t0 = time.time()
     for step in range(args.warmup + args.steps):
+        ts = time.perf_counter()
         full, tm, picked = oracle_sample(w, nodes, args.cpu_incidents, threads)
         if step >= args.warmup:
             vals.append(full)
+            walls.append(time.perf_counter() - ts)
     t_full = statistics.mean(vals)
     value = 1.0 / t_full
     sample = (f"prepare_homogeneous (all {w.material.order_count} orders x media) + "
@@ -198,12 +238,15 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "solves/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_full * 1e3, "higher_is_better": True, "scaling": "weak",
+        # a step is the bounded sample (its real wall time); value is the full solve
+        # rate extrapolated from it (T = T_hom + n_in/k T_k)
+        "ms_per_step": statistics.mean(walls) * 1e3, "extrapolated_ms_per_solve": t_full * 1e3,
+        "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY §8(d) generator)",
         "config": {"workload": f"{args.config}: {w.note}", "N": w.N, "L": w.material.order_count,
                    "layers": len(w.material.layers), "n_in": len(nodes), "n_dphi": w.n_dphi},
         "cpu_baseline": {"value": value, "unit": "solves/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "extrapolated": True, "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": time.time() - t0,
     }
@@ -544,15 +587,23 @@ def main():
     # ---------------- roofline of the dominant kernel
     # Algorithmic FP64 flops per launch (SURVEY §8(d) / Golub-Van Loan counts,
     # DESIGN.md §5); the stage times are CUDA events on the plan's stream.
+    # Units per launch are the EXECUTED ones: Be (medium, order) slots go through
+    # the eigen pipeline (the free-streaming slots -- zero kernel -- are filled
+    # analytically and cost no flops), every order through the boundary stage.
     d = 4 * N
-    B = S * L
+    Be = int(res["eigen_slots"])
     G = 2 * d * P
-    kern = {"hqr_multi_kernel (multishift Francis QR + AED + Schur vectors)": (res["t_hqr"], B * 20.0 * d ** 3),
-            "boundary LU factor (panel + swap + trsm + DMMA GEMM)": (res["t_lu_factor"], L * (2.0 / 3.0) * G ** 3),
-            "boundary LU solve (trsm + DMMA GEMM)": (res["t_lu_solve"], L * 2.0 * G ** 2 * 4 * n_in),
-            "eigen refinement (Newton step, 8N residual GEMMs)": (res["t_refine"], B * 24.0 * d ** 3),
-            "blocked Hessenberg + Q": (res["t_hessenberg"], B * (10.0 / 3.0 + 4.0 / 3.0) * d ** 3),
-            "trevc_reg_kernel (eigenvectors)": (res["t_trevc"], B * (1.0 / 3.0) * d ** 3)}
+    R = 4 * n_in
+    kern = {"hqr_multi_kernel (multishift Francis QR + AED + Schur vectors)": (res["t_hqr"], Be * 20.0 * d ** 3),
+            # the augmented [A | B] factorization also eliminates the R right-hand
+            # sides (L^-1 P B: G^2 R flops) besides the (2/3) G^3 of the LU proper
+            "boundary LU factor (augmented: Crout panels + TRSM + DMMA GEMM)":
+                (res["t_lu_factor"], L * ((2.0 / 3.0) * G ** 3 + G ** 2 * R)),
+            # back substitution U x = y for all R columns (full: the residual gate needs every unknown)
+            "boundary back substitution (TRSM + DMMA GEMM)": (res["t_lu_solve"], L * G ** 2 * R),
+            "eigen refinement (Newton step, 8N residual GEMMs)": (res["t_refine"], Be * 24.0 * d ** 3),
+            "blocked Hessenberg + Q": (res["t_hessenberg"], Be * (10.0 / 3.0 + 4.0 / 3.0) * d ** 3),
+            "trevc_grp_kernel (eigenvectors)": (res["t_trevc"], Be * (1.0 / 3.0) * d ** 3)}
     name = max(kern, key=lambda k: kern[k][0])
     t_k, flops = kern[name]
     traffic = None
@@ -570,20 +621,28 @@ def main():
                 "peak_source": "measured cuBLAS DGEMM (torch.float64 matmul 8192^3) on this GPU; "
                                "MEASURED_PEAKS.json has no FP64 entry (B200 FP64 tensor rate = FP64 rate)",
                 "algorithmic_flops_per_launch": flops,
-                "flop_model": "QR with Schur vectors 20 d^3 per (medium, order); LU (2/3) G^3 and solve "
-                              "2 G^2 R per order; Hessenberg+Q 14/3 d^3; d = 4N, G = 2dP, R = 4 n_in",
+                "flop_model": "QR with Schur vectors 20 d^3 per executed (medium, order) slot (Be of them); "
+                              "augmented LU (2/3) G^3 + G^2 R and back substitution G^2 R per order; "
+                              "Hessenberg+Q 14/3 d^3, trevc d^3/3, refinement 24 d^3 per executed slot; "
+                              "d = 4N, G = 2dP, R = 4 n_in",
+                "units": {"eigen_slots_executed": Be, "slots": int(res["slots"]), "orders": L},
                 "stage_tflops": {k: (f / t / 1e12 if t > 0 else None) for k, (t, f) in kern.items()}}
 
     # ---------------- CPU baseline (rank 0, N = 1 only)
     cpu = None
+    gpu_table = None
     if world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         full, tm, picked = oracle_sample(w, nodes, args.cpu_incidents, threads)
-        cpu = {"value": 1.0 / full, "unit": "solves/s", "cores": threads, "kind": "port",
+        cpu = {"value": 1.0 / full, "unit": "solves/s", "cores": threads, "kind": "port", "extrapolated": True,
+               "cpu_model": cpu_model(),
                "sample": f"oracle/ (reference algorithm, LAPACK) on {threads} host threads: "
                          f"prepare_homogeneous + {args.cpu_incidents} incident(s) x 4 basis at mu_in="
-                         f"{picked}, extrapolated to {n_in} incidents; measured "
-                         f"{tm['total_wall']:.1f} s for an extrapolated {full:.1f} s/solve"}
+                         f"{picked}, extrapolated to {n_in} incidents (T = T_hom + n_in/k T_k, BASELINE.md §2); "
+                         f"measured {tm['total_wall']:.1f} s for an extrapolated {full:.1f} s/solve"}
+        gb = V.compute_brdf(mat, opts, nodes, w.n_dphi)
+        gpu_table = gb.table()
+        gb.close()
 
     line = {
         "metric": METRIC,
@@ -612,6 +671,9 @@ def main():
                                                  "t_synthesis", "t_hessenberg", "t_hqr", "t_trevc",
                                                  "t_refine", "t_lu_factor", "t_lu_solve")},
         "max_eigen_residual": res["max_eigen_residual"],
+        "gates": {k: res[k] for k in ("max_boundary_residual", "max_boundary_condition", "boundary_refined",
+                                       "max_balance_residual", "max_particular_residual")},
+        "parity": parity_record(gpu_table),
     }
     print(json.dumps(line), flush=True)
     if dist:

@@ -48,6 +48,14 @@ typedef struct vrte_cuda_problem {
        n_orders = 0 means all L orders on this device. */
     int32_t m_begin, m_stride, n_orders;
     int32_t device;           /* CUDA ordinal; -1 = current device */
+    /* vrte_cuda_brdf only: with n_devices > 1 the orders are sharded cyclically
+       over these devices (m = k, k + D, ...), every shard runs the
+       pipeline on its own device, the tau = 0 stacks are gathered to devices[0]
+       (peer copies over NVLink) and synthesized there in order 0..L-1: the table
+       is bitwise identical to the single-device one.  Repeated ordinals run
+       several shards on one device. */
+    const int32_t* devices;
+    int32_t n_devices;
 } vrte_cuda_problem;
 
 typedef struct vrte_cuda_result {
@@ -71,6 +79,13 @@ typedef struct vrte_cuda_result {
     uint64_t qr_cycles[8];  /* debug: QR phase cycles / counters summed over matrices */
     double max_eigen_residual;
     double max_particular_residual;
+    double max_balance_residual;    /* particular 8N balance (particular.cpp:86-105, gate 1e-6) */
+    double max_boundary_residual;   /* |A x - b| / (|A||x| + |b|) (boundary.cpp:240-256, gate 1e-9) */
+    double max_boundary_condition;  /* lower bound of cond_1 over the orders' boundary matrices */
+    uint64_t boundary_refined;      /* 1 if the refinement step of boundary.cpp:245-248 ran */
+    uint64_t boundary_cond_warnings;/* orders whose condition bound exceeds 1e14 (boundary.cpp:259-263) */
+    uint64_t eigen_slots;   /* (medium, order) slots through the eigen pipeline (the rest are free-streaming) */
+    uint64_t slots;         /* all (medium, order) slots of the call */
     int32_t status;         /* 0 ok, 3 numerical, 5 argument */
     char message[512];
 } vrte_cuda_result;
@@ -146,6 +161,8 @@ VRTE_API int32_t vrte_cuda_synthesize(const vrte_cuda_problem* problem, const do
                                       double* table, vrte_cuda_result* result);
 
 VRTE_API int32_t vrte_cuda_device_count(void);
+/* The calling thread's current CUDA device (0 when none is set). */
+VRTE_API int32_t vrte_cuda_current_device(void);
 
 /* Kernel-level check of the batched row-major LU (lu.cu) used by the boundary
  * stage: X[b] = A[b]^-1 B[b] for `batch` row-major G x G systems with `ncol`

@@ -18,6 +18,11 @@ typedef struct vrte_brdf_device_stats {
     uint64_t dithered, clamped, polished, kernel_launches;
     double max_eigen_residual, max_particular_residual;
     uint64_t material_hash; /* FNV-1a over the numeric content (brdf.cpp:11-41) */
+    double max_balance_residual;    /* particular 8N balance residual (gate 1e-6) */
+    double max_boundary_residual;   /* boundary system relative residual (gate 1e-9) */
+    double max_boundary_condition;  /* lower bound of cond_1 of the boundary matrices */
+    uint64_t boundary_refined;      /* boundary refinement step taken (boundary.cpp:245-248) */
+    uint64_t boundary_cond_warnings;/* orders above the 1e14 warning level (boundary.cpp:259-263) */
 } vrte_brdf_device_stats;
 
 VRTE_API vrte_status vrte_brdf_device_stats_get(const vrte_brdf* brdf, vrte_brdf_device_stats* out);
@@ -30,8 +35,9 @@ VRTE_API vrte_status vrte_brdf_plan_create(const vrte_material* material, const 
                                            const double* basis, int32_t device, int32_t m_begin,
                                            int32_t m_stride, int32_t n_orders, vrte_cuda_plan** out);
 
-/* Assemble a BRDF handle from a host table computed elsewhere (multi-GPU
- * root after the order gather).  Takes a copy of `table`. */
+/* Assemble a BRDF handle from the tau = 0 upward stacks of ALL orders,
+ * up_all_orders [L][4 n_mu_in][4N] (host), gathered from order shards: the
+ * Fourier synthesis runs on the device and the stacks are read, not kept. */
 VRTE_API vrte_status vrte_brdf_from_stacks(const vrte_material* material, const vrte_options* options,
                                            const double* mu_in, size_t n_mu_in, int32_t n_dphi,
                                            const double* basis, const double* up_all_orders,

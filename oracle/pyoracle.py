@@ -77,6 +77,7 @@ def lib():
         L.oracle_particular.argtypes = [mp, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                         C.c_double, dp, dp, dp, dp, dp]
         L.oracle_set_accurate.argtypes = [C.c_int32]
+        L.oracle_set_cache_boundary.argtypes = [C.c_int32]
         L.oracle_brdf.argtypes = [mp, C.c_int32, C.c_int32, C.c_int32, dp, C.c_size_t,
                                   C.c_int32, dp, dp, C.POINTER(OracleTimings), dp]
         _lib = L
@@ -131,6 +132,17 @@ class accurate:
 
     def __exit__(self, *exc):
         lib().oracle_set_accurate(0)
+
+
+class cached_boundary:
+    """Context manager: reuse each order's boundary LU across incidents (bit-identical
+    results, see oracle_set_cache_boundary); for full-table parity tests only."""
+
+    def __enter__(self):
+        lib().oracle_set_cache_boundary(1)
+
+    def __exit__(self, *exc):
+        lib().oracle_set_cache_boundary(0)
 
 
 def quadrature(n):

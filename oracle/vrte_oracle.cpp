@@ -17,6 +17,8 @@
 #include <complex>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -531,7 +533,10 @@ static bool accurate_mode() {
     }
     return v == 1;
 }
-static double polish_threshold() { return accurate_mode() ? 0.0 : 0.5 * kEigenResidualBound; }
+static double polish_threshold() {
+    static const double acc = std::getenv("VRTE_ORACLE_POLISH") ? std::atof(std::getenv("VRTE_ORACLE_POLISH")) : 0.0;
+    return accurate_mode() ? acc : 0.5 * kEigenResidualBound;
+}
 struct Mode {
     cd nu;
     std::vector<cd> psi_plus, psi_minus;
@@ -972,10 +977,21 @@ struct OrderBoundary {
     std::vector<LayerCoef> coef[2];
     double condition = 0, residual = 0;
 };
+// Memo of one order's boundary left-hand side and its LU (tests only, see
+// oracle_set_cache_boundary): the LHS carries no incident or k dependence
+// (boundary.cpp:219), so reusing the factors of the identical matrix leaves
+// every solution bit for bit unchanged and only skips the rebuild.
+std::atomic<int> g_cache_boundary{0};
+struct BoundaryLhs {
+    std::vector<cd> lhs;
+    double anorm1 = 0.0, lhs_norm = 0.0, condition = 0.0;
+    std::unique_ptr<ZLu> lu;
+    std::mutex mu;
+};
 // boundary.cpp:142-265: complex global block system, LU, 2 RHS, refinement.
 static OrderBoundary solve_boundary(const Material& spec, double mu0, const double* stokes,
                                     const Quad& q, int m, const std::vector<const ModeSet*>& modes,
-                                    const std::vector<const Part*> parts[2]) {
+                                    const std::vector<const Part*> parts[2], BoundaryLhs* memo = nullptr) {
     const int n = q.n, d = 4 * n, P = (int)spec.layers.size(), blk = 2 * d, G = blk * P;
     std::vector<double> tau_top(P, 0.0);
     for (int p = 1; p < P; ++p) tau_top[p] = tau_top[p - 1] + spec.layers[p - 1].tau;
@@ -983,9 +999,14 @@ static OrderBoundary solve_boundary(const Material& spec, double mu0, const doub
     std::vector<std::vector<cd>> att(P);
     for (int p = 0; p < P; ++p) att[p] = mode_exp_at(*modes[p], spec.layers[p].tau);
 
-    std::vector<cd> lhs((size_t)G * G, 0.0);
+    std::unique_lock<std::mutex> memo_lock;
+    if (memo) memo_lock = std::unique_lock<std::mutex>(memo->mu);
+    const bool have_lhs = memo && memo->lu;
+    std::vector<cd> lhs_own(have_lhs ? 0 : (size_t)G * G, 0.0);
+    std::vector<cd>& lhs = have_lhs ? memo->lhs : lhs_own;
     std::vector<cd> rhs[2] = {std::vector<cd>(G, 0.0), std::vector<cd>(G, 0.0)};
     auto put = [&](int col, int row0, const std::vector<cd>& v, cd s) {
+        if (have_lhs) return;
         cd* c = lhs.data() + (size_t)col * G + row0;
         for (int i = 0; i < d; ++i) c[i] = s * v[i];
     };
@@ -1029,7 +1050,7 @@ static OrderBoundary solve_boundary(const Material& spec, double mu0, const doub
         const Mode& md = modes[qq]->modes[j];
         put(ca(qq, j), rb, md.psi_plus, att[qq][j]);
         put(cb(qq, j), rb, md.psi_minus, 1.0);
-        if (refl[0].active) {
+        if (refl[0].active && !have_lhs) {
             cd* c1 = lhs.data() + (size_t)ca(qq, j) * G + rb;
             cd* c2 = lhs.data() + (size_t)cb(qq, j) * G + rb;
             for (int i = 0; i < d; ++i) {
@@ -1045,29 +1066,49 @@ static OrderBoundary solve_boundary(const Material& spec, double mu0, const doub
         }
 
     double anorm1 = 0.0, lhs_norm = 0.0;
-    for (int j = 0; j < G; ++j) {
-        double cs = 0;
-        for (int i = 0; i < G; ++i) {
-            const double a = std::abs(lhs[(size_t)j * G + i]);
-            cs += a;
-            lhs_norm = std::max(lhs_norm, a);
-        }
-        anorm1 = std::max(anorm1, cs);
-    }
-    ZLu lu(lhs, G);
+    std::unique_ptr<ZLu> lu_own;
     OrderBoundary out;
-    out.condition = 1.0 / std::max(lu.rcond(anorm1), 1e-300);
+    if (have_lhs) {
+        anorm1 = memo->anorm1;
+        lhs_norm = memo->lhs_norm;
+        out.condition = memo->condition;
+    } else {
+        for (int j = 0; j < G; ++j) {
+            double cs = 0;
+            for (int i = 0; i < G; ++i) {
+                const double a = std::abs(lhs[(size_t)j * G + i]);
+                cs += a;
+                lhs_norm = std::max(lhs_norm, a);
+            }
+            anorm1 = std::max(anorm1, cs);
+        }
+        lu_own = std::make_unique<ZLu>(lhs, G);
+        out.condition = 1.0 / std::max(lu_own->rcond(anorm1), 1e-300);
+        if (memo) {
+            memo->anorm1 = anorm1;
+            memo->lhs_norm = lhs_norm;
+            memo->condition = out.condition;
+            memo->lhs = std::move(lhs_own);
+            memo->lu = std::move(lu_own);
+        }
+    }
+    const ZLu& lu = memo ? *memo->lu : *lu_own;
+    const std::vector<cd>& A = memo ? memo->lhs : lhs_own;
     for (int k = 0; k < 2; ++k) {
         std::vector<cd> c = lu.solve(rhs[k]);
         const double rn = max_abs(rhs[k]);
         auto resid_of = [&](const std::vector<cd>& x) {
-            std::vector<cd> r = matvec(lhs, G, G, x);
+            std::vector<cd> r = matvec(A, G, G, x);
             for (int i = 0; i < G; ++i) r[i] -= rhs[k][i];
             return r;
         };
         double scale = lhs_norm * std::max(max_abs(c), 1e-300) + rn;
         double resid = max_abs(resid_of(c));
-        if (resid > 1e-10 * scale || accurate_mode()) {
+        // accurate mode: VRTE_ORACLE_BND_STEPS refinement steps (default 1)
+        static const int acc_steps =
+            std::getenv("VRTE_ORACLE_BND_STEPS") ? std::atoi(std::getenv("VRTE_ORACLE_BND_STEPS")) : 1;
+        const int steps = accurate_mode() ? acc_steps : (resid > 1e-10 * scale ? 1 : 0);
+        for (int it = 0; it < steps; ++it) {
             std::vector<cd> r = resid_of(c);
             for (auto& v : r) v = -v;
             const std::vector<cd> dc = lu.solve(r);
@@ -1689,6 +1730,7 @@ class Solver {
             sig_[p] = s;
         }
         states_.assign(rep_.size(), std::vector<OrderState>(L_));
+        for (int m = 0; m < L_; ++m) bmemo_.push_back(std::make_unique<BoundaryLhs>());
     }
     const Quad& quad() const { return quad_; }
     int order_count() const { return L_; }
@@ -1767,7 +1809,7 @@ class Solver {
                         pk[0][p] = &parts[((size_t)m * 2 + 0) * S + sig_[p]];
                         pk[1][p] = &parts[((size_t)m * 2 + 1) * S + sig_[p]];
                     }
-                    const OrderBoundary ob = solve_boundary(spec_, mu0, stokes, quad_, m, ms, pk);
+                    const OrderBoundary ob = solve_boundary(spec_, mu0, stokes, quad_, m, ms, pk, boundary_memo(m));
                     conds[m] = ob.condition;
                     // tau = 0 upward stack of layer 0 (t_local = 0, beam_top = 1)
                     const ModeSet& m0 = *ms[0];
@@ -1838,7 +1880,7 @@ class Solver {
                     pk[0][p] = &parts[((size_t)m * 2 + 0) * S + sig_[p]];
                     pk[1][p] = &parts[((size_t)m * 2 + 1) * S + sig_[p]];
                 }
-                const OrderBoundary ob = solve_boundary(spec_, mu0, stokes, quad_, m, ms, pk);
+                const OrderBoundary ob = solve_boundary(spec_, mu0, stokes, quad_, m, ms, pk, boundary_memo(m));
                 for (int k = 0; k < 2; ++k) {
                     auto& ch = chains[m][k];
                     ch.resize(P);
@@ -1958,7 +2000,9 @@ class Solver {
     int L_ = 0;
     std::vector<int> sig_, rep_;
     std::vector<std::vector<OrderState>> states_;
+    std::vector<std::unique_ptr<BoundaryLhs>> bmemo_;
     bool ready_ = false;
+    BoundaryLhs* boundary_memo(int m) { return g_cache_boundary.load() ? bmemo_[m].get() : nullptr; }
 };
 
 // reconstruction.cpp:201-227 (FourierBasis::phi, kernel.cpp:111-122).
@@ -2142,6 +2186,7 @@ const char* oracle_last_error(void) { return g_err.c_str(); }
 uint64_t oracle_polish_count(void) { return vo::g_polish_modes.load(); }
 
 void oracle_set_accurate(int32_t on) { vo::g_accurate.store(on ? 1 : 0); }
+void oracle_set_cache_boundary(int32_t on) { vo::g_cache_boundary.store(on ? 1 : 0); }
 
 int32_t oracle_quadrature(int32_t n, double* nodes, double* weights) {
     return guarded([&] {

@@ -53,6 +53,11 @@ uint64_t oracle_polish_count(void);
 /* 1: run the reference algorithm to its fp64 limit (polish every mode, refine
  * every linear solve once); 0: exactly the reference's thresholds (default). */
 void oracle_set_accurate(int32_t on);
+/* 1: factor each order's boundary matrix once per solver and reuse the LU for
+ * every incident (the matrix has no incident or k dependence, boundary.cpp:219;
+ * results are bit-identical to 0).  Tests only: the timed CPU baseline keeps
+ * the reference's per-incident factorization (default 0). */
+void oracle_set_cache_boundary(int32_t on);
 
 /* types.cpp:27-68 */
 int32_t oracle_quadrature(int32_t n, double* nodes, double* weights);

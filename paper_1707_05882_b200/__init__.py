@@ -79,6 +79,11 @@ class DeviceStats(C.Structure):
         ("max_eigen_residual", C.c_double),
         ("max_particular_residual", C.c_double),
         ("material_hash", C.c_uint64),
+        ("max_balance_residual", C.c_double),
+        ("max_boundary_residual", C.c_double),
+        ("max_boundary_condition", C.c_double),
+        ("boundary_refined", C.c_uint64),
+        ("boundary_cond_warnings", C.c_uint64),
     ]
 
     def as_dict(self):
@@ -113,6 +118,13 @@ class CudaResult(C.Structure):
         ("qr_cycles", C.c_uint64 * 8),
         ("max_eigen_residual", C.c_double),
         ("max_particular_residual", C.c_double),
+        ("max_balance_residual", C.c_double),
+        ("max_boundary_residual", C.c_double),
+        ("max_boundary_condition", C.c_double),
+        ("boundary_refined", C.c_uint64),
+        ("boundary_cond_warnings", C.c_uint64),
+        ("eigen_slots", C.c_uint64),
+        ("slots", C.c_uint64),
         ("status", C.c_int32),
         ("message", C.c_char * 512),
     ]
@@ -136,7 +148,7 @@ EXPORTED = [
     "vrte_cuda_brdf", "vrte_cuda_plan_create", "vrte_cuda_plan_run", "vrte_cuda_plan_fetch",
     "vrte_cuda_plan_fetch_up", "vrte_cuda_plan_fetch_modes", "vrte_cuda_plan_fetch_ef",
     "vrte_cuda_plan_destroy",
-    "vrte_cuda_synthesize", "vrte_cuda_device_count", "vrte_cuda_lu_solve", "vrte_cuda_hessenberg", "vrte_cuda_schur",
+    "vrte_cuda_synthesize", "vrte_cuda_device_count", "vrte_cuda_current_device", "vrte_cuda_lu_solve", "vrte_cuda_hessenberg", "vrte_cuda_schur",
     "vrte_cuda_radiance_field", "vrte_cuda_mc_trace", "vrte_cuda_host_alloc", "vrte_cuda_host_free",
 ]
 

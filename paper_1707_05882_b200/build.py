@@ -20,6 +20,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build", "vrte")
 LIB = os.path.join(PKG, "lib", "libvrte.so")
+SONAME = "libvrte.so.1"
 INCLUDE = os.path.join(ROOT, "include")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -99,8 +100,15 @@ def build(verbose: bool = False, force: bool = False) -> str:
             if verbose:
                 sys.stdout.write(out)
     if jobs or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        _run([nvcc, "-shared", *ARCH, "-cudart", "static", "-o", LIB, *objs, "-lpthread", "-ldl",
-              "-lrt"])
+        # SONAME libvrte.so.1: the reference's SOVERSION 1 (src/CMakeLists.txt:37-42), so
+        # binaries linked against the reference's libvrte resolve to this library
+        _run([nvcc, "-shared", *ARCH, "-cudart", "static", "-Xlinker", "-soname=" + SONAME, "-o", LIB, *objs,
+              "-lpthread", "-ldl", "-lrt"])
+    link = os.path.join(os.path.dirname(LIB), SONAME)
+    if os.path.lexists(link) and os.readlink(link) != os.path.basename(LIB):
+        os.remove(link)
+    if not os.path.lexists(link):
+        os.symlink(os.path.basename(LIB), link)
     return LIB
 
 

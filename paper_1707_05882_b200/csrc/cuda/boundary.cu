@@ -7,6 +7,9 @@
 // and every (incident, Stokes channel) is a right-hand side of one blocked
 // triangular solve.  The tau = 0 upward stack (boundary.cpp:20-35) is then a
 // single GEMM per order against [psi+ | att psi-] of the top layer.
+#include <algorithm>
+#include <vector>
+
 #include "boundary.cuh"
 
 namespace vrte {
@@ -56,7 +59,19 @@ __global__ void assemble_kernel(BndArgs a) {
     double* A = a.lhs + (size_t)mo * a.sl;
     const int ca = bnd_col(p, jj, d, G);       // column A_p(jj)
     const int cbk = bnd_col(p, d + jj, d, G);  // column B_p(jj)
-    auto at = [&](int r, int c) -> double& { return A[(size_t)bnd_row(r, d, G) * a.ldl + c]; };
+    double* A0 = a.lhs0 ? a.lhs0 + (size_t)mo * a.sl : nullptr;
+    struct Ref {  // writes the factored system and its untouched copy
+        double* x;
+        double* y;
+        __device__ void operator=(double v) const {
+            *x = v;
+            if (y) *y = v;
+        }
+    };
+    auto at = [&](int r, int c) -> Ref {
+        const size_t o = (size_t)bnd_row(r, d, G) * a.ldl + c;
+        return Ref{A + o, A0 ? A0 + o : nullptr};
+    };
     if (p == 0) {
         at(i, ca) = pk(dflip(pm, i));
         at(i, cbk) = pk(att * dflip(pp, i));
@@ -136,9 +151,14 @@ __global__ void base_kernel(BndArgs a, int mo) {
     reflect_rows(a.p, v, d, lane, out);
     __syncwarp();
     double* A = a.lhs + (size_t)mo * a.sl;
+    double* A0 = a.lhs0 ? a.lhs0 + (size_t)mo * a.sl : nullptr;
     const int col = bnd_col(q, (isb ? d : 0) + jj, d, G);
     const int rb = d + 2 * d * (P - 1);
-    for (int i = lane; i < d; i += 32) A[(size_t)bnd_row(rb + i, d, G) * a.ldl + col] -= out[i];
+    for (int i = lane; i < d; i += 32) {
+        const size_t o = (size_t)bnd_row(rb + i, d, G) * a.ldl + col;
+        A[o] -= out[i];
+        if (A0) A0[o] -= out[i];
+    }
 }
 
 // Right-hand sides: warp per (order mo, column = incident*4 + channel).
@@ -152,11 +172,40 @@ __global__ void rhs_kernel(BndArgs a) {
     const int m = a.p.order_of(mo);
     const double mu0 = a.p.mu_in[ii];
     // row-major [G][R] per order (lu.cu); B(r) = rhs[mo][r * R + col]
+    // writes B (and its untouched copy in lhs0), accumulating max|b| and ||b||_1
+    double bmax = 0.0, b1 = 0.0;
+    struct Ref {
+        double* x;
+        double* y;
+        double* bmax;
+        double* b1;
+        __device__ void operator=(double v) const {
+            *x = v;
+            if (y) *y = v;
+            *bmax = fmax(*bmax, fabs(v));
+            *b1 += fabs(v);
+        }
+    };
     struct RowView {
         double* base;
+        double* base0;
         int R, d, G;
-        __device__ double& operator[](int r) const { return base[(size_t)bnd_row(r, d, G) * R]; }
-    } B{a.rhs + (size_t)mo * a.sr + col, a.ldr, d, G};
+        double* bmax;
+        double* b1;
+        __device__ Ref operator[](int r) const {
+            const size_t o = (size_t)bnd_row(r, d, G) * R;
+            return Ref{base + o, base0 ? base0 + o : nullptr, bmax, b1};
+        }
+    } B{a.rhs + (size_t)mo * a.sr + col, a.lhs0 ? a.lhs0 + (size_t)mo * a.sl + (a.rhs - a.lhs) + col : nullptr,
+        a.ldr, d, G, &bmax, &b1};
+    auto finish_norms = [&]() {
+        if (!a.bnorm) return;
+        const double mx = warp_max(bmax), s1 = warp_sum(b1);
+        if (lane == 0) {
+            a.bnorm[2 * ((size_t)mo * R + col)] = mx;
+            a.bnorm[2 * ((size_t)mo * R + col) + 1] = s1;
+        }
+    };
     auto zp = [&](int p, int i) {
         const size_t om = (size_t)a.p.medium[p] * a.p.n_orders + mo;
         return a.zp[(om * R + col) * d + i];
@@ -182,6 +231,7 @@ __global__ void rhs_kernel(BndArgs a) {
     const bool active = m == 0 && a.p.base_type != 0 && !(a.p.base_type == 1 && a.p.rho == 0.0);
     if (!active) {
         for (int i = lane; i < d; i += 32) B[rb + i] = -(bb * zp(q, i));
+        finish_norms();
         return;
     }
     double* v = sm + (size_t)w * 2 * d;
@@ -198,6 +248,7 @@ __global__ void rhs_kernel(BndArgs a) {
         if ((kc == 1) != (r < 2)) s = 0.0;
         B[rb + i] = -(bb * zp(q, i)) + (out[i] + s);
     }
+    finish_norms();
 }
 
 // up = Z+ of the top layer (then += Top0 * coefficients by GEMM).
@@ -212,7 +263,157 @@ __global__ void copy_zp0_kernel(BndArgs a) {
     a.up[idx] = a.zp[om * R * d + rest];
 }
 
+// Per order: max |A_ij| and ||A||_1 (max column sum) of the untouched copy.
+// CTA per (order, 256-column slab); thread per column, rows looped (coalesced).
+__global__ void bnd_anorm_kernel(BndArgs a, int G) {
+    const int mo = blockIdx.y, c = blockIdx.x * blockDim.x + threadIdx.x;
+    __shared__ double red[32];
+    double mx = 0.0, cs = 0.0;
+    if (c < G) {
+        const double* A0 = a.lhs0 + (size_t)mo * a.sl + c;
+        for (int r = 0; r < G; ++r) {
+            const double v = fabs(A0[(size_t)r * a.ldl]);
+            mx = fmax(mx, v);
+            cs += v;
+        }
+    }
+    mx = block_max(mx, red);
+    cs = block_max(cs, red);
+    if (threadIdx.x == 0) {
+        atomic_max_double(&a.anorm[2 * mo], mx);
+        atomic_max_double(&a.anorm[2 * mo + 1], cs);
+    }
+}
+
+// Thread per (order, right-hand side): residual column of lhs0's B part after
+// bnd_residual_gemm, solution X [mo][G][R] (row-major, unknown order).
+__global__ void bnd_check_kernel(BndArgs a, const double* X, int G, int R, int stage, DeviceStatus* status) {
+    const int mo = blockIdx.y, r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= R) return;
+    const double* res = a.lhs0 + (size_t)mo * a.sl + G + r;
+    const double* x = X + (size_t)mo * G * R + r;
+    double rmax = 0.0, xmax = 0.0, x1 = 0.0;
+    bool finite = true;
+    for (int n = 0; n < G; ++n) {
+        const double v = res[(size_t)n * a.ldl], xv = x[(size_t)n * R];
+        finite = finite && isfinite(xv);
+        rmax = fmax(rmax, fabs(v));
+        xmax = fmax(xmax, fabs(xv));
+        x1 += fabs(xv);
+    }
+    const double bmax = a.bnorm[2 * ((size_t)mo * R + r)], b1 = a.bnorm[2 * ((size_t)mo * R + r) + 1];
+    const double amax = a.anorm[2 * mo], a1 = a.anorm[2 * mo + 1];
+    const double scale = amax * fmax(xmax, 1e-300) + bmax;
+    const double rel = bmax > 0.0 ? rmax / scale : 0.0;
+    // lower bound of cond_1(A): ||A||_1 ||A^-1 b||_1 / ||b||_1
+    const double cond = b1 > 0.0 ? a1 * x1 / b1 : 0.0;
+    atomic_max_double(&a.condm[mo], cond);
+    atomic_max_double(&status->max_boundary_residual, rel);
+    const int m = a.p.order_of(mo);
+    if (!finite || !(rmax == rmax)) {
+        report_failure(status, kFailBoundary, 3, m, rmax, cond);
+        return;
+    }
+    if (stage == 0 && rmax > 1e-10 * scale) atomicExch(&status->bnd_refine, 1);
+    if (stage == 1 && bmax > 0.0 && rmax > 1e-9 * scale) report_failure(status, kFailBoundary, 3, m, rmax, cond);
+}
+
+// Refinement right-hand side: dX <- -(A x - b) gathered through the row map.
+__global__ void bnd_refine_rhs_kernel(BndArgs a, const int* perm_all, double* dX, int G, int R) {
+    const long long total = (long long)a.p.n_orders * G * R;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(e % R);
+        const long long rb = e / R;
+        const int i = (int)(rb % G), mo = (int)(rb / G);
+        dX[e] = -a.lhs0[(size_t)mo * a.sl + (size_t)perm_all[(size_t)mo * G + i] * a.ldl + G + c];
+    }
+}
+
+__global__ void add_kernel(double* X, const double* dX, long long n) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+        X[e] += dX[e];
+}
+
 }  // namespace
+
+void launch_bnd_norms(const BndArgs& a, int G, int R, cudaStream_t st) {
+    (void)R;
+    VRTE_CUDA_CHECK(cudaMemsetAsync(a.anorm, 0, sizeof(double) * 2 * (size_t)a.p.n_orders, st));
+    bnd_anorm_kernel<<<dim3((G + 255) / 256, a.p.n_orders), 256, 0, st>>>(a, G);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+// lhs0's B columns <- A x - b (or += A dx with accumulate): row-major
+// Res (G x R) = A (G x G) X (G x R) - B, i.e. the column-major
+// Res^T = X^T A^T - B^T with every operand read in place.
+// The matrix is block sparse: each row block of equations touches the columns
+// of at most two layers (bnd_row / bnd_col orders: interface p rows [2dp, 2dp+2d)
+// hold layers p and p+1, the bottom rows layer P-1, the top rows layer 0), so
+// the product runs per row block over its nonzero column range only.
+void launch_bnd_residual(const BndArgs& a, const double* X, int G, int R, bool accumulate, cudaStream_t st) {
+    const int d = a.d, P = a.p.n_layers;
+    struct Seg {
+        int r0, nr, c0, nc;
+    };
+    std::vector<Seg> segs;
+    auto layer_cols = [&](int p) { return p == 0 ? G - 2 * d : 2 * d * (p - 1); };
+    if (P == 1) {
+        segs.push_back({0, G, 0, G});
+    } else {
+        for (int p = 0; p + 1 < P; ++p) {  // interface p: layers p, p+1
+            const int c0 = layer_cols(p), c1 = layer_cols(p + 1);
+            if (c1 == c0 + 2 * d)
+                segs.push_back({2 * d * p, 2 * d, c0, 4 * d});
+            else if (P == 2)
+                segs.push_back({2 * d * p, 2 * d, 0, G});
+            else {
+                segs.push_back({2 * d * p, 2 * d, c0, 2 * d});
+                segs.push_back({2 * d * p, 2 * d, c1, 2 * d});
+            }
+        }
+        segs.push_back({2 * d * (P - 1), d, layer_cols(P - 1), 2 * d});  // bottom
+        segs.push_back({G - d, d, layer_cols(0), 2 * d});                // top
+    }
+    std::vector<int> seen(G, 0);
+    for (const Seg& q : segs) {
+        GemmBatch g{};
+        g.m = R;
+        g.n = q.nr;
+        g.k = q.nc;
+        g.a = X + (size_t)q.c0 * R;
+        g.lda = R;
+        g.stride_a = (long long)G * R;
+        g.b = a.lhs0 + (size_t)q.r0 * a.ldl + q.c0;
+        g.ldb = a.ldl;
+        g.stride_b = a.sl;
+        g.c = a.lhs0 + G + (size_t)q.r0 * a.ldl;
+        g.ldc = a.ldl;
+        g.stride_c = a.sl;
+        g.batch = a.p.n_orders;
+        g.alpha = 1.0;
+        g.beta = (accumulate || seen[q.r0]) ? 1.0 : -1.0;  // subtract b once per row
+        seen[q.r0] = 1;
+        gemm_batched(g, st);
+    }
+}
+
+void launch_bnd_check(const BndArgs& a, const double* X, int G, int R, int stage, DeviceStatus* status,
+                      cudaStream_t st) {
+    bnd_check_kernel<<<dim3((R + 127) / 128, a.p.n_orders), 128, 0, st>>>(a, X, G, R, stage, status);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_bnd_refine_rhs(const BndArgs& a, const int* perm, double* dX, int G, int R, cudaStream_t st) {
+    const long long total = (long long)a.p.n_orders * G * R;
+    bnd_refine_rhs_kernel<<<(unsigned)std::min(16384LL, (total + 255) / 256), 256, 0, st>>>(a, perm, dX, G, R);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_bnd_add(double* X, const double* dX, long long n, cudaStream_t st) {
+    add_kernel<<<(unsigned)std::min(16384LL, (n + 255) / 256), 256, 0, st>>>(X, dX, n);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
 
 void launch_bnd_assemble(const BndArgs& a, cudaStream_t st) {
     const int d = a.d, P = a.p.n_layers, G = 2 * d * P;

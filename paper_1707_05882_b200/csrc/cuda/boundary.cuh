@@ -20,7 +20,26 @@ struct BndArgs {
     int ldl, ldr;
     long long sl, sr;     // per-order strides of lhs and rhs
     double* up;           // [mo][R][d]
+    // residual gate (boundary.cpp:233-257): an untouched copy of [A | B] (same
+    // row-major layout as lhs, never factored) and per-order / per-column norms
+    double* lhs0;         // [mo] G x ldl, or null (no gate)
+    double* anorm;        // [mo][2]: max |A_ij|, ||A||_1
+    double* bnorm;        // [mo][R][2]: max |b_i|, ||b||_1
+    double* condm;        // [mo]: lower bound of cond_1(A), max over the right-hand sides
 };
+
+// The gate after the back substitution: the relative residual of every
+// right-hand side, |A x - b|_max / (|A|_max |x|_max + |b|_max); residual = lhs0's
+// B columns after bnd_residual_gemm.  stage 0: flags columns above 1e-10 for the
+// one refinement step (DeviceStatus::bnd_refine) and fails on non-finite
+// solutions; stage 1 (after refinement, or when nothing was refined): fails
+// above 1e-9 (boundary.cpp:249-254).
+void launch_bnd_norms(const BndArgs& a, int G, int R, cudaStream_t st);
+void launch_bnd_residual(const BndArgs& a, const double* X, int G, int R, bool accumulate, cudaStream_t st);
+void launch_bnd_check(const BndArgs& a, const double* X, int G, int R, int stage, DeviceStatus* status,
+                      cudaStream_t st);
+void launch_bnd_refine_rhs(const BndArgs& a, const int* perm, double* dX, int G, int R, cudaStream_t st);
+void launch_bnd_add(double* X, const double* dX, long long n, cudaStream_t st);
 
 void launch_bnd_assemble(const BndArgs& a, cudaStream_t st);
 void launch_bnd_rhs(const BndArgs& a, cudaStream_t st);
@@ -61,6 +80,11 @@ __host__ __device__ inline int bnd_row_end(int col, int d, int P) {
     const int p = b + 1;
     return (p <= P - 2) ? 2 * d * (p + 1) : 2 * d * (P - 1) + d;
 }
+// Forward + backward substitution in place on right-hand sides already gathered
+// through the row map (row i of X = row perm[i] of B): X <- A^-1 B, A factored
+// by lu_factor_rm with row stride lda.
+void lu_solve_gathered(const double* A, int G, int lda, int batch, const int* perm, double* X, int ncol,
+                       cudaStream_t st);
 int lu_rm_launch_count(int G);
 int lu_aug_launch_count(int G, int R, int row_lo);
 

@@ -20,6 +20,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <type_traits>
 #include <vector>
 
@@ -124,8 +125,15 @@ struct vrte_cuda_plan {
     // boundary
     DevBuf<double> lhs, top0, rhs_b, rhs_x, up;
     DevBuf<int> ipiv, perm;
+    // boundary residual gate (boundary.cpp:233-257)
+    DevBuf<double> lhs0, anorm, bnorm, condm, dX;
+    const double* lhs0_zeroed = nullptr;
+    int* refine_host = nullptr;  // page-locked copy of DeviceStatus::bnd_refine
     // synthesis
     DevBuf<double> out;
+    // device-sharded solves: the gathered stacks of every order (root shard only)
+    DevBuf<double> up_all;
+    DevBuf<int> slot_all;
     DeviceStatus* status = nullptr;  // pinned host-mapped would be nicer; device + copy
     DevBuf<DeviceStatus> status_buf;
     cudaEvent_t ev[16] = {};
@@ -141,6 +149,7 @@ struct vrte_cuda_plan {
     uint64_t launches = 0;
     ~vrte_cuda_plan() {
         if (resmax_host) cudaFreeHost(resmax_host);
+        if (refine_host) cudaFreeHost(refine_host);
         if (stage) cudaFreeHost(stage);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
@@ -185,6 +194,7 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     if (const char* pi = std::getenv("VRTE_PART_REFINE_ITERS")) pl.part_refine_iters = std::atoi(pi);
     if (const char* re = std::getenv("VRTE_REFINE_EXTRA")) pl.refine_extra = std::atoi(re);
     if (!pl.resmax_host) VRTE_CUDA_CHECK(cudaMallocHost(&pl.resmax_host, sizeof(double)));
+    if (!pl.refine_host) VRTE_CUDA_CHECK(cudaMallocHost(&pl.refine_host, sizeof(int)));
     pl.resmax.alloc(1);
     pl.N = p->N;
     pl.L = p->L;
@@ -303,6 +313,15 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pl.sigma.alloc((size_t)B * R * 2);
     pl.kind.alloc((size_t)B * R);
     pl.lhs.alloc((size_t)NO * G * (G + R));  // augmented [A | B] per order, row-major
+    pl.lhs0.alloc((size_t)NO * G * (G + R));  // its untouched copy (residual gate)
+    if (pl.lhs0_zeroed != pl.lhs0.p) {       // the zero blocks of the copy are never written
+        VRTE_CUDA_CHECK(cudaMemsetAsync(pl.lhs0.p, 0, sizeof(double) * pl.lhs0.n, st));
+        pl.lhs0_zeroed = pl.lhs0.p;
+    }
+    pl.anorm.alloc((size_t)NO * 2);
+    pl.bnorm.alloc((size_t)NO * R * 2);
+    pl.condm.alloc((size_t)NO);
+    pl.dX.alloc((size_t)NO * G * R);
     pl.top0.alloc((size_t)NO * d * 2 * d);
     pl.rhs_x.alloc((size_t)NO * R * G);
     pl.ipiv.alloc((size_t)NO * G);
@@ -597,6 +616,10 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     ba.sl = ba.sr = (long long)G * (G + R);
     ba.rhs = pl.lhs.p + G;
     ba.up = pl.up.p;
+    ba.lhs0 = pl.lhs0.p;
+    ba.anorm = pl.anorm.p;
+    ba.bnorm = pl.bnorm.p;
+    ba.condm = pl.condm.p;
     launch_bnd_assemble(ba, st);
     // right-hand sides on the side stream once the particular vectors are there; the
     // factorization waits for them only before its first update of those columns
@@ -604,12 +627,37 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     VRTE_CUDA_CHECK(cudaStreamWaitEvent(st2, pl.fork[3], 0));
     launch_bnd_rhs(ba, st2);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.join[3], st2));
+    // matrix norms of the untouched copy, under the factorization
+    launch_bnd_norms(ba, G, R, st2);
+    VRTE_CUDA_CHECK(cudaMemsetAsync(pl.condm.p, 0, sizeof(double) * NO, st2));
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.join[0], st2));
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[11], st));
     lu_factor_rm(pl.lhs.p, G, NO, pl.ipiv.p, pl.perm.p, pl.status, pl.order_index.p, st, d, pl.P, G + R, G + R,
                  pl.join[3]);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[12], st));
-    lu_backsolve_aug(pl.lhs.p, G, G + R, R, NO, pl.perm.p, pl.rhs_x.p, pl.full_solution ? 0 : G - 2 * d, st);
+    lu_backsolve_aug(pl.lhs.p, G, G + R, R, NO, pl.perm.p, pl.rhs_x.p, 0, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[13], st));
+    // residual gate (boundary.cpp:233-257): |A x - b| against 1e-10 scale, one
+    // refinement step for the right-hand sides above it, then 1e-9 scale
+    VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[0], 0));
+    launch_bnd_residual(ba, pl.rhs_x.p, G, R, false, st);
+    launch_bnd_check(ba, pl.rhs_x.p, G, R, 0, pl.status, st);
+    VRTE_CUDA_CHECK(cudaMemcpyAsync(pl.refine_host, &pl.status->bnd_refine, sizeof(int), cudaMemcpyDeviceToHost, st));
+    VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
+    nl += 5;
+    static const bool force_refine = std::getenv("VRTE_BND_FORCE_REFINE") != nullptr;  // experiment
+    if (*pl.refine_host || force_refine) {
+        launch_bnd_refine_rhs(ba, pl.perm.p, pl.dX.p, G, R, st);
+        lu_solve_gathered(pl.lhs.p, G, G + R, NO, pl.perm.p, pl.dX.p, R, st);
+        launch_bnd_add(pl.rhs_x.p, pl.dX.p, (long long)NO * G * R, st);
+        launch_bnd_residual(ba, pl.dX.p, G, R, true, st);
+        VRTE_CUDA_CHECK(cudaMemsetAsync(&pl.status->max_boundary_residual, 0, sizeof(double), st));
+        VRTE_CUDA_CHECK(cudaMemsetAsync(pl.condm.p, 0, sizeof(double) * NO, st));
+        launch_bnd_check(ba, pl.rhs_x.p, G, R, 1, pl.status, st);
+        const int one = 1;
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(&pl.status->bnd_refined, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+        nl += 6 + 4 * ((G + 63) / 64);
+    }
     launch_copy_zp0(ba, st);
     // up += Top0 [A_0; B_0]: layer 0's unknowns are the last 2d rows of the
     // row-major solution (bnd_col), read column-major as their transpose
@@ -617,7 +665,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
                       pl.rhs_x.p + (size_t)(G - 2 * d) * R, R, (long long)G * R, true, pl.up.p, d, dR, NO,
                       1.0, 1.0),
                  st);
-    nl += 2 + (pd.base_type != 0 ? 1 : 0) + lu_aug_launch_count(G, R, pl.full_solution ? 0 : G - 2 * d) + 2;
+    nl += 4 + (pd.base_type != 0 ? 1 : 0) + lu_aug_launch_count(G, R, 0) + 2;
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[3], st));
     // ---------------- synthesis
     if (synth) {
@@ -660,10 +708,19 @@ std::string describe_failure(const DeviceStatus& s, const std::vector<double>& r
                           s.index, s.value);
             break;
         case kFailLuSingular:
-        case kFailBoundary:
             std::snprintf(buf, sizeof buf,
                           "boundary system ill-conditioned at order m = %d (singular pivot at %g)",
                           s.index, s.value);
+            break;
+        case kFailBoundary:  // boundary.cpp:251-253
+            std::snprintf(buf, sizeof buf, "boundary system ill-conditioned at order m = %d (condition ~ %g, residual %g)",
+                          s.index, s.value2, s.value);
+            break;
+        case kFailBalance:  // particular.cpp:101-104
+            std::snprintf(buf, sizeof buf, "beam-response residual %g at order m = %d", s.value, s.index);
+            break;
+        case kFailNonFiniteTable:
+            std::snprintf(buf, sizeof buf, "brdf: non-finite table entry (index %d)", s.index);
             break;
         case kFailNegativeIntensity:
             std::snprintf(buf, sizeof buf, "brdf: negative intensity entry %f", s.value);
@@ -728,7 +785,20 @@ int finish(vrte_cuda_plan& pl, vrte_cuda_result* r) {
         for (int q = 0; q < 8; ++q) r->qr_cycles[q] = s.qr_cycles[q];
         r->max_eigen_residual = maxres;
         r->max_particular_residual = s.max_particular_residual;
+        r->max_balance_residual = s.max_balance_residual;
+        r->max_boundary_residual = s.max_boundary_residual;
+        r->boundary_refined = s.bnd_refined ? 1 : 0;
+        std::vector<double> cm((size_t)pl.NO);
+        VRTE_CUDA_CHECK(cudaMemcpy(cm.data(), pl.condm.p, sizeof(double) * cm.size(), cudaMemcpyDeviceToHost));
+        r->max_boundary_condition = 0.0;
+        r->boundary_cond_warnings = 0;
+        for (double c : cm) {
+            r->max_boundary_condition = std::max(r->max_boundary_condition, c);
+            if (c > 1e14) ++r->boundary_cond_warnings;
+        }
         r->kernel_launches = pl.launches;
+        r->eigen_slots = pl.Be;
+        r->slots = pl.B;
     }
     if (s.code == kFailNegativeIntensity && s.neg_key != 0) {
         const unsigned long long idx = ~s.neg_key;  // first offending entry, reference order
@@ -738,7 +808,7 @@ int finish(vrte_cuda_plan& pl, vrte_cuda_result* r) {
         fill_message(r, 3, describe_failure(s, res, pl.d, oi));
         return 3;
     }
-    if (!(maxres <= kEigenResidualBound) && !std::getenv("VRTE_NO_RESIDUAL_GATE")) {
+    if (!(maxres <= kEigenResidualBound)) {
         char buf[256];
         std::snprintf(buf, sizeof buf, "homogeneous mode residual %g exceeds %g at order m = %d",
                       maxres, kEigenResidualBound, worst >= 0 ? oi[worst] : -1);
@@ -855,15 +925,22 @@ int32_t vrte_cuda_device_count(void) {
     return n;
 }
 
+int32_t vrte_cuda_current_device(void) {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) return 0;
+    return d;
+}
+
 int32_t vrte_cuda_plan_create(const vrte_cuda_problem* problem, vrte_cuda_plan** out,
                               vrte_cuda_result* result) {
     return guarded(result, [&]() -> int32_t {
         if (!out) throw std::invalid_argument("null plan pointer");
+        *out = nullptr;
         auto pl = std::make_unique<vrte_cuda_plan>();
         setup_plan(*pl, problem);
         pl->launches = run_pipeline(*pl, pl->full_orders);
         const int rc = finish(*pl, result);
-        *out = pl.release();
+        if (rc == 0) *out = pl.release();  // a failed plan frees its device buffers here
         return rc;
     });
 }
@@ -948,9 +1025,132 @@ int32_t vrte_cuda_plan_fetch_ef(vrte_cuda_plan* pl, double* E, double* F) {
 
 void vrte_cuda_plan_destroy(vrte_cuda_plan* pl) { delete pl; }
 
+namespace {
+// Order-sharded solve over several devices: shard k runs the
+// orders m = k, k + D, ... on devices[k] (one host thread each: the pipeline
+// has host synchronisation points), the root (shard 0) gathers every shard's
+// tau = 0 stacks with peer copies and runs the synthesis over m = 0..L-1.
+int32_t brdf_sharded(const vrte_cuda_problem* problem, double* table, vrte_cuda_result* result) {
+    const int L = problem->L;
+    const int D = std::min(problem->n_devices, L);
+    std::vector<std::unique_ptr<PlanLease>> leases(D);
+    std::vector<vrte_cuda_result> res(D);
+    std::vector<int> rc(D, 0), count(D), offset(D);
+    std::vector<std::string> err(D);
+    for (int k = 0, off = 0; k < D; ++k) {
+        count[k] = (L - k + D - 1) / D;
+        offset[k] = off;
+        off += count[k];
+    }
+    auto shard = [&](int k) {
+        try {
+            vrte_cuda_problem pk = *problem;
+            pk.device = problem->devices[k];
+            pk.m_begin = k;
+            pk.m_stride = D;
+            pk.n_orders = count[k];
+            pk.n_devices = 1;
+            leases[k] = std::make_unique<PlanLease>(pk.device);
+            vrte_cuda_plan& pl = **leases[k];
+            setup_plan(pl, &pk);
+            pl.full_solution = false;
+            pl.launches = run_pipeline(pl, false);
+            res[k] = vrte_cuda_result{};
+            rc[k] = finish(pl, &res[k]);
+        } catch (const std::invalid_argument& e) {
+            rc[k] = 5;
+            err[k] = e.what();
+        } catch (const std::exception& e) {
+            rc[k] = 3;
+            err[k] = e.what();
+        }
+    };
+    {
+        std::vector<std::thread> th;
+        for (int k = 1; k < D; ++k) th.emplace_back(shard, k);
+        shard(0);
+        for (auto& t : th) t.join();
+    }
+    for (int k = 0; k < D; ++k)
+        if (rc[k] != 0) {
+            if (!err[k].empty()) fill_message(result, rc[k], err[k]);
+            else if (result) *result = res[k];
+            return rc[k];
+        }
+    vrte_cuda_plan& root = **leases[0];
+    VRTE_CUDA_CHECK(cudaSetDevice(root.device));
+    cudaStream_t st = root.st;
+    const size_t per = (size_t)root.R * root.d;  // one order's stacks
+    root.up_all.alloc((size_t)L * per);
+    for (int k = 0; k < D; ++k) {
+        const vrte_cuda_plan& pk = **leases[k];
+        VRTE_CUDA_CHECK(cudaMemcpyPeerAsync(root.up_all.p + offset[k] * per, root.device, pk.up.p, pk.device,
+                                            sizeof(double) * count[k] * per, st));
+    }
+    std::vector<int> slot(L);
+    for (int m = 0; m < L; ++m) slot[m] = offset[m % D] + m / D;
+    root.slot_all.upload(slot.data(), L, st);
+    VRTE_CUDA_CHECK(cudaMemsetAsync(root.status, 0, sizeof(DeviceStatus), st));
+    SynthArgs sa{};
+    sa.N = root.N;
+    sa.L = L;
+    sa.n_in = root.n_in;
+    sa.n_dphi = root.n_dphi;
+    sa.up = root.up_all.p;
+    sa.slot_of_order = root.slot_all.p;
+    sa.trig = root.trig.p;
+    sa.post = root.post.p;
+    sa.out = root.out.p;
+    sa.status = root.status;
+    launch_synth(sa, st);
+    VRTE_CUDA_CHECK(cudaMemcpyAsync(table, root.out.p, sizeof(double) * root.out.n, cudaMemcpyDeviceToHost, st));
+    DeviceStatus s{};
+    VRTE_CUDA_CHECK(cudaMemcpyAsync(&s, root.status, sizeof s, cudaMemcpyDeviceToHost, st));
+    VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (result) {  // stage times: the slowest shard; counters and maxima over the shards
+        vrte_cuda_result r = res[0];
+        for (int k = 1; k < D; ++k) {
+            const vrte_cuda_result& q = res[k];
+            for (double vrte_cuda_result::*f :
+                 {&vrte_cuda_result::t_homogeneous, &vrte_cuda_result::t_particular, &vrte_cuda_result::t_boundary,
+                  &vrte_cuda_result::t_device, &vrte_cuda_result::t_hessenberg, &vrte_cuda_result::t_hqr,
+                  &vrte_cuda_result::t_trevc, &vrte_cuda_result::t_refine, &vrte_cuda_result::t_lu_factor,
+                  &vrte_cuda_result::t_lu_solve, &vrte_cuda_result::max_eigen_residual,
+                  &vrte_cuda_result::max_particular_residual, &vrte_cuda_result::max_balance_residual,
+                  &vrte_cuda_result::max_boundary_residual, &vrte_cuda_result::max_boundary_condition})
+                r.*f = std::max(r.*f, q.*f);
+            for (uint64_t vrte_cuda_result::*f :
+                 {&vrte_cuda_result::dithered, &vrte_cuda_result::polished, &vrte_cuda_result::kernel_launches,
+                  &vrte_cuda_result::qr_sweeps, &vrte_cuda_result::qr_steps, &vrte_cuda_result::boundary_refined,
+                  &vrte_cuda_result::boundary_cond_warnings, &vrte_cuda_result::eigen_slots,
+                  &vrte_cuda_result::slots})
+                r.*f += q.*f;
+        }
+        r.clamped = s.clamped;
+        r.kernel_launches += 1;
+        *result = r;
+    }
+    if (s.code == kFailNegativeIntensity && s.neg_key != 0) {
+        const unsigned long long idx = ~s.neg_key;
+        VRTE_CUDA_CHECK(cudaMemcpy(&s.value, root.out.p + idx * 16, sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    if (s.code != 0) {
+        fill_message(result, 3, describe_failure(s, {}, 0, {}));
+        return 3;
+    }
+    if (result) {
+        result->status = 0;
+        result->message[0] = 0;
+    }
+    return 0;
+}
+}  // namespace
+
 int32_t vrte_cuda_brdf(const vrte_cuda_problem* problem, double* table, vrte_cuda_result* result) {
     return guarded(result, [&]() -> int32_t {
         if (!table) throw std::invalid_argument("null table");
+        if (problem && problem->n_devices > 1 && problem->devices && problem->n_orders <= 0)
+            return brdf_sharded(problem, table, result);
         // A leased plan (device buffers + stream): the entry point is reentrant
         // (vrte.h "every entry point is reentrant") and concurrent callers run
         // concurrently on their own streams; shape changes reallocate.

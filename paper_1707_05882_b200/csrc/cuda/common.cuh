@@ -21,6 +21,18 @@ constexpr double kEigenResidualBound = 1e-9;  // homogeneous.hpp:71
 constexpr double kUlp = 2.220446049250313e-16;      // dlamch('P')
 constexpr double kSafeMin = 2.2250738585072014e-308; // dlamch('S')
 
+// cudaFuncSetAttribute is per device: set a kernel's dynamic shared-memory
+// limit once per (kernel, device) -- `mask` is the call site's static bitmask.
+template <typename K>
+inline void smem_attr_once(K kernel, int bytes, unsigned long long& mask) {
+    int dev = 0;
+    VRTE_CUDA_CHECK(cudaGetDevice(&dev));
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (__atomic_load_n(&mask, __ATOMIC_ACQUIRE) & bit) return;
+    VRTE_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    __atomic_fetch_or(&mask, bit, __ATOMIC_ACQ_REL);
+}
+
 // Device-side failure record: the first failing (code, stage, index) wins
 // and the host turns it into a NumericalError with the reference's wording.
 struct DeviceStatus {
@@ -36,6 +48,11 @@ struct DeviceStatus {
     double max_eigen_residual;
     double max_particular_residual;
     double max_boundary_residual;
+    double max_boundary_condition;    // lower-bound estimate of cond_1 of the boundary matrices
+    unsigned long long bnd_cond_warnings;  // orders above 1e14 (boundary.cpp:259-263 warns)
+    int bnd_refine;                   // a right-hand side needs the refinement step
+    int bnd_refined;                  // ... and it was taken
+    double max_balance_residual;      // particular 8N balance residual (particular.cpp:86-105)
     unsigned long long qr_sweeps;
     unsigned long long qr_steps;
     unsigned long long qr_cycles[8];  // debug phase timers (clock64 in thread 0)
@@ -52,6 +69,8 @@ enum FailKind {
     kFailBoundary = 6,
     kFailNegativeIntensity = 7,
     kFailLuSingular = 8,
+    kFailBalance = 9,
+    kFailNonFiniteTable = 10,
 };
 
 __device__ inline void report_failure(DeviceStatus* st, int code, int stage, int index, double v,

@@ -2903,12 +2903,8 @@ void launch_hessenberg(double* A, double* Z, int d, int batch, cudaStream_t st) 
 void launch_hqr(double* H, double* Z, double* wr, double* wi, int d, int batch,
                 DeviceStatus* status, cudaStream_t st) {
     const size_t smem = (size_t)(BW + 4) * d * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        VRTE_CUDA_CHECK(cudaFuncSetAttribute(hqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             200 * 1024));
-        attr = true;
-    }
+    static unsigned long long attr = 0;
+    smem_attr_once(hqr_kernel, 200 * 1024, attr);
     static const char* mode = std::getenv("VRTE_HQR");  // multi (default) | window | band
     if (!mode || std::string(mode) == "multi") {
         static const int aed_nw = std::getenv("VRTE_AED_NW") ? std::atoi(std::getenv("VRTE_AED_NW")) : AED_NW;
@@ -2950,12 +2946,8 @@ void launch_trevc(const double* T, const double* wr, const double* wi, double* Y
                   int batch, cudaStream_t st) {
     const int warps = 8;
     const size_t smem = (size_t)warps * 2 * d * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        VRTE_CUDA_CHECK(cudaFuncSetAttribute(trevc_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
-    }
+    static unsigned long long attr = 0;
+    smem_attr_once(trevc_kernel, 200 * 1024, attr);
     static const char* tmode = std::getenv("VRTE_TREVC");  // reg (default) | smem
     if (tmode && std::string(tmode) == "smem") {
         trevc_kernel<<<batch, warps * 32, smem, st>>>(T, wr, wi, Y, d);
@@ -3006,12 +2998,8 @@ void launch_qtri_solve(const double* T, int d, long long t_stride, double* W, in
                        long long w_stride, const double* sigma, const int* kind, int batch,
                        const int* t_index, cudaStream_t st) {
     const size_t smem = ((size_t)d * (QCT + 1) + (size_t)(QBS + 1) * (QBS + 1)) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        VRTE_CUDA_CHECK(cudaFuncSetAttribute(qtri_blocked_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
-    }
+    static unsigned long long attr = 0;
+    smem_attr_once(qtri_blocked_kernel, 200 * 1024, attr);
     const int tiles = (ncol + QCT - 1) / QCT;
     qtri_blocked_kernel<<<(unsigned)(batch * tiles), 256, smem, st>>>(T, d, t_stride, W, ncol, w_stride,
                                                                      sigma, kind, t_index);

@@ -216,14 +216,14 @@ __global__ void __launch_bounds__(2 * BN, MINB) dmma_gemm_kernel(GemmBatch g) {
 
 template <bool TA, bool TB, int BK, int ST, int MINB, int BN, bool MAP = false>
 void launch(const GemmBatch& g, cudaStream_t stream) {
-    static bool attr = false;
+    static unsigned long long attr = 0;  // per-device bitmask (smem_attr_once)
     constexpr size_t smem = (size_t)ST * (Geo<BK, BN>::A_STAGE + Geo<BK, BN>::B_STAGE) * sizeof(double);
-    if (!attr) {
-        VRTE_CUDA_CHECK(cudaFuncSetAttribute(dmma_gemm_kernel<TA, TB, BK, ST, MINB, BN, MAP>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0;
+    VRTE_CUDA_CHECK(cudaGetDevice(&dev));
+    if (!(__atomic_load_n(&attr, __ATOMIC_ACQUIRE) & (1ull << (dev & 63)))) {
         VRTE_CUDA_CHECK(cudaFuncSetAttribute(dmma_gemm_kernel<TA, TB, BK, ST, MINB, BN, MAP>,
                                              cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        attr = true;
+        smem_attr_once(dmma_gemm_kernel<TA, TB, BK, ST, MINB, BN, MAP>, (int)smem, attr);
     }
     dim3 grid((g.m + BM - 1) / BM, (g.n + BN - 1) / BN, g.batch);
     dmma_gemm_kernel<TA, TB, BK, ST, MINB, BN, MAP><<<grid, 2 * BN, smem, stream>>>(g);

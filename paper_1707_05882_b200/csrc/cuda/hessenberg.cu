@@ -231,12 +231,8 @@ void launch_hessenberg_blocked(double* A, double* Z, double* work, int d, int ba
     const size_t smem =
         (2 * (size_t)d * nbmax + nbmax * nbmax + d + (d > HNT ? d : HNT) + 2 * nbmax + 32) *
         sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        VRTE_CUDA_CHECK(cudaFuncSetAttribute(hess_panel_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        attr = true;
-    }
+    static unsigned long long attr = 0;
+    smem_attr_once(hess_panel_kernel, 220 * 1024, attr);
     // (the panel kernel writes every row of each V / VT column it owns, zeros
     // included, so the Q-formation GEMMs need no cleared buffers)
     int npanel = 0;

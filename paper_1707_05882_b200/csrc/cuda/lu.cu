@@ -535,12 +535,8 @@ template <int NT, int RPT, int PB>
 void panel_launch(double* A, int G, int lda, int* map, int* ipiv, int K0, int k0, int jb, int rend,
                   DeviceStatus* status, const int* order_index, int batch, cudaStream_t st) {
     constexpr size_t smem = PanelGeo<NT, RPT, PB>::bytes;
-    static bool attr = false;
-    if (!attr) {
-        VRTE_CUDA_CHECK(cudaFuncSetAttribute(lu_panel_crout_kernel<NT, RPT, PB>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    static unsigned long long attr = 0;
+    smem_attr_once(lu_panel_crout_kernel<NT, RPT, PB>, (int)smem, attr);
     lu_panel_crout_kernel<NT, RPT, PB><<<batch, NT, smem, st>>>(A, G, lda, (long long)G * lda, map, ipiv, K0, k0,
                                                                 jb, rend, status, order_index);
     VRTE_CUDA_CHECK(cudaGetLastError());
@@ -671,9 +667,20 @@ void lu_backsolve_aug(double* A, int G, int lda, int R, int batch, const int* pe
     const long long gg = (long long)G * lda;
     const int nblk = (G + LU_NB - 1) / LU_NB;
     const int blo = max(0, row_lo) / LU_NB, rl = blo * LU_NB;
-    for (int bk = nblk - 1; bk >= blo; --bk) {
-        const int k0 = bk * LU_NB, jb = min(LU_NB, G - k0);
-        trsm_launch<false>(A, G, lda, A + G, lda, gg, k0, jb, 0, R, batch, st, perm, perm);
+    // outer blocks of 2 x 64 rows: the two triangular solves with the 64 x 64
+    // coupling update between them, then ONE update of every row above with
+    // k = 128 (the long-k GEMM runs near the DMMA rate; k = 64 does not)
+    for (int bk = nblk - 1; bk >= blo; bk -= 2) {
+        const int k1 = bk * LU_NB, jb1 = min(LU_NB, G - k1);
+        trsm_launch<false>(A, G, lda, A + G, lda, gg, k1, jb1, 0, R, batch, st, perm, perm);
+        int k0 = k1, jb = jb1;
+        if (bk - 1 >= blo) {
+            k0 = k1 - LU_NB;
+            rm_gemm(LU_NB, R, jb1, A + k1, lda, gg, A + G, lda, gg, A + G, lda, gg, batch, -1.0, 1.0, st, perm + k0,
+                    perm + k1, perm + k0, G);
+            trsm_launch<false>(A, G, lda, A + G, lda, gg, k0, LU_NB, 0, R, batch, st, perm, perm);
+            jb = LU_NB + jb1;
+        }
         if (k0 > rl)
             rm_gemm(k0 - rl, R, jb, A + k0, lda, gg, A + G, lda, gg, A + G, lda, gg, batch, -1.0, 1.0, st, perm + rl,
                     perm + k0, perm + rl, G);
@@ -717,6 +724,26 @@ void lu_solve_rm(const double* A, int G, int batch, const int* perm, const doubl
     }
 }
 
+void lu_solve_gathered(const double* A, int G, int lda, int batch, const int* perm, double* X, int ncol,
+                       cudaStream_t st) {
+    const long long gg = (long long)G * lda, gn = (long long)G * ncol;
+    for (int k0 = 0; k0 < G; k0 += LU_NB) {
+        const int jb = min(LU_NB, G - k0);
+        trsm_launch<true>(A, G, lda, X, ncol, gn, k0, jb, 0, ncol, batch, st, perm, nullptr);
+        if (G - k0 - jb > 0)
+            rm_gemm(G - k0 - jb, ncol, jb, A + k0, lda, gg, X + (size_t)k0 * ncol, ncol, gn,
+                    X + (size_t)(k0 + jb) * ncol, ncol, gn, batch, -1.0, 1.0, st, perm + k0 + jb, nullptr, nullptr, G);
+    }
+    const int nblk = (G + LU_NB - 1) / LU_NB;
+    for (int bk = nblk - 1; bk >= 0; --bk) {
+        const int k0 = bk * LU_NB, jb = min(LU_NB, G - k0);
+        trsm_launch<false>(A, G, lda, X, ncol, gn, k0, jb, 0, ncol, batch, st, perm, nullptr);
+        if (k0 > 0)
+            rm_gemm(k0, ncol, jb, A + k0, lda, gg, X + (size_t)k0 * ncol, ncol, gn, X, ncol, gn, batch, -1.0, 1.0, st,
+                    perm, nullptr, nullptr, G);
+    }
+}
+
 int lu_aug_launch_count(int G, int R, int row_lo) {
     const int PB = panel_width(G), OB = outer_block();
     int n = 1;  // row map init
@@ -726,7 +753,8 @@ int lu_aug_launch_count(int G, int R, int row_lo) {
         if (G + R - K0 - NBk > 0) n += 2 * ((NBk + LU_NB - 1) / LU_NB) - 1 + 1;
     }
     const int nblk = (G + LU_NB - 1) / LU_NB, blo = max(0, row_lo) / LU_NB;
-    n += 2 * (nblk - blo) - 1 + 1;  // backward TRSM + GEMM per block, gather
+    for (int bk = nblk - 1; bk >= blo; bk -= 2) n += (bk - 1 >= blo ? 3 : 1) + (bk - 1 > blo ? 1 : 0);
+    n += 1;  // gather
     return n;
 }
 

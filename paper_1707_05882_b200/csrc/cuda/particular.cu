@@ -80,28 +80,51 @@ __global__ void part_residual_kernel(PartArgs a) {
     if (gw >= a.batch * R) return;
     const int om = gw / R, col = gw % R;
     const double sg = a.sigma[2 * ((size_t)om * R + col)];
+    const double mu = a.mu_eff[(size_t)om * a.n_in + col / 4];
     const size_t base = ((size_t)om * R + col) * d;
-    double rmax = 0.0, bmax = 0.0, gmax = 0.0;
+    double rmax = 0.0, bmax = 0.0, gmax = 0.0, balmax = 0.0, xmax = 0.0;
     bool finite = true;
     for (int i = lane; i < d; i += 32) {
-        const double g = a.g[base + i];
-        const double r = a.feg[base + i] - sg * g - a.rhs[base + i];
+        const double g = a.g[base + i], sp = a.sp[base + i], sm = a.sm[base + i];
+        const double eg = a.eg[base + i], feg = a.feg[base + i], rhs = a.rhs[base + i];
+        const double r = feg - sg * g - rhs;
         finite = finite && isfinite(g);
         rmax = fmax(rmax, fabs(r));
-        bmax = fmax(bmax, fabs(a.rhs[base + i]));
+        bmax = fmax(bmax, fabs(rhs));
         gmax = fmax(gmax, fabs(g));
+        // unreduced balance M^-1 x - z/mu0 + Op z (particular.cpp:86-99), the 8N
+        // operator applied through E and F: with F h = mu0 (F s+ - F E g) and
+        // F s+ = rhs + s-/mu0, its upper half and the D-flipped lower half are
+        //   (x+ - (E g + F h)/2)/m - psi+/mu0,  (D x- - (E g - F h)/2)/m + psi-/mu0
+        const double inv_m = 1.0 / a.mdiag[i];
+        const double fh = mu * rhs + sm - mu * feg;
+        const double xp = 0.5 * (sp + sm), dxm = 0.5 * (sp - sm);
+        const double psip = a.zp[base + i];
+        const double psim = ((i & 3) >= 2) ? -a.zm[base + i] : a.zm[base + i];
+        const double up = (xp - 0.5 * (eg + fh)) * inv_m - psip / mu;
+        const double lo = (dxm - 0.5 * (eg - fh)) * inv_m + psim / mu;
+        balmax = fmax(balmax, fmax(fabs(up), fabs(lo)));
+        xmax = fmax(xmax, fmax(fabs(xp), fabs(dxm)) * inv_m);
     }
     rmax = warp_max(rmax);
     bmax = warp_max(bmax);
     gmax = warp_max(gmax);
+    balmax = warp_max(balmax);
+    xmax = warp_max(xmax);
     finite = __all_sync(0xffffffffu, finite);
     if (lane == 0) {
+        const int m = a.order_index ? a.order_index[om] : om;
         const double scale = bmax + (a.femax[om] + sg) * gmax;
         const double rel = scale > 0.0 ? rmax / scale : 0.0;
         atomic_max_double(&a.status->max_particular_residual, rel);
         if (!finite || rmax > 1e-8 * fmax(scale, 1e-300))
-            report_failure(a.status, kFailParticular, 2, a.order_index ? a.order_index[om] : om,
-                           a.mu_in[col / 4], rel);
+            report_failure(a.status, kFailParticular, 2, m, a.mu_in[col / 4], rel);
+        // a zero source skips the solve and its checks (particular.cpp:39-41)
+        if (xmax > 0.0) {
+            const double bal = balmax / xmax;
+            atomic_max_double(&a.status->max_balance_residual, bal);
+            if (!(bal <= 1e-6)) report_failure(a.status, kFailBalance, 2, m, bal);
+        }
     }
 }
 

@@ -50,7 +50,13 @@ __global__ void synth_kernel(SynthArgs a) {
             for (int k = 0; k < 4; ++k) s += e[r][k] * Tm[4 * k + c];
             f[4 * r + c] = s;
         }
-    if (f[0] < -1e-9) {
+    bool finite = true;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) finite = finite && isfinite(f[k]);
+    if (!finite) {
+        // a non-finite entry never leaves with VRTE_OK (the boundary gate normally stops it first)
+        report_failure(a.status, kFailNonFiniteTable, 4, (int)idx, f[0]);
+    } else if (f[0] < -1e-9) {
         // brdf.cpp:108-112 throws at the FIRST such entry in (incident, exit,
         // azimuth) order: keep the value and record the smallest index
         atomicMax(&a.status->neg_key, ~(unsigned long long)idx);

@@ -107,13 +107,46 @@ void inv4(const double in[16], double out[16]) {
         for (int c = 0; c < 4; ++c) out[4 * r + c] = a[r][c + 4];
 }
 
+// VRTE_DEVICE: CUDA ordinal of single-device calls (-1 = the caller's current device).
+int env_device() {
+    const char* dev = std::getenv("VRTE_DEVICE");
+    return dev ? std::atoi(dev) : -1;
+}
+
+// VRTE_DEVICES: comma-separated ordinals, or "all" visible devices.
+std::vector<int> env_devices() {
+    std::vector<int> out;
+    const char* e = std::getenv("VRTE_DEVICES");
+    if (!e || !*e) return out;
+    if (std::string(e) == "all") {
+        for (int k = 0; k < vrte_cuda_device_count(); ++k) out.push_back(k);
+        return out;
+    }
+    std::string cur;
+    for (const char* c = e;; ++c) {
+        if (*c == ',' || *c == 0) {
+            if (!cur.empty()) {
+                char* end = nullptr;
+                const long v = std::strtol(cur.c_str(), &end, 10);
+                if (!end || *end || v < 0) throw ValidationError("VRTE_DEVICES: bad device ordinal '" + cur + "'");
+                out.push_back((int)v);
+            }
+            cur.clear();
+            if (*c == 0) break;
+        } else if (*c != ' ') {
+            cur += *c;
+        }
+    }
+    return out;
+}
+
 // Host-side set-up of one BRDF request (brdf.cpp:43-77, pipeline.cpp:27-55):
 // validated inputs flattened into the device problem description.
 struct BrdfSetup {
     MaterialSpec spec;
     Quadrature quad;
     int L = 0;
-    std::vector<int> medium, rep;
+    std::vector<int> medium, rep, devices;
     std::vector<double> omega, greek, tau, mu_in, beam_rows, post, trig, table_flat, dphi;
     double basis[16];
     vrte_cuda_problem prob{};
@@ -259,8 +292,14 @@ void build_setup(BrdfSetup& s, const MaterialSpec& mat, const vrte_options* opti
     p.m_begin = 0;
     p.m_stride = 1;
     p.n_orders = 0;
-    const char* dev = std::getenv("VRTE_DEVICE");
-    p.device = dev ? std::atoi(dev) : -1;
+    p.device = env_device();
+    // VRTE_DEVICES="0,1,..." (or "all"): shard the orders of one solve over these
+    // devices (vrte_options is caller-allocated ABI and keeps its layout)
+    s.devices = env_devices();
+    if (s.devices.size() > 1) {
+        p.devices = s.devices.data();
+        p.n_devices = (int32_t)s.devices.size();
+    }
 }
 
 }  // namespace
@@ -508,8 +547,7 @@ vrte_status vrte_mc_trace(const vrte_material* material, const vrte_options* opt
             mc.table = table_flat.data();
             mc.table_nodes = table_nodes.data();
         }
-        const char* dev = std::getenv("VRTE_DEVICE");
-        mc.device = dev ? std::atoi(dev) : -1;
+        mc.device = env_device();
         const size_t bins = 2 * (size_t)zenith_bins * azimuth_bins;
         h->sum.assign(bins * 4, 0.0);
         h->sum_sq.assign(bins * 4, 0.0);
@@ -605,15 +643,24 @@ vrte_status vrte_mc_tally_hits(const vrte_mc_tally* tally, int32_t hemisphere, i
 }
 
 // ---------------------------------------------------------------- BRDF
-vrte_status vrte_compute_brdf(const vrte_material* material, const vrte_options* options,
-                              const double* mu_in, size_t n_mu_in, int32_t n_dphi,
-                              const double* basis, vrte_brdf** out) {
+}  // extern "C"
+
+namespace {
+// vrte_compute_brdf with an explicit device (>= -1; -2 = from the environment,
+// order-sharded over VRTE_DEVICES when it lists several).
+vrte_status compute_brdf_on(const vrte_material* material, const vrte_options* options, const double* mu_in,
+                            size_t n_mu_in, int32_t n_dphi, const double* basis, int device, vrte_brdf** out) {
     if (!material || !out || !mu_in || n_mu_in == 0) return set_error(VRTE_E_ARGUMENT, "null argument");
     return guarded([&] {
         const double t0 = wall_now();
         auto h = std::make_unique<vrte_brdf>();
         BrdfSetup s;
         build_setup(s, material->spec, options, mu_in, n_mu_in, n_dphi, basis);
+        if (device >= -1) {
+            s.prob.device = device;
+            s.prob.devices = nullptr;
+            s.prob.n_devices = 0;
+        }
         const int N = s.quad.n, np = s.prob.n_dphi;
         BrdfTable& t = h->table;
         t.mu_in = s.mu_in;
@@ -647,11 +694,25 @@ vrte_status vrte_compute_brdf(const vrte_material* material, const vrte_options*
         h->stats.kernel_launches = r.kernel_launches;
         h->stats.max_eigen_residual = r.max_eigen_residual;
         h->stats.max_particular_residual = r.max_particular_residual;
+        h->stats.max_balance_residual = r.max_balance_residual;
+        h->stats.max_boundary_residual = r.max_boundary_residual;
+        h->stats.max_boundary_condition = r.max_boundary_condition;
+        h->stats.boundary_refined = r.boundary_refined;
+        h->stats.boundary_cond_warnings = r.boundary_cond_warnings;
         h->stats.material_hash = t.material_hash;
         h->timings.total_wall = wall_now() - t0;
         *out = h.release();
         return VRTE_OK;
     });
+}
+}  // namespace
+
+extern "C" {
+
+vrte_status vrte_compute_brdf(const vrte_material* material, const vrte_options* options,
+                              const double* mu_in, size_t n_mu_in, int32_t n_dphi,
+                              const double* basis, vrte_brdf** out) {
+    return compute_brdf_on(material, options, mu_in, n_mu_in, n_dphi, basis, -2, out);
 }
 
 vrte_status vrte_compute_brdf_batch(const vrte_material* const* materials, size_t count,
@@ -660,7 +721,23 @@ vrte_status vrte_compute_brdf_batch(const vrte_material* const* materials, size_
                                     vrte_brdf** out) {
     if (!materials || !out || !mu_in || n_mu_in == 0) return set_error(VRTE_E_ARGUMENT, "null argument");
     for (size_t i = 0; i < count; ++i) out[i] = nullptr;
-    const size_t nthreads = std::min<size_t>(count, concurrency > 0 ? (size_t)concurrency : 2);
+    // Band sharding: request i runs on devices[i % D] of
+    // VRTE_DEVICES (whole bands, no order sharding inside a band); without it,
+    // every request runs on the caller's device, resolved here on the calling
+    // thread (the workers are fresh threads whose current device is 0).
+    std::vector<int> devs;
+    try {
+        devs = env_devices();
+    } catch (const std::exception& e) {
+        return set_error(VRTE_E_VALIDATION, e.what());
+    }
+    if (devs.empty()) {
+        int d = env_device();
+        if (d < 0 && vrte_cuda_device_count() > 0) d = vrte_cuda_current_device();
+        devs.push_back(d);
+    }
+    const size_t per_dev = concurrency > 0 ? (size_t)concurrency : 2;
+    const size_t nthreads = std::min<size_t>(count, per_dev * devs.size());
     std::atomic<size_t> next{0};
     std::mutex mtx;
     vrte_status first = VRTE_OK;
@@ -669,9 +746,9 @@ vrte_status vrte_compute_brdf_batch(const vrte_material* const* materials, size_
     auto worker = [&] {
         for (size_t i = next++; i < count; i = next++) {
             vrte_brdf* h = nullptr;
-            const vrte_status rc = materials[i]
-                                       ? vrte_compute_brdf(materials[i], options, mu_in, n_mu_in, n_dphi, basis, &h)
-                                       : set_error(VRTE_E_ARGUMENT, "null material");
+            const vrte_status rc = materials[i] ? compute_brdf_on(materials[i], options, mu_in, n_mu_in, n_dphi,
+                                                                  basis, devs[i % devs.size()], &h)
+                                                : set_error(VRTE_E_ARGUMENT, "null material");
             if (rc == VRTE_OK) {
                 out[i] = h;
             } else {

@@ -60,11 +60,17 @@ def sharded_brdf(material, opts, mu_in, n_dphi=19, basis=None, world=None, rank=
     rank = dist.get_rank() if rank is None else rank
     L = material.info()[0] if opts.order_cap <= 0 else min(material.info()[0], opts.order_cap)
     m_begin, m_stride, n_orders = order_shard(L, world, rank)
-    plan = V.Plan(material, opts, mu_in, n_dphi, basis, device=local_device, m_begin=m_begin,
-                  m_stride=m_stride, n_orders=n_orders)
-    local = plan.up().reshape(n_orders, -1)
+    if n_orders == 0:
+        # more ranks than orders: this rank holds no order but still joins the
+        # collective (a plan with n_orders = 0 would mean "all orders")
+        N = opts.quadrature_n
+        local = np.zeros((0, len(mu_in) * 4 * 4 * N))
+    else:
+        plan = V.Plan(material, opts, mu_in, n_dphi, basis, device=local_device, m_begin=m_begin,
+                      m_stride=m_stride, n_orders=n_orders)
+        local = plan.up().reshape(n_orders, -1)
+        plan.close()
     full = gather_orders(local, L, world, rank, device=device)
-    plan.close()
     if rank != 0:
         return None
     return V.brdf_from_stacks(material, opts, mu_in, n_dphi, basis, full)

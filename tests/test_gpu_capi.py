@@ -73,11 +73,23 @@ def test_order_cap_truncates_orders():
     assert np.abs(b.table() - r).max() < 1e-10 * np.abs(r).max()
 
 
-def test_negative_intensity_is_reported_not_clamped_silently():
-    mat = product_material(M.single_layer(M.RAYLEIGH, 0.8, 1.0, "lambertian", 0.1))
-    b = V.compute_brdf(mat, V.options(6), [0.7], 6)
+def test_f00_roundoff_clamp_counts_like_the_reference():
+    """brdf.cpp:106-117: F00 in [-1e-9, 0) is clamped to 0 and counted; the
+    count matches the oracle's on a case that has such entries: a forward-peaked
+    G(0.9, 24) phase matrix under-resolved at N = 6 has negative F00 lobes, and
+    omega = 1e-10 scales them into the clamp window (90 entries)."""
+    from helpers import oracle_material
+    desc = M.single_layer(M.generator_G(0.9, 24), 1e-10, 1.0)
+    nodes, _ = O.quadrature(6)
+    b = V.compute_brdf(product_material(desc), V.options(6), nodes, 6)
     assert np.all(b.table()[..., 0, 0] >= 0)
-    assert b.device_stats()["clamped"] >= 0
+    _, tm = O.brdf(oracle_material(desc), 6, nodes, 6)
+    assert tm["clamped_entries"] == 90
+    assert b.device_stats()["clamped"] == tm["clamped_entries"]
+    # ten times larger lobes leave the window: the reference's error, same text
+    with pytest.raises(V.VrteError) as ei:
+        V.compute_brdf(product_material(M.single_layer(M.generator_G(0.9, 24), 1e-6, 1.0)), V.options(6), nodes, 6)
+    assert ei.value.code == 3 and ei.value.message.startswith("brdf: negative intensity entry -0.000000")
 
 
 def test_spectral_batch_matches_individual_solves():
