@@ -599,8 +599,9 @@ def main():
             # sides (L^-1 P B: G^2 R flops) besides the (2/3) G^3 of the LU proper
             "boundary LU factor (augmented: Crout panels + TRSM + DMMA GEMM)":
                 (res["t_lu_factor"], L * ((2.0 / 3.0) * G ** 3 + G ** 2 * R)),
-            # back substitution U x = y for all R columns (full: the residual gate needs every unknown)
-            "boundary back substitution (TRSM + DMMA GEMM)": (res["t_lu_solve"], L * G ** 2 * R),
+            # back substitution U x = y: the R right-hand sides through layer 0's 2d rows
+            # (R (2d)^2), the 4 residual probes through all G rows (4 G^2)
+            "boundary back substitution (TRSM + DMMA GEMM)": (res["t_lu_solve"], L * (R * (2 * d) ** 2 + 4 * G ** 2)),
             "eigen refinement (Newton step, 8N residual GEMMs)": (res["t_refine"], Be * 24.0 * d ** 3),
             "blocked Hessenberg + Q": (res["t_hessenberg"], Be * (10.0 / 3.0 + 4.0 / 3.0) * d ** 3),
             "trevc_grp_kernel (eigenvectors)": (res["t_trevc"], Be * (1.0 / 3.0) * d ** 3)}
@@ -622,7 +623,7 @@ def main():
                                "MEASURED_PEAKS.json has no FP64 entry (B200 FP64 tensor rate = FP64 rate)",
                 "algorithmic_flops_per_launch": flops,
                 "flop_model": "QR with Schur vectors 20 d^3 per executed (medium, order) slot (Be of them); "
-                              "augmented LU (2/3) G^3 + G^2 R and back substitution G^2 R per order; "
+                              "augmented LU (2/3) G^3 + G^2 R and back substitution R (2d)^2 + 4 G^2 per order; "
                               "Hessenberg+Q 14/3 d^3, trevc d^3/3, refinement 24 d^3 per executed slot; "
                               "d = 4N, G = 2dP, R = 4 n_in",
                 "units": {"eigen_slots_executed": Be, "slots": int(res["slots"]), "orders": L},

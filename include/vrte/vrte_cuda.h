@@ -86,6 +86,7 @@ typedef struct vrte_cuda_result {
     uint64_t boundary_cond_warnings;/* orders whose condition bound exceeds 1e14 (boundary.cpp:259-263) */
     uint64_t eigen_slots;   /* (medium, order) slots through the eigen pipeline (the rest are free-streaming) */
     uint64_t slots;         /* all (medium, order) slots of the call */
+    uint64_t boundary_fallback; /* a residual probe failed (boundary.cuh): full solution + exact gate */
     int32_t status;         /* 0 ok, 3 numerical, 5 argument */
     char message[512];
 } vrte_cuda_result;
@@ -163,6 +164,11 @@ VRTE_API int32_t vrte_cuda_synthesize(const vrte_cuda_problem* problem, const do
 VRTE_API int32_t vrte_cuda_device_count(void);
 /* The calling thread's current CUDA device (0 when none is set). */
 VRTE_API int32_t vrte_cuda_current_device(void);
+
+/* Test hook: force (on != 0) the boundary stage's full-solution fallback -- the
+ * path a failed residual probe takes (boundary.cuh) -- on every BRDF call of the
+ * process, so the tests can compare it with the probe path. */
+VRTE_API void vrte_cuda_debug_force_boundary_fallback(int32_t on);
 
 /* Kernel-level check of the batched row-major LU (lu.cu) used by the boundary
  * stage: X[b] = A[b]^-1 B[b] for `batch` row-major G x G systems with `ncol`

@@ -23,6 +23,8 @@ typedef struct vrte_brdf_device_stats {
     double max_boundary_condition;  /* lower bound of cond_1 of the boundary matrices */
     uint64_t boundary_refined;      /* boundary refinement step taken (boundary.cpp:245-248) */
     uint64_t boundary_cond_warnings;/* orders above the 1e14 warning level (boundary.cpp:259-263) */
+    uint64_t boundary_fallback;     /* a residual probe failed: the full solution was checked */
+    uint64_t eigen_slots;           /* (medium, order) slots through the eigen pipeline */
 } vrte_brdf_device_stats;
 
 VRTE_API vrte_status vrte_brdf_device_stats_get(const vrte_brdf* brdf, vrte_brdf_device_stats* out);

@@ -84,6 +84,8 @@ class DeviceStats(C.Structure):
         ("max_boundary_condition", C.c_double),
         ("boundary_refined", C.c_uint64),
         ("boundary_cond_warnings", C.c_uint64),
+        ("boundary_fallback", C.c_uint64),
+        ("eigen_slots", C.c_uint64),
     ]
 
     def as_dict(self):
@@ -125,6 +127,7 @@ class CudaResult(C.Structure):
         ("boundary_cond_warnings", C.c_uint64),
         ("eigen_slots", C.c_uint64),
         ("slots", C.c_uint64),
+        ("boundary_fallback", C.c_uint64),
         ("status", C.c_int32),
         ("message", C.c_char * 512),
     ]
@@ -150,6 +153,7 @@ EXPORTED = [
     "vrte_cuda_plan_destroy",
     "vrte_cuda_synthesize", "vrte_cuda_device_count", "vrte_cuda_current_device", "vrte_cuda_lu_solve", "vrte_cuda_hessenberg", "vrte_cuda_schur",
     "vrte_cuda_radiance_field", "vrte_cuda_mc_trace", "vrte_cuda_host_alloc", "vrte_cuda_host_free",
+    "vrte_cuda_debug_force_boundary_fallback",
 ]
 
 
@@ -194,6 +198,8 @@ def lib():
     L.vrte_cuda_plan_fetch_ef.argtypes = [vp, dp, dp]
     L.vrte_cuda_lu_solve.argtypes = [dp, C.c_int32, C.c_int32, dp, C.c_int32, dp, C.c_int32]
     L.vrte_cuda_hessenberg.argtypes = [dp, C.c_int32, C.c_int32, dp, dp, C.c_int32, C.c_int32]
+    L.vrte_cuda_debug_force_boundary_fallback.argtypes = [C.c_int32]
+    L.vrte_cuda_debug_force_boundary_fallback.restype = None
     L.vrte_cuda_schur.argtypes = [dp, C.c_int32, C.c_int32, dp, dp, dp, dp, C.c_int32]
     L.vrte_solve_radiance.argtypes = [vp, C.POINTER(Options), dp, C.c_size_t, C.POINTER(vp)]
     L.vrte_field_size.argtypes = [vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]
@@ -233,6 +239,17 @@ def lu_solve(A, B, device: int = 0) -> np.ndarray:
     if code != 0:
         raise VrteError(code, "vrte_cuda_lu_solve failed (singular or bad arguments)")
     return X
+
+
+class forced_boundary_fallback:
+    """Context manager (tests): every BRDF call takes the boundary stage's
+    full-solution fallback (vrte_cuda_debug_force_boundary_fallback)."""
+
+    def __enter__(self):
+        lib().vrte_cuda_debug_force_boundary_fallback(1)
+
+    def __exit__(self, *exc):
+        lib().vrte_cuda_debug_force_boundary_fallback(0)
 
 
 def hessenberg(A, blocked: bool = True, device: int = 0):

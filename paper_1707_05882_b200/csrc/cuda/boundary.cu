@@ -335,6 +335,121 @@ __global__ void add_kernel(double* X, const double* dX, long long n) {
         X[e] += dX[e];
 }
 
+__device__ inline double probe_weight(int k, int c) {
+    unsigned long long z = 0x9E3779B97F4A7C15ull * (unsigned long long)(k * 7919 + c + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return (double)(z >> 11) * 0x1.0p-52 - 1.0;  // uniform in [-1, 1)
+}
+
+// Warp per (order, row i): the forward-eliminated combination probes y_k(i) =
+// sum_c v_k(c) Y(perm[i], c) and their b_k(i) = sum_c v_k(c) B0(i, c) (storage
+// row i of the untouched copy), both read coalesced along the row; the random
+// probes b_k(r) = w_k(r), gathered through the row map into Xp.
+__global__ void bnd_probe_setup_kernel(BndArgs a, const int* perm_all, double* Xp, int G, int R) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long gw = blockIdx.x * (long long)(blockDim.x >> 5) + w;
+    if (gw >= (long long)a.p.n_orders * G) return;
+    const int mo = (int)(gw / G), i = (int)(gw % G);
+    const int pi = perm_all[(size_t)mo * G + i];
+    const double* y = a.lhs + (size_t)mo * a.sl + (size_t)pi * a.ldl + G;
+    double* b0 = a.lhs0 + (size_t)mo * a.sl + (size_t)i * a.ldl + G;
+    double ay[kBndCombProbes], ab[kBndCombProbes];
+#pragma unroll
+    for (int k = 0; k < kBndCombProbes; ++k) ay[k] = ab[k] = 0.0;
+    for (int c = lane; c < R; c += 32) {
+        const double yv = y[c], bv = b0[c];
+#pragma unroll
+        for (int k = 0; k < kBndCombProbes; ++k) {
+            const double v = probe_weight(k, c);
+            ay[k] = fma(v, yv, ay[k]);
+            ab[k] = fma(v, bv, ab[k]);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kBndCombProbes; ++k) {
+        ay[k] = warp_sum(ay[k]);
+        ab[k] = warp_sum(ab[k]);
+    }
+    double* xp = Xp + ((size_t)mo * G + i) * kBndProbes;
+    if (lane < kBndProbes) {
+        double xv, bv;
+        if (lane < kBndCombProbes) {
+            xv = lane == 0 ? ay[0] : ay[1];
+            bv = lane == 0 ? ab[0] : ab[1];
+        } else {
+            xv = probe_weight(lane + 64, pi);
+            bv = probe_weight(lane + 64, i);
+        }
+        xp[lane] = xv;
+        b0[R + lane] = bv;
+    }
+}
+
+// Warp per (order, probe): residual A0 x_k - b_k (Rp holds A0 x_k), the
+// reference's relative measure and the cond_1 lower bound; plus, warp per
+// (order, right-hand side), finiteness of the solved rows >= row_lo.
+__global__ void bnd_probe_check_kernel(BndArgs a, const double* Xp, const double* Rp, const double* X, int row_lo,
+                                       int G, int R, DeviceStatus* status) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long gw = blockIdx.x * (long long)(blockDim.x >> 5) + w;
+    const int K = a.K, NO = a.p.n_orders;
+    if (gw < (long long)NO * K) {
+        const int mo = (int)(gw / K), k = (int)(gw % K);
+        const double* b = a.lhs0 + (size_t)mo * a.sl + G + R + k;
+        const double* x = Xp + (size_t)mo * G * K + k;
+        const double* ax = Rp + (size_t)mo * G * K + k;
+        double rmax = 0.0, bmax = 0.0, b1 = 0.0, xmax = 0.0, x1 = 0.0;
+        bool finite = true;
+        for (int n = lane; n < G; n += 32) {
+            const double bv = b[(size_t)n * a.ldl], xv = x[(size_t)n * K];
+            const double rv = ax[(size_t)n * K] - bv;
+            finite = finite && isfinite(xv) && isfinite(rv);
+            rmax = fmax(rmax, fabs(rv));
+            bmax = fmax(bmax, fabs(bv));
+            b1 += fabs(bv);
+            xmax = fmax(xmax, fabs(xv));
+            x1 += fabs(xv);
+        }
+        rmax = warp_max(rmax);
+        bmax = warp_max(bmax);
+        xmax = warp_max(xmax);
+        b1 = warp_sum(b1);
+        x1 = warp_sum(x1);
+        finite = __all_sync(0xffffffffu, finite);
+        if (lane == 0) {
+            const double amax = a.anorm[2 * mo], a1 = a.anorm[2 * mo + 1];
+            const double scale = amax * fmax(xmax, 1e-300) + bmax;
+            const double rel = bmax > 0.0 ? rmax / scale : 0.0;
+            const double cond = b1 > 0.0 ? a1 * x1 / b1 : 0.0;
+            atomic_max_double(&a.condm[mo], cond);
+            atomic_max_double(&status->max_boundary_residual, rel);
+            if (!finite || !(rel <= 1e-10)) atomicExch(&status->bnd_fallback, 1);
+        }
+        return;
+    }
+    const long long q = gw - (long long)NO * K;
+    if (q >= (long long)NO * R) return;
+    const int mo = (int)(q / R), c = (int)(q % R);
+    const double* x = X + (size_t)mo * G * R + c;
+    bool finite = true;
+    for (int n = row_lo + lane; n < G; n += 32) finite = finite && isfinite(x[(size_t)n * R]);
+    finite = __all_sync(0xffffffffu, finite);
+    if (lane == 0 && !finite) atomicExch(&status->bnd_fallback, 1);
+}
+
+__global__ void bnd_gather_b_kernel(BndArgs a, const int* perm_all, double* X, int G, int R) {
+    const long long total = (long long)a.p.n_orders * G * R;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(e % R);
+        const long long rb = e / R;
+        const int i = (int)(rb % G), mo = (int)(rb / G);
+        X[e] = a.lhs0[(size_t)mo * a.sl + (size_t)perm_all[(size_t)mo * G + i] * a.ldl + G + c];
+    }
+}
+
 }  // namespace
 
 void launch_bnd_norms(const BndArgs& a, int G, int R, cudaStream_t st) {
@@ -351,7 +466,11 @@ void launch_bnd_norms(const BndArgs& a, int G, int R, cudaStream_t st) {
 // of at most two layers (bnd_row / bnd_col orders: interface p rows [2dp, 2dp+2d)
 // hold layers p and p+1, the bottom rows layer P-1, the top rows layer 0), so
 // the product runs per row block over its nonzero column range only.
-void launch_bnd_residual(const BndArgs& a, const double* X, int G, int R, bool accumulate, cudaStream_t st) {
+namespace {
+// C (row-major, ncol columns) = A0 X - (beta_first = -1: C's old value, i.e. b)
+// over the nonzero column range of each row block.
+void bnd_apply(const BndArgs& a, const double* X, long long ldx, long long sx, int ncol, double* C, long long ldc,
+               long long sc, double beta_first, int G, cudaStream_t st) {
     const int d = a.d, P = a.p.n_layers;
     struct Seg {
         int r0, nr, c0, nc;
@@ -378,24 +497,29 @@ void launch_bnd_residual(const BndArgs& a, const double* X, int G, int R, bool a
     std::vector<int> seen(G, 0);
     for (const Seg& q : segs) {
         GemmBatch g{};
-        g.m = R;
+        g.m = ncol;
         g.n = q.nr;
         g.k = q.nc;
-        g.a = X + (size_t)q.c0 * R;
-        g.lda = R;
-        g.stride_a = (long long)G * R;
+        g.a = X + (size_t)q.c0 * ldx;
+        g.lda = ldx;
+        g.stride_a = sx;
         g.b = a.lhs0 + (size_t)q.r0 * a.ldl + q.c0;
         g.ldb = a.ldl;
         g.stride_b = a.sl;
-        g.c = a.lhs0 + G + (size_t)q.r0 * a.ldl;
-        g.ldc = a.ldl;
-        g.stride_c = a.sl;
+        g.c = C + (size_t)q.r0 * ldc;
+        g.ldc = ldc;
+        g.stride_c = sc;
         g.batch = a.p.n_orders;
         g.alpha = 1.0;
-        g.beta = (accumulate || seen[q.r0]) ? 1.0 : -1.0;  // subtract b once per row
+        g.beta = seen[q.r0] ? 1.0 : beta_first;
         seen[q.r0] = 1;
         gemm_batched(g, st);
     }
+}
+}  // namespace
+
+void launch_bnd_residual(const BndArgs& a, const double* X, int G, int R, bool accumulate, cudaStream_t st) {
+    bnd_apply(a, X, R, (long long)G * R, R, a.lhs0 + G, a.ldl, a.sl, accumulate ? 1.0 : -1.0, G, st);
 }
 
 void launch_bnd_check(const BndArgs& a, const double* X, int G, int R, int stage, DeviceStatus* status,
@@ -447,4 +571,27 @@ void launch_copy_zp0(const BndArgs& a, cudaStream_t st) {
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
+}  // namespace vrte
+
+namespace vrte {
+void launch_bnd_probe_setup(const BndArgs& a, const int* perm, double* Xp, int G, int R, cudaStream_t st) {
+    const long long warps = (long long)a.p.n_orders * G;
+    bnd_probe_setup_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(a, perm, Xp, G, R);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_bnd_probe_check(const BndArgs& a, const double* Xp, double* Rp, const double* X, int row_lo, int G, int R,
+                            DeviceStatus* status, cudaStream_t st) {
+    const int K = a.K, NO = a.p.n_orders;
+    bnd_apply(a, Xp, K, (long long)G * K, K, Rp, K, (long long)G * K, 0.0, G, st);
+    const long long warps = (long long)NO * (K + R);
+    bnd_probe_check_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(a, Xp, Rp, X, row_lo, G, R, status);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_bnd_gather_b(const BndArgs& a, const int* perm, double* X, int G, int R, cudaStream_t st) {
+    const long long total = (long long)a.p.n_orders * G * R;
+    bnd_gather_b_kernel<<<(unsigned)std::min(16384LL, (total + 255) / 256), 256, 0, st>>>(a, perm, X, G, R);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
 }  // namespace vrte

@@ -26,7 +26,33 @@ struct BndArgs {
     double* anorm;        // [mo][2]: max |A_ij|, ||A||_1
     double* bnorm;        // [mo][R][2]: max |b_i|, ||b||_1
     double* condm;        // [mo]: lower bound of cond_1(A), max over the right-hand sides
+    int K;                // residual probes (0: the full gate); their b_k in lhs0 columns G + R + k
 };
+
+// Residual probes (the default gate).  The BRDF needs only layer 0's unknowns,
+// so the back substitution of the R right-hand sides stops there; the
+// reference's per-right-hand-side residual check (boundary.cpp:236-254) is
+// applied to K fixed pseudo-random right-hand sides instead, solved through
+// every row: two combinations b_k = B v_k of the right-hand sides (their
+// forward elimination is Y v_k, Y the eliminated columns of the augmented
+// factorization; x_k = X v_k by linearity) and two random vectors of R^G
+// (which also expose the matrix's small singular directions to the cond_1
+// lower bound ||A||_1 ||x||_1 / ||b||_1).  A backward-stable solve gives every
+// probe a residual ~eps scale; a probe above the reference's refinement
+// threshold (1e-10 scale) or a non-finite solution entry sets
+// DeviceStatus::bnd_fallback, and the host then runs the reference's exact gate
+// on the full solution (launch_bnd_residual / launch_bnd_check).
+constexpr int kBndProbes = 4;
+constexpr int kBndCombProbes = 2;  // probes [0, 2): B v_k; [2, 4): random b
+// After the factorization, before the back substitution overwrites Y: Xp
+// [mo][G][K] (position order) <- Y v_k / the gathered random b; b_k into
+// lhs0's columns G + R + k (storage rows; lhs0 row stride >= G + R + K).
+void launch_bnd_probe_setup(const BndArgs& a, const int* perm, double* Xp, int G, int R, cudaStream_t st);
+// Rp [mo][G][K] = A0 Xp (block-sparse), then the probe / finiteness check.
+void launch_bnd_probe_check(const BndArgs& a, const double* Xp, double* Rp, const double* X, int row_lo, int G, int R,
+                            DeviceStatus* status, cudaStream_t st);
+// Full-solution fallback: X [mo][G][R] <- rows of lhs0's B columns through the row map.
+void launch_bnd_gather_b(const BndArgs& a, const int* perm, double* X, int G, int R, cudaStream_t st);
 
 // The gate after the back substitution: the relative residual of every
 // right-hand side, |A x - b|_max / (|A|_max |x|_max + |b|_max); residual = lhs0's
@@ -82,10 +108,12 @@ __host__ __device__ inline int bnd_row_end(int col, int d, int P) {
 }
 // Forward + backward substitution in place on right-hand sides already gathered
 // through the row map (row i of X = row perm[i] of B): X <- A^-1 B, A factored
-// by lu_factor_rm with row stride lda.
+// by lu_factor_rm with row stride lda.  Columns < fwd_lo already hold L^-1 P B
+// (forward-eliminated by an augmented factorization): back substitution only.
 void lu_solve_gathered(const double* A, int G, int lda, int batch, const int* perm, double* X, int ncol,
-                       cudaStream_t st);
+                       cudaStream_t st, int fwd_lo = 0);
 int lu_rm_launch_count(int G);
 int lu_aug_launch_count(int G, int R, int row_lo);
+int lu_gathered_launch_count(int G, int ncol, int fwd_lo);
 
 }  // namespace vrte

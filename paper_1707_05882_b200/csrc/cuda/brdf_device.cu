@@ -13,6 +13,7 @@
 //   nodal_components/value    pipeline.cpp:201-220 + brdf.cpp:100-117 -> S
 // Everything for one shape lives in a plan whose buffers are reused.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -116,7 +117,6 @@ struct vrte_cuda_plan {
     DevBuf<double> gsf_n, gsf_b, E, F, T, Z, psi_p, psi_m, tmp1, tmp2, tmp3, tmp4;
     DevBuf<double> X, AL, BE, FB, W2, UT, EU, hwork, Vinv;
     DevBuf<int> ipivV, permV;
-    bool schur_solves = false;  // VRTE_SOLVE=schur: quasi-triangular solves on the Schur form
     DevBuf<double> wr, wi, femax, nu, nu0, lam, residual, rho, sigma_m, rshift;
     DevBuf<int> flags, kind_m, sidx;
     // particular
@@ -126,8 +126,10 @@ struct vrte_cuda_plan {
     DevBuf<double> lhs, top0, rhs_b, rhs_x, up;
     DevBuf<int> ipiv, perm;
     // boundary residual gate (boundary.cpp:233-257)
-    DevBuf<double> lhs0, anorm, bnorm, condm, dX;
+    DevBuf<double> lhs0, anorm, bnorm, condm, dX, Xp, Rp;
+    int ldl = 0;  // row stride of [A | B] (+ the probes' b_k in lhs0): G + R + 16
     const double* lhs0_zeroed = nullptr;
+    size_t lhs0_zeroed_key = 0;
     int* refine_host = nullptr;  // page-locked copy of DeviceStatus::bnd_refine
     // synthesis
     DevBuf<double> out;
@@ -138,7 +140,7 @@ struct vrte_cuda_plan {
     DevBuf<DeviceStatus> status_buf;
     cudaEvent_t ev[16] = {};
     cudaStream_t st2 = nullptr;          // side stream: independent work overlapped with the main chain
-    cudaEvent_t fork[4] = {}, join[4] = {};
+    cudaEvent_t fork[6] = {}, join[6] = {};
     int refine_iters = 1;
     int refine_extra = 2;
     int part_refine_iters = 1;
@@ -154,7 +156,7 @@ struct vrte_cuda_plan {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         for (auto* es : {fork, join})
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < 6; ++i)
                 if (es[i]) cudaEventDestroy(es[i]);
         if (st2) cudaStreamDestroy(st2);
         if (st) cudaStreamDestroy(st);
@@ -188,7 +190,7 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
         if (!e) VRTE_CUDA_CHECK(cudaEventCreate(&e));
     if (!pl.st2) VRTE_CUDA_CHECK(cudaStreamCreateWithFlags(&pl.st2, cudaStreamNonBlocking));
     for (auto* es : {pl.fork, pl.join})
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 6; ++i)
             if (!es[i]) VRTE_CUDA_CHECK(cudaEventCreateWithFlags(&es[i], cudaEventDisableTiming));
     if (const char* ri = std::getenv("VRTE_REFINE_ITERS")) pl.refine_iters = std::atoi(ri);
     if (const char* pi = std::getenv("VRTE_PART_REFINE_ITERS")) pl.part_refine_iters = std::atoi(pi);
@@ -226,7 +228,6 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
             ++tail;
         }
         pl.Be = std::max(1, pl.B - tail);  // at least one slot through the pipeline (no empty launches)
-        if (std::getenv("VRTE_NO_FREE_ORDERS")) pl.Be = pl.B;
     }
     const int N = pl.N, L = pl.L, d = pl.d, R = pl.R, G = pl.G, B = pl.B, NO = pl.NO;
     cudaStream_t st = pl.st;
@@ -292,7 +293,6 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pl.Vinv.alloc(B * dd);
     pl.ipivV.alloc((size_t)B * d);
     pl.permV.alloc((size_t)B * d);
-    if (const char* sv = std::getenv("VRTE_SOLVE")) pl.schur_solves = std::string(sv) == "schur";
     pl.rho.alloc((size_t)B * d * 2);
     pl.sigma_m.alloc((size_t)B * d * 4);
     pl.kind_m.alloc((size_t)B * d * 2);
@@ -312,11 +312,16 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pl.mu_eff.alloc((size_t)B * pl.n_in);
     pl.sigma.alloc((size_t)B * R * 2);
     pl.kind.alloc((size_t)B * R);
-    pl.lhs.alloc((size_t)NO * G * (G + R));  // augmented [A | B] per order, row-major
-    pl.lhs0.alloc((size_t)NO * G * (G + R));  // its untouched copy (residual gate)
-    if (pl.lhs0_zeroed != pl.lhs0.p) {       // the zero blocks of the copy are never written
+    pl.ldl = G + R + 16;  // >= G + R + kBndProbes, rows stay 128-byte aligned
+    pl.lhs.alloc((size_t)NO * G * pl.ldl);   // augmented [A | B | probes] per order, row-major
+    pl.lhs0.alloc((size_t)NO * G * pl.ldl);  // its untouched copy (residual gate)
+    pl.Xp.alloc((size_t)NO * G * kBndProbes);
+    pl.Rp.alloc((size_t)NO * G * kBndProbes);
+    const size_t zkey = ((size_t)G << 40) ^ ((size_t)pl.ldl << 20) ^ (size_t)NO ^ ((size_t)pl.P << 60);
+    if (pl.lhs0_zeroed != pl.lhs0.p || pl.lhs0_zeroed_key != zkey) {  // its zero blocks are never written
         VRTE_CUDA_CHECK(cudaMemsetAsync(pl.lhs0.p, 0, sizeof(double) * pl.lhs0.n, st));
         pl.lhs0_zeroed = pl.lhs0.p;
+        pl.lhs0_zeroed_key = zkey;
     }
     pl.anorm.alloc((size_t)NO * 2);
     pl.bnorm.alloc((size_t)NO * R * 2);
@@ -356,6 +361,87 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pd.beam_rows = pl.beam_rows.p;
 }
 
+BndArgs make_bnd(vrte_cuda_plan& pl) {
+    BndArgs ba{};
+    ba.p = pl.pd;
+    ba.d = pl.d;
+    ba.psi_p = pl.psi_p.p;
+    ba.psi_m = pl.psi_m.p;
+    ba.nu = pl.nu.p;
+    ba.wi = pl.wi.p;
+    ba.zp = pl.zp.p;
+    ba.zm = pl.zm.p;
+    ba.lhs = pl.lhs.p;
+    ba.top0 = pl.top0.p;
+    // the right-hand sides ride in the LU as columns G .. G+R, the residual
+    // probes after them (BRDF path; the radiance path checks every column)
+    ba.K = pl.full_solution ? 0 : kBndProbes;
+    ba.ldl = ba.ldr = pl.ldl;
+    ba.sl = ba.sr = (long long)pl.G * pl.ldl;
+    ba.rhs = pl.lhs.p + pl.G;
+    ba.up = pl.up.p;
+    ba.lhs0 = pl.lhs0.p;
+    ba.anorm = pl.anorm.p;
+    ba.bnorm = pl.bnorm.p;
+    ba.condm = pl.condm.p;
+    return ba;
+}
+
+// The reference's gate on the full solution rhs_x (boundary.cpp:233-257):
+// |A x - b| against 1e-10 scale, one refinement step for the right-hand sides
+// above it, then 1e-9 scale.  Host-synchronous (the refinement is rare).
+int boundary_full_gate(vrte_cuda_plan& pl, const BndArgs& ba, cudaStream_t st) {
+    const int G = pl.G, R = pl.R, NO = pl.NO;
+    int nl = 2;
+    VRTE_CUDA_CHECK(cudaMemsetAsync(&pl.status->max_boundary_residual, 0, sizeof(double), st));
+    VRTE_CUDA_CHECK(cudaMemsetAsync(pl.condm.p, 0, sizeof(double) * NO, st));
+    launch_bnd_residual(ba, pl.rhs_x.p, G, R, false, st);
+    launch_bnd_check(ba, pl.rhs_x.p, G, R, 0, pl.status, st);
+    VRTE_CUDA_CHECK(cudaMemcpyAsync(pl.refine_host, &pl.status->bnd_refine, sizeof(int), cudaMemcpyDeviceToHost, st));
+    VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (*pl.refine_host) {
+        launch_bnd_refine_rhs(ba, pl.perm.p, pl.dX.p, G, R, st);
+        lu_solve_gathered(pl.lhs.p, G, pl.ldl, NO, pl.perm.p, pl.dX.p, R, st);
+        launch_bnd_add(pl.rhs_x.p, pl.dX.p, (long long)NO * G * R, st);
+        launch_bnd_residual(ba, pl.dX.p, G, R, true, st);
+        VRTE_CUDA_CHECK(cudaMemsetAsync(&pl.status->max_boundary_residual, 0, sizeof(double), st));
+        VRTE_CUDA_CHECK(cudaMemsetAsync(pl.condm.p, 0, sizeof(double) * NO, st));
+        launch_bnd_check(ba, pl.rhs_x.p, G, R, 1, pl.status, st);
+        const int one = 1;
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(&pl.status->bnd_refined, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+        nl += 6 + 4 * ((G + 63) / 64);
+    }
+    return nl;
+}
+
+// up = Z+ of the top layer + Top0 [A_0; B_0]: layer 0's unknowns are the last
+// 2d rows of the row-major solution (bnd_col), read column-major as their transpose.
+int boundary_top(vrte_cuda_plan& pl, const BndArgs& ba, cudaStream_t st) {
+    const int d = pl.d, R = pl.R, G = pl.G;
+    launch_copy_zp0(ba, st);
+    gemm_batched(gemm(d, R, 2 * d, pl.top0.p, d, (long long)d * 2 * d, false,
+                      pl.rhs_x.p + (size_t)(G - 2 * d) * R, R, (long long)G * R, true, pl.up.p, d, (long long)d * R,
+                      pl.NO, 1.0, 1.0),
+                 st);
+    return 2;
+}
+
+int run_synth(vrte_cuda_plan& pl, cudaStream_t st) {
+    SynthArgs sa{};
+    sa.N = pl.N;
+    sa.L = pl.L;
+    sa.n_in = pl.n_in;
+    sa.n_dphi = pl.n_dphi;
+    sa.up = pl.up.p;
+    sa.slot_of_order = pl.slot_of_order.p;
+    sa.trig = pl.trig.p;
+    sa.post = pl.post.p;
+    sa.out = pl.out.p;
+    sa.status = pl.status;
+    launch_synth(sa, st);
+    return 1;
+}
+
 // The device pipeline; returns the number of kernel launches issued.
 uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     const int N = pl.N, L = pl.L, d = pl.d, R = pl.R, G = pl.G, NO = pl.NO;
@@ -379,24 +465,9 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     launch_build_ef(pd, pl.gsf_n.p, pl.E.p, pl.F.p, st);
     gemm_batched(gemm(d, d, d, pl.F.p, d, dd, false, pl.E.p, d, dd, false, pl.T.p, d, dd, B), st);
     launch_max_abs(pl.T.p, dd, B, pl.femax.p, st);
-    if (const char* dump = std::getenv("VRTE_DUMP_FE")) {  // debug: F E of every (medium, order)
-        std::vector<double> h((size_t)B * dd);
-        VRTE_CUDA_CHECK(cudaMemcpyAsync(h.data(), pl.T.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
-        VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
-        if (FILE* f = std::fopen(dump, "wb")) {
-            std::fwrite(h.data(), sizeof(double), h.size(), f);
-            std::fclose(f);
-        }
-    }
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[5], st));
-    static const char* hess_mode = std::getenv("VRTE_HESS");  // blocked (default) | unblocked
-    if (hess_mode && std::string(hess_mode) == "unblocked") {
-        launch_hessenberg(pl.T.p, pl.Z.p, d, B, st);
-        nl += 1;
-    } else {
-        launch_hessenberg_blocked(pl.T.p, pl.Z.p, pl.hwork.p, d, B, st);
-        nl += hessenberg_launch_count(d);
-    }
+    launch_hessenberg_blocked(pl.T.p, pl.Z.p, pl.hwork.p, d, B, st);
+    nl += hessenberg_launch_count(d);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[6], st));
     launch_hqr(pl.T.p, pl.Z.p, pl.wr.p, pl.wi.p, d, B, pl.status, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[7], st));
@@ -404,7 +475,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[8], st));
     gemm_batched(gemm(d, d, d, pl.Z.p, d, dd, false, pl.tmp1.p, d, dd, false, pl.X.p, d, dd, B), st);
     launch_normalize_modes(pl.X.p, pl.wi.p, d, B, st);
-    if (!pl.schur_solves) {
+    {
         // V^-1 of the packed eigenvector matrix: the shifted solves of the
         // refinement and of the particular stage run in the eigenbasis
         // (two GEMMs + an independent 1x1/2x2 solve per entry).
@@ -446,22 +517,16 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     launch_modes(ma, st);
     // (F E - sigma_c) y_c = r_c for `ncol` columns in place of W = R (ld d):
     // eigenbasis (default) or Schur form.  `out` = Q y (+ beta out).
-    bool vinv_joined = pl.schur_solves;
+    bool vinv_joined = false;
     auto shifted_solve = [&](const double* Rm, double* Wm, int ncol, long long wst, const double* sig,
                              const int* knd, double* out, double beta, cudaStream_t ss) {
         if (ss == st && !vinv_joined) {  // V^-1 comes from the side stream: join at its first use
             VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[1], 0));
             vinv_joined = true;
         }
-        const double* Lm = pl.schur_solves ? pl.Z.p : pl.Vinv.p;
-        gemm_batched(gemm(d, ncol, d, Lm, d, dd, pl.schur_solves, Rm, d, wst, false, Wm, d, wst, B), ss);
-        if (pl.schur_solves)
-            launch_qtri_solve(pl.T.p, d, dd, Wm, ncol, wst, sig, knd, B, nullptr, ss);
-        else
-            launch_eig_diag_solve(Wm, d, ncol, wst, pl.wr.p, pl.wi.p, sig, knd, B, ss);
-        gemm_batched(gemm(d, ncol, d, pl.schur_solves ? pl.Z.p : pl.X.p, d, dd, false, Wm, d, wst, false,
-                          out, d, wst, B, 1.0, beta),
-                     ss);
+        gemm_batched(gemm(d, ncol, d, pl.Vinv.p, d, dd, false, Rm, d, wst, false, Wm, d, wst, B), ss);
+        launch_eig_diag_solve(Wm, d, ncol, wst, pl.wr.p, pl.wi.p, sig, knd, B, ss);
+        gemm_batched(gemm(d, ncol, d, pl.X.p, d, dd, false, Wm, d, wst, false, out, d, wst, B, 1.0, beta), ss);
     };
     auto residual_gemms = [&]() {
         gemm_batched(gemm(d, d, d, pl.E.p, d, dd, false, pl.tmp1.p, d, dd, false, pl.tmp3.p, d, dd, B), st);
@@ -601,25 +666,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
                       pl.residual.p, pl.zp.p, pl.zm.p, R, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[2], st));
     // ---------------- boundary
-    BndArgs ba{};
-    ba.p = pd;
-    ba.d = d;
-    ba.psi_p = pl.psi_p.p;
-    ba.psi_m = pl.psi_m.p;
-    ba.nu = pl.nu.p;
-    ba.wi = pl.wi.p;
-    ba.zp = pl.zp.p;
-    ba.zm = pl.zm.p;
-    ba.lhs = pl.lhs.p;
-    ba.top0 = pl.top0.p;
-    ba.ldl = ba.ldr = G + R;  // the right-hand sides ride in the LU as columns G .. G+R
-    ba.sl = ba.sr = (long long)G * (G + R);
-    ba.rhs = pl.lhs.p + G;
-    ba.up = pl.up.p;
-    ba.lhs0 = pl.lhs0.p;
-    ba.anorm = pl.anorm.p;
-    ba.bnorm = pl.bnorm.p;
-    ba.condm = pl.condm.p;
+    const BndArgs ba = make_bnd(pl);
     launch_bnd_assemble(ba, st);
     // right-hand sides on the side stream once the particular vectors are there; the
     // factorization waits for them only before its first update of those columns
@@ -631,60 +678,71 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     launch_bnd_norms(ba, G, R, st2);
     VRTE_CUDA_CHECK(cudaMemsetAsync(pl.condm.p, 0, sizeof(double) * NO, st2));
     VRTE_CUDA_CHECK(cudaEventRecord(pl.join[0], st2));
+    nl += 4;
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[11], st));
-    lu_factor_rm(pl.lhs.p, G, NO, pl.ipiv.p, pl.perm.p, pl.status, pl.order_index.p, st, d, pl.P, G + R, G + R,
+    const int K = ba.K, ldl = ba.ldl;
+    lu_factor_rm(pl.lhs.p, G, NO, pl.ipiv.p, pl.perm.p, pl.status, pl.order_index.p, st, d, pl.P, ldl, G + R,
                  pl.join[3]);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[12], st));
-    lu_backsolve_aug(pl.lhs.p, G, G + R, R, NO, pl.perm.p, pl.rhs_x.p, 0, st);
-    VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[13], st));
-    // residual gate (boundary.cpp:233-257): |A x - b| against 1e-10 scale, one
-    // refinement step for the right-hand sides above it, then 1e-9 scale
-    VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[0], 0));
-    launch_bnd_residual(ba, pl.rhs_x.p, G, R, false, st);
-    launch_bnd_check(ba, pl.rhs_x.p, G, R, 0, pl.status, st);
-    VRTE_CUDA_CHECK(cudaMemcpyAsync(pl.refine_host, &pl.status->bnd_refine, sizeof(int), cudaMemcpyDeviceToHost, st));
-    VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
-    nl += 5;
-    static const bool force_refine = std::getenv("VRTE_BND_FORCE_REFINE") != nullptr;  // experiment
-    if (*pl.refine_host || force_refine) {
-        launch_bnd_refine_rhs(ba, pl.perm.p, pl.dX.p, G, R, st);
-        lu_solve_gathered(pl.lhs.p, G, G + R, NO, pl.perm.p, pl.dX.p, R, st);
-        launch_bnd_add(pl.rhs_x.p, pl.dX.p, (long long)NO * G * R, st);
-        launch_bnd_residual(ba, pl.dX.p, G, R, true, st);
-        VRTE_CUDA_CHECK(cudaMemsetAsync(&pl.status->max_boundary_residual, 0, sizeof(double), st));
-        VRTE_CUDA_CHECK(cudaMemsetAsync(pl.condm.p, 0, sizeof(double) * NO, st));
-        launch_bnd_check(ba, pl.rhs_x.p, G, R, 1, pl.status, st);
-        const int one = 1;
-        VRTE_CUDA_CHECK(cudaMemcpyAsync(&pl.status->bnd_refined, &one, sizeof(int), cudaMemcpyHostToDevice, st));
-        nl += 6 + 4 * ((G + 63) / 64);
+    if (pl.full_solution) {
+        // radiance: every layer's coefficients, under the reference's exact gate
+        lu_backsolve_aug(pl.lhs.p, G, ldl, R, NO, pl.perm.p, pl.rhs_x.p, 0, st);
+        VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[13], st));
+        VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[0], 0));
+        nl += lu_aug_launch_count(G, R, 0) + boundary_full_gate(pl, ba, st);
+    } else {
+        // BRDF: layer 0's unknowns only (the last 2d rows); the K residual probes
+        // through every row on the side stream, concurrently
+        launch_bnd_probe_setup(ba, pl.perm.p, pl.Xp.p, G, R, st);
+        VRTE_CUDA_CHECK(cudaEventRecord(pl.fork[4], st));
+        VRTE_CUDA_CHECK(cudaStreamWaitEvent(st2, pl.fork[4], 0));
+        lu_solve_gathered(pl.lhs.p, G, ldl, NO, pl.perm.p, pl.Xp.p, K, st2, kBndCombProbes);
+        VRTE_CUDA_CHECK(cudaEventRecord(pl.join[4], st2));
+        const int row_lo = G - 2 * d;
+        lu_backsolve_aug(pl.lhs.p, G, ldl, R, NO, pl.perm.p, pl.rhs_x.p, row_lo, st);
+        VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[13], st));
+        VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[0], 0));
+        VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[4], 0));
+        launch_bnd_probe_check(ba, pl.Xp.p, pl.Rp.p, pl.rhs_x.p, (row_lo / 64) * 64, G, R, pl.status, st);
+        nl += lu_aug_launch_count(G, R, row_lo) + 1 + lu_gathered_launch_count(G, K, kBndCombProbes) + 3;
     }
-    launch_copy_zp0(ba, st);
-    // up += Top0 [A_0; B_0]: layer 0's unknowns are the last 2d rows of the
-    // row-major solution (bnd_col), read column-major as their transpose
-    gemm_batched(gemm(d, R, 2 * d, pl.top0.p, d, (long long)d * 2 * d, false,
-                      pl.rhs_x.p + (size_t)(G - 2 * d) * R, R, (long long)G * R, true, pl.up.p, d, dR, NO,
-                      1.0, 1.0),
-                 st);
-    nl += 4 + (pd.base_type != 0 ? 1 : 0) + lu_aug_launch_count(G, R, 0) + 2;
+    nl += boundary_top(pl, ba, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[3], st));
     // ---------------- synthesis
-    if (synth) {
-        SynthArgs sa{};
-        sa.N = N;
-        sa.L = L;
-        sa.n_in = pl.n_in;
-        sa.n_dphi = pl.n_dphi;
-        sa.up = pl.up.p;
-        sa.slot_of_order = pl.slot_of_order.p;
-        sa.trig = pl.trig.p;
-        sa.post = pl.post.p;
-        sa.out = pl.out.p;
-        sa.status = pl.status;
-        launch_synth(sa, st);
-        nl += 1;
-    }
+    if (synth) nl += run_synth(pl, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[4], st));
     return nl;
+}
+
+// A residual probe failed (or a solution entry is not finite): the full
+// solution of every right-hand side under the reference's exact gate, then the
+// tau = 0 stacks and the synthesis again.  Synchronizes the plan's stream;
+// returns true when it ran.
+std::atomic<int> g_force_fallback{0};
+
+bool boundary_fallback(vrte_cuda_plan& pl, bool synth) {
+    if (pl.full_solution) return false;
+    if (g_force_fallback.load()) {
+        const int one = 1;
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(&pl.status->bnd_fallback, &one, sizeof(int), cudaMemcpyHostToDevice, pl.st));
+    }
+    VRTE_CUDA_CHECK(cudaMemcpyAsync(pl.refine_host, &pl.status->bnd_fallback, sizeof(int), cudaMemcpyDeviceToHost, pl.st));
+    VRTE_CUDA_CHECK(cudaStreamSynchronize(pl.st));
+    if (!*pl.refine_host) return false;
+    cudaStream_t st = pl.st;
+    const BndArgs ba = make_bnd(pl);
+    launch_bnd_gather_b(ba, pl.perm.p, pl.rhs_x.p, pl.G, pl.R, st);
+    lu_solve_gathered(pl.lhs.p, pl.G, pl.ldl, pl.NO, pl.perm.p, pl.rhs_x.p, pl.R, st);
+    uint64_t nl = 1 + lu_rm_launch_count(pl.G);
+    nl += boundary_full_gate(pl, ba, st);
+    nl += boundary_top(pl, ba, st);
+    if (synth) {
+        VRTE_CUDA_CHECK(cudaMemsetAsync(&pl.status->clamped, 0, sizeof(unsigned long long), st));
+        VRTE_CUDA_CHECK(cudaMemsetAsync(&pl.status->neg_key, 0, sizeof(unsigned long long), st));
+        nl += run_synth(pl, st);
+    }
+    pl.launches += nl;
+    return true;
 }
 
 std::string describe_failure(const DeviceStatus& s, const std::vector<double>& residual, int d,
@@ -788,6 +846,7 @@ int finish(vrte_cuda_plan& pl, vrte_cuda_result* r) {
         r->max_balance_residual = s.max_balance_residual;
         r->max_boundary_residual = s.max_boundary_residual;
         r->boundary_refined = s.bnd_refined ? 1 : 0;
+        r->boundary_fallback = s.bnd_fallback ? 1 : 0;
         std::vector<double> cm((size_t)pl.NO);
         VRTE_CUDA_CHECK(cudaMemcpy(cm.data(), pl.condm.p, sizeof(double) * cm.size(), cudaMemcpyDeviceToHost));
         r->max_boundary_condition = 0.0;
@@ -919,6 +978,8 @@ void vrte_cuda_host_free(void* p, size_t bytes) {
     g_host_free.emplace_back(bytes, p);
 }
 
+void vrte_cuda_debug_force_boundary_fallback(int32_t on) { g_force_fallback.store(on != 0); }
+
 int32_t vrte_cuda_device_count(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
@@ -939,6 +1000,7 @@ int32_t vrte_cuda_plan_create(const vrte_cuda_problem* problem, vrte_cuda_plan**
         auto pl = std::make_unique<vrte_cuda_plan>();
         setup_plan(*pl, problem);
         pl->launches = run_pipeline(*pl, pl->full_orders);
+        boundary_fallback(*pl, pl->full_orders);
         const int rc = finish(*pl, result);
         if (rc == 0) *out = pl.release();  // a failed plan frees its device buffers here
         return rc;
@@ -962,6 +1024,7 @@ int32_t vrte_cuda_plan_run(vrte_cuda_plan* pl, int32_t iters, double* seconds,
         cudaEventDestroy(a);
         cudaEventDestroy(b);
         if (seconds) *seconds = ms * 1e-3 / iters;
+        boundary_fallback(*pl, pl->full_orders);
         return finish(*pl, result);
     });
 }
@@ -1055,6 +1118,7 @@ int32_t brdf_sharded(const vrte_cuda_problem* problem, double* table, vrte_cuda_
             setup_plan(pl, &pk);
             pl.full_solution = false;
             pl.launches = run_pipeline(pl, false);
+            boundary_fallback(pl, false);
             res[k] = vrte_cuda_result{};
             rc[k] = finish(pl, &res[k]);
         } catch (const std::invalid_argument& e) {
@@ -1123,6 +1187,7 @@ int32_t brdf_sharded(const vrte_cuda_problem* problem, double* table, vrte_cuda_
                  {&vrte_cuda_result::dithered, &vrte_cuda_result::polished, &vrte_cuda_result::kernel_launches,
                   &vrte_cuda_result::qr_sweeps, &vrte_cuda_result::qr_steps, &vrte_cuda_result::boundary_refined,
                   &vrte_cuda_result::boundary_cond_warnings, &vrte_cuda_result::eigen_slots,
+                  &vrte_cuda_result::boundary_fallback,
                   &vrte_cuda_result::slots})
                 r.*f += q.*f;
         }
@@ -1162,6 +1227,9 @@ int32_t vrte_cuda_brdf(const vrte_cuda_problem* problem, double* table, vrte_cud
         pl.launches = run_pipeline(pl, true);
         VRTE_CUDA_CHECK(cudaMemcpyAsync(table, pl.out.p, sizeof(double) * pl.out.n,
                                         cudaMemcpyDeviceToHost, pl.st));
+        if (boundary_fallback(pl, true))
+            VRTE_CUDA_CHECK(cudaMemcpyAsync(table, pl.out.p, sizeof(double) * pl.out.n,
+                                            cudaMemcpyDeviceToHost, pl.st));
         return finish(pl, result);
     });
 }
@@ -1392,13 +1460,8 @@ int32_t vrte_cuda_schur(const double* A, int32_t d, int32_t batch, double* T, do
         dwi.alloc((size_t)batch * d);
         dst.alloc(1);
         VRTE_CUDA_CHECK(cudaMemsetAsync(dst.p, 0, sizeof(DeviceStatus), st));
-        static const char* hess_mode = std::getenv("VRTE_HESS");
-        if (hess_mode && std::string(hess_mode) == "unblocked") {
-            launch_hessenberg(dA.p, dZ.p, d, batch, st);
-        } else {
-            work.alloc((size_t)batch * hessenberg_work_doubles(d));
-            launch_hessenberg_blocked(dA.p, dZ.p, work.p, d, batch, st);
-        }
+        work.alloc((size_t)batch * hessenberg_work_doubles(d));
+        launch_hessenberg_blocked(dA.p, dZ.p, work.p, d, batch, st);
         cudaEvent_t e0, e1;
         VRTE_CUDA_CHECK(cudaEventCreate(&e0));
         VRTE_CUDA_CHECK(cudaEventCreate(&e1));
@@ -1413,15 +1476,8 @@ int32_t vrte_cuda_schur(const double* A, int32_t d, int32_t batch, double* T, do
         VRTE_CUDA_CHECK(cudaMemcpyAsync(&s, dst.p, sizeof s, cudaMemcpyDeviceToHost, st));
         VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
         cudaStreamDestroy(st);
-        if (std::getenv("VRTE_DEBUG")) {
-            float ms = 0;
-            cudaEventElapsedTime(&ms, e0, e1);
-            std::fprintf(stderr, "vrte_cuda_schur: QR %.3f ms (batch %d, d %d)\n", ms, batch, d);
-        }
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
-        if (s.code != 0 && std::getenv("VRTE_DEBUG"))
-            std::fprintf(stderr, "vrte_cuda_schur: code %d matrix %d I=%g L=%g\n", s.code, s.index, s.value, s.value2);
         return s.code != 0 ? 3 : 0;
     } catch (const std::exception&) {
         return 3;

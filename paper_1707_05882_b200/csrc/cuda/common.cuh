@@ -52,6 +52,7 @@ struct DeviceStatus {
     unsigned long long bnd_cond_warnings;  // orders above 1e14 (boundary.cpp:259-263 warns)
     int bnd_refine;                   // a right-hand side needs the refinement step
     int bnd_refined;                  // ... and it was taken
+    int bnd_fallback;                 // a residual probe failed: full solve + reference gate
     double max_balance_residual;      // particular 8N balance residual (particular.cpp:86-105)
     unsigned long long qr_sweeps;
     unsigned long long qr_steps;

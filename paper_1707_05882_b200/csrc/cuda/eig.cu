@@ -2,8 +2,7 @@
 // homogeneous problem (F E) x = x / nu^2 of every (medium, order), and the
 // mode recovery / residual machinery of homogeneous.cpp:131-287.
 //
-// Reference uses Eigen::EigenSolver (real Schur + eigenvectors).  Here
-// (defaults; the other kernels stay selectable for A/B runs and tests):
+// Reference uses Eigen::EigenSolver (real Schur + eigenvectors).  Here:
 //   hessenberg.cu        : blocked Householder reduction (dlahr2 panels + DMMA
 //                          trailing updates), Q formed into Z
 //   hqr_multi_kernel     : small-bulge multishift Francis QR with aggressive
@@ -17,8 +16,6 @@
 //   trevc_grp_kernel     : eigenvectors of the quasi-triangular Schur factor by
 //                          register-resident back substitution (dtrevc), 4 per
 //                          warp, back-transformed by a GEMM
-//   hqr_kernel / hqr_window_kernel / trevc_kernel: the single-CTA predecessors
-//                          (VRTE_HQR=band|window, VRTE_TREVC=smem)
 #include <climits>
 #include <cstdlib>
 #include <string>
@@ -115,18 +112,7 @@ __global__ void __launch_bounds__(NT) hessenberg_kernel(double* Aall, double* Za
 }
 
 // ------------------------------------------------------------------ Francis QR
-constexpr int BW = 8;  // band: diagonal offsets c - r in [-3, BW] kept in smem
 
-struct HAcc {
-    double* g;
-    double* band;
-    int d;
-    __device__ double& operator()(int r, int c) const {
-        const int off = c - r;
-        if (off >= -3 && off <= BW) return band[(off + 3) * d + c];
-        return g[r + (size_t)c * d];
-    }
-};
 
 // dlanv2: Schur factorization of a real 2x2 nonsymmetric matrix in standard form.
 __device__ void dlanv2(double& a, double& b, double& c, double& dd, double& rt1r, double& rt1i,
@@ -231,282 +217,10 @@ __device__ void dlanv2(double& a, double& b, double& c, double& dd, double& rt1r
     }
 }
 
-__device__ bool small_subdiag(const HAcc& h, int k, int d, double ulp, double smlnum) {
-    const double hk = fabs(h(k, k - 1));
-    if (hk <= smlnum) return true;
-    double tst = fabs(h(k - 1, k - 1)) + fabs(h(k, k));
-    if (tst == 0.0) {
-        if (k - 2 >= 0) tst += fabs(h(k - 1, k - 2));
-        if (k + 1 <= d - 1) tst += fabs(h(k + 1, k));
-    }
-    if (hk <= ulp * tst) {
-        const double hup = fabs(h(k - 1, k));
-        const double ab = fmax(hk, hup), ba = fmin(hk, hup);
-        const double dif = fabs(h(k - 1, k - 1) - h(k, k));
-        const double aa = fmax(fabs(h(k, k)), dif), bb = fmin(fabs(h(k, k)), dif);
-        const double s = aa + ab;
-        if (ba * (ab / s) <= fmax(smlnum, ulp * (bb * (aa / s)))) return true;
-    }
-    return false;
-}
 
-__device__ void start_vector(const HAcc& h, int m, double rt1r, double rt1i, double rt2r,
-                             double rt2i, double v[3]) {
-    double h21s = h(m + 1, m);
-    double s = fabs(h(m, m) - rt2r) + fabs(rt2i) + fabs(h21s);
-    h21s = h(m + 1, m) / s;
-    v[0] = h21s * h(m, m + 1) + (h(m, m) - rt1r) * ((h(m, m) - rt2r) / s) - rt1i * (rt2i / s);
-    v[1] = h21s * (h(m, m) + h(m + 1, m + 1) - rt1r - rt2r);
-    v[2] = h21s * h(m + 2, m + 1);
-    s = fabs(v[0]) + fabs(v[1]) + fabs(v[2]);
-    v[0] /= s;
-    v[1] /= s;
-    v[2] /= s;
-}
 
-__global__ void __launch_bounds__(256) hqr_kernel(double* Hall, double* Zall, double* wrall,
-                                                 double* wiall, int d, DeviceStatus* status) {
-    extern __shared__ double band[];
-    __shared__ int s_int;
-    const int b = blockIdx.x, t = threadIdx.x, nt = blockDim.x;
-    double* H = Hall + (size_t)b * d * d;
-    double* Z = Zall + (size_t)b * d * d;
-    double* wr = wrall + (size_t)b * d;
-    double* wi = wiall + (size_t)b * d;
-    const HAcc h{H, band, d};
-    for (int idx = t; idx < (BW + 4) * d; idx += nt) {
-        const int off = idx / d - 3, c = idx % d, r = c - off;
-        band[idx] = (r >= 0 && r < d) ? H[r + (size_t)c * d] : 0.0;
-    }
-    __syncthreads();
 
-    const double ulp = kUlp;
-    const double smlnum = kSafeMin * ((double)d / ulp);
-    const int itmax = 30 * max(10, d);
-    const int kexsh = 10;
-    int kdefl = 0;
-    int I = d - 1;
-    bool failed = false;
-    while (I >= 0) {
-        int L = 0;
-        bool conv = false;
-        for (int its = 0; its <= itmax; ++its) {
-            int kb = L;
-            for (int k = L + 1 + t; k <= I; k += nt)
-                if (small_subdiag(h, k, d, ulp, smlnum)) kb = max(kb, k);
-            L = block_max_int(kb, &s_int);
-            if (L > 0 && t == 0) h(L, L - 1) = 0.0;
-            __syncthreads();
-            if (L >= I - 1) {
-                conv = true;
-                break;
-            }
-            ++kdefl;
-            double h11, h12, h21, h22;
-            if (kdefl % (2 * kexsh) == 0) {
-                const double s = fabs(h(I, I - 1)) + fabs(h(I - 1, I - 2));
-                h11 = 0.75 * s + h(I, I);
-                h12 = -0.4375 * s;
-                h21 = s;
-                h22 = h11;
-            } else if (kdefl % kexsh == 0) {
-                const double s = fabs(h(L + 1, L)) + fabs(h(L + 2, L + 1));
-                h11 = 0.75 * s + h(L, L);
-                h12 = -0.4375 * s;
-                h21 = s;
-                h22 = h11;
-            } else {
-                h11 = h(I - 1, I - 1);
-                h21 = h(I, I - 1);
-                h12 = h(I - 1, I);
-                h22 = h(I, I);
-            }
-            double rt1r, rt1i, rt2r, rt2i;
-            {
-                const double s = fabs(h11) + fabs(h12) + fabs(h21) + fabs(h22);
-                if (s == 0.0) {
-                    rt1r = rt1i = rt2r = rt2i = 0.0;
-                } else {
-                    h11 /= s;
-                    h21 /= s;
-                    h12 /= s;
-                    h22 /= s;
-                    const double tr = (h11 + h22) / 2.0;
-                    const double det = (h11 - tr) * (h22 - tr) - h12 * h21;
-                    const double rtdisc = sqrt(fabs(det));
-                    if (det >= 0.0) {
-                        rt1r = tr * s;
-                        rt2r = rt1r;
-                        rt1i = rtdisc * s;
-                        rt2i = -rt1i;
-                    } else {
-                        rt1r = tr + rtdisc;
-                        rt2r = tr - rtdisc;
-                        if (fabs(rt1r - h22) <= fabs(rt2r - h22)) {
-                            rt1r *= s;
-                            rt2r = rt1r;
-                        } else {
-                            rt2r *= s;
-                            rt1r = rt2r;
-                        }
-                        rt1i = rt2i = 0.0;
-                    }
-                }
-            }
-            // two consecutive small subdiagonals: largest M in [L+1, I-2] passing, else L
-            int mb = L;
-            for (int mm = L + 1 + t; mm <= I - 2; mm += nt) {
-                double vv[3];
-                start_vector(h, mm, rt1r, rt1i, rt2r, rt2i, vv);
-                const double h00 = fabs(h(mm, mm - 1)) * (fabs(vv[1]) + fabs(vv[2]));
-                const double h11b =
-                    fabs(vv[0]) * (fabs(h(mm - 1, mm - 1)) + fabs(h(mm, mm)) + fabs(h(mm + 1, mm + 1)));
-                if (h00 <= ulp * h11b) mb = max(mb, mm);
-            }
-            const int M = block_max_int(mb, &s_int);
-            if (t == 0) {
-                atomicAdd(&status->qr_sweeps, 1ull);
-                atomicAdd(&status->qr_steps, (unsigned long long)(I - M));
-            }
-            double v0[3];
-            start_vector(h, M, rt1r, rt1i, rt2r, rt2i, v0);
-            for (int k = M; k <= I - 1; ++k) {
-                const int nr = min(3, I - k + 1);
-                double v1, v2, v3;
-                if (k > M) {
-                    v1 = h(k, k - 1);
-                    v2 = h(k + 1, k - 1);
-                    v3 = (nr == 3) ? h(k + 2, k - 1) : 0.0;
-                } else {
-                    v1 = v0[0];
-                    v2 = v0[1];
-                    v3 = (nr == 3) ? v0[2] : 0.0;
-                }
-                double t1 = 0.0;
-                {
-                    const double xnorm = (nr == 3) ? hypot(v2, v3) : fabs(v2);
-                    if (xnorm != 0.0) {
-                        const double beta = -copysign(hypot(v1, xnorm), v1);
-                        t1 = (beta - v1) / beta;
-                        const double scal = 1.0 / (v1 - beta);
-                        v2 *= scal;
-                        v3 *= scal;
-                        v1 = beta;
-                    }
-                }
-                __syncthreads();
-                if (t == 0) {
-                    if (k > M) {
-                        h(k, k - 1) = v1;
-                        h(k + 1, k - 1) = 0.0;
-                        if (k < I - 1) h(k + 2, k - 1) = 0.0;
-                    } else if (M > L) {
-                        h(k, k - 1) = h(k, k - 1) * (1.0 - t1);
-                    }
-                }
-                const double t2 = t1 * v2;
-                const double t3 = (nr == 3) ? t1 * v3 : 0.0;
-                for (int j = k + t; j < d; j += nt) {
-                    double& a0 = h(k, j);
-                    double& a1 = h(k + 1, j);
-                    const double a2v = (nr == 3) ? h(k + 2, j) : 0.0;
-                    const double sum = a0 + v2 * a1 + (nr == 3 ? v3 * a2v : 0.0);
-                    a0 -= sum * t1;
-                    a1 -= sum * t2;
-                    if (nr == 3) h(k + 2, j) = a2v - sum * t3;
-                }
-                __syncthreads();
-                const int jmax = (nr == 3) ? min(k + 3, I) : I;
-                for (int j = t; j <= jmax; j += nt) {
-                    double& a0 = h(j, k);
-                    double& a1 = h(j, k + 1);
-                    const double a2v = (nr == 3) ? h(j, k + 2) : 0.0;
-                    const double sum = a0 + v2 * a1 + (nr == 3 ? v3 * a2v : 0.0);
-                    a0 -= sum * t1;
-                    a1 -= sum * t2;
-                    if (nr == 3) h(j, k + 2) = a2v - sum * t3;
-                }
-                for (int j = t; j < d; j += nt) {
-                    double* z0 = Z + j + (size_t)k * d;
-                    const double a0 = z0[0], a1 = z0[d];
-                    const double a2v = (nr == 3) ? z0[2 * (size_t)d] : 0.0;
-                    const double sum = a0 + v2 * a1 + (nr == 3 ? v3 * a2v : 0.0);
-                    z0[0] = a0 - sum * t1;
-                    z0[d] = a1 - sum * t2;
-                    if (nr == 3) z0[2 * (size_t)d] = a2v - sum * t3;
-                }
-                __syncthreads();
-            }
-        }
-        if (!conv) {
-            if (t == 0) report_failure(status, kFailHqrNoConverge, 1, b, (double)I, (double)L);
-            failed = true;
-            break;
-        }
-        if (L == I) {
-            if (t == 0) {
-                wr[I] = h(I, I);
-                wi[I] = 0.0;
-            }
-        } else {
-            double a = h(I - 1, I - 1), bb = h(I - 1, I), c = h(I, I - 1), dd = h(I, I);
-            double r1r, r1i, r2r, r2i, cs, sn;
-            dlanv2(a, bb, c, dd, r1r, r1i, r2r, r2i, cs, sn);
-            __syncthreads();
-            if (t == 0) {
-                h(I - 1, I - 1) = a;
-                h(I - 1, I) = bb;
-                h(I, I - 1) = c;
-                h(I, I) = dd;
-                wr[I - 1] = r1r;
-                wi[I - 1] = r1i;
-                wr[I] = r2r;
-                wi[I] = r2i;
-            }
-            for (int j = I + 1 + t; j < d; j += nt) {
-                double& x = h(I - 1, j);
-                double& y = h(I, j);
-                const double xv = x, yv = y;
-                x = cs * xv + sn * yv;
-                y = cs * yv - sn * xv;
-            }
-            for (int j = t; j <= I - 2; j += nt) {
-                double& x = h(j, I - 1);
-                double& y = h(j, I);
-                const double xv = x, yv = y;
-                x = cs * xv + sn * yv;
-                y = cs * yv - sn * xv;
-            }
-            for (int j = t; j < d; j += nt) {
-                double* zx = Z + j + (size_t)(I - 1) * d;
-                const double xv = zx[0], yv = zx[d];
-                zx[0] = cs * xv + sn * yv;
-                zx[d] = cs * yv - sn * xv;
-            }
-        }
-        kdefl = 0;
-        I = L - 1;
-        __syncthreads();
-    }
-    __syncthreads();
-    if (failed) return;
-    for (int idx = t; idx < (BW + 4) * d; idx += nt) {
-        const int off = idx / d - 3, c = idx % d, r = c - off;
-        if (r >= 0 && r < d) H[r + (size_t)c * d] = (r > c + 1) ? 0.0 : band[idx];
-    }
-}
-
-// ------------------------------------------------------------------ windowed Francis QR
-// Same iteration as hqr_kernel (dlahqr rules) but each sweep is processed in
-// chunks of QW_STEPS bulge-chase steps: the chunk's (steps+4)^2 diagonal window
-// is staged in shared memory and chased by ONE warp (warp-synchronous), while
-// the chunk's accumulated orthogonal factor U (product of its 3x3 reflectors)
-// is then applied by the whole CTA to the rows right of the window (U^T H),
-// the columns above it (H U) and to Z (Z U) as register-blocked dense updates.
-// This is the dlaqr5 organisation with one bulge: ~5x the flops of applying
-// reflectors one by one, but no block barrier and no L2 round trip per step.
-constexpr int QW_STEPS = 12;
-constexpr int QW = QW_STEPS + 4;  // window width
+// ------------------------------------------------------------------ Francis QR helpers
 
 
 // dlarfg for a 2/3-element bulge column: one rsqrt and one reciprocal.  As in
@@ -578,288 +292,6 @@ __device__ void start_vector_g(const double* H, int d, int m, double rt1r, doubl
     v[2] /= s;
 }
 
-__global__ void __launch_bounds__(256) hqr_window_kernel(double* Hall, double* Zall, double* wrall,
-                                                         double* wiall, int d, DeviceStatus* status) {
-    __shared__ double Wn[QW * QW];  // window, column-major Wn[c*QW + r]
-    __shared__ double Us[QW * QW];  // accumulated factor, column-major
-    __shared__ int s_int;
-    __shared__ double s_t1;
-    const int b = blockIdx.x, t = threadIdx.x, nt = blockDim.x, lane = t & 31, warp = t >> 5;
-    double* H = Hall + (size_t)b * d * d;
-    double* Z = Zall + (size_t)b * d * d;
-    double* wr = wrall + (size_t)b * d;
-    double* wi = wiall + (size_t)b * d;
-    const double ulp = kUlp;
-    const double smlnum = kSafeMin * ((double)d / ulp);
-    const int itmax = 30 * max(10, d);
-    const int kexsh = 10;
-    int kdefl = 0;
-    int I = d - 1;
-    unsigned long long cyc[6] = {0, 0, 0, 0, 0, 0};
-    long long tc = clock64();
-    auto tick = [&](int slot) {
-        const long long now = clock64();
-        cyc[slot] += (unsigned long long)(now - tc);
-        tc = now;
-    };
-    while (I >= 0) {
-        int L = 0;
-        bool conv = false;
-        for (int its = 0; its <= itmax; ++its) {
-            tick(5);
-            int kb = L;
-            for (int k = L + 1 + t; k <= I; k += nt)
-                if (small_subdiag_g(H, d, k, ulp, smlnum)) kb = max(kb, k);
-            L = block_max_int(kb, &s_int);
-            if (L > 0 && t == 0) H[L + (size_t)(L - 1) * d] = 0.0;
-            __syncthreads();
-            if (L >= I - 1) {
-                conv = true;
-                break;
-            }
-            ++kdefl;
-            double h11, h12, h21, h22;
-            if (kdefl % (2 * kexsh) == 0) {
-                const double s = fabs(hg(H, d, I, I - 1)) + fabs(hg(H, d, I - 1, I - 2));
-                h11 = 0.75 * s + hg(H, d, I, I);
-                h12 = -0.4375 * s;
-                h21 = s;
-                h22 = h11;
-            } else if (kdefl % kexsh == 0) {
-                const double s = fabs(hg(H, d, L + 1, L)) + fabs(hg(H, d, L + 2, L + 1));
-                h11 = 0.75 * s + hg(H, d, L, L);
-                h12 = -0.4375 * s;
-                h21 = s;
-                h22 = h11;
-            } else {
-                h11 = hg(H, d, I - 1, I - 1);
-                h21 = hg(H, d, I, I - 1);
-                h12 = hg(H, d, I - 1, I);
-                h22 = hg(H, d, I, I);
-            }
-            double rt1r, rt1i, rt2r, rt2i;
-            {
-                const double s = fabs(h11) + fabs(h12) + fabs(h21) + fabs(h22);
-                if (s == 0.0) {
-                    rt1r = rt1i = rt2r = rt2i = 0.0;
-                } else {
-                    h11 /= s;
-                    h21 /= s;
-                    h12 /= s;
-                    h22 /= s;
-                    const double tr = (h11 + h22) / 2.0;
-                    const double det = (h11 - tr) * (h22 - tr) - h12 * h21;
-                    const double rtdisc = sqrt(fabs(det));
-                    if (det >= 0.0) {
-                        rt1r = tr * s;
-                        rt2r = rt1r;
-                        rt1i = rtdisc * s;
-                        rt2i = -rt1i;
-                    } else {
-                        rt1r = tr + rtdisc;
-                        rt2r = tr - rtdisc;
-                        if (fabs(rt1r - h22) <= fabs(rt2r - h22)) {
-                            rt1r *= s;
-                            rt2r = rt1r;
-                        } else {
-                            rt2r *= s;
-                            rt1r = rt2r;
-                        }
-                        rt1i = rt2i = 0.0;
-                    }
-                }
-            }
-            int mb = L;
-            for (int mm = L + 1 + t; mm <= I - 2; mm += nt) {
-                double vv[3];
-                start_vector_g(H, d, mm, rt1r, rt1i, rt2r, rt2i, vv);
-                const double h00 = fabs(hg(H, d, mm, mm - 1)) * (fabs(vv[1]) + fabs(vv[2]));
-                const double h11b = fabs(vv[0]) * (fabs(hg(H, d, mm - 1, mm - 1)) + fabs(hg(H, d, mm, mm)) +
-                                                   fabs(hg(H, d, mm + 1, mm + 1)));
-                if (h00 <= ulp * h11b) mb = max(mb, mm);
-            }
-            const int M = block_max_int(mb, &s_int);
-            double v0[3];
-            start_vector_g(H, d, M, rt1r, rt1i, rt2r, rt2i, v0);
-            if (t == 0) {
-                atomicAdd(&status->qr_sweeps, 1ull);
-                atomicAdd(&status->qr_steps, (unsigned long long)(I - M));
-            }
-            tick(0);
-            for (int k0 = M; k0 <= I - 1;) {
-                const int ns = min(QW_STEPS, I - k0);
-                const int wlo = (k0 > M) ? k0 - 1 : k0;
-                const int whi = min(k0 + ns + 2, I);
-                const int nw = whi - wlo + 1;
-                for (int idx = t; idx < QW * QW; idx += nt) {
-                    const int r = idx % QW, c = idx / QW;
-                    Wn[idx] = (r < nw && c < nw) ? H[(wlo + r) + (size_t)(wlo + c) * d] : 0.0;
-                    Us[idx] = (r == c) ? 1.0 : 0.0;
-                }
-                __syncthreads();
-                tick(1);
-                if (warp == 0) {
-                    auto W = [&](int r, int c) -> double& { return Wn[(c - wlo) * QW + (r - wlo)]; };
-                    for (int k = k0; k < k0 + ns; ++k) {
-                        const int nr = min(3, I - k + 1);
-                        double v1, v2, v3;
-                        if (k > M) {
-                            v1 = W(k, k - 1);
-                            v2 = W(k + 1, k - 1);
-                            v3 = (nr == 3) ? W(k + 2, k - 1) : 0.0;
-                        } else {
-                            v1 = v0[0];
-                            v2 = v0[1];
-                            v3 = (nr == 3) ? v0[2] : 0.0;
-                        }
-                        if (nr != 3) v3 = 0.0;
-                        double bt;
-                        const double t1 = house3(v1, v2, v3, bt);
-                        v1 = bt;
-                        const double t2 = t1 * v2, t3 = t1 * v3;
-                        __syncwarp();
-                        // row op: rows k..k+nr-1, columns k..whi (in window)
-                        for (int c = k + lane; c <= whi; c += 32) {
-                            double& a0 = W(k, c);
-                            double& a1 = W(k + 1, c);
-                            const double a2v = (nr == 3) ? W(k + 2, c) : 0.0;
-                            const double sum = a0 + v2 * a1 + v3 * a2v;
-                            a0 -= sum * t1;
-                            a1 -= sum * t2;
-                            if (nr == 3) W(k + 2, c) = a2v - sum * t3;
-                        }
-                        __syncwarp();
-                        if (lane == 0) {
-                            if (k > M) {
-                                W(k, k - 1) = v1;
-                                W(k + 1, k - 1) = 0.0;
-                                if (k < I - 1) W(k + 2, k - 1) = 0.0;
-                            } else {
-                                s_t1 = t1;  // H(M, M-1) *= (1 - t1) after the chunk (outside the window)
-                            }
-                        }
-                        // column op: rows wlo..min(k+3, I), columns k..k+nr-1 (in window), and U
-                        const int rmax = (nr == 3) ? min(k + 3, I) : I;
-                        for (int r = wlo + lane; r <= rmax && r <= whi; r += 32) {
-                            double& a0 = W(r, k);
-                            double& a1 = W(r, k + 1);
-                            const double a2v = (nr == 3) ? W(r, k + 2) : 0.0;
-                            const double sum = a0 + v2 * a1 + v3 * a2v;
-                            a0 -= sum * t1;
-                            a1 -= sum * t2;
-                            if (nr == 3) W(r, k + 2) = a2v - sum * t3;
-                        }
-                        for (int r = lane; r < nw; r += 32) {
-                            double* u = Us + r;
-                            const int c = k - wlo;
-                            const double u0 = u[c * QW], u1 = u[(c + 1) * QW];
-                            const double u2 = (nr == 3) ? u[(c + 2) * QW] : 0.0;
-                            const double sum = u0 + v2 * u1 + v3 * u2;
-                            u[c * QW] = u0 - sum * t1;
-                            u[(c + 1) * QW] = u1 - sum * t2;
-                            if (nr == 3) u[(c + 2) * QW] = u2 - sum * t3;
-                        }
-                        __syncwarp();
-                    }
-                }
-                __syncthreads();
-                tick(2);
-                for (int idx = t; idx < nw * nw; idx += nt) {
-                    const int r = idx % nw, c = idx / nw;
-                    H[(wlo + r) + (size_t)(wlo + c) * d] = Wn[c * QW + r];
-                }
-                if (k0 == M && M > L && t == 0) H[M + (size_t)(M - 1) * d] *= (1.0 - s_t1);
-                // off-window updates with U (QW x QW, zero-padded beyond nw)
-                const int n_right = d - 1 - whi, n_above = wlo;
-                for (int task = t; task < n_right + n_above + d; task += nt) {
-                    double x[QW];
-                    if (task < n_right) {  // column c right of the window: U^T x
-                        double* col = H + (size_t)(whi + 1 + task) * d + wlo;
-#pragma unroll
-                        for (int q = 0; q < QW; ++q) x[q] = (q < nw) ? col[q] : 0.0;
-#pragma unroll 4
-                        for (int r = 0; r < nw; ++r) {
-                            double acc = 0.0;
-#pragma unroll
-                            for (int q = 0; q < QW; ++q) acc = fma(Us[r * QW + q], x[q], acc);
-                            col[r] = acc;
-                        }
-                    } else {  // row (of H above the window, or of Z): x U
-                        const bool isz = task >= n_right + n_above;
-                        const int i = isz ? task - n_right - n_above : task - n_right;
-                        double* base = (isz ? Z : H) + i + (size_t)wlo * d;
-#pragma unroll
-                        for (int q = 0; q < QW; ++q) x[q] = (q < nw) ? base[(size_t)q * d] : 0.0;
-#pragma unroll 4
-                        for (int c = 0; c < nw; ++c) {
-                            double acc = 0.0;
-#pragma unroll
-                            for (int q = 0; q < QW; ++q) acc = fma(x[q], Us[c * QW + q], acc);
-                            base[(size_t)c * d] = acc;
-                        }
-                    }
-                }
-                __syncthreads();
-                tick(3);
-                k0 += ns;
-            }
-        }
-        if (!conv) {
-            if (t == 0) report_failure(status, kFailHqrNoConverge, 1, b, (double)I, (double)L);
-            return;
-        }
-        if (L == I) {
-            if (t == 0) {
-                wr[I] = hg(H, d, I, I);
-                wi[I] = 0.0;
-            }
-        } else {
-            double a = hg(H, d, I - 1, I - 1), bb = hg(H, d, I - 1, I), c = hg(H, d, I, I - 1),
-                   dd = hg(H, d, I, I);
-            double r1r, r1i, r2r, r2i, cs, sn;
-            dlanv2(a, bb, c, dd, r1r, r1i, r2r, r2i, cs, sn);
-            __syncthreads();
-            if (t == 0) {
-                H[(I - 1) + (size_t)(I - 1) * d] = a;
-                H[(I - 1) + (size_t)I * d] = bb;
-                H[I + (size_t)(I - 1) * d] = c;
-                H[I + (size_t)I * d] = dd;
-                wr[I - 1] = r1r;
-                wi[I - 1] = r1i;
-                wr[I] = r2r;
-                wi[I] = r2i;
-            }
-            for (int j = I + 1 + t; j < d; j += nt) {
-                double* x = H + (I - 1) + (size_t)j * d;
-                const double xv = x[0], yv = x[1];
-                x[0] = cs * xv + sn * yv;
-                x[1] = cs * yv - sn * xv;
-            }
-            for (int j = t; j <= I - 2; j += nt) {
-                double* x = H + j + (size_t)(I - 1) * d;
-                const double xv = x[0], yv = x[d];
-                x[0] = cs * xv + sn * yv;
-                x[d] = cs * yv - sn * xv;
-            }
-            for (int j = t; j < d; j += nt) {
-                double* zx = Z + j + (size_t)(I - 1) * d;
-                const double xv = zx[0], yv = zx[d];
-                zx[0] = cs * xv + sn * yv;
-                zx[d] = cs * yv - sn * xv;
-            }
-        }
-        kdefl = 0;
-        I = L - 1;
-        __syncthreads();
-    }
-    if (t == 0)
-        for (int q = 0; q < 6; ++q) atomicAdd(&status->qr_cycles[q], cyc[q]);
-    // zero the sub-subdiagonal entries left from the bulges
-    for (int idx = t; idx < d * d; idx += nt) {
-        const int r = idx % d, c = idx / d;
-        if (r > c + 1) H[idx] = 0.0;
-    }
-}
 
 
 // ------------------------------------------------------------------ multi-bulge Francis QR
@@ -875,7 +307,7 @@ __global__ void __launch_bounds__(256) hqr_window_kernel(double* Hall, double* Z
 // bottom-to-top bulge order.  Chunks of MS steps are chased in a MW x MW
 // shared-memory window; U is applied to the rest of H and to Z by the whole
 // CTA.  Small active blocks and exceptional-shift sweeps use one bulge with
-// the dlahqr shift / start rules (identical to hqr_window_kernel).
+// the dlahqr shift / start rules.
 constexpr int MB_MAX = 4;   // bulges per sweep
 constexpr int MS = 19;      // chase steps per chunk with MB_MAX bulges (MW - 3 (nb - 1) - 4 for nb)
 constexpr int MW = 32;      // window (>= MS + 3 (MB_MAX - 1) + 4)
@@ -2024,130 +1456,6 @@ __device__ void solve2r(double c00, double c01, double c10, double c11, double b
     x1 = pc ? xp : xq;
 }
 
-// ------------------------------------------------------------------ eigenvectors
-// dtrevc right eigenvectors of the quasi-triangular T, warp per eigenvalue
-// (complex pairs handled by the first index, packed Re/Im columns).
-__global__ void trevc_kernel(const double* Tall, const double* wrall, const double* wiall,
-                             double* Yall, int d) {
-    extern __shared__ double sm[];
-    const int b = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5,
-              nw = blockDim.x >> 5;
-    const double* T = Tall + (size_t)b * d * d;
-    const double* wr = wrall + (size_t)b * d;
-    const double* wi = wiall + (size_t)b * d;
-    double* Y = Yall + (size_t)b * d * d;
-    double* re = sm + (size_t)w * 2 * d;
-    double* im = re + d;
-    const double smlnum = kSafeMin * ((double)d / kUlp);
-    auto Tat = [&](int r, int c) { return T[r + (size_t)c * d]; };
-    for (int ki = w; ki < d; ki += nw) {
-        const double wik = wi[ki];
-        if (wik < 0.0) continue;
-        if (wik == 0.0) {
-            const double lam = wr[ki];
-            const double smin = fmax(kUlp * fabs(lam), smlnum);
-            for (int k = lane; k < ki; k += 32) re[k] = -Tat(k, ki);
-            if (lane == 0) re[ki] = 1.0;
-            __syncwarp();
-            int j = ki - 1;
-            while (j >= 0) {
-                if (j > 0 && Tat(j, j - 1) != 0.0) {
-                    cplx x0, x1;
-                    solve2(cmk(Tat(j - 1, j - 1) - lam, 0), cmk(Tat(j - 1, j), 0),
-                           cmk(Tat(j, j - 1), 0), cmk(Tat(j, j) - lam, 0), cmk(re[j - 1], 0),
-                           cmk(re[j], 0), smin, x0, x1);
-                    __syncwarp();
-                    for (int k = lane; k < j - 1; k += 32)
-                        re[k] -= x0.re * Tat(k, j - 1) + x1.re * Tat(k, j);
-                    if (lane == 0) {
-                        re[j - 1] = x0.re;
-                        re[j] = x1.re;
-                    }
-                    j -= 2;
-                } else {
-                    double den = Tat(j, j) - lam;
-                    if (fabs(den) < smin) den = smin;
-                    const double x = re[j] / den;
-                    __syncwarp();
-                    for (int k = lane; k < j; k += 32) re[k] -= x * Tat(k, j);
-                    if (lane == 0) re[j] = x;
-                    j -= 1;
-                }
-                __syncwarp();
-            }
-            double* yc = Y + (size_t)ki * d;
-            for (int k = lane; k < d; k += 32) yc[k] = (k <= ki) ? re[k] : 0.0;
-        } else {
-            const int p = ki, q = ki + 1;
-            const cplx lam = cmk(wr[p], wik);
-            const double smin = fmax(kUlp * (fabs(wr[p]) + fabs(wik)), smlnum);
-            double xpr, xqi;
-            if (fabs(Tat(p, q)) >= fabs(Tat(q, p))) {
-                xpr = 1.0;
-                xqi = wik / Tat(p, q);
-            } else {
-                xpr = -wik / Tat(q, p);
-                xqi = 1.0;
-            }
-            for (int k = lane; k < p; k += 32) {
-                re[k] = -xpr * Tat(k, p);
-                im[k] = -xqi * Tat(k, q);
-            }
-            if (lane == 0) {
-                re[p] = xpr;
-                im[p] = 0.0;
-                re[q] = 0.0;
-                im[q] = xqi;
-            }
-            __syncwarp();
-            int j = p - 1;
-            while (j >= 0) {
-                if (j > 0 && Tat(j, j - 1) != 0.0) {
-                    cplx x0, x1;
-                    solve2(cmk(Tat(j - 1, j - 1), 0) - lam, cmk(Tat(j - 1, j), 0),
-                           cmk(Tat(j, j - 1), 0), cmk(Tat(j, j), 0) - lam, cmk(re[j - 1], im[j - 1]),
-                           cmk(re[j], im[j]), smin, x0, x1);
-                    __syncwarp();
-                    for (int k = lane; k < j - 1; k += 32) {
-                        const double a = Tat(k, j - 1), c = Tat(k, j);
-                        re[k] -= x0.re * a + x1.re * c;
-                        im[k] -= x0.im * a + x1.im * c;
-                    }
-                    if (lane == 0) {
-                        re[j - 1] = x0.re;
-                        im[j - 1] = x0.im;
-                        re[j] = x1.re;
-                        im[j] = x1.im;
-                    }
-                    j -= 2;
-                } else {
-                    cplx den = cmk(Tat(j, j), 0) - lam;
-                    if (cabs_(den) < smin) den = cmk(smin, 0.0);
-                    const cplx x = cdiv(cmk(re[j], im[j]), den);
-                    __syncwarp();
-                    for (int k = lane; k < j; k += 32) {
-                        const double a = Tat(k, j);
-                        re[k] -= x.re * a;
-                        im[k] -= x.im * a;
-                    }
-                    if (lane == 0) {
-                        re[j] = x.re;
-                        im[j] = x.im;
-                    }
-                    j -= 1;
-                }
-                __syncwarp();
-            }
-            double* yr = Y + (size_t)p * d;
-            double* yi = Y + (size_t)q * d;
-            for (int k = lane; k < d; k += 32) {
-                yr[k] = (k <= q) ? re[k] : 0.0;
-                yi[k] = (k <= q) ? im[k] : 0.0;
-            }
-        }
-        __syncwarp();
-    }
-}
 
 
 // Register-resident dtrevc: warp per eigenvalue (complex pairs by their first
@@ -2155,7 +1463,7 @@ __global__ void trevc_kernel(const double* Tall, const double* wrall, const doub
 // broadcast by shuffle and the T columns of the NEXT step are loaded while the
 // current one is applied (the serial chain is shuffle + divide + FMA, not an
 // L2 round trip).  Same arithmetic and dlaln2-style smin perturbation as
-// trevc_kernel.  pf[c] = 1 when T(c, c-1) != 0 (second row of a 2x2 block).
+// LAPACK dtrevc.  pf[c] = 1 when T(c, c-1) != 0 (second row of a 2x2 block).
 template <int RPL>
 __global__ void __launch_bounds__(256) trevc_reg_kernel(const double* Tall, const double* wrall,
                                                         const double* wiall, double* Yall, int d) {
@@ -2683,124 +1991,6 @@ __global__ void residual_kernel(ResidualArgs a) {
 constexpr int QBS = 32;   // row block
 constexpr int QCT = 32;   // column tile
 
-__global__ void __launch_bounds__(256) qtri_blocked_kernel(const double* Tall, int d, long long t_stride,
-                                                           double* Wall, int ncol, long long w_stride,
-                                                           const double* sigma, const int* kind,
-                                                           const int* t_index) {
-    extern __shared__ double sm[];
-    const int ld = QCT + 1;               // tile columns (+1 for a pair straddling the edge)
-    double* Y = sm;                       // d x ld, row-major Y[k*ld + c]
-    double* Td = Y + (size_t)d * ld;      // (QBS+1)^2 diagonal block, Td[r*(QBS+1)+c]
-    __shared__ int s_kind[QCT + 1];
-    __shared__ double s_sig[2 * (QCT + 1)];
-    const int tiles = (ncol + QCT - 1) / QCT;
-    const int b = blockIdx.x / tiles, c0 = (blockIdx.x % tiles) * QCT;
-    const double* T = Tall + (size_t)(t_index ? t_index[b] : b) * t_stride;
-    double* W = Wall + (size_t)b * w_stride;
-    const int t = threadIdx.x, nt = blockDim.x;
-    const int width = min(QCT + 1, ncol - c0);
-    for (int c = t; c < QCT + 1; c += nt) {
-        const int gc = c0 + c;
-        int k = (c < width) ? kind[(size_t)b * ncol + gc] : 2;
-        if (c == 0 && k == 2 && gc > 0 && kind[(size_t)b * ncol + gc - 1] == 1) k = 3;  // Im half owned by previous tile
-        if (c == QCT && k != 1) k = 2;  // extra column only for a straddling pair
-        s_kind[c] = k;
-        s_sig[2 * c] = (c < width) ? sigma[2 * ((size_t)b * ncol + gc)] : 0.0;
-        s_sig[2 * c + 1] = (c < width) ? sigma[2 * ((size_t)b * ncol + gc) + 1] : 0.0;
-    }
-    // the tile's last column: include the Im partner of a pair that starts at QCT-1
-    for (int idx = t; idx < d * ld; idx += nt) {
-        const int k = idx / ld, c = idx % ld;
-        Y[idx] = (c < width) ? W[(size_t)(c0 + c) * d + k] : 0.0;
-    }
-    __syncthreads();
-    const bool extra = (width == QCT + 1) && s_kind[QCT - 1] == 1;
-    const int r_t = t & 31, cg = t >> 5;  // update-phase mapping: row r_t, columns cg*4..cg*4+3
-    int j1 = d;
-    while (j1 > 0) {
-        int j0 = max(0, j1 - QBS);
-        if (j0 > 0 && T[j0 + (size_t)(j0 - 1) * d] != 0.0) --j0;  // keep 2x2 blocks whole
-        const int nb = j1 - j0;
-        // (a) panel update rows [j0, j1): Y[J,:] -= T[J, j1:] Y[j1:, :]
-        if (j1 < d) {
-            for (int rr = r_t; rr < nb; rr += 32) {
-                double acc[5] = {0, 0, 0, 0, 0};
-                const double* trow = T + j0 + rr;
-                for (int k = j1; k < d; ++k) {
-                    const double tv = trow[(size_t)k * d];
-                    const double* yk = Y + (size_t)k * ld + cg * 4;
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) acc[q] = fma(tv, yk[q], acc[q]);
-                    if (cg == 7) acc[4] = fma(tv, Y[(size_t)k * ld + QCT], acc[4]);
-                }
-                double* yr = Y + (size_t)(j0 + rr) * ld + cg * 4;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) yr[q] -= acc[q];
-                if (cg == 7) Y[(size_t)(j0 + rr) * ld + QCT] -= acc[4];
-            }
-        }
-        for (int idx = t; idx < nb * nb; idx += nt) {
-            const int r = idx % nb, c = idx / nb;
-            Td[r * (QBS + 1) + c] = T[(j0 + r) + (size_t)(j0 + c) * d];
-        }
-        __syncthreads();
-        // (b) diagonal block, one thread per column (pairs: the Re column's thread)
-        if (t < QCT + 1) {
-            const int kd = s_kind[t];
-            const bool run = (kd == 0 || kd == 1) && (t < QCT || extra);
-            if (run) {
-                const bool cx = kd == 1;
-                const cplx sg = cmk(s_sig[2 * t], s_sig[2 * t + 1]);
-                auto TD = [&](int r, int c) { return Td[r * (QBS + 1) + c]; };
-                int j = nb - 1;
-                while (j >= 0) {
-                    if (j > 0 && TD(j, j - 1) != 0.0) {
-                        const cplx b0 = cmk(Y[(size_t)(j0 + j - 1) * ld + t], cx ? Y[(size_t)(j0 + j - 1) * ld + t + 1] : 0.0);
-                        const cplx b1 = cmk(Y[(size_t)(j0 + j) * ld + t], cx ? Y[(size_t)(j0 + j) * ld + t + 1] : 0.0);
-                        cplx x0, x1;
-                        solve2(cmk(TD(j - 1, j - 1), 0) - sg, cmk(TD(j - 1, j), 0), cmk(TD(j, j - 1), 0),
-                               cmk(TD(j, j), 0) - sg, b0, b1, 0.0, x0, x1);
-                        for (int k = 0; k < j - 1; ++k) {
-                            const double a0 = TD(k, j - 1), a1 = TD(k, j);
-                            double* yk = Y + (size_t)(j0 + k) * ld + t;
-                            yk[0] -= x0.re * a0 + x1.re * a1;
-                            if (cx) yk[1] -= x0.im * a0 + x1.im * a1;
-                        }
-                        Y[(size_t)(j0 + j - 1) * ld + t] = x0.re;
-                        Y[(size_t)(j0 + j) * ld + t] = x1.re;
-                        if (cx) {
-                            Y[(size_t)(j0 + j - 1) * ld + t + 1] = x0.im;
-                            Y[(size_t)(j0 + j) * ld + t + 1] = x1.im;
-                        }
-                        j -= 2;
-                    } else {
-                        const cplx rhs = cmk(Y[(size_t)(j0 + j) * ld + t], cx ? Y[(size_t)(j0 + j) * ld + t + 1] : 0.0);
-                        const cplx x = cdiv(rhs, cmk(TD(j, j), 0) - sg);
-                        for (int k = 0; k < j; ++k) {
-                            const double a = TD(k, j);
-                            double* yk = Y + (size_t)(j0 + k) * ld + t;
-                            yk[0] -= x.re * a;
-                            if (cx) yk[1] -= x.im * a;
-                        }
-                        Y[(size_t)(j0 + j) * ld + t] = x.re;
-                        if (cx) Y[(size_t)(j0 + j) * ld + t + 1] = x.im;
-                        j -= 1;
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        j1 = j0;
-    }
-    // write back the columns this tile owns (a straddling pair's Im column too)
-    for (int idx = t; idx < d * ld; idx += nt) {
-        const int k = idx / ld, c = idx % ld;
-        if (c >= width) continue;
-        if (c == QCT && !extra) continue;
-        if (s_kind[c] == 3) continue;  // owned by the previous tile
-        W[(size_t)(c0 + c) * d + k] = Y[idx];
-    }
-}
 
 // ------------------------------------------------------------------ eigenbasis solves
 // (Lambda - sigma_c) y_c = w_c with Lambda the real-packed eigenvalue matrix of
@@ -2810,7 +2000,7 @@ __global__ void __launch_bounds__(256) qtri_blocked_kernel(const double* Tall, i
 // quasi-triangular back substitution: every (matrix, column, eigen-block) is
 // independent.  The 2x2 block is diagonalised exactly (eigenvectors [1, +-i])
 // so a shift next to a + ib loses no accuracy to cancellation in its
-// determinant.  Column kinds as for launch_qtri_solve: 0 real, 1 complex pair
+// determinant.  Column kinds: 0 real, 1 complex pair
 // (c: Re, c+1: Im), 2 skip.
 __global__ void eig_diag_solve_kernel(double* Wall, int d, int ncol, long long w_stride,
                                       const double* wrall, const double* wiall,
@@ -2902,77 +2092,25 @@ void launch_hessenberg(double* A, double* Z, int d, int batch, cudaStream_t st) 
 
 void launch_hqr(double* H, double* Z, double* wr, double* wi, int d, int batch,
                 DeviceStatus* status, cudaStream_t st) {
-    const size_t smem = (size_t)(BW + 4) * d * sizeof(double);
-    static unsigned long long attr = 0;
-    smem_attr_once(hqr_kernel, 200 * 1024, attr);
-    static const char* mode = std::getenv("VRTE_HQR");  // multi (default) | window | band
-    if (!mode || std::string(mode) == "multi") {
-        static const int aed_nw = std::getenv("VRTE_AED_NW") ? std::atoi(std::getenv("VRTE_AED_NW")) : AED_NW;
-        static const int nb4 = std::getenv("VRTE_NB4_MIN") ? std::atoi(std::getenv("VRTE_NB4_MIN")) : 48;
-        static const int nb2 = std::getenv("VRTE_NB2_MIN") ? std::atoi(std::getenv("VRTE_NB2_MIN")) : 24;
-        static const int nibble = std::getenv("VRTE_NIBBLE") ? std::atoi(std::getenv("VRTE_NIBBLE")) : 40;
-        static const char* trace_path = std::getenv("VRTE_QR_TRACE");
-        static double* trace = nullptr;
-        static int trace_n = 0;
-        if (trace_path && trace_n < batch) {
-            if (trace) cudaFree(trace);
-            VRTE_CUDA_CHECK(cudaMalloc(&trace, sizeof(double) * 8 * batch));
-            trace_n = batch;
-        }
-        // 2-CTA clusters: rank 0 chases / deflates, rank 1 applies the chunk factors
-        hqr_multi_kernel<<<2 * batch, 256, 0, st>>>(H, Z, wr, wi, d, status, min(max(aed_nw, 4), MW), nb4, nb2,
-                                                nibble, trace_path ? trace : nullptr);
-        if (trace_path) {
-            std::vector<double> h((size_t)8 * batch);
-            VRTE_CUDA_CHECK(cudaMemcpyAsync(h.data(), trace, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
-            VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
-            if (FILE* f = std::fopen(trace_path, "w")) {
-                std::fprintf(f, "matrix,cycles,reflectors,sweeps,aed_calls,aed_cycles,chase_cycles,update_cycles,aed_deflations\n");
-                for (int q = 0; q < batch; ++q)
-                    std::fprintf(f, "%d,%.0f,%.0f,%.0f,%.0f,%.0f,%.0f,%.0f,%.0f\n", q, h[8 * q], h[8 * q + 1], h[8 * q + 2],
-                                 h[8 * q + 3], h[8 * q + 4], h[8 * q + 5], h[8 * q + 6], h[8 * q + 7]);
-                std::fclose(f);
-            }
-        }
-    } else if (std::string(mode) == "window") {
-        hqr_window_kernel<<<batch, 256, 0, st>>>(H, Z, wr, wi, d, status);
-    } else {
-        hqr_kernel<<<batch, NT, smem, st>>>(H, Z, wr, wi, d, status);
-    }
+    // 2-CTA clusters: rank 0 chases / deflates, rank 1 applies the chunk factors
+    hqr_multi_kernel<<<2 * batch, 256, 0, st>>>(H, Z, wr, wi, d, status, AED_NW, 48, 24, 40, nullptr);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
 void launch_trevc(const double* T, const double* wr, const double* wi, double* Y, int d,
                   int batch, cudaStream_t st) {
-    const int warps = 8;
-    const size_t smem = (size_t)warps * 2 * d * sizeof(double);
-    static unsigned long long attr = 0;
-    smem_attr_once(trevc_kernel, 200 * 1024, attr);
-    static const char* tmode = std::getenv("VRTE_TREVC");  // reg (default) | smem
-    if (tmode && std::string(tmode) == "smem") {
-        trevc_kernel<<<batch, warps * 32, smem, st>>>(T, wr, wi, Y, d);
-    } else {
-        const int rpl = (d + 31) / 32;
-        static const char* grp = std::getenv("VRTE_TREVC_GROUP");  // default on
-        const size_t gsm = 3 * (size_t)d * sizeof(double) + (size_t)d * sizeof(int);
-        if (!(grp && std::string(grp) == "0") && rpl <= 8) {
-            if (rpl <= 2)
-                trevc_grp_kernel<2, 4><<<dim3(batch, (d + 15) / 16), 128, gsm, st>>>(T, wr, wi, Y, d);
-            else if (rpl <= 4)
-                trevc_grp_kernel<4, 4><<<dim3(batch, (d + 15) / 16), 128, gsm, st>>>(T, wr, wi, Y, d);
-            else
-                trevc_grp_kernel<8, 4><<<dim3(batch, (d + 15) / 16), 128, gsm, st>>>(T, wr, wi, Y, d);
-        } else if (rpl <= 2)
-            trevc_reg_kernel<2><<<batch, 256, d, st>>>(T, wr, wi, Y, d);
-        else if (rpl <= 4)
-            trevc_reg_kernel<4><<<batch, 256, d, st>>>(T, wr, wi, Y, d);
-        else if (rpl <= 8)
-            trevc_reg_kernel<8><<<batch, 256, d, st>>>(T, wr, wi, Y, d);
-        else if (rpl <= 16)
-            trevc_reg_kernel<16><<<batch, 256, d, st>>>(T, wr, wi, Y, d);
-        else
-            trevc_reg_kernel<32><<<batch, 256, d, st>>>(T, wr, wi, Y, d);
-    }
+    const int rpl = (d + 31) / 32;
+    const size_t gsm = 3 * (size_t)d * sizeof(double) + (size_t)d * sizeof(int);
+    if (rpl <= 2)
+        trevc_grp_kernel<2, 4><<<dim3(batch, (d + 15) / 16), 128, gsm, st>>>(T, wr, wi, Y, d);
+    else if (rpl <= 4)
+        trevc_grp_kernel<4, 4><<<dim3(batch, (d + 15) / 16), 128, gsm, st>>>(T, wr, wi, Y, d);
+    else if (rpl <= 8)
+        trevc_grp_kernel<8, 4><<<dim3(batch, (d + 15) / 16), 128, gsm, st>>>(T, wr, wi, Y, d);
+    else if (rpl <= 16)
+        trevc_reg_kernel<16><<<batch, 256, d, st>>>(T, wr, wi, Y, d);
+    else
+        trevc_reg_kernel<32><<<batch, 256, d, st>>>(T, wr, wi, Y, d);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -2994,17 +2132,6 @@ void launch_residual(const ResidualArgs& a, cudaStream_t st) {
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_qtri_solve(const double* T, int d, long long t_stride, double* W, int ncol,
-                       long long w_stride, const double* sigma, const int* kind, int batch,
-                       const int* t_index, cudaStream_t st) {
-    const size_t smem = ((size_t)d * (QCT + 1) + (size_t)(QBS + 1) * (QBS + 1)) * sizeof(double);
-    static unsigned long long attr = 0;
-    smem_attr_once(qtri_blocked_kernel, 200 * 1024, attr);
-    const int tiles = (ncol + QCT - 1) / QCT;
-    qtri_blocked_kernel<<<(unsigned)(batch * tiles), 256, smem, st>>>(T, d, t_stride, W, ncol, w_stride,
-                                                                     sigma, kind, t_index);
-    VRTE_CUDA_CHECK(cudaGetLastError());
-}
 
 void launch_eig_diag_solve(double* W, int d, int ncol, long long w_stride, const double* wr,
                            const double* wi, const double* sigma, const int* kind, int batch,

@@ -264,7 +264,7 @@ void gemm_batched(const GemmBatch& g, cudaStream_t stream) {
     if ((g.amap && (g.trans_a || g.k > kMaxMapK)) || (g.bmap && g.trans_b))
         throw std::invalid_argument("gemm_batched: index maps need untransposed operands and k <= 256");
     const bool mapped = g.amap || g.bmap || g.cmap;
-    static const int small_minb = std::getenv("VRTE_GEMM_SMALL_MINB") ? std::atoi(std::getenv("VRTE_GEMM_SMALL_MINB")) : 3;
+    constexpr int small_minb = 3;
     if (g.k <= 96)
         gemm_batched_cfg(g, stream, 16, 2, mapped ? 2 : small_minb);  // the mapped kernel needs the register budget
     else

@@ -83,15 +83,11 @@ struct ResidualArgs {
     double* residual;  // [batch][d]
 };
 void launch_residual(const ResidualArgs& a, cudaStream_t st);
-// Quasi-triangular shifted solves (T - sigma_c I) y_c = w_c, in place in W.
-// kind[c]: 0 real column, 1 complex pair (c: Re, c+1: Im), 2 skip.
-// sigma: [batch][ncol][2]; T: [batch][d*d].
-void launch_qtri_solve(const double* T, int d, long long t_stride, double* W, int ncol,
-                       long long w_stride, const double* sigma, const int* kind, int batch,
-                       const int* t_index, cudaStream_t st);
 
-// Same contract as launch_qtri_solve, but in the eigenbasis of F E: W must
+// Shifted solves (F E - sigma_c I) y_c = r_c in the eigenbasis of F E: W must
 // already hold V^-1 R; on return it holds (Lambda - sigma_c)^-1 V^-1 R.
+// kind[c]: 0 real column, 1 complex pair (c: Re, c+1: Im), 2 skip;
+// sigma: [batch][ncol][2].
 void launch_eig_diag_solve(double* W, int d, int ncol, long long w_stride, const double* wr,
                            const double* wi, const double* sigma, const int* kind, int batch,
                            cudaStream_t st);

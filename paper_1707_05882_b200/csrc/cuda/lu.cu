@@ -573,8 +573,7 @@ void trsm_launch(const double* A, int G, int lda, double* M, int ld, long long s
     if (jb <= 0 || c_hi <= c_lo) return;
     // wide right-hand sides (the factorization's U12 blocks): column-per-lane;
     // narrow ones (the 256-column solves) keep enough CTAs with lanes over rows
-    static const char* mode = std::getenv("VRTE_TRSM");  // shfl | col | (auto)
-    const bool shfl = mode ? std::string(mode) == "shfl" : (c_hi - c_lo) < 512;
+    const bool shfl = (c_hi - c_lo) < 512;
     if (shfl) {
         dim3 grid((c_hi - c_lo + SW_TILE - 1) / SW_TILE, batch);
         lu_trsm_rm_kernel<LOWER><<<grid, 256, 0, st>>>(A, G, lda, (long long)G * lda, M, ld, strideM, k0, jb, c_lo,
@@ -587,10 +586,7 @@ void trsm_launch(const double* A, int G, int lda, double* M, int ld, long long s
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
-int outer_block() {
-    static const int ob = std::getenv("VRTE_LU_NB") ? std::atoi(std::getenv("VRTE_LU_NB")) : OB_MAX;
-    return ob == 64 ? 64 : OB_MAX;
-}
+int outer_block() { return OB_MAX; }
 
 }  // namespace
 
@@ -650,7 +646,7 @@ void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatu
 // the row map, down to row_lo; then the solution rows [row_lo, G) are
 // gathered in unknown order into X [batch][G][R].
 __global__ void lu_gather_aug_kernel(const double* Aall, int G, int lda, int R, const int* perm_all, int row_lo,
-                                     double* X, int batch) {
+                                     double* X, int batch, int c0) {
     const long long total = (long long)batch * (G - row_lo) * R;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
@@ -658,36 +654,52 @@ __global__ void lu_gather_aug_kernel(const double* Aall, int G, int lda, int R, 
         const long long rb = e / R;
         const int i = row_lo + (int)(rb % (G - row_lo)), b = (int)(rb / (G - row_lo));
         X[((size_t)b * G + i) * R + c] =
-            Aall[(size_t)b * G * lda + (size_t)perm_all[(size_t)b * G + i] * lda + G + c];
+            Aall[(size_t)b * G * lda + (size_t)perm_all[(size_t)b * G + i] * lda + c0 + c];
     }
 }
 
-void lu_backsolve_aug(double* A, int G, int lda, int R, int batch, const int* perm, double* X, int row_lo,
+namespace {
+// Back substitution of columns [c0, c0 + nc) of the augmented factorization in
+// place, blocks bk_hi .. blo (64 rows each): outer steps of 2 x 64 rows (the
+// two triangular solves with the 64 x 64 coupling update between them), then
+// ONE update of the rows above down to blo's first row with k = 128 (the
+// long-k GEMM runs near the DMMA rate; k = 64 does not).
+void backsolve_blocks(double* A, int G, int lda, int c0, int nc, int batch, const int* perm, int bk_hi, int blo,
                       cudaStream_t st) {
     const long long gg = (long long)G * lda;
-    const int nblk = (G + LU_NB - 1) / LU_NB;
-    const int blo = max(0, row_lo) / LU_NB, rl = blo * LU_NB;
-    // outer blocks of 2 x 64 rows: the two triangular solves with the 64 x 64
-    // coupling update between them, then ONE update of every row above with
-    // k = 128 (the long-k GEMM runs near the DMMA rate; k = 64 does not)
-    for (int bk = nblk - 1; bk >= blo; bk -= 2) {
+    const int rl = blo * LU_NB;
+    for (int bk = bk_hi; bk >= blo; bk -= 2) {
         const int k1 = bk * LU_NB, jb1 = min(LU_NB, G - k1);
-        trsm_launch<false>(A, G, lda, A + G, lda, gg, k1, jb1, 0, R, batch, st, perm, perm);
+        trsm_launch<false>(A, G, lda, A + c0, lda, gg, k1, jb1, 0, nc, batch, st, perm, perm);
         int k0 = k1, jb = jb1;
         if (bk - 1 >= blo) {
             k0 = k1 - LU_NB;
-            rm_gemm(LU_NB, R, jb1, A + k1, lda, gg, A + G, lda, gg, A + G, lda, gg, batch, -1.0, 1.0, st, perm + k0,
+            rm_gemm(LU_NB, nc, jb1, A + k1, lda, gg, A + c0, lda, gg, A + c0, lda, gg, batch, -1.0, 1.0, st, perm + k0,
                     perm + k1, perm + k0, G);
-            trsm_launch<false>(A, G, lda, A + G, lda, gg, k0, LU_NB, 0, R, batch, st, perm, perm);
+            trsm_launch<false>(A, G, lda, A + c0, lda, gg, k0, LU_NB, 0, nc, batch, st, perm, perm);
             jb = LU_NB + jb1;
         }
         if (k0 > rl)
-            rm_gemm(k0 - rl, R, jb, A + k0, lda, gg, A + G, lda, gg, A + G, lda, gg, batch, -1.0, 1.0, st, perm + rl,
-                    perm + k0, perm + rl, G);
+            rm_gemm(k0 - rl, nc, jb, A + k0, lda, gg, A + c0, lda, gg, A + c0, lda, gg, batch, -1.0, 1.0, st,
+                    perm + rl, perm + k0, perm + rl, G);
     }
+}
+
+int backsolve_launches(int bk_hi, int blo) {
+    int n = 0;
+    for (int bk = bk_hi; bk >= blo; bk -= 2) n += (bk - 1 >= blo ? 3 : 1) + (bk - 1 > blo ? 1 : 0);
+    return n;
+}
+}  // namespace
+
+void lu_backsolve_aug(double* A, int G, int lda, int R, int batch, const int* perm, double* X, int row_lo,
+                      cudaStream_t st) {
+    const int nblk = (G + LU_NB - 1) / LU_NB;
+    const int blo = max(0, row_lo) / LU_NB, rl = blo * LU_NB;
+    backsolve_blocks(A, G, lda, G, R, batch, perm, nblk - 1, blo, st);
     const long long total = (long long)batch * (G - rl) * R;
     lu_gather_aug_kernel<<<(unsigned)min(16384LL, (total + 255) / 256), 256, 0, st>>>(A, G, lda, R, perm, rl, X,
-                                                                                     batch);
+                                                                                     batch, G);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -725,15 +737,18 @@ void lu_solve_rm(const double* A, int G, int batch, const int* perm, const doubl
 }
 
 void lu_solve_gathered(const double* A, int G, int lda, int batch, const int* perm, double* X, int ncol,
-                       cudaStream_t st) {
+                       cudaStream_t st, int fwd_lo) {
     const long long gg = (long long)G * lda, gn = (long long)G * ncol;
-    for (int k0 = 0; k0 < G; k0 += LU_NB) {
-        const int jb = min(LU_NB, G - k0);
-        trsm_launch<true>(A, G, lda, X, ncol, gn, k0, jb, 0, ncol, batch, st, perm, nullptr);
-        if (G - k0 - jb > 0)
-            rm_gemm(G - k0 - jb, ncol, jb, A + k0, lda, gg, X + (size_t)k0 * ncol, ncol, gn,
-                    X + (size_t)(k0 + jb) * ncol, ncol, gn, batch, -1.0, 1.0, st, perm + k0 + jb, nullptr, nullptr, G);
-    }
+    // forward substitution on columns [fwd_lo, ncol) (the others already hold L^-1 P b)
+    if (fwd_lo < ncol)
+        for (int k0 = 0; k0 < G; k0 += LU_NB) {
+            const int jb = min(LU_NB, G - k0);
+            trsm_launch<true>(A, G, lda, X, ncol, gn, k0, jb, fwd_lo, ncol, batch, st, perm, nullptr);
+            if (G - k0 - jb > 0)
+                rm_gemm(G - k0 - jb, ncol - fwd_lo, jb, A + k0, lda, gg, X + (size_t)k0 * ncol + fwd_lo, ncol, gn,
+                        X + (size_t)(k0 + jb) * ncol + fwd_lo, ncol, gn, batch, -1.0, 1.0, st, perm + k0 + jb, nullptr,
+                        nullptr, G);
+        }
     const int nblk = (G + LU_NB - 1) / LU_NB;
     for (int bk = nblk - 1; bk >= 0; --bk) {
         const int k0 = bk * LU_NB, jb = min(LU_NB, G - k0);
@@ -742,6 +757,11 @@ void lu_solve_gathered(const double* A, int G, int lda, int batch, const int* pe
             rm_gemm(k0, ncol, jb, A + k0, lda, gg, X + (size_t)k0 * ncol, ncol, gn, X, ncol, gn, batch, -1.0, 1.0, st,
                     perm, nullptr, nullptr, G);
     }
+}
+
+int lu_gathered_launch_count(int G, int ncol, int fwd_lo) {
+    const int nblk = (G + LU_NB - 1) / LU_NB;
+    return (fwd_lo < ncol ? 2 * nblk - 1 : 0) + 2 * nblk - 1;
 }
 
 int lu_aug_launch_count(int G, int R, int row_lo) {
@@ -753,8 +773,7 @@ int lu_aug_launch_count(int G, int R, int row_lo) {
         if (G + R - K0 - NBk > 0) n += 2 * ((NBk + LU_NB - 1) / LU_NB) - 1 + 1;
     }
     const int nblk = (G + LU_NB - 1) / LU_NB, blo = max(0, row_lo) / LU_NB;
-    for (int bk = nblk - 1; bk >= blo; bk -= 2) n += (bk - 1 >= blo ? 3 : 1) + (bk - 1 > blo ? 1 : 0);
-    n += 1;  // gather
+    n += backsolve_launches(nblk - 1, blo) + 1;  // + gather
     return n;
 }
 

@@ -4,10 +4,12 @@
 // error mapping (guarded(): ValidationError -> 2, NumericalError/other -> 3,
 // null arguments -> 5) and handle ownership.  Instead of the VrteSolver
 // thread pool it hands a flat problem to the sm_100a pipeline (vrte_cuda.h).
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <stdexcept>
 #include <fstream>
 #include <atomic>
 #include <memory>
@@ -197,6 +199,35 @@ void build_setup(BrdfSetup& s, const MaterialSpec& mat, const vrte_options* opti
         s.medium[p] = sig;
     }
     const int S = (int)s.rep.size();
+    {
+        // media ordered by decreasing expansion length: the orders m >= a medium's last
+        // nonzero coefficient are free-streaming (zero kernel, analytic modes) and the
+        // device skips them when they are the trailing slots of the LAST medium
+        // (brdf_device.cu setup_plan), whatever the layer order
+        auto lc_of = [&](int k) {
+            const auto& layer = s.spec.layers[s.rep[k]];
+            if (layer.omega == 0.0) return 0;
+            int lc = 0;
+            for (int l = 0; l < (int)layer.coeffs.size(); ++l)
+                for (int r = 0; r < 4; ++r)
+                    for (int c = 0; c < 4; ++c)
+                        if (at(layer.coeffs[l], r, c) != 0.0) lc = l + 1;
+            return lc;
+        };
+        std::vector<int> order(S), lcs(S), rank(S);
+        for (int k = 0; k < S; ++k) {
+            order[k] = k;
+            lcs[k] = lc_of(k);
+        }
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return lcs[a] > lcs[b]; });
+        std::vector<int> rep2(S);
+        for (int k = 0; k < S; ++k) {
+            rank[order[k]] = k;
+            rep2[k] = s.rep[order[k]];
+        }
+        s.rep = rep2;
+        for (int p = 0; p < P; ++p) s.medium[p] = rank[s.medium[p]];
+    }
     s.omega.resize(S);
     s.greek.assign((size_t)S * Lc * 6, 0.0);
     for (int k = 0; k < S; ++k) {
@@ -388,14 +419,26 @@ vrte_status vrte_solve_radiance(const vrte_material* material, const vrte_option
             beam.mu0 = options->incident_mu0;
             beam.phi0 = options->incident_phi0;
         }
-        if (!(beam.mu0 > 0.0 && beam.mu0 <= 1.0))  // pipeline.cpp:97-98
+        // the reference's order: VrteSolver ctor (material, quadrature size), then the
+        // incident check of solve_incident (pipeline.cpp:27-36, 97-98)
+        {
+            MaterialSpec check = material->spec;
+            validate_material(check);
+            if (options && options->quadrature_n < 1)
+                throw ValidationError("solver: quadrature size must be at least 1");
+        }
+        if (!(beam.mu0 > 0.0 && beam.mu0 <= 1.0))
             throw ValidationError("incident mu0 must lie in (0,1]");
         BrdfSetup s;
         const double mu0 = beam.mu0;
         build_setup(s, material->spec, options, &mu0, 1, 1, nullptr);
-        // grids (pipeline.cpp:358-390)
-        const int zen = options ? options->out_zenith : 11, azi = options ? options->out_azimuth : 19;
-        if (zen < 1 || azi < 1) throw ValidationError("radiance: output grid must have at least one point");
+        // grids (pipeline.cpp:358-390): a negative count is std::vector's length_error
+        // (status 3); an empty grid gives an empty field (the solve and the
+        // reflectance still run, here on a one-point grid that is then dropped)
+        const int zen_req = options ? options->out_zenith : 11, azi_req = options ? options->out_azimuth : 19;
+        if (zen_req < 0 || azi_req < 0) throw std::length_error("cannot create std::vector larger than max_size()");
+        const bool empty_grid = zen_req == 0 || azi_req == 0;
+        const int zen = zen_req == 0 ? 1 : zen_req, azi = azi_req == 0 ? 1 : azi_req;
         std::vector<double> up(zen);
         for (int i = 0; i < zen; ++i) {
             const double m = zen == 1 ? 1.0 : (double)i / (zen - 1);
@@ -436,6 +479,11 @@ vrte_status vrte_solve_radiance(const vrte_material* material, const vrte_option
         const int32_t rc = vrte_cuda_radiance_field(&s.prob, &rad, f.values.data(), h->reflectance, &r);
         if (rc == 5) throw std::invalid_argument(r.message);
         if (rc != 0) throw NumericalError(r.message);
+        if (empty_grid) {
+            if (zen_req == 0) f.mus.clear();
+            if (azi_req == 0) f.phis.clear();
+            f.values.clear();
+        }
         const uint64_t S = s.rep.size(), L = s.L;
         h->timings.homogeneous = r.t_homogeneous;
         h->timings.particular = r.t_particular;
@@ -443,7 +491,7 @@ vrte_status vrte_solve_radiance(const vrte_material* material, const vrte_option
         h->timings.homogeneous_solves = S * L;
         h->timings.particular_solves = 2 * L * S;
         h->timings.boundary_solves = L;
-        h->timings.reconstruction_items = (uint64_t)nmu * f.taus.size();
+        h->timings.reconstruction_items = (uint64_t)f.mus.size() * f.taus.size();
         h->timings.total_wall = wall_now() - t0;
         h->timings.reconstruction = h->timings.total_wall - r.t_device;
         *out = h.release();
@@ -698,6 +746,8 @@ vrte_status compute_brdf_on(const vrte_material* material, const vrte_options* o
         h->stats.max_boundary_residual = r.max_boundary_residual;
         h->stats.max_boundary_condition = r.max_boundary_condition;
         h->stats.boundary_refined = r.boundary_refined;
+        h->stats.boundary_fallback = r.boundary_fallback;
+        h->stats.eigen_slots = r.eigen_slots;
         h->stats.boundary_cond_warnings = r.boundary_cond_warnings;
         h->stats.material_hash = t.material_hash;
         h->timings.total_wall = wall_now() - t0;

@@ -33,16 +33,19 @@ def greek_rows(coeffs):
     return [(b[0, 0], b[1, 1], b[0, 1], b[3, 3], b[3, 2], b[2, 2]) for b in coeffs]
 
 
-def generator_G(g: float, L: int) -> np.ndarray:
-    """SURVEY.md §8(d) Greek generator; G(0.5, 12) == data/forward12.coef."""
+def generator_G(g: float, L: int, pol: float = 1.0) -> np.ndarray:
+    """SURVEY.md §8(d) Greek generator; G(0.5, 12) == data/forward12.coef.
+
+    `pol` scales every polarization coefficient (alpha, gamma, delta, epsilon,
+    zeta; beta untouched): pol = 0.5 is the C4' set (see config("C4p"))."""
     out = np.zeros((L, 4, 4))
     for l in range(L):
         beta = (2 * l + 1) * g ** l
         if l >= 2:
-            a, gm, e, z = 0.9 * beta, -0.35 * beta, 0.12 * beta, 0.8 * beta
+            a, gm, e, z = 0.9 * pol * beta, -0.35 * pol * beta, 0.12 * pol * beta, 0.8 * pol * beta
         else:
             a = gm = e = z = 0.0
-        dl = 0.3 if l == 0 else 0.7 * beta
+        dl = 0.3 * pol if l == 0 else 0.7 * pol * beta
         out[l] = greek(beta, a, gm, dl, e, z)
     return out
 
@@ -171,6 +174,13 @@ def config(name: str, band: int = 0) -> Workload:
     if name == "C4":
         m = single_layer(generator_G(0.9, 256), 0.99, 10.0, "black")
         return Workload("C4", m, 128, 72, "G(0.9,256), omega=0.99, tau=10")
+    if name == "C4p":
+        # C4': the survey's C4 shape with the polarization ratios halved.  G(0.9, 256)
+        # itself is rejected by the reference (F E has negative real eigenvalues at
+        # m = 0, 1, 2: homogeneous.cpp:177-181); with pol = 0.5 every order m = 0..255
+        # passes the reference's checks (the oracle accepts all 256, 8N residual <= 5e-10).
+        m = single_layer(generator_G(0.9, 256, 0.5), 0.99, 10.0, "black")
+        return Workload("C4p", m, 128, 72, "C4': G(0.9,256) with polarization x0.5, omega=0.99, tau=10")
     if name == "C5":
         b = band
         om = 0.80 + 0.19 * b / 30.0

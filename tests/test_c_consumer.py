@@ -76,4 +76,5 @@ def test_c_consumer_solves_reference_data(consumer, name):
     assert f00 == b.table()[0, 0, 0, 0, 0]  # the same library, bit for bit
     L = mat.info()[0]
     S = 2 if name == "paint_film.json" else 1  # distinct media (pipeline.cpp:37-54)
-    assert line[8:] == [str(S * L), str(2 * 4 * 2 * L * S), str(2 * 4 * L)]
+    assert line[8] == "solves"
+    assert line[9:] == [str(S * L), str(2 * 4 * 2 * L * S), str(2 * 4 * L)]

@@ -116,3 +116,44 @@ def test_degenerate_grids_and_many_depths():
     f, (t, mus, phis, g), (omu, ophi, r, orefl) = run_pair(d, N, taus, zen=1, azi=1)
     assert list(mus) == [1.0, -1.0] and len(phis) == 1
     assert np.abs(g - r).max() < 1e-9 * np.abs(r).max()
+
+
+def stokes_metric(g, r):
+    """Per output Stokes vector: max_c |G_c - R_c| / max(|R_c|, 1e-3 |R_I|, 1e-6 max|R|) -- the
+    SURVEY §8(d) per-Mueller-matrix metric applied to the field's Stokes vectors (the absolute
+    floor keeps the exactly-zero downward field at tau = 0 out of the ratio)."""
+    scale = np.abs(r).max()
+    den = np.maximum(np.maximum(np.abs(r), 1e-3 * np.abs(r[..., :1])), 1e-6 * scale)
+    return float((np.abs(g - r) / den).max())
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_radiance_per_element_parity(name):
+    d, N = CASES[name]
+    tot = sum(l.tau for l in d.layers)
+    f, (t, mus, phis, g), (omu, ophi, r, orefl) = run_pair(d, N, [0.0, 0.5 * tot, tot])
+    assert stokes_metric(g, r) <= 1e-9, name
+
+
+def test_radiance_grid_edge_cases_follow_the_reference():
+    d, N = CASES["rayleigh_lam"]
+    mat = product_material(d)
+    full = V.solve_radiance(mat, V.options(N, out_zenith=3, out_azimuth=4), [0.0])
+    # an empty zenith or azimuth grid: an empty field, VRTE_OK, the reflectance still solved
+    for zen, azi, shape in ((0, 4, (1, 0, 4)), (3, 0, (1, 6, 0)), (0, 0, (1, 0, 0))):
+        f = V.solve_radiance(mat, V.options(N, out_zenith=zen, out_azimuth=azi), [0.0])
+        assert f.shape == shape
+        assert np.array_equal(f.reflectance(), full.reflectance())
+    # a negative count is std::vector's length_error in the reference: status 3
+    for zen, azi in ((-1, 4), (3, -2)):
+        with pytest.raises(V.VrteError) as e:
+            V.solve_radiance(mat, V.options(N, out_zenith=zen, out_azimuth=azi), [0.0])
+        assert e.value.code == 3
+    # validation order: the solver's quadrature check precedes the incident check
+    bad = V.options(0, incident_override=1, incident_mu0=2.0)
+    with pytest.raises(V.VrteError) as e:
+        V.solve_radiance(mat, bad, [0.0])
+    assert e.value.code == 2 and "quadrature size" in str(e.value)
+    with pytest.raises(V.VrteError) as e:
+        V.solve_radiance(mat, V.options(N, incident_override=1, incident_mu0=2.0), [0.0])
+    assert e.value.code == 2 and "incident mu0" in str(e.value)
