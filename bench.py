@@ -673,7 +673,8 @@ def main():
                                                  "t_refine", "t_lu_factor", "t_lu_solve")},
         "max_eigen_residual": res["max_eigen_residual"],
         "gates": {k: res[k] for k in ("max_boundary_residual", "max_boundary_condition", "boundary_refined",
-                                       "max_balance_residual", "max_particular_residual")},
+                                       "boundary_fallback", "max_balance_residual", "max_particular_residual",
+                                       "particular_extra_steps")},
         "parity": parity_record(gpu_table),
     }
     print(json.dumps(line), flush=True)

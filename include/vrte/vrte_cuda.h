@@ -87,6 +87,7 @@ typedef struct vrte_cuda_result {
     uint64_t eigen_slots;   /* (medium, order) slots through the eigen pipeline (the rest are free-streaming) */
     uint64_t slots;         /* all (medium, order) slots of the call */
     uint64_t boundary_fallback; /* a residual probe failed (boundary.cuh): full solution + exact gate */
+    uint64_t particular_extra_steps; /* refinement steps of the particular stage beyond the first */
     int32_t status;         /* 0 ok, 3 numerical, 5 argument */
     char message[512];
 } vrte_cuda_result;

@@ -128,6 +128,7 @@ class CudaResult(C.Structure):
         ("eigen_slots", C.c_uint64),
         ("slots", C.c_uint64),
         ("boundary_fallback", C.c_uint64),
+        ("particular_extra_steps", C.c_uint64),
         ("status", C.c_int32),
         ("message", C.c_char * 512),
     ]

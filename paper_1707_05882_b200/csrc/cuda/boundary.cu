@@ -270,19 +270,40 @@ __global__ void bnd_anorm_kernel(BndArgs a, int G) {
     __shared__ double red[32];
     double mx = 0.0, cs = 0.0;
     if (c < G) {
+        // rows split over blockIdx.z; 8 loads in flight per thread
+        const int r0 = blockIdx.z * (G / gridDim.z), r1 = blockIdx.z + 1 == gridDim.z ? G : r0 + G / gridDim.z;
         const double* A0 = a.lhs0 + (size_t)mo * a.sl + c;
-        for (int r = 0; r < G; ++r) {
+        int r = r0;
+        for (; r + 8 <= r1; r += 8) {
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = fabs(A0[(size_t)(r + q) * a.ldl]);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                mx = fmax(mx, v[q]);
+                cs += v[q];
+            }
+        }
+        for (; r < r1; ++r) {
             const double v = fabs(A0[(size_t)r * a.ldl]);
             mx = fmax(mx, v);
             cs += v;
         }
     }
+    // column sums of the row strips meet in colsum; the last strip's CTA of a
+    // column slab (atomic ticket) reduces them into ||A||_1
     mx = block_max(mx, red);
-    cs = block_max(cs, red);
-    if (threadIdx.x == 0) {
-        atomic_max_double(&a.anorm[2 * mo], mx);
-        atomic_max_double(&a.anorm[2 * mo + 1], cs);
-    }
+    if (threadIdx.x == 0) atomic_max_double(&a.anorm[2 * mo], mx);
+    if (c < G) atomicAdd(&a.colsum[(size_t)mo * G + c], cs);
+    __threadfence();
+    __shared__ unsigned ticket;
+    if (threadIdx.x == 0) ticket = atomicAdd(&a.colsum_ticket[(size_t)mo * gridDim.x + blockIdx.x], 1u);
+    __syncthreads();
+    if (ticket + 1 != gridDim.z) return;
+    __threadfence();
+    double tot = c < G ? atomicAdd(&a.colsum[(size_t)mo * G + c], 0.0) : 0.0;
+    tot = block_max(tot, red);
+    if (threadIdx.x == 0) atomic_max_double(&a.anorm[2 * mo + 1], tot);
 }
 
 // Thread per (order, right-hand side): residual column of lhs0's B part after
@@ -455,7 +476,10 @@ __global__ void bnd_gather_b_kernel(BndArgs a, const int* perm_all, double* X, i
 void launch_bnd_norms(const BndArgs& a, int G, int R, cudaStream_t st) {
     (void)R;
     VRTE_CUDA_CHECK(cudaMemsetAsync(a.anorm, 0, sizeof(double) * 2 * (size_t)a.p.n_orders, st));
-    bnd_anorm_kernel<<<dim3((G + 255) / 256, a.p.n_orders), 256, 0, st>>>(a, G);
+    VRTE_CUDA_CHECK(cudaMemsetAsync(a.colsum, 0, sizeof(double) * (size_t)a.p.n_orders * G, st));
+    const int slabs = (G + 255) / 256;
+    VRTE_CUDA_CHECK(cudaMemsetAsync(a.colsum_ticket, 0, sizeof(unsigned) * (size_t)a.p.n_orders * slabs, st));
+    bnd_anorm_kernel<<<dim3(slabs, a.p.n_orders, 8), 256, 0, st>>>(a, G);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -26,6 +26,8 @@ struct BndArgs {
     double* anorm;        // [mo][2]: max |A_ij|, ||A||_1
     double* bnorm;        // [mo][R][2]: max |b_i|, ||b||_1
     double* condm;        // [mo]: lower bound of cond_1(A), max over the right-hand sides
+    double* colsum;       // [mo][G] scratch of the ||A||_1 reduction
+    unsigned* colsum_ticket;  // [mo][G / 256 slabs]
     int K;                // residual probes (0: the full gate); their b_k in lhs0 columns G + R + k
 };
 
@@ -112,6 +114,11 @@ __host__ __device__ inline int bnd_row_end(int col, int d, int P) {
 // (forward-eliminated by an augmented factorization): back substitution only.
 void lu_solve_gathered(const double* A, int G, int lda, int batch, const int* perm, double* X, int ncol,
                        cudaStream_t st, int fwd_lo = 0);
+// X <- A^-1 X for K = 4 columns ([batch][G][K], position order) by one CTA per
+// matrix (the boundary gate's residual probes); columns < fwd_lo already hold
+// L^-1 P b.  G <= 4096 (the columns live in shared memory).
+void lu_few_solve(const double* A, int G, int lda, int batch, const int* perm, double* X, int K, int fwd_lo,
+                  cudaStream_t st);
 int lu_rm_launch_count(int G);
 int lu_aug_launch_count(int G, int R, int row_lo);
 int lu_gathered_launch_count(int G, int ncol, int fwd_lo);

@@ -44,6 +44,8 @@ namespace vrte {
 namespace {
 
 constexpr double kRefineTarget = 5e-11;  // per-mode 8N residual after refinement
+constexpr double kPartTarget = 1e-7;     // particular 8N balance residual (gate 1e-6)
+constexpr int kPartExtraMax = 3;
 
 template <typename T>
 struct DevBuf {
@@ -126,7 +128,8 @@ struct vrte_cuda_plan {
     DevBuf<double> lhs, top0, rhs_b, rhs_x, up;
     DevBuf<int> ipiv, perm;
     // boundary residual gate (boundary.cpp:233-257)
-    DevBuf<double> lhs0, anorm, bnorm, condm, dX, Xp, Rp;
+    DevBuf<double> lhs0, anorm, bnorm, condm, dX, Xp, Rp, colsum;
+    DevBuf<int> colsum_ticket;
     int ldl = 0;  // row stride of [A | B] (+ the probes' b_k in lhs0): G + R + 16
     const double* lhs0_zeroed = nullptr;
     size_t lhs0_zeroed_key = 0;
@@ -143,14 +146,17 @@ struct vrte_cuda_plan {
     cudaEvent_t fork[6] = {}, join[6] = {};
     int refine_iters = 1;
     int refine_extra = 2;
-    int part_refine_iters = 1;
     DevBuf<double> resmax;
     double* resmax_host = nullptr;
+    double* part_host = nullptr;  // page-locked copy of DeviceStatus::part_check
+    uint64_t part_extra_iters = 0;
+    double part_prev = 0.0;
     char* stage = nullptr;  // page-locked staging for the per-call inputs (one async copy each)
     size_t stage_bytes = 0;
     uint64_t launches = 0;
     ~vrte_cuda_plan() {
         if (resmax_host) cudaFreeHost(resmax_host);
+        if (part_host) cudaFreeHost(part_host);
         if (refine_host) cudaFreeHost(refine_host);
         if (stage) cudaFreeHost(stage);
         for (auto& e : ev)
@@ -192,10 +198,8 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     for (auto* es : {pl.fork, pl.join})
         for (int i = 0; i < 6; ++i)
             if (!es[i]) VRTE_CUDA_CHECK(cudaEventCreateWithFlags(&es[i], cudaEventDisableTiming));
-    if (const char* ri = std::getenv("VRTE_REFINE_ITERS")) pl.refine_iters = std::atoi(ri);
-    if (const char* pi = std::getenv("VRTE_PART_REFINE_ITERS")) pl.part_refine_iters = std::atoi(pi);
-    if (const char* re = std::getenv("VRTE_REFINE_EXTRA")) pl.refine_extra = std::atoi(re);
     if (!pl.resmax_host) VRTE_CUDA_CHECK(cudaMallocHost(&pl.resmax_host, sizeof(double)));
+    if (!pl.part_host) VRTE_CUDA_CHECK(cudaMallocHost(&pl.part_host, sizeof(double)));
     if (!pl.refine_host) VRTE_CUDA_CHECK(cudaMallocHost(&pl.refine_host, sizeof(int)));
     pl.resmax.alloc(1);
     pl.N = p->N;
@@ -326,6 +330,8 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pl.anorm.alloc((size_t)NO * 2);
     pl.bnorm.alloc((size_t)NO * R * 2);
     pl.condm.alloc((size_t)NO);
+    pl.colsum.alloc((size_t)NO * G);
+    pl.colsum_ticket.alloc((size_t)NO * ((G + 255) / 256));
     pl.dX.alloc((size_t)NO * G * R);
     pl.top0.alloc((size_t)NO * d * 2 * d);
     pl.rhs_x.alloc((size_t)NO * R * G);
@@ -384,6 +390,8 @@ BndArgs make_bnd(vrte_cuda_plan& pl) {
     ba.anorm = pl.anorm.p;
     ba.bnorm = pl.bnorm.p;
     ba.condm = pl.condm.p;
+    ba.colsum = pl.colsum.p;
+    ba.colsum_ticket = reinterpret_cast<unsigned*>(pl.colsum_ticket.p);
     return ba;
 }
 
@@ -450,6 +458,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     cudaStream_t st = pl.st;
     const ProblemDev& pd = pl.pd;
     uint64_t nl = 0;
+    pl.part_extra_iters = 0;
     VRTE_CUDA_CHECK(cudaMemsetAsync(pl.status, 0, sizeof(DeviceStatus), st));
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[0], st));
     // ---------------- homogeneous
@@ -571,17 +580,23 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     // Iterative refinement against the true operator F (E g): the Schur form
     // carries a normwise backward error ~eps|FE| that the reference's dense LU
     // (componentwise-small on this graded matrix) does not.
-    for (int it = 0; it < pl.part_refine_iters; ++it) {
+    // One step normally suffices; the interim balance residual (the 8N check of
+    // particular.cpp:86-105) decides about more below, at the refinement's host sync.
+    auto part_iteration = [&]() {
         launch_part_refine_residual(pa, pl.fsp.p, st2);
         shifted_solve(pl.fsp.p, pl.W.p, R, dR, pl.sigma.p, pl.kind.p, pl.g.p, 1.0, st2);
         gemm_batched(gemm(d, R, d, pl.E.p, d, dd, false, pl.g.p, d, dR, false, pl.eg.p, d, dR, B), st2);
         gemm_batched(gemm(d, R, d, pl.F.p, d, dd, false, pl.eg.p, d, dR, false, pl.feg.p, d, dR, B), st2);
-        nl += 6;
-    }
-    launch_zpm(pa, st2);
-    launch_part_residual(pa, st2);
-    nl += 11;
-    VRTE_CUDA_CHECK(cudaEventRecord(pl.join[2], st2));
+        VRTE_CUDA_CHECK(cudaMemsetAsync(&pl.status->part_check, 0, sizeof(double), st2));
+        launch_zpm(pa, st2);
+        launch_part_residual(pa, st2, false);
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(pl.part_host, &pl.status->part_check, sizeof(double), cudaMemcpyDeviceToHost,
+                                        st2));
+        VRTE_CUDA_CHECK(cudaEventRecord(pl.join[5], st2));
+        nl += 8;
+    };
+    part_iteration();
+    nl += 5;
     // (the 8N residual of the unrefined modes is not needed: every refinement
     // step starts by recomputing it, and final_residual() feeds the gate)
     ResidualArgs ra{};
@@ -668,6 +683,22 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     // ---------------- boundary
     const BndArgs ba = make_bnd(pl);
     launch_bnd_assemble(ba, st);
+    // The particular stage's refinement, like the eigenpairs': another step while
+    // its balance residual exceeds kPartTarget (a tenth of the reference's 1e-6
+    // gate); decided here, with the boundary assembly already queued.
+    // Stops when a step no longer halves the residual (its fp64 floor).
+    for (int part_extra = 0, prev = 0; ; ++part_extra) {
+        VRTE_CUDA_CHECK(cudaEventSynchronize(pl.join[5]));
+        const double cur = *pl.part_host;
+        if (cur <= kPartTarget || part_extra >= kPartExtraMax || (prev && !(cur < 0.5 * pl.part_prev))) break;
+        pl.part_prev = cur;
+        prev = 1;
+        ++pl.part_extra_iters;
+        part_iteration();
+    }
+    launch_part_residual(pa, st2);  // the reference's gates on the final particular vectors
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.join[2], st2));
+    nl += 1;
     // right-hand sides on the side stream once the particular vectors are there; the
     // factorization waits for them only before its first update of those columns
     VRTE_CUDA_CHECK(cudaEventRecord(pl.fork[3], st));
@@ -696,7 +727,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
         launch_bnd_probe_setup(ba, pl.perm.p, pl.Xp.p, G, R, st);
         VRTE_CUDA_CHECK(cudaEventRecord(pl.fork[4], st));
         VRTE_CUDA_CHECK(cudaStreamWaitEvent(st2, pl.fork[4], 0));
-        lu_solve_gathered(pl.lhs.p, G, ldl, NO, pl.perm.p, pl.Xp.p, K, st2, kBndCombProbes);
+        lu_few_solve(pl.lhs.p, G, ldl, NO, pl.perm.p, pl.Xp.p, K, kBndCombProbes, st2);
         VRTE_CUDA_CHECK(cudaEventRecord(pl.join[4], st2));
         const int row_lo = G - 2 * d;
         lu_backsolve_aug(pl.lhs.p, G, ldl, R, NO, pl.perm.p, pl.rhs_x.p, row_lo, st);
@@ -704,7 +735,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
         VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[0], 0));
         VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[4], 0));
         launch_bnd_probe_check(ba, pl.Xp.p, pl.Rp.p, pl.rhs_x.p, (row_lo / 64) * 64, G, R, pl.status, st);
-        nl += lu_aug_launch_count(G, R, row_lo) + 1 + lu_gathered_launch_count(G, K, kBndCombProbes) + 3;
+        nl += lu_aug_launch_count(G, R, row_lo) + 1 + 1 + 3;
     }
     nl += boundary_top(pl, ba, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[3], st));
@@ -847,6 +878,7 @@ int finish(vrte_cuda_plan& pl, vrte_cuda_result* r) {
         r->max_boundary_residual = s.max_boundary_residual;
         r->boundary_refined = s.bnd_refined ? 1 : 0;
         r->boundary_fallback = s.bnd_fallback ? 1 : 0;
+        r->particular_extra_steps = pl.part_extra_iters;
         std::vector<double> cm((size_t)pl.NO);
         VRTE_CUDA_CHECK(cudaMemcpy(cm.data(), pl.condm.p, sizeof(double) * cm.size(), cudaMemcpyDeviceToHost));
         r->max_boundary_condition = 0.0;
@@ -1187,7 +1219,7 @@ int32_t brdf_sharded(const vrte_cuda_problem* problem, double* table, vrte_cuda_
                  {&vrte_cuda_result::dithered, &vrte_cuda_result::polished, &vrte_cuda_result::kernel_launches,
                   &vrte_cuda_result::qr_sweeps, &vrte_cuda_result::qr_steps, &vrte_cuda_result::boundary_refined,
                   &vrte_cuda_result::boundary_cond_warnings, &vrte_cuda_result::eigen_slots,
-                  &vrte_cuda_result::boundary_fallback,
+                  &vrte_cuda_result::boundary_fallback, &vrte_cuda_result::particular_extra_steps,
                   &vrte_cuda_result::slots})
                 r.*f += q.*f;
         }

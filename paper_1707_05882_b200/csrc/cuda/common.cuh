@@ -53,6 +53,7 @@ struct DeviceStatus {
     int bnd_refine;                   // a right-hand side needs the refinement step
     int bnd_refined;                  // ... and it was taken
     int bnd_fallback;                 // a residual probe failed: full solve + reference gate
+    double part_check;                // interim max balance residual (adaptive particular refinement)
     double max_balance_residual;      // particular 8N balance residual (particular.cpp:86-105)
     unsigned long long qr_sweeps;
     unsigned long long qr_steps;

@@ -588,6 +588,127 @@ void trsm_launch(const double* A, int G, int lda, double* M, int ld, long long s
 
 int outer_block() { return OB_MAX; }
 
+
+// ------------------------------------------------------------------ few-column solve
+// X <- A^-1 X for K columns (position order, [G][K] per matrix) by ONE CTA per
+// matrix: the residual probes of the boundary gate (boundary.cuh), where the
+// 64-row-block TRSM + GEMM launches of lu_solve_gathered cost ~25 us each for a
+// handful of columns.  Columns < FL already hold L^-1 P b (back substitution
+// only).  Per 64-row block: the coupling to the solved rows as a matvec (warp
+// per row, L / U rows read coalesced through the row map), then the block's
+// triangle from shared memory, one warp per column.
+// x[k0 + r][c] -= sum_{j in [j0, j1)} A(perm[k0 + r], j) x[j][c] for rows r < jb,
+// columns c >= c0: each warp takes 4 rows at once, 2 x 4 row loads in flight.
+template <int K>
+__device__ inline void few_matvec(const double* A, int lda, const int* perm, double* x, int k0, int jb, int j0,
+                                  int j1, int c0, int warp, int nw, int lane) {
+    for (int r0 = warp * 4; r0 < jb; r0 += nw * 4) {
+        const double* row[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) row[q] = A + (size_t)perm[k0 + min(r0 + q, jb - 1)] * lda;
+        double acc[4][K];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int c = 0; c < K; ++c) acc[q][c] = 0.0;
+        int j = j0 + lane;
+        for (; j + 32 < j1; j += 64) {
+            double a0[4], a1[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                a0[q] = row[q][j];
+                a1[q] = row[q][j + 32];
+            }
+#pragma unroll
+            for (int c = 0; c < K; ++c) {
+                const double x0 = x[j * K + c], x1 = x[(j + 32) * K + c];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[q][c] = fma(a1[q], x1, fma(a0[q], x0, acc[q][c]));
+            }
+        }
+        if (j < j1) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double a0 = row[q][j];
+#pragma unroll
+                for (int c = 0; c < K; ++c) acc[q][c] = fma(a0, x[j * K + c], acc[q][c]);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int c = 0; c < K; ++c) {
+                const double sv = warp_sum(acc[q][c]);
+                if (lane == 0 && c >= c0 && r0 + q < jb) x[(k0 + r0 + q) * K + c] -= sv;
+            }
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(512) lu_few_solve_kernel(const double* Aall, int G, int lda, long long strideA,
+                                                          const int* perm_all, double* Xall, int FL) {
+    extern __shared__ double sm[];
+    double* x = sm;                       // [G][K]
+    double* T = sm + (size_t)G * K;       // [64][65] diagonal block
+    const int b = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
+    const double* A = Aall + (size_t)b * strideA;
+    const int* perm = perm_all + (size_t)b * G;
+    double* X = Xall + (size_t)b * G * K;
+    for (int e = t; e < G * K; e += blockDim.x) x[e] = X[e];
+    __syncthreads();
+    const int nblk = (G + LU_NB - 1) / LU_NB;
+    // ---- forward: unit lower L, columns [FL, K)
+    if (FL < K)
+        for (int bk = 0; bk < nblk; ++bk) {
+            const int k0 = bk * LU_NB, jb = min(LU_NB, G - k0);
+            for (int e = t; e < jb * LU_NB; e += blockDim.x) {
+                const int r = e / LU_NB, c = e % LU_NB;
+                T[r * (LU_NB + 1) + c] = c < jb ? A[(size_t)perm[k0 + r] * lda + k0 + c] : 0.0;
+            }
+            few_matvec<K>(A, lda, perm, x, k0, jb, 0, k0, FL, warp, nw, lane);
+            __syncthreads();
+            if (warp < K - FL) {
+                const int c = FL + warp;
+                double v0 = lane < jb ? x[(k0 + lane) * K + c] : 0.0;
+                double v1 = lane + 32 < jb ? x[(k0 + lane + 32) * K + c] : 0.0;
+                for (int j = 0; j < jb; ++j) {
+                    const double xj = __shfl_sync(0xffffffffu, j < 32 ? v0 : v1, j & 31);
+                    if (lane > j) v0 -= T[lane * (LU_NB + 1) + j] * xj;
+                    if (lane + 32 > j && lane + 32 < jb) v1 -= T[(lane + 32) * (LU_NB + 1) + j] * xj;
+                }
+                if (lane < jb) x[(k0 + lane) * K + c] = v0;
+                if (lane + 32 < jb) x[(k0 + lane + 32) * K + c] = v1;
+            }
+            __syncthreads();
+        }
+    // ---- backward: upper U (with its diagonal), every column
+    for (int bk = nblk - 1; bk >= 0; --bk) {
+        const int k0 = bk * LU_NB, jb = min(LU_NB, G - k0), k1 = k0 + jb;
+        for (int e = t; e < jb * LU_NB; e += blockDim.x) {
+            const int r = e / LU_NB, c = e % LU_NB;
+            T[r * (LU_NB + 1) + c] = c < jb ? A[(size_t)perm[k0 + r] * lda + k0 + c] : 0.0;
+        }
+        few_matvec<K>(A, lda, perm, x, k0, jb, k1, G, 0, warp, nw, lane);
+        __syncthreads();
+        if (warp < K) {
+            const int c = warp;
+            double v0 = lane < jb ? x[(k0 + lane) * K + c] : 0.0;
+            double v1 = lane + 32 < jb ? x[(k0 + lane + 32) * K + c] : 0.0;
+            for (int j = jb - 1; j >= 0; --j) {
+                const double piv = T[j * (LU_NB + 1) + j];
+                double xj = __shfl_sync(0xffffffffu, j < 32 ? v0 : v1, j & 31) / piv;
+                if (lane == j) v0 = xj;
+                if (lane + 32 == j) v1 = xj;
+                if (lane < j) v0 -= T[lane * (LU_NB + 1) + j] * xj;
+                if (lane + 32 < j) v1 -= T[(lane + 32) * (LU_NB + 1) + j] * xj;
+            }
+            if (lane < jb) x[(k0 + lane) * K + c] = v0;
+            if (lane + 32 < jb) x[(k0 + lane + 32) * K + c] = v1;
+        }
+        __syncthreads();
+    }
+    for (int e = t; e < G * K; e += blockDim.x) X[e] = x[e];
+}
 }  // namespace
 
 void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatus* status,
@@ -790,4 +911,18 @@ int lu_rm_launch_count(int G) {
     return n;
 }
 
+}  // namespace vrte
+
+namespace vrte {
+void lu_few_solve(const double* A, int G, int lda, int batch, const int* perm, double* X, int K, int fwd_lo,
+                  cudaStream_t st) {
+    if (K != 4) throw std::invalid_argument("lu_few_solve: K = 4 only");
+    if (G > 4096) throw std::invalid_argument("lu_few_solve: G > 4096");
+    const size_t smem = ((size_t)G * K + (size_t)LU_NB * (LU_NB + 1)) * sizeof(double);
+    constexpr int smem_max = (4096 * 4 + LU_NB * (LU_NB + 1)) * (int)sizeof(double);
+    static unsigned long long attr = 0;
+    smem_attr_once(lu_few_solve_kernel<4>, smem_max, attr);
+    lu_few_solve_kernel<4><<<batch, 512, smem, st>>>(A, G, lda, (long long)G * lda, perm, X, fwd_lo);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
 }  // namespace vrte

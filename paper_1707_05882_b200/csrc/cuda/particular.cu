@@ -2,9 +2,10 @@
 // (medium, order, incident, unit Stokes channel), particular.cpp:27-107.
 //
 // The reference factors F E - mu0^-2 I afresh for every incident; here the
-// real Schur form F E = Z T Z^T from the homogeneous stage is reused, so each
-// right-hand side costs two GEMM-projections plus an O(d^2) quasi-triangular
-// back substitution (orthogonal similarity: same conditioning as the LU).
+// eigendecomposition F E = V Lambda V^-1 of the homogeneous stage is reused, so
+// each right-hand side costs two GEMMs plus an independent 1x1 / 2x2 solve per
+// entry (brdf_device.cu shifted_solve), followed by iterative refinement
+// against the true operator F (E g).
 #include "kernels.cuh"
 #include "particular.cuh"
 
@@ -74,7 +75,7 @@ __global__ void zpm_kernel(PartArgs a) {
 
 // System residual (particular.cpp:84-92): |(FE - sigma) g - rhs| against
 // 1e-8 (|rhs| + |FE - sigma| |g|); |FE - sigma| bounded by max|FE| + sigma.
-__global__ void part_residual_kernel(PartArgs a) {
+__global__ void part_residual_kernel(PartArgs a, bool final) {
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     const int d = a.d, R = 4 * a.n_in;
     if (gw >= a.batch * R) return;
@@ -112,6 +113,10 @@ __global__ void part_residual_kernel(PartArgs a) {
     balmax = warp_max(balmax);
     xmax = warp_max(xmax);
     finite = __all_sync(0xffffffffu, finite);
+    if (lane == 0 && !final) {
+        if (xmax > 0.0) atomic_max_double(&a.status->part_check, balmax / xmax);
+        return;
+    }
     if (lane == 0) {
         const int m = a.order_index ? a.order_index[om] : om;
         const double scale = bmax + (a.femax[om] + sg) * gmax;
@@ -165,9 +170,9 @@ void launch_zpm(const PartArgs& a, cudaStream_t st) {
     zpm_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(a);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
-void launch_part_residual(const PartArgs& a, cudaStream_t st) {
+void launch_part_residual(const PartArgs& a, cudaStream_t st, bool final) {
     const long long warps = (long long)a.batch * 4 * a.n_in;
-    part_residual_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(a);
+    part_residual_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(a, final);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 

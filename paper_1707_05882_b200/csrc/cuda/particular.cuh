@@ -30,7 +30,9 @@ struct PartArgs {
 void launch_dither(const PartArgs& a, cudaStream_t st);
 void launch_part_rhs(const PartArgs& a, cudaStream_t st);
 void launch_zpm(const PartArgs& a, cudaStream_t st);
-void launch_part_residual(const PartArgs& a, cudaStream_t st);
+// final = false: only the interim maximum of the balance residual (DeviceStatus::
+// part_check) for the adaptive refinement; final = true: the reference's gates.
+void launch_part_residual(const PartArgs& a, cudaStream_t st, bool final = true);
 void launch_part_refine_residual(const PartArgs& a, double* W, cudaStream_t st);
 
 }  // namespace vrte
