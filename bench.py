@@ -512,10 +512,132 @@ def run_mc7(args):
     print(json.dumps(line), flush=True)
 
 
+def run_sharded(args):
+    """N > 1 GPUs: Fourier orders sharded across the ranks, the
+    per-order tau = 0 stacks exchanged as device buffers over NCCL, the Fourier
+    synthesis on the owning GPU (paper_1707_05882_b200/distributed.py).
+      C3 (and any config but C4p): N solves in flight per step, each sharded by
+        order over all N GPUs; an all-to-all hands solve j's shards to rank j
+        ("weak": one solve's worth of orders per GPU per step).
+      C4p: ONE solve per step sharded by order over the N GPUs, gathered to
+        rank 0 ("strong").
+    value = solves per step / step time, max over ranks, CUDA events around
+    the step with device-wide synchronisation on both sides (the plans run on
+    their own streams); e2e = the public calls D.inflight_brdf / D.sharded_brdf
+    (inputs uploaded from the host, the owned table read back) each step."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_1707_05882_b200 as V
+    from paper_1707_05882_b200 import distributed as D
+
+    world, rank, local = dist_env()
+    # VRTE_BENCH_EMULATE=1 (testing the code path on a 1-GPU box): every rank on
+    # cuda:0, gloo with host staging instead of NCCL -- not a performance mode
+    emulate = os.environ.get("VRTE_BENCH_EMULATE") == "1"
+    if emulate:
+        local = 0
+    torch.cuda.set_device(local)
+    if emulate:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    os.environ["VRTE_DEVICE"] = str(local)
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if emulate else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    w = workload(args.config)
+    nodes = quad_nodes(w.N)
+    tmp = tempfile.mkdtemp(prefix=f"vrte_bench_{rank}_")
+    mat = V.Material.load(w.material.write(tmp, "m"))
+    opts = V.options(w.N)
+    single = args.config == "C4p"
+    mats = [mat] if single else [mat] * world
+    per_step = 1 if single else world
+    conc = min(4, len(mats))
+    dist.barrier()
+    sh = D.OrderShards(mats, opts, nodes, w.n_dphi, None, world, rank, local, None, conc)
+
+    def step():
+        sh.run()
+        sh.exchange()
+        sh.synthesize(fetch=False)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize()
+        e1.record()
+        e1.synchronize()
+    dev_s = e0.elapsed_time(e1) * 1e-3
+    launches = int(sum(p.last.kernel_launches for p in sh.plans)) * args.steps
+    dev_s = max_over_ranks(dev_s)
+    value = per_step * args.steps / dev_s
+    sh.close()
+    # e2e through the public calls (host inputs, host table of the owned solve)
+    call = (lambda: D.sharded_brdf(mat, opts, nodes, w.n_dphi, device=local)) if single else \
+        (lambda: D.inflight_brdf(mats, opts, nodes, w.n_dphi, device=local, concurrency=conc))
+    for _ in range(args.warmup):
+        call()
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        tab = call()
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    # bitwise check of one owned table against a single-GPU solve of the same material
+    same = None
+    if tab is not None:
+        same = bool(np.array_equal(tab, V.compute_brdf(mat, opts, nodes, w.n_dphi).table()))
+    flags = [None] * world
+    dist.all_gather_object(flags, same)
+    N, L, n_in, nd = w.N, w.material.order_count, len(nodes), w.n_dphi
+    P = len(w.material.layers)
+    R, d = 4 * n_in, 4 * N
+    if rank == 0:
+        h2d = per_step * 8 * (2 * N + 2 + 2 * L * 6 + P + n_in + n_in * N * 16 + n_in * 16 + L * nd * 2)
+        line = {
+            "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dev_s / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong" if single else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SURVEY §8(d) Greek generator G(g,L), deterministic)",
+            "config": {"workload": f"{args.config}: {w.note}", "N": N, "L": L, "layers": P, "n_in": n_in,
+                       "n_dphi": nd,
+                       "parallelism": (f"one solve per step, orders sharded x{world} (m = rank mod {world}), "
+                                       "NCCL gather of the per-order stacks to rank 0, synthesis there") if single
+                       else (f"{world} solves in flight per step, each sharded by order over the {world} GPUs "
+                             f"({world} plans per GPU, {conc} concurrent), NCCL all-to-all of the per-order "
+                             "stacks, each rank synthesizes one solve"),
+                       "exchange_bytes_per_step": per_step * 8 * L * R * d,
+                       "l2": "working set >> 126 MB L2 (no explicit flush)"},
+            "e2e": {"value": per_step * args.steps / e2e_s, "unit": "solves/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": per_step * 8 * n_in * N * nd * 16},
+            "gpu_launches": launches,
+            "bitwise_vs_single_gpu": [f for f in flags if f is not None],
+            "emulated_on_one_gpu": emulate,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if dist_env()[0] > 1 and args.config not in ("C5", "R3", "MC7"):
+        return run_sharded(args)
     if args.config == "C5":
         return run_c5(args)
     if args.config == "R3":

@@ -144,11 +144,29 @@ VRTE_API int32_t vrte_cuda_plan_create(const vrte_cuda_problem* problem, vrte_cu
 /* Run the device pipeline `iters` times with inputs already resident; the
  * average device seconds per solve is returned in *seconds (CUDA events on the
  * plan's stream).  Table stays on the device. */
+/* As vrte_cuda_plan_create, with the plan (device buffers, streams) leased from
+ * the process-wide pool that vrte_cuda_brdf uses -- no allocation when a plan of
+ * the same shape was released before; vrte_cuda_plan_release returns it. */
+VRTE_API int32_t vrte_cuda_plan_acquire(const vrte_cuda_problem* problem, vrte_cuda_plan** out,
+                                        vrte_cuda_result* result);
+VRTE_API void vrte_cuda_plan_release(vrte_cuda_plan* plan);
 VRTE_API int32_t vrte_cuda_plan_run(vrte_cuda_plan* plan, int32_t iters, double* seconds,
                                     vrte_cuda_result* result);
 VRTE_API int32_t vrte_cuda_plan_fetch(vrte_cuda_plan* plan, double* table);
 /* tau=0 upward stacks of the plan's orders: [n_orders][4 n_in][4N] (host). */
 VRTE_API int32_t vrte_cuda_plan_fetch_up(vrte_cuda_plan* plan, double* up);
+/* Device pointer to the same stacks ([n_orders][4 n_in][4N], on the plan's
+ * device; valid until the plan's next run or destroy) and its element count:
+ * the order-sharded paths exchange them with NCCL without host staging. */
+VRTE_API int32_t vrte_cuda_plan_up_device(vrte_cuda_plan* plan, double** up, size_t* count);
+/* Fourier synthesis + Mueller recovery of ALL L orders on the plan's device and
+ * stream from device stacks up_all [L][4 n_in][4N] (order m at index m, e.g.
+ * gathered from the order shards of every rank; reconstruction.cpp:201-227,
+ * brdf.cpp:100-117), into the plan's table; copied to `table` (host
+ * [n_in][N][n_dphi][16]) when not NULL.  The caller orders its own stream's
+ * writes of up_all before the call (the call synchronizes the plan's stream). */
+VRTE_API int32_t vrte_cuda_plan_synthesize_device(vrte_cuda_plan* plan, const double* up_all, double* table,
+                                                  vrte_cuda_result* result);
 /* Per-(medium, order) eigen data for debugging: wr, wi [n_media*n_orders][4N],
  * residual [n_media*n_orders][4N]. Any pointer may be NULL. */
 VRTE_API int32_t vrte_cuda_plan_fetch_modes(vrte_cuda_plan* plan, double* wr, double* wi,

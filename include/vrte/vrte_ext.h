@@ -37,6 +37,15 @@ VRTE_API vrte_status vrte_brdf_plan_create(const vrte_material* material, const 
                                            const double* basis, int32_t device, int32_t m_begin,
                                            int32_t m_stride, int32_t n_orders, vrte_cuda_plan** out);
 
+/* vrte_brdf_plan_create with the plan leased from the process pool (the
+ * order-sharded multi-GPU calls of paper_1707_05882_b200/distributed.py: one
+ * order shard solved per call, inputs uploaded, no allocation after the first
+ * call of a shape); release it with vrte_cuda_plan_release (vrte_cuda.h). */
+VRTE_API vrte_status vrte_brdf_plan_acquire(const vrte_material* material, const vrte_options* options,
+                                            const double* mu_in, size_t n_mu_in, int32_t n_dphi,
+                                            const double* basis, int32_t device, int32_t m_begin,
+                                            int32_t m_stride, int32_t n_orders, vrte_cuda_plan** out);
+
 /* Assemble a BRDF handle from the tau = 0 upward stacks of ALL orders,
  * up_all_orders [L][4 n_mu_in][4N] (host), gathered from order shards: the
  * Fourier synthesis runs on the device and the stacks are read, not kept. */

@@ -154,7 +154,8 @@ EXPORTED = [
     "vrte_cuda_plan_destroy",
     "vrte_cuda_synthesize", "vrte_cuda_device_count", "vrte_cuda_current_device", "vrte_cuda_lu_solve", "vrte_cuda_hessenberg", "vrte_cuda_schur",
     "vrte_cuda_radiance_field", "vrte_cuda_mc_trace", "vrte_cuda_host_alloc", "vrte_cuda_host_free",
-    "vrte_cuda_debug_force_boundary_fallback",
+    "vrte_cuda_debug_force_boundary_fallback", "vrte_cuda_plan_up_device", "vrte_cuda_plan_synthesize_device",
+    "vrte_cuda_plan_acquire", "vrte_cuda_plan_release", "vrte_brdf_plan_acquire",
 ]
 
 
@@ -189,6 +190,8 @@ def lib():
     L.vrte_brdf_device_stats_get.argtypes = [vp, C.POINTER(DeviceStats)]
     L.vrte_brdf_plan_create.argtypes = [vp, C.POINTER(Options), dp, C.c_size_t, C.c_int32, dp,
                                         C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(vp)]
+    L.vrte_brdf_plan_acquire.argtypes = [vp, C.POINTER(Options), dp, C.c_size_t, C.c_int32, dp,
+                                        C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(vp)]
     L.vrte_brdf_from_stacks.argtypes = [vp, C.POINTER(Options), dp, C.c_size_t, C.c_int32, dp, dp,
                                         C.POINTER(vp)]
     L.vrte_cuda_plan_run.argtypes = [vp, C.c_int32, dp, C.POINTER(CudaResult)]
@@ -201,6 +204,10 @@ def lib():
     L.vrte_cuda_hessenberg.argtypes = [dp, C.c_int32, C.c_int32, dp, dp, C.c_int32, C.c_int32]
     L.vrte_cuda_debug_force_boundary_fallback.argtypes = [C.c_int32]
     L.vrte_cuda_debug_force_boundary_fallback.restype = None
+    L.vrte_cuda_plan_up_device.argtypes = [vp, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]
+    L.vrte_cuda_plan_release.argtypes = [vp]
+    L.vrte_cuda_plan_release.restype = None
+    L.vrte_cuda_plan_synthesize_device.argtypes = [vp, C.c_void_p, dp, C.POINTER(CudaResult)]
     L.vrte_cuda_schur.argtypes = [dp, C.c_int32, C.c_int32, dp, dp, dp, dp, C.c_int32]
     L.vrte_solve_radiance.argtypes = [vp, C.POINTER(Options), dp, C.c_size_t, C.POINTER(vp)]
     L.vrte_field_size.argtypes = [vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]
@@ -565,14 +572,18 @@ class Plan:
     """Device-resident solve plan (vrte_brdf_plan_create / vrte_cuda_plan_*)."""
 
     def __init__(self, material: Material, opts: Options, mu_in, n_dphi=19, basis=None,
-                 device=-1, m_begin=0, m_stride=1, n_orders=0):
+                 device=-1, m_begin=0, m_stride=1, n_orders=0, pooled=False):
+        """Creating the plan solves once.  pooled: lease the device buffers from
+        the process pool (vrte_brdf_plan_acquire; close() returns them)."""
         mu = np.ascontiguousarray(mu_in, dtype=np.float64)
         b = None if basis is None else np.ascontiguousarray(basis, dtype=np.float64).reshape(16)
         h = C.c_void_p()
-        _check(lib().vrte_brdf_plan_create(material._h, C.byref(opts), _dp(mu), len(mu), n_dphi,
-                                           _dp(b), device, m_begin, m_stride, n_orders,
-                                           C.byref(h)))
+        fn = lib().vrte_brdf_plan_acquire if pooled else lib().vrte_brdf_plan_create
+        _check(fn(material._h, C.byref(opts), _dp(mu), len(mu), n_dphi, _dp(b), device, m_begin, m_stride, n_orders,
+                  C.byref(h)))
         self._h = h
+        self.pooled = pooled
+        self.device = device if device >= 0 else lib().vrte_cuda_current_device()
         self.n_in, self.n_dphi = len(mu), n_dphi
         self.N = opts.quadrature_n
         self.L = min(material.info()[0], opts.order_cap) if opts.order_cap > 0 else material.info()[0]
@@ -598,6 +609,35 @@ class Plan:
         _check(lib().vrte_cuda_plan_fetch_up(self._h, _dp(out)))
         return out
 
+    def up_device(self):
+        """The tau = 0 stacks on the device, zero-copy, as a torch tensor
+        [n_orders, 4 n_in, 4N] (valid until the plan's next run or close)."""
+        import torch
+        ptr, n = C.c_void_p(), C.c_size_t()
+        _check(lib().vrte_cuda_plan_up_device(self._h, C.byref(ptr), C.byref(n)))
+        shape = (self.n_orders, 4 * self.n_in, 4 * self.N)
+
+        class _View:  # __cuda_array_interface__ v3 over the plan's buffer
+            __cuda_array_interface__ = {"shape": shape, "typestr": "<f8", "data": (ptr.value, False),
+                                        "version": 3, "strides": None}
+
+        return torch.as_tensor(_View(), device=torch.device("cuda", self.device))
+
+    def synthesize_device(self, up_all, fetch: bool = True):
+        """Synthesis of all L orders from device stacks up_all (torch tensor
+        [L, 4 n_in, 4N] on this plan's device, order m at index m); returns the
+        host table [n_in, N, n_dphi, 4, 4] (fetch) or None."""
+        import torch
+        assert up_all.is_cuda and up_all.dtype == torch.float64 and up_all.is_contiguous()
+        torch.cuda.current_stream(up_all.device).synchronize()  # its writes precede the plan's stream
+        out = np.zeros((self.n_in, self.N, self.n_dphi, 4, 4)) if fetch else None
+        r = CudaResult()
+        code = lib().vrte_cuda_plan_synthesize_device(self._h, C.c_void_p(up_all.data_ptr()),
+                                                      _dp(out) if fetch else None, C.byref(r))
+        if code != 0:
+            raise VrteError(code, r.message.decode(errors="replace"))
+        return out
+
     def modes(self, n_media: int):
         d = 4 * self.N
         n = n_media * self.n_orders * d
@@ -618,7 +658,10 @@ class Plan:
 
     def close(self):
         if getattr(self, "_h", None):
-            lib().vrte_cuda_plan_destroy(self._h)
+            if getattr(self, "pooled", False):
+                lib().vrte_cuda_plan_release(self._h)
+            else:
+                lib().vrte_cuda_plan_destroy(self._h)
             self._h = None
 
     def __del__(self):

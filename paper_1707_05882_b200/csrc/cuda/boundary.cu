@@ -335,7 +335,11 @@ __global__ void bnd_check_kernel(BndArgs a, const double* X, int G, int R, int s
         report_failure(status, kFailBoundary, 3, m, rmax, cond);
         return;
     }
-    if (stage == 0 && rmax > 1e-10 * scale) atomicExch(&status->bnd_refine, 1);
+    if (stage == 0) {  // per right-hand side, as the reference (boundary.cpp:244-248)
+        const int refine = rmax > 1e-10 * scale;
+        a.col_refine[(size_t)mo * R + r] = refine;
+        if (refine) atomicExch(&status->bnd_refine, 1);
+    }
     if (stage == 1 && bmax > 0.0 && rmax > 1e-9 * scale) report_failure(status, kFailBoundary, 3, m, rmax, cond);
 }
 
@@ -351,9 +355,10 @@ __global__ void bnd_refine_rhs_kernel(BndArgs a, const int* perm_all, double* dX
     }
 }
 
-__global__ void add_kernel(double* X, const double* dX, long long n) {
+// X += dX on the right-hand sides flagged for refinement (X, dX [mo][G][R]).
+__global__ void add_kernel(double* X, const double* dX, const int* col_refine, int G, int R, long long n) {
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
-        X[e] += dX[e];
+        if (col_refine[(e / ((long long)G * R)) * R + e % R]) X[e] += dX[e];
 }
 
 __device__ inline double probe_weight(int k, int c) {
@@ -446,7 +451,10 @@ __global__ void bnd_probe_check_kernel(BndArgs a, const double* Xp, const double
             const double cond = b1 > 0.0 ? a1 * x1 / b1 : 0.0;
             atomic_max_double(&a.condm[mo], cond);
             atomic_max_double(&status->max_boundary_residual, rel);
-            if (!finite || !(rel <= 1e-10)) atomicExch(&status->bnd_fallback, 1);
+            if (!finite || !(rel <= 1e-10)) {
+                atomicExch(&status->bnd_fallback, 1);
+                atomicExch(&a.order_fail[mo], 1);
+            }
         }
         return;
     }
@@ -457,7 +465,17 @@ __global__ void bnd_probe_check_kernel(BndArgs a, const double* Xp, const double
     bool finite = true;
     for (int n = row_lo + lane; n < G; n += 32) finite = finite && isfinite(x[(size_t)n * R]);
     finite = __all_sync(0xffffffffu, finite);
-    if (lane == 0 && !finite) atomicExch(&status->bnd_fallback, 1);
+    if (lane == 0 && !finite) {
+        atomicExch(&status->bnd_fallback, 1);
+        atomicExch(&a.order_fail[mo], 1);
+    }
+}
+
+__global__ void bnd_keep_kernel(BndArgs a, const double* saved) {
+    const long long per = (long long)4 * a.p.n_in * a.d, total = (long long)a.p.n_orders * per;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x)
+        if (!a.order_fail[e / per]) a.up[e] = saved[e];
 }
 
 __global__ void bnd_gather_b_kernel(BndArgs a, const int* perm_all, double* X, int G, int R) {
@@ -558,8 +576,9 @@ void launch_bnd_refine_rhs(const BndArgs& a, const int* perm, double* dX, int G,
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_bnd_add(double* X, const double* dX, long long n, cudaStream_t st) {
-    add_kernel<<<(unsigned)std::min(16384LL, (n + 255) / 256), 256, 0, st>>>(X, dX, n);
+void launch_bnd_add(const BndArgs& a, double* X, const double* dX, int G, int R, cudaStream_t st) {
+    const long long n = (long long)a.p.n_orders * G * R;
+    add_kernel<<<(unsigned)std::min(16384LL, (n + 255) / 256), 256, 0, st>>>(X, dX, a.col_refine, G, R, n);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -618,4 +637,10 @@ void launch_bnd_gather_b(const BndArgs& a, const int* perm, double* X, int G, in
     bnd_gather_b_kernel<<<(unsigned)std::min(16384LL, (total + 255) / 256), 256, 0, st>>>(a, perm, X, G, R);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
+void launch_bnd_keep_passed(const BndArgs& a, const double* saved, cudaStream_t st) {
+    const long long total = (long long)a.p.n_orders * 4 * a.p.n_in * a.d;
+    bnd_keep_kernel<<<(unsigned)std::min(16384LL, (total + 255) / 256), 256, 0, st>>>(a, saved);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
 }  // namespace vrte

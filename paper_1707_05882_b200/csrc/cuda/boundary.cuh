@@ -28,6 +28,8 @@ struct BndArgs {
     double* condm;        // [mo]: lower bound of cond_1(A), max over the right-hand sides
     double* colsum;       // [mo][G] scratch of the ||A||_1 reduction
     unsigned* colsum_ticket;  // [mo][G / 256 slabs]
+    int* order_fail;      // [mo] a residual probe of this order failed (the fallback redoes only these)
+    int* col_refine;      // [mo][R] right-hand sides taking the refinement step (full gate)
     int K;                // residual probes (0: the full gate); their b_k in lhs0 columns G + R + k
 };
 
@@ -53,6 +55,10 @@ void launch_bnd_probe_setup(const BndArgs& a, const int* perm, double* Xp, int G
 // Rp [mo][G][K] = A0 Xp (block-sparse), then the probe / finiteness check.
 void launch_bnd_probe_check(const BndArgs& a, const double* Xp, double* Rp, const double* X, int row_lo, int G, int R,
                             DeviceStatus* status, cudaStream_t st);
+// up[mo] <- saved[mo] for the orders whose probes passed (keep = order_fail == 0):
+// the fallback's full solve replaces only the failed orders' stacks, so an
+// order's result does not depend on the other orders of the plan.
+void launch_bnd_keep_passed(const BndArgs& a, const double* saved, cudaStream_t st);
 // Full-solution fallback: X [mo][G][R] <- rows of lhs0's B columns through the row map.
 void launch_bnd_gather_b(const BndArgs& a, const int* perm, double* X, int G, int R, cudaStream_t st);
 
@@ -67,7 +73,7 @@ void launch_bnd_residual(const BndArgs& a, const double* X, int G, int R, bool a
 void launch_bnd_check(const BndArgs& a, const double* X, int G, int R, int stage, DeviceStatus* status,
                       cudaStream_t st);
 void launch_bnd_refine_rhs(const BndArgs& a, const int* perm, double* dX, int G, int R, cudaStream_t st);
-void launch_bnd_add(double* X, const double* dX, long long n, cudaStream_t st);
+void launch_bnd_add(const BndArgs& a, double* X, const double* dX, int G, int R, cudaStream_t st);
 
 void launch_bnd_assemble(const BndArgs& a, cudaStream_t st);
 void launch_bnd_rhs(const BndArgs& a, cudaStream_t st);

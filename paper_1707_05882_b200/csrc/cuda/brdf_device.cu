@@ -129,7 +129,8 @@ struct vrte_cuda_plan {
     DevBuf<int> ipiv, perm;
     // boundary residual gate (boundary.cpp:233-257)
     DevBuf<double> lhs0, anorm, bnorm, condm, dX, Xp, Rp, colsum;
-    DevBuf<int> colsum_ticket;
+    DevBuf<int> colsum_ticket, order_fail, col_refine;
+    DevBuf<double> up_save;
     int ldl = 0;  // row stride of [A | B] (+ the probes' b_k in lhs0): G + R + 16
     const double* lhs0_zeroed = nullptr;
     size_t lhs0_zeroed_key = 0;
@@ -146,17 +147,15 @@ struct vrte_cuda_plan {
     cudaEvent_t fork[6] = {}, join[6] = {};
     int refine_iters = 1;
     int refine_extra = 2;
-    DevBuf<double> resmax;
-    double* resmax_host = nullptr;
-    double* part_host = nullptr;  // page-locked copy of DeviceStatus::part_check
+    int* count_host = nullptr;  // page-locked: [0] eigen slots still refining, [1] particular slots
     uint64_t part_extra_iters = 0;
-    double part_prev = 0.0;
+    DevBuf<int> slot_on, part_on, counts;
+    DevBuf<double> part_slot, part_prev;
     char* stage = nullptr;  // page-locked staging for the per-call inputs (one async copy each)
     size_t stage_bytes = 0;
     uint64_t launches = 0;
     ~vrte_cuda_plan() {
-        if (resmax_host) cudaFreeHost(resmax_host);
-        if (part_host) cudaFreeHost(part_host);
+        if (count_host) cudaFreeHost(count_host);
         if (refine_host) cudaFreeHost(refine_host);
         if (stage) cudaFreeHost(stage);
         for (auto& e : ev)
@@ -198,10 +197,9 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     for (auto* es : {pl.fork, pl.join})
         for (int i = 0; i < 6; ++i)
             if (!es[i]) VRTE_CUDA_CHECK(cudaEventCreateWithFlags(&es[i], cudaEventDisableTiming));
-    if (!pl.resmax_host) VRTE_CUDA_CHECK(cudaMallocHost(&pl.resmax_host, sizeof(double)));
-    if (!pl.part_host) VRTE_CUDA_CHECK(cudaMallocHost(&pl.part_host, sizeof(double)));
+    if (!pl.count_host) VRTE_CUDA_CHECK(cudaMallocHost(&pl.count_host, 2 * sizeof(int)));
     if (!pl.refine_host) VRTE_CUDA_CHECK(cudaMallocHost(&pl.refine_host, sizeof(int)));
-    pl.resmax.alloc(1);
+    pl.counts.alloc(2);
     pl.N = p->N;
     pl.L = p->L;
     pl.Lc = p->L_coeffs > 0 ? p->L_coeffs : p->L;
@@ -310,6 +308,9 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pl.lam.alloc((size_t)B * d * 2);
     pl.residual.alloc((size_t)B * d);
     pl.flags.alloc((size_t)B * d);
+    for (auto* b : {&pl.slot_on, &pl.part_on}) b->alloc(B);
+    pl.part_slot.alloc(B);
+    pl.part_prev.alloc(B);
     const size_t bdr = (size_t)B * d * R;
     for (auto* b : {&pl.sp, &pl.sm, &pl.fsp, &pl.rhs, &pl.W, &pl.g, &pl.eg, &pl.feg, &pl.zp, &pl.zm})
         b->alloc(bdr);
@@ -331,6 +332,8 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pl.bnorm.alloc((size_t)NO * R * 2);
     pl.condm.alloc((size_t)NO);
     pl.colsum.alloc((size_t)NO * G);
+    pl.order_fail.alloc((size_t)NO);
+    pl.col_refine.alloc((size_t)NO * R);
     pl.colsum_ticket.alloc((size_t)NO * ((G + 255) / 256));
     pl.dX.alloc((size_t)NO * G * R);
     pl.top0.alloc((size_t)NO * d * 2 * d);
@@ -392,6 +395,8 @@ BndArgs make_bnd(vrte_cuda_plan& pl) {
     ba.condm = pl.condm.p;
     ba.colsum = pl.colsum.p;
     ba.colsum_ticket = reinterpret_cast<unsigned*>(pl.colsum_ticket.p);
+    ba.order_fail = pl.order_fail.p;
+    ba.col_refine = pl.col_refine.p;
     return ba;
 }
 
@@ -410,7 +415,7 @@ int boundary_full_gate(vrte_cuda_plan& pl, const BndArgs& ba, cudaStream_t st) {
     if (*pl.refine_host) {
         launch_bnd_refine_rhs(ba, pl.perm.p, pl.dX.p, G, R, st);
         lu_solve_gathered(pl.lhs.p, G, pl.ldl, NO, pl.perm.p, pl.dX.p, R, st);
-        launch_bnd_add(pl.rhs_x.p, pl.dX.p, (long long)NO * G * R, st);
+        launch_bnd_add(ba, pl.rhs_x.p, pl.dX.p, G, R, st);
         launch_bnd_residual(ba, pl.dX.p, G, R, true, st);
         VRTE_CUDA_CHECK(cudaMemsetAsync(&pl.status->max_boundary_residual, 0, sizeof(double), st));
         VRTE_CUDA_CHECK(cudaMemsetAsync(pl.condm.p, 0, sizeof(double) * NO, st));
@@ -582,21 +587,27 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     // (componentwise-small on this graded matrix) does not.
     // One step normally suffices; the interim balance residual (the 8N check of
     // particular.cpp:86-105) decides about more below, at the refinement's host sync.
-    auto part_iteration = [&]() {
+    // part_on: every slot refines in the first step; the per-slot decision after
+    // each interim residual (launch_part_decide) masks the later ones
+    pa.part_on = pl.part_on.p;
+    pa.part_slot = pl.part_slot.p;
+    pa.part_prev = pl.part_prev.p;
+    launch_fill_int(pl.part_on.p, B, 1, st2);
+    VRTE_CUDA_CHECK(cudaMemsetAsync(pl.part_slot.p, 0, sizeof(double) * B, st2));
+    auto part_iteration = [&](bool first) {
         launch_part_refine_residual(pa, pl.fsp.p, st2);
         shifted_solve(pl.fsp.p, pl.W.p, R, dR, pl.sigma.p, pl.kind.p, pl.g.p, 1.0, st2);
         gemm_batched(gemm(d, R, d, pl.E.p, d, dd, false, pl.g.p, d, dR, false, pl.eg.p, d, dR, B), st2);
         gemm_batched(gemm(d, R, d, pl.F.p, d, dd, false, pl.eg.p, d, dR, false, pl.feg.p, d, dR, B), st2);
-        VRTE_CUDA_CHECK(cudaMemsetAsync(&pl.status->part_check, 0, sizeof(double), st2));
         launch_zpm(pa, st2);
         launch_part_residual(pa, st2, false);
-        VRTE_CUDA_CHECK(cudaMemcpyAsync(pl.part_host, &pl.status->part_check, sizeof(double), cudaMemcpyDeviceToHost,
-                                        st2));
+        launch_part_decide(pa, kPartTarget, first, pl.counts.p + 1, st2);
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(pl.count_host + 1, pl.counts.p + 1, sizeof(int), cudaMemcpyDeviceToHost, st2));
         VRTE_CUDA_CHECK(cudaEventRecord(pl.join[5], st2));
-        nl += 8;
+        nl += 9;
     };
-    part_iteration();
-    nl += 5;
+    part_iteration(true);
+    nl += 7;
     // (the 8N residual of the unrefined modes is not needed: every refinement
     // step starts by recomputing it, and final_residual() feeds the gate)
     ResidualArgs ra{};
@@ -662,17 +673,22 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     for (int it = 0; it < pl.refine_iters; ++it) refine_iteration();
     final_residual();
     // Adaptive: one Newton step normally brings every mode below 1e-11 (the
-    // eigenbasis correction is accurate to ~eps |FE| / gap); otherwise refine
-    // again (at most refine_extra times) before the 1e-9 gate in finish().
+    // eigenbasis correction is accurate to ~eps |FE| / gap); slots above
+    // kRefineTarget refine again (at most refine_extra times; the others are
+    // masked, so a slot's result does not depend on the rest of the plan)
+    // before the 1e-9 gate in finish().
+    launch_fill_int(pl.slot_on.p, B, 1, st);
+    rf.slot_on = pl.slot_on.p;
     for (int extra = 0; extra < pl.refine_extra; ++extra) {
-        launch_max_abs(pl.residual.p, (long long)B * d, 1, pl.resmax.p, st);
-        VRTE_CUDA_CHECK(cudaMemcpyAsync(pl.resmax_host, pl.resmax.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+        launch_refine_slots(d, B, pl.residual.p, kRefineTarget, pl.slot_on.p, pl.counts.p, st);
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(pl.count_host, pl.counts.p, sizeof(int), cudaMemcpyDeviceToHost, st));
         VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
-        nl += 1;
-        if (*pl.resmax_host <= kRefineTarget) break;
+        nl += 2;
+        if (*pl.count_host == 0) break;
         refine_iteration();
         final_residual();
     }
+    rf.slot_on = nullptr;
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[10], st));
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[1], st));
     // ---------------- particular: runs on the side stream, concurrent with the refinement;
@@ -686,15 +702,12 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     // The particular stage's refinement, like the eigenpairs': another step while
     // its balance residual exceeds kPartTarget (a tenth of the reference's 1e-6
     // gate); decided here, with the boundary assembly already queued.
-    // Stops when a step no longer halves the residual (its fp64 floor).
-    for (int part_extra = 0, prev = 0; ; ++part_extra) {
+    // Per slot: stops when a step no longer halves the residual (its fp64 floor).
+    for (int part_extra = 0; part_extra < kPartExtraMax; ++part_extra) {
         VRTE_CUDA_CHECK(cudaEventSynchronize(pl.join[5]));
-        const double cur = *pl.part_host;
-        if (cur <= kPartTarget || part_extra >= kPartExtraMax || (prev && !(cur < 0.5 * pl.part_prev))) break;
-        pl.part_prev = cur;
-        prev = 1;
+        if (pl.count_host[1] == 0) break;
         ++pl.part_extra_iters;
-        part_iteration();
+        part_iteration(false);
     }
     launch_part_residual(pa, st2);  // the reference's gates on the final particular vectors
     VRTE_CUDA_CHECK(cudaEventRecord(pl.join[2], st2));
@@ -724,6 +737,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     } else {
         // BRDF: layer 0's unknowns only (the last 2d rows); the K residual probes
         // through every row on the side stream, concurrently
+        VRTE_CUDA_CHECK(cudaMemsetAsync(pl.order_fail.p, 0, sizeof(int) * NO, st));
         launch_bnd_probe_setup(ba, pl.perm.p, pl.Xp.p, G, R, st);
         VRTE_CUDA_CHECK(cudaEventRecord(pl.fork[4], st));
         VRTE_CUDA_CHECK(cudaStreamWaitEvent(st2, pl.fork[4], 0));
@@ -753,20 +767,25 @@ std::atomic<int> g_force_fallback{0};
 
 bool boundary_fallback(vrte_cuda_plan& pl, bool synth) {
     if (pl.full_solution) return false;
-    if (g_force_fallback.load()) {
+    if (g_force_fallback.load()) {  // test hook: every order "failed"
         const int one = 1;
         VRTE_CUDA_CHECK(cudaMemcpyAsync(&pl.status->bnd_fallback, &one, sizeof(int), cudaMemcpyHostToDevice, pl.st));
+        launch_fill_int(pl.order_fail.p, pl.NO, 1, pl.st);
     }
     VRTE_CUDA_CHECK(cudaMemcpyAsync(pl.refine_host, &pl.status->bnd_fallback, sizeof(int), cudaMemcpyDeviceToHost, pl.st));
     VRTE_CUDA_CHECK(cudaStreamSynchronize(pl.st));
     if (!*pl.refine_host) return false;
     cudaStream_t st = pl.st;
     const BndArgs ba = make_bnd(pl);
+    pl.up_save.alloc(pl.up.n);
+    VRTE_CUDA_CHECK(cudaMemcpyAsync(pl.up_save.p, pl.up.p, sizeof(double) * pl.up.n, cudaMemcpyDeviceToDevice, st));
     launch_bnd_gather_b(ba, pl.perm.p, pl.rhs_x.p, pl.G, pl.R, st);
     lu_solve_gathered(pl.lhs.p, pl.G, pl.ldl, pl.NO, pl.perm.p, pl.rhs_x.p, pl.R, st);
     uint64_t nl = 1 + lu_rm_launch_count(pl.G);
     nl += boundary_full_gate(pl, ba, st);
     nl += boundary_top(pl, ba, st);
+    launch_bnd_keep_passed(ba, pl.up_save.p, st);  // only the failed orders change
+    nl += 1;
     if (synth) {
         VRTE_CUDA_CHECK(cudaMemsetAsync(&pl.status->clamped, 0, sizeof(unsigned long long), st));
         VRTE_CUDA_CHECK(cudaMemsetAsync(&pl.status->neg_key, 0, sizeof(unsigned long long), st));
@@ -1039,6 +1058,32 @@ int32_t vrte_cuda_plan_create(const vrte_cuda_problem* problem, vrte_cuda_plan**
     });
 }
 
+int32_t vrte_cuda_plan_acquire(const vrte_cuda_problem* problem, vrte_cuda_plan** out, vrte_cuda_result* result) {
+    return guarded(result, [&]() -> int32_t {
+        if (!out || !problem) throw std::invalid_argument("null plan pointer");
+        *out = nullptr;
+        PlanLease lease(problem->device);
+        vrte_cuda_plan& pl = *lease;
+        setup_plan(pl, problem);
+        pl.full_solution = false;
+        pl.launches = run_pipeline(pl, pl.full_orders);
+        boundary_fallback(pl, pl.full_orders);
+        const int rc = finish(pl, result);
+        if (rc == 0) *out = lease.p.release();  // the caller's until vrte_cuda_plan_release
+        return rc;
+    });
+}
+
+void vrte_cuda_plan_release(vrte_cuda_plan* pl) {
+    if (!pl) return;
+    std::unique_ptr<vrte_cuda_plan> p(pl);
+    int dev = pl->device;
+    if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_pool.push_back(std::move(p));
+    g_pool_dev.push_back(dev);
+}
+
 int32_t vrte_cuda_plan_run(vrte_cuda_plan* pl, int32_t iters, double* seconds,
                            vrte_cuda_result* result) {
     return guarded(result, [&]() -> int32_t {
@@ -1083,6 +1128,61 @@ int32_t vrte_cuda_plan_fetch_up(vrte_cuda_plan* pl, double* up) {
         return 3;
     }
     return 0;
+}
+
+int32_t vrte_cuda_plan_up_device(vrte_cuda_plan* pl, double** up, size_t* count) {
+    if (!pl || !up || !count) return 5;
+    *up = pl->up.p;
+    *count = pl->up.n;
+    return 0;
+}
+
+int32_t vrte_cuda_plan_synthesize_device(vrte_cuda_plan* pl, const double* up_all, double* table,
+                                         vrte_cuda_result* result) {
+    return guarded(result, [&]() -> int32_t {
+        if (!pl || !up_all) throw std::invalid_argument("null plan or stacks");
+        if (pl->device >= 0) VRTE_CUDA_CHECK(cudaSetDevice(pl->device));
+        cudaStream_t st = pl->st;
+        const int L = pl->L;
+        std::vector<int> slot(L);
+        for (int m = 0; m < L; ++m) slot[m] = m;
+        pl->slot_all.upload(slot.data(), L, st);
+        VRTE_CUDA_CHECK(cudaMemsetAsync(pl->status, 0, sizeof(DeviceStatus), st));
+        SynthArgs sa{};
+        sa.N = pl->N;
+        sa.L = L;
+        sa.n_in = pl->n_in;
+        sa.n_dphi = pl->n_dphi;
+        sa.up = up_all;
+        sa.slot_of_order = pl->slot_all.p;
+        sa.trig = pl->trig.p;
+        sa.post = pl->post.p;
+        sa.out = pl->out.p;
+        sa.status = pl->status;
+        launch_synth(sa, st);
+        if (table)
+            VRTE_CUDA_CHECK(cudaMemcpyAsync(table, pl->out.p, sizeof(double) * pl->out.n, cudaMemcpyDeviceToHost, st));
+        DeviceStatus s{};
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(&s, pl->status, sizeof s, cudaMemcpyDeviceToHost, st));
+        VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
+        if (result) {
+            result->clamped = s.clamped;
+            result->kernel_launches = 1;
+        }
+        if (s.code == kFailNegativeIntensity && s.neg_key != 0) {
+            const unsigned long long idx = ~s.neg_key;
+            VRTE_CUDA_CHECK(cudaMemcpy(&s.value, pl->out.p + idx * 16, sizeof(double), cudaMemcpyDeviceToHost));
+        }
+        if (s.code != 0) {
+            fill_message(result, 3, describe_failure(s, {}, 0, {}));
+            return 3;
+        }
+        if (result) {
+            result->status = 0;
+            result->message[0] = 0;
+        }
+        return 0;
+    });
 }
 
 int32_t vrte_cuda_plan_fetch_modes(vrte_cuda_plan* pl, double* wr, double* wi, double* residual,

@@ -2151,6 +2151,17 @@ __global__ void set_identity_batched_kernel(double* Z, int d, long long total) {
     }
 }
 
+__global__ void fill_int_kernel(int* p, int n, int v) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+void launch_fill_int(int* p, int n, int value, cudaStream_t st) {
+    if (n <= 0) return;
+    fill_int_kernel<<<(n + 255) / 256, 256, 0, st>>>(p, n, value);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
 void launch_set_identity(double* Z, int d, int batch, cudaStream_t st) {
     const long long total = (long long)d * d * batch;
     const long long blocks = (total + 255) / 256;

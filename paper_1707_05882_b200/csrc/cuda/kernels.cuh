@@ -92,6 +92,7 @@ void launch_eig_diag_solve(double* W, int d, int ncol, long long w_stride, const
                            const double* wi, const double* sigma, const int* kind, int batch,
                            cudaStream_t st);
 void launch_set_identity(double* Z, int d, int batch, cudaStream_t st);
+void launch_fill_int(int* p, int n, int value, cudaStream_t st);
 // Analytic modes / zero particular solution of free-streaming (kernel-free)
 // slots [b0, b1) (eig.cu).
 void launch_free_modes(int d, int b0, int b1, const double* mdiag, double* psi_p, double* psi_m,

@@ -114,7 +114,10 @@ __global__ void part_residual_kernel(PartArgs a, bool final) {
     xmax = warp_max(xmax);
     finite = __all_sync(0xffffffffu, finite);
     if (lane == 0 && !final) {
-        if (xmax > 0.0) atomic_max_double(&a.status->part_check, balmax / xmax);
+        if (xmax > 0.0) {
+            atomic_max_double(&a.status->part_check, balmax / xmax);
+            if (a.part_slot) atomic_max_double(&a.part_slot[om], balmax / xmax);
+        }
         return;
     }
     if (lane == 0) {
@@ -144,7 +147,18 @@ __global__ void refine_residual_kernel(PartArgs a, double* W) {
     const int om = (int)(idx / ((long long)R * d));
     const int col = (int)((idx / d) % R);
     const double sg = a.sigma[2 * ((size_t)om * R + col)];
-    W[idx] = a.rhs[idx] - (a.feg[idx] - sg * a.g[idx]);
+    W[idx] = (a.part_on && !a.part_on[om]) ? 0.0 : a.rhs[idx] - (a.feg[idx] - sg * a.g[idx]);
+}
+
+__global__ void part_decide_kernel(PartArgs a, double target, int first, int* count) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= a.batch) return;
+    const double cur = a.part_slot[b];
+    const int on = a.part_on[b] && cur > target && (first || cur < 0.5 * a.part_prev[b]);
+    a.part_on[b] = on;
+    a.part_prev[b] = cur;
+    a.part_slot[b] = 0.0;  // ready for the next interim residual
+    if (on) atomicAdd(count, 1);
 }
 
 }  // namespace
@@ -173,6 +187,12 @@ void launch_zpm(const PartArgs& a, cudaStream_t st) {
 void launch_part_residual(const PartArgs& a, cudaStream_t st, bool final) {
     const long long warps = (long long)a.batch * 4 * a.n_in;
     part_residual_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(a, final);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_part_decide(const PartArgs& a, double target, bool first, int* count, cudaStream_t st) {
+    VRTE_CUDA_CHECK(cudaMemsetAsync(count, 0, sizeof(int), st));
+    part_decide_kernel<<<(a.batch + 127) / 128, 128, 0, st>>>(a, target, first ? 1 : 0, count);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 

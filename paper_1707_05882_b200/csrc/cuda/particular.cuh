@@ -25,6 +25,10 @@ struct PartArgs {
     double* zp;                   // Z+ [batch][R][d]
     double* zm;                   // Z-
     DeviceStatus* status;
+    // per-slot adaptive refinement (null: every slot, no bookkeeping)
+    int* part_on;                 // [batch] slot still refining
+    double* part_slot;            // [batch] interim max balance residual
+    double* part_prev;            // [batch] its value at the previous decision
 };
 
 void launch_dither(const PartArgs& a, cudaStream_t st);
@@ -34,5 +38,9 @@ void launch_zpm(const PartArgs& a, cudaStream_t st);
 // part_check) for the adaptive refinement; final = true: the reference's gates.
 void launch_part_residual(const PartArgs& a, cudaStream_t st, bool final = true);
 void launch_part_refine_residual(const PartArgs& a, double* W, cudaStream_t st);
+// After an interim launch_part_residual: part_on[b] stays on while its balance
+// residual exceeds `target` and (first decision, or) halved since the last one;
+// count = slots still on.  Off slots get a zero correction (g unchanged).
+void launch_part_decide(const PartArgs& a, double target, bool first, int* count, cudaStream_t st);
 
 }  // namespace vrte

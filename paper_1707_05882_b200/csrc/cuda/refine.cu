@@ -97,6 +97,7 @@ __global__ void normalize_kernel(RefineArgs a) {
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     MRef m;
     if (!mref(gw, a, m)) return;
+    if (a.slot_on && !a.slot_on[m.b]) return;
     const int d = m.d;
     if (!active(a, m)) {
         // conservative modes: only refresh the residual inputs
@@ -145,6 +146,7 @@ __global__ void setup_kernel(RefineArgs a) {
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     MRef m;
     if (!mref(gw, a, m)) return;
+    if (a.slot_on && !a.slot_on[m.b]) return;
     const int d = m.d;
     const bool act = active(a, m);
     const size_t kb = (size_t)m.b * 2 * d;
@@ -184,6 +186,7 @@ __global__ void rhs_kernel(RefineArgs a) {
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     MRef m;
     if (!mref(gw, a, m) || !active(a, m)) return;
+    if (a.slot_on && !a.slot_on[m.b]) return;
     const int d = m.d;
     const cplx s = (1.0 + a.shift[m.vb + m.j]) * cmk(a.rho[2 * (m.vb + m.j)], a.rho[2 * (m.vb + m.j) + 1]);
     for (int set = 0; set < 2; ++set) {
@@ -199,6 +202,7 @@ __global__ void update_kernel(RefineArgs a) {
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     MRef m;
     if (!mref(gw, a, m) || !active(a, m)) return;
+    if (a.slot_on && !a.slot_on[m.b]) return;
     const int d = m.d;
     const cplx s = (1.0 + a.shift[m.vb + m.j]) * cmk(a.rho[2 * (m.vb + m.j)], a.rho[2 * (m.vb + m.j) + 1]);
     const int si = a.sidx[m.vb + m.j];
@@ -257,6 +261,20 @@ __global__ void nu_rho_kernel(RefineArgs a, int to_rho) {
     }
 }
 
+__global__ void refine_slots_kernel(int d, int batch, const double* residual, double target, int* slot_on,
+                                    int* count) {
+    const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (b >= batch) return;
+    double mx = 0.0;
+    for (int j = lane; j < d; j += 32) mx = fmax(mx, residual[(size_t)b * d + j]);
+    mx = warp_max(mx);
+    if (lane == 0) {
+        const int on = slot_on[b] && mx > target;
+        slot_on[b] = on;
+        if (on) atomicAdd(count, 1);
+    }
+}
+
 inline unsigned warps_grid(int batch, int d) {
     return (unsigned)(((long long)batch * d * 32 + 255) / 256);
 }
@@ -286,6 +304,13 @@ void launch_refine_update(const RefineArgs& a, cudaStream_t st) {
 void launch_nu_rho(const RefineArgs& a, bool to_rho, cudaStream_t st) {
     const int n = a.batch * a.d;
     nu_rho_kernel<<<(n + 255) / 256, 256, 0, st>>>(a, to_rho ? 1 : 0);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_refine_slots(int d, int batch, const double* residual, double target, int* slot_on, int* count,
+                         cudaStream_t st) {
+    VRTE_CUDA_CHECK(cudaMemsetAsync(count, 0, sizeof(int), st));
+    refine_slots_kernel<<<(batch + 7) / 8, 256, 0, st>>>(d, batch, residual, target, slot_on, count);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -30,6 +30,7 @@ struct RefineArgs {
     double* EU;           // E u~
     double* sigma;        // [batch][2d][2]
     int* kind;            // [batch][2d]
+    const int* slot_on;   // [batch] or null: slots whose modes are refined this step
 };
 
 void launch_refine_shift(const RefineArgs& a, cudaStream_t st);
@@ -38,5 +39,10 @@ void launch_refine_setup(const RefineArgs& a, cudaStream_t st);
 void launch_refine_rhs(const RefineArgs& a, cudaStream_t st);
 void launch_refine_update(const RefineArgs& a, cudaStream_t st);
 void launch_nu_rho(const RefineArgs& a, bool to_rho, cudaStream_t st);
+// slot_on[b] &= (max_j residual[b][j] > target); count = number of slots left on.
+// The refinement's extra steps are decided per (medium, order) slot, so a slot's
+// result does not depend on which other slots share the plan (order shards).
+void launch_refine_slots(int d, int batch, const double* residual, double target, int* slot_on, int* count,
+                         cudaStream_t st);
 
 }  // namespace vrte

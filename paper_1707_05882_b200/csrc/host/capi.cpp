@@ -907,6 +907,28 @@ vrte_status vrte_brdf_plan_create(const vrte_material* material, const vrte_opti
     });
 }
 
+vrte_status vrte_brdf_plan_acquire(const vrte_material* material, const vrte_options* options,
+                                   const double* mu_in, size_t n_mu_in, int32_t n_dphi,
+                                   const double* basis, int32_t device, int32_t m_begin,
+                                   int32_t m_stride, int32_t n_orders, vrte_cuda_plan** out) {
+    if (!material || !out || !mu_in || n_mu_in == 0) return set_error(VRTE_E_ARGUMENT, "null argument");
+    return guarded([&] {
+        BrdfSetup s;
+        build_setup(s, material->spec, options, mu_in, n_mu_in, n_dphi, basis);
+        s.prob.device = device;
+        s.prob.m_begin = m_begin;
+        s.prob.m_stride = m_stride > 0 ? m_stride : 1;
+        s.prob.n_orders = n_orders;
+        s.prob.devices = nullptr;
+        s.prob.n_devices = 0;
+        vrte_cuda_result r{};
+        const int32_t rc = vrte_cuda_plan_acquire(&s.prob, out, &r);
+        if (rc == 5) throw std::invalid_argument(r.message);
+        if (rc != 0) throw NumericalError(r.message);
+        return VRTE_OK;
+    });
+}
+
 vrte_status vrte_brdf_from_stacks(const vrte_material* material, const vrte_options* options,
                                   const double* mu_in, size_t n_mu_in, int32_t n_dphi,
                                   const double* basis, const double* up_all_orders, vrte_brdf** out) {

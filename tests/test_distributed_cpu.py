@@ -70,9 +70,20 @@ def _worker(rank, world, port, q):
     local = up[m_begin::m_stride]
     assert local.shape[0] == n
     full = D.gather_orders(local.reshape(n, -1), L, world, rank).reshape(up.shape)
+    # the product's point-to-point gather (to rank 0) and all-to-all (solve j to rank j)
+    import torch
+    g = D.gather_order_stacks(torch.from_numpy(np.ascontiguousarray(local)), L, world, rank)
+    # W in-flight solves: solve j = the stacks scaled by (j + 1) (distinct data per solve)
+    a2a = D.alltoall_order_stacks([torch.from_numpy(np.ascontiguousarray(local * (j + 1))) for j in range(world)],
+                                  L, world, rank)
+    ok_a2a = bool(np.array_equal(a2a.numpy(), up * (rank + 1)))
+    oks = [None] * world
+    dist.all_gather_object(oks, ok_a2a)
     if rank == 0:
-        q.put((np.array_equal(full, up), float(np.abs(synthesize(full, nodes[:3], 7) - ref).max()),
-               float(np.abs(ref).max())))
+        q.put((np.array_equal(full, up) and np.array_equal(g.numpy(), up) and all(oks),
+               float(np.abs(synthesize(full, nodes[:3], 7) - ref).max()), float(np.abs(ref).max())))
+    else:
+        assert g is None
     dist.barrier()
     dist.destroy_process_group()
 
