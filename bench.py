@@ -690,6 +690,7 @@ def main():
     for _ in range(args.steps):
         b = V.compute_brdf(mat, opts, nodes, w.n_dphi)
         stats = b.device_stats()
+        n_out = b.shape[1]  # N, or the refraction cone's nodes under a Fresnel interface
         b.close()
     e2e_s = time.perf_counter() - t0
     t_e2e = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
@@ -699,7 +700,7 @@ def main():
     N, L, n_in, nd = w.N, w.material.order_count, len(nodes), w.n_dphi
     P, S = len(w.material.layers), 2
     h2d = 8 * (2 * N + S + S * L * 6 + P + n_in + n_in * N * 16 + n_in * 16 + L * nd * 2) + 4 * P
-    d2h = 8 * n_in * N * nd * 16
+    d2h = 8 * n_in * n_out * nd * 16
 
     if rank != 0:
         if dist:

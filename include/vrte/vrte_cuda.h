@@ -56,6 +56,15 @@ typedef struct vrte_cuda_problem {
        several shards on one device. */
     const int32_t* devices;
     int32_t n_devices;
+    /* Fresnel top interface (extension; NULL / 0 without one): refl_top [N][16]
+       row-major Mueller reflection of the upward field at tau = 0 into the
+       downward one (top boundary rows: down - R up = 0); pre [N][16] the
+       left factor of the synthesized exit Mueller matrix per output node
+       (T_out / n^2); the table keeps output nodes out_lo .. N-1 (the
+       refraction cone). */
+    const double* refl_top;
+    const double* pre;
+    int32_t out_lo;
 } vrte_cuda_problem;
 
 typedef struct vrte_cuda_result {

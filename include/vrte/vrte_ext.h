@@ -29,6 +29,11 @@ typedef struct vrte_brdf_device_stats {
 
 VRTE_API vrte_status vrte_brdf_device_stats_get(const vrte_brdf* brdf, vrte_brdf_device_stats* out);
 
+/* The table's grids (any pointer may be NULL): mu_in [n_in] as requested,
+ * mu_out [n_out] the exit cosines (the quadrature nodes; with a Fresnel
+ * interface the refraction cone's nodes mapped to the outside), dphi [n_dphi]. */
+VRTE_API vrte_status vrte_brdf_grid(const vrte_brdf* brdf, double* mu_in, double* mu_out, double* dphi);
+
 /* Build the device problem of a BRDF request without solving it (benchmark
  * plan creation; see vrte_cuda.h).  Returns an opaque plan. */
 typedef struct vrte_cuda_plan vrte_cuda_plan;

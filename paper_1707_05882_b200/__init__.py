@@ -146,7 +146,7 @@ EXPORTED = [
     "vrte_brdf_timings", "vrte_brdf_free", "vrte_mc_trace", "vrte_mc_tally_row",
     "vrte_mc_tally_write_csv", "vrte_mc_tally_free",
     # vrte_ext.h
-    "vrte_brdf_device_stats_get", "vrte_brdf_plan_create", "vrte_brdf_from_stacks",
+    "vrte_brdf_device_stats_get", "vrte_brdf_plan_create", "vrte_brdf_from_stacks", "vrte_brdf_grid",
     "vrte_compute_brdf_batch", "vrte_mc_tally_hits",
     # vrte_cuda.h
     "vrte_cuda_brdf", "vrte_cuda_plan_create", "vrte_cuda_plan_run", "vrte_cuda_plan_fetch",
@@ -188,6 +188,7 @@ def lib():
     L.vrte_brdf_timings.argtypes = [vp, C.POINTER(Timings)]
     L.vrte_brdf_free.argtypes = [vp]
     L.vrte_brdf_device_stats_get.argtypes = [vp, C.POINTER(DeviceStats)]
+    L.vrte_brdf_grid.argtypes = [vp, dp, dp, dp]
     L.vrte_brdf_plan_create.argtypes = [vp, C.POINTER(Options), dp, C.c_size_t, C.c_int32, dp,
                                         C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(vp)]
     L.vrte_brdf_plan_acquire.argtypes = [vp, C.POINTER(Options), dp, C.c_size_t, C.c_int32, dp,
@@ -361,6 +362,12 @@ class Brdf:
                 for p in range(npd):
                     _check(lib().vrte_brdf_entry(self._h, i, o, p, _dp(e)))
                     out[i, o, p] = e.reshape(4, 4)
+        return out
+
+    def mu_out(self) -> np.ndarray:
+        """Exit cosines of the table (vrte_brdf_grid, vrte_ext.h)."""
+        out = np.zeros(self.shape[1])
+        _check(lib().vrte_brdf_grid(self._h, None, _dp(out), None))
         return out
 
     def reflectance(self, i) -> np.ndarray:

@@ -73,8 +73,24 @@ __global__ void assemble_kernel(BndArgs a) {
         return Ref{A + o, A0 ? A0 + o : nullptr};
     };
     if (p == 0) {
-        at(i, ca) = pk(dflip(pm, i));
-        at(i, cbk) = pk(att * dflip(pp, i));
+        if (a.p.refl_top) {
+            // Fresnel interface (extension): top rows are down - R up = 0, R the
+            // interface reflection of node i/4 applied to the upward Stokes vector
+            const double* Rm = a.p.refl_top + (size_t)(i >> 2) * 16 + 4 * (i & 3);
+            cplx ua = cmk(0.0, 0.0), ub = cmk(0.0, 0.0);
+            for (int q = 0; q < 4; ++q) {
+                cplx ppq, pmq, nuq;
+                bool imq;
+                mv.load(om, jj, (i & ~3) + q, ppq, pmq, nuq, imq);
+                ua = ua + Rm[q] * ppq;
+                ub = ub + Rm[q] * (att * pmq);
+            }
+            at(i, ca) = pk(dflip(pm, i) - ua);
+            at(i, cbk) = pk(att * dflip(pp, i) - ub);
+        } else {
+            at(i, ca) = pk(dflip(pm, i));
+            at(i, cbk) = pk(att * dflip(pp, i));
+        }
         double* T0 = a.top0 + (size_t)mo * d * 2 * d;
         T0[(size_t)jj * d + i] = pk(pp);
         T0[(size_t)(d + jj) * d + i] = pk(att * pm);
@@ -214,7 +230,16 @@ __global__ void rhs_kernel(BndArgs a) {
         const size_t om = (size_t)a.p.medium[p] * a.p.n_orders + mo;
         return a.zm[(om * R + col) * d + i];
     };
-    for (int i = lane; i < d; i += 32) B[i] = -zm(0, i);
+    if (a.p.refl_top) {  // Fresnel interface: down - R up = -Z- + R Z+ at tau = 0
+        for (int i = lane; i < d; i += 32) {
+            const double* Rm = a.p.refl_top + (size_t)(i >> 2) * 16 + 4 * (i & 3);
+            double r = -zm(0, i);
+            for (int q = 0; q < 4; ++q) r += Rm[q] * zp(0, (i & ~3) + q);
+            B[i] = r;
+        }
+    } else {
+        for (int i = lane; i < d; i += 32) B[i] = -zm(0, i);
+    }
     double tau_top = 0.0;
     for (int p = 0; p + 1 < P; ++p) {
         tau_top += a.p.tau[p];

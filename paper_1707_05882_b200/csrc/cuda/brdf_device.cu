@@ -113,7 +113,8 @@ struct vrte_cuda_plan {
     } rad;
     ProblemDev pd{};
     // inputs
-    DevBuf<double> nodes, weights, mdiag, omega, greek, tau, mu_in, table, beam_rows, post, trig;
+    DevBuf<double> nodes, weights, mdiag, omega, greek, tau, mu_in, table, beam_rows, post, trig, refl_top, pre;
+    int out_lo = 0;
     DevBuf<int> medium, order_index, slot_of_order;
     // homogeneous
     DevBuf<double> gsf_n, gsf_b, E, F, T, Z, psi_p, psi_m, tmp1, tmp2, tmp3, tmp4;
@@ -248,7 +249,7 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     // (pageable sources would be staged by the driver one copy at a time)
     {
         const size_t tab_n = p->base_type == 2 ? (size_t)p->table_n * p->table_n * 16 : 16;
-        const size_t need_d = 2 * (size_t)N + d + pl.S + (size_t)pl.S * pl.Lc * 6 + pl.P + pl.n_in + tab_n +
+        const size_t need_d = 2 * (size_t)N + d + pl.S + (size_t)pl.S * pl.Lc * 6 + pl.P + pl.n_in + tab_n + 32 * (size_t)N +
                               (size_t)pl.n_in * N * 16 + (size_t)pl.n_in * 16 + (size_t)L * pl.n_dphi * 2;
         const size_t need = need_d * sizeof(double) + ((size_t)pl.P + B + L) * sizeof(int) + 32 * 256;
         if (pl.stage_bytes < need) {
@@ -281,6 +282,11 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     put(pl.beam_rows, p->beam_rows, (size_t)pl.n_in * N * 16);
     put(pl.post, p->post, (size_t)pl.n_in * 16);
     put(pl.trig, p->trig, (size_t)L * pl.n_dphi * 2);
+    pl.out_lo = p->refl_top ? p->out_lo : 0;
+    if (p->refl_top) {
+        put(pl.refl_top, p->refl_top, (size_t)N * 16);
+        put(pl.pre, p->pre, (size_t)N * 16);
+    }
     put(pl.order_index, order_index.data(), B);
     put(pl.slot_of_order, slot.data(), L);
 
@@ -341,7 +347,7 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pl.ipiv.alloc((size_t)NO * G);
     pl.perm.alloc((size_t)NO * G);
     pl.up.alloc((size_t)NO * R * d);
-    pl.out.alloc((size_t)pl.n_in * N * pl.n_dphi * 16);
+    pl.out.alloc((size_t)pl.n_in * (N - pl.out_lo) * pl.n_dphi * 16);
     pl.status_buf.alloc(1);
     pl.status = pl.status_buf.p;
 
@@ -368,6 +374,7 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pd.table_n = p->table_n;
     pd.table = pl.table.p;
     pd.beam_rows = pl.beam_rows.p;
+    pd.refl_top = p->refl_top ? pl.refl_top.p : nullptr;
 }
 
 BndArgs make_bnd(vrte_cuda_plan& pl) {
@@ -451,6 +458,8 @@ int run_synth(vrte_cuda_plan& pl, cudaStream_t st) {
     sa.post = pl.post.p;
     sa.out = pl.out.p;
     sa.status = pl.status;
+    sa.pre = pl.pd.refl_top ? pl.pre.p : nullptr;
+    sa.out_lo = pl.out_lo;
     launch_synth(sa, st);
     return 1;
 }
@@ -1159,6 +1168,8 @@ int32_t vrte_cuda_plan_synthesize_device(vrte_cuda_plan* pl, const double* up_al
         sa.post = pl->post.p;
         sa.out = pl->out.p;
         sa.status = pl->status;
+        sa.pre = pl->pd.refl_top ? pl->pre.p : nullptr;
+        sa.out_lo = pl->out_lo;
         launch_synth(sa, st);
         if (table)
             VRTE_CUDA_CHECK(cudaMemcpyAsync(table, pl->out.p, sizeof(double) * pl->out.n, cudaMemcpyDeviceToHost, st));
@@ -1298,6 +1309,8 @@ int32_t brdf_sharded(const vrte_cuda_problem* problem, double* table, vrte_cuda_
     sa.post = root.post.p;
     sa.out = root.out.p;
     sa.status = root.status;
+    sa.pre = root.pd.refl_top ? root.pre.p : nullptr;
+    sa.out_lo = root.out_lo;
     launch_synth(sa, st);
     VRTE_CUDA_CHECK(cudaMemcpyAsync(table, root.out.p, sizeof(double) * root.out.n, cudaMemcpyDeviceToHost, st));
     DeviceStatus s{};
@@ -1473,7 +1486,7 @@ int32_t vrte_cuda_synthesize(const vrte_cuda_problem* problem, const double* up,
         VRTE_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         const int N = problem->N, L = problem->L, n_in = problem->n_in, np = problem->n_dphi;
         const size_t upn = (size_t)L * 4 * n_in * 4 * N;
-        DevBuf<double> dup, dtrig, dpost, dout;
+        DevBuf<double> dup, dtrig, dpost, dout, dpre;
         DevBuf<int> dslot;
         DevBuf<DeviceStatus> dst;
         std::vector<int> slot(L);
@@ -1482,7 +1495,9 @@ int32_t vrte_cuda_synthesize(const vrte_cuda_problem* problem, const double* up,
         dtrig.upload(problem->trig, (size_t)L * np * 2, st);
         dpost.upload(problem->post, (size_t)n_in * 16, st);
         dslot.upload(slot.data(), L, st);
-        dout.alloc((size_t)n_in * N * np * 16);
+        const int out_lo = problem->refl_top ? problem->out_lo : 0;
+        if (problem->refl_top) dpre.upload(problem->pre, (size_t)N * 16, st);
+        dout.alloc((size_t)n_in * (N - out_lo) * np * 16);
         dst.alloc(1);
         VRTE_CUDA_CHECK(cudaMemsetAsync(dst.p, 0, sizeof(DeviceStatus), st));
         SynthArgs sa{};
@@ -1494,6 +1509,8 @@ int32_t vrte_cuda_synthesize(const vrte_cuda_problem* problem, const double* up,
         sa.slot_of_order = dslot.p;
         sa.trig = dtrig.p;
         sa.post = dpost.p;
+        sa.pre = problem->refl_top ? dpre.p : nullptr;
+        sa.out_lo = out_lo;
         sa.out = dout.p;
         sa.status = dst.p;
         launch_synth(sa, st);

@@ -24,6 +24,7 @@ struct ProblemDev {
     int table_n;
     const double* table;      // [table_n*table_n][16] row-major
     const double* beam_rows;  // [n_in][N][16] base_row_at(mu_i, mu0) (boundary.cpp:37-71)
+    const double* refl_top;   // [N][16] Fresnel interface: down = R up at tau = 0 (null: none)
     __host__ __device__ int order_of(int mo) const { return m_begin + mo * m_stride; }
 };
 

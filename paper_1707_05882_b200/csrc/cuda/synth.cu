@@ -15,11 +15,12 @@ namespace {
 __global__ void synth_kernel(SynthArgs a) {
     const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     const int N = a.N, np = a.n_dphi, d = 4 * N, R = 4 * a.n_in;
-    const long long total = (long long)a.n_in * N * np;
+    const int No = N - a.out_lo;
+    const long long total = (long long)a.n_in * No * np;
     if (idx >= total) return;
     const int ip = (int)(idx % np);
-    const int io = (int)((idx / np) % N);
-    const int ii = (int)(idx / ((long long)np * N));
+    const int io = a.out_lo + (int)((idx / np) % No);
+    const int ii = (int)(idx / ((long long)np * No));
     double e[4][4];
 #pragma unroll
     for (int r = 0; r < 4; ++r)
@@ -38,6 +39,19 @@ __global__ void synth_kernel(SynthArgs a) {
 #pragma unroll
             for (int r = 0; r < 4; ++r) e[r][c] += 0.5 * ((c < 2 ? p1[r] : p2[r]) * col[r]);
         }
+    }
+    if (a.pre) {  // exit through the interface: e <- pre(node) e
+        const double* P = a.pre + (size_t)io * 16;
+        double t[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) t[r][c] = P[4 * r] * e[0][c] + P[4 * r + 1] * e[1][c] + P[4 * r + 2] * e[2][c] +
+                                                  P[4 * r + 3] * e[3][c];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) e[r][c] = t[r][c];
     }
     const double* Tm = a.post + (size_t)ii * 16;
     double f[16];
@@ -73,7 +87,7 @@ __global__ void synth_kernel(SynthArgs a) {
 }  // namespace
 
 void launch_synth(const SynthArgs& a, cudaStream_t st) {
-    const long long total = (long long)a.n_in * a.N * a.n_dphi;
+    const long long total = (long long)a.n_in * (a.N - a.out_lo) * a.n_dphi;
     synth_kernel<<<(unsigned)((total + 127) / 128), 128, 0, st>>>(a);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }

@@ -150,6 +150,8 @@ struct BrdfSetup {
     int L = 0;
     std::vector<int> medium, rep, devices;
     std::vector<double> omega, greek, tau, mu_in, beam_rows, post, trig, table_flat, dphi;
+    std::vector<double> mu_in_user, refl_top, pre;  // Fresnel interface (mu_in = refracted cosines)
+    Quadrature quad_out;  // output nodes / weights of the table (= quad without an interface)
     double basis[16];
     vrte_cuda_problem prob{};
 };
@@ -177,7 +179,17 @@ void build_setup(BrdfSetup& s, const MaterialSpec& mat, const vrte_options* opti
     for (size_t i = 0; i < n_in; ++i)
         if (!(mu_in[i] > 0.0 && mu_in[i] <= 1.0))
             throw ValidationError("brdf: incident cosines must lie in (0,1]");
-    s.quad = build_double_gauss_quadrature(qn);
+    const double nif = s.spec.interface_n;
+    const bool fresnel = nif > 1.0;
+    int n_hi = qn;
+    if (fresnel) {
+        // the refraction cone mu > mu_c and the total-internal-reflection range each
+        // get a Gauss rule; the cone's nodes are the table's output directions
+        n_hi = (qn + 1) / 2;
+        s.quad = build_split_gauss_quadrature(qn, std::sqrt(1.0 - 1.0 / (nif * nif)), n_hi);
+    } else {
+        s.quad = build_double_gauss_quadrature(qn);
+    }
     s.L = s.spec.order_count();
     if (options && options->order_cap > 0) s.L = std::min(s.L, options->order_cap);
     const int N = s.quad.n, L = s.L, P = (int)s.spec.layers.size();
@@ -246,7 +258,10 @@ void build_setup(BrdfSetup& s, const MaterialSpec& mat, const vrte_options* opti
     }
     s.tau.resize(P);
     for (int p = 0; p < P; ++p) s.tau[p] = s.spec.layers[p].tau;
+    s.mu_in_user.assign(mu_in, mu_in + n_in);
     s.mu_in.assign(mu_in, mu_in + n_in);
+    if (fresnel)
+        for (auto& m : s.mu_in) m = refract_in(nif, m);  // the beam inside the medium
     // base rows at the beam (boundary.cpp:125-139): Lambertian uses node 0's row
     s.beam_rows.assign(n_in * (size_t)N * 16, 0.0);
     const bool lam = std::holds_alternative<LambertianBase>(s.spec.base);
@@ -289,6 +304,44 @@ void build_setup(BrdfSetup& s, const MaterialSpec& mat, const vrte_options* opti
                 s.post[ii * 16 + 4 * c + col] = acc;
             }
     }
+    s.quad_out = s.quad;
+    s.refl_top.clear();
+    s.pre.clear();
+    if (fresnel) {
+        // beam: inside Stokes = (mu0 / mu0') T_in(mu0) I0 (power through the surface);
+        // post' = that factor times B (mu0 B)^+; exits: T_out(mu) / n^2 (radiance theorem)
+        for (size_t ii = 0; ii < n_in; ++ii) {
+            const Mat4 T = fresnel_transmit_in(nif, mu_in[ii]);
+            const double f = mu_in[ii] / s.mu_in[ii];
+            double np[16];
+            for (int c = 0; c < 4; ++c)
+                for (int col = 0; col < 4; ++col) {
+                    double acc = 0.0;
+                    for (int k = 0; k < 4; ++k) acc += f * at(T, c, k) * s.post[ii * 16 + 4 * k + col];
+                    np[4 * c + col] = acc;
+                }
+            std::memcpy(&s.post[ii * 16], np, sizeof np);
+        }
+        s.refl_top.resize((size_t)N * 16);
+        s.pre.assign((size_t)N * 16, 0.0);
+        for (int i = 0; i < N; ++i) {
+            const Mat4 Rm = fresnel_reflect_inside(nif, s.quad.nodes[i]);
+            std::memcpy(&s.refl_top[(size_t)i * 16], Rm.data(), 128);
+            if (i >= N - n_hi) {
+                const Mat4 To = fresnel_transmit_out(nif, s.quad.nodes[i]);
+                for (int e = 0; e < 16; ++e) s.pre[(size_t)i * 16 + e] = To[e] / (nif * nif);
+            }
+        }
+        // output directions outside and their weights: mu' dmu' = n^2 mu dmu
+        s.quad_out.n = n_hi;
+        s.quad_out.nodes.clear();
+        s.quad_out.weights.clear();
+        for (int i = N - n_hi; i < N; ++i) {
+            const double mo = refract_out(nif, s.quad.nodes[i]);
+            s.quad_out.nodes.push_back(mo);
+            s.quad_out.weights.push_back(nif * nif * s.quad.weights[i] * s.quad.nodes[i] / mo);
+        }
+    }
     s.dphi.resize(n_dphi);
     for (int j = 0; j < n_dphi; ++j) s.dphi[j] = kTwoPi * j / n_dphi;
     s.trig.resize((size_t)L * n_dphi * 2);
@@ -323,6 +376,9 @@ void build_setup(BrdfSetup& s, const MaterialSpec& mat, const vrte_options* opti
     p.m_begin = 0;
     p.m_stride = 1;
     p.n_orders = 0;
+    p.refl_top = fresnel ? s.refl_top.data() : nullptr;
+    p.pre = fresnel ? s.pre.data() : nullptr;
+    p.out_lo = fresnel ? N - n_hi : 0;
     p.device = env_device();
     // VRTE_DEVICES="0,1,..." (or "all"): shard the orders of one solve over these
     // devices (vrte_options is caller-allocated ABI and keeps its layout)
@@ -426,6 +482,8 @@ vrte_status vrte_solve_radiance(const vrte_material* material, const vrte_option
             validate_material(check);
             if (options && options->quadrature_n < 1)
                 throw ValidationError("solver: quadrature size must be at least 1");
+            if (check.interface_n != 1.0)
+                throw ValidationError("radiance: the Fresnel interface extension is BRDF-only");
         }
         if (!(beam.mu0 > 0.0 && beam.mu0 <= 1.0))
             throw ValidationError("incident mu0 must lie in (0,1]");
@@ -568,6 +626,8 @@ vrte_status vrte_mc_trace(const vrte_material* material, const vrte_options* opt
                 g[5] = at(bm, 2, 2);
             }
         }
+        if (spec.interface_n != 1.0)
+            throw ValidationError("mc: the Fresnel interface extension is BRDF-only");
         vrte_cuda_mc mc{};
         mc.n_layers = P;
         mc.Lc = Lc;
@@ -711,18 +771,18 @@ vrte_status compute_brdf_on(const vrte_material* material, const vrte_options* o
         }
         const int N = s.quad.n, np = s.prob.n_dphi;
         BrdfTable& t = h->table;
-        t.mu_in = s.mu_in;
-        t.mu_out = s.quad.nodes;
+        t.mu_in = s.mu_in_user;
+        t.mu_out = s.quad_out.nodes;
         t.dphi = s.dphi;
         t.quadrature_n = N;
         t.order_count = s.L;
         t.material_hash = material_hash(s.spec);
-        t.entries.resize(n_mu_in * (size_t)N * np * 16);  // overwritten by the device result
+        t.entries.resize(n_mu_in * (size_t)s.quad_out.n * np * 16);  // overwritten by the device result
         vrte_cuda_result r{};
         const int32_t rc = vrte_cuda_brdf(&s.prob, t.entries.data(), &r);
         if (rc == 5) throw std::invalid_argument(r.message);
         if (rc != 0) throw NumericalError(r.message);
-        h->quadrature = s.quad;
+        h->quadrature = s.quad_out;
         const uint64_t S = s.rep.size(), L = s.L, nb = 4;
         h->timings.homogeneous = r.t_homogeneous;
         h->timings.particular = r.t_particular;
@@ -881,6 +941,15 @@ vrte_status vrte_brdf_timings(const vrte_brdf* brdf, vrte_timings* out) {
 void vrte_brdf_free(vrte_brdf* brdf) { delete brdf; }
 
 // ---------------------------------------------------------------- extensions
+vrte_status vrte_brdf_grid(const vrte_brdf* brdf, double* mu_in, double* mu_out, double* dphi) {
+    if (!brdf) return set_error(VRTE_E_ARGUMENT, "null brdf");
+    const auto& t = brdf->table;
+    if (mu_in) std::memcpy(mu_in, t.mu_in.data(), sizeof(double) * t.mu_in.size());
+    if (mu_out) std::memcpy(mu_out, t.mu_out.data(), sizeof(double) * t.mu_out.size());
+    if (dphi) std::memcpy(dphi, t.dphi.data(), sizeof(double) * t.dphi.size());
+    return VRTE_OK;
+}
+
 vrte_status vrte_brdf_device_stats_get(const vrte_brdf* brdf, vrte_brdf_device_stats* out) {
     if (!brdf || !out) return set_error(VRTE_E_ARGUMENT, "null argument");
     *out = brdf->stats;
@@ -941,18 +1010,18 @@ vrte_status vrte_brdf_from_stacks(const vrte_material* material, const vrte_opti
         build_setup(s, material->spec, options, mu_in, n_mu_in, n_dphi, basis);
         const int N = s.quad.n, np = s.prob.n_dphi;
         BrdfTable& t = h->table;
-        t.mu_in = s.mu_in;
-        t.mu_out = s.quad.nodes;
+        t.mu_in = s.mu_in_user;
+        t.mu_out = s.quad_out.nodes;
         t.dphi = s.dphi;
         t.quadrature_n = N;
         t.order_count = s.L;
         t.material_hash = material_hash(s.spec);
-        t.entries.resize(n_mu_in * (size_t)N * np * 16);
+        t.entries.resize(n_mu_in * (size_t)s.quad_out.n * np * 16);
         vrte_cuda_result r{};
         const int32_t rc = vrte_cuda_synthesize(&s.prob, up_all_orders, t.entries.data(), &r);
         if (rc == 5) throw std::invalid_argument(r.message);
         if (rc != 0) throw NumericalError(r.message);
-        h->quadrature = s.quad;
+        h->quadrature = s.quad_out;
         h->stats.clamped = r.clamped;
         h->stats.material_hash = t.material_hash;
         h->timings.total_wall = wall_now() - t0;

@@ -53,6 +53,10 @@ struct MaterialSpec {  // material.hpp:59-71
     std::vector<LayerSpec> layers;
     BaseReflector base = BlackBase{};
     BeamSource source;
+    // Extension (absent from the reference): a smooth
+    // dielectric interface on top of the stack, refractive index of the medium
+    // relative to the outside; 1 = no interface (the reference's model).
+    double interface_n = 1.0;
     int order_count() const { return layers.empty() ? 0 : layers.front().order_count(); }
 };
 
@@ -62,6 +66,22 @@ struct Quadrature {
 };
 
 Quadrature build_double_gauss_quadrature(int n);  // types.cpp:27-68
+// Gauss-Legendre on (0, mu_c) with n - n_hi nodes and on (mu_c, 1) with n_hi
+// nodes (the Fresnel interface's refraction cone and total-internal-reflection
+// range each get a full Gauss rule); ascending nodes.
+Quadrature build_split_gauss_quadrature(int n, double mu_c, int n_hi);
+// Fresnel Mueller matrices of a smooth interface between the medium (relative
+// index n > 1 against the outside) and the outside, row-major, Stokes
+// (I, Q = I_par - I_perp, U, V) in the meridian frame (= plane of incidence):
+//   reflection for light inside the medium hitting the interface at cosine mu
+//   (total internal reflection below the critical cosine), power
+//   transmittance outside -> inside at outside cosine mu, and inside -> outside
+//   at inside cosine mu; 0 / identity at n = 1.
+Mat4 fresnel_reflect_inside(double n, double mu);
+Mat4 fresnel_transmit_in(double n, double mu_out);
+Mat4 fresnel_transmit_out(double n, double mu_in);
+double refract_in(double n, double mu_out);   // outside cosine -> inside cosine
+double refract_out(double n, double mu_in);   // inside cosine -> outside (0 beyond the critical angle)
 void validate_material(MaterialSpec& spec);       // material.cpp:43-109
 std::vector<Mat4> load_coefficient_file(const std::string& path);
 MaterialSpec parse_material_json(const std::string& text, const std::string& base_dir);

@@ -99,6 +99,7 @@ class MaterialDesc:
     mu0: float = 0.6
     phi0: float = 0.0
     stokes: tuple = (1.0, 0.0, 0.0, 0.0)
+    interface_n: float = 1.0      # Fresnel top interface (extension; 1 = none, the reference's model)
 
     @property
     def order_count(self) -> int:
@@ -134,6 +135,8 @@ class MaterialDesc:
         else:
             doc["base"] = {"type": "black"}
         doc["source"] = {"mu0": self.mu0, "phi0": self.phi0, "stokes": list(self.stokes)}
+        if self.interface_n != 1.0:
+            doc["interface"] = {"type": "fresnel", "n": self.interface_n}
         path = os.path.join(directory, f"{name}.json")
         with open(path, "w") as f:
             json.dump(doc, f, indent=2)
@@ -174,6 +177,12 @@ def config(name: str, band: int = 0) -> Workload:
     if name == "C4":
         m = single_layer(generator_G(0.9, 256), 0.99, 10.0, "black")
         return Workload("C4", m, 128, 72, "G(0.9,256), omega=0.99, tau=10")
+    if name == "C3F":
+        # C3 with the Fresnel top interface of the paint's binder (n = 1.5; BASELINE
+        # config 3 "with a Fresnel interface" -- an extension, absent from the reference)
+        w = config("C3")
+        w.material.interface_n = 1.5
+        return Workload("C3F", w.material, 64, 19, "paint C3 under a Fresnel interface, n = 1.5")
     if name == "C4p":
         # C4': the survey's C4 shape with the polarization ratios halved.  G(0.9, 256)
         # itself is rejected by the reference (F E has negative real eigenvalues at
