@@ -65,6 +65,17 @@ typedef struct vrte_cuda_problem {
     const double* refl_top;
     const double* pre;
     int32_t out_lo;
+    /* Debug dumps (vrte_options dump_*_path, pipeline.cpp:333-357,
+       kernel.cpp:188-214): HOST buffers filled by the call when not NULL.
+       dump_kernel [L][N][N][2][16]: A^m(+mu_i, +mu_j), A^m(+mu_i, -mu_j) of
+       layer 0's medium; dump_nu [n_media][L][4N][2] and dump_residual
+       [n_media][L][4N]: the modes' separation constants and 8N residuals;
+       dump_boundary [L][2]: per order the cond_1 lower bound and the largest
+       relative residual of the boundary system. */
+    double* dump_kernel;
+    double* dump_nu;
+    double* dump_residual;
+    double* dump_boundary;
 } vrte_cuda_problem;
 
 typedef struct vrte_cuda_result {

@@ -355,6 +355,7 @@ __global__ void bnd_check_kernel(BndArgs a, const double* X, int G, int R, int s
     const double cond = b1 > 0.0 ? a1 * x1 / b1 : 0.0;
     atomic_max_double(&a.condm[mo], cond);
     atomic_max_double(&status->max_boundary_residual, rel);
+    atomic_max_double(&a.resm[mo], rel);
     const int m = a.p.order_of(mo);
     if (!finite || !(rmax == rmax)) {
         report_failure(status, kFailBoundary, 3, m, rmax, cond);
@@ -476,6 +477,7 @@ __global__ void bnd_probe_check_kernel(BndArgs a, const double* Xp, const double
             const double cond = b1 > 0.0 ? a1 * x1 / b1 : 0.0;
             atomic_max_double(&a.condm[mo], cond);
             atomic_max_double(&status->max_boundary_residual, rel);
+            atomic_max_double(&a.resm[mo], rel);
             if (!finite || !(rel <= 1e-10)) {
                 atomicExch(&status->bnd_fallback, 1);
                 atomicExch(&a.order_fail[mo], 1);

@@ -30,6 +30,7 @@ struct BndArgs {
     unsigned* colsum_ticket;  // [mo][G / 256 slabs]
     int* order_fail;      // [mo] a residual probe of this order failed (the fallback redoes only these)
     int* col_refine;      // [mo][R] right-hand sides taking the refinement step (full gate)
+    double* resm;         // [mo] largest relative residual of the order (dumps)
     int K;                // residual probes (0: the full gate); their b_k in lhs0 columns G + R + k
 };
 

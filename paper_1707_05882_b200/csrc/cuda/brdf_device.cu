@@ -131,6 +131,9 @@ struct vrte_cuda_plan {
     // boundary residual gate (boundary.cpp:233-257)
     DevBuf<double> lhs0, anorm, bnorm, condm, dX, Xp, Rp, colsum;
     DevBuf<int> colsum_ticket, order_fail, col_refine;
+    DevBuf<double> resm, kdump;
+    double *dump_kernel = nullptr, *dump_nu = nullptr, *dump_residual = nullptr, *dump_boundary = nullptr;
+    int medium0 = 0;
     DevBuf<double> up_save;
     int ldl = 0;  // row stride of [A | B] (+ the probes' b_k in lhs0): G + R + 16
     const double* lhs0_zeroed = nullptr;
@@ -283,6 +286,11 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     put(pl.post, p->post, (size_t)pl.n_in * 16);
     put(pl.trig, p->trig, (size_t)L * pl.n_dphi * 2);
     pl.out_lo = p->refl_top ? p->out_lo : 0;
+    pl.dump_kernel = p->dump_kernel;
+    pl.dump_nu = p->dump_nu;
+    pl.dump_residual = p->dump_residual;
+    pl.dump_boundary = p->dump_boundary;
+    pl.medium0 = p->medium[0];
     if (p->refl_top) {
         put(pl.refl_top, p->refl_top, (size_t)N * 16);
         put(pl.pre, p->pre, (size_t)N * 16);
@@ -339,6 +347,7 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pl.condm.alloc((size_t)NO);
     pl.colsum.alloc((size_t)NO * G);
     pl.order_fail.alloc((size_t)NO);
+    pl.resm.alloc((size_t)NO);
     pl.col_refine.alloc((size_t)NO * R);
     pl.colsum_ticket.alloc((size_t)NO * ((G + 255) / 256));
     pl.dX.alloc((size_t)NO * G * R);
@@ -404,6 +413,7 @@ BndArgs make_bnd(vrte_cuda_plan& pl) {
     ba.colsum_ticket = reinterpret_cast<unsigned*>(pl.colsum_ticket.p);
     ba.order_fail = pl.order_fail.p;
     ba.col_refine = pl.col_refine.p;
+    ba.resm = pl.resm.p;
     return ba;
 }
 
@@ -415,6 +425,7 @@ int boundary_full_gate(vrte_cuda_plan& pl, const BndArgs& ba, cudaStream_t st) {
     int nl = 2;
     VRTE_CUDA_CHECK(cudaMemsetAsync(&pl.status->max_boundary_residual, 0, sizeof(double), st));
     VRTE_CUDA_CHECK(cudaMemsetAsync(pl.condm.p, 0, sizeof(double) * NO, st));
+    VRTE_CUDA_CHECK(cudaMemsetAsync(pl.resm.p, 0, sizeof(double) * NO, st));
     launch_bnd_residual(ba, pl.rhs_x.p, G, R, false, st);
     launch_bnd_check(ba, pl.rhs_x.p, G, R, 0, pl.status, st);
     VRTE_CUDA_CHECK(cudaMemcpyAsync(pl.refine_host, &pl.status->bnd_refine, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -426,6 +437,7 @@ int boundary_full_gate(vrte_cuda_plan& pl, const BndArgs& ba, cudaStream_t st) {
         launch_bnd_residual(ba, pl.dX.p, G, R, true, st);
         VRTE_CUDA_CHECK(cudaMemsetAsync(&pl.status->max_boundary_residual, 0, sizeof(double), st));
         VRTE_CUDA_CHECK(cudaMemsetAsync(pl.condm.p, 0, sizeof(double) * NO, st));
+        VRTE_CUDA_CHECK(cudaMemsetAsync(pl.resm.p, 0, sizeof(double) * NO, st));
         launch_bnd_check(ba, pl.rhs_x.p, G, R, 1, pl.status, st);
         const int one = 1;
         VRTE_CUDA_CHECK(cudaMemcpyAsync(&pl.status->bnd_refined, &one, sizeof(int), cudaMemcpyHostToDevice, st));
@@ -478,6 +490,11 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     // ---------------- homogeneous
     launch_gsf(pd, pl.nodes.p, N, 1.0, pl.gsf_n.p, st);
     launch_gsf(pd, pl.mu_in.p, pl.n_in, -1.0, pl.gsf_b.p, st);
+    if (pl.dump_kernel) {  // debug dump of layer 0's kernel blocks (kernel.cpp:188-214)
+        pl.kdump.alloc((size_t)NO * N * N * 32);
+        launch_kernel_dump(pd, pl.gsf_n.p, pl.medium0, pl.kdump.p, st);
+        ++nl;
+    }
     // the beam source terms (particular.cpp:7-25) need only the GSF tables: side stream,
     // overlapped with the homogeneous stage
     cudaStream_t st2 = pl.st2;
@@ -707,6 +724,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[2], st));
     // ---------------- boundary
     const BndArgs ba = make_bnd(pl);
+    VRTE_CUDA_CHECK(cudaMemsetAsync(pl.resm.p, 0, sizeof(double) * NO, st));
     launch_bnd_assemble(ba, st);
     // The particular stage's refinement, like the eigenpairs': another step while
     // its balance residual exceeds kPartTarget (a tenth of the reference's 1e-6
@@ -918,6 +936,22 @@ int finish(vrte_cuda_plan& pl, vrte_cuda_result* r) {
         r->kernel_launches = pl.launches;
         r->eigen_slots = pl.Be;
         r->slots = pl.B;
+    }
+    // debug dumps (host buffers of the problem)
+    if (pl.dump_kernel && pl.kdump.p)
+        VRTE_CUDA_CHECK(cudaMemcpy(pl.dump_kernel, pl.kdump.p, sizeof(double) * pl.kdump.n, cudaMemcpyDeviceToHost));
+    if (pl.dump_nu)
+        VRTE_CUDA_CHECK(cudaMemcpy(pl.dump_nu, pl.nu.p, sizeof(double) * 2 * (size_t)pl.B * pl.d,
+                                   cudaMemcpyDeviceToHost));
+    if (pl.dump_residual) std::memcpy(pl.dump_residual, res.data(), sizeof(double) * res.size());
+    if (pl.dump_boundary) {
+        std::vector<double> cm((size_t)pl.NO), rm((size_t)pl.NO);
+        VRTE_CUDA_CHECK(cudaMemcpy(cm.data(), pl.condm.p, sizeof(double) * cm.size(), cudaMemcpyDeviceToHost));
+        VRTE_CUDA_CHECK(cudaMemcpy(rm.data(), pl.resm.p, sizeof(double) * rm.size(), cudaMemcpyDeviceToHost));
+        for (int mo = 0; mo < pl.NO; ++mo) {
+            pl.dump_boundary[2 * mo] = cm[mo];
+            pl.dump_boundary[2 * mo + 1] = rm[mo];
+        }
     }
     if (s.code == kFailNegativeIntensity && s.neg_key != 0) {
         const unsigned long long idx = ~s.neg_key;  // first offending entry, reference order

@@ -33,6 +33,7 @@ void launch_gsf(const ProblemDev& p, const double* mus, int count, double sign, 
                 cudaStream_t st);
 void launch_build_ef(const ProblemDev& p, const double* gsf, double* E, double* F,
                      cudaStream_t st);
+void launch_kernel_dump(const ProblemDev& p, const double* gsf, int s, double* out, cudaStream_t st);
 void launch_beam_source(const ProblemDev& p, const double* gsf_nodes, const double* gsf_beam,
                         double* sp, double* sm, cudaStream_t st);
 

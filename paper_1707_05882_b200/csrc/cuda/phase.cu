@@ -78,20 +78,12 @@ __global__ void gsf_kernel(int n_m, int L, int count, const double* __restrict__
     }
 }
 
-// E, F of every (medium s, order m) -- homogeneous.cpp:43-73 with A(+,+) and
-// A(+,-) (kernel.cpp:45-63) accumulated per node pair (i, j) in registers.
-// One thread per (s, m, i, j).
-__global__ void build_ef_kernel(const ProblemDev p, const double* __restrict__ gsf,
-                                double* __restrict__ E, double* __restrict__ F) {
-    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    const int N = p.N, L = p.Lc, d = 4 * N;
-    const long long total = (long long)p.n_media * p.n_orders * N * N;
-    if (idx >= total) return;
-    const int i = (int)(idx % N);
-    const int j = (int)((idx / N) % N);
-    const int om = (int)(idx / ((long long)N * N));  // s * n_orders + mo
-    const int s = om / p.n_orders, m = p.order_of(om % p.n_orders);
-    double app[4][4], apm[4][4];
+// A^m(+mu_i, +mu_j) and A^m(+mu_i, -mu_j) of medium s (kernel.cpp:45-63: the
+// "phase-matrix Fourier coefficients Z^m" pp / pm blocks), accumulated over l
+// in registers with the 2+2 sparsity of Pi B Pi.
+__device__ __forceinline__ void kernel_blocks(const ProblemDev& p, const double* __restrict__ gsf, int s, int m,
+                                              int i, int j, double app[4][4], double apm[4][4]) {
+    const int N = p.N, L = p.Lc;
 #pragma unroll
     for (int r = 0; r < 4; ++r)
 #pragma unroll
@@ -141,6 +133,23 @@ __global__ void build_ef_kernel(const ProblemDev p, const double* __restrict__ g
         apm[3][2] += sl * (x32 * Rj);
         apm[3][3] += sl * (x33 * Pj);
     }
+}
+
+// E, F of every (medium s, order m) -- homogeneous.cpp:43-73 with A(+,+) and
+// A(+,-) (kernel.cpp:45-63) accumulated per node pair (i, j) in registers.
+// One thread per (s, m, i, j).
+__global__ void build_ef_kernel(const ProblemDev p, const double* __restrict__ gsf,
+                                double* __restrict__ E, double* __restrict__ F) {
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const int N = p.N, d = 4 * N;
+    const long long total = (long long)p.n_media * p.n_orders * N * N;
+    if (idx >= total) return;
+    const int i = (int)(idx % N);
+    const int j = (int)((idx / N) % N);
+    const int om = (int)(idx / ((long long)N * N));  // s * n_orders + mo
+    const int s = om / p.n_orders, m = p.order_of(om % p.n_orders);
+    double app[4][4], apm[4][4];
+    kernel_blocks(p, gsf, s, m, i, j, app, apm);
     const double half_omega = 0.5 * p.omega[s];
     const double sc = half_omega * p.weights[j];
     const double inv_mu = 1.0 / p.nodes[j];
@@ -231,6 +240,29 @@ void launch_gsf(const ProblemDev& p, const double* mus, int count, double sign, 
                 cudaStream_t st) {
     const int total = p.L * count;
     gsf_kernel<<<(total + 127) / 128, 128, 0, st>>>(p.L, p.Lc, count, mus, sign, out, count);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+// Debug dump (kernel.cpp:188-214): the pp / pm blocks of medium s for the
+// plan's orders, out [mo][i][j][2][16] row-major.  Thread per (mo, i, j).
+__global__ void kernel_dump_kernel(const ProblemDev p, const double* __restrict__ gsf, int s, double* out) {
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const int N = p.N;
+    if (idx >= (long long)p.n_orders * N * N) return;
+    const int j = (int)(idx % N), i = (int)((idx / N) % N), mo = (int)(idx / ((long long)N * N));
+    double app[4][4], apm[4][4];
+    kernel_blocks(p, gsf, s, p.order_of(mo), i, j, app, apm);
+    double* o = out + idx * 32;
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c) {
+            o[4 * r + c] = app[r][c];
+            o[16 + 4 * r + c] = apm[r][c];
+        }
+}
+
+void launch_kernel_dump(const ProblemDev& p, const double* gsf, int s, double* out, cudaStream_t st) {
+    const long long total = (long long)p.n_orders * p.N * p.N;
+    kernel_dump_kernel<<<(unsigned)((total + 127) / 128), 128, 0, st>>>(p, gsf, s, out);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -8,6 +8,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <complex>
 #include <cstring>
 #include <stdexcept>
 #include <fstream>
@@ -149,6 +150,7 @@ struct BrdfSetup {
     Quadrature quad;
     int L = 0;
     std::vector<int> medium, rep, devices;
+    std::vector<int> sig_to_medium;  // reference signature k (first appearance) -> device medium index
     std::vector<double> omega, greek, tau, mu_in, beam_rows, post, trig, table_flat, dphi;
     std::vector<double> mu_in_user, refl_top, pre;  // Fresnel interface (mu_in = refracted cosines)
     Quadrature quad_out;  // output nodes / weights of the table (= quad without an interface)
@@ -239,6 +241,7 @@ void build_setup(BrdfSetup& s, const MaterialSpec& mat, const vrte_options* opti
         }
         s.rep = rep2;
         for (int p = 0; p < P; ++p) s.medium[p] = rank[s.medium[p]];
+        s.sig_to_medium = rank;
     }
     s.omega.resize(S);
     s.greek.assign((size_t)S * Lc * 6, 0.0);
@@ -756,6 +759,105 @@ vrte_status vrte_mc_tally_hits(const vrte_mc_tally* tally, int32_t hemisphere, i
 namespace {
 // vrte_compute_brdf with an explicit device (>= -1; -2 = from the environment,
 // order-sharded over VRTE_DEVICES when it lists several).
+// Debug dumps of vrte_options (pipeline.cpp:333-357, kernel.cpp:188-214): the
+// same files and formats as the reference.  Differences: one boundary line per
+// order (the boundary matrix is factored once per order for every incident),
+// its residual the largest over the order's right-hand sides / residual probes.
+struct Dumps {
+    std::string eigen, boundary, kernel;
+    std::vector<double> nu, residual, bnd, kern;
+    bool any() const { return !eigen.empty() || !boundary.empty() || !kernel.empty(); }
+};
+
+Dumps prepare_dumps(const vrte_options* options, BrdfSetup& s) {
+    Dumps d;
+    if (!options) return d;
+    if (options->dump_eigen_path) d.eigen = options->dump_eigen_path;
+    if (options->dump_boundary_path) d.boundary = options->dump_boundary_path;
+    if (options->dump_kernel_path) d.kernel = options->dump_kernel_path;
+    if (!d.any()) return d;
+    const size_t S = s.rep.size(), L = s.L, dd = 4 * (size_t)s.quad.n, N = s.quad.n;
+    if (!d.eigen.empty()) {
+        d.nu.resize(S * L * dd * 2);
+        d.residual.resize(S * L * dd);
+        s.prob.dump_nu = d.nu.data();
+        s.prob.dump_residual = d.residual.data();
+    }
+    if (!d.boundary.empty()) {
+        d.bnd.resize(L * 2);
+        s.prob.dump_boundary = d.bnd.data();
+    }
+    if (!d.kernel.empty()) {
+        d.kern.resize(L * N * N * 32);
+        s.prob.dump_kernel = d.kern.data();
+    }
+    s.prob.devices = nullptr;  // dumps come from the single-device path
+    s.prob.n_devices = 0;
+    return d;
+}
+
+void write_dumps(const Dumps& d, const BrdfSetup& s) {
+    const int L = s.L, N = s.quad.n, dd = 4 * N;
+    char buf[200];
+    if (!d.kernel.empty()) {
+        std::ofstream out(d.kernel);
+        if (!out) throw ValidationError("cannot open kernel dump file: " + d.kernel);
+        out << "m,i,j,sign_i,sign_j";
+        for (int e = 0; e < 16; ++e) out << ",a" << (e / 4) << (e % 4);
+        out << "\n";
+        const double ds[4] = {1.0, 1.0, -1.0, -1.0};  // parity_conjugate (kernel.cpp:20-27)
+        for (int m = 0; m < L; ++m)
+            for (int si = 0; si < 2; ++si)
+                for (int sj = 0; sj < 2; ++sj)
+                    for (int i = 0; i < N; ++i)
+                        for (int j = 0; j < N; ++j) {
+                            // pp, pm from the device; mp = D pm D, mm = D pp D
+                            const double* blk = &d.kern[(((size_t)m * N + i) * N + j) * 32 + (si == sj ? 0 : 16)];
+                            out << m << ',' << i << ',' << j << ',' << (si == 0 ? 1 : -1) << ',' << (sj == 0 ? 1 : -1);
+                            for (int r = 0; r < 4; ++r)
+                                for (int c = 0; c < 4; ++c) {
+                                    const double v = si == 0 ? blk[4 * r + c] : ds[r] * ds[c] * blk[4 * r + c];
+                                    std::snprintf(buf, sizeof buf, "%.17g", v);
+                                    out << ',' << buf;
+                                }
+                            out << "\n";
+                        }
+    }
+    if (!d.eigen.empty()) {
+        std::ofstream out(d.eigen);
+        out << "m,lambda_re,lambda_im,nu_re,nu_im,residual\n";
+        for (size_t sig = 0; sig < s.sig_to_medium.size(); ++sig) {
+            const int med = s.sig_to_medium[sig];
+            for (int m = 0; m < L; ++m) {
+                const size_t base = ((size_t)med * L + m) * dd;
+                std::vector<int> idx(dd);
+                for (int j = 0; j < dd; ++j) idx[j] = j;
+                // the reference's mode order (homogeneous.cpp:272-276)
+                std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
+                    const double ar = d.nu[2 * (base + a)], br = d.nu[2 * (base + b)];
+                    if (ar != br) return ar > br;
+                    return d.nu[2 * (base + a) + 1] < d.nu[2 * (base + b) + 1];
+                });
+                for (int j : idx) {
+                    const std::complex<double> nu(d.nu[2 * (base + j)], d.nu[2 * (base + j) + 1]);
+                    const std::complex<double> lambda = 1.0 / (nu * nu);
+                    std::snprintf(buf, sizeof buf, "%d,%.17g,%.17g,%.17g,%.17g,%.3g\n", m, lambda.real(), lambda.imag(),
+                                  nu.real(), nu.imag(), d.residual[base + j]);
+                    out << buf;
+                }
+            }
+        }
+    }
+    if (!d.boundary.empty()) {
+        std::ofstream out(d.boundary);
+        out << "m,condition_estimate,residual\n";
+        for (int m = 0; m < L; ++m) {
+            std::snprintf(buf, sizeof buf, "%d,%.6g,%.3g\n", m, d.bnd[2 * m], d.bnd[2 * m + 1]);
+            out << buf;
+        }
+    }
+}
+
 vrte_status compute_brdf_on(const vrte_material* material, const vrte_options* options, const double* mu_in,
                             size_t n_mu_in, int32_t n_dphi, const double* basis, int device, vrte_brdf** out) {
     if (!material || !out || !mu_in || n_mu_in == 0) return set_error(VRTE_E_ARGUMENT, "null argument");
@@ -769,6 +871,7 @@ vrte_status compute_brdf_on(const vrte_material* material, const vrte_options* o
             s.prob.devices = nullptr;
             s.prob.n_devices = 0;
         }
+        const Dumps dumps = prepare_dumps(options, s);
         const int N = s.quad.n, np = s.prob.n_dphi;
         BrdfTable& t = h->table;
         t.mu_in = s.mu_in_user;
@@ -782,6 +885,7 @@ vrte_status compute_brdf_on(const vrte_material* material, const vrte_options* o
         const int32_t rc = vrte_cuda_brdf(&s.prob, t.entries.data(), &r);
         if (rc == 5) throw std::invalid_argument(r.message);
         if (rc != 0) throw NumericalError(r.message);
+        if (dumps.any()) write_dumps(dumps, s);
         h->quadrature = s.quad_out;
         const uint64_t S = s.rep.size(), L = s.L, nb = 4;
         h->timings.homogeneous = r.t_homogeneous;
