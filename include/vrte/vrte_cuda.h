@@ -224,6 +224,12 @@ VRTE_API int32_t vrte_cuda_hessenberg(const double* A, int32_t d, int32_t batch,
  * wr/wi [batch][d].  Returns 0, or 3 if the QR did not converge. */
 VRTE_API int32_t vrte_cuda_schur(const double* A, int32_t d, int32_t batch, double* T, double* Z, double* wr,
                                  double* wi, int32_t device);
+/* Same, with the QR kernel's per-matrix profile (debug): trace [batch][8] =
+ * cycles, reflectors, sweeps, AED calls, AED cycles, chase cycles,
+ * update-wait cycles, AED deflations (either pointer may be NULL; qr_ms: the
+ * QR kernel's device time). */
+VRTE_API int32_t vrte_cuda_schur_trace(const double* A, int32_t d, int32_t batch, double* T, double* Z, double* wr,
+                                       double* wi, int32_t device, double* trace, double* qr_ms);
 
 #ifdef __cplusplus
 }

@@ -155,7 +155,7 @@ EXPORTED = [
     "vrte_cuda_synthesize", "vrte_cuda_device_count", "vrte_cuda_current_device", "vrte_cuda_lu_solve", "vrte_cuda_hessenberg", "vrte_cuda_schur",
     "vrte_cuda_radiance_field", "vrte_cuda_mc_trace", "vrte_cuda_host_alloc", "vrte_cuda_host_free",
     "vrte_cuda_debug_force_boundary_fallback", "vrte_cuda_plan_up_device", "vrte_cuda_plan_synthesize_device",
-    "vrte_cuda_plan_acquire", "vrte_cuda_plan_release", "vrte_brdf_plan_acquire",
+    "vrte_cuda_plan_acquire", "vrte_cuda_plan_release", "vrte_brdf_plan_acquire", "vrte_cuda_schur_trace",
 ]
 
 
@@ -210,6 +210,7 @@ def lib():
     L.vrte_cuda_plan_release.restype = None
     L.vrte_cuda_plan_synthesize_device.argtypes = [vp, C.c_void_p, dp, C.POINTER(CudaResult)]
     L.vrte_cuda_schur.argtypes = [dp, C.c_int32, C.c_int32, dp, dp, dp, dp, C.c_int32]
+    L.vrte_cuda_schur_trace.argtypes = [dp, C.c_int32, C.c_int32, dp, dp, dp, dp, C.c_int32, dp, dp]
     L.vrte_solve_radiance.argtypes = [vp, C.POINTER(Options), dp, C.c_size_t, C.POINTER(vp)]
     L.vrte_field_size.argtypes = [vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]
     L.vrte_field_row.argtypes = [vp, C.c_size_t, C.c_size_t, C.c_size_t, dp]
@@ -286,6 +287,22 @@ def schur(A, device: int = 0):
     if code != 0:
         raise VrteError(code, "vrte_cuda_schur: QR did not converge")
     return T.transpose(0, 2, 1).copy(), Z.transpose(0, 2, 1).copy(), wr + 1j * wi
+
+
+def schur_trace(A, device: int = 0):
+    """Debug: schur() plus the QR kernel's per-matrix profile [batch, 8] (cycles,
+    reflectors, sweeps, AED calls, AED cycles, chase cycles, update-wait cycles,
+    AED deflations) and its device time in ms."""
+    A = np.asarray(A, dtype=np.float64)
+    batch, d, _ = A.shape
+    Ac = np.ascontiguousarray(A.transpose(0, 2, 1))
+    T, Z = np.zeros_like(Ac), np.zeros_like(Ac)
+    wr, wi = np.zeros((batch, d)), np.zeros((batch, d))
+    tr, ms = np.zeros((batch, 8)), np.zeros(1)
+    code = lib().vrte_cuda_schur_trace(_dp(Ac), d, batch, _dp(T), _dp(Z), _dp(wr), _dp(wi), device, _dp(tr), _dp(ms))
+    if code != 0:
+        raise VrteError(code, "vrte_cuda_schur: QR did not converge")
+    return tr, float(ms[0])
 
 
 def version() -> str:

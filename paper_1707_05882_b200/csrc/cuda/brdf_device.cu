@@ -1629,6 +1629,11 @@ int32_t vrte_cuda_hessenberg(const double* A, int32_t d, int32_t batch, double* 
 
 int32_t vrte_cuda_schur(const double* A, int32_t d, int32_t batch, double* T, double* Z, double* wr,
                         double* wi, int32_t device) {
+    return vrte_cuda_schur_trace(A, d, batch, T, Z, wr, wi, device, nullptr, nullptr);
+}
+
+int32_t vrte_cuda_schur_trace(const double* A, int32_t d, int32_t batch, double* T, double* Z, double* wr,
+                              double* wi, int32_t device, double* trace, double* qr_ms) {
     if (!A || !T || !Z || !wr || !wi || d < 1 || batch < 1) return 5;
     try {
         if (device >= 0) VRTE_CUDA_CHECK(cudaSetDevice(device));
@@ -1649,8 +1654,12 @@ int32_t vrte_cuda_schur(const double* A, int32_t d, int32_t batch, double* T, do
         VRTE_CUDA_CHECK(cudaEventCreate(&e0));
         VRTE_CUDA_CHECK(cudaEventCreate(&e1));
         VRTE_CUDA_CHECK(cudaEventRecord(e0, st));
-        launch_hqr(dA.p, dZ.p, dwr.p, dwi.p, d, batch, dst.p, st);
+        DevBuf<double> dtr;
+        if (trace) dtr.alloc((size_t)batch * 8);
+        launch_hqr(dA.p, dZ.p, dwr.p, dwi.p, d, batch, dst.p, st, trace ? dtr.p : nullptr);
         VRTE_CUDA_CHECK(cudaEventRecord(e1, st));
+        if (trace)
+            VRTE_CUDA_CHECK(cudaMemcpyAsync(trace, dtr.p, sizeof(double) * dtr.n, cudaMemcpyDeviceToHost, st));
         VRTE_CUDA_CHECK(cudaMemcpyAsync(T, dA.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
         VRTE_CUDA_CHECK(cudaMemcpyAsync(Z, dZ.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
         VRTE_CUDA_CHECK(cudaMemcpyAsync(wr, dwr.p, sizeof(double) * batch * d, cudaMemcpyDeviceToHost, st));
@@ -1659,6 +1668,11 @@ int32_t vrte_cuda_schur(const double* A, int32_t d, int32_t batch, double* T, do
         VRTE_CUDA_CHECK(cudaMemcpyAsync(&s, dst.p, sizeof s, cudaMemcpyDeviceToHost, st));
         VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
         cudaStreamDestroy(st);
+        if (qr_ms) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            *qr_ms = ms;
+        }
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         return s.code != 0 ? 3 : 0;

@@ -732,7 +732,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) hqr_multi_ke
                                                         int aed_nw, int nb4_min, int nb2_min, int nibble,
                                                         double* trace) {
     __shared__ double Wn[MW * LDW];  // window, column-major Wn[c*LDW + r]
-    __shared__ double Us2[2 * MW * LDW];  // chunk factors (double buffered), column-major [c*LDW + r]
+    __shared__ double Us2[3 * MW * LDW];  // chunk factors (triple buffered), column-major [c*LDW + r]
     double* const Us = Us2;               // buffer 0: AED factor / first chunk
     __shared__ double Sm[TQ * TQ];  // trailing block for the shifts
     __shared__ double s_sr[TQ], s_si[TQ];
@@ -745,7 +745,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) hqr_multi_ke
     // cluster job queue (used in rank 0's shared memory): rank 0 posts chunk
     // factors, rank 1 applies them to the rest of H and to Z
     __shared__ unsigned s_posted, s_done;
-    __shared__ int s_job[2][8];  // buf, wlo, whi, nw, c_lo, c_hi, above_z, stop
+    __shared__ int s_job[2][9];  // buf, wlo, whi, nw, c_lo, c_hi, above_z, stop, c_split
+    __shared__ unsigned s_partial;
     const int b = blockIdx.x >> 1, crank = blockIdx.x & 1;
     const int t = threadIdx.x, nt = blockDim.x, lane = t & 31, warp = t >> 5;
     double* H = Hall + (size_t)b * d * d;
@@ -864,9 +865,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) hqr_multi_ke
     if (t == 0) {
         s_posted = 0u;
         s_done = 0u;
+        s_partial = 0u;
     }
     cluster_sync_all();
     const unsigned a_posted = dsmem_addr(&s_posted, 0), a_done = dsmem_addr(&s_done, 0);
+    const unsigned a_partial = dsmem_addr(&s_partial, 0);
     if (crank == 1) {
         // ---- updater CTA: apply posted chunk factors to H and Z, in order
         for (unsigned next = 0;; ++next) {
@@ -875,12 +878,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) hqr_multi_ke
             __syncthreads();
             (void)ld_acquire_cluster(a_posted);
             const unsigned jb = dsmem_addr(&s_job[next & 1][0], 0);
-            int jd[8];
+            int jd[9];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) jd[q] = ld_cluster_s32(jb + 4u * q);
+            for (int q = 0; q < 9; ++q) jd[q] = ld_cluster_s32(jb + 4u * q);
             if (jd[7]) break;
             const unsigned ua = dsmem_addr(Us2 + (size_t)jd[0] * (MW * LDW), 0);
-            apply_part(nullptr, jd[1], jd[2], jd[3], jd[4], jd[5], jd[6] != 0, warp, nt / 32, ua);
+            // phase A: the columns the chaser's next-but-one chunk updates itself
+            // ([c_lo, c_split)), published early; phase B: the rest of H and Z
+            const int cs = min(max(jd[8], jd[4]), jd[5]);
+            if (cs > jd[4]) apply_part(nullptr, jd[1], jd[2], jd[3], jd[4], cs, false, warp, nt / 32, ua);
+            fence_cluster();
+            __syncthreads();
+            if (t == 0) st_release_cluster(a_partial, next + 1);
+            apply_part(nullptr, jd[1], jd[2], jd[3], cs, jd[5], jd[6] != 0, warp, nt / 32, ua);
             fence_cluster();
             __syncthreads();
             if (t == 0) st_release_cluster(a_done, next + 1);
@@ -889,9 +899,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) hqr_multi_ke
         return;
     }
     unsigned jid = 0;  // jobs posted so far (rank 0)
-    auto post_job = [&](int buf, int wlo, int whi, int nw, int c_lo, int c_hi, int above_z, int stop) {
+    auto post_job = [&](int buf, int wlo, int whi, int nw, int c_lo, int c_hi, int above_z, int stop,
+                        int c_split = 0) {
         // caller: one thread
         int* j = s_job[jid & 1];
+        j[8] = c_split;
         j[0] = buf;
         j[1] = wlo;
         j[2] = whi;
@@ -905,6 +917,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) hqr_multi_ke
     };
     auto wait_done = [&](unsigned upto) {  // caller: one thread
         while (ld_acquire_cluster(a_done) < upto) __nanosleep(32);
+    };
+    auto wait_partial = [&](unsigned upto) {  // caller: one thread
+        while (ld_acquire_cluster(a_partial) < upto) __nanosleep(32);
     };
     while (I >= 0) {
         int L = 0;
@@ -1198,7 +1213,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) hqr_multi_ke
                     int wlo, whi;
                     geom(c, wlo, whi);
                     const int nw = whi - wlo + 1;
-                    double* Uc = Us2 + (c & 1) * (MW * LDW);
+                    // U_c in buffer c % 3: its last user, job c - 3, is done (chunk c - 1
+                    // waited for job c - 2's phase A, and jobs run in order)
+                    double* Uc = Us2 + (c % 3) * (MW * LDW);
                     {
                         // all loads in flight before the first shared store (a generic H
                         // may alias shared memory, so interleaving would serialise them)
@@ -1305,13 +1322,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) hqr_multi_ke
                     // with U_{c-1} (they cover the same columns), then apply U_c there
                     int wlo_n = wlo, whi_n = whi;
                     if (c + 1 < nchunk) geom(c + 1, wlo_n, whi_n);
-                    // the updater CTA must be done with U_{c-1} (it covers these columns)
-                    if (c >= 1 && t == 0) wait_done(jid);
+                    // the updater CTA must be done with U_{c-1} on these columns: its job
+                    // publishes them first (phase A), and jobs run in order, so every
+                    // earlier job is done too
+                    if (c >= 1 && t == 0) wait_partial(jid);
                     named_bar(3, 128);
                     if (whi_n > whi) apply_part(Uc, wlo, whi, nw, whi + 1, whi_n + 1, false, warp, 4);
                     fence_cluster();
                     named_bar(3, 128);
-                    if (t == 0) post_job(c & 1, wlo, whi, nw, max(whi, whi_n) + 1, d, 1, 0);
+                    if (t == 0) {
+                        // the columns chunk c + 2 will update itself: [c_lo, whi_{c+2}]
+                        int c_split = 0;
+                        if (c + 2 < nchunk) {
+                            int w2lo, w2hi;
+                            geom(c + 2, w2lo, w2hi);
+                            c_split = w2hi + 1;
+                        }
+                        post_job(c % 3, wlo, whi, nw, max(whi, whi_n) + 1, d, 1, 0, c_split);
+                    }
                     ++jid;
                     if (t == 0) tick(3);
                 }
@@ -1376,7 +1404,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) hqr_multi_ke
         atomicAdd(&status->qr_sweeps, nsweep);
         atomicAdd(&status->qr_steps, nstep);
         for (int q = 0; q < 8; ++q) atomicAdd(&status->qr_cycles[q], cyc[q]);
-        if (trace) {  // debug (VRTE_QR_TRACE): per-matrix cost profile
+        if (trace) {  // debug (vrte_cuda_schur trace): per-matrix cost profile
             double* tr = trace + (size_t)b * 8;
             tr[0] = (double)(cyc[0] + cyc[1] + cyc[2] + cyc[3]);
             tr[1] = (double)nstep;
@@ -2091,9 +2119,9 @@ void launch_hessenberg(double* A, double* Z, int d, int batch, cudaStream_t st) 
 }
 
 void launch_hqr(double* H, double* Z, double* wr, double* wi, int d, int batch,
-                DeviceStatus* status, cudaStream_t st) {
+                DeviceStatus* status, cudaStream_t st, double* trace) {
     // 2-CTA clusters: rank 0 chases / deflates, rank 1 applies the chunk factors
-    hqr_multi_kernel<<<2 * batch, 256, 0, st>>>(H, Z, wr, wi, d, status, AED_NW, 48, 24, 40, nullptr);
+    hqr_multi_kernel<<<2 * batch, 256, 0, st>>>(H, Z, wr, wi, d, status, AED_NW, 48, 24, 40, trace);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 

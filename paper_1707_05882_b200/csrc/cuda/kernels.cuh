@@ -47,8 +47,11 @@ size_t hessenberg_work_doubles(int d);
 void launch_hessenberg_blocked(double* A, double* Z, double* work, int d, int batch,
                                cudaStream_t st);
 int hessenberg_launch_count(int d);
+// trace (debug, may be null): [batch][8] per matrix: cycles of rank 0,
+// reflectors, sweeps, AED calls, AED cycles, chase cycles, update-wait cycles,
+// AED deflations
 void launch_hqr(double* H, double* Z, double* wr, double* wi, int d, int batch,
-                DeviceStatus* status, cudaStream_t st);
+                DeviceStatus* status, cudaStream_t st, double* trace = nullptr);
 void launch_trevc(const double* T, const double* wr, const double* wi, double* Y, int d,
                   int batch, cudaStream_t st);
 // Normalize packed eigenvector columns by their max complex modulus; returns
