@@ -13,9 +13,10 @@
 //                          the rest of H and to Z on the FP64 tensor cores;
 //                          dlahqr rules (Ahues-Kressner deflation, exceptional
 //                          shifts, dlanv2 standardization) for small blocks
-//   trevc_grp_kernel     : eigenvectors of the quasi-triangular Schur factor by
-//                          register-resident back substitution (dtrevc), 4 per
-//                          warp, back-transformed by a GEMM
+//   trevc_blk_kernel     : eigenvectors of the quasi-triangular Schur factor by
+//                          blocked back substitution (dtrevc3 organisation: shifted
+//                          32-row diagonal blocks per eigenvector, shift-free
+//                          block updates for all at once), back-transformed by a GEMM
 #include <climits>
 #include <cstdlib>
 #include <string>
@@ -1486,385 +1487,206 @@ __device__ void solve2r(double c00, double c01, double c10, double c11, double b
 
 
 
-// Register-resident dtrevc: warp per eigenvalue (complex pairs by their first
-// index), lane l owns rows l + 32 i of the solution; the solved entry is
-// broadcast by shuffle and the T columns of the NEXT step are loaded while the
-// current one is applied (the serial chain is shuffle + divide + FMA, not an
-// L2 round trip).  Same arithmetic and dlaln2-style smin perturbation as
-// LAPACK dtrevc.  pf[c] = 1 when T(c, c-1) != 0 (second row of a 2x2 block).
-template <int RPL>
-__global__ void __launch_bounds__(256) trevc_reg_kernel(const double* Tall, const double* wrall,
-                                                        const double* wiall, double* Yall, int d) {
-    extern __shared__ unsigned char pf[];
-    const int b = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+
+
+
+
+// ------------------------------------------------------------------ blocked trevc
+// Right eigenvectors of the quasi-triangular Schur factor by BLOCKED back
+// substitution (the dtrevc3 organisation): rows in blocks of TBK from the
+// bottom; per block, every eigenvector solves its shifted diagonal block (a
+// group of 4 threads per eigen-block leader: one solves each row, the four
+// share the row updates; the block's rows and T's diagonal block in shared
+// memory), then ONE shift-free update of every row above by all the
+// slice's eigenvectors, Y[0:j0, :] -= T[0:j0, j0:j1] Y[j0:j1, :] (the
+// off-diagonal part of T - lambda I carries no shift).  CTA per (matrix,
+// slice of W leader columns); the slice of Y lives in shared memory.  Same
+// arithmetic choices as LAPACK dtrevc (dlaln2-style smin, solve2 / solve2r
+// on 2x2 blocks, the complex pair's fixed entries).
+constexpr int TBK = 32;
+template <int W, int GS>
+__global__ void __launch_bounds__(256) trevc_blk_kernel(const double* Tall, const double* wrall, const double* wiall,
+                                                        double* Yall, int d, int stage_t) {
+    extern __shared__ double shm[];
+    constexpr int LDY = W + 4;       // slice columns (a leader's pair partner may be column W), padded to 4
+    constexpr int LDD = TBK + 2;     // diagonal block [TBK + 1]^2
+    double* Ys = shm;                          // [d][LDY]
+    double* Td = Ys + (size_t)d * LDY;         // [TBK + 1][LDD]
+    double* Tp = Td + (size_t)(TBK + 1) * LDD;  // [d][LDD] column panel T[0:j0, j0:j1] (stage_t)
+    __shared__ int s_top;
+    const int b = blockIdx.x, c0 = blockIdx.y * W, t = threadIdx.x, nt = blockDim.x;
     const double* T = Tall + (size_t)b * d * d;
     const double* wr = wrall + (size_t)b * d;
     const double* wi = wiall + (size_t)b * d;
     double* Y = Yall + (size_t)b * d * d;
-    for (int c = threadIdx.x; c < d; c += blockDim.x) pf[c] = (c > 0 && T[c + (size_t)(c - 1) * d] != 0.0);
+    auto Tg = [&](int r, int c) { return T[r + (size_t)c * d]; };
+    for (int e = t; e < d * LDY; e += nt) Ys[e] = 0.0;
+    if (t == 0) s_top = -1;
     __syncthreads();
-    const double smlnum = kSafeMin * ((double)d / kUlp);
-    auto Tat = [&](int r, int c) { return T[r + (size_t)c * d]; };
-    // column c of T restricted to rows < lim, this lane's rows
-    auto load_col = [&](double* dst, int c, int lim) {
-#pragma unroll
-        for (int i = 0; i < RPL; ++i) {
-            const int r = lane + 32 * i;
-            dst[i] = (c >= 0 && r < lim) ? T[r + (size_t)c * d] : 0.0;
-        }
-    };
-    auto pick = [&](const double* v, int r) {  // value of row r from its owner lane
-        double x = 0.0;
-#pragma unroll
-        for (int i = 0; i < RPL; ++i)
-            if (i == (r >> 5)) x = v[i];
-        return __shfl_sync(0xffffffffu, x, r & 31);
-    };
-    auto put = [&](double* v, int r, double x) {
-#pragma unroll
-        for (int i = 0; i < RPL; ++i)
-            if (i == (r >> 5) && lane == (r & 31)) v[i] = x;
-    };
-    for (int ki = w; ki < d; ki += nw) {
-        const double wik = wi[ki];
-        if (wik < 0.0) continue;
-        double re[RPL], im[RPL], t1[RPL], t2[RPL], n1[RPL], n2[RPL];
-        const bool cxv = wik != 0.0;
-        int top;  // first row of the eigenvalue's own block
-        cplx lam;
-        double smin;
-        if (!cxv) {
-            top = ki;
-            lam = cmk(wr[ki], 0.0);
-            smin = fmax(kUlp * fabs(lam.re), smlnum);
-            load_col(re, ki, ki);
-#pragma unroll
-            for (int i = 0; i < RPL; ++i) {
-                re[i] = -re[i];
-                im[i] = 0.0;
-                if (lane + 32 * i == ki) re[i] = 1.0;
-            }
+    // leader state: a group of 4 threads per local column lc (W <= nt / 4); lane q = 0
+    // of the group solves each row, the 4 lanes share the row updates
+    const int lc = t / GS, q = t % GS;
+    const unsigned gmask = (GS >= 32) ? 0xffffffffu : (((1u << GS) - 1u) << ((t & 31) & ~(GS - 1)));
+    const int k = c0 + lc;
+    const bool lead = lc < W && k < d && wi[k] >= 0.0;
+    const bool cx = lead && wi[k] > 0.0;
+    const double lr = lead ? wr[k] : 0.0, li = lead ? wi[k] : 0.0;
+    const double sm = lead ? fmax(kUlp * (fabs(lr) + fabs(li)), kSafeMin * ((double)d / kUlp)) : 1.0;
+    const int top = lead ? (cx ? k + 1 : k) : -1;
+    if (lead && q == 0) {
+        if (!cx) {
+            Ys[(size_t)k * LDY + lc] = 1.0;
         } else {
-            const int pp = ki, q = ki + 1;
-            top = pp;
-            lam = cmk(wr[pp], wik);
-            smin = fmax(kUlp * (fabs(wr[pp]) + fabs(wik)), smlnum);
             double xpr, xqi;
-            if (fabs(Tat(pp, q)) >= fabs(Tat(q, pp))) {
+            const double tu = Tg(k, k + 1), tl = Tg(k + 1, k);
+            if (fabs(tu) >= fabs(tl)) {
                 xpr = 1.0;
-                xqi = wik / Tat(pp, q);
+                xqi = li / tu;
             } else {
-                xpr = -wik / Tat(q, pp);
+                xpr = -li / tl;
                 xqi = 1.0;
             }
-            load_col(re, pp, pp);
-            load_col(im, q, pp);
-#pragma unroll
-            for (int i = 0; i < RPL; ++i) {
-                const int r = lane + 32 * i;
-                re[i] *= -xpr;
-                im[i] *= -xqi;
-                if (r == pp) {
-                    re[i] = xpr;
-                    im[i] = 0.0;
-                }
-                if (r == q) {
-                    re[i] = 0.0;
-                    im[i] = xqi;
-                }
-            }
+            Ys[(size_t)k * LDY + lc] = xpr;
+            Ys[(size_t)(k + 1) * LDY + lc + 1] = xqi;
         }
-        int j = top - 1;
-        // prefetch the first step's columns (and, for real eigenvalues, the
-        // reciprocal pivot of a 1x1 step, off the serial chain)
-        bool pair = j > 0 && pf[j];
-        load_col(t1, j, pair ? j - 1 : j);
-        load_col(t2, pair ? j - 1 : -1, j - 1);
-        auto rpiv = [&](int c) {
-            double den = (c >= 0) ? Tat(c, c) - lam.re : 1.0;
-            if (fabs(den) < smin) den = smin;
-            return 1.0 / den;
-        };
-        double rd = (!cxv && !pair && j >= 0) ? rpiv(j) : 0.0;
-        while (j >= 0) {
-            const int jn = j - (pair ? 2 : 1);
-            const bool pairn = jn > 0 && pf[jn];
-            load_col(n1, jn, pairn ? jn - 1 : jn);
-            load_col(n2, pairn ? jn - 1 : -1, jn - 1);
-            const double rdn = (!cxv && !pairn && jn >= 0) ? rpiv(jn) : 0.0;
-            if (!cxv) {
-                if (pair) {
-                    double x0, x1;
-                    solve2r(Tat(j - 1, j - 1) - lam.re, Tat(j - 1, j), Tat(j, j - 1), Tat(j, j) - lam.re,
-                            pick(re, j - 1), pick(re, j), smin, x0, x1);
-#pragma unroll
-                    for (int i = 0; i < RPL; ++i) re[i] = fma(-x0, t2[i], fma(-x1, t1[i], re[i]));
-                    put(re, j - 1, x0);
-                    put(re, j, x1);
-                } else {
-                    const double x = pick(re, j) * rd;
-#pragma unroll
-                    for (int i = 0; i < RPL; ++i) re[i] = fma(-x, t1[i], re[i]);
-                    put(re, j, x);
-                }
-            } else if (pair) {
-                const double ajj = Tat(j - 1, j - 1), aj1 = Tat(j - 1, j), a1j = Tat(j, j - 1), a11 = Tat(j, j);
-                const cplx b0 = cmk(pick(re, j - 1), pick(im, j - 1));
-                const cplx b1 = cmk(pick(re, j), pick(im, j));
-                cplx x0, x1;
-                solve2(cmk(ajj, 0) - lam, cmk(aj1, 0), cmk(a1j, 0), cmk(a11, 0) - lam, b0, b1, smin, x0, x1);
-                // t2 = column j-1, t1 = column j (rows < j-1)
-#pragma unroll
-                for (int i = 0; i < RPL; ++i) {
-                    re[i] = fma(-x0.re, t2[i], fma(-x1.re, t1[i], re[i]));
-                    im[i] = fma(-x0.im, t2[i], fma(-x1.im, t1[i], im[i]));
-                }
-                put(re, j - 1, x0.re);
-                put(re, j, x1.re);
-                put(im, j - 1, x0.im);
-                put(im, j, x1.im);
-            } else {
-                cplx den = cmk(Tat(j, j), 0.0) - lam;
-                if (cabs_(den) < smin) den = cmk(smin, 0.0);
-                const cplx x = cdiv(cmk(pick(re, j), pick(im, j)), den);
-#pragma unroll
-                for (int i = 0; i < RPL; ++i) {
-                    re[i] = fma(-x.re, t1[i], re[i]);
-                    im[i] = fma(-x.im, t1[i], im[i]);
-                }
-                put(re, j, x.re);
-                put(im, j, x.im);
-            }
-#pragma unroll
-            for (int i = 0; i < RPL; ++i) {
-                t1[i] = n1[i];
-                t2[i] = n2[i];
-            }
-            j = jn;
-            pair = pairn;
-            rd = rdn;
-        }
-        const int last = cxv ? ki + 1 : ki;
-        double* yr = Y + (size_t)ki * d;
-#pragma unroll
-        for (int i = 0; i < RPL; ++i) {
-            const int r = lane + 32 * i;
-            if (r < d) yr[r] = (r <= last) ? re[i] : 0.0;
-        }
-        if (cxv) {
-            double* yi = Y + (size_t)(ki + 1) * d;
-#pragma unroll
-            for (int i = 0; i < RPL; ++i) {
-                const int r = lane + 32 * i;
-                if (r < d) yi[r] = (r <= last) ? im[i] : 0.0;
-            }
-        }
-    }
-}
-
-
-// Grouped register-resident dtrevc: a warp back-substitutes G eigenvectors at
-// once (G consecutive eigen-blocks, complex pairs by their first index), so
-// every column of T loaded for a step feeds G independent substitution chains
-// and the L2 latency of the (one step ahead) prefetch is amortised G-fold.
-// Diagonal / super- / subdiagonal of T and the 2x2 flags live in shared
-// memory.  Arithmetic per vector identical to trevc_reg_kernel.
-template <int RPL, int G>
-__global__ void __launch_bounds__(256) trevc_grp_kernel(const double* Tall, const double* wrall,
-                                                        const double* wiall, double* Yall, int d) {
-    extern __shared__ double shm[];
-    double* tdg = shm;
-    double* tup = tdg + d;
-    double* tlo = tup + d;
-    int* lead = reinterpret_cast<int*>(tlo + d);
-    __shared__ int s_nl;
-    const int b = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const double* T = Tall + (size_t)b * d * d;
-    const double* wr = wrall + (size_t)b * d;
-    const double* wi = wiall + (size_t)b * d;
-    double* Y = Yall + (size_t)b * d * d;
-    for (int c = threadIdx.x; c < d; c += blockDim.x) {
-        tdg[c] = T[c + (size_t)c * d];
-        tup[c] = (c + 1 < d) ? T[c + (size_t)(c + 1) * d] : 0.0;
-        tlo[c] = (c > 0) ? T[c + (size_t)(c - 1) * d] : 0.0;
-    }
-    if (threadIdx.x == 0) {  // eigen-block leaders in ascending order
-        int n = 0;
-        for (int k = 0; k < d; ++k)
-            if (wi[k] >= 0.0) lead[n++] = k;
-        s_nl = n;
+        atomicMax(&s_top, top);
     }
     __syncthreads();
-    const int nl = s_nl;
-    const double smlnum = kSafeMin * ((double)d / kUlp);
-    auto load_col = [&](double (&dst)[RPL], int c, int lim) {
-#pragma unroll
-        for (int i = 0; i < RPL; ++i) {
-            const int r = lane + 32 * i;
-            dst[i] = (c >= 0 && r < lim) ? T[r + (size_t)c * d] : 0.0;
+    int j1 = s_top + 1;
+    const int ncol = min(W + 1, d - c0);  // slice columns touched (leaders and partners)
+    while (j1 > 0) {
+        int j0 = max(0, j1 - TBK);
+        if (j0 > 0 && Tg(j0, j0 - 1) != 0.0) --j0;  // never split a 2x2 Schur block
+        const int nb = j1 - j0;
+        for (int e = t; e < nb * nb; e += nt) {
+            const int r = e % nb, c = e / nb;
+            Td[r * LDD + c] = Tg(j0 + r, j0 + c);
         }
-    };
-    auto pick = [&](const double (&v)[RPL], int r) {
-        double x = 0.0;
-#pragma unroll
-        for (int i = 0; i < RPL; ++i)
-            if (i == (r >> 5)) x = v[i];
-        return __shfl_sync(0xffffffffu, x, r & 31);
-    };
-    auto put = [&](double (&v)[RPL], int r, double x) {
-#pragma unroll
-        for (int i = 0; i < RPL; ++i)
-            if (i == (r >> 5) && lane == (r & 31)) v[i] = x;
-    };
-    // eigen-block groups spread over the CTAs of this matrix (blockIdx.y) and
-    // interleaved so every CTA mixes short and long back substitutions
-    for (int g0 = (w * gridDim.y + blockIdx.y) * G; g0 < nl; g0 += nw * gridDim.y * G) {
-        double re[G][RPL], im[G][RPL];
-        int top[G], kid[G];
-        bool cx[G], on[G];
-        double lr[G], li[G], sm[G];
-        int jmax = -1;
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            on[g] = g0 + g < nl;
-            const int ki = on[g] ? lead[g0 + g] : 0;
-            kid[g] = ki;
-            const double wik = on[g] ? wi[ki] : 0.0;
-            cx[g] = wik != 0.0;
-            top[g] = on[g] ? ki : -1;
-            lr[g] = on[g] ? wr[ki] : 0.0;
-            li[g] = wik;
-            if (!on[g]) {
-#pragma unroll
-                for (int i = 0; i < RPL; ++i) re[g][i] = im[g][i] = 0.0;
-                sm[g] = 1.0;
-                continue;
+        if (stage_t && j0 > 0)
+            for (int e = t; e < j0 * nb; e += nt) {
+                const int r = e % j0, c = e / j0;  // coalesced along the column
+                Tp[(size_t)r * LDD + c] = Tg(r, j0 + c);
             }
-            if (!cx[g]) {
-                sm[g] = fmax(kUlp * fabs(lr[g]), smlnum);
-                load_col(re[g], ki, ki);
-#pragma unroll
-                for (int i = 0; i < RPL; ++i) {
-                    re[g][i] = -re[g][i];
-                    im[g][i] = 0.0;
-                    if (lane + 32 * i == ki) re[g][i] = 1.0;
-                }
-            } else {
-                const int pp = ki, q = ki + 1;
-                sm[g] = fmax(kUlp * (fabs(lr[g]) + fabs(wik)), smlnum);
-                double xpr, xqi;
-                if (fabs(tup[pp]) >= fabs(tlo[q])) {
-                    xpr = 1.0;
-                    xqi = wik / tup[pp];
-                } else {
-                    xpr = -wik / tlo[q];
-                    xqi = 1.0;
-                }
-                load_col(re[g], pp, pp);
-                load_col(im[g], q, pp);
-#pragma unroll
-                for (int i = 0; i < RPL; ++i) {
-                    const int r = lane + 32 * i;
-                    re[g][i] *= -xpr;
-                    im[g][i] *= -xqi;
-                    if (r == pp) {
-                        re[g][i] = xpr;
-                        im[g][i] = 0.0;
-                    }
-                    if (r == q) {
-                        re[g][i] = 0.0;
-                        im[g][i] = xqi;
-                    }
-                }
-            }
-            jmax = max(jmax, top[g] - 1);
-        }
-        int j = jmax;
-        double t1[RPL], t2[RPL], n1[RPL], n2[RPL];
-        bool pair = j > 0 && tlo[j] != 0.0;
-        load_col(t1, j, pair ? j - 1 : j);
-        load_col(t2, pair ? j - 1 : -1, j - 1);
-        while (j >= 0) {
-            const int jn = j - (pair ? 2 : 1);
-            const bool pairn = jn > 0 && tlo[jn] != 0.0;
-            load_col(n1, jn, pairn ? jn - 1 : jn);
-            load_col(n2, pairn ? jn - 1 : -1, jn - 1);
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                if (!on[g] || j >= top[g]) continue;
-                const cplx lam = cmk(lr[g], li[g]);
-                if (!cx[g]) {
-                    if (pair) {
-                        double x0, x1;
-                        solve2r(tdg[j - 1] - lam.re, tup[j - 1], tlo[j], tdg[j] - lam.re, pick(re[g], j - 1),
-                                pick(re[g], j), sm[g], x0, x1);
-#pragma unroll
-                        for (int i = 0; i < RPL; ++i) re[g][i] = fma(-x0, t2[i], fma(-x1, t1[i], re[g][i]));
-                        put(re[g], j - 1, x0);
-                        put(re[g], j, x1);
+        __syncthreads();
+        // ---- per-eigenvector solve of the diagonal block
+        if (lead && j0 <= top) {
+            auto Td_ = [&](int r, int c) { return Td[(r - j0) * LDD + (c - j0)]; };
+            double* yr = Ys + lc;
+            double* yi = Ys + lc + 1;
+            for (int j = min(j1 - 1, top); j >= j0; --j) {
+                const bool pr = j > j0 && Td_(j, j - 1) != 0.0;  // rows (j-1, j): a 2x2 Schur block
+                const bool two = pr || (cx && j == top);
+                if (q == 0 && j != top) {  // the solve of row j (rows j-1, j of a 2x2 block)
+                    if (!cx) {
+                        if (pr) {
+                            double x0, x1;
+                            solve2r(Td_(j - 1, j - 1) - lr, Td_(j - 1, j), Td_(j, j - 1), Td_(j, j) - lr,
+                                    yr[(size_t)(j - 1) * LDY], yr[(size_t)j * LDY], sm, x0, x1);
+                            yr[(size_t)(j - 1) * LDY] = x0;
+                            yr[(size_t)j * LDY] = x1;
+                        } else {
+                            double den = Td_(j, j) - lr;
+                            if (fabs(den) < sm) den = sm;
+                            yr[(size_t)j * LDY] /= den;
+                        }
                     } else {
-                        double den = tdg[j] - lam.re;
-                        if (fabs(den) < sm[g]) den = sm[g];
-                        const double x = pick(re[g], j) / den;
-#pragma unroll
-                        for (int i = 0; i < RPL; ++i) re[g][i] = fma(-x, t1[i], re[g][i]);
-                        put(re[g], j, x);
+                        const cplx lam = cmk(lr, li);
+                        if (pr) {
+                            const cplx b0 = cmk(yr[(size_t)(j - 1) * LDY], yi[(size_t)(j - 1) * LDY]);
+                            const cplx b1 = cmk(yr[(size_t)j * LDY], yi[(size_t)j * LDY]);
+                            cplx x0, x1;
+                            solve2(cmk(Td_(j - 1, j - 1), 0.0) - lam, cmk(Td_(j - 1, j), 0.0),
+                                   cmk(Td_(j, j - 1), 0.0), cmk(Td_(j, j), 0.0) - lam, b0, b1, sm, x0, x1);
+                            yr[(size_t)(j - 1) * LDY] = x0.re;
+                            yi[(size_t)(j - 1) * LDY] = x0.im;
+                            yr[(size_t)j * LDY] = x1.re;
+                            yi[(size_t)j * LDY] = x1.im;
+                        } else {
+                            cplx den = cmk(Td_(j, j), 0.0) - lam;
+                            if (cabs_(den) < sm) den = cmk(sm, 0.0);
+                            const cplx x = cdiv(cmk(yr[(size_t)j * LDY], yi[(size_t)j * LDY]), den);
+                            yr[(size_t)j * LDY] = x.re;
+                            yi[(size_t)j * LDY] = x.im;
+                        }
                     }
-                } else if (pair) {
-                    const cplx b0 = cmk(pick(re[g], j - 1), pick(im[g], j - 1));
-                    const cplx b1 = cmk(pick(re[g], j), pick(im[g], j));
-                    cplx x0, x1;
-                    solve2(cmk(tdg[j - 1], 0) - lam, cmk(tup[j - 1], 0), cmk(tlo[j], 0), cmk(tdg[j], 0) - lam, b0,
-                           b1, sm[g], x0, x1);
-#pragma unroll
-                    for (int i = 0; i < RPL; ++i) {
-                        re[g][i] = fma(-x0.re, t2[i], fma(-x1.re, t1[i], re[g][i]));
-                        im[g][i] = fma(-x0.im, t2[i], fma(-x1.im, t1[i], im[g][i]));
+                }
+                __syncwarp(gmask);
+                // rows above inside the block, split over the group's GS lanes
+                const int lim = two ? j - 1 : j;
+                const double x1r = yr[(size_t)j * LDY];
+                const double x0r = two ? yr[(size_t)(j - 1) * LDY] : 0.0;
+                if (!cx) {
+                    for (int i = j0 + q; i < lim; i += GS) {
+                        double v = yr[(size_t)i * LDY] - Td_(i, j) * x1r;
+                        if (two) v -= Td_(i, j - 1) * x0r;
+                        yr[(size_t)i * LDY] = v;
                     }
-                    put(re[g], j - 1, x0.re);
-                    put(re[g], j, x1.re);
-                    put(im[g], j - 1, x0.im);
-                    put(im[g], j, x1.im);
                 } else {
-                    cplx den = cmk(tdg[j], 0.0) - lam;
-                    if (cabs_(den) < sm[g]) den = cmk(sm[g], 0.0);
-                    const cplx x = cdiv(cmk(pick(re[g], j), pick(im[g], j)), den);
-#pragma unroll
-                    for (int i = 0; i < RPL; ++i) {
-                        re[g][i] = fma(-x.re, t1[i], re[g][i]);
-                        im[g][i] = fma(-x.im, t1[i], im[g][i]);
+                    const double x1i = yi[(size_t)j * LDY];
+                    const double x0i = two ? yi[(size_t)(j - 1) * LDY] : 0.0;
+                    for (int i = j0 + q; i < lim; i += GS) {
+                        double vr = yr[(size_t)i * LDY] - Td_(i, j) * x1r;
+                        double vi = yi[(size_t)i * LDY] - Td_(i, j) * x1i;
+                        if (two) {
+                            vr -= Td_(i, j - 1) * x0r;
+                            vi -= Td_(i, j - 1) * x0i;
+                        }
+                        yr[(size_t)i * LDY] = vr;
+                        yi[(size_t)i * LDY] = vi;
                     }
-                    put(re[g], j, x.re);
-                    put(im[g], j, x.im);
                 }
-            }
-#pragma unroll
-            for (int i = 0; i < RPL; ++i) {
-                t1[i] = n1[i];
-                t2[i] = n2[i];
-            }
-            j = jn;
-            pair = pairn;
-        }
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            if (!on[g]) continue;
-            const int ki = kid[g], last = cx[g] ? ki + 1 : ki;
-            double* yr = Y + (size_t)ki * d;
-#pragma unroll
-            for (int i = 0; i < RPL; ++i) {
-                const int r = lane + 32 * i;
-                if (r < d) yr[r] = (r <= last) ? re[g][i] : 0.0;
-            }
-            if (cx[g]) {
-                double* yi = Y + (size_t)(ki + 1) * d;
-#pragma unroll
-                for (int i = 0; i < RPL; ++i) {
-                    const int r = lane + 32 * i;
-                    if (r < d) yi[r] = (r <= last) ? im[g][i] : 0.0;
-                }
+                __syncwarp(gmask);
+                if (two) --j;
             }
         }
+        __syncthreads();
+        // ---- shift-free update of the rows above: Y[0:j0, :] -= T[0:j0, j0:j1] Y[j0:j1, :],
+        // 4 x 4 register tiles per thread (columns padded to LDY, a multiple of 4)
+        {
+            const int rt = (j0 + 3) / 4, ct = (ncol + 3) / 4;
+            for (int e = t; e < rt * ct; e += nt) {
+                const int r0 = 4 * (e / ct), cc = 4 * (e % ct);
+                double acc[4][4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+                for (int q = 0; q < nb; ++q) {
+                    double tv[4];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) {
+                        const int r = min(r0 + a, j0 - 1);
+                        tv[a] = stage_t ? Tp[(size_t)r * LDD + q] : Tg(r, j0 + q);
+                    }
+                    const double* yq = Ys + (size_t)(j0 + q) * LDY + cc;
+                    const double y0 = yq[0], y1 = yq[1], y2 = yq[2], y3 = yq[3];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) {
+                        acc[a][0] = fma(tv[a], y0, acc[a][0]);
+                        acc[a][1] = fma(tv[a], y1, acc[a][1]);
+                        acc[a][2] = fma(tv[a], y2, acc[a][2]);
+                        acc[a][3] = fma(tv[a], y3, acc[a][3]);
+                    }
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+                    if (r0 + a < j0)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) Ys[(size_t)(r0 + a) * LDY + cc + c] -= acc[a][c];
+            }
+        }
+        __syncthreads();
+        j1 = j0;
+    }
+    // write the slice's columns: leaders k (and their partners k + 1)
+    for (int e = t; e < d * ncol; e += nt) {
+        const int r = e % d, c = e / d;
+        const int kk = c0 + c;
+        if (kk >= d) continue;
+        const bool own = c < W ? true : (wi[kk] < 0.0);  // column W: the partner of the last leader
+        if (c < W && c == 0 && wi[kk] < 0.0) continue;  // column c0 is the previous slice's partner
+        if (!own) continue;
+        Y[(size_t)kk * d + r] = Ys[(size_t)r * LDY + c];
     }
 }
 
@@ -2127,18 +1949,21 @@ void launch_hqr(double* H, double* Z, double* wr, double* wi, int d, int batch,
 
 void launch_trevc(const double* T, const double* wr, const double* wi, double* Y, int d,
                   int batch, cudaStream_t st) {
-    const int rpl = (d + 31) / 32;
-    const size_t gsm = 3 * (size_t)d * sizeof(double) + (size_t)d * sizeof(int);
-    if (rpl <= 2)
-        trevc_grp_kernel<2, 4><<<dim3(batch, (d + 15) / 16), 128, gsm, st>>>(T, wr, wi, Y, d);
-    else if (rpl <= 4)
-        trevc_grp_kernel<4, 4><<<dim3(batch, (d + 15) / 16), 128, gsm, st>>>(T, wr, wi, Y, d);
-    else if (rpl <= 8)
-        trevc_grp_kernel<8, 4><<<dim3(batch, (d + 15) / 16), 128, gsm, st>>>(T, wr, wi, Y, d);
-    else if (rpl <= 16)
-        trevc_reg_kernel<16><<<batch, 256, d, st>>>(T, wr, wi, Y, d);
-    else
-        trevc_reg_kernel<32><<<batch, 256, d, st>>>(T, wr, wi, Y, d);
+    // blocked back substitution (trevc_blk_kernel): W leader columns per CTA and GS
+    // threads per leader (W GS = 256), the slice of Y in shared memory sized for
+    // two CTAs per SM; T's column panel is read from L2
+    auto smem = [&](int W) { return ((size_t)d * (W + 4) + (size_t)(TBK + 1) * (TBK + 2)) * sizeof(double); };
+    static unsigned long long a32 = 0, a16 = 0, a8 = 0;
+    if (d <= 256) {
+        smem_attr_once(trevc_blk_kernel<32, 8>, 110 * 1024, a32);
+        trevc_blk_kernel<32, 8><<<dim3(batch, (d + 31) / 32), 256, smem(32), st>>>(T, wr, wi, Y, d, 0);
+    } else if (d <= 512) {
+        smem_attr_once(trevc_blk_kernel<16, 16>, 110 * 1024, a16);
+        trevc_blk_kernel<16, 16><<<dim3(batch, (d + 15) / 16), 256, smem(16), st>>>(T, wr, wi, Y, d, 0);
+    } else {
+        smem_attr_once(trevc_blk_kernel<8, 32>, 110 * 1024, a8);
+        trevc_blk_kernel<8, 32><<<dim3(batch, (d + 7) / 8), 256, smem(8), st>>>(T, wr, wi, Y, d, 0);
+    }
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
