@@ -727,7 +727,7 @@ def main():
             "boundary back substitution (TRSM + DMMA GEMM)": (res["t_lu_solve"], L * (R * (2 * d) ** 2 + 4 * G ** 2)),
             "eigen refinement (Newton step, 8N residual GEMMs)": (res["t_refine"], Be * 24.0 * d ** 3),
             "blocked Hessenberg + Q": (res["t_hessenberg"], Be * (10.0 / 3.0 + 4.0 / 3.0) * d ** 3),
-            "trevc_grp_kernel (eigenvectors)": (res["t_trevc"], Be * (1.0 / 3.0) * d ** 3)}
+            "trevc_blk_kernel (eigenvectors)": (res["t_trevc"], Be * (1.0 / 3.0) * d ** 3)}
     name = max(kern, key=lambda k: kern[k][0])
     t_k, flops = kern[name]
     traffic = None
@@ -783,7 +783,7 @@ def main():
         "data": "synthetic (SURVEY §8(d) Greek generator G(g,L), deterministic)",
         "config": {"workload": f"{args.config}: {w.note}", "N": N, "L": L, "layers": P,
                    "n_in": n_in, "n_dphi": nd, "basis": "default 4-vector",
-                   "parallelism": f"solve-sharded x{world} (independent BRDFs per rank, no collective)",
+                   "parallelism": "single GPU, one solve per step (bench.py --gpus N: orders sharded over N GPUs)",
                    "l2": "working set ~1.5 GB per solve >> 126 MB L2 (no explicit flush)"},
         "e2e": {"value": world * args.steps / e2e_s, "unit": "solves/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
