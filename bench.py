@@ -555,11 +555,19 @@ def run_sharded(args):
     mat = V.Material.load(w.material.write(tmp, "m"))
     opts = V.options(w.N)
     single = args.config == "C4p"
-    mats = [mat] if single else [mat] * world
+    # in-flight layout: groups of g <= 4 GPUs, orders sharded g ways inside a group,
+    # g solves in flight per group (an 8-way order shard of C3 is too small to keep
+    # a GPU busy: scripts/shard_probe.py)
+    g = world if single or world <= 4 or world % 4 else 4
+    groups = [list(range(i, i + g)) for i in range(0, world, g)]
+    handles = [dist.new_group(ranks=r) for r in groups] if g < world else [None]
+    mine = rank // g
+    my_group, my_ranks = (handles[mine], groups[mine]) if g < world else (None, None)
+    mats = [mat] if single else [mat] * g
     per_step = 1 if single else world
     conc = min(4, len(mats))
     dist.barrier()
-    sh = D.OrderShards(mats, opts, nodes, w.n_dphi, None, world, rank, local, None, conc)
+    sh = D.OrderShards(mats, opts, nodes, w.n_dphi, None, g, rank % g, local, my_group, conc, ranks=my_ranks)
 
     def step():
         sh.run()
@@ -585,7 +593,7 @@ def run_sharded(args):
     sh.close()
     # e2e through the public calls (host inputs, host table of the owned solve)
     call = (lambda: D.sharded_brdf(mat, opts, nodes, w.n_dphi, device=local)) if single else \
-        (lambda: D.inflight_brdf(mats, opts, nodes, w.n_dphi, device=local, concurrency=conc))
+        (lambda: D.inflight_brdf(mats, opts, nodes, w.n_dphi, group=my_group, device=local, concurrency=conc))
     for _ in range(args.warmup):
         call()
     dist.barrier()
@@ -615,9 +623,9 @@ def run_sharded(args):
                        "n_dphi": nd,
                        "parallelism": (f"one solve per step, orders sharded x{world} (m = rank mod {world}), "
                                        "NCCL gather of the per-order stacks to rank 0, synthesis there") if single
-                       else (f"{world} solves in flight per step, each sharded by order over the {world} GPUs "
-                             f"({world} plans per GPU, {conc} concurrent), NCCL all-to-all of the per-order "
-                             "stacks, each rank synthesizes one solve"),
+                       else (f"{world} solves in flight per step: {world // g} group(s) of {g} GPUs, each solve "
+                             f"sharded by order over its group ({g} plans per GPU, {conc} concurrent), NCCL "
+                             "all-to-all of the per-order stacks inside the group, each rank synthesizes one solve"),
                        "exchange_bytes_per_step": per_step * 8 * L * R * d,
                        "l2": "working set >> 126 MB L2 (no explicit flush)"},
             "e2e": {"value": per_step * args.steps / e2e_s, "unit": "solves/s", "h2d_bytes_per_step": h2d,

@@ -17,6 +17,9 @@ Two layouts over W ranks:
     order shard of each of W solves (W plans on its GPU, run concurrently) and
     an all-to-all hands solve j's shards to rank j, which synthesizes it -- the
     per-GPU work is one solve's worth, split into W order shards.
+Both take a process group: on 8 GPUs the throughput layout runs as two groups
+of 4 (orders sharded 4 ways inside a group, 4 solves in flight per group):
+an order shard of a C3 solve stays large enough to keep its GPU busy.
 """
 from __future__ import annotations
 
@@ -39,17 +42,23 @@ def _dist():
     return dist
 
 
-def gather_order_stacks(local, L: int, world: int, rank: int, dst: int = 0, group=None):
+def _peer(ranks, j):
+    """Global rank of group member j (ranks: the group's global ranks, or None)."""
+    return j if ranks is None else ranks[j]
+
+
+def gather_order_stacks(local, L: int, world: int, rank: int, dst: int = 0, group=None, ranks=None):
     """Point-to-point gather of the order shards to `dst`: `local` is this
     rank's tensor [n_r, ...] of orders m = rank + k world; on dst returns the
     full [L, ...] tensor (order m at index m), None elsewhere.  CUDA tensors go
-    over NCCL, CPU tensors over gloo."""
+    over NCCL, CPU tensors over gloo.  world / rank / dst are positions in
+    `ranks` (the group's global ranks; None = the default group)."""
     import torch
     dist = _dist()
     shape = tuple(local.shape[1:])
     if rank != dst:
         if local.shape[0] > 0:
-            for r in dist.batch_isend_irecv([dist.P2POp(dist.isend, local.contiguous(), dst, group)]):
+            for r in dist.batch_isend_irecv([dist.P2POp(dist.isend, local.contiguous(), _peer(ranks, dst), group)]):
                 r.wait()
         return None
     full = torch.empty((L,) + shape, dtype=local.dtype, device=local.device)
@@ -62,7 +71,7 @@ def gather_order_stacks(local, L: int, world: int, rank: int, dst: int = 0, grou
             full[src::world] = local
             continue
         bufs[src] = torch.empty((n,) + shape, dtype=local.dtype, device=local.device)
-        ops.append(dist.P2POp(dist.irecv, bufs[src], src, group))
+        ops.append(dist.P2POp(dist.irecv, bufs[src], _peer(ranks, src), group))
     if ops:
         for r in dist.batch_isend_irecv(ops):
             r.wait()
@@ -71,7 +80,7 @@ def gather_order_stacks(local, L: int, world: int, rank: int, dst: int = 0, grou
     return full
 
 
-def alltoall_order_stacks(locals_by_owner, L: int, world: int, rank: int, group=None):
+def alltoall_order_stacks(locals_by_owner, L: int, world: int, rank: int, group=None, ranks=None):
     """All-to-all of order shards: locals_by_owner[j] is this rank's shard of
     solve j (orders m = rank + k world, [n_rank, ...]); returns the full
     [L, ...] stacks of solve `rank`, assembled from every rank's shard."""
@@ -84,13 +93,13 @@ def alltoall_order_stacks(locals_by_owner, L: int, world: int, rank: int, group=
     ops, bufs = [], {}
     for j in range(world):
         if j != rank and locals_by_owner[j].shape[0] > 0:
-            ops.append(dist.P2POp(dist.isend, locals_by_owner[j].contiguous(), j, group))
+            ops.append(dist.P2POp(dist.isend, locals_by_owner[j].contiguous(), _peer(ranks, j), group))
     for src in range(world):
         n = len(range(src, L, world))
         if src == rank or n == 0:
             continue
         bufs[src] = torch.empty((n,) + shape, dtype=mine.dtype, device=mine.device)
-        ops.append(dist.P2POp(dist.irecv, bufs[src], src, group))
+        ops.append(dist.P2POp(dist.irecv, bufs[src], _peer(ranks, src), group))
     if ops:
         for r in dist.batch_isend_irecv(ops):
             r.wait()
@@ -152,11 +161,11 @@ class OrderShards:
     builds the owned table on the device."""
 
     def __init__(self, materials, opts, mu_in, n_dphi=19, basis=None, world=1, rank=0, device=0,
-                 group=None, concurrency=4, pooled=True):
+                 group=None, concurrency=4, pooled=True, ranks=None):
         import paper_1707_05882_b200 as V
         if len(materials) not in (1, world):
             raise ValueError("OrderShards: one solve, or one solve per rank")
-        self.world, self.rank, self.group, self.device = world, rank, group, device
+        self.world, self.rank, self.group, self.device, self.ranks = world, rank, group, device, ranks
         self.concurrency = max(1, concurrency)
         L = materials[0].info()[0]
         if any(m.info()[0] != L for m in materials):
@@ -191,9 +200,9 @@ class OrderShards:
         if host:
             ups = [u.cpu() for u in ups]
         if len(self.plans) == 1:
-            full = gather_order_stacks(ups[0], self.L, self.world, self.rank, 0, self.group)
+            full = gather_order_stacks(ups[0], self.L, self.world, self.rank, 0, self.group, self.ranks)
         else:
-            full = alltoall_order_stacks(ups, self.L, self.world, self.rank, self.group)
+            full = alltoall_order_stacks(ups, self.L, self.world, self.rank, self.group, self.ranks)
         if host and full is not None:
             import torch
             full = full.to(torch.device("cuda", self.plans[0].device))
@@ -224,6 +233,13 @@ def _world(group):
     return dist.get_world_size(group), dist.get_rank(group)
 
 
+def _group_ranks(group):
+    if group is None:
+        return None
+    dist = _dist()
+    return dist.get_process_group_ranks(group)
+
+
 def sharded_brdf(material, opts, mu_in, n_dphi=19, basis=None, group=None, device=None):
     """ONE BRDF table with its orders sharded across the ranks of the process
     group: host table [n_in, N, n_dphi, 4, 4] on rank 0, None elsewhere."""
@@ -233,7 +249,7 @@ def sharded_brdf(material, opts, mu_in, n_dphi=19, basis=None, group=None, devic
     if order_shard(L, world, rank)[2] == 0:
         return None  # more ranks than orders: nothing to solve or send here (rank 0 always has m = 0)
     dev = torch.cuda.current_device() if device is None else device
-    sh = OrderShards([material], opts, mu_in, n_dphi, basis, world, rank, dev, group)
+    sh = OrderShards([material], opts, mu_in, n_dphi, basis, world, rank, dev, group, ranks=_group_ranks(group))
     try:
         sh.exchange()
         return sh.synthesize(True)
@@ -248,7 +264,8 @@ def inflight_brdf(materials, opts, mu_in, n_dphi=19, basis=None, group=None, dev
     import torch
     world, rank = _world(group)
     dev = torch.cuda.current_device() if device is None else device
-    sh = OrderShards(materials, opts, mu_in, n_dphi, basis, world, rank, dev, group, concurrency)
+    sh = OrderShards(materials, opts, mu_in, n_dphi, basis, world, rank, dev, group, concurrency,
+                     ranks=_group_ranks(group))
     try:
         sh.exchange()
         return sh.synthesize(True)

@@ -5,13 +5,14 @@
   concW  : the W shards run concurrently (W host threads / streams) -> the
            per-GPU work of W in-flight solves each sharded over W GPUs
            (throughput mode)
-Usage: python scripts/shard_probe.py [C3|C4p] [W,...]"""
+Usage: python scripts/shard_probe.py [C3|C4p] [W,...] [concurrency,...]"""
 import json, os, sys, tempfile, threading, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import bench, paper_1707_05882_b200 as V
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C3"
 Ws = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "2,4,8").split(",")]
+Ks = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [0]  # 0: all W at once
 w = bench.workload(cfg)
 nodes = bench.quad_nodes(w.N)
 L = w.material.order_count
@@ -30,11 +31,15 @@ for W in Ws:
     for q in plans:
         q.run(1)
         alone.append(q.run(steps) * 1e3)
-    ths = [threading.Thread(target=q.run, args=(steps,)) for q in plans]
-    t = time.perf_counter()
-    for th in ths: th.start()
-    for th in ths: th.join()
-    conc = (time.perf_counter() - t) / steps * 1e3
-    out[f"W{W}"] = {"shard_alone_ms_max": max(alone), "shard_alone_ms": alone, "concurrent_ms_per_solve": conc}
+    rec = {"shard_alone_ms_max": max(alone), "shard_alone_ms": alone}
+    for K in Ks:
+        K = K or W
+        groups = [plans[i::K] for i in range(K)]
+        ths = [threading.Thread(target=lambda g=g: [q.run(steps) for q in g]) for g in groups]
+        t = time.perf_counter()
+        for th in ths: th.start()
+        for th in ths: th.join()
+        rec[f"concurrent{K}_ms_per_solve"] = (time.perf_counter() - t) / steps * 1e3
+    out[f"W{W}"] = rec
     for q in plans: q.close()
     print(json.dumps(out), flush=True)

@@ -111,3 +111,41 @@ def test_shard_partition_covers_every_order_once():
             assert seen == list(range(L))
             sizes = [D.order_shard(L, world, r)[2] for r in range(world)]
             assert max(sizes) - min(sizes) <= 1
+
+
+def _group_worker(rank, world, port, q):
+    """Two groups of 2 ranks: the all-to-all inside each group (global ranks
+    mapped through the group's rank list)."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    groups = [[0, 1], [2, 3]]
+    handles = [dist.new_group(ranks=g) for g in groups]
+    mine = rank // 2
+    L, g = 7, 2
+    pos = rank % 2
+    full = {j: np.arange(L * 3, dtype=np.float64).reshape(L, 3) * (10 * mine + j + 1) for j in range(g)}
+    local = [torch.from_numpy(np.ascontiguousarray(full[j][pos::g])) for j in range(g)]
+    got = D.alltoall_order_stacks(local, L, g, pos, handles[mine], groups[mine])
+    ok = bool(np.array_equal(got.numpy(), full[pos]))
+    oks = [None] * world
+    dist.all_gather_object(oks, ok)
+    if rank == 0:
+        q.put(all(oks))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_alltoall_inside_process_subgroups():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_group_worker, args=(r, 4, port, q)) for r in range(4)]
+    for p in procs:
+        p.start()
+    ok = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert ok

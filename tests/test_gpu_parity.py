@@ -105,7 +105,7 @@ def test_c3_partial_table_matches_oracle():
     g, b = gpu_table(w.material, w.N, nodes, 19)
     pick = [0, 40, 63]
     r, _ = O.brdf(oracle_material(w.material), w.N, nodes[pick], 19)
-    assert matrix_metric(g[pick], r) < 5e-9  # measured 7e-10 (reference's own error)
+    assert matrix_metric(g[pick], r) < 1e-9  # measured 7.0e-10 (the reference's own error)
     assert b.device_stats()["max_eigen_residual"] < 1e-10
     with O.accurate():
         ra, _ = O.brdf(oracle_material(w.material), w.N, nodes[[40]], 19)
