@@ -178,13 +178,39 @@ __global__ void base_kernel(BndArgs a, int mo) {
 }
 
 // Right-hand sides: warp per (order mo, column = incident*4 + channel).
+// CTA per (order, RHS_TW consecutive columns), warp per column: the columns are
+// built in a shared-memory tile [G][RHS_TW] and written to the augmented system
+// and its untouched copy as whole row segments (a warp writing one column of
+// the row-major system would touch one 32-byte sector per element).
+template <int RHS_TW>
+__device__ void rhs_column(const BndArgs& a, int mo, int col, double* tile, double* sm, int w, int lane);
+
+template <int RHS_TW>
 __global__ void rhs_kernel(BndArgs a) {
-    extern __shared__ double sm[];
+    extern __shared__ double shm[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gw = blockIdx.x * (blockDim.x >> 5) + w;
     const int d = a.d, P = a.p.n_layers, G = 2 * d * P, R = 4 * a.p.n_in;
-    if (gw >= a.p.n_orders * R) return;
-    const int mo = gw / R, col = gw % R, ii = col / 4, c = col % 4;
+    const int mo = blockIdx.y, col0 = blockIdx.x * RHS_TW, col = col0 + w;
+    double* tile = shm;                              // [G][RHS_TW]
+    double* sm = shm + (size_t)G * RHS_TW;           // per-warp scratch [2d]
+    if (col < R) rhs_column<RHS_TW>(a, mo, col, tile, sm, w, lane);
+    __syncthreads();
+    const int nc = min(RHS_TW, R - col0);
+    double* A = a.lhs + (size_t)mo * a.sl + G + col0;
+    double* A0 = a.lhs0 ? a.lhs0 + (size_t)mo * a.sl + G + col0 : nullptr;
+    for (int e = threadIdx.x; e < G * RHS_TW; e += blockDim.x) {
+        const int r = e / RHS_TW, cc = e % RHS_TW;
+        if (cc >= nc) continue;
+        const double v = tile[e];
+        A[(size_t)r * a.ldl + cc] = v;
+        if (A0) A0[(size_t)r * a.ldl + cc] = v;
+    }
+}
+
+template <int RHS_TW>
+__device__ void rhs_column(const BndArgs& a, int mo, int col, double* tile, double* sm, int w, int lane) {
+    const int d = a.d, P = a.p.n_layers, G = 2 * d * P, R = 4 * a.p.n_in;
+    const int ii = col / 4, c = col % 4;
     const int m = a.p.order_of(mo);
     const double mu0 = a.p.mu_in[ii];
     // row-major [G][R] per order (lu.cu); B(r) = rhs[mo][r * R + col]
@@ -192,28 +218,23 @@ __global__ void rhs_kernel(BndArgs a) {
     double bmax = 0.0, b1 = 0.0;
     struct Ref {
         double* x;
-        double* y;
         double* bmax;
         double* b1;
         __device__ void operator=(double v) const {
             *x = v;
-            if (y) *y = v;
             *bmax = fmax(*bmax, fabs(v));
             *b1 += fabs(v);
         }
     };
-    struct RowView {
+    struct RowView {  // storage row bnd_row(r) of this column in the tile
         double* base;
-        double* base0;
-        int R, d, G;
+        int d, G;
         double* bmax;
         double* b1;
         __device__ Ref operator[](int r) const {
-            const size_t o = (size_t)bnd_row(r, d, G) * R;
-            return Ref{base + o, base0 ? base0 + o : nullptr, bmax, b1};
+            return Ref{base + (size_t)bnd_row(r, d, G) * RHS_TW, bmax, b1};
         }
-    } B{a.rhs + (size_t)mo * a.sr + col, a.lhs0 ? a.lhs0 + (size_t)mo * a.sl + (a.rhs - a.lhs) + col : nullptr,
-        a.ldr, d, G, &bmax, &b1};
+    } B{tile + w, d, G, &bmax, &b1};
     auto finish_norms = [&]() {
         if (!a.bnorm) return;
         const double mx = warp_max(bmax), s1 = warp_sum(b1);
@@ -260,6 +281,7 @@ __global__ void rhs_kernel(BndArgs a) {
         return;
     }
     double* v = sm + (size_t)w * 2 * d;
+    (void)R;
     double* out = v + d;
     for (int i = lane; i < d; i += 32) v[i] = bb * zm(q, i);
     __syncwarp();
@@ -628,10 +650,17 @@ void launch_bnd_assemble(const BndArgs& a, cudaStream_t st) {
 }
 
 void launch_bnd_rhs(const BndArgs& a, cudaStream_t st) {
-    const int warps = 4;
-    const long long total = (long long)a.p.n_orders * 4 * a.p.n_in;
-    rhs_kernel<<<(unsigned)((total + warps - 1) / warps), warps * 32,
-                 warps * 2 * a.d * sizeof(double), st>>>(a);
+    // tile width 8 (64-byte row segments) while the tile fits, else 2
+    const int R = 4 * a.p.n_in, G = 2 * a.d * a.p.n_layers;
+    auto smem = [&](int tw) { return ((size_t)G * tw + (size_t)tw * 2 * a.d) * sizeof(double); };
+    static unsigned long long attr8 = 0, attr2 = 0;
+    if (smem(8) <= 200 * 1024) {
+        smem_attr_once(rhs_kernel<8>, 200 * 1024, attr8);
+        rhs_kernel<8><<<dim3((R + 7) / 8, a.p.n_orders), 8 * 32, smem(8), st>>>(a);
+    } else {
+        smem_attr_once(rhs_kernel<2>, 200 * 1024, attr2);
+        rhs_kernel<2><<<dim3((R + 1) / 2, a.p.n_orders), 2 * 32, smem(2), st>>>(a);
+    }
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
