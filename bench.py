@@ -281,7 +281,7 @@ def run_c5(args):
     mats = [V.Material.load(w.material.write(tmp, f"b{b}")) for b, w in zip(bands, ws)]
     opts = V.options(N)
     peak = fp64_peak_tflops(torch.device("cuda", local)) if rank == 0 else None
-    plans = [V.Plan(m, opts, nodes, nd, device=local) for m in mats]
+    plans = [V.Plan(m, opts, nodes, nd, device=local, pooled=True) for m in mats]  # concurrent: lean kernels
     K = max(1, args.concurrency)
 
     def run_all(steps):

@@ -76,6 +76,10 @@ typedef struct vrte_cuda_problem {
     double* dump_nu;
     double* dump_residual;
     double* dump_boundary;
+    /* Scheduling hint: non-zero when this solve runs concurrently with others on
+       the same device (spectral batch, pooled order shards): kernels pick their
+       lower-register builds that let two CTAs share an SM. */
+    int32_t concurrent;
 } vrte_cuda_problem;
 
 typedef struct vrte_cuda_result {

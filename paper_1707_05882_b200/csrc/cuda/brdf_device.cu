@@ -115,6 +115,7 @@ struct vrte_cuda_plan {
     // inputs
     DevBuf<double> nodes, weights, mdiag, omega, greek, tau, mu_in, table, beam_rows, post, trig, refl_top, pre;
     int out_lo = 0;
+    bool lean = false;  // problem->concurrent: lower-register kernel builds
     DevBuf<int> medium, order_index, slot_of_order;
     // homogeneous
     DevBuf<double> gsf_n, gsf_b, E, F, T, Z, psi_p, psi_m, tmp1, tmp2, tmp3, tmp4;
@@ -286,6 +287,7 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     put(pl.post, p->post, (size_t)pl.n_in * 16);
     put(pl.trig, p->trig, (size_t)L * pl.n_dphi * 2);
     pl.out_lo = p->refl_top ? p->out_lo : 0;
+    pl.lean = p->concurrent != 0;
     pl.dump_kernel = p->dump_kernel;
     pl.dump_nu = p->dump_nu;
     pl.dump_residual = p->dump_residual;
@@ -509,7 +511,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     launch_hessenberg_blocked(pl.T.p, pl.Z.p, pl.hwork.p, d, B, st);
     nl += hessenberg_launch_count(d);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[6], st));
-    launch_hqr(pl.T.p, pl.Z.p, pl.wr.p, pl.wi.p, d, B, pl.status, st);
+    launch_hqr(pl.T.p, pl.Z.p, pl.wr.p, pl.wi.p, d, B, pl.status, st, nullptr, pl.lean);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[7], st));
     launch_trevc(pl.T.p, pl.wr.p, pl.wi.p, pl.tmp1.p, d, B, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[8], st));

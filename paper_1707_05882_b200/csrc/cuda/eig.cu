@@ -728,7 +728,8 @@ __device__ inline void cluster_sync_all() {
 }
 __device__ inline void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) hqr_multi_kernel(double* Hall, double* Zall, double* wrall,
+template <int MINB>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, MINB) hqr_multi_kernel(double* Hall, double* Zall, double* wrall,
                                                         double* wiall, int d, DeviceStatus* status,
                                                         int aed_nw, int nb4_min, int nb2_min, int nibble,
                                                         double* trace) {
@@ -1941,9 +1942,15 @@ void launch_hessenberg(double* A, double* Z, int d, int batch, cudaStream_t st) 
 }
 
 void launch_hqr(double* H, double* Z, double* wr, double* wi, int d, int batch,
-                DeviceStatus* status, cudaStream_t st, double* trace) {
-    // 2-CTA clusters: rank 0 chases / deflates, rank 1 applies the chunk factors
-    hqr_multi_kernel<<<2 * batch, 256, 0, st>>>(H, Z, wr, wi, d, status, AED_NW, 48, 24, 40, trace);
+                DeviceStatus* status, cudaStream_t st, double* trace, bool lean) {
+    // 2-CTA clusters: rank 0 chases / deflates, rank 1 applies the chunk factors.
+    // lean: the 128-register build (some spills, 2 CTAs per SM) for plans that run
+    // concurrently with others (spectral batch, order shards in flight); a lone
+    // solve takes the 229-register build (1 CTA per SM, no spills, ~9% faster)
+    if (lean)
+        hqr_multi_kernel<2><<<2 * batch, 256, 0, st>>>(H, Z, wr, wi, d, status, AED_NW, 48, 24, 40, trace);
+    else
+        hqr_multi_kernel<1><<<2 * batch, 256, 0, st>>>(H, Z, wr, wi, d, status, AED_NW, 48, 24, 40, trace);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -51,7 +51,7 @@ int hessenberg_launch_count(int d);
 // reflectors, sweeps, AED calls, AED cycles, chase cycles, update-wait cycles,
 // AED deflations
 void launch_hqr(double* H, double* Z, double* wr, double* wi, int d, int batch,
-                DeviceStatus* status, cudaStream_t st, double* trace = nullptr);
+                DeviceStatus* status, cudaStream_t st, double* trace = nullptr, bool lean = false);
 void launch_trevc(const double* T, const double* wr, const double* wi, double* Y, int d,
                   int batch, cudaStream_t st);
 // Normalize packed eigenvector columns by their max complex modulus; returns

@@ -859,7 +859,8 @@ void write_dumps(const Dumps& d, const BrdfSetup& s) {
 }
 
 vrte_status compute_brdf_on(const vrte_material* material, const vrte_options* options, const double* mu_in,
-                            size_t n_mu_in, int32_t n_dphi, const double* basis, int device, vrte_brdf** out) {
+                            size_t n_mu_in, int32_t n_dphi, const double* basis, int device, vrte_brdf** out,
+                            bool concurrent = false) {
     if (!material || !out || !mu_in || n_mu_in == 0) return set_error(VRTE_E_ARGUMENT, "null argument");
     return guarded([&] {
         const double t0 = wall_now();
@@ -872,6 +873,7 @@ vrte_status compute_brdf_on(const vrte_material* material, const vrte_options* o
             s.prob.n_devices = 0;
         }
         const Dumps dumps = prepare_dumps(options, s);
+        s.prob.concurrent = concurrent ? 1 : 0;
         const int N = s.quad.n, np = s.prob.n_dphi;
         BrdfTable& t = h->table;
         t.mu_in = s.mu_in_user;
@@ -961,7 +963,7 @@ vrte_status vrte_compute_brdf_batch(const vrte_material* const* materials, size_
         for (size_t i = next++; i < count; i = next++) {
             vrte_brdf* h = nullptr;
             const vrte_status rc = materials[i] ? compute_brdf_on(materials[i], options, mu_in, n_mu_in, n_dphi,
-                                                                  basis, devs[i % devs.size()], &h)
+                                                                  basis, devs[i % devs.size()], &h, nthreads > 1)
                                                 : set_error(VRTE_E_ARGUMENT, "null material");
             if (rc == VRTE_OK) {
                 out[i] = h;
@@ -1094,6 +1096,7 @@ vrte_status vrte_brdf_plan_acquire(const vrte_material* material, const vrte_opt
         s.prob.n_orders = n_orders;
         s.prob.devices = nullptr;
         s.prob.n_devices = 0;
+        s.prob.concurrent = 1;  // pooled order shards run several plans per device
         vrte_cuda_result r{};
         const int32_t rc = vrte_cuda_plan_acquire(&s.prob, out, &r);
         if (rc == 5) throw std::invalid_argument(r.message);
