@@ -715,6 +715,33 @@ def main():
             dist.destroy_process_group()
         return
 
+    # ---------------- concurrent solves (secondary: K independent solves of the same
+    # shape in flight on one GPU, one pooled plan / stream each -- what concurrent
+    # callers of the reentrant C ABI get; the headline `value` stays one solve at a time)
+    concurrent = None
+    if world == 1 and args.config not in ("C4p",):
+        import threading
+        K = 4
+        cplans = [V.Plan(mat, opts, nodes, w.n_dphi, device=local, pooled=True) for _ in range(K)]
+        for q in cplans:
+            q.run(1)
+        torch.cuda.synchronize()
+        ths = [threading.Thread(target=q.run, args=(args.steps,)) for q in cplans]
+        ce0, ce1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ce0.record()
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        torch.cuda.synchronize()
+        ce1.record()
+        ce1.synchronize()
+        csec = ce0.elapsed_time(ce1) * 1e-3
+        concurrent = {"solves_per_s": K * args.steps / csec, "plans": K,
+                      "note": "K identical solves in flight (pooled plans, own streams); not the headline"}
+        for q in cplans:
+            q.close()
+
     # ---------------- roofline of the dominant kernel
     # Algorithmic FP64 flops per launch (SURVEY §8(d) / Golub-Van Loan counts,
     # DESIGN.md §5); the stage times are CUDA events on the plan's stream.
@@ -807,6 +834,7 @@ def main():
                                        "boundary_fallback", "max_balance_residual", "max_particular_residual",
                                        "particular_extra_steps")},
         "parity": parity_record(gpu_table),
+        "concurrent": concurrent,
     }
     print(json.dumps(line), flush=True)
     if dist:

@@ -25,8 +25,9 @@ p.run(1)
 out["single_ms"] = p.run(steps) * 1e3
 p.close()
 for W in Ws:
-    plans = [V.Plan(mat, opts, nodes, w.n_dphi, device=0, m_begin=r, m_stride=W, n_orders=len(range(r, L, W)))
-             for r in range(W)]
+    # pooled plans, as the distributed layer uses them (the lean kernel builds)
+    plans = [V.Plan(mat, opts, nodes, w.n_dphi, device=0, m_begin=r, m_stride=W, n_orders=len(range(r, L, W)),
+                    pooled=True) for r in range(W)]
     alone = []
     for q in plans:
         q.run(1)
