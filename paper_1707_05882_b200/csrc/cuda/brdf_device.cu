@@ -235,6 +235,12 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
             ++tail;
         }
         pl.Be = std::max(1, pl.B - tail);  // at least one slot through the pipeline (no empty launches)
+        // the lean QR build only pays when concurrent plans of this size oversubscribe the
+        // SMs (a plan alone already fills half of them: 2 CTAs per matrix); small order
+        // shards keep the faster 229-register build
+        int dev = 0, sms = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        pl.lean = p->concurrent != 0 && 2 * pl.Be >= sms / 2;
     }
     const int N = pl.N, L = pl.L, d = pl.d, R = pl.R, G = pl.G, B = pl.B, NO = pl.NO;
     cudaStream_t st = pl.st;
@@ -287,7 +293,6 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     put(pl.post, p->post, (size_t)pl.n_in * 16);
     put(pl.trig, p->trig, (size_t)L * pl.n_dphi * 2);
     pl.out_lo = p->refl_top ? p->out_lo : 0;
-    pl.lean = p->concurrent != 0;
     pl.dump_kernel = p->dump_kernel;
     pl.dump_nu = p->dump_nu;
     pl.dump_residual = p->dump_residual;
