@@ -218,6 +218,14 @@ VRTE_API void vrte_cuda_debug_force_boundary_fallback(int32_t on);
  * right-hand sides (host arrays, row-major).  Returns 0, 3 (singular) or 5. */
 VRTE_API int32_t vrte_cuda_lu_solve(const double* A, int32_t G, int32_t batch, const double* B,
                                     int32_t ncol, double* X, int32_t device);
+/* Kernel-level check of the batched row-major LU factorization with partial
+ * pivoting (lu.cu), in place: A [batch][G][ncols] row-major, the columns past G
+ * eliminated along (augmented system); on return A holds L (unit lower, strictly
+ * below the diagonal) and U at the physical rows, perm [batch][G] the row of each
+ * position.  lookahead = 1 runs the boundary stage's one-block look-ahead
+ * schedule (two streams), 0 the serial one.  Returns 0, 3 (singular) or 5. */
+VRTE_API int32_t vrte_cuda_lu_factor(double* A, int32_t G, int32_t ncols, int32_t batch, int32_t lookahead,
+                                     int32_t* perm, int32_t device);
 /* Kernel-level check of the blocked Hessenberg reduction (hessenberg.cu):
  * A[b] = Q[b] H[b] Q[b]^T for `batch` column-major d x d matrices (host arrays).
  * blocked = 0 selects the unblocked reference kernel. */

@@ -152,7 +152,7 @@ EXPORTED = [
     "vrte_cuda_brdf", "vrte_cuda_plan_create", "vrte_cuda_plan_run", "vrte_cuda_plan_fetch",
     "vrte_cuda_plan_fetch_up", "vrte_cuda_plan_fetch_modes", "vrte_cuda_plan_fetch_ef",
     "vrte_cuda_plan_destroy",
-    "vrte_cuda_synthesize", "vrte_cuda_device_count", "vrte_cuda_current_device", "vrte_cuda_lu_solve", "vrte_cuda_hessenberg", "vrte_cuda_schur",
+    "vrte_cuda_synthesize", "vrte_cuda_device_count", "vrte_cuda_current_device", "vrte_cuda_lu_solve", "vrte_cuda_lu_factor", "vrte_cuda_hessenberg", "vrte_cuda_schur",
     "vrte_cuda_radiance_field", "vrte_cuda_mc_trace", "vrte_cuda_host_alloc", "vrte_cuda_host_free",
     "vrte_cuda_debug_force_boundary_fallback", "vrte_cuda_plan_up_device", "vrte_cuda_plan_synthesize_device",
     "vrte_cuda_plan_acquire", "vrte_cuda_plan_release", "vrte_brdf_plan_acquire", "vrte_cuda_schur_trace",
@@ -202,6 +202,7 @@ def lib():
     L.vrte_cuda_plan_destroy.argtypes = [vp]
     L.vrte_cuda_plan_fetch_ef.argtypes = [vp, dp, dp]
     L.vrte_cuda_lu_solve.argtypes = [dp, C.c_int32, C.c_int32, dp, C.c_int32, dp, C.c_int32]
+    L.vrte_cuda_lu_factor.argtypes = [dp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32]
     L.vrte_cuda_hessenberg.argtypes = [dp, C.c_int32, C.c_int32, dp, dp, C.c_int32, C.c_int32]
     L.vrte_cuda_debug_force_boundary_fallback.argtypes = [C.c_int32]
     L.vrte_cuda_debug_force_boundary_fallback.restype = None
@@ -249,6 +250,22 @@ def lu_solve(A, B, device: int = 0) -> np.ndarray:
     if code != 0:
         raise VrteError(code, "vrte_cuda_lu_solve failed (singular or bad arguments)")
     return X
+
+
+def lu_factor(A, G: int, lookahead: bool = True, device: int = 0):
+    """Batched in-place row-major LU (kernel-level check): A [batch, G, ncols]
+    (columns past G carried along) -> (factors at the physical rows, perm
+    [batch, G]: physical row of each position)."""
+    A = np.array(A, dtype=np.float64, order="C", copy=True)
+    batch, g, ncols = A.shape
+    if g != G:
+        raise ValueError("lu_factor: A must be [batch, G, ncols]")
+    perm = np.zeros((batch, G), dtype=np.int32)
+    code = lib().vrte_cuda_lu_factor(_dp(A), G, ncols, batch, int(bool(lookahead)),
+                                     perm.ctypes.data_as(C.POINTER(C.c_int32)), device)
+    if code != 0:
+        raise VrteError(code, "vrte_cuda_lu_factor failed (singular or bad arguments)")
+    return A, perm
 
 
 class forced_boundary_fallback:

@@ -86,9 +86,18 @@ void launch_copy_zp0(const BndArgs& a, cudaStream_t st);
 // (bnd_row_end); rows past a column block's profile are skipped.
 // lda: row stride (0 = G); ncols > G: the columns past G (right-hand sides of
 // an augmented system [A | B]) are carried through the elimination.
+// la (optional): look-ahead by one outer block -- the panels of block K+1 (and
+// the update of block K+1's columns) on the high-priority stream la->hi while the
+// rest of block K's trailing update runs on la->lo through a snapshot of the
+// row map; both fork from and join back into st.
+struct LuLookahead {
+    cudaStream_t hi = nullptr, lo = nullptr;
+    int* snap = nullptr;  // [batch][G]
+    cudaEvent_t ev[4] = {};
+};
 void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatus* status,
                   const int* order_index, cudaStream_t st, int prof_d = 0, int prof_P = 0, int lda = 0,
-                  int ncols = 0, cudaEvent_t cols_ready = nullptr);
+                  int ncols = 0, cudaEvent_t cols_ready = nullptr, const LuLookahead* la = nullptr);
 // Back substitution of an augmented factorization (ncols = G + R) in place, down
 // to row_lo (rounded down to a 64-row block); X [batch][G][R] receives rows >= that.
 void lu_backsolve_aug(double* A, int G, int lda, int R, int batch, const int* perm, double* X, int row_lo,

@@ -150,6 +150,8 @@ struct vrte_cuda_plan {
     cudaEvent_t ev[16] = {};
     cudaStream_t st2 = nullptr;          // side stream: independent work overlapped with the main chain
     cudaEvent_t fork[6] = {}, join[6] = {};
+    LuLookahead lula;  // the boundary factorization's look-ahead streams (lu.cu)
+    DevBuf<int> lu_snap;
     int refine_iters = 1;
     int refine_extra = 2;
     int* count_host = nullptr;  // page-locked: [0] eigen slots still refining, [1] particular slots
@@ -168,6 +170,10 @@ struct vrte_cuda_plan {
         for (auto* es : {fork, join})
             for (int i = 0; i < 6; ++i)
                 if (es[i]) cudaEventDestroy(es[i]);
+        for (auto& e : lula.ev)
+            if (e) cudaEventDestroy(e);
+        if (lula.hi) cudaStreamDestroy(lula.hi);
+        if (lula.lo) cudaStreamDestroy(lula.lo);
         if (st2) cudaStreamDestroy(st2);
         if (st) cudaStreamDestroy(st);
     }
@@ -202,6 +208,13 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     for (auto* es : {pl.fork, pl.join})
         for (int i = 0; i < 6; ++i)
             if (!es[i]) VRTE_CUDA_CHECK(cudaEventCreateWithFlags(&es[i], cudaEventDisableTiming));
+    if (!pl.lula.hi) {
+        int lo_prio = 0, hi_prio = 0;
+        VRTE_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+        VRTE_CUDA_CHECK(cudaStreamCreateWithPriority(&pl.lula.hi, cudaStreamNonBlocking, hi_prio));
+        VRTE_CUDA_CHECK(cudaStreamCreateWithPriority(&pl.lula.lo, cudaStreamNonBlocking, lo_prio));
+        for (auto& e : pl.lula.ev) VRTE_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     if (!pl.count_host) VRTE_CUDA_CHECK(cudaMallocHost(&pl.count_host, 2 * sizeof(int)));
     if (!pl.refine_host) VRTE_CUDA_CHECK(cudaMallocHost(&pl.refine_host, sizeof(int)));
     pl.counts.alloc(2);
@@ -362,6 +375,8 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pl.rhs_x.alloc((size_t)NO * R * G);
     pl.ipiv.alloc((size_t)NO * G);
     pl.perm.alloc((size_t)NO * G);
+    pl.lu_snap.alloc((size_t)NO * G);
+    pl.lula.snap = pl.lu_snap.p;
     pl.up.alloc((size_t)NO * R * d);
     pl.out.alloc((size_t)pl.n_in * (N - pl.out_lo) * pl.n_dphi * 16);
     pl.status_buf.alloc(1);
@@ -760,7 +775,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[11], st));
     const int K = ba.K, ldl = ba.ldl;
     lu_factor_rm(pl.lhs.p, G, NO, pl.ipiv.p, pl.perm.p, pl.status, pl.order_index.p, st, d, pl.P, ldl, G + R,
-                 pl.join[3]);
+                 pl.join[3], &pl.lula);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[12], st));
     if (pl.full_solution) {
         // radiance: every layer's coefficients, under the reference's exact gate
@@ -1601,6 +1616,46 @@ int32_t vrte_cuda_lu_solve(const double* A, int32_t G, int32_t batch, const doub
         DeviceStatus s{};
         VRTE_CUDA_CHECK(cudaMemcpyAsync(&s, dst.p, sizeof s, cudaMemcpyDeviceToHost, st));
         VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
+        cudaStreamDestroy(st);
+        return s.code != 0 ? 3 : 0;
+    } catch (const std::exception&) {
+        return 3;
+    }
+}
+
+int32_t vrte_cuda_lu_factor(double* A, int32_t G, int32_t ncols, int32_t batch, int32_t lookahead, int32_t* perm_out,
+                            int32_t device) {
+    if (!A || !perm_out || G < 1 || ncols < G || batch < 1) return 5;
+    try {
+        if (device >= 0) VRTE_CUDA_CHECK(cudaSetDevice(device));
+        cudaStream_t st;
+        VRTE_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        LuLookahead la;
+        int lo_prio = 0, hi_prio = 0;
+        VRTE_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+        VRTE_CUDA_CHECK(cudaStreamCreateWithPriority(&la.hi, cudaStreamNonBlocking, hi_prio));
+        VRTE_CUDA_CHECK(cudaStreamCreateWithPriority(&la.lo, cudaStreamNonBlocking, lo_prio));
+        for (auto& e : la.ev) VRTE_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        DevBuf<double> dA;
+        DevBuf<int> ipiv, perm, snap;
+        DevBuf<DeviceStatus> dst;
+        dA.upload(A, (size_t)batch * G * ncols, st);
+        ipiv.alloc((size_t)batch * G);
+        perm.alloc((size_t)batch * G);
+        snap.alloc((size_t)batch * G);
+        la.snap = snap.p;
+        dst.alloc(1);
+        VRTE_CUDA_CHECK(cudaMemsetAsync(dst.p, 0, sizeof(DeviceStatus), st));
+        lu_factor_rm(dA.p, G, batch, ipiv.p, perm.p, dst.p, nullptr, st, 0, 0, ncols, ncols, nullptr,
+                     lookahead ? &la : nullptr);
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(A, dA.p, sizeof(double) * dA.n, cudaMemcpyDeviceToHost, st));
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(perm_out, perm.p, sizeof(int) * perm.n, cudaMemcpyDeviceToHost, st));
+        DeviceStatus s{};
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(&s, dst.p, sizeof s, cudaMemcpyDeviceToHost, st));
+        VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
+        for (auto& e : la.ev) cudaEventDestroy(e);
+        cudaStreamDestroy(la.hi);
+        cudaStreamDestroy(la.lo);
         cudaStreamDestroy(st);
         return s.code != 0 ? 3 : 0;
     } catch (const std::exception&) {

@@ -569,11 +569,12 @@ int panel_width(int G) { return G <= 1024 ? 16 : (G <= 2048 ? 8 : 4); }
 
 template <bool LOWER>
 void trsm_launch(const double* A, int G, int lda, double* M, int ld, long long strideM, int k0, int jb, int c_lo,
-                 int c_hi, int batch, cudaStream_t st, const int* tmap, const int* mmap) {
+                 int c_hi, int batch, cudaStream_t st, const int* tmap, const int* mmap, int wide = -1) {
     if (jb <= 0 || c_hi <= c_lo) return;
     // wide right-hand sides (the factorization's U12 blocks): column-per-lane;
-    // narrow ones (the 256-column solves) keep enough CTAs with lanes over rows
-    const bool shfl = (c_hi - c_lo) < 512;
+    // narrow ones (the 256-column solves) keep enough CTAs with lanes over rows.
+    // (The two round differently: a split of one update passes the choice down.)
+    const bool shfl = wide < 0 ? (c_hi - c_lo) < 512 : wide == 0;
     if (shfl) {
         dim3 grid((c_hi - c_lo + SW_TILE - 1) / SW_TILE, batch);
         lu_trsm_rm_kernel<LOWER><<<grid, 256, 0, st>>>(A, G, lda, (long long)G * lda, M, ld, strideM, k0, jb, c_lo,
@@ -711,55 +712,116 @@ __global__ void __launch_bounds__(512) lu_few_solve_kernel(const double* Aall, i
 }
 }  // namespace
 
+namespace {
+// Outer block [K0, K0 + NBk) (rows to rend) applied to columns [c_lo, c_hi):
+// U12 = L11^-1 A12 on the block's pivot rows by 64-row halves, then the
+// trailing update A22 -= L21 U12 (rows past the profile have zero multipliers).
+// wide: the TRSM variant, chosen from the whole update's width (both pieces of a
+// split update must round alike).
+void block_update(double* A, int G, int lda, long long gg, const int* map, int K0, int NBk, int rend, int c_lo,
+                  int c_hi, int batch, cudaStream_t st, bool wide) {
+    const int nc = c_hi - c_lo;
+    if (nc <= 0) return;
+    for (int r0 = K0; r0 < K0 + NBk; r0 += LU_NB) {
+        const int rb = min(LU_NB, K0 + NBk - r0);
+        trsm_launch<true>(A, G, lda, A, lda, gg, r0, rb, c_lo, c_hi, batch, st, map, map, wide ? 1 : 0);
+        const int below = K0 + NBk - (r0 + rb);
+        if (below > 0)
+            rm_gemm(below, nc, rb, A + r0, lda, gg, A + c_lo, lda, gg, A + c_lo, lda, gg, batch, -1.0, 1.0, st,
+                    map + r0 + rb, map + r0, map + r0 + rb, G);
+    }
+    if (rend - K0 - NBk > 0)
+        rm_gemm(rend - K0 - NBk, nc, NBk, A + K0, lda, gg, A + c_lo, lda, gg, A + c_lo, lda, gg, batch, -1.0, 1.0, st,
+                map + K0 + NBk, map + K0, map + K0 + NBk, G);
+}
+
+void block_panels(double* A, int G, int lda, int* map, int* ipiv, int K0, int NBk, int rend, DeviceStatus* status,
+                  const int* order_index, int batch, cudaStream_t st) {
+    const int PB = panel_width(G);
+    for (int k0 = K0; k0 < K0 + NBk; k0 += PB) {
+        const int jb = min(PB, K0 + NBk - k0);
+        const int np = rend - k0;
+        if (PB == 16)
+            panel_dispatch<16>(np, A, G, lda, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
+        else if (PB == 8)
+            panel_dispatch<8>(np, A, G, lda, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
+        else
+            panel_dispatch<4>(np, A, G, lda, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
+    }
+}
+}  // namespace
+
 void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatus* status,
                   const int* order_index, cudaStream_t st, int prof_d, int prof_P, int lda, int ncols,
-                  cudaEvent_t cols_ready) {
+                  cudaEvent_t cols_ready, const LuLookahead* la) {
     if (G > 4096) throw std::invalid_argument("vrte_cuda: boundary system larger than 4096 rows");
     if (lda <= 0) lda = G;
     if (ncols <= 0) ncols = G;  // columns past G: right-hand sides eliminated along (augmented system)
-    const int PB = panel_width(G), OB = outer_block();
+    const int OB = outer_block();
     const long long gg = (long long)G * lda;
     int* map = perm;  // the row map IS the net permutation: row i of P A = row perm[i] of A
-    {
-        const long long total = (long long)batch * G;
-        lu_map_init_kernel<<<(unsigned)min(4096LL, (total + 255) / 256), 256, 0, st>>>(map, total, G);
-        VRTE_CUDA_CHECK(cudaGetLastError());
-    }
     auto row_end = [&](int col) { return prof_d > 0 ? min(G, bnd_row_end(col, prof_d, prof_P)) : G; };
-    for (int K0 = 0; K0 < G; K0 += OB) {
-        const int NBk = min(OB, G - K0);
-        const int rend = row_end(K0 + NBk - 1);  // profile is non-decreasing in the column
-        for (int k0 = K0; k0 < K0 + NBk; k0 += PB) {
-            const int jb = min(PB, K0 + NBk - k0);
-            const int np = rend - k0;
-            if (PB == 16)
-                panel_dispatch<16>(np, A, G, lda, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
-            else if (PB == 8)
-                panel_dispatch<8>(np, A, G, lda, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
-            else
-                panel_dispatch<4>(np, A, G, lda, map, ipiv, K0, k0, jb, rend, status, order_index, batch, st);
-        }
-        const int rest = ncols - K0 - NBk;
-        if (cols_ready) {  // the columns past G (right-hand sides) are written by another stream
-            VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, cols_ready, 0));
-            cols_ready = nullptr;
-        }
-        if (rest > 0) {
-            // U12 = L11^-1 A12 on the block's pivot rows, by 64-row halves
-            for (int r0 = K0; r0 < K0 + NBk; r0 += LU_NB) {
-                const int rb = min(LU_NB, K0 + NBk - r0);
-                trsm_launch<true>(A, G, lda, A, lda, gg, r0, rb, K0 + NBk, ncols, batch, st, map, map);
-                const int below = K0 + NBk - (r0 + rb);
-                if (below > 0)
-                    rm_gemm(below, rest, rb, A + r0, lda, gg, A + K0 + NBk, lda, gg, A + K0 + NBk, lda, gg, batch,
-                            -1.0, 1.0, st, map + r0 + rb, map + r0, map + r0 + rb, G);
+    auto map_init = [&](cudaStream_t s) {
+        const long long total = (long long)batch * G;
+        lu_map_init_kernel<<<(unsigned)min(4096LL, (total + 255) / 256), 256, 0, s>>>(map, total, G);
+        VRTE_CUDA_CHECK(cudaGetLastError());
+    };
+    if (!la || G <= OB) {
+        map_init(st);
+        for (int K0 = 0; K0 < G; K0 += OB) {
+            const int NBk = min(OB, G - K0);
+            const int rend = row_end(K0 + NBk - 1);  // profile is non-decreasing in the column
+            block_panels(A, G, lda, map, ipiv, K0, NBk, rend, status, order_index, batch, st);
+            if (cols_ready && ncols > K0 + NBk) {  // the columns past G (right-hand sides) come from another stream
+                VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, cols_ready, 0));
+                cols_ready = nullptr;
             }
-            // trailing update: rows past the profile have zero multipliers
-            if (rend - K0 - NBk > 0)
-                rm_gemm(rend - K0 - NBk, rest, NBk, A + K0, lda, gg, A + K0 + NBk, lda, gg, A + K0 + NBk, lda, gg,
-                        batch, -1.0, 1.0, st, map + K0 + NBk, map + K0, map + K0 + NBk, G);
+            block_update(A, G, lda, gg, map, K0, NBk, rend, K0 + NBk, ncols, batch, st, ncols - K0 - NBk >= 512);
         }
+        return;
     }
+    // Look-ahead by one block.  hi: panels(K), [wait rest(K-1)], map snapshot,
+    // update of block K+1's columns, panels(K+1), ...; lo: the update of the
+    // columns past block K+1 (the right-hand sides included) by block K, through
+    // the snapshot -- the panels of block K+1 permute the positions past block K
+    // while it runs, the snapshot keeps the set of rows block K's multipliers
+    // live in.  Each row is updated by exactly the same operations as without
+    // look-ahead, in the same order: the factors are bitwise identical.
+    cudaStream_t hi = la->hi, lo = la->lo;
+    VRTE_CUDA_CHECK(cudaEventRecord(la->ev[0], st));
+    VRTE_CUDA_CHECK(cudaStreamWaitEvent(hi, la->ev[0], 0));
+    VRTE_CUDA_CHECK(cudaStreamWaitEvent(lo, la->ev[0], 0));
+    if (cols_ready) VRTE_CUDA_CHECK(cudaStreamWaitEvent(lo, cols_ready, 0));
+    map_init(hi);
+    block_panels(A, G, lda, map, ipiv, 0, min(OB, G), row_end(min(OB, G) - 1), status, order_index, batch, hi);
+    bool rest_pending = false;
+    for (int K0 = 0; K0 < G; K0 += OB) {
+        const int NBk = min(OB, G - K0), c1 = K0 + NBk;
+        const int rend = row_end(c1 - 1);
+        const int nxt = min(OB, G - c1);  // block K+1's width (0: K is the last block)
+        const bool wide = ncols - c1 >= 512;
+        if (rest_pending) VRTE_CUDA_CHECK(cudaStreamWaitEvent(hi, la->ev[2], 0));
+        rest_pending = false;
+        if (nxt == 0) {  // last block: the right-hand sides only
+            if (cols_ready) VRTE_CUDA_CHECK(cudaStreamWaitEvent(hi, cols_ready, 0));
+            block_update(A, G, lda, gg, map, K0, NBk, rend, c1, ncols, batch, hi, wide);
+            break;
+        }
+        if (ncols > c1 + nxt) {
+            VRTE_CUDA_CHECK(cudaMemcpyAsync(la->snap, map, sizeof(int) * (size_t)batch * G, cudaMemcpyDeviceToDevice, hi));
+            VRTE_CUDA_CHECK(cudaEventRecord(la->ev[1], hi));
+            VRTE_CUDA_CHECK(cudaStreamWaitEvent(lo, la->ev[1], 0));
+            block_update(A, G, lda, gg, la->snap, K0, NBk, rend, c1 + nxt, ncols, batch, lo, wide);
+            VRTE_CUDA_CHECK(cudaEventRecord(la->ev[2], lo));
+            rest_pending = true;
+        }
+        block_update(A, G, lda, gg, map, K0, NBk, rend, c1, c1 + nxt, batch, hi, wide);
+        block_panels(A, G, lda, map, ipiv, c1, nxt, row_end(c1 + nxt - 1), status, order_index, batch, hi);
+    }
+    VRTE_CUDA_CHECK(cudaEventRecord(la->ev[3], lo));
+    VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, la->ev[3], 0));
+    VRTE_CUDA_CHECK(cudaEventRecord(la->ev[3], hi));
+    VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, la->ev[3], 0));
 }
 
 // Back substitution on an augmented factorization ([A | B] factored with

@@ -89,3 +89,26 @@ def test_qr_converges_through_underflowing_bulge():
     assert np.abs(Z[0] @ T[0] @ Z[0].T - H).max() < 1e-13
     ref = np.sort_complex(np.linalg.eigvals(H))
     assert np.abs(np.sort_complex(lam[0]) - ref).max() < 1e-12
+
+
+@pytest.mark.parametrize("G,ncols,batch", [(384, 384, 3), (1024, 1280, 4), (1000, 1100, 2), (2048, 2056, 1)])
+def test_lu_lookahead_schedule_is_bitwise_identical(G, ncols, batch):
+    """The boundary stage's look-ahead schedule (panels of block K+1 under the
+    rest of block K's trailing update, lu.cu) performs the same operations on
+    every row as the serial schedule: identical factors and row maps; and the
+    factors reproduce P A = L U on the augmented columns too."""
+    rng = np.random.default_rng(G + ncols)
+    A = rng.standard_normal((batch, G, ncols))
+    A *= np.exp(-rng.uniform(0, 6, (batch, G, 1)))
+    F1, p1 = V.lu_factor(A, G, lookahead=True)
+    F0, p0 = V.lu_factor(A, G, lookahead=False)
+    assert np.array_equal(p0, p1)
+    assert np.array_equal(F0, F1)
+    for b in range(batch):
+        P = F1[b][p1[b]]  # position order
+        Lm = np.tril(P[:, :G], -1) + np.eye(G)
+        U = np.triu(P[:, :G])
+        PA = A[b][p1[b]]
+        assert np.abs(Lm @ U - PA[:, :G]).max() <= 1e-13 * np.abs(A[b]).max() * np.sqrt(G)
+        if ncols > G:  # the carried columns hold L^-1 P B
+            assert np.abs(Lm @ P[:, G:] - PA[:, G:]).max() <= 1e-13 * np.abs(A[b]).max() * np.sqrt(G)
