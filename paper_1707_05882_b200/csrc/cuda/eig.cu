@@ -272,25 +272,24 @@ __device__ bool small_subdiag_g(const double* H, int d, int k, double ulp, doubl
         const double ab = fmax(hk, hup), ba = fmin(hk, hup);
         const double dif = fabs(hg(H, d, k - 1, k - 1) - hg(H, d, k, k));
         const double aa = fmax(fabs(hg(H, d, k, k)), dif), bb = fmin(fabs(hg(H, d, k, k)), dif);
-        const double s = aa + ab;
-        if (ba * (ab / s) <= fmax(smlnum, ulp * (bb * (aa / s)))) return true;
+        const double rs = 1.0 / (aa + ab);
+        if (ba * (ab * rs) <= fmax(smlnum, ulp * (bb * (aa * rs)))) return true;
     }
     return false;
 }
 
 __device__ void start_vector_g(const double* H, int d, int m, double rt1r, double rt1i, double rt2r,
                                double rt2i, double v[3]) {
+    // (dlaqr1; scalings by reciprocals -- one FP64 division on the chain instead of
+    // four: the reflector house3 builds from v does not depend on v's scale)
     double h21s = hg(H, d, m + 1, m);
-    double s = fabs(hg(H, d, m, m) - rt2r) + fabs(rt2i) + fabs(h21s);
-    h21s = hg(H, d, m + 1, m) / s;
-    v[0] = h21s * hg(H, d, m, m + 1) + (hg(H, d, m, m) - rt1r) * ((hg(H, d, m, m) - rt2r) / s) -
-           rt1i * (rt2i / s);
+    const double s = fabs(hg(H, d, m, m) - rt2r) + fabs(rt2i) + fabs(h21s);
+    const double rs = 1.0 / s;
+    h21s = hg(H, d, m + 1, m) * rs;
+    v[0] = h21s * hg(H, d, m, m + 1) + (hg(H, d, m, m) - rt1r) * ((hg(H, d, m, m) - rt2r) * rs) -
+           rt1i * (rt2i * rs);
     v[1] = h21s * (hg(H, d, m, m) + hg(H, d, m + 1, m + 1) - rt1r - rt2r);
     v[2] = h21s * hg(H, d, m + 2, m + 1);
-    s = fabs(v[0]) + fabs(v[1]) + fabs(v[2]);
-    v[0] /= s;
-    v[1] /= s;
-    v[2] /= s;
 }
 
 
@@ -327,7 +326,7 @@ __device__ inline void named_bar(int id, int nthreads) {
 // lane-parallel.
 __device__ void warp_tiny_eig(double* S, int n, double* sr, double* si) {
     const int lane = threadIdx.x & 31;
-    const double ulp = kUlp, smlnum = kSafeMin * ((double)n / ulp);
+    const double ulp = kUlp, smlnum = kSafeMin * ((double)n * (1.0 / kUlp));  // 1/ulp = 2^52: exact
     auto A = [&](int r, int c) -> double& { return S[r + c * TQ]; };
     int I = n - 1;
     int kdefl = 0;
@@ -375,10 +374,11 @@ __device__ void warp_tiny_eig(double* S, int n, double* sr, double* si) {
                 if (s == 0.0) {
                     rt1r = rt1i = rt2r = rt2i = 0.0;
                 } else {
-                    h11 /= s;
-                    h21 /= s;
-                    h12 /= s;
-                    h22 /= s;
+                    const double rs = 1.0 / s;
+                    h11 *= rs;
+                    h21 *= rs;
+                    h12 *= rs;
+                    h22 *= rs;
                     const double tr = (h11 + h22) / 2.0;
                     const double det = (h11 - tr) * (h22 - tr) - h12 * h21;
                     const double rtdisc = sqrt(fabs(det));
@@ -420,7 +420,7 @@ __device__ void warp_tiny_eig(double* S, int n, double* sr, double* si) {
                 const double t1 = house3(v1, v2, v3, bt);
                 v1 = bt;
                 const double t2 = t1 * v2, t3 = t1 * v3;
-                __syncwarp();
+                if (k == M) __syncwarp();  // the start vector read columns M, M+1 (k > M: column k-1 only)
                 const int c = k + lane;
                 if (c <= I) {
                     const double a0 = A(k, c), a1 = A(k + 1, c), a2 = nr == 3 ? A(k + 2, c) : 0.0;
@@ -478,7 +478,7 @@ __device__ void warp_tiny_eig(double* S, int n, double* sr, double* si) {
 // the eigenvalues by diagonal position.  Returns false if it did not converge.
 __device__ bool warp_small_schur(double* T, double* V, int n, double* sr, double* si) {
     const int lane = threadIdx.x & 31;
-    const double ulp = kUlp, smlnum = kSafeMin * ((double)n / ulp);
+    const double ulp = kUlp, smlnum = kSafeMin * ((double)n * (1.0 / kUlp));  // 1/ulp = 2^52: exact
     auto A = [&](int r, int c) -> double& { return T[r + c * LDW]; };
     int I = n - 1;
     int kdefl = 0;
@@ -524,10 +524,11 @@ __device__ bool warp_small_schur(double* T, double* V, int n, double* sr, double
                 if (s == 0.0) {
                     rt1r = rt1i = rt2r = rt2i = 0.0;
                 } else {
-                    h11 /= s;
-                    h21 /= s;
-                    h12 /= s;
-                    h22 /= s;
+                    const double rs = 1.0 / s;
+                    h11 *= rs;
+                    h21 *= rs;
+                    h12 *= rs;
+                    h22 *= rs;
                     const double tr = (h11 + h22) / 2.0;
                     const double det = (h11 - tr) * (h22 - tr) - h12 * h21;
                     const double rtdisc = sqrt(fabs(det));
@@ -569,7 +570,7 @@ __device__ bool warp_small_schur(double* T, double* V, int n, double* sr, double
                 const double t1 = house3(v1, v2, v3, bt);
                 v1 = bt;
                 const double t2 = t1 * v2, t3 = t1 * v3;
-                __syncwarp();
+                if (k == M) __syncwarp();  // the start vector read columns M, M+1 (k > M: column k-1 only)
                 const int c = k + lane;
                 if (c < n) {
                     const double a0 = A(k, c), a1 = A(k + 1, c), a2 = nr == 3 ? A(k + 2, c) : 0.0;
@@ -651,14 +652,28 @@ __device__ bool warp_small_schur(double* T, double* V, int n, double* sr, double
 // Householder reflector applied by one warp: x <- (I - tau v v^T) x on rows
 // [r0, r0+len) of the columns [c0, c1) of A (ld MW) -- left -- or on columns
 // [r0, r0+len) of the rows [c0, c1) -- right.  v[0] = 1 implicitly stored.
+// (the dot products in four interleaved partial sums, unrolled by four: the
+// loads are independent and the FMA chains a quarter as long)
+__device__ inline double strided_dot(const double* v, const double* x, long long st, int len) {
+    double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+    int q = 0;
+    for (; q + 3 < len; q += 4) {
+        w0 = fma(v[q], x[q * st], w0);
+        w1 = fma(v[q + 1], x[(q + 1) * st], w1);
+        w2 = fma(v[q + 2], x[(q + 2) * st], w2);
+        w3 = fma(v[q + 3], x[(q + 3) * st], w3);
+    }
+    for (; q < len; ++q) w0 = fma(v[q], x[q * st], w0);
+    return (w0 + w1) + (w2 + w3);
+}
 __device__ void warp_refl_left(double* A, int ld, const double* v, int len, double tau, int r0, int c0,
                                int c1) {
     const int lane = threadIdx.x & 31;
     for (int c = c0 + lane; c < c1; c += 32) {
-        double w = 0.0;
-        for (int q = 0; q < len; ++q) w = fma(v[q], A[(r0 + q) + c * ld], w);
-        w *= tau;
-        for (int q = 0; q < len; ++q) A[(r0 + q) + c * ld] -= w * v[q];
+        double* x = A + r0 + c * ld;
+        const double w = tau * strided_dot(v, x, 1, len);
+#pragma unroll 4
+        for (int q = 0; q < len; ++q) x[q] -= w * v[q];
     }
     __syncwarp();
 }
@@ -666,10 +681,10 @@ __device__ void warp_refl_right(double* A, int ld, const double* v, int len, dou
                                 int c1) {
     const int lane = threadIdx.x & 31;
     for (int r = c0 + lane; r < c1; r += 32) {
-        double w = 0.0;
-        for (int q = 0; q < len; ++q) w = fma(A[r + (r0 + q) * ld], v[q], w);
-        w *= tau;
-        for (int q = 0; q < len; ++q) A[r + (r0 + q) * ld] -= w * v[q];
+        double* x = A + r + r0 * ld;
+        const double w = tau * strided_dot(v, x, ld, len);
+#pragma unroll 4
+        for (int q = 0; q < len; ++q) x[q * ld] -= w * v[q];
     }
     __syncwarp();
 }
@@ -678,8 +693,7 @@ __device__ void warp_refl_right(double* A, int ld, const double* v, int len, dou
 __device__ double warp_dlarfg(double* v, int len, double* beta) {
     const int lane = threadIdx.x & 31;
     const double alpha = v[0];
-    double xn = 0.0;
-    for (int q = 1; q < len; ++q) xn = fma(v[q], v[q], xn);
+    const double xn = len > 1 ? strided_dot(v + 1, v + 1, 1, len - 1) : 0.0;
     __syncwarp();
     if (xn == 0.0) {
         *beta = alpha;
@@ -969,10 +983,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, MINB) hqr_multi
                     if (s == 0.0) {
                         rt1r = rt1i = rt2r = rt2i = 0.0;
                     } else {
-                        h11 /= s;
-                        h21 /= s;
-                        h12 /= s;
-                        h22 /= s;
+                        const double rs = 1.0 / s;
+                        h11 *= rs;
+                        h21 *= rs;
+                        h12 *= rs;
+                        h22 *= rs;
                         const double tr = (h11 + h22) / 2.0;
                         const double det = (h11 - tr) * (h22 - tr) - h12 * h21;
                         const double rtdisc = sqrt(fabs(det));
