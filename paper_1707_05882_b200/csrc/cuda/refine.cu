@@ -127,10 +127,13 @@ __global__ void normalize_kernel(RefineArgs a) {
         }
     }
     const cplx vs = bi < d ? ld(a.psi_p, m.cb, d, m.pair, bi) : ld(a.psi_m, m.cb, d, m.pair, bi - d);
+    const cplx rvs = cdiv(cmk(1.0, 0.0), vs);  // one complex division per mode, not per element
     __syncwarp();
     for (int i = lane; i < d; i += 32) {
-        const cplx p = cdiv(ld(a.psi_p, m.cb, d, m.pair, i), vs);
-        const cplx q = cdiv(ld(a.psi_m, m.cb, d, m.pair, i), vs);
+        cplx p = ld(a.psi_p, m.cb, d, m.pair, i) * rvs;
+        cplx q = ld(a.psi_m, m.cb, d, m.pair, i) * rvs;
+        if (i == bi) p = cmk(1.0, 0.0);  // the normalized component is exactly 1
+        if (i + d == bi) q = cmk(1.0, 0.0);
         st(a.psi_p, m.cb, d, m.pair, i, p);
         st(a.psi_m, m.cb, d, m.pair, i, q);
         st(a.ab_sum, m.cb, d, m.pair, i, a.mdiag[i] * (p + q));
@@ -206,10 +209,10 @@ __global__ void update_kernel(RefineArgs a) {
     const int d = m.d;
     const cplx s = (1.0 + a.shift[m.vb + m.j]) * cmk(a.rho[2 * (m.vb + m.j)], a.rho[2 * (m.vb + m.j) + 1]);
     const int si = a.sidx[m.vb + m.j];
-    auto unfold = [&](size_t cb, int i, cplx& p, cplx& q) {
-        const double im = 1.0 / a.mdiag[i];
+    const cplx rs = cdiv(cmk(1.0, 0.0), s);  // one complex division per mode
+    auto unfold = [&](size_t cb, int i, double im, cplx& p, cplx& q) {
         const cplx ut = ld(a.UT, cb, d, m.pair, i);
-        const cplx tt = cdiv(ld(a.EU, cb, d, m.pair, i) + ld(a.BE, cb, d, m.pair, i), s);
+        const cplx tt = (ld(a.EU, cb, d, m.pair, i) + ld(a.BE, cb, d, m.pair, i)) * rs;
         const cplx u = im * ut, t = cmk(-im * tt.re, -im * tt.im);
         p = 0.5 * (u + t);
         q = 0.5 * (u - t);
@@ -217,9 +220,10 @@ __global__ void update_kernel(RefineArgs a) {
     cplx as, bs;
     {
         const int i = si < d ? si : si - d;
+        const double im = 1.0 / a.mdiag[i];
         cplx ap, aq, bp, bq;
-        unfold(m.cb2, i, ap, aq);
-        unfold(setb(m), i, bp, bq);
+        unfold(m.cb2, i, im, ap, aq);
+        unfold(setb(m), i, im, bp, bq);
         as = si < d ? ap : aq;
         bs = si < d ? bp : bq;
     }
@@ -227,9 +231,10 @@ __global__ void update_kernel(RefineArgs a) {
     bool fin = isfinite(dr.re) && isfinite(dr.im);
     if (!fin) return;  // keep the current pair (the reference's `break` on non-finite)
     for (int i = lane; i < d; i += 32) {
+        const double im = 1.0 / a.mdiag[i];
         cplx ap, aq, bp, bq;
-        unfold(m.cb2, i, ap, aq);
-        unfold(setb(m), i, bp, bq);
+        unfold(m.cb2, i, im, ap, aq);
+        unfold(setb(m), i, im, bp, bq);
         const cplx p = ld(a.psi_p, m.cb, d, m.pair, i), q = ld(a.psi_m, m.cb, d, m.pair, i);
         st(a.psi_p, m.cb, d, m.pair, i, p - bp + dr * ap);
         st(a.psi_m, m.cb, d, m.pair, i, q - bq + dr * aq);
