@@ -38,81 +38,126 @@ struct ModeView {
 __device__ inline cplx dflip(cplx v, int i) { return ((i & 3) >= 2) ? cmk(-v.re, -v.im) : v; }
 __device__ inline cplx att_of(double tau, cplx nu) { return cexp_(cdiv(cmk(-tau, 0.0), nu)); }
 
-// Thread per (order mo, layer p, row i, packed column jj); the system is stored
-// ROW-major (lu.cu), lhs[mo][r * G + c].
-__global__ void assemble_kernel(BndArgs a) {
-    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+// CTA per (order mo, layer p, 32 x 32 tile of (mode component i, packed column
+// jj)); the system is stored ROW-major (lu.cu), lhs[mo][r * ldl + c].  The mode
+// vectors are read along i (coalesced, column-major storage) into shared
+// memory, the per-mode attenuation exp(-tau/nu) is computed once per column,
+// and the system rows are written along jj (coalesced, row-major).
+constexpr int AT = 32;  // tile edge
+__global__ void __launch_bounds__(256) assemble_kernel(BndArgs a) {
+    __shared__ double s_pr[AT][AT + 1], s_pi[AT][AT + 1], s_mr[AT][AT + 1], s_mi[AT][AT + 1];  // [jj][i]
+    __shared__ double s_ar[AT], s_ai[AT];
+    __shared__ int s_im[AT];
     const int d = a.d, P = a.p.n_layers, G = 2 * d * P;
-    const long long total = (long long)a.p.n_orders * P * d * d;
-    if (idx >= total) return;
-    const int jj = (int)(idx % d);
-    const int i = (int)((idx / d) % d);
-    const int p = (int)((idx / ((long long)d * d)) % P);
-    const int mo = (int)(idx / ((long long)d * d * P));
+    const int jj0 = blockIdx.x * AT, i0 = blockIdx.y * AT;
+    const int p = blockIdx.z % P, mo = blockIdx.z / P;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
     const size_t om = (size_t)a.p.medium[p] * a.p.n_orders + mo;
-    const ModeView mv{a.psi_p, a.psi_m, a.nu, a.wi, d};
-    cplx pp, pm, nu;
-    bool imc;
-    mv.load(om, jj, i, pp, pm, nu, imc);
-    const cplx att = att_of(a.p.tau[p], nu);
-    auto pk = [&](cplx v) { return imc ? v.im : v.re; };
+    const size_t vb = om * d;
+    if (ty == 0) {
+        const int jj = jj0 + tx;
+        cplx att = cmk(0.0, 0.0);
+        int imc = 0;
+        if (jj < d) {
+            const double w = a.wi[vb + jj];
+            const int j = (w < 0.0) ? jj - 1 : jj;
+            imc = w < 0.0;
+            att = att_of(a.p.tau[p], cmk(a.nu[2 * (vb + j)], a.nu[2 * (vb + j) + 1]));
+        }
+        s_ar[tx] = att.re;
+        s_ai[tx] = att.im;
+        s_im[tx] = imc;
+    }
+    // read: lanes along i
+    for (int q = ty; q < AT; q += 8) {
+        const int jj = jj0 + q, i = i0 + tx;
+        double pr = 0.0, pi = 0.0, mr = 0.0, mi = 0.0;
+        if (jj < d && i < d) {
+            const double w = a.wi[vb + jj];
+            const int j = (w < 0.0) ? jj - 1 : jj;
+            const size_t cb = om * d * d + (size_t)j * d;
+            pr = a.psi_p[cb + i];
+            mr = a.psi_m[cb + i];
+            if (w != 0.0) {
+                pi = a.psi_p[cb + d + i];
+                mi = a.psi_m[cb + d + i];
+            }
+        }
+        s_pr[q][tx] = pr;
+        s_pi[q][tx] = pi;
+        s_mr[q][tx] = mr;
+        s_mi[q][tx] = mi;
+    }
+    __syncthreads();
+    auto pk = [&](cplx v, int q) { return s_im[q] ? v.im : v.re; };
+    // tau = 0 stacks of the top layer: T0[mo][jj][i] (column-major in jj), lanes along i
+    if (p == 0) {
+        double* T0 = a.top0 + (size_t)mo * d * 2 * d;
+        for (int q = ty; q < AT; q += 8) {
+            const int jj = jj0 + q, i = i0 + tx;
+            if (jj >= d || i >= d) continue;
+            const cplx pp = cmk(s_pr[q][tx], s_pi[q][tx]), pm = cmk(s_mr[q][tx], s_mi[q][tx]);
+            const cplx att = cmk(s_ar[q], s_ai[q]);
+            T0[(size_t)jj * d + i] = pk(pp, q);
+            T0[(size_t)(d + jj) * d + i] = pk(att * pm, q);
+        }
+    }
+    // write: lanes along jj (the system's columns)
     double* A = a.lhs + (size_t)mo * a.sl;
+    double* A0 = a.lhs0 ? a.lhs0 + (size_t)mo * a.sl : nullptr;
+    const int jj = jj0 + tx, q = tx;
+    if (jj >= d) return;
     const int ca = bnd_col(p, jj, d, G);       // column A_p(jj)
     const int cbk = bnd_col(p, d + jj, d, G);  // column B_p(jj)
-    double* A0 = a.lhs0 ? a.lhs0 + (size_t)mo * a.sl : nullptr;
-    struct Ref {  // writes the factored system and its untouched copy
-        double* x;
-        double* y;
-        __device__ void operator=(double v) const {
-            *x = v;
-            if (y) *y = v;
-        }
-    };
-    auto at = [&](int r, int c) -> Ref {
+    const cplx att = cmk(s_ar[q], s_ai[q]);
+    auto put = [&](int r, int c, double v) {
         const size_t o = (size_t)bnd_row(r, d, G) * a.ldl + c;
-        return Ref{A + o, A0 ? A0 + o : nullptr};
+        A[o] = v;
+        if (A0) A0[o] = v;
     };
-    if (p == 0) {
-        if (a.p.refl_top) {
-            // Fresnel interface (extension): top rows are down - R up = 0, R the
-            // interface reflection of node i/4 applied to the upward Stokes vector
-            const double* Rm = a.p.refl_top + (size_t)(i >> 2) * 16 + 4 * (i & 3);
-            cplx ua = cmk(0.0, 0.0), ub = cmk(0.0, 0.0);
-            for (int q = 0; q < 4; ++q) {
-                cplx ppq, pmq, nuq;
-                bool imq;
-                mv.load(om, jj, (i & ~3) + q, ppq, pmq, nuq, imq);
-                ua = ua + Rm[q] * ppq;
-                ub = ub + Rm[q] * (att * pmq);
+    for (int ii = ty; ii < AT; ii += 8) {
+        const int i = i0 + ii;
+        if (i >= d) break;
+        const cplx pp = cmk(s_pr[q][ii], s_pi[q][ii]), pm = cmk(s_mr[q][ii], s_mi[q][ii]);
+        if (p == 0) {
+            if (a.p.refl_top) {
+                // Fresnel interface (extension): top rows are down - R up = 0, R the
+                // interface reflection of node i/4 applied to the upward Stokes vector
+                const double* Rm = a.p.refl_top + (size_t)(i >> 2) * 16 + 4 * (i & 3);
+                const int g0 = ii & ~3;
+                cplx ua = cmk(0.0, 0.0), ub = cmk(0.0, 0.0);
+                for (int k = 0; k < 4; ++k) {
+                    const cplx ppk = cmk(s_pr[q][g0 + k], s_pi[q][g0 + k]);
+                    const cplx pmk = cmk(s_mr[q][g0 + k], s_mi[q][g0 + k]);
+                    ua = ua + Rm[k] * ppk;
+                    ub = ub + Rm[k] * (att * pmk);
+                }
+                put(i, ca, pk(dflip(pm, i) - ua, q));
+                put(i, cbk, pk(att * dflip(pp, i) - ub, q));
+            } else {
+                put(i, ca, pk(dflip(pm, i), q));
+                put(i, cbk, pk(att * dflip(pp, i), q));
             }
-            at(i, ca) = pk(dflip(pm, i) - ua);
-            at(i, cbk) = pk(att * dflip(pp, i) - ub);
-        } else {
-            at(i, ca) = pk(dflip(pm, i));
-            at(i, cbk) = pk(att * dflip(pp, i));
         }
-        double* T0 = a.top0 + (size_t)mo * d * 2 * d;
-        T0[(size_t)jj * d + i] = pk(pp);
-        T0[(size_t)(d + jj) * d + i] = pk(att * pm);
-    }
-    if (p < P - 1) {
-        const int ru = d + 2 * d * p;
-        at(ru + i, ca) = pk(att * pp);
-        at(ru + d + i, ca) = pk(att * dflip(pm, i));
-        at(ru + i, cbk) = pk(pm);
-        at(ru + d + i, cbk) = pk(dflip(pp, i));
-    }
-    if (p > 0) {
-        const int ru = d + 2 * d * (p - 1);
-        at(ru + i, ca) = -pk(pp);
-        at(ru + d + i, ca) = -pk(dflip(pm, i));
-        at(ru + i, cbk) = -pk(att * pm);
-        at(ru + d + i, cbk) = -pk(att * dflip(pp, i));
-    }
-    if (p == P - 1) {
-        const int rb = d + 2 * d * (P - 1);
-        at(rb + i, ca) = pk(att * pp);
-        at(rb + i, cbk) = pk(pm);
+        if (p < P - 1) {
+            const int ru = d + 2 * d * p;
+            put(ru + i, ca, pk(att * pp, q));
+            put(ru + d + i, ca, pk(att * dflip(pm, i), q));
+            put(ru + i, cbk, pk(pm, q));
+            put(ru + d + i, cbk, pk(dflip(pp, i), q));
+        }
+        if (p > 0) {
+            const int ru = d + 2 * d * (p - 1);
+            put(ru + i, ca, -pk(pp, q));
+            put(ru + d + i, ca, -pk(dflip(pm, i), q));
+            put(ru + i, cbk, -pk(att * pm, q));
+            put(ru + d + i, cbk, -pk(att * dflip(pp, i), q));
+        }
+        if (p == P - 1) {
+            const int rb = d + 2 * d * (P - 1);
+            put(rb + i, ca, pk(att * pp, q));
+            put(rb + i, cbk, pk(pm, q));
+        }
     }
 }
 
@@ -634,8 +679,8 @@ void launch_bnd_add(const BndArgs& a, double* X, const double* dX, int G, int R,
 void launch_bnd_assemble(const BndArgs& a, cudaStream_t st) {
     const int d = a.d, P = a.p.n_layers, G = 2 * d * P;
     VRTE_CUDA_CHECK(cudaMemsetAsync(a.lhs, 0, sizeof(double) * (size_t)a.p.n_orders * a.sl, st));
-    const long long total = (long long)a.p.n_orders * P * d * d;
-    assemble_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(a);
+    const dim3 grid((d + AT - 1) / AT, (d + AT - 1) / AT, (unsigned)(a.p.n_orders * P));
+    assemble_kernel<<<grid, 256, 0, st>>>(a);
     VRTE_CUDA_CHECK(cudaGetLastError());
     const bool active = a.p.base_type != 0 && !(a.p.base_type == 1 && a.p.rho == 0.0);
     if (active) {

@@ -11,70 +11,102 @@
 namespace vrte {
 namespace {
 
-// wigner.cpp:11-27
-__device__ double wigner_start(int m, int n, double x) {
+// wigner.cpp:11-27: d^lmin_{m n}(x) = exp(lf) 2^-lmin (1-x)^{|m-n|/2} (1+x)^{|m+n|/2},
+// lf = (1/2) log((2 lmin)! / (|m-n|! |m+n|!)) -- the x-independent part once per (m, n)
+// (one warp: the lanes sum strided terms, then a butterfly)
+__device__ double wigner_logfac(int m, int n) {
+    const int lane = threadIdx.x & 31;
     const int lmin = max(abs(m), abs(n));
     const int a = abs(m - n), b = abs(m + n);
     double lf = 0.0;
-    for (int k = 2; k <= 2 * lmin; ++k) lf += log((double)k);
-    for (int k = 2; k <= a; ++k) lf -= log((double)k);
-    for (int k = 2; k <= b; ++k) lf -= log((double)k);
-    double v = exp(0.5 * lf - lmin * log(2.0));
+    for (int k = 2 + lane; k <= 2 * lmin; k += 32) lf += log((double)k);
+    for (int k = 2 + lane; k <= a; k += 32) lf -= log((double)k);
+    for (int k = 2 + lane; k <= b; k += 32) lf -= log((double)k);
+    lf = warp_sum(lf);
+    return 0.5 * lf - lmin * log(2.0);
+}
+__device__ double wigner_start(int m, int n, double x, double lf) {
+    const int a = abs(m - n), b = abs(m + n);
+    double v = exp(lf);
     v *= pow(fmax(0.0, 1.0 - x), 0.5 * a) * pow(fmax(0.0, 1.0 + x), 0.5 * b);
     if (n < m && ((m - n) & 1)) v = -v;
     return v;
 }
 
-// One thread per (m, mu): the three d^l_{m n} sequences (n = 0, 2, -2) by the
-// upward recurrence (wigner.cpp:31-62), combined into P, R, T (wigner.cpp:64-81).
+// CTA per order m, thread per mu: the three d^l_{m n} sequences (n = 0, 2, -2) by
+// the upward recurrence (wigner.cpp:31-62), combined into P, R, T
+// (wigner.cpp:64-81).  The recurrence coefficients depend on (l, m, n) only:
+// tabulated once per CTA in shared memory as
+//   d^{l}= (ca x + cb) d^{l-1} - cc d^{l-2},  ca = (2l-1)(l-1) l / c0,
+//   cb = -(2l-1) m n / c0,  cc = l sqrt(((l-1)^2 - m^2)((l-1)^2 - n^2)) / c0,
+//   c0 = (l-1) sqrt((l^2 - m^2)(l^2 - n^2)),
+// so each step is three FMAs instead of two square roots and a division.
 // Output layout: out[((m*Lc + l)*3 + {P,R,T})*ld + mu_index], l < Lc (coefficient count).
 __global__ void gsf_kernel(int n_m, int L, int count, const double* __restrict__ mus,
                            double sign_mu, double* __restrict__ out, int ld) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= n_m * count) return;
-    const int m = idx / count, iu = idx % count;
-    const double x = sign_mu * mus[iu];
+    extern __shared__ double coef[];  // [L][3][3]: ca, cb, cc per (l, q)
+    __shared__ double s_lf[3];
+    const int m = blockIdx.x;
+    const int ns[3] = {0, 2, -2};
+    for (int e = threadIdx.x; e < 3 * L; e += blockDim.x) {
+        const int l = e / 3, q = e % 3, n = ns[q];
+        const int lm = l - 1;
+        double ca = 0.0, cb = 0.0, cc = 0.0;
+        if (lm >= 1 && l > max(m, abs(n))) {
+            const double lp = l;
+            const double c0 = lm * sqrt((lp * lp - (double)m * m) * (lp * lp - (double)n * n));
+            const double rc0 = 1.0 / c0;
+            ca = (2.0 * lm + 1.0) * (lm * lp) * rc0;
+            cb = -(2.0 * lm + 1.0) * ((double)m * n) * rc0;
+            cc = lp * sqrt(((double)lm * lm - (double)m * m) * ((double)lm * lm - (double)n * n)) * rc0;
+        }
+        coef[e * 3 + 0] = ca;
+        coef[e * 3 + 1] = cb;
+        coef[e * 3 + 2] = cc;
+    }
+    if (threadIdx.x < 96) {  // warp q: the start value's factorial part for n = ns[q]
+        const double lf = wigner_logfac(m, ns[threadIdx.x >> 5]);
+        if ((threadIdx.x & 31) == 0) s_lf[threadIdx.x >> 5] = lf;
+    }
+    __syncthreads();
     const int lmax = L - 1;
     const double sgn = (m & 1) ? -1.0 : 1.0;
-    // three independent recurrences advanced together
-    const int ns[3] = {0, 2, -2};
-    double prev[3], cur[3];
-    int lmin[3];
-    for (int q = 0; q < 3; ++q) {
-        lmin[q] = max(m, abs(ns[q]));
-        prev[q] = 0.0;
-        cur[q] = (lmin[q] <= lmax) ? wigner_start(m, ns[q], x) : 0.0;
-    }
-    for (int l = 0; l <= lmax; ++l) {
-        double dv[3];
+    for (int iu = threadIdx.x; iu < count; iu += blockDim.x) {
+        const double x = sign_mu * mus[iu];
+        // three independent recurrences advanced together
+        double prev[3], cur[3];
+        int lmin[3];
         for (int q = 0; q < 3; ++q) {
-            if (l < lmin[q]) {
-                dv[q] = 0.0;
-            } else if (l == lmin[q]) {
-                dv[q] = cur[q];
-            } else {
-                // advance from l-1 to l
-                const int n = ns[q];
-                const int lm = l - 1;
-                double next;
-                if (lm == 0) {
-                    next = x;
-                } else {
-                    const double lp = lm + 1.0;
-                    const double c0 = lm * sqrt((lp * lp - (double)m * m) * (lp * lp - (double)n * n));
-                    const double c1 = (2.0 * lm + 1.0) * (lm * lp * x - (double)m * n);
-                    const double c2 = lp * sqrt(((double)lm * lm - (double)m * m) * ((double)lm * lm - (double)n * n));
-                    next = (c1 * cur[q] - c2 * prev[q]) / c0;
-                }
-                prev[q] = cur[q];
-                cur[q] = next;
-                dv[q] = next;
-            }
+            lmin[q] = max(m, abs(ns[q]));
+            prev[q] = 0.0;
+            cur[q] = (lmin[q] <= lmax) ? wigner_start(m, ns[q], x, s_lf[q]) : 0.0;
         }
-        const size_t base = ((size_t)m * L + l) * 3;
-        out[(base + 0) * ld + iu] = sgn * dv[0];
-        out[(base + 1) * ld + iu] = 0.5 * sgn * (dv[1] + dv[2]);
-        out[(base + 2) * ld + iu] = -0.5 * sgn * (dv[1] - dv[2]);
+        for (int l = 0; l <= lmax; ++l) {
+            double dv[3];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                if (l < lmin[q]) {
+                    dv[q] = 0.0;
+                } else if (l == lmin[q]) {
+                    dv[q] = cur[q];
+                } else {
+                    double next;
+                    if (l == 1) {
+                        next = x;
+                    } else {
+                        const double* c = coef + (l * 3 + q) * 3;
+                        next = fma(fma(c[0], x, c[1]), cur[q], -c[2] * prev[q]);
+                    }
+                    prev[q] = cur[q];
+                    cur[q] = next;
+                    dv[q] = next;
+                }
+            }
+            const size_t base = ((size_t)m * L + l) * 3;
+            out[(base + 0) * ld + iu] = sgn * dv[0];
+            out[(base + 1) * ld + iu] = 0.5 * sgn * (dv[1] + dv[2]);
+            out[(base + 2) * ld + iu] = -0.5 * sgn * (dv[1] - dv[2]);
+        }
     }
 }
 
@@ -238,8 +270,12 @@ __global__ void beam_source_kernel(const ProblemDev p, const double* __restrict_
 
 void launch_gsf(const ProblemDev& p, const double* mus, int count, double sign, double* out,
                 cudaStream_t st) {
-    const int total = p.L * count;
-    gsf_kernel<<<(total + 127) / 128, 128, 0, st>>>(p.L, p.Lc, count, mus, sign, out, count);
+    const size_t smem = (size_t)9 * p.Lc * sizeof(double);
+    if (smem > 48 * 1024) {
+        static unsigned long long attr = 0;
+        smem_attr_once(gsf_kernel, 200 * 1024, attr);
+    }
+    gsf_kernel<<<p.L, 128, smem, st>>>(p.L, p.Lc, count, mus, sign, out, count);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
