@@ -326,7 +326,8 @@ __global__ void __launch_bounds__(256) lu_trsm_rm_kernel(const double* Aall, int
                                                          int jb, int c_lo, int c_hi, const int* tmap_all,
                                                          const int* mmap_all) {
     __shared__ double Ts[LU_NB][LU_NB + 1];
-    __shared__ int s_mrow[LU_NB];
+    __shared__ double s_rd[LU_NB];
+    __shared__ int s_trow[LU_NB], s_mrow[LU_NB];
     const int b = blockIdx.y, t = threadIdx.x, lane = t & 31, w = t >> 5;
     const int col0 = c_lo + blockIdx.x * SW_TILE;
     if (col0 >= c_hi) return;
@@ -339,15 +340,20 @@ __global__ void __launch_bounds__(256) lu_trsm_rm_kernel(const double* Aall, int
     long long tr[5];
     tr[0] = clock64();
 #endif
-    for (int r = w; r < jb; r += 8) {
-        const double* src = A + (size_t)(tmap ? tmap[k0 + r] : k0 + r) * lda + k0;
-        for (int cc = lane; cc < jb; cc += 32) Ts[r][cc] = src[cc];
-        if (lane == 0) s_mrow[r] = mmap ? mmap[k0 + r] : k0 + r;
+    if (t < jb) {
+        s_trow[t] = tmap ? tmap[k0 + t] : k0 + t;
+        s_mrow[t] = mmap ? mmap[k0 + t] : k0 + t;
     }
     __syncthreads();
-#ifdef VRTE_LU_TRACE
-    tr[1] = clock64();
-#endif
+    // every global load of the prologue in flight before the first is consumed
+    // (the triangle: 16 entries per thread; the M rows: 8)
+    constexpr int TQN = LU_NB * LU_NB / 256;
+    double tv[TQN];
+#pragma unroll
+    for (int q = 0; q < TQN; ++q) {
+        const int e = t + 256 * q, r = e / LU_NB, cc = e % LU_NB;
+        tv[q] = (r < jb && cc < jb) ? A[(size_t)s_trow[r] * lda + k0 + cc] : 0.0;
+    }
     // lane rows r0, r1; the warp's 4 consecutive columns (one 32-byte sector per row)
     const int r0 = lane, r1 = lane + 32, cw = col0 + w * 4;
     double x0[4], x1[4];
@@ -359,8 +365,16 @@ __global__ void __launch_bounds__(256) lu_trsm_rm_kernel(const double* Aall, int
         x0[q] = (r0 < jb && lv[q]) ? M[m0 + cw + q] : 0.0;
         x1[q] = (r1 < jb && lv[q]) ? M[m1 + cw + q] : 0.0;
     }
+#pragma unroll
+    for (int q = 0; q < TQN; ++q) {
+        const int e = t + 256 * q;
+        Ts[e / LU_NB][e % LU_NB] = tv[q];
+    }
+    __syncthreads();
+    if (!LOWER && t < jb) s_rd[t] = 1.0 / Ts[t][t];
+    if (!LOWER) __syncthreads();
 #ifdef VRTE_LU_TRACE
-    tr[2] = clock64();
+    tr[1] = tr[2] = clock64();
 #endif
     if (LOWER) {
         for (int j = 0; j < jb; ++j) {
@@ -377,7 +391,7 @@ __global__ void __launch_bounds__(256) lu_trsm_rm_kernel(const double* Aall, int
     } else {
         for (int j = jb - 1; j >= 0; --j) {
             const int src = j & 31;
-            const double rd = 1.0 / Ts[j][j];
+            const double rd = s_rd[j];
             const double u0 = (r0 < j) ? Ts[r0][j] : 0.0;
             const double u1 = (r1 < j) ? Ts[r1][j] : 0.0;
 #pragma unroll
