@@ -91,13 +91,19 @@ __global__ void __launch_bounds__(HNT) hess_panel_kernel(double* Aall, double* V
         double ss = 0.0;
         for (int r = k + 2 + t; r < d; r += HNT) ss = fma(col[r], col[r], ss);
         ss = block_sum_h(ss, red);
-        const double alpha = col[k + 1];
-        const double xnorm = sqrt(ss);
-        double tau = 0.0, beta = alpha, scal = 0.0;
-        if (xnorm != 0.0) {
-            beta = -copysign(hypot(alpha, xnorm), alpha);
-            tau = (beta - alpha) / beta;
-            scal = 1.0 / (alpha - beta);
+        // the reflector's scalars only in the threads that use them (rows < d,
+        // and the T column's t < j): 32 warps of redundant FP64 division /
+        // square-root sequences would queue on the SM's FP64 pipe
+        double tau = 0.0, beta = 0.0, scal = 0.0;
+        if (t < d) {
+            const double alpha = col[k + 1];
+            const double xnorm = sqrt(ss);
+            beta = alpha;
+            if (xnorm != 0.0) {
+                beta = -copysign(hypot(alpha, xnorm), alpha);
+                tau = (beta - alpha) / beta;
+                scal = 1.0 / (alpha - beta);
+            }
         }
         double* vj = Vs + (size_t)j * d;
         for (int r = t; r < d; r += HNT) {
@@ -128,6 +134,13 @@ __global__ void __launch_bounds__(HNT) hess_panel_kernel(double* Aall, double* V
                 double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                 const double* ap = A + r;
                 int c = ca;
+                for (; c + 15 < ce; c += 16) {  // 16 loads in flight per thread
+                    double x[16];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) x[q] = ap[(size_t)(c + q) * d];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) a[q & 7] = fma(x[q], vj[c + q], a[q & 7]);
+                }
                 for (; c + 7 < ce; c += 8) {
 #pragma unroll
                     for (int q = 0; q < 8; ++q) a[q] = fma(ap[(size_t)(c + q) * d], vj[c + q], a[q]);
