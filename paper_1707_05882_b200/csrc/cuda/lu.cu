@@ -627,6 +627,24 @@ __device__ inline void few_matvec(const double* A, int lda, const int* perm, dou
 #pragma unroll
             for (int c = 0; c < K; ++c) acc[q][c] = 0.0;
         int j = j0 + lane;
+        for (; j + 96 < j1; j += 128) {  // 4 rows x 4 loads in flight per lane
+            double a0[4], a1[4], a2[4], a3[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                a0[q] = row[q][j];
+                a1[q] = row[q][j + 32];
+                a2[q] = row[q][j + 64];
+                a3[q] = row[q][j + 96];
+            }
+#pragma unroll
+            for (int c = 0; c < K; ++c) {
+                const double x0 = x[j * K + c], x1 = x[(j + 32) * K + c];
+                const double x2 = x[(j + 64) * K + c], x3 = x[(j + 96) * K + c];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    acc[q][c] = fma(a3[q], x3, fma(a2[q], x2, fma(a1[q], x1, fma(a0[q], x0, acc[q][c]))));
+            }
+        }
         for (; j + 32 < j1; j += 64) {
             double a0[4], a1[4];
 #pragma unroll
