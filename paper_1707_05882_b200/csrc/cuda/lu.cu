@@ -583,12 +583,11 @@ int panel_width(int G) { return G <= 1024 ? 16 : (G <= 2048 ? 8 : 4); }
 
 template <bool LOWER>
 void trsm_launch(const double* A, int G, int lda, double* M, int ld, long long strideM, int k0, int jb, int c_lo,
-                 int c_hi, int batch, cudaStream_t st, const int* tmap, const int* mmap, int wide = -1) {
+                 int c_hi, int batch, cudaStream_t st, const int* tmap, const int* mmap) {
     if (jb <= 0 || c_hi <= c_lo) return;
-    // wide right-hand sides (the factorization's U12 blocks): column-per-lane;
-    // narrow ones (the 256-column solves) keep enough CTAs with lanes over rows.
-    // (The two round differently: a split of one update passes the choice down.)
-    const bool shfl = wide < 0 ? (c_hi - c_lo) < 512 : wide == 0;
+    // wide right-hand sides: column-per-lane; narrow ones (the 256-column
+    // solves) keep enough CTAs with lanes over rows
+    const bool shfl = (c_hi - c_lo) < 512;
     if (shfl) {
         dim3 grid((c_hi - c_lo + SW_TILE - 1) / SW_TILE, batch);
         lu_trsm_rm_kernel<LOWER><<<grid, 256, 0, st>>>(A, G, lda, (long long)G * lda, M, ld, strideM, k0, jb, c_lo,
@@ -745,23 +744,165 @@ __global__ void __launch_bounds__(512) lu_few_solve_kernel(const double* Aall, i
 }  // namespace
 
 namespace {
+// U12 = L11^-1 A12 of an outer block (positions K0..K0+nb through the row map,
+// nb <= OB_MAX) on a 32-column strip, one CTA per (strip, matrix), 2 CTAs per
+// SM: L11's strict lower triangle packed in shared memory (row r at r(r-1)/2)
+// and the strip in shared memory, both brought in by cp.async.  Rows in
+// groups of 8: the group's coupling to every row above it,
+//   X[g] -= L[g, 0:r0] X[0:r0],
+// is an [8 x r0] x [r0 x 32] product on the FP64 tensor cores (warp per 8x8
+// output tile, two accumulator chains), and the group's own 8 x 8 unit-lower
+// triangle is applied as its explicit inverse (formed once per CTA: 16 tiny
+// forward substitutions), x_i = sum_{j <= i} Li[i][j] y_j -- eight independent
+// FMAs per row instead of a dependent chain.  The strips of one matrix are
+// independent, so a split of the columns does not change any column's
+// arithmetic.
+constexpr int BT_W = 32;                            // strip width
+constexpr int BT_L = OB_MAX * (OB_MAX + 1) / 2;     // packed triangle (upper: with its diagonal)
+constexpr int BT_XL = BT_W + 4;                     // strip row stride (B fragments: 2-way at most)
+constexpr int BT_G = OB_MAX / 8;                    // 8-row groups
+constexpr size_t BT_SMEM = (size_t)(BT_L + OB_MAX * BT_XL + BT_G * 64) * sizeof(double);
+// packed offsets: strict lower row r at r(r-1)/2 (entries j < r); upper row r at
+// r nb - r(r-1)/2 (entries j = r .. nb-1, at offset j - r)
+__device__ inline int bt_lo(int r) { return r * (r - 1) / 2; }
+__device__ inline int bt_up(int r, int nb) { return r * nb - r * (r - 1) / 2; }
+
+template <bool UPPER>
+__global__ void __launch_bounds__(256, 2) lu_block_trsm_kernel(double* Aall, int G, int lda, long long strideA,
+                                                               const int* map_all, int K0, int nb, int c_lo,
+                                                               int c_hi) {
+    extern __shared__ double btm[];
+    double* Tp = btm;                      // packed triangle of the diagonal block
+    double* Xs = btm + BT_L;               // [OB_MAX][BT_XL]
+    double* Li = Xs + OB_MAX * BT_XL;      // [BT_G][8][8] inverses of the 8 x 8 diagonal blocks
+    __shared__ int s_row[OB_MAX];
+    const int b = blockIdx.y, t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int col0 = c_lo + blockIdx.x * BT_W;
+    double* A = Aall + (size_t)b * strideA;
+    const int* map = map_all + (size_t)b * G;
+    if (t < nb) s_row[t] = map[K0 + t];
+    __syncthreads();
+    const int c = col0 + lane;
+    const bool live = c < c_hi;
+    for (int r = w; r < OB_MAX; r += 8) {
+        if (r < nb) {
+            const double* src = A + (size_t)s_row[r] * lda;
+            if (UPPER) {
+                for (int j = r + lane; j < nb; j += 32) cp_async8(Tp + bt_up(r, nb) + (j - r), src + K0 + j);
+            } else {
+                for (int j = lane; j < r; j += 32) cp_async8(Tp + bt_lo(r) + j, src + K0 + j);
+            }
+            if (live) cp_async8(Xs + r * BT_XL + lane, src + c);
+            else Xs[r * BT_XL + lane] = 0.0;
+        } else {
+            Xs[r * BT_XL + lane] = 0.0;
+        }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    // T(r, j) for r, j inside the diagonal block (callers: the right triangle only)
+    auto T = [&](int r, int j) -> double { return UPPER ? Tp[bt_up(r, nb) + (j - r)] : Tp[bt_lo(r) + j]; };
+    // inverses of the diagonal 8 x 8 blocks: thread per (group, column jj)
+    if (t < BT_G * 8) {
+        const int g = t >> 3, jj = t & 7, r0 = 8 * g;
+        double x[8];
+        if (UPPER) {
+#pragma unroll
+            for (int i = 7; i >= 0; --i) {
+                double v = (i == jj) ? 1.0 : 0.0;
+                if (r0 + i < nb) {
+                    if (i <= jj) {
+#pragma unroll
+                        for (int m = 0; m < 8; ++m)
+                            if (m > i && m <= jj && r0 + m < nb) v = fma(-T(r0 + i, r0 + m), x[m], v);
+                        v /= T(r0 + i, r0 + i);
+                    } else {
+                        v = 0.0;
+                    }
+                }
+                x[i] = v;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                double v = (i == jj) ? 1.0 : 0.0;
+                if (i > jj && r0 + i < nb) {
+#pragma unroll
+                    for (int m = 0; m < 8; ++m)
+                        if (m >= jj && m < i) v = fma(-T(r0 + i, r0 + m), x[m], v);
+                }
+                x[i] = v;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) Li[g * 64 + i * 8 + jj] = x[i];
+    }
+    __syncthreads();
+    const int ngr = (nb + 7) / 8;
+    for (int gi = 0; gi < ngr; ++gi) {
+        const int g = UPPER ? ngr - 1 - gi : gi, r0 = 8 * g;
+        // coupling to the solved rows (above for L, below for U) on the tensor
+        // cores: warp w < 4 owns the columns 8w..8w+7, two accumulator chains
+        const int k_lo = UPPER ? r0 + 8 : 0, k_hi = UPPER ? ngr * 8 : r0;
+        if (k_hi > k_lo && w < 4) {
+            const int ra = r0 + gq;
+            const bool rok = ra < nb;
+            const int rr = min(ra, nb - 1);
+            double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+            for (int k = k_lo; k < k_hi; k += 8) {  // (k_hi - k_lo is a multiple of 8)
+                const int ka = k + tq, kb = k + 4 + tq;
+                const double a0 = (rok && ka < nb) ? T(rr, ka) : 0.0, a1 = (rok && kb < nb) ? T(rr, kb) : 0.0;
+                const double b0 = Xs[ka * BT_XL + 8 * w + gq], b1 = Xs[kb * BT_XL + 8 * w + gq];
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                             : "+d"(c0[0]), "+d"(c0[1]) : "d"(a0), "d"(b0));
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                             : "+d"(c1[0]), "+d"(c1[1]) : "d"(a1), "d"(b1));
+            }
+            if (rok) {
+                double* xr = Xs + ra * BT_XL + 8 * w + 2 * tq;
+                xr[0] -= c0[0] + c1[0];
+                xr[1] -= c0[1] + c1[1];
+            }
+        }
+        __syncthreads();
+        // the group's triangle by its inverse: warp w -> row r0 + w
+        double x = 0.0;
+        const double* lrow = Li + g * 64 + w * 8;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (UPPER ? j >= w : j <= w) x = fma(lrow[j], Xs[(r0 + j) * BT_XL + lane], x);
+        __syncthreads();
+        if (r0 + w < nb) Xs[(r0 + w) * BT_XL + lane] = x;
+        __syncthreads();
+    }
+    if (live)
+        for (int r = w; r < nb; r += 8) A[(size_t)s_row[r] * lda + c] = Xs[r * BT_XL + lane];
+}
+
+// the diagonal block [K0, K0 + nb) (nb <= 128, rows through map) applied to the
+// columns [c_lo, c_hi) of A: L^-1 (unit lower) or U^-1 (upper with its diagonal)
+template <bool UPPER>
+void block_trsm_launch(double* A, int G, int lda, long long gg, const int* map, int K0, int nb, int c_lo, int c_hi,
+                       int batch, cudaStream_t st) {
+    if (c_hi <= c_lo || nb <= 0) return;
+    constexpr int smem = (int)BT_SMEM;
+    static unsigned long long attr = 0;
+    smem_attr_once(lu_block_trsm_kernel<UPPER>, smem, attr);
+    const dim3 grid((c_hi - c_lo + BT_W - 1) / BT_W, batch);
+    lu_block_trsm_kernel<UPPER><<<grid, 256, smem, st>>>(A, G, lda, gg, map, K0, nb, c_lo, c_hi);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
 // Outer block [K0, K0 + NBk) (rows to rend) applied to columns [c_lo, c_hi):
-// U12 = L11^-1 A12 on the block's pivot rows by 64-row halves, then the
-// trailing update A22 -= L21 U12 (rows past the profile have zero multipliers).
-// wide: the TRSM variant, chosen from the whole update's width (both pieces of a
-// split update must round alike).
+// U12 = L11^-1 A12 on the block's pivot rows (the fused 128-row solve), then
+// the trailing update A22 -= L21 U12 (rows past the profile have zero
+// multipliers).
 void block_update(double* A, int G, int lda, long long gg, const int* map, int K0, int NBk, int rend, int c_lo,
-                  int c_hi, int batch, cudaStream_t st, bool wide) {
+                  int c_hi, int batch, cudaStream_t st) {
     const int nc = c_hi - c_lo;
     if (nc <= 0) return;
-    for (int r0 = K0; r0 < K0 + NBk; r0 += LU_NB) {
-        const int rb = min(LU_NB, K0 + NBk - r0);
-        trsm_launch<true>(A, G, lda, A, lda, gg, r0, rb, c_lo, c_hi, batch, st, map, map, wide ? 1 : 0);
-        const int below = K0 + NBk - (r0 + rb);
-        if (below > 0)
-            rm_gemm(below, nc, rb, A + r0, lda, gg, A + c_lo, lda, gg, A + c_lo, lda, gg, batch, -1.0, 1.0, st,
-                    map + r0 + rb, map + r0, map + r0 + rb, G);
-    }
+    block_trsm_launch<false>(A, G, lda, gg, map, K0, NBk, c_lo, c_hi, batch, st);
     if (rend - K0 - NBk > 0)
         rm_gemm(rend - K0 - NBk, nc, NBk, A + K0, lda, gg, A + c_lo, lda, gg, A + c_lo, lda, gg, batch, -1.0, 1.0, st,
                 map + K0 + NBk, map + K0, map + K0 + NBk, G);
@@ -808,7 +949,7 @@ void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatu
                 VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, cols_ready, 0));
                 cols_ready = nullptr;
             }
-            block_update(A, G, lda, gg, map, K0, NBk, rend, K0 + NBk, ncols, batch, st, ncols - K0 - NBk >= 512);
+            block_update(A, G, lda, gg, map, K0, NBk, rend, K0 + NBk, ncols, batch, st);
         }
         return;
     }
@@ -831,23 +972,22 @@ void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatu
         const int NBk = min(OB, G - K0), c1 = K0 + NBk;
         const int rend = row_end(c1 - 1);
         const int nxt = min(OB, G - c1);  // block K+1's width (0: K is the last block)
-        const bool wide = ncols - c1 >= 512;
         if (rest_pending) VRTE_CUDA_CHECK(cudaStreamWaitEvent(hi, la->ev[2], 0));
         rest_pending = false;
         if (nxt == 0) {  // last block: the right-hand sides only
             if (cols_ready) VRTE_CUDA_CHECK(cudaStreamWaitEvent(hi, cols_ready, 0));
-            block_update(A, G, lda, gg, map, K0, NBk, rend, c1, ncols, batch, hi, wide);
+            block_update(A, G, lda, gg, map, K0, NBk, rend, c1, ncols, batch, hi);
             break;
         }
         if (ncols > c1 + nxt) {
             VRTE_CUDA_CHECK(cudaMemcpyAsync(la->snap, map, sizeof(int) * (size_t)batch * G, cudaMemcpyDeviceToDevice, hi));
             VRTE_CUDA_CHECK(cudaEventRecord(la->ev[1], hi));
             VRTE_CUDA_CHECK(cudaStreamWaitEvent(lo, la->ev[1], 0));
-            block_update(A, G, lda, gg, la->snap, K0, NBk, rend, c1 + nxt, ncols, batch, lo, wide);
+            block_update(A, G, lda, gg, la->snap, K0, NBk, rend, c1 + nxt, ncols, batch, lo);
             VRTE_CUDA_CHECK(cudaEventRecord(la->ev[2], lo));
             rest_pending = true;
         }
-        block_update(A, G, lda, gg, map, K0, NBk, rend, c1, c1 + nxt, batch, hi, wide);
+        block_update(A, G, lda, gg, map, K0, NBk, rend, c1, c1 + nxt, batch, hi);
         block_panels(A, G, lda, map, ipiv, c1, nxt, row_end(c1 + nxt - 1), status, order_index, batch, hi);
     }
     VRTE_CUDA_CHECK(cudaEventRecord(la->ev[3], lo));
@@ -875,25 +1015,18 @@ __global__ void lu_gather_aug_kernel(const double* Aall, int G, int lda, int R, 
 
 namespace {
 // Back substitution of columns [c0, c0 + nc) of the augmented factorization in
-// place, blocks bk_hi .. blo (64 rows each): outer steps of 2 x 64 rows (the
-// two triangular solves with the 64 x 64 coupling update between them), then
-// ONE update of the rows above down to blo's first row with k = 128 (the
-// long-k GEMM runs near the DMMA rate; k = 64 does not).
+// place, blocks bk_hi .. blo (64 rows each): outer steps of 2 x 64 rows, each
+// the fused 128-row upper solve (lu_block_trsm_kernel<true>) and ONE update of
+// the rows above down to blo's first row with k = 128 (the long-k GEMM runs
+// near the DMMA rate; k = 64 does not).
 void backsolve_blocks(double* A, int G, int lda, int c0, int nc, int batch, const int* perm, int bk_hi, int blo,
                       cudaStream_t st) {
     const long long gg = (long long)G * lda;
     const int rl = blo * LU_NB;
     for (int bk = bk_hi; bk >= blo; bk -= 2) {
         const int k1 = bk * LU_NB, jb1 = min(LU_NB, G - k1);
-        trsm_launch<false>(A, G, lda, A + c0, lda, gg, k1, jb1, 0, nc, batch, st, perm, perm);
-        int k0 = k1, jb = jb1;
-        if (bk - 1 >= blo) {
-            k0 = k1 - LU_NB;
-            rm_gemm(LU_NB, nc, jb1, A + k1, lda, gg, A + c0, lda, gg, A + c0, lda, gg, batch, -1.0, 1.0, st, perm + k0,
-                    perm + k1, perm + k0, G);
-            trsm_launch<false>(A, G, lda, A + c0, lda, gg, k0, LU_NB, 0, nc, batch, st, perm, perm);
-            jb = LU_NB + jb1;
-        }
+        const int k0 = (bk - 1 >= blo) ? k1 - LU_NB : k1, jb = k1 + jb1 - k0;
+        block_trsm_launch<true>(A, G, lda, gg, perm, k0, jb, c0, c0 + nc, batch, st);
         if (k0 > rl)
             rm_gemm(k0 - rl, nc, jb, A + k0, lda, gg, A + c0, lda, gg, A + c0, lda, gg, batch, -1.0, 1.0, st,
                     perm + rl, perm + k0, perm + rl, G);
@@ -902,7 +1035,7 @@ void backsolve_blocks(double* A, int G, int lda, int c0, int nc, int batch, cons
 
 int backsolve_launches(int bk_hi, int blo) {
     int n = 0;
-    for (int bk = bk_hi; bk >= blo; bk -= 2) n += (bk - 1 >= blo ? 3 : 1) + (bk - 1 > blo ? 1 : 0);
+    for (int bk = bk_hi; bk >= blo; bk -= 2) n += 1 + (bk - 1 > blo ? 1 : 0);
     return n;
 }
 }  // namespace
