@@ -8,9 +8,10 @@
 // later kernel addresses rows through it (the GEMMs through their index maps,
 // common.cuh), so the row-interchange traffic of dlaswp -- a full HBM pass per
 // pivot block -- disappears.  The factorization is blocked twice:
-//   outer blocks of 128 columns, right-looking: U12 by a warp-parallel
-//     unit-lower triangular solve (64-row halves) and the trailing update as
-//     one DMMA GEMM with k = 128 over the rows inside the staircase profile;
+//   outer blocks of 128 columns, right-looking: U12 by the fused 128-row
+//     block solve (lu_block_trsm_kernel) and the trailing update as one DMMA
+//     GEMM with k = 128 over the rows inside the staircase profile; with a
+//     one-block look-ahead on two streams for the boundary systems;
 //   inner panels of 16 (8, 4 for taller matrices) columns, left-looking
 //     (Crout) inside the outer block and fused into ONE kernel per panel: the
 //     panel's U rows (unit-lower solve with the block's L, in shared memory),
@@ -18,8 +19,8 @@
 //     kk from registers), then register-resident factorization with
 //     block-wide argmax pivoting (LAPACK's first-index tie break).
 // The solve gathers the right-hand sides through the row map, then runs
-// blocked forward / backward substitution (TRSM on 64-row blocks + GEMM
-// updates), reading L and U rows through the map.
+// blocked forward / backward substitution (the fused solve on 128-row diagonal
+// blocks + GEMM couplings), reading L and U rows through the map.
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -30,7 +31,6 @@ namespace vrte {
 namespace {
 
 constexpr int LU_NB = 64;  // outer block
-constexpr int SW_TILE = 32;
 
 // ------------------------------------------------------------------ Crout panel (lazy pivoting)
 constexpr int OB_MAX = 128;  // outer block width (bounds the panel kernel's shared memory)
@@ -315,189 +315,6 @@ __global__ void lu_map_init_kernel(int* map, long long total, int G) {
         map[e] = (int)(e % G);
 }
 
-// ------------------------------------------------------------------ triangular block solves
-// M[k0:k0+jb, c_lo:c_hi] <- T^-1 M[...] with T = A[k0:k0+jb, k0:k0+jb] (row-major
-// ld G): unit lower (LOWER) or upper.  CTA per 32-column tile; warp per 4
-// columns, lanes over rows (two rows per lane), the solved entry broadcast by
-// shuffle -- substitution, not an explicit inverse.
-template <bool LOWER>
-__global__ void __launch_bounds__(256) lu_trsm_rm_kernel(const double* Aall, int G, int lda, long long strideA,
-                                                         double* Mall, int ld, long long strideM, int k0,
-                                                         int jb, int c_lo, int c_hi, const int* tmap_all,
-                                                         const int* mmap_all) {
-    __shared__ double Ts[LU_NB][LU_NB + 1];
-    __shared__ double s_rd[LU_NB];
-    __shared__ int s_trow[LU_NB], s_mrow[LU_NB];
-    const int b = blockIdx.y, t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const int col0 = c_lo + blockIdx.x * SW_TILE;
-    if (col0 >= c_hi) return;
-    const double* A = Aall + (size_t)b * strideA;
-    double* M = Mall + (size_t)b * strideM;
-    // T rows (positions k0..k0+jb of A) and M rows, through the row maps if given
-    const int* tmap = tmap_all ? tmap_all + (size_t)b * G : nullptr;
-    const int* mmap = mmap_all ? mmap_all + (size_t)b * G : nullptr;
-#ifdef VRTE_LU_TRACE
-    long long tr[5];
-    tr[0] = clock64();
-#endif
-    if (t < jb) {
-        s_trow[t] = tmap ? tmap[k0 + t] : k0 + t;
-        s_mrow[t] = mmap ? mmap[k0 + t] : k0 + t;
-    }
-    __syncthreads();
-    // every global load of the prologue in flight before the first is consumed
-    // (the triangle: 16 entries per thread; the M rows: 8)
-    constexpr int TQN = LU_NB * LU_NB / 256;
-    double tv[TQN];
-#pragma unroll
-    for (int q = 0; q < TQN; ++q) {
-        const int e = t + 256 * q, r = e / LU_NB, cc = e % LU_NB;
-        tv[q] = (r < jb && cc < jb) ? A[(size_t)s_trow[r] * lda + k0 + cc] : 0.0;
-    }
-    // lane rows r0, r1; the warp's 4 consecutive columns (one 32-byte sector per row)
-    const int r0 = lane, r1 = lane + 32, cw = col0 + w * 4;
-    double x0[4], x1[4];
-    bool lv[4];
-    const size_t m0 = r0 < jb ? (size_t)s_mrow[r0] * ld : 0, m1 = r1 < jb ? (size_t)s_mrow[r1] * ld : 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        lv[q] = cw + q < c_hi;
-        x0[q] = (r0 < jb && lv[q]) ? M[m0 + cw + q] : 0.0;
-        x1[q] = (r1 < jb && lv[q]) ? M[m1 + cw + q] : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < TQN; ++q) {
-        const int e = t + 256 * q;
-        Ts[e / LU_NB][e % LU_NB] = tv[q];
-    }
-    __syncthreads();
-    if (!LOWER && t < jb) s_rd[t] = 1.0 / Ts[t][t];
-    if (!LOWER) __syncthreads();
-#ifdef VRTE_LU_TRACE
-    tr[1] = tr[2] = clock64();
-#endif
-    if (LOWER) {
-        for (int j = 0; j < jb; ++j) {
-            const int src = j & 31;
-            const double l0 = (r0 > j && r0 < jb) ? Ts[r0][j] : 0.0;
-            const double l1 = (r1 > j && r1 < jb) ? Ts[r1][j] : 0.0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const double xj = __shfl_sync(0xffffffffu, j < 32 ? x0[q] : x1[q], src);
-                x0[q] = fma(-l0, xj, x0[q]);
-                x1[q] = fma(-l1, xj, x1[q]);
-            }
-        }
-    } else {
-        for (int j = jb - 1; j >= 0; --j) {
-            const int src = j & 31;
-            const double rd = s_rd[j];
-            const double u0 = (r0 < j) ? Ts[r0][j] : 0.0;
-            const double u1 = (r1 < j) ? Ts[r1][j] : 0.0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const double xj = __shfl_sync(0xffffffffu, j < 32 ? x0[q] : x1[q], src) * rd;
-                if (r0 == j) x0[q] = xj;
-                if (r1 == j) x1[q] = xj;
-                x0[q] = fma(-u0, xj, x0[q]);
-                x1[q] = fma(-u1, xj, x1[q]);
-            }
-        }
-    }
-#ifdef VRTE_LU_TRACE
-    tr[3] = clock64();
-#endif
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        if (r0 < jb && lv[q]) M[m0 + cw + q] = x0[q];
-        if (r1 < jb && lv[q]) M[m1 + cw + q] = x1[q];
-    }
-#ifdef VRTE_LU_TRACE
-    __syncthreads();
-    tr[4] = clock64();
-    if (t == 0 && b == 0 && blockIdx.x == 0)
-        printf("trsm%d k0=%4d jb=%2d cols=%4d | Ts %6lld  M %6lld  solve %6lld  store %6lld cycles\n", (int)LOWER, k0, jb,
-               c_hi - c_lo, tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2], tr[4] - tr[3]);
-#endif
-}
-
-// Column-per-lane substitution: lane = one column of M, the jb-row column in
-// registers, the triangle in shared memory read as warp-wide broadcasts (LDS.128 =
-// two entries), four partial sums per row to shorten the FMA chains.  Every
-// global access of the prologue is issued before the first is consumed (row
-// indices, then the triangle by cp.async, then the column), so a CTA pays two
-// L2 round trips instead of one per row -- and no shuffles: the lane-over-rows
-// variant above is bound by 8 SHFL per 8 FMA on the MIO pipe.  CTA = 2 warps.
-template <bool LOWER>
-__global__ void __launch_bounds__(64, 6) lu_trsm_col_kernel(const double* Aall, int G, int lda, long long strideA,
-                                                            double* Mall, int ld, long long strideM, int k0, int jb,
-                                                            int c_lo, int c_hi, const int* tmap_all,
-                                                            const int* mmap_all) {
-    __shared__ __align__(16) double Ts[LU_NB * LU_NB];
-    __shared__ double s_rd[LU_NB];
-    __shared__ int s_trow[LU_NB], s_mrow[LU_NB];
-    const int b = blockIdx.y, t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const double* A = Aall + (size_t)b * strideA;
-    double* M = Mall + (size_t)b * strideM;
-    const int* tmap = tmap_all ? tmap_all + (size_t)b * G : nullptr;
-    const int* mmap = mmap_all ? mmap_all + (size_t)b * G : nullptr;
-    for (int q = t; q < jb; q += 64) {
-        s_trow[q] = tmap ? tmap[k0 + q] : k0 + q;
-        s_mrow[q] = mmap ? mmap[k0 + q] : k0 + q;
-    }
-    __syncthreads();
-    for (int r = w; r < jb; r += 2) {
-        const double* src = A + (size_t)s_trow[r] * lda + k0;
-        if (LOWER) {
-            for (int c = lane; c < r; c += 32) cp_async8(Ts + r * LU_NB + c, src + c);
-        } else {
-            for (int c = r + lane; c < jb; c += 32) cp_async8(Ts + r * LU_NB + c, src + c);
-        }
-    }
-    cp_async_wait_all();
-    const int col = c_lo + blockIdx.x * 64 + w * 32 + lane;
-    const bool live = col < c_hi;
-    double x[LU_NB];
-#pragma unroll
-    for (int r = 0; r < LU_NB; ++r) x[r] = (live && r < jb) ? M[(size_t)s_mrow[r] * ld + col] : 0.0;
-    __syncthreads();
-    if (!LOWER)
-        for (int q = t; q < jb; q += 64) s_rd[q] = 1.0 / Ts[q * LU_NB + q];
-    __syncthreads();
-    if (LOWER) {
-#pragma unroll
-        for (int r = 1; r < LU_NB; ++r) {
-            if (r >= jb) break;
-            const double2* Lr = reinterpret_cast<const double2*>(Ts + r * LU_NB);
-            double acc[4] = {x[r], 0.0, 0.0, 0.0};
-#pragma unroll
-            for (int s2 = 0; s2 < r / 2; ++s2) {
-                const double2 l = Lr[s2];
-                acc[(2 * s2) & 3] = fma(-l.x, x[2 * s2], acc[(2 * s2) & 3]);
-                acc[(2 * s2 + 1) & 3] = fma(-l.y, x[2 * s2 + 1], acc[(2 * s2 + 1) & 3]);
-            }
-            if (r & 1) acc[(r - 1) & 3] = fma(-Ts[r * LU_NB + r - 1], x[r - 1], acc[(r - 1) & 3]);
-            x[r] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-        }
-    } else {
-#pragma unroll
-        for (int r = LU_NB - 1; r >= 0; --r) {
-            if (r < jb) {
-                double acc[4] = {x[r], 0.0, 0.0, 0.0};
-#pragma unroll
-                for (int s = r + 1; s < LU_NB; ++s)
-                    if (s < jb) acc[s & 3] = fma(-Ts[r * LU_NB + s], x[s], acc[s & 3]);
-                x[r] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) * s_rd[r];
-            }
-        }
-    }
-    if (live) {
-#pragma unroll
-        for (int r = 0; r < LU_NB; ++r)
-            if (r < jb) M[(size_t)s_mrow[r] * ld + col] = x[r];
-    }
-}
-
 __global__ void lu_gather_rows_kernel(const double* In, long long strideIn, double* Out,
                                       long long strideOut, const int* perm_all, int G, int ncol,
                                       int batch) {
@@ -580,25 +397,6 @@ void panel_dispatch(int np, double* A, int G, int lda, int* map, int* ipiv, int 
 }
 
 int panel_width(int G) { return G <= 1024 ? 16 : (G <= 2048 ? 8 : 4); }
-
-template <bool LOWER>
-void trsm_launch(const double* A, int G, int lda, double* M, int ld, long long strideM, int k0, int jb, int c_lo,
-                 int c_hi, int batch, cudaStream_t st, const int* tmap, const int* mmap) {
-    if (jb <= 0 || c_hi <= c_lo) return;
-    // wide right-hand sides: column-per-lane; narrow ones (the 256-column
-    // solves) keep enough CTAs with lanes over rows
-    const bool shfl = (c_hi - c_lo) < 512;
-    if (shfl) {
-        dim3 grid((c_hi - c_lo + SW_TILE - 1) / SW_TILE, batch);
-        lu_trsm_rm_kernel<LOWER><<<grid, 256, 0, st>>>(A, G, lda, (long long)G * lda, M, ld, strideM, k0, jb, c_lo,
-                                                       c_hi, tmap, mmap);
-    } else {
-        dim3 grid((c_hi - c_lo + 63) / 64, batch);
-        lu_trsm_col_kernel<LOWER><<<grid, 64, 0, st>>>(A, G, lda, (long long)G * lda, M, ld, strideM, k0, jb, c_lo,
-                                                       c_hi, tmap, mmap);
-    }
-    VRTE_CUDA_CHECK(cudaGetLastError());
-}
 
 int outer_block() { return OB_MAX; }
 
@@ -768,20 +566,26 @@ __device__ inline int bt_lo(int r) { return r * (r - 1) / 2; }
 __device__ inline int bt_up(int r, int nb) { return r * nb - r * (r - 1) / 2; }
 
 template <bool UPPER>
-__global__ void __launch_bounds__(256, 2) lu_block_trsm_kernel(double* Aall, int G, int lda, long long strideA,
-                                                               const int* map_all, int K0, int nb, int c_lo,
-                                                               int c_hi) {
+__global__ void __launch_bounds__(256, 2) lu_block_trsm_kernel(const double* Aall, int G, int lda, long long strideA,
+                                                               const int* map_all, int K0, int nb, double* Mall,
+                                                               int ldm, long long strideM, const int* mmap_all,
+                                                               int c_lo, int c_hi) {
     extern __shared__ double btm[];
     double* Tp = btm;                      // packed triangle of the diagonal block
     double* Xs = btm + BT_L;               // [OB_MAX][BT_XL]
     double* Li = Xs + OB_MAX * BT_XL;      // [BT_G][8][8] inverses of the 8 x 8 diagonal blocks
-    __shared__ int s_row[OB_MAX];
+    __shared__ int s_row[OB_MAX], s_mrow[OB_MAX];
     const int b = blockIdx.y, t = threadIdx.x, lane = t & 31, w = t >> 5;
     const int gq = lane >> 2, tq = lane & 3;
     const int col0 = c_lo + blockIdx.x * BT_W;
-    double* A = Aall + (size_t)b * strideA;
+    const double* A = Aall + (size_t)b * strideA;
+    double* M = Mall + (size_t)b * strideM;
     const int* map = map_all + (size_t)b * G;
-    if (t < nb) s_row[t] = map[K0 + t];
+    const int* mmap = mmap_all ? mmap_all + (size_t)b * G : nullptr;
+    if (t < nb) {
+        s_row[t] = map[K0 + t];
+        s_mrow[t] = mmap ? mmap[K0 + t] : K0 + t;
+    }
     __syncthreads();
     const int c = col0 + lane;
     const bool live = c < c_hi;
@@ -793,7 +597,7 @@ __global__ void __launch_bounds__(256, 2) lu_block_trsm_kernel(double* Aall, int
             } else {
                 for (int j = lane; j < r; j += 32) cp_async8(Tp + bt_lo(r) + j, src + K0 + j);
             }
-            if (live) cp_async8(Xs + r * BT_XL + lane, src + c);
+            if (live) cp_async8(Xs + r * BT_XL + lane, M + (size_t)s_mrow[r] * ldm + c);
             else Xs[r * BT_XL + lane] = 0.0;
         } else {
             Xs[r * BT_XL + lane] = 0.0;
@@ -877,21 +681,28 @@ __global__ void __launch_bounds__(256, 2) lu_block_trsm_kernel(double* Aall, int
         __syncthreads();
     }
     if (live)
-        for (int r = w; r < nb; r += 8) A[(size_t)s_row[r] * lda + c] = Xs[r * BT_XL + lane];
+        for (int r = w; r < nb; r += 8) M[(size_t)s_mrow[r] * ldm + c] = Xs[r * BT_XL + lane];
 }
 
 // the diagonal block [K0, K0 + nb) (nb <= 128, rows through map) applied to the
 // columns [c_lo, c_hi) of A: L^-1 (unit lower) or U^-1 (upper with its diagonal)
+// (M: the strip's matrix, rows mmap[K0 + r] or K0 + r when mmap is null)
 template <bool UPPER>
-void block_trsm_launch(double* A, int G, int lda, long long gg, const int* map, int K0, int nb, int c_lo, int c_hi,
-                       int batch, cudaStream_t st) {
+void block_trsm_launch(const double* A, int G, int lda, long long gg, const int* map, int K0, int nb, double* M,
+                       int ldm, long long strideM, const int* mmap, int c_lo, int c_hi, int batch, cudaStream_t st) {
     if (c_hi <= c_lo || nb <= 0) return;
     constexpr int smem = (int)BT_SMEM;
     static unsigned long long attr = 0;
     smem_attr_once(lu_block_trsm_kernel<UPPER>, smem, attr);
     const dim3 grid((c_hi - c_lo + BT_W - 1) / BT_W, batch);
-    lu_block_trsm_kernel<UPPER><<<grid, 256, smem, st>>>(A, G, lda, gg, map, K0, nb, c_lo, c_hi);
+    lu_block_trsm_kernel<UPPER><<<grid, 256, smem, st>>>(A, G, lda, gg, map, K0, nb, M, ldm, strideM, mmap, c_lo,
+                                                         c_hi);
     VRTE_CUDA_CHECK(cudaGetLastError());
+}
+template <bool UPPER>
+void block_trsm_launch(double* A, int G, int lda, long long gg, const int* map, int K0, int nb, int c_lo, int c_hi,
+                       int batch, cudaStream_t st) {
+    block_trsm_launch<UPPER>(A, G, lda, gg, map, K0, nb, A, lda, gg, map, c_lo, c_hi, batch, st);
 }
 
 // Outer block [K0, K0 + NBk) (rows to rend) applied to columns [c_lo, c_hi):
@@ -1061,23 +872,24 @@ void lu_solve_rm(const double* A, int G, int batch, const int* perm, const doubl
             Bin, gn, X, gn, perm, G, ncol, batch);
         VRTE_CUDA_CHECK(cudaGetLastError());
     }
-    // L and U rows are read through the row map (perm)
-    for (int k0 = 0; k0 < G; k0 += LU_NB) {
-        const int jb = min(LU_NB, G - k0);
-        (void)prof_d;
-        (void)prof_P;
-        trsm_launch<true>(A, G, G, X, ncol, gn, k0, jb, 0, ncol, batch, st, perm, nullptr);
+    // L and U rows are read through the row map (perm); 128-row diagonal blocks
+    // by the fused solve, the couplings as GEMMs
+    (void)prof_d;
+    (void)prof_P;
+    for (int k0 = 0; k0 < G; k0 += OB_MAX) {
+        const int jb = min(OB_MAX, G - k0);
+        block_trsm_launch<false>(A, G, G, gg, perm, k0, jb, X, ncol, gn, nullptr, 0, ncol, batch, st);
         if (G - k0 - jb > 0)
             rm_gemm(G - k0 - jb, ncol, jb, A + k0, G, gg, X + (size_t)k0 * ncol, ncol, gn,
                     X + (size_t)(k0 + jb) * ncol, ncol, gn, batch, -1.0, 1.0, st, perm + k0 + jb, nullptr, nullptr, G);
     }
-    // back substitution only down to row_lo: the unknowns above it are not
-    // wanted (X rows < row_lo are left holding the forward solution)
-    const int nblk = (G + LU_NB - 1) / LU_NB;
-    const int blo = max(0, row_lo) / LU_NB, rl = blo * LU_NB;
+    // back substitution only down to row_lo's block: the unknowns above it are
+    // not wanted (X rows there are left holding the forward solution)
+    const int nblk = (G + OB_MAX - 1) / OB_MAX;
+    const int blo = max(0, row_lo) / OB_MAX, rl = blo * OB_MAX;
     for (int bk = nblk - 1; bk >= blo; --bk) {
-        const int k0 = bk * LU_NB, jb = min(LU_NB, G - k0);
-        trsm_launch<false>(A, G, G, X, ncol, gn, k0, jb, 0, ncol, batch, st, perm, nullptr);
+        const int k0 = bk * OB_MAX, jb = min(OB_MAX, G - k0);
+        block_trsm_launch<true>(A, G, G, gg, perm, k0, jb, X, ncol, gn, nullptr, 0, ncol, batch, st);
         if (k0 > rl)
             rm_gemm(k0 - rl, ncol, jb, A + k0, G, gg, X + (size_t)k0 * ncol, ncol, gn, X + (size_t)rl * ncol, ncol,
                     gn, batch, -1.0, 1.0, st, perm + rl, nullptr, nullptr, G);
@@ -1089,18 +901,18 @@ void lu_solve_gathered(const double* A, int G, int lda, int batch, const int* pe
     const long long gg = (long long)G * lda, gn = (long long)G * ncol;
     // forward substitution on columns [fwd_lo, ncol) (the others already hold L^-1 P b)
     if (fwd_lo < ncol)
-        for (int k0 = 0; k0 < G; k0 += LU_NB) {
-            const int jb = min(LU_NB, G - k0);
-            trsm_launch<true>(A, G, lda, X, ncol, gn, k0, jb, fwd_lo, ncol, batch, st, perm, nullptr);
+        for (int k0 = 0; k0 < G; k0 += OB_MAX) {
+            const int jb = min(OB_MAX, G - k0);
+            block_trsm_launch<false>(A, G, lda, gg, perm, k0, jb, X, ncol, gn, nullptr, fwd_lo, ncol, batch, st);
             if (G - k0 - jb > 0)
                 rm_gemm(G - k0 - jb, ncol - fwd_lo, jb, A + k0, lda, gg, X + (size_t)k0 * ncol + fwd_lo, ncol, gn,
                         X + (size_t)(k0 + jb) * ncol + fwd_lo, ncol, gn, batch, -1.0, 1.0, st, perm + k0 + jb, nullptr,
                         nullptr, G);
         }
-    const int nblk = (G + LU_NB - 1) / LU_NB;
+    const int nblk = (G + OB_MAX - 1) / OB_MAX;
     for (int bk = nblk - 1; bk >= 0; --bk) {
-        const int k0 = bk * LU_NB, jb = min(LU_NB, G - k0);
-        trsm_launch<false>(A, G, lda, X, ncol, gn, k0, jb, 0, ncol, batch, st, perm, nullptr);
+        const int k0 = bk * OB_MAX, jb = min(OB_MAX, G - k0);
+        block_trsm_launch<true>(A, G, lda, gg, perm, k0, jb, X, ncol, gn, nullptr, 0, ncol, batch, st);
         if (k0 > 0)
             rm_gemm(k0, ncol, jb, A + k0, lda, gg, X + (size_t)k0 * ncol, ncol, gn, X, ncol, gn, batch, -1.0, 1.0, st,
                     perm, nullptr, nullptr, G);
@@ -1108,33 +920,40 @@ void lu_solve_gathered(const double* A, int G, int lda, int batch, const int* pe
 }
 
 int lu_gathered_launch_count(int G, int ncol, int fwd_lo) {
-    const int nblk = (G + LU_NB - 1) / LU_NB;
+    const int nblk = (G + OB_MAX - 1) / OB_MAX;
     return (fwd_lo < ncol ? 2 * nblk - 1 : 0) + 2 * nblk - 1;
 }
 
+// the factorization with the look-ahead schedule (the boundary systems): per
+// outer block its panels, then the update of the next block's columns (fused
+// solve + GEMM) and of the rest (the same, on the other stream)
 int lu_aug_launch_count(int G, int R, int row_lo) {
     const int PB = panel_width(G), OB = outer_block();
     int n = 1;  // row map init
     for (int K0 = 0; K0 < G; K0 += OB) {
-        const int NBk = min(OB, G - K0);
+        const int NBk = min(OB, G - K0), c1 = K0 + NBk, nxt = min(OB, G - c1);
         n += (NBk + PB - 1) / PB;
-        if (G + R - K0 - NBk > 0) n += 2 * ((NBk + LU_NB - 1) / LU_NB) - 1 + 1;
+        if (nxt == 0)
+            n += R > 0 ? 1 : 0;
+        else
+            n += 2 + (G + R > c1 + nxt ? 2 : 0);
     }
     const int nblk = (G + LU_NB - 1) / LU_NB, blo = max(0, row_lo) / LU_NB;
     n += backsolve_launches(nblk - 1, blo) + 1;  // + gather
     return n;
 }
 
+// serial factorization + gathered solve (the eigenvector inverse)
 int lu_rm_launch_count(int G) {
     const int PB = panel_width(G), OB = outer_block();
     int n = 1;  // row map init
     for (int K0 = 0; K0 < G; K0 += OB) {
         const int NBk = min(OB, G - K0);
         n += (NBk + PB - 1) / PB;  // fused Crout panels
-        if (G - K0 - NBk > 0) n += 2 * ((NBk + LU_NB - 1) / LU_NB) - 1 + 1;
+        if (G - K0 - NBk > 0) n += 2;  // fused block solve + trailing GEMM
     }
-    const int nblk = (G + LU_NB - 1) / LU_NB;
-    n += 1 + 2 * nblk - 1 + 2 * nblk - 1;  // gather + forward + backward (upper bound)
+    const int nblk = (G + OB_MAX - 1) / OB_MAX;
+    n += 1 + 2 * nblk - 1 + 2 * nblk - 1;  // gather + forward + backward
     return n;
 }
 
