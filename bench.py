@@ -755,11 +755,11 @@ def main():
     kern = {"hqr_multi_kernel (multishift Francis QR + AED + Schur vectors)": (res["t_hqr"], Be * 20.0 * d ** 3),
             # the augmented [A | B] factorization also eliminates the R right-hand
             # sides (L^-1 P B: G^2 R flops) besides the (2/3) G^3 of the LU proper
-            "boundary LU factor (augmented: Crout panels + TRSM + DMMA GEMM)":
+            "boundary LU factor (augmented: Crout panels + fused block solves + DMMA GEMM, look-ahead)":
                 (res["t_lu_factor"], L * ((2.0 / 3.0) * G ** 3 + G ** 2 * R)),
             # back substitution U x = y: the R right-hand sides through layer 0's 2d rows
             # (R (2d)^2), the 4 residual probes through all G rows (4 G^2)
-            "boundary back substitution (TRSM + DMMA GEMM)": (res["t_lu_solve"], L * (R * (2 * d) ** 2 + 4 * G ** 2)),
+            "boundary back substitution (fused block solves + DMMA GEMM)": (res["t_lu_solve"], L * (R * (2 * d) ** 2 + 4 * G ** 2)),
             "eigen refinement (Newton step, 8N residual GEMMs)": (res["t_refine"], Be * 24.0 * d ** 3),
             "blocked Hessenberg + Q": (res["t_hessenberg"], Be * (10.0 / 3.0 + 4.0 / 3.0) * d ** 3),
             "trevc_blk_kernel (eigenvectors)": (res["t_trevc"], Be * (1.0 / 3.0) * d ** 3)}

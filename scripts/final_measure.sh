@@ -18,3 +18,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/la
 timeout 600 python scripts/shard_probe.py C3 2,4,8 4 > $O/shard_c3.jsonl 2>&1
 timeout 900 python scripts/shard_probe.py C4p 2,4,8 > $O/shard_c4p.jsonl 2>&1
 timeout 600 python scripts/qr_profile.py C3 > $O/qr_profile_c3.json 2>/dev/null
+# ncu --set full of the top kernels, summarised on the box (the reports are large)
+bash scripts/ncu_capture.sh
+python scripts/ncu_summary.py $O/ncu_summary.json gpurun_out/ncu_*.ncu-rep > $O/ncu_summary.log 2>&1
+rm -f gpurun_out/ncu_*.ncu-rep

@@ -9,9 +9,9 @@ run() {  # name, kernel regex, launch skip, count
 }
 run hqr hqr_multi_kernel 0 1
 run hess_panel hess_panel_kernel 0 1
-run trevc trevc_grp_kernel 0 1
+run trevc trevc_blk_kernel 0 1
 run lu_panel lu_panel_crout_kernel 16 1
-run lu_trsm lu_trsm_rm_kernel 0 1
+run lu_block_trsm lu_block_trsm_kernel 1 1
 run few_solve lu_few_solve_kernel 0 1
 run gemm_fe dmma_gemm_kernel 0 1
 run gemm_lu dmma_gemm_kernel 68 2
