@@ -116,6 +116,7 @@ struct vrte_cuda_plan {
     DevBuf<double> nodes, weights, mdiag, omega, greek, tau, mu_in, table, beam_rows, post, trig, refl_top, pre;
     int out_lo = 0;
     bool lean = false;  // problem->concurrent: lower-register kernel builds
+    bool concurrent = false;  // other plans share the device: no look-ahead streams
     DevBuf<int> medium, order_index, slot_of_order;
     // homogeneous
     DevBuf<double> gsf_n, gsf_b, E, F, T, Z, psi_p, psi_m, tmp1, tmp2, tmp3, tmp4;
@@ -254,6 +255,7 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
         int dev = 0, sms = 148;
         if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         pl.lean = p->concurrent != 0 && 2 * pl.Be >= sms / 2;
+        pl.concurrent = p->concurrent != 0;
     }
     const int N = pl.N, L = pl.L, d = pl.d, R = pl.R, G = pl.G, B = pl.B, NO = pl.NO;
     cudaStream_t st = pl.st;
@@ -774,8 +776,10 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     nl += 4;
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[11], st));
     const int K = ba.K, ldl = ba.ldl;
+    // look-ahead only for a plan alone on its device: with plans in flight the
+    // other plans fill the SMs the look-ahead would, at twice the launches
     lu_factor_rm(pl.lhs.p, G, NO, pl.ipiv.p, pl.perm.p, pl.status, pl.order_index.p, st, d, pl.P, ldl, G + R,
-                 pl.join[3], &pl.lula);
+                 pl.join[3], pl.concurrent ? nullptr : &pl.lula);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[12], st));
     if (pl.full_solution) {
         // radiance: every layer's coefficients, under the reference's exact gate
