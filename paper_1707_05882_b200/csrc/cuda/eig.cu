@@ -1885,8 +1885,14 @@ __global__ void eig_diag_solve_kernel(double* Wall, int d, int ncol, long long w
     double* wre = Wall + (size_t)b * w_stride + (size_t)c * d;
     double* wim = wre + d;
     const double a = wrall[(size_t)b * d + k];
+    // x / den as x conj(den) / |den|^2: one FP64 division instead of three (the
+    // denominators are eigenvalue gaps, far from the squares' over/underflow)
+    auto qdiv = [](cplx x, cplx den) {
+        const double r = 1.0 / fma(den.re, den.re, den.im * den.im);
+        return cmk(fma(x.re, den.re, x.im * den.im) * r, fma(x.im, den.re, -x.re * den.im) * r);
+    };
     if (wik == 0.0) {
-        const cplx x = cdiv(cmk(wre[k], cx ? wim[k] : 0.0), cmk(a, 0.0) - sg);
+        const cplx x = qdiv(cmk(wre[k], cx ? wim[k] : 0.0), cmk(a, 0.0) - sg);
         wre[k] = x.re;
         if (cx) wim[k] = x.im;
         return;
@@ -1895,8 +1901,8 @@ __global__ void eig_diag_solve_kernel(double* Wall, int d, int ncol, long long w
     const cplx w0 = cmk(wre[k], cx ? wim[k] : 0.0);
     const cplx w1 = cmk(wre[k + 1], cx ? wim[k + 1] : 0.0);
     const cplx iw1 = cmk(-w1.im, w1.re);
-    const cplx al = cdiv(0.5 * (w0 - iw1), cmk(a, wik) - sg);
-    const cplx be = cdiv(0.5 * (w0 + iw1), cmk(a, -wik) - sg);
+    const cplx al = qdiv(0.5 * (w0 - iw1), cmk(a, wik) - sg);
+    const cplx be = qdiv(0.5 * (w0 + iw1), cmk(a, -wik) - sg);
     const cplx y0 = al + be, dif = al - be;
     const cplx y1 = cmk(-dif.im, dif.re);
     wre[k] = y0.re;
