@@ -105,17 +105,21 @@ int main(int argc, char** argv) {
         for (int ta = 0; ta < 2; ++ta)
             for (int tb = 0; tb < 2; ++tb)
                 for (double beta : {0.0, 0.7, 1.0}) fails += run(s[0], s[1], s[2], 3, ta, tb, beta, false) >= 1e-14;
-    run(256, 256, 256, 128, false, false, 0.0, true);
-    run(256, 512, 256, 128, false, false, 0.0, true);
-    run(256, 512, 256, 128, true, false, 0.0, true);
-    run(256, 256, 512, 64, false, false, 1.0, true);
-    run(512, 512, 512, 64, false, false, 0.0, true);
+    // the solver's shapes (C3, round 2): eigen refinement / particular products
+    run(256, 256, 256, 67, false, false, 0.0, true);
+    run(256, 512, 256, 67, false, false, 0.0, true);
+    // boundary top (Top0 [A_0; B_0], B transposed, beta = 1)
+    run(256, 256, 512, 64, false, true, 1.0, true);
+    // LU trailing updates (k = 128, beta = 1): first block's rest / look-ahead piece
+    run(896, 1152, 128, 64, false, false, 1.0, true);
+    run(896, 128, 128, 64, false, false, 1.0, true);
+    // back substitution coupling (k = 128)
+    run(384, 256, 128, 64, false, false, 1.0, true);
+    // Hessenberg trailing updates (k = 32) and the left-update product (A transposed)
+    run(256, 224, 32, 67, false, false, 1.0, true);
+    run(32, 224, 255, 67, true, false, 0.0, true);
+    // large square reference point
     run(4096, 4096, 4096, 1, false, false, 0.0, true);
-    // LU / solve trailing updates (k = 64, beta = 1)
-    run(960, 960, 64, 64, false, false, 1.0, true);
-    run(256, 960, 64, 64, false, false, 1.0, true);
-    run(448, 448, 64, 64, false, false, 1.0, true);
-    run(256, 224, 32, 128, false, false, 1.0, true);
     std::printf("fails=%d\n", fails);
     return fails != 0;
 }
