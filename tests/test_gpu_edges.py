@@ -44,6 +44,13 @@ def test_smallest_problem(coeffs):
     compare(slab(coeffs, 0.8, 0.7), 1, [0.6], 1)
 
 
+@pytest.mark.parametrize("N", [3, 5, 7])
+def test_odd_quadratures(N):
+    # d = 4N not a multiple of 8: the fused 128-row block solves (lu.cu) pad the
+    # eigenvector inverse's diagonal block to 8-row groups
+    compare(slab(M.FULL, 0.85, 0.9, "lambertian", 0.2), N, [0.45, 0.9], 3)
+
+
 def test_resonant_incidence_dithers_like_the_reference():
     desc = slab(M.ISOTROPIC, 0.5, 1.0)
     N = 4
