@@ -230,6 +230,23 @@ __global__ void update_kernel(RefineArgs a) {
     const cplx dr = cdiv(bs, as);
     bool fin = isfinite(dr.re) && isfinite(dr.im);
     if (!fin) return;  // keep the current pair (the reference's `break` on non-finite)
+    // Safeguard: v is normalized to a largest component of 1 and the eigenpair is
+    // already close (Schur-form accuracy), so a correction of half the vector (or
+    // an eigenvalue move above 1e-3 relative) is the approximate Jacobian failing
+    // -- an exactly repeated eigenvalue, whose eigenvectors span a plane the
+    // bordered system does not fix -- not a better eigenpair: keep the current pair.
+    double dmax = 0.0;
+    for (int i = lane; i < d; i += 32) {
+        const double im = 1.0 / a.mdiag[i];
+        cplx ap, aq, bp, bq;
+        unfold(m.cb2, i, im, ap, aq);
+        unfold(setb(m), i, im, bp, bq);
+        const cplx dp = dr * ap - bp, dq = dr * aq - bq;
+        dmax = fmax(dmax, fmax(fmax(fabs(dp.re), fabs(dp.im)), fmax(fabs(dq.re), fabs(dq.im))));
+    }
+    dmax = warp_max(dmax);
+    const cplx rho0 = cmk(a.rho[2 * (m.vb + m.j)], a.rho[2 * (m.vb + m.j) + 1]);
+    if (!(dmax <= 0.5) || cabs_(dr) > 1e-3 * cabs_(rho0)) return;
     for (int i = lane; i < d; i += 32) {
         const double im = 1.0 / a.mdiag[i];
         cplx ap, aq, bp, bq;
