@@ -152,6 +152,8 @@ struct vrte_cuda_plan {
     cudaStream_t st2 = nullptr;          // side stream: independent work overlapped with the main chain
     cudaEvent_t fork[6] = {}, join[6] = {};
     LuLookahead lula;  // the boundary factorization's look-ahead streams (lu.cu)
+    DevBuf<double> Qh;          // Hessenberg Q, formed on the side stream under the QR
+    cudaEvent_t evq[2] = {};    // reduction done / Q formed
     DevBuf<int> lu_snap;
     int refine_iters = 1;
     int refine_extra = 2;
@@ -172,6 +174,8 @@ struct vrte_cuda_plan {
             for (int i = 0; i < 6; ++i)
                 if (es[i]) cudaEventDestroy(es[i]);
         for (auto& e : lula.ev)
+            if (e) cudaEventDestroy(e);
+        for (auto& e : evq)
             if (e) cudaEventDestroy(e);
         if (lula.hi) cudaStreamDestroy(lula.hi);
         if (lula.lo) cudaStreamDestroy(lula.lo);
@@ -202,7 +206,15 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     check_problem(p);
     pl.device = p->device;
     if (pl.device >= 0) VRTE_CUDA_CHECK(cudaSetDevice(pl.device));
-    if (!pl.st) VRTE_CUDA_CHECK(cudaStreamCreateWithFlags(&pl.st, cudaStreamNonBlocking));
+    if (!pl.st) {
+        // the main chain at the highest priority: side-stream work (Q formation,
+        // beam source, particular stage) fills the SMs it leaves free
+        int lo_prio = 0, hi_prio = 0;
+        VRTE_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+        VRTE_CUDA_CHECK(cudaStreamCreateWithPriority(&pl.st, cudaStreamNonBlocking, hi_prio));
+    }
+    for (auto& e : pl.evq)
+        if (!e) VRTE_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : pl.ev)
         if (!e) VRTE_CUDA_CHECK(cudaEventCreate(&e));
     if (!pl.st2) VRTE_CUDA_CHECK(cudaStreamCreateWithFlags(&pl.st2, cudaStreamNonBlocking));
@@ -328,6 +340,7 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
         b->alloc(B * dd);
     for (auto* b : {&pl.AL, &pl.BE, &pl.FB, &pl.W2, &pl.UT, &pl.EU}) b->alloc(2 * B * dd);
     pl.hwork.alloc((size_t)B * hessenberg_work_doubles(d));
+    pl.Qh.alloc((size_t)B * d * d);
     pl.Vinv.alloc(B * dd);
     pl.ipivV.alloc((size_t)B * d);
     pl.permV.alloc((size_t)B * d);
@@ -530,14 +543,24 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     gemm_batched(gemm(d, d, d, pl.F.p, d, dd, false, pl.E.p, d, dd, false, pl.T.p, d, dd, B), st);
     launch_max_abs(pl.T.p, dd, B, pl.femax.p, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[5], st));
-    launch_hessenberg_blocked(pl.T.p, pl.Z.p, pl.hwork.p, d, B, st);
-    nl += hessenberg_launch_count(d);
+    // Hessenberg reduction; its Q (independent of the reduced matrix) is formed on
+    // the side stream while the QR runs from Z = I on the main stream, and the
+    // eigenvectors are X = Q (Z Y)
+    launch_hessenberg_reduce(pl.T.p, pl.hwork.p, d, B, st);
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.evq[0], st));
+    VRTE_CUDA_CHECK(cudaStreamWaitEvent(st2, pl.evq[0], 0));
+    launch_hessenberg_formq(pl.Qh.p, pl.hwork.p, d, B, st2);
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.evq[1], st2));
+    launch_set_identity(pl.Z.p, d, B, st);
+    nl += hessenberg_launch_count(d) + 2;
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[6], st));
     launch_hqr(pl.T.p, pl.Z.p, pl.wr.p, pl.wi.p, d, B, pl.status, st, nullptr, pl.lean);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[7], st));
     launch_trevc(pl.T.p, pl.wr.p, pl.wi.p, pl.tmp1.p, d, B, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[8], st));
-    gemm_batched(gemm(d, d, d, pl.Z.p, d, dd, false, pl.tmp1.p, d, dd, false, pl.X.p, d, dd, B), st);
+    gemm_batched(gemm(d, d, d, pl.Z.p, d, dd, false, pl.tmp1.p, d, dd, false, pl.tmp3.p, d, dd, B), st);
+    VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.evq[1], 0));
+    gemm_batched(gemm(d, d, d, pl.Qh.p, d, dd, false, pl.tmp3.p, d, dd, false, pl.X.p, d, dd, B), st);
     launch_normalize_modes(pl.X.p, pl.wi.p, d, B, st);
     {
         // V^-1 of the packed eigenvector matrix: the shifted solves of the

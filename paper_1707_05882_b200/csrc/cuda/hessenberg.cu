@@ -232,8 +232,7 @@ size_t hessenberg_work_doubles(int d) {
     return 2 * (size_t)d * d + 3 * (size_t)d * nb;  // V, VT, Y, V T^T, W
 }
 
-void launch_hessenberg_blocked(double* A, double* Z, double* work, int d, int batch,
-                               cudaStream_t st) {
+void launch_hessenberg_reduce(double* A, double* work, int d, int batch, cudaStream_t st) {
     const int nbmax = hessenberg_panel_width(d);
     const long long dd = (long long)d * d, dn = (long long)d * nbmax;
     double* V = work;
@@ -269,7 +268,21 @@ void launch_hessenberg_blocked(double* A, double* Z, double* work, int d, int ba
                         Ar + (c0 + 1), d, dd, batch, -1.0, 1.0),
                      st);
     }
-    // Q = Q_0 Q_1 ... Q_{P-1}, accumulated backward on the trailing blocks
+}
+
+// Q = Q_0 Q_1 ... Q_{P-1} of a finished reduction (its reflectors in `work`),
+// accumulated backward on the trailing blocks.  Independent of the reduced
+// matrix: the BRDF pipeline forms it on the side stream under the Francis QR.
+void launch_hessenberg_formq(double* Z, double* work, int d, int batch, cudaStream_t st) {
+    const int nbmax = hessenberg_panel_width(d);
+    const long long dd = (long long)d * d, dn = (long long)d * nbmax;
+    double* V = work;
+    double* VT = V + dd * batch;
+    double* Y = VT + dd * batch;
+    double* VTt = Y + dn * batch;
+    double* W = VTt + dn * batch;  // nbmax x d per matrix
+    int npanel = 0;
+    for (int c0 = 0; c0 < d - 2; c0 += nbmax) ++npanel;
     {
         const long long total = dd * batch;
         set_identity_kernel<<<(unsigned)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096), 256, 0,
@@ -288,6 +301,11 @@ void launch_hessenberg_blocked(double* A, double* Z, double* work, int d, int ba
                         false, Qs, d, dd, batch, -1.0, 1.0),
                      st);
     }
+}
+
+void launch_hessenberg_blocked(double* A, double* Z, double* work, int d, int batch, cudaStream_t st) {
+    launch_hessenberg_reduce(A, work, d, batch, st);
+    launch_hessenberg_formq(Z, work, d, batch, st);
 }
 
 int hessenberg_launch_count(int d) {

@@ -44,6 +44,9 @@ void launch_hessenberg(double* A, double* Z, int d, int batch, cudaStream_t st);
 // explicit Q in Z; `work` holds hessenberg_work_doubles(d) doubles per matrix.
 int hessenberg_panel_width(int d);
 size_t hessenberg_work_doubles(int d);
+// (the two halves: the reduction of A, then Q from the reflectors left in work)
+void launch_hessenberg_reduce(double* A, double* work, int d, int batch, cudaStream_t st);
+void launch_hessenberg_formq(double* Z, double* work, int d, int batch, cudaStream_t st);
 void launch_hessenberg_blocked(double* A, double* Z, double* work, int d, int batch,
                                cudaStream_t st);
 int hessenberg_launch_count(int d);
