@@ -676,9 +676,13 @@ void launch_bnd_add(const BndArgs& a, double* X, const double* dX, int G, int R,
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_bnd_assemble(const BndArgs& a, cudaStream_t st) {
-    const int d = a.d, P = a.p.n_layers, G = 2 * d * P;
+void launch_bnd_zero(const BndArgs& a, cudaStream_t st) {
     VRTE_CUDA_CHECK(cudaMemsetAsync(a.lhs, 0, sizeof(double) * (size_t)a.p.n_orders * a.sl, st));
+}
+
+void launch_bnd_assemble(const BndArgs& a, cudaStream_t st, bool zeroed) {
+    const int d = a.d, P = a.p.n_layers, G = 2 * d * P;
+    if (!zeroed) launch_bnd_zero(a, st);
     const dim3 grid((d + AT - 1) / AT, (d + AT - 1) / AT, (unsigned)(a.p.n_orders * P));
     assemble_kernel<<<grid, 256, 0, st>>>(a);
     VRTE_CUDA_CHECK(cudaGetLastError());

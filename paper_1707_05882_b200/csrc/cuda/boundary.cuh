@@ -76,7 +76,10 @@ void launch_bnd_check(const BndArgs& a, const double* X, int G, int R, int stage
 void launch_bnd_refine_rhs(const BndArgs& a, const int* perm, double* dX, int G, int R, cudaStream_t st);
 void launch_bnd_add(const BndArgs& a, double* X, const double* dX, int G, int R, cudaStream_t st);
 
-void launch_bnd_assemble(const BndArgs& a, cudaStream_t st);
+// zeroed: lhs already cleared by launch_bnd_zero (the pipeline clears it on the
+// side stream under the eigen stage)
+void launch_bnd_zero(const BndArgs& a, cudaStream_t st);
+void launch_bnd_assemble(const BndArgs& a, cudaStream_t st, bool zeroed = false);
 void launch_bnd_rhs(const BndArgs& a, cudaStream_t st);
 void launch_copy_zp0(const BndArgs& a, cudaStream_t st);
 // lu.cu: batched LU with partial pivoting on ROW-major G x G matrices.

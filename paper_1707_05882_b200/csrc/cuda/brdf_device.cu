@@ -153,7 +153,7 @@ struct vrte_cuda_plan {
     cudaEvent_t fork[6] = {}, join[6] = {};
     LuLookahead lula;  // the boundary factorization's look-ahead streams (lu.cu)
     DevBuf<double> Qh;          // Hessenberg Q, formed on the side stream under the QR
-    cudaEvent_t evq[2] = {};    // reduction done / Q formed
+    cudaEvent_t evq[3] = {};    // reduction done / Q formed / boundary system cleared
     DevBuf<int> lu_snap;
     int refine_iters = 1;
     int refine_extra = 2;
@@ -551,6 +551,12 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     VRTE_CUDA_CHECK(cudaStreamWaitEvent(st2, pl.evq[0], 0));
     launch_hessenberg_formq(pl.Qh.p, pl.hwork.p, d, B, st2);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.evq[1], st2));
+    // also under the QR (latency-bound, it leaves bandwidth and 14 SMs): F s+ of the
+    // particular right-hand side (F and the beam source only) and the boundary
+    // systems' zero fill (the factorization fills them in)
+    gemm_batched(gemm(d, R, d, pl.F.p, d, dd, false, pl.sp.p, d, dR, false, pl.fsp.p, d, dR, B), st2);
+    launch_bnd_zero(make_bnd(pl), st2);
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.evq[2], st2));
     launch_set_identity(pl.Z.p, d, B, st);
     nl += hessenberg_launch_count(d) + 2;
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[6], st));
@@ -650,7 +656,6 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     pa.zm = pl.zm.p;
     pa.status = pl.status;
     launch_dither(pa, st2);
-    gemm_batched(gemm(d, R, d, pl.F.p, d, dd, false, pl.sp.p, d, dR, false, pl.fsp.p, d, dR, B), st2);
     launch_part_rhs(pa, st2);
     shifted_solve(pl.rhs.p, pl.W.p, R, dR, pl.sigma.p, pl.kind.p, pl.g.p, 0.0, st2);
     gemm_batched(gemm(d, R, d, pl.E.p, d, dd, false, pl.g.p, d, dR, false, pl.eg.p, d, dR, B), st2);
@@ -772,7 +777,8 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     // ---------------- boundary
     const BndArgs ba = make_bnd(pl);
     VRTE_CUDA_CHECK(cudaMemsetAsync(pl.resm.p, 0, sizeof(double) * NO, st));
-    launch_bnd_assemble(ba, st);
+    VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.evq[2], 0));
+    launch_bnd_assemble(ba, st, true);
     // The particular stage's refinement, like the eigenpairs': another step while
     // its balance residual exceeds kPartTarget (a tenth of the reference's 1e-6
     // gate); decided here, with the boundary assembly already queued.
