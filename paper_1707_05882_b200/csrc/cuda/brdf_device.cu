@@ -159,7 +159,7 @@ struct vrte_cuda_plan {
     int refine_extra = 2;
     int* count_host = nullptr;  // page-locked: [0] eigen slots still refining, [1] particular slots
     uint64_t part_extra_iters = 0;
-    DevBuf<int> slot_on, part_on, counts;
+    DevBuf<int> slot_on, part_on, counts, slot_list, slot_n, part_list, part_n;
     DevBuf<double> part_slot, part_prev;
     char* stage = nullptr;  // page-locked staging for the per-call inputs (one async copy each)
     size_t stage_bytes = 0;
@@ -357,7 +357,9 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pl.lam.alloc((size_t)B * d * 2);
     pl.residual.alloc((size_t)B * d);
     pl.flags.alloc((size_t)B * d);
-    for (auto* b : {&pl.slot_on, &pl.part_on}) b->alloc(B);
+    for (auto* b : {&pl.slot_on, &pl.part_on, &pl.slot_list, &pl.part_list}) b->alloc(B);
+    pl.slot_n.alloc(1);
+    pl.part_n.alloc(1);
     pl.part_slot.alloc(B);
     pl.part_prev.alloc(B);
     const size_t bdr = (size_t)B * d * R;
@@ -611,19 +613,30 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     // (F E - sigma_c) y_c = r_c for `ncol` columns in place of W = R (ld d):
     // eigenbasis (default) or Schur form.  `out` = Q y (+ beta out).
     bool vinv_joined = false;
+    // the refinement's extra steps run their GEMMs on the compacted list of the
+    // slots still above target (slot_list / slot_n, set below); main stream only
+    const int* zl = nullptr;
+    const int* zn = nullptr;
+    const int* zl2 = nullptr;  // the particular stage's extra steps (side stream)
+    const int* zn2 = nullptr;
+    auto mgemm = [&](GemmBatch g, cudaStream_t ss) {
+        g.zmap = ss == st ? zl : zl2;
+        g.zcount = ss == st ? zn : zn2;
+        gemm_batched(g, ss);
+    };
     auto shifted_solve = [&](const double* Rm, double* Wm, int ncol, long long wst, const double* sig,
                              const int* knd, double* out, double beta, cudaStream_t ss) {
         if (ss == st && !vinv_joined) {  // V^-1 comes from the side stream: join at its first use
             VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[1], 0));
             vinv_joined = true;
         }
-        gemm_batched(gemm(d, ncol, d, pl.Vinv.p, d, dd, false, Rm, d, wst, false, Wm, d, wst, B), ss);
+        mgemm(gemm(d, ncol, d, pl.Vinv.p, d, dd, false, Rm, d, wst, false, Wm, d, wst, B), ss);
         launch_eig_diag_solve(Wm, d, ncol, wst, pl.wr.p, pl.wi.p, sig, knd, B, ss);
-        gemm_batched(gemm(d, ncol, d, pl.X.p, d, dd, false, Wm, d, wst, false, out, d, wst, B, 1.0, beta), ss);
+        mgemm(gemm(d, ncol, d, pl.X.p, d, dd, false, Wm, d, wst, false, out, d, wst, B, 1.0, beta), ss);
     };
     auto residual_gemms = [&]() {
-        gemm_batched(gemm(d, d, d, pl.E.p, d, dd, false, pl.tmp1.p, d, dd, false, pl.tmp3.p, d, dd, B), st);
-        gemm_batched(gemm(d, d, d, pl.F.p, d, dd, false, pl.tmp4.p, d, dd, false, pl.tmp2.p, d, dd, B), st);
+        mgemm(gemm(d, d, d, pl.E.p, d, dd, false, pl.tmp1.p, d, dd, false, pl.tmp3.p, d, dd, B), st);
+        mgemm(gemm(d, d, d, pl.F.p, d, dd, false, pl.tmp4.p, d, dd, false, pl.tmp2.p, d, dd, B), st);
     };
     // ---------------- particular (particular.cpp:27-107) on the side stream: it needs
     // V^-1 (queued before it there), the beam source and the modes' nu, none of which
@@ -673,10 +686,17 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     launch_fill_int(pl.part_on.p, B, 1, st2);
     VRTE_CUDA_CHECK(cudaMemsetAsync(pl.part_slot.p, 0, sizeof(double) * B, st2));
     auto part_iteration = [&](bool first) {
+        if (!first) {  // the extra steps: GEMMs only on the slots still refining
+            launch_compact_slots(pl.part_on.p, B, pl.part_list.p, pl.part_n.p, st2);
+            zl2 = pl.part_list.p;
+            zn2 = pl.part_n.p;
+            nl += 1;
+        }
         launch_part_refine_residual(pa, pl.fsp.p, st2);
         shifted_solve(pl.fsp.p, pl.W.p, R, dR, pl.sigma.p, pl.kind.p, pl.g.p, 1.0, st2);
-        gemm_batched(gemm(d, R, d, pl.E.p, d, dd, false, pl.g.p, d, dR, false, pl.eg.p, d, dR, B), st2);
-        gemm_batched(gemm(d, R, d, pl.F.p, d, dd, false, pl.eg.p, d, dR, false, pl.feg.p, d, dR, B), st2);
+        mgemm(gemm(d, R, d, pl.E.p, d, dd, false, pl.g.p, d, dR, false, pl.eg.p, d, dR, B), st2);
+        mgemm(gemm(d, R, d, pl.F.p, d, dd, false, pl.eg.p, d, dR, false, pl.feg.p, d, dR, B), st2);
+        zl2 = zn2 = nullptr;
         launch_zpm(pa, st2);
         launch_part_residual(pa, st2, false);
         launch_part_decide(pa, kPartTarget, first, pl.counts.p + 1, st2);
@@ -734,10 +754,10 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
         launch_refine_normalize(rf, st);
         residual_gemms();
         launch_refine_setup(rf, st);
-        gemm_batched(gemm(d, 2 * d, d, pl.F.p, d, dd, false, pl.BE.p, d, d2, false, pl.FB.p, d, d2, B), st);
+        mgemm(gemm(d, 2 * d, d, pl.F.p, d, dd, false, pl.BE.p, d, d2, false, pl.FB.p, d, d2, B), st);
         launch_refine_rhs(rf, st);
         shifted_solve(pl.FB.p, pl.W2.p, 2 * d, d2, pl.sigma_m.p, pl.kind_m.p, pl.UT.p, 0.0, st);
-        gemm_batched(gemm(d, 2 * d, d, pl.E.p, d, dd, false, pl.UT.p, d, d2, false, pl.EU.p, d, d2, B), st);
+        mgemm(gemm(d, 2 * d, d, pl.E.p, d, dd, false, pl.UT.p, d, d2, false, pl.EU.p, d, d2, B), st);
         launch_refine_update(rf, st);
         nl += 11;
     };
@@ -763,9 +783,14 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
         VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
         nl += 2;
         if (*pl.count_host == 0) break;
+        launch_compact_slots(pl.slot_on.p, B, pl.slot_list.p, pl.slot_n.p, st);
+        zl = pl.slot_list.p;
+        zn = pl.slot_n.p;
         refine_iteration();
         final_residual();
+        nl += 1;
     }
+    zl = zn = nullptr;
     rf.slot_on = nullptr;
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[10], st));
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[1], st));

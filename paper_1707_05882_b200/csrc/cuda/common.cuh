@@ -184,6 +184,10 @@ struct GemmBatch {
     const int* bmap;
     const int* cmap;
     long long map_stride;
+    // optional batch compaction: grid z < *zcount runs batch entry zmap[z] (the
+    // refinement's extra steps on the slots still above target); null = all
+    const int* zmap;
+    const int* zcount;
 };
 constexpr int kMaxMapK = 256;
 void gemm_batched(const GemmBatch& g, cudaStream_t stream);

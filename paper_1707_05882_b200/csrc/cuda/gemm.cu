@@ -61,7 +61,11 @@ __global__ void __launch_bounds__(2 * BN, MINB) dmma_gemm_kernel(GemmBatch g) {
     extern __shared__ double smem[];
     double* As0 = smem;
     double* Bs0 = smem + ST * A_STAGE;
-    const int bz = blockIdx.z;
+    int bz = blockIdx.z;
+    if (g.zcount) {  // compacted batch (uniform per CTA: before any barrier)
+        if (bz >= *g.zcount) return;
+        bz = g.zmap[bz];
+    }
     const double* A = g.a + bz * g.stride_a;
     const double* B = g.b + bz * g.stride_b;
     double* C = g.c + bz * g.stride_c;

@@ -297,6 +297,11 @@ __global__ void refine_slots_kernel(int d, int batch, const double* residual, do
     }
 }
 
+__global__ void compact_slots_kernel(const int* slot_on, int batch, int* list, int* n) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < batch; b += gridDim.x * blockDim.x)
+        if (slot_on[b]) list[atomicAdd(n, 1)] = b;
+}
+
 inline unsigned warps_grid(int batch, int d) {
     return (unsigned)(((long long)batch * d * 32 + 255) / 256);
 }
@@ -333,6 +338,14 @@ void launch_refine_slots(int d, int batch, const double* residual, double target
                          cudaStream_t st) {
     VRTE_CUDA_CHECK(cudaMemsetAsync(count, 0, sizeof(int), st));
     refine_slots_kernel<<<(batch + 7) / 8, 256, 0, st>>>(d, batch, residual, target, slot_on, count);
+    VRTE_CUDA_CHECK(cudaGetLastError());
+}
+
+// the slots still refining as a list (any order: every slot's GEMMs are independent
+// of which CTA runs them), for the compacted GEMMs of the extra steps
+void launch_compact_slots(const int* slot_on, int batch, int* list, int* n, cudaStream_t st) {
+    VRTE_CUDA_CHECK(cudaMemsetAsync(n, 0, sizeof(int), st));
+    compact_slots_kernel<<<(batch + 255) / 256, 256, 0, st>>>(slot_on, batch, list, n);
     VRTE_CUDA_CHECK(cudaGetLastError());
 }
 

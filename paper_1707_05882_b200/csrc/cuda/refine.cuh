@@ -42,6 +42,7 @@ void launch_nu_rho(const RefineArgs& a, bool to_rho, cudaStream_t st);
 // slot_on[b] &= (max_j residual[b][j] > target); count = number of slots left on.
 // The refinement's extra steps are decided per (medium, order) slot, so a slot's
 // result does not depend on which other slots share the plan (order shards).
+void launch_compact_slots(const int* slot_on, int batch, int* list, int* n, cudaStream_t st);
 void launch_refine_slots(int d, int batch, const double* residual, double target, int* slot_on, int* count,
                          cudaStream_t st);
 
