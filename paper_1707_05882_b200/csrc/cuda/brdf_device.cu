@@ -261,12 +261,12 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
             ++tail;
         }
         pl.Be = std::max(1, pl.B - tail);  // at least one slot through the pipeline (no empty launches)
-        // the lean QR build only pays when concurrent plans of this size oversubscribe the
-        // SMs (a plan alone already fills half of them: 2 CTAs per matrix); small order
-        // shards keep the faster 229-register build
+        // the lean QR build only pays when the clusters oversubscribe the SMs: concurrent
+        // plans of this size, or one plan with more matrices than SM pairs (C4': 256);
+        // small order shards and C3 (67 matrices, 134 SMs) keep the faster 225-register build
         int dev = 0, sms = 148;
         if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        pl.lean = p->concurrent != 0 && 2 * pl.Be >= sms / 2;
+        pl.lean = (p->concurrent != 0 && 2 * pl.Be >= sms / 2) || 2 * pl.Be > sms;  // (or alone but > 1 wave)
         pl.concurrent = p->concurrent != 0;
     }
     const int N = pl.N, L = pl.L, d = pl.d, R = pl.R, G = pl.G, B = pl.B, NO = pl.NO;
