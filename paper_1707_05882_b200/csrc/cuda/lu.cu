@@ -404,8 +404,8 @@ int outer_block() { return OB_MAX; }
 // ------------------------------------------------------------------ few-column solve
 // X <- A^-1 X for K columns (position order, [G][K] per matrix) by ONE CTA per
 // matrix: the residual probes of the boundary gate (boundary.cuh), where the
-// 64-row-block TRSM + GEMM launches of lu_solve_gathered cost ~25 us each for a
-// handful of columns.  Columns < FL already hold L^-1 P b (back substitution
+// block-solve + GEMM launches of lu_solve_gathered cost tens of microseconds each
+// for a handful of columns.  Columns < FL already hold L^-1 P b (back substitution
 // only).  Per 64-row block: the coupling to the solved rows as a matvec (warp
 // per row, L / U rows read coalesced through the row map), then the block's
 // triangle from shared memory, one warp per column.
