@@ -98,9 +98,27 @@ struct LuLookahead {
     int* snap = nullptr;  // [batch][G]
     cudaEvent_t ev[4] = {};
 };
+// rd (optional): the right-hand sides are NOT carried through the factorization
+// (ncols = G): the row map after each outer block's panels is saved in
+// rd->snaps[K] and rd->ev[K] recorded, so lu_rhs_forward can apply each block's
+// update to the right-hand-side columns later, on another stream, with exactly
+// the arithmetic the augmented factorization would have used.
+struct LuRhsDefer {
+    int* snaps = nullptr;       // [nblocks][batch][G]
+    cudaEvent_t* ev = nullptr;  // [nblocks]
+    int nblocks = 0;
+};
+int lu_outer_blocks(int G);
 void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatus* status,
                   const int* order_index, cudaStream_t st, int prof_d = 0, int prof_P = 0, int lda = 0,
-                  int ncols = 0, cudaEvent_t cols_ready = nullptr, const LuLookahead* la = nullptr);
+                  int ncols = 0, cudaEvent_t cols_ready = nullptr, const LuLookahead* la = nullptr,
+                  const LuRhsDefer* rd = nullptr);
+// L^-1 P B in place in the columns [G, G + R) of a factorization run with rd:
+// block K's update (fused block solve + GEMM over the staircase rows, through
+// rd->snaps[K]) once rd->ev[K] has fired.
+void lu_rhs_forward(double* A, int G, int lda, int R, int batch, const LuRhsDefer& rd, int prof_d, int prof_P,
+                    cudaStream_t st);
+int lu_rhs_forward_launch_count(int G);
 // Back substitution of an augmented factorization (ncols = G + R) in place, down
 // to row_lo (rounded down to a 64-row block); X [batch][G][R] receives rows >= that.
 void lu_backsolve_aug(double* A, int G, int lda, int R, int batch, const int* perm, double* X, int row_lo,

@@ -155,6 +155,13 @@ struct vrte_cuda_plan {
     DevBuf<double> Qh;          // Hessenberg Q, formed on the side stream under the QR
     cudaEvent_t evq[3] = {};    // reduction done / Q formed / boundary system cleared
     DevBuf<int> lu_snap;
+    // the right-hand sides' elimination, deferred off the factorization (lu.cu
+    // LuRhsDefer): per-block row-map snapshots / events, its stream and its end
+    LuRhsDefer lurd;
+    DevBuf<int> lu_rsnap;
+    cudaEvent_t rev[32] = {};
+    cudaStream_t st3 = nullptr;
+    cudaEvent_t evr = nullptr;
     int refine_iters = 1;
     int refine_extra = 2;
     int* count_host = nullptr;  // page-locked: [0] eigen slots still refining, [1] particular slots
@@ -177,6 +184,10 @@ struct vrte_cuda_plan {
             if (e) cudaEventDestroy(e);
         for (auto& e : evq)
             if (e) cudaEventDestroy(e);
+        for (auto& e : rev)
+            if (e) cudaEventDestroy(e);
+        if (evr) cudaEventDestroy(evr);
+        if (st3) cudaStreamDestroy(st3);
         if (lula.hi) cudaStreamDestroy(lula.hi);
         if (lula.lo) cudaStreamDestroy(lula.lo);
         if (st2) cudaStreamDestroy(st2);
@@ -215,6 +226,10 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     }
     for (auto& e : pl.evq)
         if (!e) VRTE_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : pl.rev)
+        if (!e) VRTE_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    if (!pl.evr) VRTE_CUDA_CHECK(cudaEventCreateWithFlags(&pl.evr, cudaEventDisableTiming));
+    if (!pl.st3) VRTE_CUDA_CHECK(cudaStreamCreateWithFlags(&pl.st3, cudaStreamNonBlocking));
     for (auto& e : pl.ev)
         if (!e) VRTE_CUDA_CHECK(cudaEventCreate(&e));
     if (!pl.st2) VRTE_CUDA_CHECK(cudaStreamCreateWithFlags(&pl.st2, cudaStreamNonBlocking));
@@ -394,6 +409,11 @@ void setup_plan(vrte_cuda_plan& pl, const vrte_cuda_problem* p) {
     pl.perm.alloc((size_t)NO * G);
     pl.lu_snap.alloc((size_t)NO * G);
     pl.lula.snap = pl.lu_snap.p;
+    if (lu_outer_blocks(G) > 32) throw std::invalid_argument("vrte_cuda: boundary system with more than 32 outer blocks");
+    pl.lu_rsnap.alloc((size_t)lu_outer_blocks(G) * NO * G);
+    pl.lurd.snaps = pl.lu_rsnap.p;
+    pl.lurd.ev = pl.rev;
+    pl.lurd.nblocks = lu_outer_blocks(G);
     pl.up.alloc((size_t)NO * R * d);
     pl.out.alloc((size_t)pl.n_in * (N - pl.out_lo) * pl.n_dphi * 16);
     pl.status_buf.alloc(1);
@@ -804,9 +824,22 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     VRTE_CUDA_CHECK(cudaMemsetAsync(pl.resm.p, 0, sizeof(double) * NO, st));
     VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.evq[2], 0));
     launch_bnd_assemble(ba, st, true);
+    // (the right-hand sides need the modes, the free-streaming slots' particular
+    // vectors and the assembled system: all queued on the main stream by now)
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.fork[3], st));
+    // The system matrix is factored as soon as it is assembled: its right-hand
+    // sides wait for the particular stage (side stream) and are eliminated on a
+    // third stream block by block behind the factorization (lu.cu LuRhsDefer:
+    // the same arithmetic as carrying them along).  Look-ahead only for a plan
+    // alone on its device: with plans in flight the other plans fill the SMs
+    // the look-ahead would, at twice the launches.
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[11], st));
+    const int K = ba.K, ldl = ba.ldl;
+    lu_factor_rm(pl.lhs.p, G, NO, pl.ipiv.p, pl.perm.p, pl.status, pl.order_index.p, st, d, pl.P, ldl, G, nullptr,
+                 pl.concurrent ? nullptr : &pl.lula, &pl.lurd);
     // The particular stage's refinement, like the eigenpairs': another step while
     // its balance residual exceeds kPartTarget (a tenth of the reference's 1e-6
-    // gate); decided here, with the boundary assembly already queued.
+    // gate); decided here, with the factorization already queued.
     // Per slot: stops when a step no longer halves the residual (its fp64 floor).
     for (int part_extra = 0; part_extra < kPartExtraMax; ++part_extra) {
         VRTE_CUDA_CHECK(cudaEventSynchronize(pl.join[5]));
@@ -817,9 +850,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     launch_part_residual(pa, st2);  // the reference's gates on the final particular vectors
     VRTE_CUDA_CHECK(cudaEventRecord(pl.join[2], st2));
     nl += 1;
-    // right-hand sides on the side stream once the particular vectors are there; the
-    // factorization waits for them only before its first update of those columns
-    VRTE_CUDA_CHECK(cudaEventRecord(pl.fork[3], st));
+    // right-hand sides on the side stream once the particular vectors are there
     VRTE_CUDA_CHECK(cudaStreamWaitEvent(st2, pl.fork[3], 0));
     launch_bnd_rhs(ba, st2);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.join[3], st2));
@@ -828,19 +859,19 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
     VRTE_CUDA_CHECK(cudaMemsetAsync(pl.condm.p, 0, sizeof(double) * NO, st2));
     VRTE_CUDA_CHECK(cudaEventRecord(pl.join[0], st2));
     nl += 4;
-    VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[11], st));
-    const int K = ba.K, ldl = ba.ldl;
-    // look-ahead only for a plan alone on its device: with plans in flight the
-    // other plans fill the SMs the look-ahead would, at twice the launches
-    lu_factor_rm(pl.lhs.p, G, NO, pl.ipiv.p, pl.perm.p, pl.status, pl.order_index.p, st, d, pl.P, ldl, G + R,
-                 pl.join[3], pl.concurrent ? nullptr : &pl.lula);
+    // their elimination, each block's as soon as both it and the right-hand sides exist
+    VRTE_CUDA_CHECK(cudaStreamWaitEvent(pl.st3, pl.join[3], 0));
+    lu_rhs_forward(pl.lhs.p, G, ldl, R, NO, pl.lurd, d, pl.P, pl.st3);
+    VRTE_CUDA_CHECK(cudaEventRecord(pl.evr, pl.st3));
+    VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.evr, 0));
+    nl += lu_rhs_forward_launch_count(G);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[12], st));
     if (pl.full_solution) {
         // radiance: every layer's coefficients, under the reference's exact gate
         lu_backsolve_aug(pl.lhs.p, G, ldl, R, NO, pl.perm.p, pl.rhs_x.p, 0, st);
         VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[13], st));
         VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[0], 0));
-        nl += lu_aug_launch_count(G, R, 0) + boundary_full_gate(pl, ba, st);
+        nl += lu_aug_launch_count(G, 0, 0) + boundary_full_gate(pl, ba, st);
     } else {
         // BRDF: layer 0's unknowns only (the last 2d rows); the K residual probes
         // through every row on the side stream, concurrently
@@ -856,7 +887,7 @@ uint64_t run_pipeline(vrte_cuda_plan& pl, bool synth) {
         VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[0], 0));
         VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, pl.join[4], 0));
         launch_bnd_probe_check(ba, pl.Xp.p, pl.Rp.p, pl.rhs_x.p, (row_lo / 64) * 64, G, R, pl.status, st);
-        nl += lu_aug_launch_count(G, R, row_lo) + 1 + 1 + 3;
+        nl += lu_aug_launch_count(G, 0, row_lo) + 1 + 1 + 3;
     }
     nl += boundary_top(pl, ba, st);
     VRTE_CUDA_CHECK(cudaEventRecord(pl.ev[3], st));

@@ -735,9 +735,11 @@ void block_panels(double* A, int G, int lda, int* map, int* ipiv, int K0, int NB
 }
 }  // namespace
 
+int lu_outer_blocks(int G) { return (G + OB_MAX - 1) / OB_MAX; }
+
 void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatus* status,
                   const int* order_index, cudaStream_t st, int prof_d, int prof_P, int lda, int ncols,
-                  cudaEvent_t cols_ready, const LuLookahead* la) {
+                  cudaEvent_t cols_ready, const LuLookahead* la, const LuRhsDefer* rd) {
     if (G > 4096) throw std::invalid_argument("vrte_cuda: boundary system larger than 4096 rows");
     if (lda <= 0) lda = G;
     if (ncols <= 0) ncols = G;  // columns past G: right-hand sides eliminated along (augmented system)
@@ -750,12 +752,21 @@ void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatu
         lu_map_init_kernel<<<(unsigned)min(4096LL, (total + 255) / 256), 256, 0, s>>>(map, total, G);
         VRTE_CUDA_CHECK(cudaGetLastError());
     };
+    // deferred right-hand sides: the row map as it stands after block K's panels
+    auto rhs_snapshot = [&](int K0, cudaStream_t s) {
+        if (!rd) return;
+        const int kb = K0 / OB;
+        VRTE_CUDA_CHECK(cudaMemcpyAsync(rd->snaps + (size_t)kb * batch * G, map, sizeof(int) * (size_t)batch * G,
+                                        cudaMemcpyDeviceToDevice, s));
+        VRTE_CUDA_CHECK(cudaEventRecord(rd->ev[kb], s));
+    };
     if (!la || G <= OB) {
         map_init(st);
         for (int K0 = 0; K0 < G; K0 += OB) {
             const int NBk = min(OB, G - K0);
             const int rend = row_end(K0 + NBk - 1);  // profile is non-decreasing in the column
             block_panels(A, G, lda, map, ipiv, K0, NBk, rend, status, order_index, batch, st);
+            rhs_snapshot(K0, st);
             if (cols_ready && ncols > K0 + NBk) {  // the columns past G (right-hand sides) come from another stream
                 VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, cols_ready, 0));
                 cols_ready = nullptr;
@@ -778,6 +789,7 @@ void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatu
     if (cols_ready) VRTE_CUDA_CHECK(cudaStreamWaitEvent(lo, cols_ready, 0));
     map_init(hi);
     block_panels(A, G, lda, map, ipiv, 0, min(OB, G), row_end(min(OB, G) - 1), status, order_index, batch, hi);
+    rhs_snapshot(0, hi);
     bool rest_pending = false;
     for (int K0 = 0; K0 < G; K0 += OB) {
         const int NBk = min(OB, G - K0), c1 = K0 + NBk;
@@ -800,11 +812,31 @@ void lu_factor_rm(double* A, int G, int batch, int* ipiv, int* perm, DeviceStatu
         }
         block_update(A, G, lda, gg, map, K0, NBk, rend, c1, c1 + nxt, batch, hi);
         block_panels(A, G, lda, map, ipiv, c1, nxt, row_end(c1 + nxt - 1), status, order_index, batch, hi);
+        rhs_snapshot(c1, hi);
     }
     VRTE_CUDA_CHECK(cudaEventRecord(la->ev[3], lo));
     VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, la->ev[3], 0));
     VRTE_CUDA_CHECK(cudaEventRecord(la->ev[3], hi));
     VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, la->ev[3], 0));
+}
+
+void lu_rhs_forward(double* A, int G, int lda, int R, int batch, const LuRhsDefer& rd, int prof_d, int prof_P,
+                    cudaStream_t st) {
+    const int OB = outer_block();
+    const long long gg = (long long)G * lda;
+    for (int K0 = 0; K0 < G; K0 += OB) {
+        const int NBk = min(OB, G - K0), kb = K0 / OB;
+        const int rend = prof_d > 0 ? min(G, bnd_row_end(K0 + NBk - 1, prof_d, prof_P)) : G;
+        VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, rd.ev[kb], 0));
+        block_update(A, G, lda, gg, rd.snaps + (size_t)kb * batch * G, K0, NBk, rend, G, G + R, batch, st);
+    }
+}
+
+int lu_rhs_forward_launch_count(int G) {
+    const int OB = outer_block();
+    int n = 0;
+    for (int K0 = 0; K0 < G; K0 += OB) n += 2;  // fused block solve + trailing GEMM (the last: rows below may be none)
+    return n;
 }
 
 // Back substitution on an augmented factorization ([A | B] factored with
