@@ -30,6 +30,11 @@ import tempfile
 import threading
 import time
 
+# every plan runs on several streams (main, side, right-hand sides, look-ahead); with
+# plans in flight together the default 8 hardware work queues would alias streams
+# onto one queue (false dependencies): give the context the maximum before it exists
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 

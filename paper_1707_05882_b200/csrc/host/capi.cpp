@@ -28,6 +28,16 @@ using namespace vrte::host;
 
 namespace {
 
+// Every plan drives several CUDA streams (main, side, right-hand sides, factorization
+// look-ahead); with plans in flight together (batch API, order shards) the default
+// 8 hardware work queues would alias streams onto one queue.  Ask for the maximum
+// when the library is loaded -- effective if the process has not created its CUDA
+// context yet, never overriding a value the application set.
+const bool g_connections = [] {
+    setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
+    return true;
+}();
+
 thread_local std::string g_last_error;
 
 vrte_status set_error(vrte_status code, const std::string& message) {

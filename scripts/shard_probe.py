@@ -7,6 +7,7 @@
            (throughput mode)
 Usage: python scripts/shard_probe.py [C3|C4p] [W,...] [concurrency,...]"""
 import json, os, sys, tempfile, threading, time
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # (as bench.py: many streams in flight)
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import bench, paper_1707_05882_b200 as V
