@@ -903,13 +903,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, MINB) hqr_multi
             // ([c_lo, c_split)), published early; phase B: the rest of H and Z
             const int cs = min(max(jd[8], jd[4]), jd[5]);
             if (cs > jd[4]) apply_part(nullptr, jd[1], jd[2], jd[3], jd[4], cs, false, warp, nt / 32, ua);
-            fence_cluster();
+            // publication: the CTA barrier orders every thread's writes before thread
+            // 0's cluster-scope fence + release, which is cumulative over them -- one
+            // fence per hand-off instead of one per thread
             __syncthreads();
-            if (t == 0) st_release_cluster(a_partial, next + 1);
+            if (t == 0) {
+                fence_cluster();
+                st_release_cluster(a_partial, next + 1);
+            }
             apply_part(nullptr, jd[1], jd[2], jd[3], cs, jd[5], jd[6] != 0, warp, nt / 32, ua);
-            fence_cluster();
             __syncthreads();
-            if (t == 0) st_release_cluster(a_done, next + 1);
+            if (t == 0) {
+                fence_cluster();
+                st_release_cluster(a_done, next + 1);
+            }
         }
         cluster_sync_all();
         return;
@@ -1345,8 +1352,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, MINB) hqr_multi
                     if (c >= 1 && t == 0) wait_partial(jid);
                     named_bar(3, 128);
                     if (whi_n > whi) apply_part(Uc, wlo, whi, nw, whi + 1, whi_n + 1, false, warp, 4);
-                    fence_cluster();
-                    named_bar(3, 128);
+                    named_bar(3, 128);  // (post_job: thread 0's fence + release, cumulative)
                     if (t == 0) {
                         // the columns chunk c + 2 will update itself: [c_lo, whi_{c+2}]
                         int c_split = 0;
