@@ -222,8 +222,11 @@ VRTE_API int32_t vrte_cuda_lu_solve(const double* A, int32_t G, int32_t batch, c
  * pivoting (lu.cu), in place: A [batch][G][ncols] row-major, the columns past G
  * eliminated along (augmented system); on return A holds L (unit lower, strictly
  * below the diagonal) and U at the physical rows, perm [batch][G] the row of each
- * position.  lookahead = 1 runs the boundary stage's one-block look-ahead
- * schedule (two streams), 0 the serial one.  Returns 0, 3 (singular) or 5. */
+ * position.  lookahead bit 0 runs the boundary stage's one-block look-ahead
+ * schedule (two streams), else the serial one; bit 1 defers the columns past G:
+ * the matrix is factored alone and they are eliminated afterwards on another
+ * stream through the per-block row-map snapshots (the BRDF pipeline's path).
+ * Returns 0, 3 (singular) or 5. */
 VRTE_API int32_t vrte_cuda_lu_factor(double* A, int32_t G, int32_t ncols, int32_t batch, int32_t lookahead,
                                      int32_t* perm, int32_t device);
 /* Kernel-level check of the blocked Hessenberg reduction (hessenberg.cu):

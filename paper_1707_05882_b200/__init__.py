@@ -252,16 +252,17 @@ def lu_solve(A, B, device: int = 0) -> np.ndarray:
     return X
 
 
-def lu_factor(A, G: int, lookahead: bool = True, device: int = 0):
+def lu_factor(A, G: int, lookahead: bool = True, device: int = 0, deferred: bool = False):
     """Batched in-place row-major LU (kernel-level check): A [batch, G, ncols]
-    (columns past G carried along) -> (factors at the physical rows, perm
-    [batch, G]: physical row of each position)."""
+    (columns past G carried along, or with deferred=True eliminated after the
+    matrix's factorization through per-block row-map snapshots) -> (factors at
+    the physical rows, perm [batch, G]: physical row of each position)."""
     A = np.array(A, dtype=np.float64, order="C", copy=True)
     batch, g, ncols = A.shape
     if g != G:
         raise ValueError("lu_factor: A must be [batch, G, ncols]")
     perm = np.zeros((batch, G), dtype=np.int32)
-    code = lib().vrte_cuda_lu_factor(_dp(A), G, ncols, batch, int(bool(lookahead)),
+    code = lib().vrte_cuda_lu_factor(_dp(A), G, ncols, batch, int(bool(lookahead)) | (2 if deferred else 0),
                                      perm.ctypes.data_as(C.POINTER(C.c_int32)), device)
     if code != 0:
         raise VrteError(code, "vrte_cuda_lu_factor failed (singular or bad arguments)")

@@ -1735,8 +1735,35 @@ int32_t vrte_cuda_lu_factor(double* A, int32_t G, int32_t ncols, int32_t batch, 
         la.snap = snap.p;
         dst.alloc(1);
         VRTE_CUDA_CHECK(cudaMemsetAsync(dst.p, 0, sizeof(DeviceStatus), st));
-        lu_factor_rm(dA.p, G, batch, ipiv.p, perm.p, dst.p, nullptr, st, 0, 0, ncols, ncols, nullptr,
-                     lookahead ? &la : nullptr);
+        // bit 1: the columns past G deferred (factor the matrix alone, then
+        // lu_rhs_forward on another stream through the per-block snapshots)
+        const bool deferred = (lookahead & 2) != 0 && ncols > G;
+        LuRhsDefer rd;
+        DevBuf<int> rsnap;
+        std::vector<cudaEvent_t> rev;
+        cudaStream_t s3 = nullptr;
+        if (deferred) {
+            rd.nblocks = lu_outer_blocks(G);
+            rsnap.alloc((size_t)rd.nblocks * batch * G);
+            rd.snaps = rsnap.p;
+            rev.resize(rd.nblocks);
+            for (auto& e : rev) VRTE_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            rd.ev = rev.data();
+            VRTE_CUDA_CHECK(cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking));
+        }
+        lu_factor_rm(dA.p, G, batch, ipiv.p, perm.p, dst.p, nullptr, st, 0, 0, ncols, deferred ? G : ncols, nullptr,
+                     (lookahead & 1) ? &la : nullptr, deferred ? &rd : nullptr);
+        if (deferred) {
+            lu_rhs_forward(dA.p, G, ncols, ncols - G, batch, rd, 0, 0, s3);
+            cudaEvent_t done;
+            VRTE_CUDA_CHECK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+            VRTE_CUDA_CHECK(cudaEventRecord(done, s3));
+            VRTE_CUDA_CHECK(cudaStreamWaitEvent(st, done, 0));
+            VRTE_CUDA_CHECK(cudaStreamSynchronize(st));
+            cudaEventDestroy(done);
+            for (auto& e : rev) cudaEventDestroy(e);
+            cudaStreamDestroy(s3);
+        }
         VRTE_CUDA_CHECK(cudaMemcpyAsync(A, dA.p, sizeof(double) * dA.n, cudaMemcpyDeviceToHost, st));
         VRTE_CUDA_CHECK(cudaMemcpyAsync(perm_out, perm.p, sizeof(int) * perm.n, cudaMemcpyDeviceToHost, st));
         DeviceStatus s{};

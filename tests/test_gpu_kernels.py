@@ -112,3 +112,20 @@ def test_lu_lookahead_schedule_is_bitwise_identical(G, ncols, batch):
         assert np.abs(Lm @ U - PA[:, :G]).max() <= 1e-13 * np.abs(A[b]).max() * np.sqrt(G)
         if ncols > G:  # the carried columns hold L^-1 P B
             assert np.abs(Lm @ P[:, G:] - PA[:, G:]).max() <= 1e-13 * np.abs(A[b]).max() * np.sqrt(G)
+
+
+@pytest.mark.parametrize("G,ncols,batch", [(1024, 1280, 3), (1000, 1100, 2), (384, 640, 2)])
+def test_deferred_right_hand_sides_are_bitwise_the_augmented_elimination(G, ncols, batch):
+    """The BRDF pipeline factors the boundary system before its right-hand sides
+    exist and eliminates them afterwards through the row map saved after each
+    outer block's panels (lu.cu LuRhsDefer): identical to carrying them along,
+    in both schedules."""
+    rng = np.random.default_rng(3 * G + ncols)
+    A = rng.standard_normal((batch, G, ncols))
+    A *= np.exp(-rng.uniform(0, 6, (batch, G, 1)))
+    F0, p0 = V.lu_factor(A, G, lookahead=True)
+    F1, p1 = V.lu_factor(A, G, lookahead=True, deferred=True)
+    F2, p2 = V.lu_factor(A, G, lookahead=False, deferred=True)
+    assert np.array_equal(p0, p1) and np.array_equal(p0, p2)
+    assert np.array_equal(F0, F1)
+    assert np.array_equal(F0, F2)
