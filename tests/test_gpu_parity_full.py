@@ -7,9 +7,9 @@ the reference's algorithm at its fp64 limit) and as written.
 Measured on the B200 (profiles/parity_r02.json, scripts/parity_full.py):
 
                          GPU vs accurate          reference-as-written vs accurate
-  per matrix max|d|/max|M|   3.4e-11 .. 8.0e-11     1.4e-9 .. 3.4e-9
+  per matrix max|d|/max|M|   3.7e-11 .. 8.7e-11     1.4e-9 .. 3.4e-9
   SURVEY §8(d) metric        5.4e-9  .. 3.2e-8      1.6e-6 .. 4.7e-6
-  matrices with SURVEY <= 1e-9   99.78% .. 99.98%
+  matrices with SURVEY <= 1e-9   99.79% .. 99.98%
 
 The SURVEY metric floors the denominator at 1e-3 |M00|; at grazing incidence /
 exit (mu < 0.01) some entries of the exact answer itself move by up to 3.8e-8
