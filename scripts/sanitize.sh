@@ -10,3 +10,7 @@ if [ "${1:-}" = "c3" ]; then
     timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python scripts/profile_step.py C3 > $O/c3_$tool.log 2>&1; echo "rc=$?" >> $O/c3_$tool.log
   done
 fi
+# C4' (N = 128, 256 orders: the 128-register QR build, d = 512) under memcheck when asked
+if [ "${1:-}" = "c4p" ]; then
+  timeout 1800 compute-sanitizer --tool memcheck --print-limit 20 python scripts/profile_step.py C4p > $O/c4p_memcheck.log 2>&1; echo "rc=$?" >> $O/c4p_memcheck.log
+fi
