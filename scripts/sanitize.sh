@@ -14,3 +14,8 @@ fi
 if [ "${1:-}" = "c4p" ]; then
   timeout 1800 compute-sanitizer --tool memcheck --print-limit 20 python scripts/profile_step.py C4p > $O/c4p_memcheck.log 2>&1; echo "rc=$?" >> $O/c4p_memcheck.log
 fi
+# the batch API (concurrent plans on their own threads/streams, lean QR build) and the kernel tests under memcheck
+if [ "${1:-}" = "batch" ]; then
+  timeout 1800 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest -q -p no:cacheprovider \
+    tests/test_gpu_capi.py tests/test_gpu_kernels.py tests/test_gpu_multidevice.py > $O/batch_memcheck.log 2>&1; echo "rc=$?" >> $O/batch_memcheck.log
+fi
